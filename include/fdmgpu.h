@@ -1,0 +1,172 @@
+/*
+ * fdmgpu.h — C ABI of the B200 (sm_100a, FP64) vertex-star FDM Schwarz path.
+ *
+ * Drop-in boundary for the reference's Poisson/PCG hot path
+ * (/root/reference/proj).  Every entry point names the reference interface it
+ * replaces; the reference-side binding a maintainer would add is shown in
+ * INTEGRATION.md.  Conventions:
+ *   - plain pointers and sizes only; no torch / Eigen types;
+ *   - every call returns fdmgpu_status; fdmgpu_last_error(h) gives the message
+ *     (same text as the reference's exception where one exists);
+ *   - one CUDA stream per handle (fdmgpu_set_stream to share a caller's
+ *     stream); calls on one handle are not thread-safe, distinct handles are;
+ *   - vectors are global DOF vectors of length ndof in the reference's
+ *     first-touch numbering (src/discretization.cpp:70-264); "device" calls
+ *     take device pointers, "_host" calls take host pointers and copy.
+ *   - there is no CPU fallback: without a CUDA device every call that needs
+ *     one fails with FDMGPU_CUDA_ERROR.
+ */
+#ifndef FDMGPU_H
+#define FDMGPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct fdmgpu_context* fdmgpu_handle;
+
+typedef enum {
+  FDMGPU_OK = 0,
+  FDMGPU_INVALID_ARGUMENT = 1, /* std::invalid_argument (e.g. src/kron.cpp:23-25)            */
+  FDMGPU_NOT_SPD = 2,          /* "cholesky: matrix not SPD at pivot k" (src/cholesky.cpp:80) */
+  FDMGPU_INDEFINITE = 3,       /* "pcg: indefinite operator at iteration k" (src/krylov.cpp:50) */
+  FDMGPU_OUT_OF_MEMORY = 4,
+  FDMGPU_CUDA_ERROR = 5,
+  FDMGPU_UNSUPPORTED = 6 /* patch topology outside the shared-lattice pattern, 2D facet flips */
+} fdmgpu_status;
+
+/* KrylovReport (include/fdmstar/krylov.hpp:12-20). */
+typedef struct {
+  int32_t iterations;
+  int32_t converged;
+  double kappa;
+  double lambda_min;
+  double lambda_max;
+  double final_residual;
+  double wall_time;
+} fdmgpu_krylov_report;
+
+/* Shared patch layout and factor statistics (PatchSolver::factor_nnz,
+ * CholFactor::flops: include/fdmstar/schwarz.hpp:44, cholesky.hpp:21-24). */
+typedef struct {
+  int32_t npatch;        /* vertex-star patches                                   */
+  int32_t n;             /* DOFs per patch, (2p-1)^d                              */
+  int32_t n_interior;    /* cell-interior DOFs per patch, 2^d (p-1)^d             */
+  int32_t n_interface;   /* separator DOFs per patch                              */
+  int32_t tile;          /* dense tile edge of the interface factor               */
+  int32_t tile_cols;     /* interface tile rows/columns                           */
+  int32_t tiles;         /* stored (non-zero) lower tiles per patch               */
+  int32_t pad_;
+  int64_t nnz_L;         /* nnz(L_j) of the reference factor (symbolic), per patch */
+  int64_t flops_ref;     /* CholFactor::flops per patch (multiply-adds)           */
+  int64_t factor_bytes;  /* device bytes of the stored factor, all patches        */
+  int64_t tile_gemms;    /* tile updates per patch (factorisation work units)     */
+} fdmgpu_layout;
+
+/* Operator ids for fdmgpu_apply. */
+enum {
+  FDMGPU_OP_APPLY_ST = 0,   /* TransformedSystem::apply_St (src/assembly.cpp:326-342)  */
+  FDMGPU_OP_APPLY_S = 1,    /* TransformedSystem::apply_S  (src/assembly.cpp:308-324)  */
+  FDMGPU_OP_PATCH = 2,      /* PatchSolver::apply          (src/schwarz.cpp:41-54)     */
+  FDMGPU_OP_SMOOTH = 3,     /* TwoLevel::smooth            (src/schwarz.cpp:121-123)   */
+  FDMGPU_OP_A = 4,          /* GlobalOperator::apply       (src/assembly.cpp:56-88)    */
+  FDMGPU_OP_VCYCLE = 5      /* TwoLevel::apply             (src/schwarz.cpp:125-133)   */
+};
+
+const char* fdmgpu_last_error(fdmgpu_handle h);
+const char* fdmgpu_status_string(fdmgpu_status s);
+
+/* ---- construction ---------------------------------------------------------- */
+/* Replaces the device-side half of build_poisson_twolevel
+ * (src/schwarz.cpp:230-252): a handle for a scalar Q_p space of dimension
+ * dim (2|3) and degree p on ncells cells with ndof global DOFs. */
+fdmgpu_status fdmgpu_create(fdmgpu_handle* out, int32_t dim, int32_t p, int32_t ncells, int64_t ndof,
+                            int32_t device);
+fdmgpu_status fdmgpu_destroy(fdmgpu_handle h);
+fdmgpu_status fdmgpu_set_stream(fdmgpu_handle h, void* cuda_stream);
+fdmgpu_status fdmgpu_synchronize(fdmgpu_handle h);
+
+/* FdmBasis (include/fdmstar/fdm_basis.hpp:21-32) and the reference interval
+ * (reference_interval.hpp:15-27).  All (p+1)^2 arrays column-major:
+ * S, A_t = S^T A S, B_t = S^T B S (values + structural 0/1 patterns), lambda
+ * (p-1 interior eigenvalues), A_hat / B_hat (reference stiffness / mass),
+ * and the GL(q) tables Vq, Dq (q x (p+1), column-major) with weights wq used
+ * by the true-form trilinear operator (src/assembly.cpp:198-215, q = p+2). */
+fdmgpu_status fdmgpu_set_basis(fdmgpu_handle h, const double* S, const double* lambda, const double* A_t,
+                               const double* B_t, const uint8_t* A_t_pattern, const uint8_t* B_t_pattern,
+                               const double* A_hat, const double* B_hat, int32_t q, const double* Vq,
+                               const double* Dq, const double* wq);
+
+/* Discretization::Component maps (include/fdmstar/discretization.hpp:22-34):
+ * cell_dofs / cell_modes ncells x (p+1)^d (axis 0 fastest), optional
+ * mode_signs (+-1, same shape; NULL = all +1), multiplicity and the strong
+ * Dirichlet mask (ndof). */
+fdmgpu_status fdmgpu_set_mesh_maps(fdmgpu_handle h, const int32_t* cell_dofs, const int32_t* cell_modes,
+                                   const double* mode_signs, const double* multiplicity,
+                                   const uint8_t* constrained);
+
+/* Per-cell data of cell_geometry (src/geometry.cpp:45-104): kind (0
+ * Cartesian, 1 affine, 2 bilinear/trilinear), mu = kappa_K * mu^K (ncells x
+ * dim; the separable surrogate of the patch solver and the exact Cartesian
+ * coefficients), corner coordinates (ncells x 2^dim x 3, tensor corner order;
+ * may be NULL when every cell is Cartesian) and kappa (ncells; NULL = 1). */
+fdmgpu_status fdmgpu_set_cell_coeffs(fdmgpu_handle h, const uint8_t* kind, const double* mu,
+                                     const double* corner_xyz, const double* kappa);
+
+/* PatchSolver::Patch lists (src/schwarz.cpp:62-83): for patch j, the vertex,
+ * its ascending star_dofs dofs[ptr[j]..ptr[j+1]) (src/discretization.cpp:
+ * 266-297), the patch_ordering permutation perm (local indices,
+ * src/ordering.cpp:17-45) and its 2^dim star cells (ascending ids). */
+fdmgpu_status fdmgpu_set_patches(fdmgpu_handle h, int32_t npatch, const int32_t* vertex, const int64_t* ptr,
+                                 const int32_t* dofs, const int32_t* perm, const int32_t* star_cells);
+
+/* Coarse level of TwoLevel (include/fdmstar/schwarz.hpp:52-66): dense
+ * inverse of the assembled coarse matrix (ndof_c^2, row-major) and the
+ * prolongation CSR (ndof rows, src/schwarz.cpp:139-165). */
+fdmgpu_status fdmgpu_set_coarse(fdmgpu_handle h, int32_t ndof_c, const double* coarse_inverse,
+                                const int64_t* P_ptr, const int32_t* P_col, const double* P_val);
+
+/* Batched numeric factorisation of every patch matrix A~_j under its
+ * patch ordering (replaces cholesky(), src/cholesky.cpp:9-87, inside
+ * build_patch_solver, src/schwarz.cpp:84-93).  Returns FDMGPU_NOT_SPD with
+ * "cholesky: matrix not SPD at pivot k (patch j)" on a non-positive pivot. */
+fdmgpu_status fdmgpu_factor(fdmgpu_handle h);
+fdmgpu_status fdmgpu_get_layout(fdmgpu_handle h, fdmgpu_layout* out);
+/* Per-patch global DOFs in elimination order (npatch x n): dofs[perm[k]]. */
+fdmgpu_status fdmgpu_get_patch_elimination_dofs(fdmgpu_handle h, int32_t* out);
+
+/* ---- operators ----------------------------------------------------------------- */
+/* Generic entry: op = FDMGPU_OP_*, omega used by FDMGPU_OP_VCYCLE, host != 0
+ * means `in` / `out` are host pointers (copied inside, synchronous). */
+fdmgpu_status fdmgpu_apply(fdmgpu_handle h, int32_t op, double omega, const double* in, double* out,
+                           int32_t host);
+fdmgpu_status fdmgpu_transform(fdmgpu_handle h, int32_t dir, const double* in, double* out); /* 0 S^T, 1 S */
+fdmgpu_status fdmgpu_patch_solve(fdmgpu_handle h, const double* r_modal, double* z_modal);
+fdmgpu_status fdmgpu_smooth(fdmgpu_handle h, const double* r, double* z);
+fdmgpu_status fdmgpu_apply_A(fdmgpu_handle h, const double* x, double* y);
+fdmgpu_status fdmgpu_vcycle(fdmgpu_handle h, double omega, const double* r, double* z);
+
+/* pcg (src/krylov.cpp:29-83) with A = GlobalOperator::apply and
+ * precond 0 = identity, 1 = smooth, 2 = V(1,1) cycle at the handle's omega.
+ * b, x device vectors; residuals (optional, host, maxit entries) receives the
+ * relative residual history. */
+fdmgpu_status fdmgpu_pcg(fdmgpu_handle h, const double* b, double* x, double rtol, int32_t maxit,
+                         int32_t precond, fdmgpu_krylov_report* report, double* residuals);
+
+/* calibrate_damping (src/schwarz.cpp:97-119, 167-228): formula 0 TwoGrid,
+ * 1 Smoother, 2 Paper; sets and returns omega with the Lanczos extremes. */
+fdmgpu_status fdmgpu_calibrate_damping(fdmgpu_handle h, int32_t lanczos_steps, uint32_t seed, int32_t formula,
+                                       double* omega, double* lambda_min, double* lambda_max);
+fdmgpu_status fdmgpu_set_omega(fdmgpu_handle h, double omega);
+fdmgpu_status fdmgpu_get_omega(fdmgpu_handle h, double* omega);
+
+/* Number of kernels this handle has launched so far (evidence for bench.py). */
+int64_t fdmgpu_launch_count(fdmgpu_handle h);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FDMGPU_H */

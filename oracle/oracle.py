@@ -199,8 +199,11 @@ class Problem:
         self._twolevel = False
 
     def __del__(self):
-        if getattr(self, "h", None):
-            lib().oracle_destroy(self.h)
+        if getattr(self, "h", None) and _lib is not None:
+            try:
+                _lib.oracle_destroy(self.h)
+            except Exception:
+                pass
             self.h = None
 
     def rhs(self):

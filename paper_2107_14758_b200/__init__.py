@@ -1,0 +1,303 @@
+"""B200-native (sm_100a, FP64) vertex-star FDM Schwarz relaxation.
+
+Python mirror of the reference's public entry points for the Poisson/PCG hot
+path (/root/reference/proj/include/fdmstar): problem setup (cartesian_mesh,
+q_space, make_bundle, star_dofs / patch_ordering), the batched patch
+factorisation (build_patch_solver), the relaxation (TwoLevel::smooth), the
+V(1,1) cycle (TwoLevel::apply), the matrix-free operator
+(GlobalOperator::apply), damping calibration and PCG.  Everything goes
+through the C ABI of lib/libfdmgpu.so (include/fdmgpu.h); torch is only used
+for device memory and streams.  There is no CPU fallback: without the
+library or a CUDA device the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libfdmgpu.so")
+_lib = None
+
+OP_APPLY_ST, OP_APPLY_S, OP_PATCH, OP_SMOOTH, OP_A, OP_VCYCLE = range(6)
+STATUS = {0: "ok", 1: "invalid argument", 2: "matrix not SPD", 3: "indefinite operator", 4: "out of memory",
+          5: "CUDA error", 6: "unsupported"}
+
+
+class FdmGpuError(RuntimeError):
+    """Raised for every non-OK fdmgpu status; .status holds the code."""
+
+    def __init__(self, status, msg):
+        super().__init__(msg)
+        self.status = status
+
+
+class NotSPDError(FdmGpuError):
+    pass
+
+
+class IndefiniteError(FdmGpuError):
+    pass
+
+
+class Layout(C.Structure):
+    _fields_ = [("npatch", C.c_int32), ("n", C.c_int32), ("n_interior", C.c_int32), ("n_interface", C.c_int32),
+                ("tile", C.c_int32), ("tile_cols", C.c_int32), ("tiles", C.c_int32), ("pad_", C.c_int32),
+                ("nnz_L", C.c_int64), ("flops_ref", C.c_int64), ("factor_bytes", C.c_int64),
+                ("tile_gemms", C.c_int64)]
+
+
+class KrylovReport(C.Structure):
+    _fields_ = [("iterations", C.c_int32), ("converged", C.c_int32), ("kappa", C.c_double),
+                ("lambda_min", C.c_double), ("lambda_max", C.c_double), ("final_residual", C.c_double),
+                ("wall_time", C.c_double)]
+
+
+_vp = C.c_void_p
+
+
+def lib():
+    """Load lib/libfdmgpu.so (built by __graft_entry__.build()); raises if absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise FdmGpuError(5, f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = C.CDLL(LIB_PATH)
+        L.fdmgpu_last_error.restype = C.c_char_p
+        L.fdmgpu_last_error.argtypes = [_vp]
+        L.fdmhost_last_error.restype = C.c_char_p
+        L.fdmhost_problem_create.restype = _vp
+        L.fdmhost_problem_create.argtypes = [C.c_int, C.c_int, C.c_int]
+        L.fdmhost_problem_destroy.argtypes = [_vp]
+        L.fdmhost_problem_info.argtypes = [_vp, _vp]
+        L.fdmhost_get_rhs.argtypes = [_vp, _vp]
+        L.fdmhost_get_maps.argtypes = [_vp] * 7
+        L.fdmhost_get_geometry.argtypes = [_vp] * 6
+        L.fdmhost_get_basis.argtypes = [_vp] * 11
+        L.fdmhost_get_patches.argtypes = [_vp] * 7
+        L.fdmhost_get_coarse.argtypes = [_vp] * 5
+        L.fdmhost_attach.argtypes = [_vp, C.c_int, C.POINTER(_vp)]
+        L.fdmgpu_destroy.argtypes = [_vp]
+        L.fdmgpu_set_stream.argtypes = [_vp, _vp]
+        L.fdmgpu_synchronize.argtypes = [_vp]
+        L.fdmgpu_factor.argtypes = [_vp]
+        L.fdmgpu_get_layout.argtypes = [_vp, C.POINTER(Layout)]
+        L.fdmgpu_get_patch_elimination_dofs.argtypes = [_vp, _vp]
+        L.fdmgpu_apply.argtypes = [_vp, C.c_int32, C.c_double, _vp, _vp, C.c_int32]
+        L.fdmgpu_pcg.argtypes = [_vp, _vp, _vp, C.c_double, C.c_int32, C.c_int32, C.POINTER(KrylovReport), _vp]
+        L.fdmgpu_calibrate_damping.argtypes = [_vp, C.c_int32, C.c_uint32, C.c_int32, C.POINTER(C.c_double),
+                                               C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        L.fdmgpu_set_omega.argtypes = [_vp, C.c_double]
+        L.fdmgpu_get_omega.argtypes = [_vp, C.POINTER(C.c_double)]
+        L.fdmgpu_launch_count.restype = C.c_int64
+        L.fdmgpu_launch_count.argtypes = [_vp]
+        _lib = L
+    return _lib
+
+
+def _host_chk(rc):
+    if rc != 0:
+        raise FdmGpuError(1, lib().fdmhost_last_error().decode())
+
+
+def _ptr(a):
+    return None if a is None else _vp(a.ctypes.data)
+
+
+class Problem:
+    """One synthetic configuration (BASELINE.json configs 1..5), optionally
+    reduced to n cells per axis / degree p, built by the host setup mirror."""
+
+    def __init__(self, config: int, n: int = 0, p: int = 0):
+        L = lib()
+        self.h = L.fdmhost_problem_create(config, n, p)
+        if not self.h:
+            raise FdmGpuError(1, L.fdmhost_last_error().decode())
+        info = np.zeros(15, np.int64)
+        _host_chk(L.fdmhost_problem_info(self.h, _ptr(info)))
+        (self.dim, self.p, self.ncells, self.ndof, self.nfree, self.npatches, self.nvertices, self.npc,
+         self.sum_nj, self.ncoarse, self.P_nnz, self.q, self.config, self.n, cart) = (int(v) for v in info)
+        self.all_cartesian = bool(cart)
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            try:
+                _lib.fdmhost_problem_destroy(self.h)
+            except Exception:
+                pass
+            self.h = None
+
+    def rhs(self):
+        out = np.zeros(self.ndof)
+        _host_chk(lib().fdmhost_get_rhs(self.h, _ptr(out)))
+        return out
+
+    def maps(self):
+        cd = np.zeros(self.ncells * self.npc, np.int32)
+        cm = np.zeros_like(cd)
+        con = np.zeros(self.ndof, np.uint8)
+        mult = np.zeros(self.ndof)
+        lc, le = np.zeros(self.ndof, np.int32), np.zeros(self.ndof, np.int32)
+        _host_chk(lib().fdmhost_get_maps(self.h, _ptr(cd), _ptr(cm), _ptr(con), _ptr(mult), _ptr(lc), _ptr(le)))
+        return dict(cell_dofs=cd.reshape(self.ncells, self.npc), cell_modes=cm.reshape(self.ncells, self.npc),
+                    constrained=con, multiplicity=mult, label_cls=lc, label_entity=le)
+
+    def geometry(self):
+        v = np.zeros(self.nvertices * 3)
+        k = np.zeros(self.ncells)
+        mu = np.zeros(self.ncells * self.dim)
+        kind = np.zeros(self.ncells, np.uint8)
+        xyz = np.zeros(self.ncells * (1 << self.dim) * 3)
+        _host_chk(lib().fdmhost_get_geometry(self.h, _ptr(v), _ptr(k), _ptr(mu), _ptr(kind), _ptr(xyz)))
+        return dict(vertices=v.reshape(-1, 3), kappa=k, mu=mu.reshape(self.ncells, self.dim), kind=kind,
+                    corner_xyz=xyz.reshape(self.ncells, 1 << self.dim, 3))
+
+    def basis(self):
+        n = self.p + 1
+        S, At, Bt, Ah, Bh = (np.zeros(n * n) for _ in range(5))
+        Anz, Bnz = np.zeros(n * n, np.uint8), np.zeros(n * n, np.uint8)
+        lam, par, nodes = np.zeros(max(self.p - 1, 1)), np.zeros(n), np.zeros(n)
+        _host_chk(lib().fdmhost_get_basis(self.h, _ptr(S), _ptr(At), _ptr(Bt), _ptr(Anz), _ptr(Bnz), _ptr(lam),
+                                          _ptr(par), _ptr(Ah), _ptr(Bh), _ptr(nodes)))
+        f = lambda a: a.reshape(n, n, order="F")
+        return dict(S=f(S), At=f(At), Bt=f(Bt), Atnz=f(Anz).astype(bool), Btnz=f(Bnz).astype(bool),
+                    lam=lam[: self.p - 1], parity=par, A_hat=f(Ah), B_hat=f(Bh), nodes=nodes)
+
+    def patches(self):
+        vert = np.zeros(self.npatches, np.int32)
+        ptr = np.zeros(self.npatches + 1, np.int64)
+        dofs, perm = np.zeros(self.sum_nj, np.int32), np.zeros(self.sum_nj, np.int32)
+        cells = np.zeros(self.npatches * (1 << self.dim), np.int32)
+        colour = np.zeros(self.npatches, np.int32)
+        _host_chk(lib().fdmhost_get_patches(self.h, _ptr(vert), _ptr(ptr), _ptr(dofs), _ptr(perm), _ptr(cells),
+                                            _ptr(colour)))
+        return dict(vertex=vert, ptr=ptr, dofs=dofs, perm=perm, cells=cells.reshape(self.npatches, -1),
+                    colour=colour)
+
+    def coarse(self):
+        inv = np.zeros(self.ncoarse * self.ncoarse)
+        ptr = np.zeros(self.ndof + 1, np.int64)
+        col, val = np.zeros(self.P_nnz, np.int32), np.zeros(self.P_nnz)
+        _host_chk(lib().fdmhost_get_coarse(self.h, _ptr(inv), _ptr(ptr), _ptr(col), _ptr(val)))
+        return dict(inverse=inv.reshape(self.ncoarse, self.ncoarse), P_ptr=ptr, P_col=col, P_val=val)
+
+
+class Solver:
+    """GPU handle for one Problem: the device-side TwoLevel / PatchSolver.
+
+    Vector arguments are either torch CUDA float64 tensors (device path) or
+    numpy float64 arrays (host path: copied in and out inside the call, the
+    LinOp drop-in of src/krylov.hpp:10)."""
+
+    def __init__(self, problem: Problem, device: int = 0, stream=None):
+        self.problem = problem
+        self.ndof = problem.ndof
+        h = _vp()
+        rc = lib().fdmhost_attach(problem.h, device, C.byref(h))
+        if rc != 0:
+            raise FdmGpuError(rc, lib().fdmhost_last_error().decode())
+        self.h = h
+        if stream is not None:
+            self.set_stream(stream)
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            try:
+                _lib.fdmgpu_destroy(self.h)
+            except Exception:
+                pass
+            self.h = None
+
+    def _chk(self, rc):
+        if rc != 0:
+            msg = lib().fdmgpu_last_error(self.h).decode()
+            cls = NotSPDError if rc == 2 else IndefiniteError if rc == 3 else FdmGpuError
+            raise cls(rc, msg)
+
+    def set_stream(self, stream):
+        """Run on a caller's CUDA stream (e.g. torch.cuda.current_stream())."""
+        handle = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+        self._chk(lib().fdmgpu_set_stream(self.h, _vp(handle)))
+
+    def synchronize(self):
+        self._chk(lib().fdmgpu_synchronize(self.h))
+
+    def factor(self):
+        self._chk(lib().fdmgpu_factor(self.h))
+
+    def layout(self):
+        L = Layout()
+        self._chk(lib().fdmgpu_get_layout(self.h, C.byref(L)))
+        return {k: getattr(L, k) for k, _ in Layout._fields_ if k != "pad_"}
+
+    def elimination_dofs(self):
+        L = self.layout()
+        out = np.zeros(L["npatch"] * L["n"], np.int32)
+        self._chk(lib().fdmgpu_get_patch_elimination_dofs(self.h, _ptr(out)))
+        return out.reshape(L["npatch"], L["n"])
+
+    def launch_count(self):
+        return int(lib().fdmgpu_launch_count(self.h))
+
+    # ---- operators ---------------------------------------------------------
+    def apply(self, op, x, out=None, omega=0.0):
+        if isinstance(x, np.ndarray):
+            x = np.ascontiguousarray(x, np.float64)
+            out = np.zeros(self.ndof) if out is None else out
+            self._chk(lib().fdmgpu_apply(self.h, op, omega, _ptr(x), _ptr(out), 1))
+            return out
+        import torch
+        assert x.is_cuda and x.dtype == torch.float64 and x.is_contiguous()
+        out = torch.empty_like(x) if out is None else out
+        self._chk(lib().fdmgpu_apply(self.h, op, omega, _vp(x.data_ptr()), _vp(out.data_ptr()), 0))
+        return out
+
+    def apply_St(self, x, out=None):
+        return self.apply(OP_APPLY_ST, x, out)
+
+    def apply_S(self, x, out=None):
+        return self.apply(OP_APPLY_S, x, out)
+
+    def patch_apply(self, x, out=None):
+        return self.apply(OP_PATCH, x, out)
+
+    def smooth(self, x, out=None):
+        return self.apply(OP_SMOOTH, x, out)
+
+    def apply_A(self, x, out=None):
+        return self.apply(OP_A, x, out)
+
+    def vcycle(self, x, out=None, omega=None):
+        return self.apply(OP_VCYCLE, x, out, self.omega if omega is None else omega)
+
+    @property
+    def omega(self):
+        w = C.c_double()
+        self._chk(lib().fdmgpu_get_omega(self.h, C.byref(w)))
+        return w.value
+
+    @omega.setter
+    def omega(self, w):
+        self._chk(lib().fdmgpu_set_omega(self.h, float(w)))
+
+    def calibrate_damping(self, lanczos_steps=10, seed=0x5EED, formula=0):
+        w, lo, hi = C.c_double(), C.c_double(), C.c_double()
+        self._chk(lib().fdmgpu_calibrate_damping(self.h, lanczos_steps, seed, formula, C.byref(w), C.byref(lo),
+                                                 C.byref(hi)))
+        return dict(omega=w.value, lambda_min=lo.value, lambda_max=hi.value)
+
+    def pcg(self, b, x=None, rtol=1e-8, maxit=200, precond=2):
+        """pcg (src/krylov.cpp:29-83): b, x torch CUDA tensors; precond 0/1/2 =
+        identity / smooth / V(1,1) cycle.  Returns (x, report dict)."""
+        import torch
+        x = torch.empty_like(b) if x is None else x
+        rep = KrylovReport()
+        res = np.zeros(max(maxit, 1))
+        self._chk(lib().fdmgpu_pcg(self.h, _vp(b.data_ptr()), _vp(x.data_ptr()), rtol, maxit, precond,
+                                   C.byref(rep), _ptr(res)))
+        d = {k: getattr(rep, k) for k, _ in KrylovReport._fields_}
+        d["converged"] = bool(d["converged"])
+        d["residuals"] = res[: rep.iterations].copy()
+        return x, d

@@ -1,0 +1,673 @@
+// extern "C" implementation of include/fdmgpu.h: uploads, the batched
+// factorisation schedule, and the host-driven V-cycle / PCG / damping
+// calibration around the device operators.  All arithmetic on vectors of
+// length ndof runs on the GPU; the host only sees scalars (dot products) and
+// the Lanczos tridiagonal, as in src/krylov.cpp:29-83.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <random>
+#include <string>
+
+#include "context.hpp"
+
+namespace fdmgpu {
+void analyze_patches(Context& c, int npatch, const int32_t* vertex, const int64_t* ptr, const int32_t* dofs,
+                     const int32_t* perm, const int32_t* star_cells);
+
+void Context::check_ready(bool need_patches, bool need_factor, bool need_coarse) const {
+  if (!have_basis || !have_maps || !have_coeffs)
+    throw Error(FDMGPU_INVALID_ARGUMENT, "fdmgpu: basis, mesh maps and cell coefficients must be set first");
+  if (need_patches && !have_patches) throw Error(FDMGPU_INVALID_ARGUMENT, "fdmgpu: patches not set");
+  if (need_factor && !factored) throw Error(FDMGPU_INVALID_ARGUMENT, "fdmgpu: patches not factored");
+  if (need_coarse && !have_coarse) throw Error(FDMGPU_INVALID_ARGUMENT, "fdmgpu: coarse level not set");
+}
+
+namespace {
+
+// Gather CSR: for each DOF, its (cell, lattice) slots in ascending cell order.
+void build_gather(const std::vector<int32_t>& map, int64_t ndof, std::vector<int32_t>& ptr,
+                  std::vector<int32_t>& idx) {
+  ptr.assign(ndof + 1, 0);
+  for (int32_t g : map) {
+    if (g < 0 || g >= ndof) throw Error(FDMGPU_INVALID_ARGUMENT, "cell map entry out of range");
+    ++ptr[g + 1];
+  }
+  for (int64_t i = 0; i < ndof; ++i) ptr[i + 1] += ptr[i];
+  idx.assign(map.size(), 0);
+  std::vector<int32_t> pos(ptr.begin(), ptr.end() - 1);
+  for (size_t e = 0; e < map.size(); ++e) idx[pos[map[e]]++] = int32_t(e);
+}
+
+double host_dot(Context& c, const double* x, const double* y) {
+  launch_dot_partials(c, c.ndof, x, y, 0);
+  c.h_red.resize(kRedBlocks);
+  FDM_CUDA(cudaMemcpyAsync(c.h_red.data(), c.red.p, kRedBlocks * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+  FDM_CUDA(cudaStreamSynchronize(c.stream));
+  double s = 0.0;
+  for (int b = 0; b < kRedBlocks; ++b) s += c.h_red[b];
+  return s;
+}
+
+void copy_dev(Context& c, double* dst, const double* src) {
+  FDM_CUDA(cudaMemcpyAsync(dst, src, c.ndof * sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
+}
+
+// ---- device operators ----------------------------------------------------------
+void op_transform(Context& c, int dir, const double* in, double* out) {
+  launch_cells_transform(c, dir, in);
+  launch_gather(c, dir, c.E.p, nullptr, out);
+}
+
+void op_patch(Context& c, const double* in, double* out) {
+  launch_patch_solve(c, in);
+  launch_patch_gather(c, out);
+}
+
+void op_smooth(Context& c, const double* r, double* z) {  // src/schwarz.cpp:121-123
+  op_transform(c, 0, r, c.w[6].p);
+  op_patch(c, c.w[6].p, c.w[7].p);
+  op_transform(c, 1, c.w[7].p, z);
+}
+
+void op_A(Context& c, const double* x, double* y) {  // src/assembly.cpp:56-88
+  launch_cells_stiffness(c, x);
+  launch_gather(c, 2, c.E.p, x, y);
+}
+
+void op_vcycle(Context& c, double omega, const double* r, double* z) {  // src/schwarz.cpp:125-133
+  double* t1 = c.w[3].p;
+  double* t2 = c.w[4].p;
+  double* t3 = c.w[5].p;
+  op_smooth(c, r, t1);
+  launch_axpby(c, c.ndof, omega, t1, 0.0, t1, z);  // z = omega * smooth(r)
+  op_A(c, z, t2);
+  launch_axpby(c, c.ndof, 1.0, r, -1.0, t2, t3);  // r1 = r - A z
+  launch_restrict(c, t3, c.rc.p);
+  launch_coarse_solve(c, c.rc.p, c.zc.p);
+  launch_prolong_add(c, c.zc.p, z);  // z += P A_c^{-1} P^T r1
+  op_A(c, z, t2);
+  launch_axpby(c, c.ndof, 1.0, r, -1.0, t2, t3);  // r2 = r - A z
+  op_smooth(c, t3, t1);
+  launch_axpby(c, c.ndof, omega, t1, 1.0, z, z);  // z += omega * smooth(r2)
+}
+
+void op_precond(Context& c, int precond, double omega, const double* r, double* z) {
+  if (precond == 0)
+    copy_dev(c, z, r);
+  else if (precond == 1)
+    op_smooth(c, r, z);
+  else
+    op_vcycle(c, omega, r, z);
+}
+
+// Extremal eigenvalues of a symmetric tridiagonal (Sturm bisection); the
+// reference uses Eigen::SelfAdjointEigenSolver (src/krylov.cpp:18-27).
+std::pair<double, double> tridiag_extremes(const std::vector<double>& dg, const std::vector<double>& off) {
+  const int n = int(dg.size());
+  if (n == 0) return {0.0, 0.0};
+  double lo = dg[0], hi = dg[0];
+  for (int i = 0; i < n; ++i) {
+    const double r = (i > 0 ? std::abs(off[i - 1]) : 0.0) + (i + 1 < n ? std::abs(off[i]) : 0.0);
+    lo = std::min(lo, dg[i] - r);
+    hi = std::max(hi, dg[i] + r);
+  }
+  auto count = [&](double x) {
+    int cnt = 0;
+    double q = 1.0;
+    for (int i = 0; i < n; ++i) {
+      q = dg[i] - x - (i > 0 ? off[i - 1] * off[i - 1] / q : 0.0);
+      if (q == 0.0) q = -1e-300;
+      if (q < 0) ++cnt;
+    }
+    return cnt;
+  };
+  auto kth = [&](int k) {
+    double a = lo, b = hi;
+    for (int it = 0; it < 200; ++it) {
+      const double m = 0.5 * (a + b);
+      if (m <= a || m >= b) break;
+      if (count(m) > k)
+        b = m;
+      else
+        a = m;
+    }
+    return 0.5 * (a + b);
+  };
+  return {kth(0), kth(n - 1)};
+}
+
+// pcg (src/krylov.cpp:29-83) on device vectors; x must not alias b.
+void run_pcg(Context& c, const double* b, double* x, double rtol, int maxit, int precond, double omega,
+             fdmgpu_krylov_report* rep, std::vector<double>* residuals) {
+  const auto t0 = std::chrono::steady_clock::now();
+  fdmgpu_krylov_report R{};
+  double* r = c.w[0].p;
+  double* z = c.w[1].p;
+  double* p = c.w[2].p;
+  double* Ap = c.w[8].p;
+  FDM_CUDA(cudaMemsetAsync(x, 0, c.ndof * sizeof(double), c.stream));
+  const double bnorm = std::sqrt(host_dot(c, b, b));
+  if (residuals) residuals->clear();
+  if (bnorm == 0.0) {
+    R.converged = 1;
+    R.kappa = 1.0;
+    *rep = R;
+    return;
+  }
+  copy_dev(c, r, b);
+  op_precond(c, precond, omega, r, z);
+  copy_dev(c, p, z);
+  double rz = host_dot(c, r, z);
+  std::vector<double> alphas, betas;
+  for (int k = 0; k < maxit; ++k) {
+    op_A(c, p, Ap);
+    const double pAp = host_dot(c, p, Ap);
+    if (!(pAp > 0.0))
+      throw Error(FDMGPU_INDEFINITE, "pcg: indefinite operator at iteration " + std::to_string(k + 1));
+    const double alpha = rz / pAp;
+    launch_axpby(c, c.ndof, alpha, p, 1.0, x, x);
+    launch_axpby(c, c.ndof, -alpha, Ap, 1.0, r, r);
+    alphas.push_back(alpha);
+    const double res = std::sqrt(host_dot(c, r, r)) / bnorm;
+    if (residuals) residuals->push_back(res);
+    R.final_residual = res;
+    R.iterations = k + 1;
+    if (res <= rtol) {
+      R.converged = 1;
+      break;
+    }
+    op_precond(c, precond, omega, r, z);
+    const double rz_new = host_dot(c, r, z);
+    const double beta = rz_new / rz;
+    betas.push_back(beta);
+    rz = rz_new;
+    launch_axpby(c, c.ndof, 1.0, z, beta, p, p);
+  }
+  std::vector<double> td, to;
+  for (size_t k = 0; k < alphas.size(); ++k) {
+    double dk = 1.0 / alphas[k];
+    if (k > 0) dk += betas[k - 1] / alphas[k - 1];
+    td.push_back(dk);
+    if (k + 1 < alphas.size()) to.push_back(std::sqrt(betas[k]) / alphas[k]);
+  }
+  auto [lmin, lmax] = tridiag_extremes(td, to);
+  R.lambda_min = lmin;
+  R.lambda_max = lmax;
+  R.kappa = lmin > 0 ? lmax / lmin : 0.0;
+  R.wall_time = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  *rep = R;
+}
+
+std::vector<double> random_free(Context& c, uint64_t seed) {
+  std::mt19937_64 rng(seed);
+  std::uniform_real_distribution<double> uni(-1.0, 1.0);
+  std::vector<double> b(c.ndof);
+  for (auto& v : b) v = uni(rng);
+  for (int64_t i = 0; i < c.ndof; ++i)
+    if (c.h_constrained[i]) b[i] = 0.0;
+  return b;
+}
+
+template <class Fn>
+fdmgpu_status guarded(fdmgpu_handle h, Fn&& fn) {
+  Context* c = reinterpret_cast<Context*>(h);
+  if (!c) return FDMGPU_INVALID_ARGUMENT;
+  try {
+    if (c->device >= 0) cudaSetDevice(c->device);
+    fn(*c);
+    return FDMGPU_OK;
+  } catch (const Error& e) {
+    c->err = e.what();
+    return e.status;
+  } catch (const std::bad_alloc&) {
+    c->err = "host allocation failed";
+    return FDMGPU_OUT_OF_MEMORY;
+  } catch (const std::exception& e) {
+    c->err = e.what();
+    return FDMGPU_INVALID_ARGUMENT;
+  }
+}
+
+}  // namespace
+}  // namespace fdmgpu
+
+using fdmgpu::Context;
+using fdmgpu::Error;
+
+struct fdmgpu_context : fdmgpu::Context {};
+
+extern "C" {
+
+const char* fdmgpu_last_error(fdmgpu_handle h) { return h ? h->err.c_str() : "null handle"; }
+
+const char* fdmgpu_status_string(fdmgpu_status s) {
+  switch (s) {
+    case FDMGPU_OK: return "ok";
+    case FDMGPU_INVALID_ARGUMENT: return "invalid argument";
+    case FDMGPU_NOT_SPD: return "matrix not SPD";
+    case FDMGPU_INDEFINITE: return "indefinite operator";
+    case FDMGPU_OUT_OF_MEMORY: return "out of memory";
+    case FDMGPU_CUDA_ERROR: return "CUDA error";
+    case FDMGPU_UNSUPPORTED: return "unsupported";
+  }
+  return "unknown";
+}
+
+fdmgpu_status fdmgpu_create(fdmgpu_handle* out, int32_t dim, int32_t p, int32_t ncells, int64_t ndof, int32_t device) {
+  if (!out) return FDMGPU_INVALID_ARGUMENT;
+  *out = nullptr;
+  if ((dim != 2 && dim != 3) || p < 1 || ncells < 1 || ndof < 1) return FDMGPU_INVALID_ARGUMENT;
+  auto* c = new fdmgpu_context();
+  c->device = device;
+  c->dim = dim;
+  c->p = p;
+  c->n1 = p + 1;
+  c->npc = dim == 3 ? c->n1 * c->n1 * c->n1 : c->n1 * c->n1;
+  c->ncells = ncells;
+  c->ndof = ndof;
+  fdmgpu_status st = fdmgpu::guarded(c, [](Context& cc) {
+    int n = 0;
+    FDM_CUDA(cudaGetDeviceCount(&n));
+    if (cc.device < 0 || cc.device >= n) throw Error(FDMGPU_CUDA_ERROR, "no such CUDA device");
+    FDM_CUDA(cudaSetDevice(cc.device));
+    FDM_CUDA(cudaStreamCreateWithFlags(&cc.stream, cudaStreamNonBlocking));
+    cc.own_stream = true;
+    cc.E.alloc(size_t(cc.ncells) * cc.npc);
+    for (auto& v : cc.w) v.alloc(cc.ndof);
+    cc.red.alloc(4 * fdmgpu::kRedBlocks);
+    cc.d_err.alloc(1);
+  });
+  if (st != FDMGPU_OK) {
+    *out = nullptr;
+    delete c;
+    return st;
+  }
+  *out = c;
+  return FDMGPU_OK;
+}
+
+fdmgpu_status fdmgpu_destroy(fdmgpu_handle h) {
+  if (!h) return FDMGPU_INVALID_ARGUMENT;
+  if (h->device >= 0) cudaSetDevice(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  cudaStream_t s = h->own_stream ? h->stream : nullptr;
+  delete h;
+  if (s) cudaStreamDestroy(s);
+  return FDMGPU_OK;
+}
+
+fdmgpu_status fdmgpu_set_stream(fdmgpu_handle h, void* stream) {
+  return fdmgpu::guarded(h, [&](Context& c) {
+    FDM_CUDA(cudaStreamSynchronize(c.stream));
+    if (c.own_stream) cudaStreamDestroy(c.stream);
+    c.stream = static_cast<cudaStream_t>(stream);
+    c.own_stream = false;
+  });
+}
+
+fdmgpu_status fdmgpu_synchronize(fdmgpu_handle h) {
+  return fdmgpu::guarded(h, [](Context& c) { FDM_CUDA(cudaStreamSynchronize(c.stream)); });
+}
+
+fdmgpu_status fdmgpu_set_basis(fdmgpu_handle h, const double* S, const double* lambda, const double* A_t,
+                               const double* B_t, const uint8_t* A_t_pattern, const uint8_t* B_t_pattern,
+                               const double* A_hat, const double* B_hat, int32_t q, const double* Vq,
+                               const double* Dq, const double* wq) {
+  (void)lambda;
+  return fdmgpu::guarded(h, [&](Context& c) {
+    if (!S || !A_t || !B_t || !A_t_pattern || !B_t_pattern || !A_hat || !B_hat)
+      throw Error(FDMGPU_INVALID_ARGUMENT, "set_basis: null array");
+    const int n1 = c.n1, nn = n1 * n1;
+    std::vector<double> St(nn), At(nn), Bt(nn);
+    for (int i = 0; i < n1; ++i)
+      for (int j = 0; j < n1; ++j) St[i + n1 * j] = S[j + n1 * i];
+    c.h_Anz.assign(A_t_pattern, A_t_pattern + nn);
+    c.h_Bnz.assign(B_t_pattern, B_t_pattern + nn);
+    for (int k = 0; k < nn; ++k) {  // values outside the stored pattern are structural zeros
+      At[k] = c.h_Anz[k] ? A_t[k] : 0.0;
+      Bt[k] = c.h_Bnz[k] ? B_t[k] : 0.0;
+    }
+    c.h_At = At;
+    c.h_Bt = Bt;
+    c.S.upload(S, nn, c.stream);
+    c.St.upload(St, c.stream);
+    c.At.upload(At, c.stream);
+    c.Bt.upload(Bt, c.stream);
+    c.Ahat.upload(A_hat, nn, c.stream);
+    c.Bhat.upload(B_hat, nn, c.stream);
+    c.q = q;
+    if (q > 0 && Vq && Dq && wq) {
+      c.Vq.upload(Vq, size_t(q) * n1, c.stream);
+      c.Dq.upload(Dq, size_t(q) * n1, c.stream);
+      c.wq.upload(wq, q, c.stream);
+    }
+    FDM_CUDA(cudaStreamSynchronize(c.stream));
+    c.have_basis = true;
+  });
+}
+
+fdmgpu_status fdmgpu_set_mesh_maps(fdmgpu_handle h, const int32_t* cell_dofs, const int32_t* cell_modes,
+                                   const double* mode_signs, const double* multiplicity, const uint8_t* constrained) {
+  return fdmgpu::guarded(h, [&](Context& c) {
+    if (!cell_dofs || !multiplicity || !constrained) throw Error(FDMGPU_INVALID_ARGUMENT, "set_mesh_maps: null array");
+    const size_t nm = size_t(c.ncells) * c.npc;
+    c.h_cell_dofs.assign(cell_dofs, cell_dofs + nm);
+    c.h_cell_modes.assign(cell_modes ? cell_modes : cell_dofs, (cell_modes ? cell_modes : cell_dofs) + nm);
+    c.modes_alias = c.h_cell_modes == c.h_cell_dofs;
+    c.h_constrained.assign(constrained, constrained + c.ndof);
+    std::vector<double> inv(c.ndof);
+    for (int64_t i = 0; i < c.ndof; ++i) {
+      if (!(multiplicity[i] > 0)) throw Error(FDMGPU_INVALID_ARGUMENT, "set_mesh_maps: multiplicity must be > 0");
+      inv[i] = 1.0 / multiplicity[i];
+    }
+    std::vector<int32_t> ptr, idx;
+    fdmgpu::build_gather(c.h_cell_dofs, c.ndof, ptr, idx);
+    c.cell_dofs.upload(c.h_cell_dofs, c.stream);
+    c.g_ptr.upload(ptr, c.stream);
+    c.g_idx.upload(idx, c.stream);
+    if (!c.modes_alias) {
+      fdmgpu::build_gather(c.h_cell_modes, c.ndof, ptr, idx);
+      c.cell_modes.upload(c.h_cell_modes, c.stream);
+      c.gm_ptr.upload(ptr, c.stream);
+      c.gm_idx.upload(idx, c.stream);
+    } else {
+      c.cell_modes.upload(c.h_cell_dofs, c.stream);
+    }
+    bool unit = true;
+    if (mode_signs)
+      for (size_t k = 0; k < nm; ++k) unit = unit && mode_signs[k] == 1.0;
+    if (!unit)
+      c.mode_sign.upload(mode_signs, nm, c.stream);
+    else
+      c.mode_sign.reset();
+    c.inv_mult.upload(inv, c.stream);
+    c.constrained.upload(c.h_constrained, c.stream);
+    FDM_CUDA(cudaStreamSynchronize(c.stream));
+    c.have_maps = true;
+  });
+}
+
+fdmgpu_status fdmgpu_set_cell_coeffs(fdmgpu_handle h, const uint8_t* kind, const double* mu, const double* xyz,
+                                     const double* kappa) {
+  return fdmgpu::guarded(h, [&](Context& c) {
+    if (!kind || !mu) throw Error(FDMGPU_INVALID_ARGUMENT, "set_cell_coeffs: null array");
+    c.all_cartesian = true;
+    for (int k = 0; k < c.ncells; ++k) c.all_cartesian = c.all_cartesian && kind[k] == 0;
+    if (!c.all_cartesian && !xyz)
+      throw Error(FDMGPU_INVALID_ARGUMENT, "set_cell_coeffs: non-Cartesian cells need corner coordinates");
+    c.kind.upload(kind, c.ncells, c.stream);
+    c.h_mu.assign(mu, mu + size_t(c.ncells) * c.dim);
+    c.mu.upload(c.h_mu, c.stream);
+    if (xyz) c.xyz.upload(xyz, size_t(c.ncells) * (1 << c.dim) * 3, c.stream);
+    std::vector<double> kap(c.ncells, 1.0);
+    if (kappa) kap.assign(kappa, kappa + c.ncells);
+    c.kappa.upload(kap, c.stream);
+    FDM_CUDA(cudaStreamSynchronize(c.stream));
+    c.have_coeffs = true;
+    c.factored = false;
+  });
+}
+
+fdmgpu_status fdmgpu_set_patches(fdmgpu_handle h, int32_t npatch, const int32_t* vertex, const int64_t* ptr,
+                                 const int32_t* dofs, const int32_t* perm, const int32_t* star_cells) {
+  return fdmgpu::guarded(h, [&](Context& c) {
+    c.check_ready(false, false, false);
+    if (npatch < 1 || !vertex || !ptr || !dofs || !perm || !star_cells)
+      throw Error(FDMGPU_INVALID_ARGUMENT, "set_patches: bad arguments");
+    if (c.mode_sign.p || !c.modes_alias)
+      throw Error(FDMGPU_UNSUPPORTED, "set_patches: facet mode flips (2D non-lattice meshes) are not supported");
+    fdmgpu::analyze_patches(c, npatch, vertex, ptr, dofs, perm, star_cells);
+    c.npatch = npatch;
+    const auto& L = c.L;
+    const size_t tile_bytes = size_t(npatch) * L.ntiles * fdmgpu::kTile * fdmgpu::kTile * sizeof(double);
+    size_t free_b = 0, total_b = 0;
+    FDM_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    if (tile_bytes + size_t(npatch) * L.n * 12 > free_b)
+      throw Error(FDMGPU_OUT_OF_MEMORY, "set_patches: factor needs " + std::to_string(tile_bytes >> 20) +
+                                            " MiB, free " + std::to_string(free_b >> 20) + " MiB");
+    c.pdofs.upload(c.h_pdofs, c.stream);
+    c.lat.upload(L.lat, c.stream);
+    c.pos_of_lat.upload(L.pos_of_lat, c.stream);
+    c.pcells.upload(c.h_pcells, c.stream);
+    c.tile_row.upload(L.tile_row, c.stream);
+    c.tile_col.upload(L.tile_col, c.stream);
+    c.col_start.upload(L.col_start, c.stream);
+    c.pair_ptr.upload(L.pair_ptr, c.stream);
+    if (L.pair_a.empty()) {
+      c.pair_a.alloc(1);
+      c.pair_b.alloc(1);
+    } else {
+      c.pair_a.upload(L.pair_a, c.stream);
+      c.pair_b.upload(L.pair_b, c.stream);
+    }
+    std::vector<int32_t> pptr, pidx;
+    fdmgpu::build_gather(c.h_pdofs, c.ndof, pptr, pidx);  // ascending (patch, position) per DOF
+    c.pg_ptr.upload(pptr, c.stream);
+    c.pg_idx.upload(pidx, c.stream);
+    c.corr.alloc(size_t(npatch) * L.n);
+    c.tiles.alloc(size_t(npatch) * L.ntiles * fdmgpu::kTile * fdmgpu::kTile);
+    FDM_CUDA(cudaStreamSynchronize(c.stream));
+    c.have_patches = true;
+    c.factored = false;
+  });
+}
+
+fdmgpu_status fdmgpu_set_coarse(fdmgpu_handle h, int32_t ndof_c, const double* cinv, const int64_t* P_ptr,
+                                const int32_t* P_col, const double* P_val) {
+  return fdmgpu::guarded(h, [&](Context& c) {
+    if (ndof_c < 1 || !cinv || !P_ptr || !P_col || !P_val) throw Error(FDMGPU_INVALID_ARGUMENT, "set_coarse: bad args");
+    c.nc = ndof_c;
+    c.cinv.upload(cinv, size_t(ndof_c) * ndof_c, c.stream);
+    const int64_t nnz = P_ptr[c.ndof];
+    std::vector<int32_t> ptr(c.ndof + 1), tptr(ndof_c + 1, 0), tcol(nnz);
+    std::vector<double> tval(nnz);
+    for (int64_t i = 0; i <= c.ndof; ++i) ptr[i] = int32_t(P_ptr[i]);
+    for (int64_t qq = 0; qq < nnz; ++qq) ++tptr[P_col[qq] + 1];
+    for (int i = 0; i < ndof_c; ++i) tptr[i + 1] += tptr[i];
+    std::vector<int32_t> pos(tptr.begin(), tptr.end() - 1);
+    for (int64_t i = 0; i < c.ndof; ++i)
+      for (int64_t qq = P_ptr[i]; qq < P_ptr[i + 1]; ++qq) {
+        tcol[pos[P_col[qq]]] = int32_t(i);
+        tval[pos[P_col[qq]]++] = P_val[qq];
+      }
+    c.P_ptr.upload(ptr, c.stream);
+    c.P_col.upload(P_col, nnz, c.stream);
+    c.P_val.upload(P_val, nnz, c.stream);
+    c.PT_ptr.upload(tptr, c.stream);
+    c.PT_col.upload(tcol, c.stream);
+    c.PT_val.upload(tval, c.stream);
+    c.rc.alloc(ndof_c);
+    c.zc.alloc(ndof_c);
+    FDM_CUDA(cudaStreamSynchronize(c.stream));
+    c.have_coarse = true;
+  });
+}
+
+fdmgpu_status fdmgpu_factor(fdmgpu_handle h) {
+  return fdmgpu::guarded(h, [&](Context& c) {
+    c.check_ready(true, false, false);
+    const unsigned long long none = ~0ULL;
+    FDM_CUDA(cudaMemcpyAsync(c.d_err.p, &none, sizeof(none), cudaMemcpyHostToDevice, c.stream));
+    fdmgpu::launch_patch_assemble(c);
+    for (int K = 0; K < c.L.nT; ++K) {
+      fdmgpu::launch_patch_update(c, K);
+      fdmgpu::launch_patch_trsm(c, K);
+    }
+    unsigned long long e = 0;
+    FDM_CUDA(cudaMemcpyAsync(&e, c.d_err.p, sizeof(e), cudaMemcpyDeviceToHost, c.stream));
+    FDM_CUDA(cudaStreamSynchronize(c.stream));
+    c.factored = false;
+    if (e != none)
+      throw Error(FDMGPU_NOT_SPD, "cholesky: matrix not SPD at pivot " + std::to_string(e & 0xffffffffULL) +
+                                      " (patch " + std::to_string(e >> 32) + ")");
+    c.factored = true;
+  });
+}
+
+fdmgpu_status fdmgpu_get_layout(fdmgpu_handle h, fdmgpu_layout* out) {
+  return fdmgpu::guarded(h, [&](Context& c) {
+    c.check_ready(true, false, false);
+    fdmgpu_layout L{};
+    L.npatch = c.npatch;
+    L.n = c.L.n;
+    L.n_interior = c.L.nI;
+    L.n_interface = c.L.m;
+    L.tile = fdmgpu::kTile;
+    L.tile_cols = c.L.nT;
+    L.tiles = c.L.ntiles;
+    L.nnz_L = c.L.nnz_L;
+    L.flops_ref = c.L.flops_ref;
+    L.factor_bytes = int64_t(c.tiles.bytes());
+    L.tile_gemms = c.L.tile_gemms;
+    *out = L;
+  });
+}
+
+fdmgpu_status fdmgpu_get_patch_elimination_dofs(fdmgpu_handle h, int32_t* out) {
+  return fdmgpu::guarded(h, [&](Context& c) {
+    c.check_ready(true, false, false);
+    std::memcpy(out, c.h_pdofs.data(), c.h_pdofs.size() * sizeof(int32_t));
+  });
+}
+
+fdmgpu_status fdmgpu_apply(fdmgpu_handle h, int32_t op, double omega, const double* in, double* out, int32_t host) {
+  return fdmgpu::guarded(h, [&](Context& c) {
+    if (!in || !out) throw Error(FDMGPU_INVALID_ARGUMENT, "apply: null vector");
+    const bool needs_factor = op == FDMGPU_OP_PATCH || op == FDMGPU_OP_SMOOTH || op == FDMGPU_OP_VCYCLE;
+    c.check_ready(needs_factor, needs_factor, op == FDMGPU_OP_VCYCLE);
+    const double* din = in;
+    double* dout = out;
+    const size_t bytes = c.ndof * sizeof(double);
+    if (host) {
+      FDM_CUDA(cudaMemcpyAsync(c.w[9].p, in, bytes, cudaMemcpyHostToDevice, c.stream));
+      din = c.w[9].p;
+      dout = c.w[10].p;
+    } else if (in == out) {
+      throw Error(FDMGPU_INVALID_ARGUMENT, "apply: in and out must not alias");
+    }
+    switch (op) {
+      case FDMGPU_OP_APPLY_ST: fdmgpu::op_transform(c, 0, din, dout); break;
+      case FDMGPU_OP_APPLY_S: fdmgpu::op_transform(c, 1, din, dout); break;
+      case FDMGPU_OP_PATCH: fdmgpu::op_patch(c, din, dout); break;
+      case FDMGPU_OP_SMOOTH: fdmgpu::op_smooth(c, din, dout); break;
+      case FDMGPU_OP_A: fdmgpu::op_A(c, din, dout); break;
+      case FDMGPU_OP_VCYCLE: fdmgpu::op_vcycle(c, omega, din, dout); break;
+      default: throw Error(FDMGPU_INVALID_ARGUMENT, "apply: unknown operator id");
+    }
+    if (host) {
+      FDM_CUDA(cudaMemcpyAsync(out, dout, bytes, cudaMemcpyDeviceToHost, c.stream));
+      FDM_CUDA(cudaStreamSynchronize(c.stream));
+    }
+  });
+}
+
+fdmgpu_status fdmgpu_transform(fdmgpu_handle h, int32_t dir, const double* in, double* out) {
+  return fdmgpu_apply(h, dir == 0 ? FDMGPU_OP_APPLY_ST : FDMGPU_OP_APPLY_S, 0.0, in, out, 0);
+}
+fdmgpu_status fdmgpu_patch_solve(fdmgpu_handle h, const double* r, double* z) {
+  return fdmgpu_apply(h, FDMGPU_OP_PATCH, 0.0, r, z, 0);
+}
+fdmgpu_status fdmgpu_smooth(fdmgpu_handle h, const double* r, double* z) {
+  return fdmgpu_apply(h, FDMGPU_OP_SMOOTH, 0.0, r, z, 0);
+}
+fdmgpu_status fdmgpu_apply_A(fdmgpu_handle h, const double* x, double* y) {
+  return fdmgpu_apply(h, FDMGPU_OP_A, 0.0, x, y, 0);
+}
+fdmgpu_status fdmgpu_vcycle(fdmgpu_handle h, double omega, const double* r, double* z) {
+  return fdmgpu_apply(h, FDMGPU_OP_VCYCLE, omega, r, z, 0);
+}
+
+fdmgpu_status fdmgpu_pcg(fdmgpu_handle h, const double* b, double* x, double rtol, int32_t maxit, int32_t precond,
+                         fdmgpu_krylov_report* report, double* residuals) {
+  return fdmgpu::guarded(h, [&](Context& c) {
+    if (!b || !x || !report || maxit < 0 || b == x) throw Error(FDMGPU_INVALID_ARGUMENT, "pcg: bad arguments");
+    c.check_ready(precond > 0, precond > 0, precond == 2);
+    std::vector<double> res;
+    fdmgpu::run_pcg(c, b, x, rtol, maxit, precond, c.omega, report, residuals ? &res : nullptr);
+    if (residuals) std::copy(res.begin(), res.end(), residuals);
+  });
+}
+
+fdmgpu_status fdmgpu_calibrate_damping(fdmgpu_handle h, int32_t lanczos_steps, uint32_t seed, int32_t formula,
+                                       double* omega, double* lambda_min, double* lambda_max) {
+  return fdmgpu::guarded(h, [&](Context& c) {
+    c.check_ready(true, true, true);
+    double* b = c.w[11].p;
+    double* x = c.w[9].p;
+    fdmgpu_krylov_report rep{};
+    // estimate_damping (src/schwarz.cpp:97-119): CG-Lanczos of the smoother.
+    auto hb = fdmgpu::random_free(c, seed);
+    FDM_CUDA(cudaMemcpyAsync(b, hb.data(), c.ndof * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+    double est_omega = 1.0, est_lmin = 0.0, est_lmax = 0.0;
+    try {
+      fdmgpu::run_pcg(c, b, x, 1e-12, lanczos_steps, 1, 1.0, &rep, nullptr);
+      if (rep.lambda_min > 0.0 && rep.lambda_max > 0.0) {
+        est_lmin = rep.lambda_min;
+        est_lmax = rep.lambda_max;
+        est_omega = formula == 2 ? 0.5 * (est_lmax + est_lmin) : 2.0 / (est_lmax + est_lmin);
+      }
+    } catch (const Error& e) {
+      if (e.status != FDMGPU_INDEFINITE) throw;
+    }
+    c.lambda_min = est_lmin;
+    c.lambda_max = est_lmax;
+    if (est_lmax <= 0.0) {
+      c.omega = 1.0;
+    } else if (formula != 0) {
+      c.omega = est_omega;
+    } else {
+      // Two-grid calibration (src/schwarz.cpp:184-227).
+      const double omega0 = 1.0 / est_lmax;
+      auto hb2 = fdmgpu::random_free(c, uint64_t(seed) + 1);
+      FDM_CUDA(cudaMemcpyAsync(b, hb2.data(), c.ndof * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+      auto cycle_kappa = [&](double w) {
+        try {
+          fdmgpu::run_pcg(c, b, x, 1e-12, lanczos_steps, 2, w, &rep, nullptr);
+          if (rep.lambda_min <= 0.0) return std::numeric_limits<double>::infinity();
+          return rep.lambda_max / rep.lambda_min;
+        } catch (const Error& e) {
+          if (e.status != FDMGPU_INDEFINITE) throw;
+          return std::numeric_limits<double>::infinity();
+        }
+      };
+      double mu_c = est_lmin;
+      try {
+        fdmgpu::run_pcg(c, b, x, 1e-12, lanczos_steps, 2, omega0, &rep, nullptr);
+        if (rep.lambda_min > 0.0 && rep.lambda_min < 1.0) mu_c = (1.0 - std::sqrt(1.0 - rep.lambda_min)) / omega0;
+      } catch (const Error& e) {
+        if (e.status != FDMGPU_INDEFINITE) throw;
+      }
+      mu_c = std::min(std::max(mu_c, est_lmin), est_lmax);
+      double best_omega = 2.0 / (mu_c + est_lmax);
+      double best_kappa = cycle_kappa(best_omega);
+      for (double f : {0.8, 1.2, 1.4}) {
+        const double w = f * omega0;
+        if (w >= 2.0 * omega0 || std::abs(w - best_omega) < 1e-3) continue;
+        const double k = cycle_kappa(w);
+        if (k < best_kappa) {
+          best_kappa = k;
+          best_omega = w;
+        }
+      }
+      c.omega = best_omega;
+    }
+    if (omega) *omega = c.omega;
+    if (lambda_min) *lambda_min = c.lambda_min;
+    if (lambda_max) *lambda_max = c.lambda_max;
+  });
+}
+
+fdmgpu_status fdmgpu_set_omega(fdmgpu_handle h, double omega) {
+  return fdmgpu::guarded(h, [&](Context& c) { c.omega = omega; });
+}
+
+fdmgpu_status fdmgpu_get_omega(fdmgpu_handle h, double* omega) {
+  return fdmgpu::guarded(h, [&](Context& c) { *omega = c.omega; });
+}
+
+int64_t fdmgpu_launch_count(fdmgpu_handle h) { return h ? h->launches : -1; }
+
+}  // extern "C"

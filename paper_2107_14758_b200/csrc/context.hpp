@@ -1,0 +1,144 @@
+// Internal state of an fdmgpu handle (see include/fdmgpu.h) and the launch
+// interface between the host orchestration (capi.cpp) and the sm_100a
+// kernels (kernels/*.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/fdmgpu.h"
+
+namespace fdmgpu {
+
+constexpr int kTile = 64;  // dense tile edge of the interface factor
+
+struct Error : std::runtime_error {
+  fdmgpu_status status;
+  Error(fdmgpu_status s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+
+#define FDM_CUDA(call)                                                                        \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess)                                                                    \
+      throw ::fdmgpu::Error(e_ == cudaErrorMemoryAllocation ? FDMGPU_OUT_OF_MEMORY : FDMGPU_CUDA_ERROR, \
+                            std::string(#call) + ": " + cudaGetErrorString(e_));              \
+  } while (0)
+
+// Owning device allocation.
+template <class T>
+struct DevArray {
+  T* p = nullptr;
+  size_t n = 0;
+  DevArray() = default;
+  DevArray(const DevArray&) = delete;
+  DevArray& operator=(const DevArray&) = delete;
+  ~DevArray() { reset(); }
+  void reset() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void alloc(size_t count) {
+    reset();
+    if (count == 0) return;
+    FDM_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    n = count;
+  }
+  void upload(const T* host, size_t count, cudaStream_t s) {
+    alloc(count);
+    if (count) FDM_CUDA(cudaMemcpyAsync(p, host, count * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+  void upload(const std::vector<T>& v, cudaStream_t s) { upload(v.data(), v.size(), s); }
+  size_t bytes() const { return n * sizeof(T); }
+};
+
+// Shared symbolic structure of all interior vertex-star patches (one
+// canonical lattice pattern).
+struct PatchLayout {
+  int n = 0, nI = 0, m = 0, mpad = 0, nT = 0, ntiles = 0;
+  int span = 0;                      // 2p+1 lattice points per axis
+  std::vector<int32_t> lat;          // n: packed patch-lattice coords P (elimination order)
+  std::vector<int32_t> pos_of_lat;   // span^d: elimination position or -1
+  std::vector<int32_t> tile_row, tile_col, col_start;  // tile pattern, column-major order
+  std::vector<int32_t> pair_ptr, pair_a, pair_b;       // left-looking update pairs per tile
+  int64_t nnz_L = 0, flops_ref = 0, tile_gemms = 0;
+};
+
+struct Context {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  std::string err;
+  int64_t launches = 0;
+
+  int dim = 3, p = 1, n1 = 2, npc = 8, ncells = 0;
+  int64_t ndof = 0;
+
+  // basis
+  DevArray<double> S, St, Ahat, Bhat, At, Bt, Vq, Dq, wq;
+  std::vector<double> h_At, h_Bt;
+  std::vector<uint8_t> h_Anz, h_Bnz;
+  int q = 0;
+  bool have_basis = false;
+
+  // maps
+  DevArray<int32_t> cell_dofs, cell_modes, g_ptr, g_idx, gm_ptr, gm_idx;
+  DevArray<double> mode_sign, inv_mult, E, E2;
+  DevArray<uint8_t> constrained;
+  std::vector<int32_t> h_cell_dofs, h_cell_modes;
+  std::vector<uint8_t> h_constrained;
+  bool modes_alias = true, have_maps = false;
+
+  // cell coefficients
+  DevArray<uint8_t> kind;
+  DevArray<double> mu, xyz, kappa;
+  std::vector<double> h_mu;
+  bool all_cartesian = true, have_coeffs = false;
+
+  // patches
+  int npatch = 0;
+  PatchLayout L;
+  DevArray<int32_t> pdofs, lat, pos_of_lat, pcells, pg_ptr, pg_idx;
+  DevArray<int32_t> tile_row, tile_col, col_start, pair_ptr, pair_a, pair_b;
+  DevArray<double> corr, tiles;
+  std::vector<int32_t> h_pdofs, h_pcells;
+  bool have_patches = false, factored = false;
+  DevArray<unsigned long long> d_err;
+
+  // coarse level
+  int nc = 0;
+  DevArray<double> cinv, P_val, PT_val, rc, zc;
+  DevArray<int32_t> P_ptr, P_col, PT_ptr, PT_col;
+  bool have_coarse = false;
+
+  // work vectors (ndof)
+  DevArray<double> w[12];
+  DevArray<double> red;   // reduction partials
+  std::vector<double> h_red;
+  double omega = 1.0, lambda_min = 0.0, lambda_max = 0.0;
+
+  void check_ready(bool need_patches, bool need_factor, bool need_coarse) const;
+};
+
+// ---- kernel launchers (kernels/*.cu) -------------------------------------------
+void launch_cells_transform(Context& c, int dir, const double* in);  // writes c.E
+void launch_gather(Context& c, int mode, const double* E, const double* x, double* out);
+void launch_cells_stiffness(Context& c, const double* x);            // writes c.E
+void launch_patch_assemble(Context& c);
+void launch_patch_update(Context& c, int K);
+void launch_patch_trsm(Context& c, int K);
+void launch_patch_solve(Context& c, const double* r_modal);          // writes c.corr
+void launch_patch_gather(Context& c, double* z_modal);
+void launch_axpby(Context& c, int64_t n, double a, const double* x, double b, const double* y, double* out);
+void launch_dot_partials(Context& c, int64_t n, const double* x, const double* y, int k);
+void launch_restrict(Context& c, const double* fine, double* coarse);
+void launch_coarse_solve(Context& c, const double* rc, double* zc);
+void launch_prolong_add(Context& c, const double* coarse, double* fine);
+constexpr int kRedBlocks = 296;  // fixed reduction grid: deterministic partial sums
+
+}  // namespace fdmgpu

@@ -1,0 +1,170 @@
+// extern "C" surface of the host setup (the mirror of the reference's
+// cartesian_mesh / q_space / make_bundle / build_patch_solver inputs) and
+// fdmhost_attach, which feeds a problem into an fdmgpu handle through the
+// public C ABI only (include/fdmgpu.h) — the same calls a reference-side
+// integration makes.
+#include <cstring>
+#include <exception>
+#include <string>
+
+#include "../../../include/fdmgpu.h"
+#include "fdm_host.hpp"
+
+using namespace fdmgpu::host;
+
+namespace {
+thread_local std::string g_err;
+template <class Fn>
+int guard(Fn&& fn) {
+  try {
+    fn();
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+template <class T>
+void put(T* dst, const std::vector<T>& v) {
+  if (dst && !v.empty()) std::memcpy(dst, v.data(), v.size() * sizeof(T));
+}
+}  // namespace
+
+extern "C" {
+
+const char* fdmhost_last_error() { return g_err.c_str(); }
+
+void* fdmhost_problem_create(int config, int n, int p) {
+  Problem* out = nullptr;
+  if (guard([&] { out = make_problem(config, n, p).release(); })) return nullptr;
+  return out;
+}
+
+void fdmhost_problem_destroy(void* ph) { delete static_cast<Problem*>(ph); }
+
+// out: dim, p, ncells, ndof, nfree, npatch, nvertices, npc, sum n_j, ncoarse,
+//      P nnz, q, config, n (cells per axis), all_cartesian
+int fdmhost_problem_info(void* ph, int64_t* out) {
+  return guard([&] {
+    const Problem& P = *static_cast<Problem*>(ph);
+    bool cart = true;
+    for (auto k : P.cell_kind) cart = cart && k == 0;
+    const int64_t v[15] = {P.dim, P.p, P.mesh.num_cells(), P.space.ndof, P.space.num_free(),
+                           int64_t(P.patches.vertex.size()), P.mesh.num_vertices(), P.space.npc,
+                           P.patches.ptr.back(), P.coarse.ndof, int64_t(P.coarse.P_col.size()), P.basis.q,
+                           P.config, P.n, cart ? 1 : 0};
+    std::memcpy(out, v, sizeof(v));
+  });
+}
+
+int fdmhost_get_rhs(void* ph, double* out) {
+  return guard([&] { put(out, static_cast<Problem*>(ph)->rhs); });
+}
+
+int fdmhost_get_maps(void* ph, int32_t* cell_dofs, int32_t* cell_modes, uint8_t* constrained, double* multiplicity,
+                     int32_t* label_cls, int32_t* label_entity) {
+  return guard([&] {
+    const Space& s = static_cast<Problem*>(ph)->space;
+    put(cell_dofs, s.cell_dofs);
+    put(cell_modes, s.cell_modes);
+    put(constrained, s.constrained);
+    put(multiplicity, s.multiplicity);
+    put(label_cls, s.label_cls);
+    put(label_entity, s.label_entity);
+  });
+}
+
+int fdmhost_get_geometry(void* ph, double* vertices, double* kappa, double* mu, uint8_t* kind, double* corner_xyz) {
+  return guard([&] {
+    const Problem& P = *static_cast<Problem*>(ph);
+    if (vertices)
+      for (int v = 0; v < P.mesh.num_vertices(); ++v)
+        for (int a = 0; a < 3; ++a) vertices[3 * v + a] = P.mesh.vertices[v][a];
+    put(kappa, P.cell_kappa);
+    put(mu, P.cell_mu);
+    put(kind, P.cell_kind);
+    put(corner_xyz, P.cell_xyz);
+  });
+}
+
+int fdmhost_get_basis(void* ph, double* S, double* At, double* Bt, uint8_t* Anz, uint8_t* Bnz, double* lambda,
+                      double* parity, double* Ahat, double* Bhat, double* nodes) {
+  return guard([&] {
+    const Basis1D& b = static_cast<Problem*>(ph)->basis;
+    put(S, b.S.a);
+    put(At, b.A_t.a);
+    put(Bt, b.B_t.a);
+    put(Anz, b.A_nz);
+    put(Bnz, b.B_nz);
+    put(lambda, b.lambda);
+    put(parity, b.parity);
+    put(Ahat, b.A_hat.a);
+    put(Bhat, b.B_hat.a);
+    put(nodes, b.nodes);
+  });
+}
+
+int fdmhost_get_patches(void* ph, int32_t* vertex, int64_t* ptr, int32_t* dofs, int32_t* perm, int32_t* cells,
+                        int32_t* colour) {
+  return guard([&] {
+    const Patches& P = static_cast<Problem*>(ph)->patches;
+    put(vertex, P.vertex);
+    put(ptr, P.ptr);
+    put(dofs, P.dofs);
+    put(perm, P.perm);
+    put(cells, P.cells);
+    put(colour, P.colour);
+  });
+}
+
+int fdmhost_get_coarse(void* ph, double* inverse, int64_t* P_ptr, int32_t* P_col, double* P_val) {
+  return guard([&] {
+    const Coarse& C = static_cast<Problem*>(ph)->coarse;
+    put(inverse, C.inverse);
+    put(P_ptr, C.P_ptr);
+    put(P_col, C.P_col);
+    put(P_val, C.P_val);
+  });
+}
+
+// Creates an fdmgpu handle for the problem and uploads every input through
+// the public C ABI (does not factor).  Returns the fdmgpu status.
+int fdmhost_attach(void* ph, int device, fdmgpu_handle* out) {
+  Problem& P = *static_cast<Problem*>(ph);
+  fdmgpu_handle h = nullptr;
+  fdmgpu_status st = fdmgpu_create(&h, P.dim, P.p, P.mesh.num_cells(), P.space.ndof, device);
+  if (st != FDMGPU_OK) {
+    g_err = h ? fdmgpu_last_error(h) : "fdmgpu_create failed (no CUDA device?)";
+    return st;
+  }
+  auto fail = [&](fdmgpu_status s) {
+    g_err = fdmgpu_last_error(h);
+    fdmgpu_destroy(h);
+    return int(s);
+  };
+  const Basis1D& b = P.basis;
+  if ((st = fdmgpu_set_basis(h, b.S.a.data(), b.lambda.data(), b.A_t.a.data(), b.B_t.a.data(), b.A_nz.data(),
+                             b.B_nz.data(), b.A_hat.a.data(), b.B_hat.a.data(), b.q, b.Vq.a.data(), b.Dq.a.data(),
+                             b.wq.data())) != FDMGPU_OK)
+    return fail(st);
+  const Space& s = P.space;
+  if ((st = fdmgpu_set_mesh_maps(h, s.cell_dofs.data(), s.cell_modes.data(),
+                                 s.mode_sign.empty() ? nullptr : s.mode_sign.data(), s.multiplicity.data(),
+                                 s.constrained.data())) != FDMGPU_OK)
+    return fail(st);
+  if ((st = fdmgpu_set_cell_coeffs(h, P.cell_kind.data(), P.cell_mu.data(), P.cell_xyz.data(),
+                                   P.cell_kappa.data())) != FDMGPU_OK)
+    return fail(st);
+  const Patches& pt = P.patches;
+  if ((st = fdmgpu_set_patches(h, int32_t(pt.vertex.size()), pt.vertex.data(), pt.ptr.data(), pt.dofs.data(),
+                               pt.perm.data(), pt.cells.data())) != FDMGPU_OK)
+    return fail(st);
+  const Coarse& C = P.coarse;
+  if ((st = fdmgpu_set_coarse(h, C.ndof, C.inverse.data(), C.P_ptr.data(), C.P_col.data(), C.P_val.data())) !=
+      FDMGPU_OK)
+    return fail(st);
+  *out = h;
+  return FDMGPU_OK;
+}
+
+}  // extern "C"

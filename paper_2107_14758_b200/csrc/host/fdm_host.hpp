@@ -1,0 +1,146 @@
+// Host-side setup of the B200 vertex-star FDM Schwarz path: the parts of
+// the reference that run once per problem on the CPU and produce the index
+// maps, 1D FDM basis and patch lists the device path consumes.  They mirror
+// the reference entry points (names and semantics) of
+//   include/fdmstar/{quadrature,reference_interval,dense_eig,fdm_basis,
+//                    mesh,geometry,discretization,ordering,schwarz}.hpp
+// for the scalar continuous Q_p space on conforming quad/hex meshes.
+// Index maps are bit-exact with the reference's first-touch numbering
+// (src/discretization.cpp:70-264), which the tests check against the oracle.
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+namespace fdmgpu::host {
+
+using Vec = std::vector<double>;
+
+// Column-major dense matrix.
+struct Dense {
+  int r = 0, c = 0;
+  std::vector<double> a;
+  Dense() = default;
+  Dense(int rows, int cols) : r(rows), c(cols), a(size_t(rows) * cols, 0.0) {}
+  double& operator()(int i, int j) { return a[i + size_t(r) * j]; }
+  double operator()(int i, int j) const { return a[i + size_t(r) * j]; }
+};
+
+// ---- 1D: quadrature (src/quadrature.cpp), reference interval
+// (src/reference_interval.cpp), FDM basis (src/fdm_basis.cpp) -----------------
+Vec gll_nodes(int p);
+void gauss_legendre(int n, Vec& pts, Vec& wts);
+void lagrange_eval(const Vec& nodes, const Vec& pts, Dense& V, Dense& D);
+
+struct Basis1D {
+  int p = 0;
+  Vec nodes;          // GLL nodes
+  Dense A_hat, B_hat; // reference stiffness / mass, GL(p+1)-exact
+  Dense S;            // FDM modes (nodal coefficients), (p+1)^2
+  Vec lambda;         // p-1 interior eigenvalues, ascending
+  Dense A_t, B_t;     // S^T A S, S^T B S with their structural patterns
+  std::vector<uint8_t> A_nz, B_nz;
+  Vec parity;
+  // GL(p+2) interpolation / derivative tables for the true-form trilinear apply
+  int q = 0;
+  Dense Vq, Dq;       // q x (p+1)
+  Vec wq;
+};
+Basis1D make_bundle(int p);  // src/assembly.cpp:37-54 (CG family)
+
+// ---- mesh (src/mesh.cpp), geometry (src/geometry.cpp) ------------------------
+struct Facet {
+  std::array<int, 2> cell{-1, -1}, axis{-1, -1}, side{0, 0};
+  bool flip = false, oriented = true;
+  std::vector<int> vertices;
+  int ncells() const { return cell[1] >= 0 ? 2 : 1; }
+};
+struct Mesh {
+  int dim = 3;
+  std::vector<std::array<double, 3>> vertices;
+  std::vector<std::vector<int>> cells;
+  std::vector<Facet> facets;
+  std::vector<std::vector<int>> vertex_cells;
+  std::vector<double> kappa;  // per-cell coefficient (config C4), empty => 1
+  int num_cells() const { return int(cells.size()); }
+  int num_vertices() const { return int(vertices.size()); }
+  double coeff(int c) const { return kappa.empty() ? 1.0 : kappa[c]; }
+  void finalize();  // src/mesh.cpp:33-91
+};
+Mesh cartesian_mesh(int dim, const std::vector<int>& counts, const std::vector<double>& lengths);
+Mesh tensor_grid_mesh(int dim, const std::vector<std::vector<double>>& coords);
+std::vector<char> boundary_vertices(const Mesh& m);
+
+// Cell classification and surrogate coefficients (src/geometry.cpp:45-104).
+enum class MapKind { Cartesian = 0, Affine = 1, Bilinear = 2 };
+struct CellCoeffs {
+  MapKind kind;
+  std::array<double, 3> mu;  // kappa * mu^K (surrogate), per axis
+};
+CellCoeffs cell_coeffs(const Mesh& m, int cell, const Basis1D& b);
+
+// ---- discretization (src/discretization.cpp) ---------------------------------
+enum class DofClass { Interior = 0, Facet = 1, Edge = 2, Vertex = 3 };
+struct Space {
+  const Mesh* mesh = nullptr;
+  int p = 0, npc = 0, ndof = 0;
+  std::vector<int32_t> cell_dofs;  // ncells x npc, lattice axis 0 fastest
+  std::vector<int32_t> cell_modes; // equal to cell_dofs unless a 2D facet flips
+  std::vector<double> mode_sign;   // ncells x npc (+-1), empty when all +1
+  std::vector<double> multiplicity;
+  std::vector<uint8_t> constrained;
+  std::vector<int32_t> label_cls, label_entity;
+  std::vector<uint8_t> owner_kind;  // 0 cell, 1 facet, 2 edge, 3 vertex
+  std::vector<int32_t> owner_id;
+  std::vector<std::array<int, 2>> edge_vertices;
+  int num_free() const;
+  std::vector<int32_t> star_dofs(int v) const;  // src/discretization.cpp:266-297
+};
+Space q_space(const Mesh& m, int p);
+
+// patch_ordering (src/ordering.cpp:17-45): interiors, then facet / edge groups
+// by entity id, vertex last; ties on the position in `dofs`.
+std::vector<int32_t> patch_ordering(const Space& s, const std::vector<int32_t>& dofs);
+
+// Vertex-star patch lists in the order of build_patch_solver (src/schwarz.cpp:62-83).
+struct Patches {
+  std::vector<int32_t> vertex;
+  std::vector<int64_t> ptr;   // npatch+1
+  std::vector<int32_t> dofs;  // ascending star_dofs per patch
+  std::vector<int32_t> perm;  // patch_ordering, local indices
+  std::vector<int32_t> cells; // npatch x 2^dim star cells (ascending ids)
+  std::vector<int32_t> colour;  // vertex-parity colouring
+};
+Patches vertex_patches(const Space& s, bool skip_boundary);
+
+// ---- coarse level (src/schwarz.cpp:139-165, 239-243) -------------------------
+struct Coarse {
+  int ndof = 0;
+  std::vector<double> inverse;  // dense A_c^{-1} (identity rows on constrained)
+  std::vector<int64_t> P_ptr;   // prolongation CSR, fine rows
+  std::vector<int32_t> P_col;
+  std::vector<double> P_val;
+};
+Coarse build_coarse(const Mesh& m, const Space& fine, const Basis1D& fb);
+
+// ---- synthetic configurations C1..C5 ------------------------
+struct Problem {
+  int config = 0, dim = 3, n = 8, p = 15;
+  Mesh mesh;
+  Basis1D basis;
+  Space space;
+  std::vector<double> rhs;
+  std::vector<uint8_t> cell_kind;   // MapKind per cell
+  std::vector<double> cell_mu;      // ncells x dim: kappa * mu^K
+  std::vector<double> cell_xyz;     // ncells x 2^dim x 3 corner coordinates
+  std::vector<double> cell_kappa;   // ncells
+  Patches patches;
+  Coarse coarse;
+};
+std::unique_ptr<Problem> make_problem(int config, int n_override, int p_override);
+
+}  // namespace fdmgpu::host

@@ -1,0 +1,671 @@
+// Vertex-star patch kernels: batched numeric factorisation (K2), the
+// patch relaxation solve (K3) and the deterministic patch owner-gather.
+//
+// Reference path replaced (src/schwarz.cpp:41-54, 84-93; src/cholesky.cpp:9-110):
+//   for each patch j: A~_j = R_j A~ R_j^T, P A~_j P^T = L L^T (up-looking),
+//   c_j = L^{-T} L^{-1} P r_j, then z += R_j^T c_j in ascending j.
+//
+// B200 layout.  All interior patches share one elimination order on the
+// (2p-1)^d patch lattice (layout.cpp).  Interior DOFs are eliminated first
+// and couple only to their cell's d near facets (zero fill),
+// so their factor columns are never stored: the kernels rebuild
+// D_k = A~_kk and A~_{f,k} from the per-cell mu and the 1D tables A_t / B_t.
+// What is stored is the Cholesky factor of the separator Schur complement
+// S_G = A~_GG - A~_GI D^{-1} A~_IG as dense 64x64 tiles on one shared tile
+// pattern (diagonal tiles hold L_KK^{-1}, so the solves are pure GEMVs),
+// streamed by the solve kernel through a TMA-bulk-copy / mbarrier ring.
+#include "common.cuh"
+
+namespace fdmgpu {
+
+namespace {
+
+constexpr int T = kTile;
+constexpr int TT = kTile * kTile;
+
+struct PatchArgs {
+  int dim, p, n1, n, nI, m, mpad, nT, ntiles, span;
+  const int32_t* lat;
+  const int32_t* pos_of_lat;
+  const int32_t* pcells;
+  const double* mu;
+  const double* At;
+  const double* Bt;
+  unsigned long long* err;
+};
+
+PatchArgs make_args(Context& c) {
+  PatchArgs a;
+  a.dim = c.dim;
+  a.p = c.p;
+  a.n1 = c.n1;
+  a.n = c.L.n;
+  a.nI = c.L.nI;
+  a.m = c.L.m;
+  a.mpad = c.L.mpad;
+  a.nT = c.L.nT;
+  a.ntiles = c.L.ntiles;
+  a.span = c.L.span;
+  a.lat = c.lat.p;
+  a.pos_of_lat = c.pos_of_lat.p;
+  a.pcells = c.pcells.p;
+  a.mu = c.mu.p;
+  a.At = c.At.p;
+  a.Bt = c.Bt.p;
+  a.err = c.d_err.p;
+  return a;
+}
+
+__device__ __forceinline__ void unpack(int32_t v, int* P) {
+  P[0] = v & 255;
+  P[1] = (v >> 8) & 255;
+  P[2] = (v >> 16) & 255;
+}
+
+__device__ __forceinline__ int lin_of(const PatchArgs& a, const int* P) {
+  int v = P[a.dim - 1];
+  for (int b = a.dim - 2; b >= 0; --b) v = v * a.span + P[b];
+  return v;
+}
+
+// The single axis on which lattice point P lies on a separator plane through
+// the vertex (P_a == p), or -1 when it is interior (none) or edge/vertex (>1).
+__device__ __forceinline__ int facet_axis(const PatchArgs& a, const int* P) {
+  int fa = -1, cnt = 0;
+  for (int b = 0; b < a.dim; ++b)
+    if (P[b] == a.p) {
+      fa = b;
+      ++cnt;
+    }
+  return cnt == 1 ? fa : -1;
+}
+
+// A~^K_kk for a cell-interior lattice point l of cell with coefficients mus.
+__device__ __forceinline__ double diag_interior(const PatchArgs& a, const double* mus, const int* l,
+                                                const double* At, const double* Bt) {
+  double s = 0.0;
+  for (int q = 0; q < a.dim; ++q) {
+    double prod = mus[q];
+    for (int b = a.dim - 1; b >= 0; --b) prod *= (b == q ? At : Bt)[l[b] + a.n1 * l[b]];
+    s += prod;
+  }
+  return s;
+}
+
+// A~^K(f, x) for facet point f (endpoint e on axis fa) and the interior point x
+// that shares f's tangential indices; x_fa is the interior index.
+__device__ __forceinline__ double facet_coupling(const PatchArgs& a, const double* mus, int fa, int e, int xa,
+                                                 const int* l, const double* At, const double* Bt) {
+  double prod = mus[fa] * At[e + a.n1 * xa];
+  for (int b = 0; b < a.dim; ++b)
+    if (b != fa) prod *= Bt[l[b] + a.n1 * l[b]];
+  return prod;
+}
+
+// Entry (r, c) of the separator Schur complement S_G, r,c in [0, m).
+__device__ double schur_entry(const PatchArgs& a, const double* __restrict__ mu_patch, int r, int c,
+                              const double* At, const double* Bt) {
+  int P[3] = {0, 0, 0}, Q[3] = {0, 0, 0};
+  unpack(a.lat[a.nI + r], P);
+  unpack(a.lat[a.nI + c], Q);
+  int lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+  for (int b = 0; b < a.dim; ++b) {
+    const int plo = P[b] > a.p ? 1 : 0, phi = P[b] < a.p ? 0 : 1;
+    const int qlo = Q[b] > a.p ? 1 : 0, qhi = Q[b] < a.p ? 0 : 1;
+    lo[b] = max(plo, qlo);
+    hi[b] = min(phi, qhi);
+    if (lo[b] > hi[b]) return 0.0;  // no common cell
+  }
+  const int fr = facet_axis(a, P), fc = facet_axis(a, Q);
+  double v = 0.0;
+  for (int s2 = lo[2]; s2 <= hi[2]; ++s2)
+    for (int s1 = lo[1]; s1 <= hi[1]; ++s1)
+      for (int s0 = lo[0]; s0 <= hi[0]; ++s0) {
+        const int s[3] = {s0, s1, s2};
+        const int slot = s0 | (s1 << 1) | (s2 << 2);
+        const double* mus = mu_patch + slot * a.dim;
+        int lr[3] = {0, 0, 0}, lc[3] = {0, 0, 0};
+        for (int b = 0; b < a.dim; ++b) {
+          lr[b] = P[b] - s[b] * a.p;
+          lc[b] = Q[b] - s[b] * a.p;
+        }
+        // cell block sum_q mu_q (x)_b (b == q ? A_t : B_t)  (src/assembly.cpp:263-270)
+        double cv = 0.0;
+        for (int q = 0; q < a.dim; ++q) {
+          double prod = 1.0;
+          for (int b = a.dim - 1; b >= 0; --b) prod *= (b == q ? At : Bt)[lr[b] + a.n1 * lc[b]];
+          cv += prod * mus[q];
+        }
+        // minus the elimination of this cell's interior block
+        double sc = 0.0;
+        if (fr >= 0 && fc >= 0) {
+          bool same_tan = true;
+          for (int b = 0; b < a.dim; ++b)
+            if (b != fr && b != fc && lr[b] != lc[b]) same_tan = false;
+          if (same_tan) {
+            if (fr == fc) {
+              int x[3] = {lr[0], lr[1], lr[2]};
+              for (int xi = 1; xi < a.p; ++xi) {
+                x[fr] = xi;
+                const double cp = facet_coupling(a, mus, fr, lr[fr], xi, x, At, Bt);
+                sc += cp * cp / diag_interior(a, mus, x, At, Bt);
+              }
+            } else {
+              int x[3] = {lr[0], lr[1], lr[2]};
+              x[fr] = lc[fr];
+              x[fc] = lr[fc];
+              const double cr = facet_coupling(a, mus, fr, lr[fr], x[fr], x, At, Bt);
+              const double cc = facet_coupling(a, mus, fc, lc[fc], x[fc], x, At, Bt);
+              sc = cr * cc / diag_interior(a, mus, x, At, Bt);
+            }
+          }
+        }
+        v += cv - sc;
+      }
+  return v;
+}
+
+__device__ __forceinline__ void record_pivot_error(unsigned long long* err, int patch, int pivot) {
+  atomicMin(err, (static_cast<unsigned long long>(patch) << 32) | static_cast<unsigned>(pivot));
+}
+
+__global__ void k_patch_assemble(PatchArgs a, const int32_t* __restrict__ tile_row,
+                                 const int32_t* __restrict__ tile_col, double* __restrict__ tiles) {
+  extern __shared__ double sm[];
+  double* At = sm;
+  double* Bt = At + a.n1 * a.n1;
+  double* mup = Bt + a.n1 * a.n1;  // 2^d x d
+  const int t = blockIdx.x, j = blockIdx.y;
+  const int ncorner = 1 << a.dim;
+  for (int i = threadIdx.x; i < a.n1 * a.n1; i += blockDim.x) {
+    At[i] = a.At[i];
+    Bt[i] = a.Bt[i];
+  }
+  for (int i = threadIdx.x; i < ncorner * a.dim; i += blockDim.x) {
+    const int s = i / a.dim, q = i % a.dim;
+    mup[i] = a.mu[size_t(a.pcells[size_t(j) * ncorner + s]) * a.dim + q];
+  }
+  __syncthreads();
+  const int I = tile_row[t], K = tile_col[t];
+  double* out = tiles + (size_t(j) * a.ntiles + t) * TT;
+  for (int e = threadIdx.x; e < TT; e += blockDim.x) {
+    const int rr = e % T, cc = e / T;
+    const int r = I * T + rr, c = K * T + cc;
+    double v;
+    if (r >= a.m || c >= a.m)
+      v = (r == c) ? 1.0 : 0.0;
+    else if (I == K && rr < cc)
+      v = 0.0;
+    else
+      v = schur_entry(a, mup, r, c, At, Bt);
+    out[tsw(rr, cc)] = v;
+  }
+  // interior pivots D_k > 0 (the first n_I pivots of the reference order)
+  if (t == 0) {
+    for (int k = threadIdx.x; k < a.nI; k += blockDim.x) {
+      int P[3] = {0, 0, 0}, s[3] = {0, 0, 0}, l[3] = {0, 0, 0};
+      unpack(a.lat[k], P);
+      for (int b = 0; b < a.dim; ++b) {
+        s[b] = P[b] > a.p ? 1 : 0;
+        l[b] = P[b] - s[b] * a.p;
+      }
+      const int slot = s[0] | (s[1] << 1) | (s[2] << 2);
+      if (!(diag_interior(a, mup + slot * a.dim, l, At, Bt) > 0.0)) record_pivot_error(a.err, j, k);
+    }
+  }
+}
+
+// acc(16 per thread) += A B^T over one 64-deep k panel; thread (tr, tc) owns
+// rows tr + 16 i and columns tc + 16 jj (conflict-free on the swizzle).
+__device__ __forceinline__ void tile_gemm_abt(const double* __restrict__ A, const double* __restrict__ B, int tr,
+                                              int tc, double acc[4][4]) {
+#pragma unroll 4
+  for (int k = 0; k < T; ++k) {
+    double av[4], bv[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) av[i] = A[tsw(tr + 16 * i, k)];
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) bv[jj] = B[tsw(tc + 16 * jj, k)];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) acc[i][jj] = fma(av[i], bv[jj], acc[i][jj]);
+  }
+}
+
+// POTRF + triangular inverse of the 64x64 tile in Dm (column-major, ld 65),
+// writes L^{-1} (lower, diag included) swizzled into `out`.
+__device__ void diag_factor_invert(double* Dm, double* Wm, double* out, const PatchArgs& a, int K, int patch) {
+  constexpr int LD = T + 1;
+  const int tid = threadIdx.x;
+  for (int jc = 0; jc < T; ++jc) {
+    if (tid == 0) {
+      double d = Dm[jc * LD + jc];
+      if (!(d > 0.0)) {
+        const int pos = K * T + jc;
+        if (pos < a.m) record_pivot_error(a.err, patch, a.nI + pos);
+        d = 1.0;
+      }
+      Dm[jc * LD + jc] = sqrt(d);
+    }
+    __syncthreads();
+    const double piv = Dm[jc * LD + jc];
+    for (int r = jc + 1 + tid; r < T; r += blockDim.x) Dm[jc * LD + r] /= piv;
+    __syncthreads();
+    for (int e = tid; e < TT; e += blockDim.x) {
+      const int r = e % T, cc = e / T;
+      if (cc > jc && r >= cc) Dm[cc * LD + r] -= Dm[jc * LD + r] * Dm[jc * LD + cc];
+    }
+    __syncthreads();
+  }
+  // Row-sequential inverse: Linv(r, cc) = (delta - sum_{k=cc}^{r-1} L(r,k) Linv(k,cc)) / L(r,r);
+  // 4 threads per column split the k-sum.
+  const int col = tid >> 2, part = tid & 3;
+  for (int r = 0; r < T; ++r) {
+    double s = 0.0;
+    if (col <= r)
+      for (int k = col + part; k < r; k += 4) s = fma(Dm[k * LD + r], Wm[col * LD + k], s);
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    if (part == 0 && col <= r) Wm[col * LD + r] = ((r == col ? 1.0 : 0.0) - s) / Dm[r * LD + r];
+    __syncthreads();
+  }
+  for (int e = tid; e < TT; e += blockDim.x) {
+    const int r = e % T, cc = e / T;
+    out[tsw(r, cc)] = r >= cc ? Wm[cc * LD + r] : 0.0;
+  }
+}
+
+constexpr int kUpdThreads = 256;
+
+// Left-looking update of tile column K: C(I,K) = A(I,K) - sum_J L(I,J) L(K,J)^T
+// for every stored tile (I,K); the CTA owning the diagonal tile then factors
+// and inverts it.  Operand tiles arrive by TMA bulk copy, double-buffered.
+__global__ void __launch_bounds__(kUpdThreads) k_patch_update(PatchArgs a, int K, const int32_t* __restrict__ col_start,
+                                                                const int32_t* __restrict__ tile_row,
+                                                                const int32_t* __restrict__ pair_ptr,
+                                                                const int32_t* __restrict__ pair_a,
+                                                                const int32_t* __restrict__ pair_b,
+                                                                double* __restrict__ tiles) {
+  extern __shared__ __align__(128) double sm[];
+  double* buf = sm;                                   // [2 stages][A,B][TT]
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + 4 * TT);
+  const int t = col_start[K] + blockIdx.x, j = blockIdx.y;
+  const int I = tile_row[t];
+  double* base = tiles + size_t(j) * a.ntiles * TT;
+  const int p0 = pair_ptr[t], np = pair_ptr[t + 1] - p0;
+  const int tid = threadIdx.x, tr = tid >> 4, tc = tid & 15;
+  if (tid == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int s = 0; s < 2 && s < np; ++s) {
+      mbar_arrive_expect_tx(&full[s], 2 * TT * sizeof(double));
+      bulk_g2s(buf + (2 * s) * TT, base + size_t(pair_a[p0 + s]) * TT, TT * sizeof(double), &full[s]);
+      bulk_g2s(buf + (2 * s + 1) * TT, base + size_t(pair_b[p0 + s]) * TT, TT * sizeof(double), &full[s]);
+    }
+  double acc[4][4] = {};
+  for (int i = 0; i < np; ++i) {
+    const int s = i & 1;
+    mbar_wait(&full[s], (i >> 1) & 1);
+    tile_gemm_abt(buf + (2 * s) * TT, buf + (2 * s + 1) * TT, tr, tc, acc);
+    __syncthreads();
+    if (tid == 0 && i + 2 < np) {
+      mbar_arrive_expect_tx(&full[s], 2 * TT * sizeof(double));
+      bulk_g2s(buf + (2 * s) * TT, base + size_t(pair_a[p0 + i + 2]) * TT, TT * sizeof(double), &full[s]);
+      bulk_g2s(buf + (2 * s + 1) * TT, base + size_t(pair_b[p0 + i + 2]) * TT, TT * sizeof(double), &full[s]);
+    }
+  }
+  double* ct = base + size_t(t) * TT;
+  if (I != K) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) {
+        const int idx = tsw(tr + 16 * i, tc + 16 * jj);
+        ct[idx] -= acc[i][jj];
+      }
+    return;
+  }
+  constexpr int LD = T + 1;
+  double* Dm = buf;           // reuse the operand buffers (all copies consumed)
+  double* Wm = buf + T * LD;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) {
+      const int r = tr + 16 * i, cc = tc + 16 * jj;
+      Dm[cc * LD + r] = ct[tsw(r, cc)] - acc[i][jj];
+    }
+  for (int e = tid; e < T * LD; e += blockDim.x) Wm[e] = 0.0;
+  __syncthreads();
+  diag_factor_invert(Dm, Wm, ct, a, K, j);
+}
+
+// L(I,K) = C(I,K) L_KK^{-T} for the off-diagonal tiles of column K.
+__global__ void __launch_bounds__(kUpdThreads) k_patch_trsm(PatchArgs a, int K, const int32_t* __restrict__ col_start,
+                                                              double* __restrict__ tiles) {
+  extern __shared__ __align__(128) double sm[];
+  double* Cs = sm;
+  double* Ls = sm + TT;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + 2 * TT);
+  const int t0 = col_start[K];
+  const int t = t0 + 1 + blockIdx.x, j = blockIdx.y;
+  double* base = tiles + size_t(j) * a.ntiles * TT;
+  const int tid = threadIdx.x, tr = tid >> 4, tc = tid & 15;
+  if (tid == 0) {
+    mbar_init(&full[0], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    mbar_arrive_expect_tx(&full[0], 2 * TT * sizeof(double));
+    bulk_g2s(Cs, base + size_t(t) * TT, TT * sizeof(double), &full[0]);
+    bulk_g2s(Ls, base + size_t(t0) * TT, TT * sizeof(double), &full[0]);
+  }
+  mbar_wait(&full[0], 0);
+  double acc[4][4] = {};
+  tile_gemm_abt(Cs, Ls, tr, tc, acc);
+  double* out = base + size_t(t) * TT;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) out[tsw(tr + 16 * i, tc + 16 * jj)] = acc[i][jj];
+}
+
+
+// ---- K3: patch relaxation solve -------------------------------------------------
+constexpr int kSolveConsumers = 8;                         // consumer warps
+constexpr int kSolveThreads = 32 * (kSolveConsumers + 1);  // + 1 TMA producer warp
+
+// One CTA per patch.  A producer warp streams the patch's separator factor
+// (forward order, then backward by column) through a `stages`-deep ring of
+// 32 KB shared-memory slots with cp.async.bulk + mbarrier; eight consumer
+// warps run the separator RHS, the tile GEMVs and the interior
+// back-substitution.  Output: the patch correction c_j in elimination order.
+__global__ void __launch_bounds__(kSolveThreads)
+    k_patch_solve(PatchArgs a, int stages, const double* __restrict__ rt, double* __restrict__ corr,
+                  const double* __restrict__ tiles, const int32_t* __restrict__ pdofs,
+                  const int32_t* __restrict__ col_start, const int32_t* __restrict__ tile_row) {
+  extern __shared__ __align__(128) double sm[];
+  double* ring = sm;                          // stages x TT
+  double* y = ring + size_t(stages) * TT;     // mpad
+  double* part = y + a.mpad;                  // kSolveConsumers x T
+  uint64_t* full = reinterpret_cast<uint64_t*>(part + kSolveConsumers * T);
+  uint64_t* empty = full + stages;
+  const int j = blockIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int ncorner = 1 << a.dim;
+  const int32_t* pd = pdofs + size_t(j) * a.n;
+  const double* tb = tiles + size_t(j) * a.ntiles * TT;
+  if (tid == 0) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  if (warp == kSolveConsumers) {
+    if (lane == 0) {
+      int q = 0;
+      auto issue = [&](int t) {
+        const int s = q % stages;
+        if (q >= stages) mbar_wait(&empty[s], ((q / stages) - 1) & 1);
+        mbar_arrive_expect_tx(&full[s], TT * sizeof(double));
+        bulk_g2s(ring + size_t(s) * TT, tb + size_t(t) * TT, TT * sizeof(double), &full[s]);
+        ++q;
+      };
+      for (int t = 0; t < a.ntiles; ++t) issue(t);
+      for (int K = a.nT - 1; K >= 0; --K) {
+        const int t0 = col_start[K], t1 = col_start[K + 1];
+        for (int t = t0 + 1; t < t1; ++t) issue(t);
+        issue(t0);
+      }
+    }
+    return;
+  }
+
+  constexpr int NC = 32 * kSolveConsumers;
+  const double* At = a.At;
+  const double* Bt = a.Bt;
+  double mup[24];
+  for (int i = 0; i < ncorner * a.dim; ++i)
+    mup[i] = a.mu[size_t(a.pcells[size_t(j) * ncorner + i / a.dim]) * a.dim + i % a.dim];
+
+  // ---- phase A: separator RHS  b_G - A~_GI D^{-1} b_I (interiors in elimination order)
+  for (int r = tid; r < a.mpad; r += NC) {
+    double b = 0.0;
+    if (r < a.m) {
+      int P[3] = {0, 0, 0};
+      unpack(a.lat[a.nI + r], P);
+      b = rt[pd[a.nI + r]];
+      const int fa = facet_axis(a, P);
+      if (fa >= 0) {
+        for (int sf = 0; sf < 2; ++sf) {
+          int s[3] = {0, 0, 0}, l[3] = {0, 0, 0};
+          for (int qq = 0; qq < a.dim; ++qq) {
+            s[qq] = qq == fa ? sf : (P[qq] > a.p ? 1 : 0);
+            l[qq] = P[qq] - s[qq] * a.p;
+          }
+          const double* mus = mup + (s[0] | (s[1] << 1) | (s[2] << 2)) * a.dim;
+          const int e = l[fa];
+          int x[3] = {l[0], l[1], l[2]};
+          for (int xi = 1; xi < a.p; ++xi) {
+            x[fa] = xi;
+            int Px[3] = {0, 0, 0};
+            for (int qq = 0; qq < a.dim; ++qq) Px[qq] = s[qq] * a.p + x[qq];
+            const double bx = rt[pd[a.pos_of_lat[lin_of(a, Px)]]];
+            b -= facet_coupling(a, mus, fa, e, xi, x, At, Bt) * bx / diag_interior(a, mus, x, At, Bt);
+          }
+        }
+      }
+    }
+    y[r] = b;
+  }
+  named_sync(1, NC);
+
+  // ---- phase B: forward substitution over tile columns (y <- L_G^{-1} y) ----------------
+  int q = 0;  // stream position, mirrors the producer
+  for (int K = 0; K < a.nT; ++K) {
+    const int t0 = col_start[K], cnt = col_start[K + 1] - t0;
+    double* yK = y + K * T;
+    if (warp == 0) {
+      const int s = q % stages;
+      mbar_wait(&full[s], (q / stages) & 1);
+      const double* Li = ring + size_t(s) * TT;  // L_KK^{-1}
+      double v0 = 0.0, v1 = 0.0;
+      for (int c = 0; c <= lane + 32 && c < T; ++c) {
+        const double yc = yK[c];
+        if (c <= lane) v0 = fma(Li[tsw(lane, c)], yc, v0);
+        v1 = fma(Li[tsw(lane + 32, c)], yc, v1);
+      }
+      __syncwarp();
+      yK[lane] = v0;
+      yK[lane + 32] = v1;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    ++q;
+    named_sync(1, NC);
+    for (int i = 1; i < cnt; ++i, ++q) {
+      if ((i - 1) % kSolveConsumers != warp) continue;
+      const int s = q % stages;
+      mbar_wait(&full[s], (q / stages) & 1);
+      const double* Lt = ring + size_t(s) * TT;
+      double v0 = 0.0, v1 = 0.0;
+#pragma unroll 8
+      for (int c = 0; c < T; ++c) {
+        const double yc = yK[c];
+        v0 = fma(Lt[tsw(lane, c)], yc, v0);
+        v1 = fma(Lt[tsw(lane + 32, c)], yc, v1);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      double* yI = y + tile_row[t0 + i] * T;
+      yI[lane] -= v0;
+      yI[lane + 32] -= v1;
+    }
+    named_sync(1, NC);
+  }
+
+  // ---- phase C: backward substitution (x <- L_G^{-T} y), columns descending ---------------
+  for (int K = a.nT - 1; K >= 0; --K) {
+    const int t0 = col_start[K], cnt = col_start[K + 1] - t0;
+    double a0 = 0.0, a1 = 0.0;
+    for (int i = 1; i < cnt; ++i, ++q) {
+      if ((i - 1) % kSolveConsumers != warp) continue;
+      const int s = q % stages;
+      mbar_wait(&full[s], (q / stages) & 1);
+      const double* Lt = ring + size_t(s) * TT;
+      const double* xI = y + tile_row[t0 + i] * T;
+#pragma unroll 8
+      for (int r = 0; r < T; ++r) {
+        const double xr = xI[r];
+        a0 = fma(Lt[tsw(r, lane)], xr, a0);
+        a1 = fma(Lt[tsw(r, lane + 32)], xr, a1);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    part[warp * T + lane] = a0;
+    part[warp * T + lane + 32] = a1;
+    named_sync(1, NC);
+    if (warp == 0) {
+      double* yK = y + K * T;
+      double u0 = yK[lane], u1 = yK[lane + 32];
+      for (int w = 0; w < kSolveConsumers; ++w) {
+        u0 -= part[w * T + lane];
+        u1 -= part[w * T + lane + 32];
+      }
+      yK[lane] = u0;
+      yK[lane + 32] = u1;
+      __syncwarp();
+      const int s = q % stages;
+      mbar_wait(&full[s], (q / stages) & 1);
+      const double* Li = ring + size_t(s) * TT;  // x_K = L_KK^{-T} y_K
+      double v0 = 0.0, v1 = 0.0;
+      for (int r = lane; r < T; ++r) {
+        const double yr = yK[r];
+        v0 = fma(Li[tsw(r, lane)], yr, v0);
+        if (r >= lane + 32) v1 = fma(Li[tsw(r, lane + 32)], yr, v1);
+      }
+      __syncwarp();
+      yK[lane] = v0;
+      yK[lane + 32] = v1;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    ++q;
+    named_sync(1, NC);
+  }
+
+  // ---- phase D: interiors x_I = D^{-1} (b_I - A~_IG x_G); write c_j -------------------------
+  double* cj = corr + size_t(j) * a.n;
+  for (int k = tid; k < a.nI; k += NC) {
+    int P[3] = {0, 0, 0}, s[3] = {0, 0, 0}, l[3] = {0, 0, 0};
+    unpack(a.lat[k], P);
+    for (int b = 0; b < a.dim; ++b) {
+      s[b] = P[b] > a.p ? 1 : 0;
+      l[b] = P[b] - s[b] * a.p;
+    }
+    const double* mus = mup + (s[0] | (s[1] << 1) | (s[2] << 2)) * a.dim;
+    double v = rt[pd[k]];
+    for (int fa = 0; fa < a.dim; ++fa) {
+      int Pf[3] = {P[0], P[1], P[2]};
+      Pf[fa] = a.p;
+      const int e = s[fa] == 0 ? a.p : 0;
+      const double xf = y[a.pos_of_lat[lin_of(a, Pf)] - a.nI];
+      v -= facet_coupling(a, mus, fa, e, l[fa], l, At, Bt) * xf;
+    }
+    cj[k] = v / diag_interior(a, mus, l, At, Bt);
+  }
+  for (int r = tid; r < a.m; r += NC) cj[a.nI + r] = y[r];
+}
+
+// z[g] = sum of patch corrections of DOF g in ascending patch order
+// (src/schwarz.cpp:49-53 order, no atomics).
+__global__ void k_patch_gather(int64_t ndof, const double* __restrict__ corr, const int32_t* __restrict__ ptr,
+                               const int32_t* __restrict__ idx, double* __restrict__ z) {
+  const int64_t g = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (g >= ndof) return;
+  double s = 0.0;
+  for (int q = ptr[g]; q < ptr[g + 1]; ++q) s += corr[idx[q]];
+  z[g] = s;
+}
+
+}  // namespace
+
+void launch_patch_assemble(Context& c) {
+  PatchArgs a = make_args(c);
+  const size_t smem = sizeof(double) * (2 * size_t(c.n1) * c.n1 + 24);
+  dim3 grid(c.L.ntiles, c.npatch);
+  k_patch_assemble<<<grid, 256, smem, c.stream>>>(a, c.tile_row.p, c.tile_col.p, c.tiles.p);
+  FDM_LAUNCH_CHECK(c);
+}
+
+void launch_patch_update(Context& c, int K) {
+  PatchArgs a = make_args(c);
+  const size_t smem = sizeof(double) * 4 * TT + 64;
+  static bool attr = false;
+  if (!attr) {
+    FDM_CUDA(cudaFuncSetAttribute(k_patch_update, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    attr = true;
+  }
+  dim3 grid(c.L.col_start[K + 1] - c.L.col_start[K], c.npatch);
+  k_patch_update<<<grid, kUpdThreads, smem, c.stream>>>(a, K, c.col_start.p, c.tile_row.p, c.pair_ptr.p,
+                                                         c.pair_a.p, c.pair_b.p, c.tiles.p);
+  FDM_LAUNCH_CHECK(c);
+}
+
+void launch_patch_trsm(Context& c, int K) {
+  const int cnt = c.L.col_start[K + 1] - c.L.col_start[K] - 1;
+  if (cnt <= 0) return;
+  PatchArgs a = make_args(c);
+  const size_t smem = sizeof(double) * 2 * TT + 64;
+  static bool attr = false;
+  if (!attr) {
+    FDM_CUDA(cudaFuncSetAttribute(k_patch_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    attr = true;
+  }
+  dim3 grid(cnt, c.npatch);
+  k_patch_trsm<<<grid, kUpdThreads, smem, c.stream>>>(a, K, c.col_start.p, c.tiles.p);
+  FDM_LAUNCH_CHECK(c);
+}
+
+static int solve_stages(const Context& c, size_t* smem_out) {
+  const size_t fixed = sizeof(double) * (size_t(c.L.mpad) + kSolveConsumers * T);
+  const size_t budget = 227 * 1024;
+  int stages = 8;
+  while (stages > 2 && fixed + stages * (sizeof(double) * TT + 16) > budget) --stages;
+  *smem_out = fixed + stages * sizeof(double) * TT + 2 * stages * sizeof(uint64_t);
+  if (*smem_out > budget) throw Error(FDMGPU_UNSUPPORTED, "separator too large for the shared-memory solve");
+  return stages;
+}
+
+void launch_patch_solve(Context& c, const double* r_modal) {
+  PatchArgs a = make_args(c);
+  size_t smem = 0;
+  const int stages = solve_stages(c, &smem);
+  static bool attr = false;
+  if (!attr) {
+    FDM_CUDA(cudaFuncSetAttribute(k_patch_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    attr = true;
+  }
+  k_patch_solve<<<c.npatch, kSolveThreads, smem, c.stream>>>(a, stages, r_modal, c.corr.p, c.tiles.p, c.pdofs.p,
+                                                              c.col_start.p, c.tile_row.p);
+  FDM_LAUNCH_CHECK(c);
+}
+
+void launch_patch_gather(Context& c, double* z_modal) {
+  const int threads = 256;
+  const int64_t blocks = (c.ndof + threads - 1) / threads;
+  k_patch_gather<<<unsigned(blocks), threads, 0, c.stream>>>(c.ndof, c.corr.p, c.pg_ptr.p, c.pg_idx.p, z_modal);
+  FDM_LAUNCH_CHECK(c);
+}
+
+}  // namespace fdmgpu

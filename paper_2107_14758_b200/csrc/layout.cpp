@@ -1,0 +1,233 @@
+// Shared symbolic analysis of the vertex-star patches (host, once per handle).
+//
+// Every interior vertex star of a conforming hex/quad mesh is a (2p-1)^d
+// lattice of DOFs; with the reference's patch_ordering (src/ordering.cpp:
+// 17-45) all interior stars of a lattice-topology mesh induce the same
+// elimination order on that lattice.  This file
+//   1. maps each patch's elimination order onto patch-lattice coordinates
+//      P in [1, 2p-1]^d and verifies that every patch uses one canonical
+//      order (otherwise FDMGPU_UNSUPPORTED: no silent per-patch fallback);
+//   2. runs the reference's symbolic pass (etree + column counts,
+//      src/cholesky.cpp:18-31) on the canonical patch pattern, generated
+//      from the structural Kronecker pattern of A_t / B_t
+//      (src/fdm_basis.cpp:58-76, src/assembly.cpp:263-283);
+//   3. derives the dense-tile pattern of the interface (separator) factor and
+//      the left-looking tile-update pairs used by the batched factorisation.
+// Interior columns have exactly d+1 entries (zero fill)
+// and are never stored: the kernels rebuild them from mu and the 1D tables.
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <unordered_map>
+
+#include "context.hpp"
+
+namespace fdmgpu {
+
+namespace {
+
+inline int32_t pack(const int* P) { return P[0] | (P[1] << 8) | (P[2] << 16); }
+inline void unpack(int32_t v, int* P) {
+  P[0] = v & 255;
+  P[1] = (v >> 8) & 255;
+  P[2] = (v >> 16) & 255;
+}
+
+}  // namespace
+
+// Builds c.L, c.h_pdofs, c.h_pcells from the patch lists.
+void analyze_patches(Context& c, int npatch, const int32_t* vertex, const int64_t* ptr, const int32_t* dofs,
+                     const int32_t* perm, const int32_t* star_cells) {
+  const int d = c.dim, p = c.p, n1 = p + 1, ncorner = 1 << d;
+  PatchLayout& L = c.L;
+  L = PatchLayout();
+  L.span = 2 * p + 1;
+  int expect_n = 1, expect_nI = ncorner;
+  for (int a = 0; a < d; ++a) {
+    expect_n *= 2 * p - 1;
+    expect_nI *= p - 1;
+  }
+  L.n = expect_n;
+  L.nI = expect_nI;
+  L.m = L.n - L.nI;
+  c.h_pdofs.assign(size_t(npatch) * L.n, 0);
+  c.h_pcells.assign(size_t(npatch) * ncorner, -1);
+  std::vector<int32_t> where(c.ndof, -1), touched;
+  std::vector<int32_t> lat0;
+  for (int j = 0; j < npatch; ++j) {
+    const int64_t b = ptr[j], nj = ptr[j + 1] - ptr[j];
+    if (nj != L.n)
+      throw Error(FDMGPU_UNSUPPORTED, "patch " + std::to_string(j) + " (vertex " + std::to_string(vertex[j]) +
+                                          ") has " + std::to_string(nj) + " DOFs, expected (2p-1)^d = " +
+                                          std::to_string(L.n) + " (boundary or non-lattice star)");
+    const int gv = dofs[b + perm[b + nj - 1]];  // the vertex DOF is eliminated last
+    for (int k = 0; k < ncorner; ++k) {
+      const int K = star_cells[size_t(j) * ncorner + k];
+      if (K < 0 || K >= c.ncells) throw Error(FDMGPU_UNSUPPORTED, "patch star is not 2^d cells");
+      int bits = -1;
+      for (int cb = 0; cb < ncorner && bits < 0; ++cb) {
+        int l = 0, stride = 1;
+        for (int a = 0; a < d; ++a, stride *= n1) l += ((cb >> a) & 1) * p * stride;
+        if (c.h_cell_dofs[size_t(K) * c.npc + l] == gv) bits = cb;
+      }
+      if (bits < 0) throw Error(FDMGPU_UNSUPPORTED, "star cell does not contain the patch vertex");
+      const int slot = (~bits) & (ncorner - 1);
+      if (c.h_pcells[size_t(j) * ncorner + slot] >= 0) throw Error(FDMGPU_UNSUPPORTED, "star cells overlap a slot");
+      c.h_pcells[size_t(j) * ncorner + slot] = K;
+      int l[3] = {0, 0, 0};
+      for (int lin = 0; lin < c.npc; ++lin) {
+        int P[3] = {0, 0, 0};
+        bool in = true;
+        for (int a = 0; a < d; ++a) {
+          P[a] = ((slot >> a) & 1) * p + l[a];
+          in = in && P[a] >= 1 && P[a] <= 2 * p - 1;
+        }
+        if (in) {
+          const int g = c.h_cell_dofs[size_t(K) * c.npc + lin];
+          const int32_t code = pack(P);
+          if (where[g] == -1) {
+            where[g] = code;
+            touched.push_back(g);
+          } else if (where[g] != code) {
+            throw Error(FDMGPU_UNSUPPORTED, "inconsistent lattice position of a shared DOF");
+          }
+        }
+        for (int a = 0; a < d; ++a) {
+          if (++l[a] <= p) break;
+          l[a] = 0;
+        }
+      }
+    }
+    std::vector<int32_t> latj(L.n);
+    for (int k = 0; k < L.n; ++k) {
+      const int g = dofs[b + perm[b + k]];
+      c.h_pdofs[size_t(j) * L.n + k] = g;
+      latj[k] = where[g];
+      if (latj[k] < 0) throw Error(FDMGPU_UNSUPPORTED, "patch DOF outside its star lattice");
+    }
+    for (int g : touched) where[g] = -1;
+    touched.clear();
+    if (j == 0)
+      lat0 = latj;
+    else if (latj != lat0)
+      throw Error(FDMGPU_UNSUPPORTED, "patch " + std::to_string(j) +
+                                          " does not share the canonical elimination order (non-lattice mesh)");
+  }
+  L.lat = lat0;
+  int span_d = 1;
+  for (int a = 0; a < d; ++a) span_d *= L.span;
+  L.pos_of_lat.assign(span_d, -1);
+  auto lin_of = [&](const int* P) {
+    int v = 0, s = 1;
+    for (int a = 0; a < d; ++a, s *= L.span) v += P[a] * s;
+    return v;
+  };
+  for (int k = 0; k < L.n; ++k) {
+    int P[3];
+    unpack(L.lat[k], P);
+    L.pos_of_lat[lin_of(P)] = k;
+    bool interior = true;
+    for (int a = 0; a < d; ++a) interior = interior && P[a] != p;
+    if (interior != (k < L.nI)) throw Error(FDMGPU_UNSUPPORTED, "patch ordering does not eliminate interiors first");
+  }
+
+  // ---- symbolic factorisation of the canonical patch (src/cholesky.cpp:18-31)
+  const int T = kTile;
+  L.nT = (L.m + T - 1) / T;
+  L.mpad = L.nT * T;
+  std::vector<std::vector<int>> Acols(n1);
+  for (int i = 0; i < n1; ++i)
+    for (int jj = 0; jj < n1; ++jj)
+      if (c.h_Anz[i + size_t(n1) * jj] || c.h_Bnz[i + size_t(n1) * jj]) Acols[i].push_back(jj);
+  auto has = [&](const std::vector<uint8_t>& nz, int i, int jj) { return nz[i + size_t(n1) * jj] != 0; };
+  std::vector<int> parent(L.n, -1), flag(L.n, -1), colcount(L.n, 1), mark(L.n, -1), row;
+  std::vector<uint8_t> tmark(size_t(L.nT) * L.nT, 0);
+  for (int k = 0; k < L.n; ++k) {
+    int P[3];
+    unpack(L.lat[k], P);
+    row.clear();
+    // cells containing P: per axis s_a in {0} (P<p), {1} (P>p) or {0,1} (P==p)
+    int lo[3], hi[3];
+    for (int a = 0; a < 3; ++a) {
+      lo[a] = a < d ? (P[a] > p ? 1 : 0) : 0;
+      hi[a] = a < d ? (P[a] < p ? 0 : 1) : 0;
+    }
+    for (int s2 = lo[2]; s2 <= hi[2]; ++s2)
+      for (int s1 = lo[1]; s1 <= hi[1]; ++s1)
+        for (int s0 = lo[0]; s0 <= hi[0]; ++s0) {
+          const int s[3] = {s0, s1, s2};
+          int l[3] = {0, 0, 0};
+          for (int a = 0; a < d; ++a) l[a] = P[a] - s[a] * p;
+          const auto& c0 = Acols[l[0]];
+          const auto& c1 = Acols[l[1]];
+          static const std::vector<int> zero{0};
+          const auto& c2 = d == 3 ? Acols[l[2]] : zero;
+          for (int x2 : c2)
+            for (int x1 : c1)
+              for (int x0 : c0) {
+                const int x[3] = {x0, x1, x2};
+                bool any = false;
+                for (int a = 0; a < d && !any; ++a) {
+                  bool all = true;
+                  for (int bb = 0; bb < d && all; ++bb) all = has(bb == a ? c.h_Anz : c.h_Bnz, l[bb], x[bb]);
+                  any = all;
+                }
+                if (!any) continue;
+                int Q[3] = {0, 0, 0};
+                bool in = true;
+                for (int a = 0; a < d; ++a) {
+                  Q[a] = s[a] * p + x[a];
+                  in = in && Q[a] >= 1 && Q[a] <= 2 * p - 1;
+                }
+                if (!in) continue;
+                const int pos = L.pos_of_lat[lin_of(Q)];
+                if (pos >= 0 && pos < k && mark[pos] != k) {
+                  mark[pos] = k;
+                  row.push_back(pos);
+                }
+              }
+        }
+    flag[k] = k;
+    for (int j0 : row) {
+      for (int jj = j0; jj < k && flag[jj] != k; jj = parent[jj]) {
+        if (parent[jj] == -1) parent[jj] = k;
+        ++colcount[jj];
+        flag[jj] = k;
+        if (k >= L.nI && jj >= L.nI) tmark[size_t((k - L.nI) / T) * L.nT + (jj - L.nI) / T] = 1;
+      }
+    }
+  }
+  for (int k = 0; k < L.n; ++k) {
+    L.nnz_L += colcount[k];
+    L.flops_ref += int64_t(colcount[k]) * (colcount[k] - 1) / 2;
+  }
+  for (int K = 0; K < L.nT; ++K) tmark[size_t(K) * L.nT + K] = 1;
+  std::vector<int32_t> tidx(size_t(L.nT) * L.nT, -1);
+  for (int K = 0; K < L.nT; ++K) {
+    L.col_start.push_back(int32_t(L.tile_row.size()));
+    for (int I = K; I < L.nT; ++I)
+      if (tmark[size_t(I) * L.nT + K]) {
+        tidx[size_t(I) * L.nT + K] = int32_t(L.tile_row.size());
+        L.tile_row.push_back(I);
+        L.tile_col.push_back(K);
+      }
+  }
+  L.col_start.push_back(int32_t(L.tile_row.size()));
+  L.ntiles = int(L.tile_row.size());
+  L.pair_ptr.push_back(0);
+  for (int t = 0; t < L.ntiles; ++t) {
+    const int I = L.tile_row[t], K = L.tile_col[t];
+    for (int J = 0; J < K; ++J) {
+      const int a = tidx[size_t(I) * L.nT + J], bb = tidx[size_t(K) * L.nT + J];
+      if (a >= 0 && bb >= 0) {
+        L.pair_a.push_back(a);
+        L.pair_b.push_back(bb);
+      }
+    }
+    L.pair_ptr.push_back(int32_t(L.pair_a.size()));
+    if (I != K) ++L.tile_gemms;  // TRSM against the diagonal inverse
+  }
+  L.tile_gemms += int64_t(L.pair_a.size());
+}
+
+}  // namespace fdmgpu
