@@ -57,19 +57,29 @@ void copy_dev(Context& c, double* dst, const double* src) {
 
 // ---- device operators ----------------------------------------------------------
 void op_transform(Context& c, int dir, const double* in, double* out) {
-  launch_cells_transform(c, dir, in);
+  launch_cells_transform(c, dir, in, 0, nullptr);
   launch_gather(c, dir, c.E.p, nullptr, out);
 }
 
+// PatchSolver::apply on a modal vector (src/schwarz.cpp:41-54): Schur-reduced
+// separator RHS, batched separator solves, patch sum, interior rebuild.
 void op_patch(Context& c, const double* in, double* out) {
-  launch_patch_solve(c, in);
+  launch_cells_schur(c, in);
+  launch_gather(c, 3, c.E.p, in, c.w[6].p);
+  launch_patch_solve(c, c.w[6].p);
   launch_patch_gather(c, out);
+  launch_cells_recon(c, out, in);
 }
 
-void op_smooth(Context& c, const double* r, double* z) {  // src/schwarz.cpp:121-123
-  op_transform(c, 0, r, c.w[6].p);
-  op_patch(c, c.w[6].p, c.w[7].p);
-  op_transform(c, 1, c.w[7].p, z);
+// TwoLevel::smooth (src/schwarz.cpp:121-123) = S * PatchSolver(S^T r), with
+// the interior elimination fused into the two cell transforms.
+void op_smooth(Context& c, const double* r, double* z) {
+  launch_cells_transform(c, 0, r, 1, nullptr);  // S^T r, minus each cell's interior-elimination share
+  launch_gather(c, 0, c.E.p, nullptr, c.w[6].p);
+  launch_patch_solve(c, c.w[6].p);               // separator solves
+  launch_patch_gather(c, c.w[7].p);              // patch-summed separator corrections
+  launch_cells_transform(c, 1, c.w[7].p, 2, c.w[6].p);  // rebuild interiors, S
+  launch_gather(c, 1, c.E.p, nullptr, z);
 }
 
 void op_A(Context& c, const double* x, double* y) {  // src/assembly.cpp:56-88
@@ -428,7 +438,17 @@ fdmgpu_status fdmgpu_set_patches(fdmgpu_handle h, int32_t npatch, const int32_t*
     if (tile_bytes + size_t(npatch) * L.n * 12 > free_b)
       throw Error(FDMGPU_OUT_OF_MEMORY, "set_patches: factor needs " + std::to_string(tile_bytes >> 20) +
                                             " MiB, free " + std::to_string(free_b >> 20) + " MiB");
-    c.pdofs.upload(c.h_pdofs, c.stream);
+    // separator DOFs per patch (elimination positions n_I..n-1) and n_K per cell
+    const int m = L.m;
+    std::vector<int32_t> sep(size_t(npatch) * m);
+    std::vector<double> nK(c.ncells, 0.0);
+    for (int j = 0; j < npatch; ++j) {
+      std::copy(c.h_pdofs.begin() + size_t(j) * L.n + L.nI, c.h_pdofs.begin() + size_t(j + 1) * L.n,
+                sep.begin() + size_t(j) * m);
+      for (int k = 0; k < (1 << c.dim); ++k) nK[c.h_pcells[size_t(j) * (1 << c.dim) + k]] += 1.0;
+    }
+    c.pdofs.upload(sep, c.stream);
+    c.nK.upload(nK, c.stream);
     c.lat.upload(L.lat, c.stream);
     c.pos_of_lat.upload(L.pos_of_lat, c.stream);
     c.pcells.upload(c.h_pcells, c.stream);
@@ -444,10 +464,10 @@ fdmgpu_status fdmgpu_set_patches(fdmgpu_handle h, int32_t npatch, const int32_t*
       c.pair_b.upload(L.pair_b, c.stream);
     }
     std::vector<int32_t> pptr, pidx;
-    fdmgpu::build_gather(c.h_pdofs, c.ndof, pptr, pidx);  // ascending (patch, position) per DOF
+    fdmgpu::build_gather(sep, c.ndof, pptr, pidx);  // ascending (patch, position) per separator DOF
     c.pg_ptr.upload(pptr, c.stream);
     c.pg_idx.upload(pidx, c.stream);
-    c.corr.alloc(size_t(npatch) * L.n);
+    c.corr.alloc(size_t(npatch) * m);
     c.tiles.alloc(size_t(npatch) * L.ntiles * fdmgpu::kTile * fdmgpu::kTile);
     FDM_CUDA(cudaStreamSynchronize(c.stream));
     c.have_patches = true;

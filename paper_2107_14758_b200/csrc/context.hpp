@@ -105,7 +105,7 @@ struct Context {
   PatchLayout L;
   DevArray<int32_t> pdofs, lat, pos_of_lat, pcells, pg_ptr, pg_idx;
   DevArray<int32_t> tile_row, tile_col, col_start, pair_ptr, pair_a, pair_b;
-  DevArray<double> corr, tiles;
+  DevArray<double> corr, tiles, nK;
   std::vector<int32_t> h_pdofs, h_pcells;
   bool have_patches = false, factored = false;
   DevArray<unsigned long long> d_err;
@@ -126,7 +126,9 @@ struct Context {
 };
 
 // ---- kernel launchers (kernels/*.cu) -------------------------------------------
-void launch_cells_transform(Context& c, int dir, const double* in);  // writes c.E
+void launch_cells_transform(Context& c, int dir, const double* in, int flags, const double* aux);  // writes c.E
+void launch_cells_schur(Context& c, const double* in);              // writes c.E
+void launch_cells_recon(Context& c, double* z, const double* rb);
 void launch_gather(Context& c, int mode, const double* E, const double* x, double* out);
 void launch_cells_stiffness(Context& c, const double* x);            // writes c.E
 void launch_patch_assemble(Context& c);

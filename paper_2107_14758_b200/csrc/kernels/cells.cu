@@ -13,11 +13,26 @@
 // to a cell-local E-vector; k_gather then sums each global DOF's cell
 // contributions in ascending cell order (the reference's scatter_add order),
 // so there are no FP64 atomics and results are run-to-run deterministic.
+//
+// FDM-interior fusion (used inside the relaxation).  In the FDM basis a
+// cell-interior mode x of cell K couples only to itself (D^K_x = A~_xx) and
+// to the facet modes of K that share its tangential indices.  Every vertex
+// star containing a facet mode contains both cells adjacent to it, so
+//   * the interior-elimination part of each patch's right-hand side,
+//     b_f - sum_{K ∋ f} sum_x A~^K_fx b_x / D^K_x, is the same for every patch:
+//     the S^T kernel subtracts its cell's share at the facet points (SCHUR);
+//   * the patch-summed interior correction is
+//     z_x = (n_K b_x - sum_{faces (a,e) of K} A~^K_{x,f(a,e,x)} z_f) / D^K_x,
+//     with z_f the patch-summed facet correction and n_K the number of stars
+//     containing K: the S kernel rebuilds it before contracting (RECON).
+// The patch kernel is then left with the separator solve only.
 #include "common.cuh"
 
 namespace fdmgpu {
 
 namespace {
+
+enum : int { kSchur = 1, kRecon = 2 };
 
 // out[.., k, ..] = alpha * sum_j M1[k + n1 j] in1[.., j, ..] (+ beta * same with M2/in2)
 __device__ __forceinline__ void contract(int n1, int npc, int stride, const double* __restrict__ M1,
@@ -35,16 +50,127 @@ __device__ __forceinline__ void contract(int n1, int npc, int stride, const doub
   }
 }
 
-__global__ void k_cells_transform(int dim, int n1, int npc, int dir, const double* __restrict__ in,
-                                  double* __restrict__ E, const int32_t* __restrict__ cdofs,
-                                  const double* __restrict__ inv_mult, const uint8_t* __restrict__ cons,
-                                  const double* __restrict__ sign, const double* __restrict__ M) {
+struct CellFdm {
+  int dim, n1, p, ni;     // ni = (p-1)^dim interior points
+  const double* At;       // shared-memory copies, (p+1)^2 column-major
+  const double* Bt;
+  double mu[3];
+  double* invD;           // ni
+};
+
+// lattice index of interior point number ii (each coordinate in 1..p-1)
+__device__ __forceinline__ int interior_lat(const CellFdm& f, int ii, int* x) {
+  const int pm = f.p - 1;
+  int lin = 0, stride = 1;
+  for (int a = 0; a < f.dim; ++a, stride *= f.n1) {
+    x[a] = 1 + ii % pm;
+    ii /= pm;
+    lin += x[a] * stride;
+  }
+  return lin;
+}
+
+__device__ void compute_invD(const CellFdm& f) {
+  for (int ii = threadIdx.x; ii < f.ni; ii += blockDim.x) {
+    int x[3];
+    interior_lat(f, ii, x);
+    double s = 0.0;
+    for (int q = 0; q < f.dim; ++q) {
+      double prod = f.mu[q];
+      for (int b = f.dim - 1; b >= 0; --b) prod *= (b == q ? f.At : f.Bt)[x[b] * (f.n1 + 1)];
+      s += prod;
+    }
+    f.invD[ii] = 1.0 / s;
+  }
+}
+
+// u[facet point] -= sum_x A~_{f x} u[x] / D_x for the 2 dim faces of the cell.
+__device__ void schur_faces(const CellFdm& f, double* u) {
+  const int pm = f.p - 1;
+  int nt = 1;
+  for (int a = 1; a < f.dim; ++a) nt *= pm;
+  for (int idx = threadIdx.x; idx < 2 * f.dim * nt; idx += blockDim.x) {
+    const int face = idx / nt, a = face >> 1, e = (face & 1) ? f.p : 0;
+    int t = idx % nt;
+    int x[3] = {0, 0, 0};
+    double coef = f.mu[a];
+    for (int b = 0; b < f.dim; ++b) {
+      if (b == a) continue;
+      x[b] = 1 + t % pm;
+      t /= pm;
+      coef *= f.Bt[x[b] * (f.n1 + 1)];
+    }
+    int stride_a = 1, lin0 = 0, ii0 = 0, istride_a = 1;
+    for (int b = 0, s = 1, is = 1; b < f.dim; ++b, s *= f.n1, is *= pm) {
+      if (b == a) {
+        stride_a = s;
+        istride_a = is;
+      } else {
+        lin0 += x[b] * s;
+        ii0 += (x[b] - 1) * is;
+      }
+    }
+    double acc = 0.0;
+    for (int xa = 1; xa < f.p; ++xa)
+      acc = fma(f.At[e + f.n1 * xa] * u[lin0 + xa * stride_a], f.invD[ii0 + (xa - 1) * istride_a], acc);
+    u[lin0 + e * stride_a] -= coef * acc;
+  }
+}
+
+// u[x] = (nK * b[x] - sum_{a, e} A~_{x, f(a,e)} u[f(a,e)]) / D_x for every interior x.
+__device__ void recon_interior(const CellFdm& f, double* u, const double* __restrict__ rb,
+                               const int32_t* __restrict__ cd, double nK) {
+  for (int ii = threadIdx.x; ii < f.ni; ii += blockDim.x) {
+    int x[3];
+    const int lin = interior_lat(f, ii, x);
+    double v = nK * rb[cd[lin]];
+    for (int a = 0, s = 1; a < f.dim; ++a, s *= f.n1) {
+      double coef = f.mu[a];
+      for (int b = 0; b < f.dim; ++b)
+        if (b != a) coef *= f.Bt[x[b] * (f.n1 + 1)];
+      const int base = lin - x[a] * s;
+      const double fsum = f.At[x[a] + f.n1 * 0] * u[base] + f.At[x[a] + f.n1 * f.p] * u[base + f.p * s];
+      v -= coef * fsum;
+    }
+    u[lin] = v * f.invD[ii];
+  }
+}
+
+__device__ void load_cell_fdm(CellFdm& f, double* smem_tables, int dim, int n1, int c, const double* __restrict__ mu,
+                              const double* __restrict__ At, const double* __restrict__ Bt) {
+  f.dim = dim;
+  f.n1 = n1;
+  f.p = n1 - 1;
+  f.ni = 1;
+  for (int a = 0; a < dim; ++a) f.ni *= f.p - 1;
+  double* at = smem_tables;
+  double* bt = at + n1 * n1;
+  for (int i = threadIdx.x; i < n1 * n1; i += blockDim.x) {
+    at[i] = At[i];
+    bt[i] = Bt[i];
+  }
+  f.At = at;
+  f.Bt = bt;
+  for (int a = 0; a < 3; ++a) f.mu[a] = a < dim ? mu[size_t(c) * dim + a] : 0.0;
+  f.invD = bt + n1 * n1;
+}
+
+__global__ void k_cells_transform(int dim, int n1, int npc, int dir, int flags, const double* __restrict__ in,
+                                  const double* __restrict__ aux, double* __restrict__ E,
+                                  const int32_t* __restrict__ cdofs, const double* __restrict__ inv_mult,
+                                  const uint8_t* __restrict__ cons, const double* __restrict__ sign,
+                                  const double* __restrict__ M, const double* __restrict__ mu,
+                                  const double* __restrict__ At, const double* __restrict__ Bt,
+                                  const double* __restrict__ nK) {
   extern __shared__ double sm[];
   double* Ms = sm;
   double* b0 = Ms + n1 * n1;
   double* b1 = b0 + npc;
+  double* tables = b1 + npc;  // At, Bt, invD (only with flags)
   const int c = blockIdx.x;
   for (int i = threadIdx.x; i < n1 * n1; i += blockDim.x) Ms[i] = M[i];
+  CellFdm f;
+  if (flags) load_cell_fdm(f, tables, dim, n1, c, mu, At, Bt);
   const int32_t* cd = cdofs + size_t(c) * npc;
   for (int l = threadIdx.x; l < npc; l += blockDim.x) {
     const int g = cd[l];
@@ -56,6 +182,14 @@ __global__ void k_cells_transform(int dim, int n1, int npc, int dir, const doubl
     b0[l] = v;
   }
   __syncthreads();
+  if (flags) {
+    compute_invD(f);
+    __syncthreads();
+  }
+  if (flags & kRecon) {
+    recon_interior(f, b0, aux, cd, nK[c]);
+    __syncthreads();
+  }
   double* src = b0;
   double* dst = b1;
   int stride = 1;
@@ -66,11 +200,77 @@ __global__ void k_cells_transform(int dim, int n1, int npc, int dir, const doubl
     src = dst;
     dst = t;
   }
+  if (dir == 0 && sign) {
+    for (int l = threadIdx.x; l < npc; l += blockDim.x) src[l] *= sign[size_t(c) * npc + l];
+    __syncthreads();
+  }
+  if (flags & kSchur) {
+    schur_faces(f, src);
+    __syncthreads();
+  }
+  double* e = E + size_t(c) * npc;
+  for (int l = threadIdx.x; l < npc; l += blockDim.x) e[l] = src[l];
+}
+
+// PatchSolver-only helpers on modal vectors (FDMGPU_OP_PATCH):
+// E = -(cell share of the interior elimination) at facet points, 0 elsewhere.
+__global__ void k_cells_schur(int dim, int n1, int npc, const double* __restrict__ in, double* __restrict__ E,
+                              const int32_t* __restrict__ cdofs, const uint8_t* __restrict__ cons,
+                              const double* __restrict__ mu, const double* __restrict__ At,
+                              const double* __restrict__ Bt) {
+  extern __shared__ double sm[];
+  double* u = sm;
+  double* tables = u + npc;
+  const int c = blockIdx.x;
+  CellFdm f;
+  load_cell_fdm(f, tables, dim, n1, c, mu, At, Bt);
+  const int32_t* cd = cdofs + size_t(c) * npc;
+  for (int l = threadIdx.x; l < npc; l += blockDim.x) {
+    const int g = cd[l];
+    u[l] = cons[g] ? 0.0 : in[g];
+  }
+  __syncthreads();
+  compute_invD(f);
+  __syncthreads();
+  // keep the interior values, zero everything else, then subtract at facets
+  for (int l = threadIdx.x; l < npc; l += blockDim.x) {
+    bool interior = true;
+    for (int a = 0, r = l; a < dim; ++a, r /= n1) interior = interior && (r % n1 != 0) && (r % n1 != n1 - 1);
+    if (!interior) u[l] = 0.0;
+  }
+  __syncthreads();
+  schur_faces(f, u);
+  __syncthreads();
   double* e = E + size_t(c) * npc;
   for (int l = threadIdx.x; l < npc; l += blockDim.x) {
-    double v = src[l];
-    if (dir == 0 && sign) v *= sign[size_t(c) * npc + l];
-    e[l] = v;
+    bool interior = true;
+    for (int a = 0, r = l; a < dim; ++a, r /= n1) interior = interior && (r % n1 != 0) && (r % n1 != n1 - 1);
+    e[l] = interior ? 0.0 : u[l];
+  }
+}
+
+// Writes the reconstructed interior modes of every cell into z (in place).
+__global__ void k_cells_recon(int dim, int n1, int npc, double* __restrict__ z, const double* __restrict__ rb,
+                              const int32_t* __restrict__ cdofs, const double* __restrict__ mu,
+                              const double* __restrict__ At, const double* __restrict__ Bt,
+                              const double* __restrict__ nK) {
+  extern __shared__ double sm[];
+  double* u = sm;
+  double* tables = u + npc;
+  const int c = blockIdx.x;
+  CellFdm f;
+  load_cell_fdm(f, tables, dim, n1, c, mu, At, Bt);
+  const int32_t* cd = cdofs + size_t(c) * npc;
+  for (int l = threadIdx.x; l < npc; l += blockDim.x) u[l] = z[cd[l]];
+  __syncthreads();
+  compute_invD(f);
+  __syncthreads();
+  recon_interior(f, u, rb, cd, nK[c]);
+  __syncthreads();
+  for (int ii = threadIdx.x; ii < f.ni; ii += blockDim.x) {
+    int x[3];
+    const int lin = interior_lat(f, ii, x);
+    z[cd[lin]] = u[lin];
   }
 }
 
@@ -120,7 +320,7 @@ __global__ void k_cells_stiffness(int dim, int n1, int npc, const double* __rest
 }
 
 // mode 0: apply_St (sum, project); 1: apply_S (sum * inv_mult, project);
-// 2: operator (sum; constrained rows y_i = x_i).
+// 2: operator (sum; constrained rows y_i = x_i); 3: x + sum (project).
 __global__ void k_gather(int64_t ndof, int mode, const double* __restrict__ E, const int32_t* __restrict__ ptr,
                          const int32_t* __restrict__ idx, const double* __restrict__ inv_mult,
                          const uint8_t* __restrict__ cons, const double* __restrict__ x, double* __restrict__ out) {
@@ -129,29 +329,54 @@ __global__ void k_gather(int64_t ndof, int mode, const double* __restrict__ E, c
   double s = 0.0;
   for (int q = ptr[g]; q < ptr[g + 1]; ++q) s += E[idx[q]];
   if (mode == 1) s *= inv_mult[g];
+  if (mode == 3) s += x[g];
   if (cons[g]) s = (mode == 2) ? x[g] : 0.0;
   out[g] = s;
 }
 
+size_t fdm_tables_bytes(const Context& c) {
+  int ni = 1;
+  for (int a = 0; a < c.dim; ++a) ni *= c.p - 1;
+  return sizeof(double) * (2 * size_t(c.n1) * c.n1 + size_t(ni));
+}
+
+template <class K>
+void set_smem(K kernel, size_t smem) {
+  if (smem > 227 * 1024) throw Error(FDMGPU_UNSUPPORTED, "cell tile exceeds shared memory (p too large for dim)");
+  FDM_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+}
+
+int cell_threads(const Context& c) { return c.npc >= 1024 ? 512 : 256; }
+
 }  // namespace
 
-void launch_cells_transform(Context& c, int dir, const double* in) {
-  const size_t smem = sizeof(double) * (size_t(c.n1) * c.n1 + 2 * size_t(c.npc));
-  if (smem > 227 * 1024) throw Error(FDMGPU_UNSUPPORTED, "cell tile exceeds shared memory (p too large for dim)");
-  static bool attr_set = false;
-  if (!attr_set) {
-    FDM_CUDA(cudaFuncSetAttribute(k_cells_transform, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    attr_set = true;
-  }
-  const int threads = c.npc >= 1024 ? 512 : 256;
-  k_cells_transform<<<c.ncells, threads, smem, c.stream>>>(
-      c.dim, c.n1, c.npc, dir, in, c.E.p, dir == 0 ? c.cell_dofs.p : c.cell_modes.p, c.inv_mult.p, c.constrained.p,
-      c.mode_sign.p, dir == 0 ? c.St.p : c.S.p);
+void launch_cells_transform(Context& c, int dir, const double* in, int flags, const double* aux) {
+  const size_t smem = sizeof(double) * (size_t(c.n1) * c.n1 + 2 * size_t(c.npc)) + (flags ? fdm_tables_bytes(c) : 0);
+  set_smem(k_cells_transform, smem);
+  k_cells_transform<<<c.ncells, cell_threads(c), smem, c.stream>>>(
+      c.dim, c.n1, c.npc, dir, flags, in, aux, c.E.p, dir == 0 ? c.cell_dofs.p : c.cell_modes.p, c.inv_mult.p,
+      c.constrained.p, c.mode_sign.p, dir == 0 ? c.St.p : c.S.p, c.mu.p, c.At.p, c.Bt.p, c.nK.p);
+  FDM_LAUNCH_CHECK(c);
+}
+
+void launch_cells_schur(Context& c, const double* in) {
+  const size_t smem = sizeof(double) * size_t(c.npc) + fdm_tables_bytes(c);
+  set_smem(k_cells_schur, smem);
+  k_cells_schur<<<c.ncells, cell_threads(c), smem, c.stream>>>(c.dim, c.n1, c.npc, in, c.E.p, c.cell_modes.p,
+                                                               c.constrained.p, c.mu.p, c.At.p, c.Bt.p);
+  FDM_LAUNCH_CHECK(c);
+}
+
+void launch_cells_recon(Context& c, double* z, const double* rb) {
+  const size_t smem = sizeof(double) * size_t(c.npc) + fdm_tables_bytes(c);
+  set_smem(k_cells_recon, smem);
+  k_cells_recon<<<c.ncells, cell_threads(c), smem, c.stream>>>(c.dim, c.n1, c.npc, z, rb, c.cell_modes.p, c.mu.p,
+                                                               c.At.p, c.Bt.p, c.nK.p);
   FDM_LAUNCH_CHECK(c);
 }
 
 void launch_gather(Context& c, int mode, const double* E, const double* x, double* out) {
-  const bool modes = (mode == 0) && !c.modes_alias;
+  const bool modes = (mode == 0 || mode == 3) && !c.modes_alias;
   const int threads = 256;
   const int64_t blocks = (c.ndof + threads - 1) / threads;
   k_gather<<<unsigned(blocks), threads, 0, c.stream>>>(c.ndof, mode, E, modes ? c.gm_ptr.p : c.g_ptr.p,
@@ -163,15 +388,9 @@ void launch_gather(Context& c, int mode, const double* E, const double* x, doubl
 void launch_cells_stiffness(Context& c, const double* x) {
   if (!c.all_cartesian) throw Error(FDMGPU_UNSUPPORTED, "non-Cartesian cells need the quadrature operator");
   const size_t smem = sizeof(double) * (2 * size_t(c.n1) * c.n1 + 4 * size_t(c.npc));
-  if (smem > 227 * 1024) throw Error(FDMGPU_UNSUPPORTED, "cell tile exceeds shared memory (p too large for dim)");
-  static bool attr_set = false;
-  if (!attr_set) {
-    FDM_CUDA(cudaFuncSetAttribute(k_cells_stiffness, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    attr_set = true;
-  }
-  const int threads = c.npc >= 1024 ? 512 : 256;
-  k_cells_stiffness<<<c.ncells, threads, smem, c.stream>>>(c.dim, c.n1, c.npc, x, c.E.p, c.cell_dofs.p,
-                                                           c.constrained.p, c.mu.p, c.Ahat.p, c.Bhat.p);
+  set_smem(k_cells_stiffness, smem);
+  k_cells_stiffness<<<c.ncells, cell_threads(c), smem, c.stream>>>(c.dim, c.n1, c.npc, x, c.E.p, c.cell_dofs.p,
+                                                                   c.constrained.p, c.mu.p, c.Ahat.p, c.Bhat.p);
   FDM_LAUNCH_CHECK(c);
 }
 

@@ -398,8 +398,6 @@ __global__ void __launch_bounds__(kSolveThreads)
   uint64_t* empty = full + stages;
   const int j = blockIdx.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int ncorner = 1 << a.dim;
-  const int32_t* pd = pdofs + size_t(j) * a.n;
   const double* tb = tiles + size_t(j) * a.ntiles * TT;
   if (tid == 0) {
     for (int s = 0; s < stages; ++s) {
@@ -431,70 +429,41 @@ __global__ void __launch_bounds__(kSolveThreads)
   }
 
   constexpr int NC = 32 * kSolveConsumers;
-  const double* At = a.At;
-  const double* Bt = a.Bt;
-  double mup[24];
-  for (int i = 0; i < ncorner * a.dim; ++i)
-    mup[i] = a.mu[size_t(a.pcells[size_t(j) * ncorner + i / a.dim]) * a.dim + i % a.dim];
-
-  // ---- phase A: separator RHS  b_G - A~_GI D^{-1} b_I (interiors in elimination order)
-  for (int r = tid; r < a.mpad; r += NC) {
-    double b = 0.0;
-    if (r < a.m) {
-      int P[3] = {0, 0, 0};
-      unpack(a.lat[a.nI + r], P);
-      b = rt[pd[a.nI + r]];
-      const int fa = facet_axis(a, P);
-      if (fa >= 0) {
-        for (int sf = 0; sf < 2; ++sf) {
-          int s[3] = {0, 0, 0}, l[3] = {0, 0, 0};
-          for (int qq = 0; qq < a.dim; ++qq) {
-            s[qq] = qq == fa ? sf : (P[qq] > a.p ? 1 : 0);
-            l[qq] = P[qq] - s[qq] * a.p;
-          }
-          const double* mus = mup + (s[0] | (s[1] << 1) | (s[2] << 2)) * a.dim;
-          const int e = l[fa];
-          int x[3] = {l[0], l[1], l[2]};
-          for (int xi = 1; xi < a.p; ++xi) {
-            x[fa] = xi;
-            int Px[3] = {0, 0, 0};
-            for (int qq = 0; qq < a.dim; ++qq) Px[qq] = s[qq] * a.p + x[qq];
-            const double bx = rt[pd[a.pos_of_lat[lin_of(a, Px)]]];
-            b -= facet_coupling(a, mus, fa, e, xi, x, At, Bt) * bx / diag_interior(a, mus, x, At, Bt);
-          }
-        }
-      }
-    }
-    y[r] = b;
-  }
+  // ---- phase A: gather the Schur-reduced separator RHS (the interior elimination
+  // was folded into the S^T cell kernel: bhat is patch independent) ----------------
+  const int32_t* pdI = pdofs + size_t(j) * a.m;
+  for (int r = tid; r < a.mpad; r += NC) y[r] = r < a.m ? rt[pdI[r]] : 0.0;
   named_sync(1, NC);
 
+  // Ring slot s = q % stages is owned by consumer warp s (stages <= 8), so
+  // every slot's fills are waited on by one warp, in order: the mbarrier
+  // parity can never be two phases ahead of its waiter.
   // ---- phase B: forward substitution over tile columns (y <- L_G^{-1} y) ----------------
   int q = 0;  // stream position, mirrors the producer
   for (int K = 0; K < a.nT; ++K) {
     const int t0 = col_start[K], cnt = col_start[K + 1] - t0;
     double* yK = y + K * T;
-    if (warp == 0) {
+    if (warp == q % stages) {
       const int s = q % stages;
       mbar_wait(&full[s], (q / stages) & 1);
-      const double* Li = ring + size_t(s) * TT;  // L_KK^{-1}
+      const double* Li = ring + size_t(s) * TT;  // L_KK^{-1} (lower, zero above)
       double v0 = 0.0, v1 = 0.0;
-      for (int c = 0; c <= lane + 32 && c < T; ++c) {
+#pragma unroll 8
+      for (int c = 0; c < T; ++c) {
         const double yc = yK[c];
-        if (c <= lane) v0 = fma(Li[tsw(lane, c)], yc, v0);
+        v0 = fma(Li[tsw(lane, c)], yc, v0);
         v1 = fma(Li[tsw(lane + 32, c)], yc, v1);
       }
       __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
       yK[lane] = v0;
       yK[lane + 32] = v1;
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
     }
     ++q;
     named_sync(1, NC);
     for (int i = 1; i < cnt; ++i, ++q) {
-      if ((i - 1) % kSolveConsumers != warp) continue;
       const int s = q % stages;
+      if (s != warp) continue;
       mbar_wait(&full[s], (q / stages) & 1);
       const double* Lt = ring + size_t(s) * TT;
       double v0 = 0.0, v1 = 0.0;
@@ -518,8 +487,8 @@ __global__ void __launch_bounds__(kSolveThreads)
     const int t0 = col_start[K], cnt = col_start[K + 1] - t0;
     double a0 = 0.0, a1 = 0.0;
     for (int i = 1; i < cnt; ++i, ++q) {
-      if ((i - 1) % kSolveConsumers != warp) continue;
       const int s = q % stages;
+      if (s != warp) continue;
       mbar_wait(&full[s], (q / stages) & 1);
       const double* Lt = ring + size_t(s) * TT;
       const double* xI = y + tile_row[t0 + i] * T;
@@ -535,7 +504,7 @@ __global__ void __launch_bounds__(kSolveThreads)
     part[warp * T + lane] = a0;
     part[warp * T + lane + 32] = a1;
     named_sync(1, NC);
-    if (warp == 0) {
+    if (warp == q % stages) {
       double* yK = y + K * T;
       double u0 = yK[lane], u1 = yK[lane + 32];
       for (int w = 0; w < kSolveConsumers; ++w) {
@@ -549,42 +518,24 @@ __global__ void __launch_bounds__(kSolveThreads)
       mbar_wait(&full[s], (q / stages) & 1);
       const double* Li = ring + size_t(s) * TT;  // x_K = L_KK^{-T} y_K
       double v0 = 0.0, v1 = 0.0;
-      for (int r = lane; r < T; ++r) {
+#pragma unroll 8
+      for (int r = 0; r < T; ++r) {
         const double yr = yK[r];
         v0 = fma(Li[tsw(r, lane)], yr, v0);
-        if (r >= lane + 32) v1 = fma(Li[tsw(r, lane + 32)], yr, v1);
+        v1 = fma(Li[tsw(r, lane + 32)], yr, v1);
       }
       __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
       yK[lane] = v0;
       yK[lane + 32] = v1;
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
     }
     ++q;
     named_sync(1, NC);
   }
 
-  // ---- phase D: interiors x_I = D^{-1} (b_I - A~_IG x_G); write c_j -------------------------
-  double* cj = corr + size_t(j) * a.n;
-  for (int k = tid; k < a.nI; k += NC) {
-    int P[3] = {0, 0, 0}, s[3] = {0, 0, 0}, l[3] = {0, 0, 0};
-    unpack(a.lat[k], P);
-    for (int b = 0; b < a.dim; ++b) {
-      s[b] = P[b] > a.p ? 1 : 0;
-      l[b] = P[b] - s[b] * a.p;
-    }
-    const double* mus = mup + (s[0] | (s[1] << 1) | (s[2] << 2)) * a.dim;
-    double v = rt[pd[k]];
-    for (int fa = 0; fa < a.dim; ++fa) {
-      int Pf[3] = {P[0], P[1], P[2]};
-      Pf[fa] = a.p;
-      const int e = s[fa] == 0 ? a.p : 0;
-      const double xf = y[a.pos_of_lat[lin_of(a, Pf)] - a.nI];
-      v -= facet_coupling(a, mus, fa, e, l[fa], l, At, Bt) * xf;
-    }
-    cj[k] = v / diag_interior(a, mus, l, At, Bt);
-  }
-  for (int r = tid; r < a.m; r += NC) cj[a.nI + r] = y[r];
+  // ---- phase D: write the separator solution x_G (interiors are rebuilt per cell)
+  double* cj = corr + size_t(j) * a.m;
+  for (int r = tid; r < a.m; r += NC) cj[r] = y[r];
 }
 
 // z[g] = sum of patch corrections of DOF g in ascending patch order
@@ -640,7 +591,7 @@ void launch_patch_trsm(Context& c, int K) {
 static int solve_stages(const Context& c, size_t* smem_out) {
   const size_t fixed = sizeof(double) * (size_t(c.L.mpad) + kSolveConsumers * T);
   const size_t budget = 227 * 1024;
-  int stages = 8;
+  int stages = kSolveConsumers;  // one ring slot per consumer warp at most
   while (stages > 2 && fixed + stages * (sizeof(double) * TT + 16) > budget) --stages;
   *smem_out = fixed + stages * sizeof(double) * TT + 2 * stages * sizeof(uint64_t);
   if (*smem_out > budget) throw Error(FDMGPU_UNSUPPORTED, "separator too large for the shared-memory solve");
