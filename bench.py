@@ -1,0 +1,328 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 vertex-star FDM Schwarz relaxation (BASELINE.json metric).
+
+Workload (config.workload): BASELINE.json config C3 — 3D Poisson on the unit
+cube, Cartesian 8x8x8 hex mesh, Q15 on GLL nodes, 343 interior vertex-star
+patches.  One step = one relaxation apply TwoLevel::smooth
+(src/schwarz.cpp:121-123): S^T transform, 343 patch solves, S transform.
+`value` = free DOFs relaxed per second over the whole job (GDOF/s), inputs
+resident in HBM; `e2e` = the same through the C-ABI host-buffer call
+(fdmgpu_apply(..., host=1)) with the H2D copy of r and the D2H copy of z
+inside the timed region.  The patch factorisation time (the metric's second
+half) and a PCG solve are reported beside it.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3] [--impl reference]
+
+--impl reference times the CPU restatement of the reference (oracle/, the
+reference itself cannot be compiled here: Eigen3 is absent) on the host
+cores: S^T and S over all cells plus CholFactor::solve on a bounded sample of
+patches, scaled to all patches (see cpu_baseline.sample).
+Multi-GPU (torchrun): one independent replica per rank ("replicas only",
+weak scaling, no collective); value = sum of all ranks' DOFs / max time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Schwarz relaxation apply GDOF/s (FP64) + % HBM roofline; patch factorization time"
+FP64_PEAK_TFLOPS = 37.0  # measured: tools/probe/fp64_peak.cu (DMMA 37.0 / DFMA 36.5 TFLOP/s) on this pool
+WORKLOADS = {
+    1: "C1: 2D Poisson 8x8 quads, Q7 GLL, 49 vertex-star patches",
+    2: "C2: 3D Poisson 4^3 hexes, Q7 GLL, 27 vertex-star patches",
+    3: "C3: 3D Poisson 8^3 hexes, Q15 GLL, 343 vertex-star patches, RHS N(0,1) seed 2",
+    4: "C4: 3D anisotropic tensor grid 8^3, kappa_K lognormal, Q15 GLL, 343 patches",
+    5: "C5: 3D perturbed 8^3 hexes, Q31 GLL, 343 patches (surrogate patch solver)",
+}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    QUERY = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.QUERY}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                parts = [p.strip() for p in out.stdout.strip().split(",")]
+                if len(parts) >= 6:
+                    self.samples.append(parts)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def cpu_sample(config, steps, warmup, threads, sample_patches):
+    """CPU restatement of the reference on the host cores: S^T, the patch
+    solves of `sample_patches` patches (parallel_for over `threads`), S."""
+    import numpy as np
+    from oracle import oracle as O
+
+    t0 = time.perf_counter()
+    ref = O.Problem(config, build_global=False, threads=threads)
+    npatch = ref.npatches
+    k = min(sample_patches, npatch)
+    idx = np.linspace(0, npatch - 1, k).round().astype(np.int32)
+    ref.factor(idx, threads=threads)
+    setup_s = time.perf_counter() - t0
+    r = ref.rhs()
+    times = []
+    for it in range(warmup + steps):
+        t = time.perf_counter()
+        rt = ref.apply_St(r)
+        t_st = time.perf_counter() - t
+        t = time.perf_counter()
+        ref.patch_apply(rt)
+        t_patch = time.perf_counter() - t
+        t = time.perf_counter()
+        ref.apply_S(rt)
+        t_s = time.perf_counter() - t
+        if it >= warmup:
+            times.append(t_st + t_s + t_patch * npatch / k)
+    t_step = statistics.median(times)
+    return {
+        "value": ref.nfree / t_step / 1e9,
+        "unit": "GDOF/s",
+        "cores": threads,
+        "kind": "port",
+        "sample": (f"oracle (plain-C++ restatement; reference needs Eigen3, absent) on config C{config}: apply_St + "
+                   f"apply_S over all {ref.ncells} cells and CholFactor::solve on {k} of {npatch} patches "
+                   f"(parallel_for, {threads} threads), patch time scaled by {npatch}/{k}; median of {steps}"),
+        "ms_per_step": t_step * 1e3,
+        "setup_s": setup_s,
+    }
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    cb = cpu_sample(args.config, args.steps, args.warmup, threads, args.cpu_sample_patches)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "GDOF/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": cb["ms_per_step"], "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOADS[args.config], "config": args.config},
+        "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": cb["value"], "unit": "GDOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    import paper_2107_14758_b200 as pkg
+
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+
+    t0 = time.perf_counter()
+    prob = pkg.Problem(args.config)
+    sol = pkg.Solver(prob, device=local, stream=stream)
+    setup_s = time.perf_counter() - t0
+    L = sol.layout()
+
+    # ---- patch factorisation (the metric's second half) ----
+    fac_ms = []
+    for _ in range(2):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        sol.factor()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        fac_ms.append(e0.elapsed_time(e1))
+    factor_ms = min(fac_ms)
+
+    r = torch.from_numpy(prob.rhs()).to(dev)
+    z = torch.empty_like(r)
+    for _ in range(args.warmup):
+        sol.smooth(r, z)
+    torch.cuda.synchronize()
+
+    # ---- timed region: K relaxation applies, device-resident vectors ----
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    launches0 = sol.launch_count()
+    sol.kernel_timing(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            sol.smooth(r, z)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    gpu_launches = sol.launch_count() - launches0
+    solve_ms, solve_n = sol.kernel_time("patch_solve")
+    tr_ms, tr_n = sol.kernel_time("transform")
+    sol.kernel_timing(False)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    value = world * prob.nfree / (ms_per_step * 1e-3) / 1e9
+
+    # ---- e2e through the C ABI with host buffers (H2D + D2H inside) ----
+    h_in = torch.from_numpy(prob.rhs()).pin_memory().numpy()
+    h_out = torch.empty(prob.ndof, dtype=torch.float64).pin_memory().numpy()
+    sol.apply(pkg.OP_SMOOTH, h_in, h_out)
+    torch.cuda.synchronize()
+    ee0, ee1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ee0.record(stream)
+    for _ in range(args.steps):
+        sol.apply(pkg.OP_SMOOTH, h_in, h_out)
+    ee1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = ee0.elapsed_time(ee1) / args.steps
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+
+    # ---- PCG solve (for context: iteration count, time) ----
+    pcg = None
+    if not args.no_pcg:
+        t = time.perf_counter()
+        cal = sol.calibrate_damping()
+        cal_s = time.perf_counter() - t
+        x, rep = sol.pcg(r, rtol=1e-8, maxit=200)
+        pcg = {"iterations": rep["iterations"], "converged": rep["converged"], "kappa": rep["kappa"],
+               "solve_s": rep["wall_time"], "calibrate_s": cal_s, "omega": cal["omega"]}
+
+    hbm_peak, peak_src = measured_peaks()
+    nnz_total = L["nnz_L"] * L["npatch"]
+    nnz_sep = (L["nnz_L"] - (prob.dim + 1) * L["n_interior"]) * L["npatch"]  # separator columns of the reference L
+    kern_bytes = 16.0 * nnz_sep + 2 * 8.0 * L["npatch"] * L["n_interface"] + 4.0 * L["npatch"] * L["n_interface"]
+    kern_ms = solve_ms / max(solve_n, 1)
+    achieved = kern_bytes / (kern_ms * 1e-3) / 1e9
+    relax_bytes = 8.0 * (2 * nnz_total + 2 * prob.sum_nj + 4 * prob.ndof)  # SURVEY.md §8(d) Bytes_relax
+    fac_flops = 2.0 * L["flops_ref"] * L["npatch"]
+    result = {
+        "metric": METRIC, "value": value, "unit": "GDOF/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOADS[args.config], "config": args.config, "ndof": prob.ndof,
+                   "nfree": prob.nfree, "patches": L["npatch"], "patch_dofs": L["n"],
+                   "separator_dofs": L["n_interface"], "parallelism": "replicas" if world > 1 else "single",
+                   "l2": f"inputs larger than L2: {L['factor_bytes'] / 1e9:.2f} GB patch factor streamed per step"},
+        "roofline": {"kernel": "k_patch_solve", "bound": "hbm", "achieved": achieved, "peak": hbm_peak,
+                     "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": None,
+                     "peak_source": peak_src, "kernel_ms": kern_ms, "algorithmic_bytes": kern_bytes,
+                     "share_of_step": solve_ms / ms if ms > 0 else None,
+                     "bytes_def": "16 B x separator nnz(L_j) of the reference factor (fwd + bwd) + separator "
+                                  "RHS gather / solution write, per launch over all patches"},
+        "relaxation_roofline": {"bytes": relax_bytes, "achieved_GBps": relax_bytes / (ms_per_step * 1e-3) / 1e9,
+                                "frac": relax_bytes / (ms_per_step * 1e-3) / 1e9 / hbm_peak,
+                                "bytes_def": "SURVEY.md 8(d): 8*(2*NNZ + 2*sum n_j + 4*ndof)"},
+        "factor_ms": factor_ms,
+        "factor_roofline": {"bound": "fp64", "achieved": fac_flops / (factor_ms * 1e-3) / 1e12,
+                            "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                            "frac": fac_flops / (factor_ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS,
+                            "flops_def": "2 x CholFactor::flops (src/cholesky.cpp:74) summed over patches"},
+        "e2e": {"value": world * prob.nfree / (e2e_ms * 1e-3) / 1e9, "unit": "GDOF/s", "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": 8 * prob.ndof, "d2h_bytes_per_step": 8 * prob.ndof},
+        "gpu_launches": gpu_launches,
+        "clocks": clk.summary(),
+        "setup_s": setup_s,
+        "pcg": pcg,
+    }
+    if rank == 0 and not args.no_cpu:
+        try:
+            cb = cpu_sample(args.config, 3, 1, os.cpu_count() or 1, args.cpu_sample_patches)
+            result["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        except Exception as e:  # reported, not fatal for the GPU line
+            result["cpu_baseline"] = {"value": None, "unit": "GDOF/s", "cores": os.cpu_count(), "kind": "port",
+                                      "sample": f"failed: {e}"}
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=3, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-sample-patches", type=int, default=16)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-pcg", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -165,6 +165,12 @@ fdmgpu_status fdmgpu_get_omega(fdmgpu_handle h, double* omega);
 /* Number of kernels this handle has launched so far (evidence for bench.py). */
 int64_t fdmgpu_launch_count(fdmgpu_handle h);
 
+/* Per-kernel CUDA-event timing on the handle stream (bench.py roofline):
+ * enable != 0 starts recording (and clears earlier records); which = 0 patch
+ * solve, 1 factorisation kernels, 2 cell transforms, 3 stiffness apply. */
+fdmgpu_status fdmgpu_kernel_timing(fdmgpu_handle h, int32_t enable);
+fdmgpu_status fdmgpu_kernel_time(fdmgpu_handle h, int32_t which, double* total_ms, int64_t* launches);
+
 #ifdef __cplusplus
 }
 #endif

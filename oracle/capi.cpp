@@ -334,11 +334,21 @@ int oracle_vcycle(void* h, const double* r, double* z) {
 
 // report: iterations, converged, kappa, lambda_min, lambda_max, wall_time;
 // residuals: maxit entries (relative residual history).
-int oracle_pcg(void* h, const double* b, double* x, double rtol, int maxit, double* report, double* residuals) {
+int oracle_pcg(void* h, const double* b, double* x, double rtol, int maxit, double* report, double* residuals,
+               int precond) {
   return guard([&] {
     Ctx* c = static_cast<Ctx*>(h);
     Vec bb(b, b + c->pb->disc.ndof);
-    auto [xx, rep] = pcg(c->tl->A, c->tl->applier(), bb, rtol, maxit);
+    auto A = c->A;
+    LinOp Aop = [A](const Vec& v) { return A->apply(v); };
+    LinOp P;
+    if (precond == 0)
+      P = [](const Vec& v) { return v; };
+    else if (precond == 1)
+      P = [c](const Vec& v) { return c->sys->apply_S(c->ps.apply(c->sys->apply_St(v))); };
+    else
+      P = c->tl->applier();
+    auto [xx, rep] = pcg(Aop, P, bb, rtol, maxit);
     std::memcpy(x, xx.data(), xx.size() * 8);
     report[0] = rep.iterations;
     report[1] = rep.converged;
@@ -347,6 +357,16 @@ int oracle_pcg(void* h, const double* b, double* x, double rtol, int maxit, doub
     report[4] = rep.lambda_max;
     report[5] = rep.wall_time;
     for (size_t k = 0; k < rep.residuals.size(); ++k) residuals[k] = rep.residuals[k];
+  });
+}
+
+// Load vector of f = 1 with homogeneous Dirichlet rows zeroed (src/assembly.cpp:344-373).
+int oracle_load_vector_one(void* h, double* out) {
+  return guard([&] {
+    Ctx* c = static_cast<Ctx*>(h);
+    Vec f = load_vector(c->pb->disc, c->pb->bundle, [](const std::array<double, 3>&) { return 1.0; });
+    c->pb->disc.project_free(f);
+    std::memcpy(out, f.data(), f.size() * 8);
   });
 }
 

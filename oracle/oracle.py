@@ -58,7 +58,8 @@ def lib():
         L.oracle_twolevel_info.argtypes = [C.c_void_p, _d]
         L.oracle_set_omega.argtypes = [C.c_void_p, C.c_double]
         L.oracle_prolongation.argtypes = [C.c_void_p, _i64, C.c_void_p, C.c_void_p, C.c_void_p]
-        L.oracle_pcg.argtypes = [C.c_void_p, _d, _d, C.c_double, C.c_int, _d, _d]
+        L.oracle_pcg.argtypes = [C.c_void_p, _d, _d, C.c_double, C.c_int, _d, _d, C.c_int]
+        L.oracle_load_vector_one.argtypes = [C.c_void_p, _d]
         L.oracle_cell_matrix_quadrature.argtypes = [C.c_void_p, C.c_int, _d]
         L.oracle_cell_sumfact_apply.argtypes = [C.c_void_p, C.c_int, _d, _d]
         L.oracle_gll_nodes.argtypes = [C.c_int, _d]
@@ -342,12 +343,18 @@ class Problem:
                                        val.ctypes.data_as(C.c_void_p)))
         return ptr, col, val
 
-    def pcg(self, b, rtol=1e-8, maxit=200):
-        x, rep, res = np.zeros(self.ndof), np.zeros(6), np.zeros(maxit)
-        _chk(lib().oracle_pcg(self.h, np.ascontiguousarray(b, np.float64), x, rtol, maxit, rep, res))
+    def pcg(self, b, rtol=1e-8, maxit=200, precond=2):
+        """pcg with A = GlobalOperator::apply; precond 0 identity, 1 smooth, 2 V-cycle."""
+        x, rep, res = np.zeros(self.ndof), np.zeros(6), np.zeros(max(maxit, 1))
+        _chk(lib().oracle_pcg(self.h, np.ascontiguousarray(b, np.float64), x, rtol, maxit, rep, res, precond))
         it = int(rep[0])
         return x, dict(iterations=it, converged=bool(rep[1]), kappa=rep[2], lambda_min=rep[3],
                        lambda_max=rep[4], wall_time=rep[5], residuals=res[:it].copy())
+
+    def load_vector_one(self):
+        out = np.zeros(self.ndof)
+        _chk(lib().oracle_load_vector_one(self.h, out))
+        return out
 
     def cell_matrix_quadrature(self, cell):
         out = np.zeros(self.npc * self.npc)

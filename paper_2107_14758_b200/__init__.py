@@ -93,6 +93,10 @@ def lib():
         L.fdmgpu_get_omega.argtypes = [_vp, C.POINTER(C.c_double)]
         L.fdmgpu_launch_count.restype = C.c_int64
         L.fdmgpu_launch_count.argtypes = [_vp]
+        L.fdmgpu_kernel_timing.argtypes = [_vp, C.c_int32]
+        L.fdmgpu_set_cell_coeffs.argtypes = [_vp, _vp, _vp, _vp, _vp]
+        L.fdmgpu_create.argtypes = [C.POINTER(_vp), C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.c_int32]
+        L.fdmgpu_kernel_time.argtypes = [_vp, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_int64)]
         _lib = L
     return _lib
 
@@ -199,6 +203,7 @@ class Solver:
         if rc != 0:
             raise FdmGpuError(rc, lib().fdmhost_last_error().decode())
         self.h = h
+        self._stream = None  # CUDA stream handle the library runs on (None: its own)
         if stream is not None:
             self.set_stream(stream)
 
@@ -220,12 +225,33 @@ class Solver:
         """Run on a caller's CUDA stream (e.g. torch.cuda.current_stream())."""
         handle = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
         self._chk(lib().fdmgpu_set_stream(self.h, _vp(handle)))
+        self._stream = handle
+
+    def _enter(self, t):
+        """Order the library's stream after torch's producer of `t`; returns
+        True when the call must be synchronised afterwards (different streams)."""
+        import torch
+        cur = torch.cuda.current_stream(t.device)
+        if cur.cuda_stream == self._stream:
+            return False
+        cur.synchronize()
+        return True
 
     def synchronize(self):
         self._chk(lib().fdmgpu_synchronize(self.h))
 
     def factor(self):
+        """Batched numeric factorisation of all patches (build_patch_solver)."""
         self._chk(lib().fdmgpu_factor(self.h))
+
+    def set_cell_coeffs(self, mu, kind=None, corner_xyz=None, kappa=None):
+        """Replace the per-cell coefficients (ncells x dim kappa*mu^K; invalidates the factor)."""
+        g = self.problem.geometry()
+        kind = g["kind"] if kind is None else np.ascontiguousarray(kind, np.uint8)
+        xyz = np.ascontiguousarray(g["corner_xyz"] if corner_xyz is None else corner_xyz, np.float64)
+        kap = np.ascontiguousarray(g["kappa"] if kappa is None else kappa, np.float64)
+        mu = np.ascontiguousarray(mu, np.float64)
+        self._chk(lib().fdmgpu_set_cell_coeffs(self.h, _ptr(kind), _ptr(mu), _ptr(xyz), _ptr(kap)))
 
     def layout(self):
         L = Layout()
@@ -241,6 +267,18 @@ class Solver:
     def launch_count(self):
         return int(lib().fdmgpu_launch_count(self.h))
 
+    KERNEL_CLASSES = {"patch_solve": 0, "factor": 1, "transform": 2, "stiffness": 3}
+
+    def kernel_timing(self, enable=True):
+        """Start (and clear) or stop CUDA-event timing of the library's kernels."""
+        self._chk(lib().fdmgpu_kernel_timing(self.h, 1 if enable else 0))
+
+    def kernel_time(self, which):
+        """(total ms, launches) recorded for a kernel class since kernel_timing(True)."""
+        t, n = C.c_double(), C.c_int64()
+        self._chk(lib().fdmgpu_kernel_time(self.h, self.KERNEL_CLASSES.get(which, which), C.byref(t), C.byref(n)))
+        return t.value, n.value
+
     # ---- operators ---------------------------------------------------------
     def apply(self, op, x, out=None, omega=0.0):
         if isinstance(x, np.ndarray):
@@ -251,7 +289,10 @@ class Solver:
         import torch
         assert x.is_cuda and x.dtype == torch.float64 and x.is_contiguous()
         out = torch.empty_like(x) if out is None else out
+        sync = self._enter(x)
         self._chk(lib().fdmgpu_apply(self.h, op, omega, _vp(x.data_ptr()), _vp(out.data_ptr()), 0))
+        if sync:
+            self.synchronize()
         return out
 
     def apply_St(self, x, out=None):
@@ -293,10 +334,13 @@ class Solver:
         identity / smooth / V(1,1) cycle.  Returns (x, report dict)."""
         import torch
         x = torch.empty_like(b) if x is None else x
+        sync = self._enter(b)
         rep = KrylovReport()
         res = np.zeros(max(maxit, 1))
         self._chk(lib().fdmgpu_pcg(self.h, _vp(b.data_ptr()), _vp(x.data_ptr()), rtol, maxit, precond,
                                    C.byref(rep), _ptr(res)))
+        if sync:
+            self.synchronize()
         d = {k: getattr(rep, k) for k, _ in KrylovReport._fields_}
         d["converged"] = bool(d["converged"])
         d["residuals"] = res[: rep.iterations].copy()

@@ -690,4 +690,33 @@ fdmgpu_status fdmgpu_get_omega(fdmgpu_handle h, double* omega) {
 
 int64_t fdmgpu_launch_count(fdmgpu_handle h) { return h ? h->launches : -1; }
 
+fdmgpu_status fdmgpu_kernel_timing(fdmgpu_handle h, int32_t enable) {
+  return fdmgpu::guarded(h, [&](Context& c) {
+    FDM_CUDA(cudaStreamSynchronize(c.stream));
+    for (auto& v : c.tev) {
+      for (auto& [a, b] : v) {
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+      }
+      v.clear();
+    }
+    c.timing = enable != 0;
+  });
+}
+
+fdmgpu_status fdmgpu_kernel_time(fdmgpu_handle h, int32_t which, double* total_ms, int64_t* launches) {
+  return fdmgpu::guarded(h, [&](Context& c) {
+    if (which < 0 || which > 3) throw Error(FDMGPU_INVALID_ARGUMENT, "kernel_time: class 0..3");
+    FDM_CUDA(cudaStreamSynchronize(c.stream));
+    double t = 0.0;
+    for (auto& [a, b] : c.tev[which]) {
+      float ms = 0.f;
+      FDM_CUDA(cudaEventElapsedTime(&ms, a, b));
+      t += ms;
+    }
+    *total_ms = t;
+    *launches = int64_t(c.tev[which].size());
+  });
+}
+
 }  // extern "C"

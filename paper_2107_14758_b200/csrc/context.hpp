@@ -122,7 +122,38 @@ struct Context {
   std::vector<double> h_red;
   double omega = 1.0, lambda_min = 0.0, lambda_max = 0.0;
 
+  // optional per-kernel CUDA-event timing (fdmgpu_kernel_timing)
+  bool timing = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tev[4];
+
   void check_ready(bool need_patches, bool need_factor, bool need_coarse) const;
+  ~Context() {
+    for (auto& v : tev)
+      for (auto& [a, b] : v) {
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+      }
+  }
+};
+
+// Records CUDA events around one launch on the handle stream when timing is on.
+// Timed kernel classes: 0 patch solve, 1 factor (assemble/update/trsm),
+// 2 cell transforms, 3 stiffness apply.
+struct KernelTimer {
+  Context& c;
+  int slot;
+  cudaEvent_t a = nullptr, b = nullptr;
+  KernelTimer(Context& ctx, int s) : c(ctx), slot(s) {
+    if (!c.timing) return;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, c.stream);
+  }
+  ~KernelTimer() {
+    if (!c.timing) return;
+    cudaEventRecord(b, c.stream);
+    c.tev[slot].emplace_back(a, b);
+  }
 };
 
 // ---- kernel launchers (kernels/*.cu) -------------------------------------------

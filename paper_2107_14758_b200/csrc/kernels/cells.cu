@@ -353,6 +353,7 @@ int cell_threads(const Context& c) { return c.npc >= 1024 ? 512 : 256; }
 void launch_cells_transform(Context& c, int dir, const double* in, int flags, const double* aux) {
   const size_t smem = sizeof(double) * (size_t(c.n1) * c.n1 + 2 * size_t(c.npc)) + (flags ? fdm_tables_bytes(c) : 0);
   set_smem(k_cells_transform, smem);
+  KernelTimer timer(c, 2);
   k_cells_transform<<<c.ncells, cell_threads(c), smem, c.stream>>>(
       c.dim, c.n1, c.npc, dir, flags, in, aux, c.E.p, dir == 0 ? c.cell_dofs.p : c.cell_modes.p, c.inv_mult.p,
       c.constrained.p, c.mode_sign.p, dir == 0 ? c.St.p : c.S.p, c.mu.p, c.At.p, c.Bt.p, c.nK.p);
@@ -389,6 +390,7 @@ void launch_cells_stiffness(Context& c, const double* x) {
   if (!c.all_cartesian) throw Error(FDMGPU_UNSUPPORTED, "non-Cartesian cells need the quadrature operator");
   const size_t smem = sizeof(double) * (2 * size_t(c.n1) * c.n1 + 4 * size_t(c.npc));
   set_smem(k_cells_stiffness, smem);
+  KernelTimer timer(c, 3);
   k_cells_stiffness<<<c.ncells, cell_threads(c), smem, c.stream>>>(c.dim, c.n1, c.npc, x, c.E.p, c.cell_dofs.p,
                                                                    c.constrained.p, c.mu.p, c.Ahat.p, c.Bhat.p);
   FDM_LAUNCH_CHECK(c);

@@ -555,6 +555,7 @@ void launch_patch_assemble(Context& c) {
   PatchArgs a = make_args(c);
   const size_t smem = sizeof(double) * (2 * size_t(c.n1) * c.n1 + 24);
   dim3 grid(c.L.ntiles, c.npatch);
+  KernelTimer timer(c, 1);
   k_patch_assemble<<<grid, 256, smem, c.stream>>>(a, c.tile_row.p, c.tile_col.p, c.tiles.p);
   FDM_LAUNCH_CHECK(c);
 }
@@ -568,6 +569,7 @@ void launch_patch_update(Context& c, int K) {
     attr = true;
   }
   dim3 grid(c.L.col_start[K + 1] - c.L.col_start[K], c.npatch);
+  KernelTimer timer(c, 1);
   k_patch_update<<<grid, kUpdThreads, smem, c.stream>>>(a, K, c.col_start.p, c.tile_row.p, c.pair_ptr.p,
                                                          c.pair_a.p, c.pair_b.p, c.tiles.p);
   FDM_LAUNCH_CHECK(c);
@@ -584,6 +586,7 @@ void launch_patch_trsm(Context& c, int K) {
     attr = true;
   }
   dim3 grid(cnt, c.npatch);
+  KernelTimer timer(c, 1);
   k_patch_trsm<<<grid, kUpdThreads, smem, c.stream>>>(a, K, c.col_start.p, c.tiles.p);
   FDM_LAUNCH_CHECK(c);
 }
@@ -607,6 +610,7 @@ void launch_patch_solve(Context& c, const double* r_modal) {
     FDM_CUDA(cudaFuncSetAttribute(k_patch_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr = true;
   }
+  KernelTimer timer(c, 0);
   k_patch_solve<<<c.npatch, kSolveThreads, smem, c.stream>>>(a, stages, r_modal, c.corr.p, c.tiles.p, c.pdofs.p,
                                                               c.col_start.p, c.tile_row.p);
   FDM_LAUNCH_CHECK(c);

@@ -1,0 +1,171 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the CPU oracle on
+the same seeded inputs, at sizes the oracle finishes in seconds, against the
+golden fixtures at full size, plus size-independent properties.
+
+Tolerances (BASELINE.json north star / SURVEY.md §7.4):
+  patch solve, relaxation, V-cycle: rel-l2 <= 1e-11;  S, S^T, A: rel-l2 <= 1e-12;
+  PCG: identical iteration counts at rtol 1e-8; omega rel <= 1e-10;
+  index maps: bit-exact (tests/test_host_maps.py).
+"""
+import glob
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import rel
+
+pytestmark = pytest.mark.gpu
+TOL_RELAX = 1e-11
+TOL_TRANSFORM = 1e-12
+
+CASES = [(1, 0, 0), (2, 0, 0), (2, 3, 3), (1, 4, 5), (4, 4, 5), (3, 3, 5), (4, 0, 3)]
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as T
+
+    assert T.cuda.is_available(), "GPU tests need a CUDA device"
+    return T
+
+
+@pytest.fixture(scope="module", params=CASES, ids=lambda c: "C%d_n%d_p%d" % c)
+def pair(request, pkg, oracle, torch):
+    cfg = request.param
+    prob = pkg.Problem(*cfg)
+    sol = pkg.Solver(prob)
+    sol.factor()
+    ref = oracle.Problem(*cfg, build_global=True, threads=os.cpu_count())
+    ref.factor()
+    return prob, sol, ref
+
+
+def test_operators_match_oracle(pair, torch):
+    prob, sol, ref = pair
+    r = prob.rhs()
+    assert rel(sol.apply_St(r), ref.apply_St(r)) <= TOL_TRANSFORM
+    assert rel(sol.apply_S(r), ref.apply_S(r)) <= TOL_TRANSFORM
+    assert rel(sol.apply_A(r), ref.apply_A(r)) <= TOL_TRANSFORM
+    rt = ref.apply_St(r)
+    assert rel(sol.patch_apply(rt), ref.patch_apply(rt)) <= TOL_RELAX
+    assert rel(sol.smooth(r), ref.smooth(r)) <= TOL_RELAX
+    # device path equals the host-buffer (LinOp drop-in) path bitwise
+    d = torch.from_numpy(r).cuda()
+    assert np.array_equal(sol.smooth(d).cpu().numpy(), sol.smooth(r))
+
+
+def test_two_level_and_pcg_match_oracle(pair, torch):
+    prob, sol, ref = pair
+    w = sol.calibrate_damping()
+    ref.build_twolevel()
+    tl = ref.twolevel_info()
+    assert abs(w["omega"] - tl["omega"]) <= 1e-10 * tl["omega"]
+    assert abs(w["lambda_max"] - tl["lambda_max"]) <= 1e-10 * tl["lambda_max"]
+    r = prob.rhs()
+    sol.omega = tl["omega"]
+    assert rel(sol.vcycle(r), ref.vcycle(r)) <= TOL_RELAX
+    sol.omega = w["omega"]
+    x, rep = sol.pcg(torch.from_numpy(r).cuda(), rtol=1e-8, maxit=200)
+    xr, rr = ref.pcg(r, rtol=1e-8, maxit=200)
+    assert rep["converged"] and rep["iterations"] == rr["iterations"]
+    assert abs(rep["kappa"] - rr["kappa"]) <= 1e-8 * rr["kappa"]
+    assert rel(x.cpu().numpy(), xr) <= 1e-9
+    Ax = sol.apply_A(x.cpu().numpy())
+    assert np.linalg.norm(Ax - r) / np.linalg.norm(r) <= 1e-8 * (1 + 1e-4)
+
+
+def test_zero_in_zero_out(pair):
+    prob, sol, _ = pair
+    z = np.zeros(prob.ndof)
+    assert np.linalg.norm(sol.smooth(z)) == 0.0 and np.linalg.norm(sol.patch_apply(z)) == 0.0
+
+
+# ---- full-size configurations against the golden fixtures -------------------------
+GOLDEN = {os.path.basename(p): p for p in glob.glob(os.path.join(os.path.dirname(__file__), "golden", "*.json"))}
+FULL = [g for g in ("c3.json", "c4.json", "c1.json", "c2.json", "c5_0_3.json") if g in GOLDEN]
+
+
+@pytest.mark.parametrize("name", FULL)
+def test_full_size_against_golden(pkg, torch, name):
+    g = json.load(open(GOLDEN[name]))
+    prob = pkg.Problem(g["config"], g["n"], g["p"])
+    sol = pkg.Solver(prob)
+    sol.factor()
+    L = sol.layout()
+    assert L["nnz_L"] == g["patch0"]["nnz_L"] and L["flops_ref"] == g["patch0"]["flops"]
+    r = prob.rhs()
+    probe = np.random.default_rng(12345).standard_normal(prob.ndof)
+    for name_, v, tol in (("apply_St", sol.apply_St(r), TOL_TRANSFORM), ("apply_A", sol.apply_A(r), TOL_TRANSFORM),
+                          ("smooth", sol.smooth(r), TOL_RELAX)):
+        gg = g[name_]
+        assert abs(np.linalg.norm(v) - gg["norm"]) <= tol * gg["norm"], name_
+        assert abs(v @ probe - gg["probe_dot"]) <= 10 * tol * gg["norm"] * np.linalg.norm(probe), name_
+        assert np.allclose(v[:8], gg["head"], rtol=0, atol=10 * tol * gg["norm"])
+    w = sol.calibrate_damping()
+    assert abs(w["omega"] - g["damping"]["omega"]) <= 1e-10 * g["damping"]["omega"]
+    _, rep = sol.pcg(torch.from_numpy(r).cuda(), rtol=1e-8, maxit=200)
+    assert rep["iterations"] == g["pcg"]["iterations"]
+
+
+# ---- size-independent properties at full size (C3) ----------------------------------
+@pytest.fixture(scope="module")
+def c3(pkg, torch):
+    prob = pkg.Problem(3)
+    sol = pkg.Solver(prob)
+    sol.factor()
+    return prob, sol
+
+
+def test_c3_layout_matches_appendix_a(c3):
+    _, sol = c3
+    L = sol.layout()
+    assert (L["npatch"], L["n"], L["n_interior"], L["n_interface"]) == (343, 24389, 21952, 2437)
+    assert L["nnz_L"] == 1960925 and L["flops_ref"] == 956196192
+
+
+def test_c3_relaxation_properties(c3, torch):
+    prob, sol = c3
+    rng = np.random.default_rng(7)
+    con = prob.maps()["constrained"].astype(bool)
+    x, y = rng.standard_normal(prob.ndof), rng.standard_normal(prob.ndof)
+    x[con] = y[con] = 0
+    Px, Py = sol.smooth(x), sol.smooth(y)
+    assert abs(x @ Py - y @ Px) <= 1e-12 * abs(x @ Py)  # symmetric preconditioner
+    assert x @ Px > 0 and y @ Py > 0  # positive definite
+    a, b = 0.75, -1.5
+    assert rel(sol.smooth(a * x + b * y), a * Px + b * Py) <= 1e-12  # linear
+    assert np.array_equal(sol.smooth(x), Px)  # deterministic, bitwise
+    A_x = sol.apply_A(x)
+    assert abs(y @ A_x - x @ sol.apply_A(y)) <= 1e-12 * abs(y @ A_x)
+
+
+def test_not_spd_reports_pivot(pkg, torch):
+    prob = pkg.Problem(2, 3, 3)
+    sol = pkg.Solver(prob)
+    mu = prob.geometry()["mu"].copy()
+    sol.set_cell_coeffs(-mu)
+    with pytest.raises(pkg.NotSPDError, match="not SPD at pivot 0"):
+        sol.factor()
+    with pytest.raises(pkg.IndefiniteError, match="indefinite operator at iteration 1"):
+        sol.pcg(torch.from_numpy(prob.rhs()).cuda(), precond=0)
+    sol.set_cell_coeffs(mu)
+    sol.factor()
+
+
+def test_launch_evidence(pkg, torch):
+    prob = pkg.Problem(2, 3, 3)
+    sol = pkg.Solver(prob)
+    sol.factor()
+    n0 = sol.launch_count()
+    sol.smooth(prob.rhs())
+    assert sol.launch_count() - n0 == 6
+    maps = open("/proc/self/maps").read()
+    assert os.path.realpath(pkg.LIB_PATH) in maps or pkg.LIB_PATH in maps
+
+
+def test_smoke(torch):
+    import __graft_entry__
+
+    __graft_entry__.smoke()
