@@ -92,12 +92,13 @@ fdmgpu_status fdmgpu_synchronize(fdmgpu_handle h);
  * (reference_interval.hpp:15-27).  All (p+1)^2 arrays column-major:
  * S, A_t = S^T A S, B_t = S^T B S (values + structural 0/1 patterns), lambda
  * (p-1 interior eigenvalues), A_hat / B_hat (reference stiffness / mass),
- * and the GL(q) tables Vq, Dq (q x (p+1), column-major) with weights wq used
- * by the true-form trilinear operator (src/assembly.cpp:198-215, q = p+2). */
+ * and the GL(q) rule (points, weights) with its tables Vq, Dq (q x (p+1),
+ * column-major) used by the true-form trilinear operator
+ * (src/assembly.cpp:198-215, q = p+2). */
 fdmgpu_status fdmgpu_set_basis(fdmgpu_handle h, const double* S, const double* lambda, const double* A_t,
                                const double* B_t, const uint8_t* A_t_pattern, const uint8_t* B_t_pattern,
-                               const double* A_hat, const double* B_hat, int32_t q, const double* Vq,
-                               const double* Dq, const double* wq);
+                               const double* A_hat, const double* B_hat, int32_t q, const double* q_points,
+                               const double* wq, const double* Vq, const double* Dq);
 
 /* Discretization::Component maps (include/fdmstar/discretization.hpp:22-34):
  * cell_dofs / cell_modes ncells x (p+1)^d (axis 0 fastest), optional

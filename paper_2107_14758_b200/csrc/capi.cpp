@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <random>
@@ -285,6 +286,8 @@ fdmgpu_status fdmgpu_create(fdmgpu_handle* out, int32_t dim, int32_t p, int32_t 
     FDM_CUDA(cudaSetDevice(cc.device));
     FDM_CUDA(cudaStreamCreateWithFlags(&cc.stream, cudaStreamNonBlocking));
     cc.own_stream = true;
+    const char* fs = std::getenv("FDMGPU_FORCE_STAGED");
+    cc.force_staged = fs && fs[0] == '1';
     cc.E.alloc(size_t(cc.ncells) * cc.npc);
     for (auto& v : cc.w) v.alloc(cc.ndof);
     cc.red.alloc(4 * fdmgpu::kRedBlocks);
@@ -324,8 +327,8 @@ fdmgpu_status fdmgpu_synchronize(fdmgpu_handle h) {
 
 fdmgpu_status fdmgpu_set_basis(fdmgpu_handle h, const double* S, const double* lambda, const double* A_t,
                                const double* B_t, const uint8_t* A_t_pattern, const uint8_t* B_t_pattern,
-                               const double* A_hat, const double* B_hat, int32_t q, const double* Vq,
-                               const double* Dq, const double* wq) {
+                               const double* A_hat, const double* B_hat, int32_t q, const double* q_points,
+                               const double* wq, const double* Vq, const double* Dq) {
   (void)lambda;
   return fdmgpu::guarded(h, [&](Context& c) {
     if (!S || !A_t || !B_t || !A_t_pattern || !B_t_pattern || !A_hat || !B_hat)
@@ -349,7 +352,8 @@ fdmgpu_status fdmgpu_set_basis(fdmgpu_handle h, const double* S, const double* l
     c.Ahat.upload(A_hat, nn, c.stream);
     c.Bhat.upload(B_hat, nn, c.stream);
     c.q = q;
-    if (q > 0 && Vq && Dq && wq) {
+    if (q > 0 && Vq && Dq && wq && q_points) {
+      c.qpts.upload(q_points, q, c.stream);
       c.Vq.upload(Vq, size_t(q) * n1, c.stream);
       c.Dq.upload(Dq, size_t(q) * n1, c.stream);
       c.wq.upload(wq, q, c.stream);

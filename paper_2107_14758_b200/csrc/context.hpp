@@ -80,7 +80,7 @@ struct Context {
   int64_t ndof = 0;
 
   // basis
-  DevArray<double> S, St, Ahat, Bhat, At, Bt, Vq, Dq, wq;
+  DevArray<double> S, St, Ahat, Bhat, At, Bt, Vq, Dq, wq, qpts, Qbuf;
   std::vector<double> h_At, h_Bt;
   std::vector<uint8_t> h_Anz, h_Bnz;
   int q = 0;
@@ -124,6 +124,7 @@ struct Context {
 
   // optional per-kernel CUDA-event timing (fdmgpu_kernel_timing)
   bool timing = false;
+  bool force_staged = false;  // FDMGPU_FORCE_STAGED=1: staged cell kernels for every p (tests)
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tev[4];
 
   void check_ready(bool need_patches, bool need_factor, bool need_coarse) const;
@@ -162,6 +163,7 @@ void launch_cells_schur(Context& c, const double* in);              // writes c.
 void launch_cells_recon(Context& c, double* z, const double* rb);
 void launch_gather(Context& c, int mode, const double* E, const double* x, double* out);
 void launch_cells_stiffness(Context& c, const double* x);            // writes c.E
+void launch_cells_quadrature(Context& c, const double* x);           // writes c.E (true form)
 void launch_patch_assemble(Context& c);
 void launch_patch_update(Context& c, int K);
 void launch_patch_trsm(Context& c, int K);

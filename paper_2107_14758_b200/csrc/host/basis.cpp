@@ -362,9 +362,8 @@ Basis1D make_bundle(int p) {
   }
   // True-form quadrature tables (src/assembly.cpp:198-215 uses GL(p+2)).
   b.q = p + 2;
-  Vec qp;
-  gauss_legendre(b.q, qp, b.wq);
-  lagrange_eval(b.nodes, qp, b.Vq, b.Dq);
+  gauss_legendre(b.q, b.qp, b.wq);
+  lagrange_eval(b.nodes, b.qp, b.Vq, b.Dq);
   return b;
 }
 

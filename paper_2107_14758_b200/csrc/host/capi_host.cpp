@@ -144,8 +144,8 @@ int fdmhost_attach(void* ph, int device, fdmgpu_handle* out) {
   };
   const Basis1D& b = P.basis;
   if ((st = fdmgpu_set_basis(h, b.S.a.data(), b.lambda.data(), b.A_t.a.data(), b.B_t.a.data(), b.A_nz.data(),
-                             b.B_nz.data(), b.A_hat.a.data(), b.B_hat.a.data(), b.q, b.Vq.a.data(), b.Dq.a.data(),
-                             b.wq.data())) != FDMGPU_OK)
+                             b.B_nz.data(), b.A_hat.a.data(), b.B_hat.a.data(), b.q, b.qp.data(), b.wq.data(),
+                             b.Vq.a.data(), b.Dq.a.data())) != FDMGPU_OK)
     return fail(st);
   const Space& s = P.space;
   if ((st = fdmgpu_set_mesh_maps(h, s.cell_dofs.data(), s.cell_modes.data(),

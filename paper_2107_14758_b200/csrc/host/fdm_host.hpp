@@ -48,7 +48,7 @@ struct Basis1D {
   // GL(p+2) interpolation / derivative tables for the true-form trilinear apply
   int q = 0;
   Dense Vq, Dq;       // q x (p+1)
-  Vec wq;
+  Vec wq, qp;
 };
 Basis1D make_bundle(int p);  // src/assembly.cpp:37-54 (CG family)
 

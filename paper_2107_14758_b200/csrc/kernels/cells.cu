@@ -350,7 +350,7 @@ int cell_threads(const Context& c) { return c.npc >= 1024 ? 512 : 256; }
 
 }  // namespace
 
-void launch_cells_transform(Context& c, int dir, const double* in, int flags, const double* aux) {
+void launch_cells_transform_fused(Context& c, int dir, const double* in, int flags, const double* aux) {
   const size_t smem = sizeof(double) * (size_t(c.n1) * c.n1 + 2 * size_t(c.npc)) + (flags ? fdm_tables_bytes(c) : 0);
   set_smem(k_cells_transform, smem);
   KernelTimer timer(c, 2);
@@ -360,7 +360,7 @@ void launch_cells_transform(Context& c, int dir, const double* in, int flags, co
   FDM_LAUNCH_CHECK(c);
 }
 
-void launch_cells_schur(Context& c, const double* in) {
+void launch_cells_schur_fused(Context& c, const double* in) {
   const size_t smem = sizeof(double) * size_t(c.npc) + fdm_tables_bytes(c);
   set_smem(k_cells_schur, smem);
   k_cells_schur<<<c.ncells, cell_threads(c), smem, c.stream>>>(c.dim, c.n1, c.npc, in, c.E.p, c.cell_modes.p,
@@ -368,7 +368,7 @@ void launch_cells_schur(Context& c, const double* in) {
   FDM_LAUNCH_CHECK(c);
 }
 
-void launch_cells_recon(Context& c, double* z, const double* rb) {
+void launch_cells_recon_fused(Context& c, double* z, const double* rb) {
   const size_t smem = sizeof(double) * size_t(c.npc) + fdm_tables_bytes(c);
   set_smem(k_cells_recon, smem);
   k_cells_recon<<<c.ncells, cell_threads(c), smem, c.stream>>>(c.dim, c.n1, c.npc, z, rb, c.cell_modes.p, c.mu.p,
@@ -386,8 +386,7 @@ void launch_gather(Context& c, int mode, const double* E, const double* x, doubl
   FDM_LAUNCH_CHECK(c);
 }
 
-void launch_cells_stiffness(Context& c, const double* x) {
-  if (!c.all_cartesian) throw Error(FDMGPU_UNSUPPORTED, "non-Cartesian cells need the quadrature operator");
+void launch_cells_stiffness_kron(Context& c, const double* x) {
   const size_t smem = sizeof(double) * (2 * size_t(c.n1) * c.n1 + 4 * size_t(c.npc));
   set_smem(k_cells_stiffness, smem);
   KernelTimer timer(c, 3);
