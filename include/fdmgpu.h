@@ -59,10 +59,14 @@ typedef struct {
   int32_t tile_cols;     /* interface tile rows/columns                           */
   int32_t tiles;         /* stored (non-zero) lower tiles per patch               */
   int32_t pad_;
-  int64_t nnz_L;         /* nnz(L_j) of the reference factor (symbolic), per patch */
-  int64_t flops_ref;     /* CholFactor::flops per patch (multiply-adds)           */
+  int64_t nnz_L;         /* nnz(L_j) under the separator order in use, per patch  */
+  int64_t flops_ref;     /* CholFactor::flops per patch (multiply-adds), same     */
   int64_t factor_bytes;  /* device bytes of the stored factor, all patches        */
   int64_t tile_gemms;    /* tile updates per patch (factorisation work units)     */
+  int64_t nnz_L_reference;   /* nnz(L_j) under the reference patch_ordering       */
+  int64_t flops_reference;   /* CholFactor::flops under the reference ordering    */
+  int32_t separator_order;   /* 0 plane, 1 reference                              */
+  int32_t pad2_;
 } fdmgpu_layout;
 
 /* Operator ids for fdmgpu_apply. */
@@ -162,6 +166,13 @@ fdmgpu_status fdmgpu_calibrate_damping(fdmgpu_handle h, int32_t lanczos_steps, u
                                        double* omega, double* lambda_min, double* lambda_max);
 fdmgpu_status fdmgpu_set_omega(fdmgpu_handle h, double omega);
 fdmgpu_status fdmgpu_get_omega(fdmgpu_handle h, double* omega);
+
+/* Internal elimination order of the separator DOFs, applied by the next
+ * fdmgpu_set_patches: 0 = facet groups plane by plane (default; ~45 % fewer
+ * factor nonzeros), 1 = the reference patch_ordering (src/ordering.cpp:17-45).
+ * Patch solutions agree to rounding either way.  Env FDMGPU_SEP_ORDER=reference
+ * selects 1 at fdmgpu_create. */
+fdmgpu_status fdmgpu_set_separator_order(fdmgpu_handle h, int32_t order);
 
 /* Number of kernels this handle has launched so far (evidence for bench.py). */
 int64_t fdmgpu_launch_count(fdmgpu_handle h);

@@ -46,7 +46,8 @@ class Layout(C.Structure):
     _fields_ = [("npatch", C.c_int32), ("n", C.c_int32), ("n_interior", C.c_int32), ("n_interface", C.c_int32),
                 ("tile", C.c_int32), ("tile_cols", C.c_int32), ("tiles", C.c_int32), ("pad_", C.c_int32),
                 ("nnz_L", C.c_int64), ("flops_ref", C.c_int64), ("factor_bytes", C.c_int64),
-                ("tile_gemms", C.c_int64)]
+                ("tile_gemms", C.c_int64), ("nnz_L_reference", C.c_int64), ("flops_reference", C.c_int64),
+                ("separator_order", C.c_int32), ("pad2_", C.c_int32)]
 
 
 class KrylovReport(C.Structure):
@@ -78,7 +79,7 @@ def lib():
         L.fdmhost_get_basis.argtypes = [_vp] * 11
         L.fdmhost_get_patches.argtypes = [_vp] * 7
         L.fdmhost_get_coarse.argtypes = [_vp] * 5
-        L.fdmhost_attach.argtypes = [_vp, C.c_int, C.POINTER(_vp)]
+        L.fdmhost_attach.argtypes = [_vp, C.c_int, C.c_int, C.POINTER(_vp)]
         L.fdmgpu_destroy.argtypes = [_vp]
         L.fdmgpu_set_stream.argtypes = [_vp, _vp]
         L.fdmgpu_synchronize.argtypes = [_vp]
@@ -195,11 +196,12 @@ class Solver:
     numpy float64 arrays (host path: copied in and out inside the call, the
     LinOp drop-in of src/krylov.hpp:10)."""
 
-    def __init__(self, problem: Problem, device: int = 0, stream=None):
+    def __init__(self, problem: Problem, device: int = 0, stream=None, separator_order: str = "plane"):
         self.problem = problem
         self.ndof = problem.ndof
         h = _vp()
-        rc = lib().fdmhost_attach(problem.h, device, C.byref(h))
+        order = {"plane": 0, "reference": 1}[separator_order]
+        rc = lib().fdmhost_attach(problem.h, device, order, C.byref(h))
         if rc != 0:
             raise FdmGpuError(rc, lib().fdmhost_last_error().decode())
         self.h = h
@@ -256,7 +258,7 @@ class Solver:
     def layout(self):
         L = Layout()
         self._chk(lib().fdmgpu_get_layout(self.h, C.byref(L)))
-        return {k: getattr(L, k) for k, _ in Layout._fields_ if k != "pad_"}
+        return {k: getattr(L, k) for k, _ in Layout._fields_ if not k.startswith("pad")}
 
     def elimination_dofs(self):
         L = self.layout()

@@ -288,6 +288,8 @@ fdmgpu_status fdmgpu_create(fdmgpu_handle* out, int32_t dim, int32_t p, int32_t 
     cc.own_stream = true;
     const char* fs = std::getenv("FDMGPU_FORCE_STAGED");
     cc.force_staged = fs && fs[0] == '1';
+    const char* so = std::getenv("FDMGPU_SEP_ORDER");
+    cc.sep_order = (so && std::string(so) == "reference") ? 1 : 0;
     cc.E.alloc(size_t(cc.ncells) * cc.npc);
     for (auto& v : cc.w) v.alloc(cc.ndof);
     cc.red.alloc(4 * fdmgpu::kRedBlocks);
@@ -460,6 +462,7 @@ fdmgpu_status fdmgpu_set_patches(fdmgpu_handle h, int32_t npatch, const int32_t*
     c.tile_col.upload(L.tile_col, c.stream);
     c.col_start.upload(L.col_start, c.stream);
     c.pair_ptr.upload(L.pair_ptr, c.stream);
+    c.entries.upload(L.entries, c.stream);
     if (L.pair_a.empty()) {
       c.pair_a.alloc(1);
       c.pair_b.alloc(1);
@@ -546,6 +549,9 @@ fdmgpu_status fdmgpu_get_layout(fdmgpu_handle h, fdmgpu_layout* out) {
     L.flops_ref = c.L.flops_ref;
     L.factor_bytes = int64_t(c.tiles.bytes());
     L.tile_gemms = c.L.tile_gemms;
+    L.nnz_L_reference = c.L.nnz_L_reference;
+    L.flops_reference = c.L.flops_reference;
+    L.separator_order = c.sep_order;
     *out = L;
   });
 }
@@ -693,6 +699,13 @@ fdmgpu_status fdmgpu_get_omega(fdmgpu_handle h, double* omega) {
 }
 
 int64_t fdmgpu_launch_count(fdmgpu_handle h) { return h ? h->launches : -1; }
+
+fdmgpu_status fdmgpu_set_separator_order(fdmgpu_handle h, int32_t order) {
+  return fdmgpu::guarded(h, [&](Context& c) {
+    if (order != 0 && order != 1) throw Error(FDMGPU_INVALID_ARGUMENT, "separator order: 0 plane, 1 reference");
+    c.sep_order = order;
+  });
+}
 
 fdmgpu_status fdmgpu_kernel_timing(fdmgpu_handle h, int32_t enable) {
   return fdmgpu::guarded(h, [&](Context& c) {

@@ -66,7 +66,9 @@ struct PatchLayout {
   std::vector<int32_t> pos_of_lat;   // span^d: elimination position or -1
   std::vector<int32_t> tile_row, tile_col, col_start;  // tile pattern, column-major order
   std::vector<int32_t> pair_ptr, pair_a, pair_b;       // left-looking update pairs per tile
-  int64_t nnz_L = 0, flops_ref = 0, tile_gemms = 0;
+  std::vector<int32_t> entries;      // structural nonzeros of S_G: tile << 12 | col << 6 | row
+  int64_t nnz_L = 0, flops_ref = 0, tile_gemms = 0;          // order in use
+  int64_t nnz_L_reference = 0, flops_reference = 0;         // reference patch_ordering
 };
 
 struct Context {
@@ -104,7 +106,7 @@ struct Context {
   int npatch = 0;
   PatchLayout L;
   DevArray<int32_t> pdofs, lat, pos_of_lat, pcells, pg_ptr, pg_idx;
-  DevArray<int32_t> tile_row, tile_col, col_start, pair_ptr, pair_a, pair_b;
+  DevArray<int32_t> tile_row, tile_col, col_start, pair_ptr, pair_a, pair_b, entries;
   DevArray<double> corr, tiles, nK;
   std::vector<int32_t> h_pdofs, h_pcells;
   bool have_patches = false, factored = false;
@@ -124,7 +126,8 @@ struct Context {
 
   // optional per-kernel CUDA-event timing (fdmgpu_kernel_timing)
   bool timing = false;
-  bool force_staged = false;  // FDMGPU_FORCE_STAGED=1: staged cell kernels for every p (tests)
+  bool force_staged = false;
+  int sep_order = 0;  // 0 plane-by-plane facets (default), 1 reference patch_ordering (FDMGPU_SEP_ORDER)  // FDMGPU_FORCE_STAGED=1: staged cell kernels for every p (tests)
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tev[4];
 
   void check_ready(bool need_patches, bool need_factor, bool need_coarse) const;

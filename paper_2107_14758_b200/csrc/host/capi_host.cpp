@@ -129,7 +129,8 @@ int fdmhost_get_coarse(void* ph, double* inverse, int64_t* P_ptr, int32_t* P_col
 
 // Creates an fdmgpu handle for the problem and uploads every input through
 // the public C ABI (does not factor).  Returns the fdmgpu status.
-int fdmhost_attach(void* ph, int device, fdmgpu_handle* out) {
+// sep_order: 0 plane-by-plane separator (default), 1 reference patch_ordering, -1 keep.
+int fdmhost_attach(void* ph, int device, int sep_order, fdmgpu_handle* out) {
   Problem& P = *static_cast<Problem*>(ph);
   fdmgpu_handle h = nullptr;
   fdmgpu_status st = fdmgpu_create(&h, P.dim, P.p, P.mesh.num_cells(), P.space.ndof, device);
@@ -142,6 +143,7 @@ int fdmhost_attach(void* ph, int device, fdmgpu_handle* out) {
     fdmgpu_destroy(h);
     return int(s);
   };
+  if (sep_order >= 0 && (st = fdmgpu_set_separator_order(h, sep_order)) != FDMGPU_OK) return fail(st);
   const Basis1D& b = P.basis;
   if ((st = fdmgpu_set_basis(h, b.S.a.data(), b.lambda.data(), b.A_t.a.data(), b.B_t.a.data(), b.A_nz.data(),
                              b.B_nz.data(), b.A_hat.a.data(), b.B_hat.a.data(), b.q, b.qp.data(), b.wq.data(),

@@ -17,11 +17,24 @@ namespace fdmgpu {
   } while (0)
 
 // Interface-factor tiles are kTile x kTile doubles, column-major with the row
-// index XOR-swizzled by the column's low 4 bits: both a warp reading a column
-// (lanes over rows) and a warp reading a row (lanes over columns) hit 16
-// distinct 8-byte banks per half-warp, so the forward (L x) and backward
-// (L^T x) tile GEMVs and the factor GEMMs are bank-conflict free.
-__host__ __device__ __forceinline__ int tsw(int r, int c) { return c * kTile + (r ^ (c & 15)); }
+// index XOR-swizzled by f(c) = ((c & 3) << 2) | ((c >> 2) & 3), a bit
+// permutation of the column's low 4 bits.  Per half-warp (16 lanes, one
+// 128-byte wavefront of doubles) this is bank-conflict free for
+//   * a column read (lanes over 16 rows, fixed c): r ^ const,
+//   * a row read (lanes over 16 columns, fixed r): f is a permutation of 0..15,
+//   * a DMMA m8n8k4 fragment read (lanes over 4 aligned rows x 4 aligned
+//     columns): rows fill bits 0-1, (c & 3) fills bits 2-3,
+// so the forward (L x) / backward (L^T x) tile GEMVs and the DMMA factor GEMMs
+// all run at full shared-memory bandwidth.
+__host__ __device__ __forceinline__ int tile_swz(int c) { return ((c & 3) << 2) | ((c >> 2) & 3); }
+__host__ __device__ __forceinline__ int tsw(int r, int c) { return c * kTile + (r ^ tile_swz(c)); }
+
+// D = A(8x4, row) * B(4x8, col) + D on the FP64 tensor pipe (SASS DMMA.884).
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

@@ -169,13 +169,16 @@ __device__ __forceinline__ void record_pivot_error(unsigned long long* err, int 
   atomicMin(err, (static_cast<unsigned long long>(patch) << 32) | static_cast<unsigned>(pivot));
 }
 
-__global__ void k_patch_assemble(PatchArgs a, const int32_t* __restrict__ tile_row,
-                                 const int32_t* __restrict__ tile_col, double* __restrict__ tiles) {
+// Separator Schur complement S_G on the structural nonzeros only (`entries`,
+// shared by all patches); all other stored tile entries were zeroed first.
+__global__ void k_patch_assemble(PatchArgs a, int nentries, const int32_t* __restrict__ entries,
+                                 const int32_t* __restrict__ tile_row, const int32_t* __restrict__ tile_col,
+                                 double* __restrict__ tiles) {
   extern __shared__ double sm[];
   double* At = sm;
   double* Bt = At + a.n1 * a.n1;
   double* mup = Bt + a.n1 * a.n1;  // 2^d x d
-  const int t = blockIdx.x, j = blockIdx.y;
+  const int j = blockIdx.y;
   const int ncorner = 1 << a.dim;
   for (int i = threadIdx.x; i < a.n1 * a.n1; i += blockDim.x) {
     At[i] = a.At[i];
@@ -186,50 +189,64 @@ __global__ void k_patch_assemble(PatchArgs a, const int32_t* __restrict__ tile_r
     mup[i] = a.mu[size_t(a.pcells[size_t(j) * ncorner + s]) * a.dim + q];
   }
   __syncthreads();
-  const int I = tile_row[t], K = tile_col[t];
-  double* out = tiles + (size_t(j) * a.ntiles + t) * TT;
-  for (int e = threadIdx.x; e < TT; e += blockDim.x) {
-    const int rr = e % T, cc = e / T;
-    const int r = I * T + rr, c = K * T + cc;
-    double v;
-    if (r >= a.m || c >= a.m)
-      v = (r == c) ? 1.0 : 0.0;
-    else if (I == K && rr < cc)
-      v = 0.0;
-    else
-      v = schur_entry(a, mup, r, c, At, Bt);
-    out[tsw(rr, cc)] = v;
-  }
-  // interior pivots D_k > 0 (the first n_I pivots of the reference order)
-  if (t == 0) {
-    for (int k = threadIdx.x; k < a.nI; k += blockDim.x) {
-      int P[3] = {0, 0, 0}, s[3] = {0, 0, 0}, l[3] = {0, 0, 0};
-      unpack(a.lat[k], P);
-      for (int b = 0; b < a.dim; ++b) {
-        s[b] = P[b] > a.p ? 1 : 0;
-        l[b] = P[b] - s[b] * a.p;
-      }
-      const int slot = s[0] | (s[1] << 1) | (s[2] << 2);
-      if (!(diag_interior(a, mup + slot * a.dim, l, At, Bt) > 0.0)) record_pivot_error(a.err, j, k);
-    }
+  double* base = tiles + size_t(j) * a.ntiles * TT;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nentries; e += gridDim.x * blockDim.x) {
+    const int code = entries[e];
+    const int t = code >> 12, cc = (code >> 6) & 63, rr = code & 63;
+    const int r = tile_row[t] * T + rr, c = tile_col[t] * T + cc;
+    base[size_t(t) * TT + tsw(rr, cc)] = schur_entry(a, mup, r, c, At, Bt);
   }
 }
 
-// acc(16 per thread) += A B^T over one 64-deep k panel; thread (tr, tc) owns
-// rows tr + 16 i and columns tc + 16 jj (conflict-free on the swizzle).
-__device__ __forceinline__ void tile_gemm_abt(const double* __restrict__ A, const double* __restrict__ B, int tr,
-                                              int tc, double acc[4][4]) {
+// Identity on the padded separator positions m..mpad-1 (last diagonal tile)
+// and the interior pivots D_k > 0 (the first n_I pivots of the reference order).
+__global__ void k_patch_pad_check(PatchArgs a, double* __restrict__ tiles, int last_diag) {
+  const int j = blockIdx.x;
+  double* dt = tiles + (size_t(j) * a.ntiles + last_diag) * TT;
+  for (int r = a.m + threadIdx.x; r < a.mpad; r += blockDim.x) dt[tsw(r % T, r % T)] = 1.0;
+  const int ncorner = 1 << a.dim;
+  double mup[24];
+  for (int i = 0; i < ncorner * a.dim; ++i)
+    mup[i] = a.mu[size_t(a.pcells[size_t(j) * ncorner + i / a.dim]) * a.dim + i % a.dim];
+  for (int k = threadIdx.x; k < a.nI; k += blockDim.x) {
+    int P[3] = {0, 0, 0}, s[3] = {0, 0, 0}, l[3] = {0, 0, 0};
+    unpack(a.lat[k], P);
+    for (int b = 0; b < a.dim; ++b) {
+      s[b] = P[b] > a.p ? 1 : 0;
+      l[b] = P[b] - s[b] * a.p;
+    }
+    const int slot = s[0] | (s[1] << 1) | (s[2] << 2);
+    if (!(diag_interior(a, mup + slot * a.dim, l, a.At, a.Bt) > 0.0)) record_pivot_error(a.err, j, k);
+  }
+}
+
+// Warp-tiled FP64 tensor-core GEMM on swizzled 64x64 tiles: acc += A B^T.
+// 8 warps; warp w owns rows 32 (w >> 2) .. +31 and columns 16 (w & 3) .. +15
+// as 4 x 2 DMMA m8n8k4 accumulators (16 doubles per thread).  Fragment loads
+// are conflict-free on the tile swizzle (common.cuh).
+struct TileAcc {
+  double v[4][2][2];
+  __device__ __forceinline__ int row(int i) const { return 32 * ((threadIdx.x >> 5) >> 2) + 8 * i + ((threadIdx.x & 31) >> 2); }
+  __device__ __forceinline__ int col(int j, int e) const {
+    return 16 * ((threadIdx.x >> 5) & 3) + 8 * j + 2 * (threadIdx.x & 3) + e;
+  }
+};
+
+__device__ __forceinline__ void tile_gemm_abt(const double* __restrict__ A, const double* __restrict__ B, TileAcc& acc) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int r0 = 32 * (w >> 2) + (lane >> 2), c0 = 16 * (w & 3) + (lane >> 2), kl = lane & 3;
 #pragma unroll 4
-  for (int k = 0; k < T; ++k) {
-    double av[4], bv[4];
+  for (int k0 = 0; k0 < T; k0 += 4) {
+    const int k = k0 + kl;
+    double av[4], bv[2];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) av[i] = A[tsw(tr + 16 * i, k)];
+    for (int i = 0; i < 4; ++i) av[i] = A[tsw(r0 + 8 * i, k)];
 #pragma unroll
-    for (int jj = 0; jj < 4; ++jj) bv[jj] = B[tsw(tc + 16 * jj, k)];
+    for (int jj = 0; jj < 2; ++jj) bv[jj] = B[tsw(c0 + 8 * jj, k)];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int jj = 0; jj < 4; ++jj) acc[i][jj] = fma(av[i], bv[jj], acc[i][jj]);
+      for (int jj = 0; jj < 2; ++jj) dmma884(acc.v[i][jj][0], acc.v[i][jj][1], av[i], bv[jj]);
   }
 }
 
@@ -294,7 +311,7 @@ __global__ void __launch_bounds__(kUpdThreads) k_patch_update(PatchArgs a, int K
   const int I = tile_row[t];
   double* base = tiles + size_t(j) * a.ntiles * TT;
   const int p0 = pair_ptr[t], np = pair_ptr[t + 1] - p0;
-  const int tid = threadIdx.x, tr = tid >> 4, tc = tid & 15;
+  const int tid = threadIdx.x;
   if (tid == 0) {
     mbar_init(&full[0], 1);
     mbar_init(&full[1], 1);
@@ -307,11 +324,11 @@ __global__ void __launch_bounds__(kUpdThreads) k_patch_update(PatchArgs a, int K
       bulk_g2s(buf + (2 * s) * TT, base + size_t(pair_a[p0 + s]) * TT, TT * sizeof(double), &full[s]);
       bulk_g2s(buf + (2 * s + 1) * TT, base + size_t(pair_b[p0 + s]) * TT, TT * sizeof(double), &full[s]);
     }
-  double acc[4][4] = {};
+  TileAcc acc = {};
   for (int i = 0; i < np; ++i) {
     const int s = i & 1;
     mbar_wait(&full[s], (i >> 1) & 1);
-    tile_gemm_abt(buf + (2 * s) * TT, buf + (2 * s + 1) * TT, tr, tc, acc);
+    tile_gemm_abt(buf + (2 * s) * TT, buf + (2 * s + 1) * TT, acc);
     __syncthreads();
     if (tid == 0 && i + 2 < np) {
       mbar_arrive_expect_tx(&full[s], 2 * TT * sizeof(double));
@@ -324,10 +341,9 @@ __global__ void __launch_bounds__(kUpdThreads) k_patch_update(PatchArgs a, int K
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int jj = 0; jj < 4; ++jj) {
-        const int idx = tsw(tr + 16 * i, tc + 16 * jj);
-        ct[idx] -= acc[i][jj];
-      }
+      for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) ct[tsw(acc.row(i), acc.col(jj, e))] -= acc.v[i][jj][e];
     return;
   }
   constexpr int LD = T + 1;
@@ -336,10 +352,12 @@ __global__ void __launch_bounds__(kUpdThreads) k_patch_update(PatchArgs a, int K
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int jj = 0; jj < 4; ++jj) {
-      const int r = tr + 16 * i, cc = tc + 16 * jj;
-      Dm[cc * LD + r] = ct[tsw(r, cc)] - acc[i][jj];
-    }
+    for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int r = acc.row(i), cc = acc.col(jj, e);
+        Dm[cc * LD + r] = ct[tsw(r, cc)] - acc.v[i][jj][e];
+      }
   for (int e = tid; e < T * LD; e += blockDim.x) Wm[e] = 0.0;
   __syncthreads();
   diag_factor_invert(Dm, Wm, ct, a, K, j);
@@ -355,7 +373,7 @@ __global__ void __launch_bounds__(kUpdThreads) k_patch_trsm(PatchArgs a, int K, 
   const int t0 = col_start[K];
   const int t = t0 + 1 + blockIdx.x, j = blockIdx.y;
   double* base = tiles + size_t(j) * a.ntiles * TT;
-  const int tid = threadIdx.x, tr = tid >> 4, tc = tid & 15;
+  const int tid = threadIdx.x;
   if (tid == 0) {
     mbar_init(&full[0], 1);
     mbar_fence_init();
@@ -367,13 +385,15 @@ __global__ void __launch_bounds__(kUpdThreads) k_patch_trsm(PatchArgs a, int K, 
     bulk_g2s(Ls, base + size_t(t0) * TT, TT * sizeof(double), &full[0]);
   }
   mbar_wait(&full[0], 0);
-  double acc[4][4] = {};
-  tile_gemm_abt(Cs, Ls, tr, tc, acc);
+  TileAcc acc = {};
+  tile_gemm_abt(Cs, Ls, acc);
   double* out = base + size_t(t) * TT;
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int jj = 0; jj < 4; ++jj) out[tsw(tr + 16 * i, tc + 16 * jj)] = acc[i][jj];
+    for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) out[tsw(acc.row(i), acc.col(jj, e))] = acc.v[i][jj][e];
 }
 
 
@@ -553,10 +573,14 @@ __global__ void k_patch_gather(int64_t ndof, const double* __restrict__ corr, co
 
 void launch_patch_assemble(Context& c) {
   PatchArgs a = make_args(c);
-  const size_t smem = sizeof(double) * (2 * size_t(c.n1) * c.n1 + 24);
-  dim3 grid(c.L.ntiles, c.npatch);
   KernelTimer timer(c, 1);
-  k_patch_assemble<<<grid, 256, smem, c.stream>>>(a, c.tile_row.p, c.tile_col.p, c.tiles.p);
+  FDM_CUDA(cudaMemsetAsync(c.tiles.p, 0, c.tiles.bytes(), c.stream));
+  const size_t smem = sizeof(double) * (2 * size_t(c.n1) * c.n1 + 24);
+  const int ne = int(c.L.entries.size());
+  dim3 grid(unsigned((ne + 255) / 256 < 64 ? (ne + 255) / 256 : 64), c.npatch);
+  k_patch_assemble<<<grid, 256, smem, c.stream>>>(a, ne, c.entries.p, c.tile_row.p, c.tile_col.p, c.tiles.p);
+  FDM_LAUNCH_CHECK(c);
+  k_patch_pad_check<<<c.npatch, 256, 0, c.stream>>>(a, c.tiles.p, c.L.col_start[c.L.nT - 1]);
   FDM_LAUNCH_CHECK(c);
 }
 

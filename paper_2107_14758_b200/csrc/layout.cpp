@@ -16,6 +16,8 @@
 // Interior columns have exactly d+1 entries (zero fill)
 // and are never stored: the kernels rebuild them from mu and the 1D tables.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <unordered_map>
@@ -113,6 +115,40 @@ void analyze_patches(Context& c, int npatch, const int32_t* vertex, const int64_
       throw Error(FDMGPU_UNSUPPORTED, "patch " + std::to_string(j) +
                                           " does not share the canonical elimination order (non-lattice mesh)");
   }
+  // Internal separator elimination order.  Default (sep_order 0, "plane"):
+  // the facet groups plane by plane -- the facets of one plane never share a
+  // cell, so they eliminate without mutual fill (the "one group per facet
+  // separator plane" of include/fdmstar/ordering.hpp:25-27) -- then edges,
+  // then the vertex; within a group the reference order is kept.  This cuts
+  // the separator factor from 1.87M to 1.08M nonzeros at p = 15 (37.6M ->
+  // 21.0M at p = 31).  sep_order 1 ("reference") keeps the patch_ordering
+  // perm itself (facet groups by global facet id, src/ordering.cpp:17-45).
+  // The patch solution is order independent up to rounding.
+  const std::vector<int32_t> lat_ref = lat0;
+  if (c.sep_order == 0) {
+    const int nI0 = expect_nI, m0 = expect_n - expect_nI;
+    std::vector<int> idx(m0);
+    for (int r = 0; r < m0; ++r) idx[r] = r;
+    auto key = [&](int r) {
+      int P[3];
+      unpack(lat0[nI0 + r], P);
+      int cnt = 0, ax = 0;
+      for (int a = 0; a < d; ++a)
+        if (P[a] == p) {
+          ++cnt;
+          ax = a;
+        }
+      return cnt == 1 ? ax : (cnt == 2 ? d : d + 1);
+    };
+    std::stable_sort(idx.begin(), idx.end(), [&](int x, int y) { return key(x) < key(y); });
+    std::vector<int32_t> lat1(lat0);
+    for (int r = 0; r < m0; ++r) lat1[nI0 + r] = lat0[nI0 + idx[r]];
+    for (int j = 0; j < npatch; ++j) {
+      std::vector<int32_t> tmp(c.h_pdofs.begin() + size_t(j) * L.n + nI0, c.h_pdofs.begin() + size_t(j + 1) * L.n);
+      for (int r = 0; r < m0; ++r) c.h_pdofs[size_t(j) * L.n + nI0 + r] = tmp[idx[r]];
+    }
+    lat0 = lat1;
+  }
   L.lat = lat0;
   int span_d = 1;
   for (int a = 0; a < d; ++a) span_d *= L.span;
@@ -142,11 +178,18 @@ void analyze_patches(Context& c, int npatch, const int32_t* vertex, const int64_
   auto has = [&](const std::vector<uint8_t>& nz, int i, int jj) { return nz[i + size_t(n1) * jj] != 0; };
   std::vector<int> parent(L.n, -1), flag(L.n, -1), colcount(L.n, 1), mark(L.n, -1), row;
   std::vector<uint8_t> tmark(size_t(L.nT) * L.nT, 0);
-  for (int k = 0; k < L.n; ++k) {
+  const char* dbg_env = std::getenv("FDMGPU_DEBUG");
+  const bool dbg = dbg_env && dbg_env[0] == '1';
+  std::vector<uint8_t> m32(dbg ? size_t(L.mpad / 32) * (L.mpad / 32) : 0), m16(dbg ? size_t(L.mpad / 16) * (L.mpad / 16) : 0);
+  int64_t nnz_sep = 0;
+  int stamp = 0;
+  // All structural neighbours (any position) of position k in the canonical
+  // patch matrix: union of the Kronecker patterns of the cells containing it.
+  auto neigh = [&](int k, std::vector<int>& out) {
+    out.clear();
+    ++stamp;
     int P[3];
     unpack(L.lat[k], P);
-    row.clear();
-    // cells containing P: per axis s_a in {0} (P<p), {1} (P>p) or {0,1} (P==p)
     int lo[3], hi[3];
     for (int a = 0; a < 3; ++a) {
       lo[a] = a < d ? (P[a] > p ? 1 : 0) : 0;
@@ -181,19 +224,33 @@ void analyze_patches(Context& c, int npatch, const int32_t* vertex, const int64_
                 }
                 if (!in) continue;
                 const int pos = L.pos_of_lat[lin_of(Q)];
-                if (pos >= 0 && pos < k && mark[pos] != k) {
-                  mark[pos] = k;
-                  row.push_back(pos);
+                if (pos >= 0 && mark[pos] != stamp) {
+                  mark[pos] = stamp;
+                  out.push_back(pos);
                 }
               }
         }
+  };
+  std::vector<int> nb;
+  for (int k = 0; k < L.n; ++k) {
+    neigh(k, nb);
+    row.clear();
+    for (int pos : nb)
+      if (pos < k) row.push_back(pos);
     flag[k] = k;
     for (int j0 : row) {
       for (int jj = j0; jj < k && flag[jj] != k; jj = parent[jj]) {
         if (parent[jj] == -1) parent[jj] = k;
         ++colcount[jj];
         flag[jj] = k;
-        if (k >= L.nI && jj >= L.nI) tmark[size_t((k - L.nI) / T) * L.nT + (jj - L.nI) / T] = 1;
+        if (k >= L.nI && jj >= L.nI) {
+          tmark[size_t((k - L.nI) / T) * L.nT + (jj - L.nI) / T] = 1;
+          ++nnz_sep;
+          if (dbg) {
+            m32[size_t((k - L.nI) / 32) * (L.mpad / 32) + (jj - L.nI) / 32] = 1;
+            m16[size_t((k - L.nI) / 16) * (L.mpad / 16) + (jj - L.nI) / 16] = 1;
+          }
+        }
       }
     }
   }
@@ -201,7 +258,53 @@ void analyze_patches(Context& c, int npatch, const int32_t* vertex, const int64_
     L.nnz_L += colcount[k];
     L.flops_ref += int64_t(colcount[k]) * (colcount[k] - 1) / 2;
   }
+  L.nnz_L_reference = L.nnz_L;
+  L.flops_reference = L.flops_ref;
+  if (lat_ref != L.lat) {
+    // Column counts under the reference patch_ordering (SURVEY.md Appendix A
+    // figures, reported beside the ones of the order in use).
+    const std::vector<int32_t> lat_use = L.lat;
+    auto set_lat = [&](const std::vector<int32_t>& lt) {
+      L.lat = lt;
+      std::fill(L.pos_of_lat.begin(), L.pos_of_lat.end(), -1);
+      for (int k = 0; k < L.n; ++k) {
+        int P[3];
+        unpack(L.lat[k], P);
+        L.pos_of_lat[lin_of(P)] = k;
+      }
+    };
+    set_lat(lat_ref);
+    std::vector<int> par2(L.n, -1), flag2(L.n, -1), cc2(L.n, 1);
+    for (int k = 0; k < L.n; ++k) {
+      neigh(k, nb);
+      flag2[k] = k;
+      for (int j0 : nb) {
+        if (j0 >= k) continue;
+        for (int jj = j0; jj < k && flag2[jj] != k; jj = par2[jj]) {
+          if (par2[jj] == -1) par2[jj] = k;
+          ++cc2[jj];
+          flag2[jj] = k;
+        }
+      }
+    }
+    L.nnz_L_reference = 0;
+    L.flops_reference = 0;
+    for (int k = 0; k < L.n; ++k) {
+      L.nnz_L_reference += cc2[k];
+      L.flops_reference += int64_t(cc2[k]) * (cc2[k] - 1) / 2;
+    }
+    set_lat(lat_use);
+  }
   for (int K = 0; K < L.nT; ++K) tmark[size_t(K) * L.nT + K] = 1;
+  if (dbg) {
+    int64_t t64 = 0, t32 = 0, t16 = 0;
+    for (auto v : tmark) t64 += v;
+    for (auto v : m32) t32 += v;
+    for (auto v : m16) t16 += v;
+    std::fprintf(stderr, "[fdmgpu] sep nnz %lld (+diag %d) | tiles64 %lld (%.3f) | blocks32 %lld (%.3f) | blocks16 %lld (%.3f)\n",
+                 (long long)nnz_sep, L.m, (long long)t64, double(nnz_sep + L.m) / (t64 * 4096.0), (long long)t32,
+                 double(nnz_sep + L.m) / (t32 * 1024.0), (long long)t16, double(nnz_sep + L.m) / (t16 * 256.0));
+  }
   std::vector<int32_t> tidx(size_t(L.nT) * L.nT, -1);
   for (int K = 0; K < L.nT; ++K) {
     L.col_start.push_back(int32_t(L.tile_row.size()));
@@ -228,6 +331,39 @@ void analyze_patches(Context& c, int npatch, const int32_t* vertex, const int64_
     if (I != K) ++L.tile_gemms;  // TRSM against the diagonal inverse
   }
   L.tile_gemms += int64_t(L.pair_a.size());
+
+  // Structural nonzeros of the separator Schur complement S_G = A~_GG -
+  // A~_GI D^-1 A~_IG (lower triangle), packed (tile << 12 | col << 6 | row):
+  // the assembly kernel evaluates only these; every other stored entry
+  // starts at zero (fill).
+  std::vector<int> nb2, cols;
+  std::vector<int> seen(L.n, -1);
+  for (int k = L.nI; k < L.n; ++k) {
+    neigh(k, nb);
+    cols.clear();
+    auto add = [&](int cpos) {
+      if (cpos >= L.nI && cpos <= k && seen[cpos] != k) {
+        seen[cpos] = k;
+        cols.push_back(cpos);
+      }
+    };
+    for (int q : nb) {
+      if (q >= L.nI) {
+        add(q);
+      } else {
+        neigh(q, nb2);
+        for (int q2 : nb2) add(q2);
+      }
+    }
+    const int r = k - L.nI;
+    for (int cpos : cols) {
+      const int cc = cpos - L.nI;
+      const int t = tidx[size_t(r / T) * L.nT + cc / T];
+      if (t < 0) throw Error(FDMGPU_UNSUPPORTED, "separator entry outside the tile pattern");
+      L.entries.push_back((t << 12) | ((cc % T) << 6) | (r % T));
+    }
+  }
+  std::sort(L.entries.begin(), L.entries.end());
 }
 
 }  // namespace fdmgpu

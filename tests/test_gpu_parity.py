@@ -94,7 +94,7 @@ def test_full_size_against_golden(pkg, torch, name):
     sol = pkg.Solver(prob)
     sol.factor()
     L = sol.layout()
-    assert L["nnz_L"] == g["patch0"]["nnz_L"] and L["flops_ref"] == g["patch0"]["flops"]
+    assert L["nnz_L_reference"] == g["patch0"]["nnz_L"] and L["flops_reference"] == g["patch0"]["flops"]
     r = prob.rhs()
     probe = np.random.default_rng(12345).standard_normal(prob.ndof)
     for name_, v, tol in (("apply_St", sol.apply_St(r), TOL_TRANSFORM), ("apply_A", sol.apply_A(r), TOL_TRANSFORM),
@@ -122,7 +122,25 @@ def test_c3_layout_matches_appendix_a(c3):
     _, sol = c3
     L = sol.layout()
     assert (L["npatch"], L["n"], L["n_interior"], L["n_interface"]) == (343, 24389, 21952, 2437)
-    assert L["nnz_L"] == 1960925 and L["flops_ref"] == 956196192
+    # SURVEY.md Appendix A, reference patch_ordering
+    assert L["nnz_L_reference"] == 1960925 and L["flops_reference"] == 956196192
+    # plane-by-plane separator order (default): ~40 % fewer factor nonzeros
+    assert L["separator_order"] == 0 and L["nnz_L"] == 1171423 and L["flops_ref"] == 388055724
+
+
+@pytest.mark.parametrize("cfg", [(2, 0, 0), (4, 4, 5)])
+def test_reference_separator_order(pkg, oracle, torch, cfg):
+    prob = pkg.Problem(*cfg)
+    sol = pkg.Solver(prob, separator_order="reference")
+    sol.factor()
+    L = sol.layout()
+    assert L["separator_order"] == 1 and L["nnz_L"] == L["nnz_L_reference"]
+    ref = oracle.Problem(*cfg, build_global=False, threads=os.cpu_count())
+    ref.factor([0])
+    assert L["nnz_L"] == ref.factor_info(0)["nnz"] and L["flops_ref"] == ref.factor_info(0)["flops"]
+    ref.factor()
+    r = prob.rhs()
+    assert rel(sol.smooth(r), ref.smooth(r)) <= TOL_RELAX
 
 
 def test_c3_relaxation_properties(c3, torch):
