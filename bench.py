@@ -292,14 +292,14 @@ def run_ours(args):
         "config": {"workload": WORKLOADS[args.config], "config": args.config, "ndof": prob.ndof,
                    "nfree": prob.nfree, "patches": L["npatch"], "patch_dofs": L["n"],
                    "separator_dofs": L["n_interface"], "parallelism": "replicas" if world > 1 else "single",
-                   "l2": f"inputs larger than L2: {L['factor_bytes'] / 1e9:.2f} GB patch factor streamed per step"},
+                   "l2": f"inputs larger than L2: 2 x {L['stream_bytes'] / 1e9:.2f} GB packed patch factor streamed per step"},
         "roofline": {"kernel": "k_patch_solve", "bound": "hbm", "achieved": achieved, "peak": hbm_peak,
                      "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": None,
                      "peak_source": peak_src, "kernel_ms": kern_ms, "algorithmic_bytes": kern_bytes,
                      "share_of_step": solve_ms / ms if ms > 0 else None,
                      "bytes_def": "16 B x separator nnz(L_j) of the factor in use (fwd + bwd; plane-by-plane "
                                   "separator order) + separator RHS gather / solution write, per launch, all patches",
-                     "stored_bytes_per_pass": L["factor_bytes"]},
+                     "stored_bytes_per_pass": L["stream_bytes"]},
         "relaxation_roofline": {"bytes": relax_bytes, "achieved_GBps": relax_bytes / (ms_per_step * 1e-3) / 1e9,
                                 "frac": relax_bytes / (ms_per_step * 1e-3) / 1e9 / hbm_peak,
                                 "bytes_def": "SURVEY.md 8(d): 8*(2*NNZ + 2*sum n_j + 4*ndof), NNZ of the reference "

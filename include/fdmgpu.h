@@ -67,6 +67,7 @@ typedef struct {
   int64_t flops_reference;   /* CholFactor::flops under the reference ordering    */
   int32_t separator_order;   /* 0 plane, 1 reference                              */
   int32_t pad2_;
+  int64_t stream_bytes;      /* packed factor bytes streamed per sweep, all patches */
 } fdmgpu_layout;
 
 /* Operator ids for fdmgpu_apply. */

@@ -463,6 +463,8 @@ fdmgpu_status fdmgpu_set_patches(fdmgpu_handle h, int32_t npatch, const int32_t*
     c.col_start.upload(L.col_start, c.stream);
     c.pair_ptr.upload(L.pair_ptr, c.stream);
     c.entries.upload(L.entries, c.stream);
+    c.tile_mask.upload(L.tile_mask, c.stream);
+    c.tile_poff.upload(L.tile_poff, c.stream);
     if (L.pair_a.empty()) {
       c.pair_a.alloc(1);
       c.pair_b.alloc(1);
@@ -523,6 +525,7 @@ fdmgpu_status fdmgpu_factor(fdmgpu_handle h) {
       fdmgpu::launch_patch_update(c, K);
       fdmgpu::launch_patch_trsm(c, K);
     }
+    fdmgpu::launch_patch_pack(c);  // dense tiles -> packed 16x16 sub-blocks for the solve stream
     unsigned long long e = 0;
     FDM_CUDA(cudaMemcpyAsync(&e, c.d_err.p, sizeof(e), cudaMemcpyDeviceToHost, c.stream));
     FDM_CUDA(cudaStreamSynchronize(c.stream));
@@ -552,6 +555,7 @@ fdmgpu_status fdmgpu_get_layout(fdmgpu_handle h, fdmgpu_layout* out) {
     L.nnz_L_reference = c.L.nnz_L_reference;
     L.flops_reference = c.L.flops_reference;
     L.separator_order = c.sep_order;
+    L.stream_bytes = int64_t(c.L.tile_poff.back()) * 256 * 8 * c.npatch;
     *out = L;
   });
 }

@@ -67,6 +67,7 @@ struct PatchLayout {
   std::vector<int32_t> tile_row, tile_col, col_start;  // tile pattern, column-major order
   std::vector<int32_t> pair_ptr, pair_a, pair_b;       // left-looking update pairs per tile
   std::vector<int32_t> entries;      // structural nonzeros of S_G: tile << 12 | col << 6 | row
+  std::vector<int32_t> tile_mask, tile_poff;  // packed 16x16 sub-blocks per tile (solve stream)
   int64_t nnz_L = 0, flops_ref = 0, tile_gemms = 0;          // order in use
   int64_t nnz_L_reference = 0, flops_reference = 0;         // reference patch_ordering
 };
@@ -106,7 +107,7 @@ struct Context {
   int npatch = 0;
   PatchLayout L;
   DevArray<int32_t> pdofs, lat, pos_of_lat, pcells, pg_ptr, pg_idx;
-  DevArray<int32_t> tile_row, tile_col, col_start, pair_ptr, pair_a, pair_b, entries;
+  DevArray<int32_t> tile_row, tile_col, col_start, pair_ptr, pair_a, pair_b, entries, tile_mask, tile_poff;
   DevArray<double> corr, tiles, nK;
   std::vector<int32_t> h_pdofs, h_pcells;
   bool have_patches = false, factored = false;
@@ -170,6 +171,7 @@ void launch_cells_quadrature(Context& c, const double* x);           // writes c
 void launch_patch_assemble(Context& c);
 void launch_patch_update(Context& c, int K);
 void launch_patch_trsm(Context& c, int K);
+void launch_patch_pack(Context& c);
 void launch_patch_solve(Context& c, const double* r_modal);          // writes c.corr
 void launch_patch_gather(Context& c, double* z_modal);
 void launch_axpby(Context& c, int64_t n, double a, const double* x, double b, const double* y, double* out);

@@ -400,16 +400,98 @@ __global__ void __launch_bounds__(kUpdThreads) k_patch_trsm(PatchArgs a, int K, 
 // ---- K3: patch relaxation solve -------------------------------------------------
 constexpr int kSolveConsumers = 8;                         // consumer warps
 constexpr int kSolveThreads = 32 * (kSolveConsumers + 1);  // + 1 TMA producer warp
+constexpr int SB = 256;                                    // doubles per packed 16x16 sub-block
 
-// One CTA per patch.  A producer warp streams the patch's separator factor
-// (forward order, then backward by column) through a `stages`-deep ring of
-// 32 KB shared-memory slots with cp.async.bulk + mbarrier; eight consumer
-// warps run the separator RHS, the tile GEMVs and the interior
-// back-substitution.  Output: the patch correction c_j in elimination order.
+// Packed solve stream.  After factorisation every 64x64 tile is compacted to
+// its structurally nonzero 16x16 sub-blocks (mask bit bi*4 + bj, packed in bit
+// order; element (r, c) of a sub-block at c*16 + (r ^ c), conflict free for
+// both row and column sweeps).  Exact: the dropped sub-blocks are structural
+// zeros of the factor, which the factorisation produces as exact 0.0.
+__global__ void k_patch_pack(int ntiles, const int32_t* __restrict__ mask, const int32_t* __restrict__ poff,
+                             double* __restrict__ tiles) {
+  extern __shared__ __align__(16) double tile[];
+  double* base = tiles + size_t(blockIdx.x) * ntiles * TT;
+  for (int t = 0; t < ntiles; ++t) {
+    const double2* src = reinterpret_cast<const double2*>(base + size_t(t) * TT);
+    for (int e = threadIdx.x; e < TT / 2; e += blockDim.x) reinterpret_cast<double2*>(tile)[e] = src[e];
+    __syncthreads();
+    const int m = mask[t];
+    const int cnt = __popc(m);
+    double* dst = base + size_t(poff[t]) * SB;
+    for (int d = threadIdx.x; d < cnt * SB; d += blockDim.x) {
+      const int q = d / SB, w = d % SB;
+      int bit = -1, seen = -1;
+      for (int b2 = 0; b2 < 16 && seen < q; ++b2)
+        if ((m >> b2) & 1) {
+          ++seen;
+          bit = b2;
+        }
+      const int bi = bit >> 2, bj = bit & 3, cc = w >> 4, rr = (w & 15) ^ cc;
+      dst[d] = tile[tsw(16 * bi + rr, 16 * bj + cc)];
+    }
+    __syncthreads();
+  }
+}
+
+// out[bi] (rows 16 bi + (lane & 15)) = sum over the tile's sub-blocks of
+// block-row bi of L_sub * x[16 bj ..]; half-warps split the 16 columns.
+__device__ __forceinline__ void packed_fwd(const double* __restrict__ slot, int mask, const double* __restrict__ x,
+                                           int lane, double out[4]) {
+  const int rr = lane & 15, h = lane >> 4;
+  int q = 0;
+#pragma unroll
+  for (int bi = 0; bi < 4; ++bi) {
+    double acc = 0.0;
+#pragma unroll
+    for (int bj = 0; bj < 4; ++bj) {
+      if ((mask >> (bi * 4 + bj)) & 1) {
+        const double* B = slot + q * SB;
+        const double* xv = x + 16 * bj + 8 * h;
+        ++q;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int cc = 8 * h + k;
+          acc = fma(B[cc * 16 + (rr ^ cc)], xv[k], acc);
+        }
+      }
+    }
+    out[bi] = acc + __shfl_xor_sync(0xffffffffu, acc, 16);
+  }
+}
+
+// out[bj] (columns 16 bj + (lane & 15)) = sum over block-column bj of L_sub^T x[16 bi ..].
+__device__ __forceinline__ void packed_bwd(const double* __restrict__ slot, int mask, const double* __restrict__ x,
+                                           int lane, double out[4]) {
+  const int cc = lane & 15, h = lane >> 4;
+#pragma unroll
+  for (int bj = 0; bj < 4; ++bj) {
+    double acc = 0.0;
+#pragma unroll
+    for (int bi = 0; bi < 4; ++bi) {
+      const int bit = bi * 4 + bj;
+      if ((mask >> bit) & 1) {
+        const double* B = slot + __popc(mask & ((1 << bit) - 1)) * SB;
+        const double* xv = x + 16 * bi + 8 * h;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int rr = 8 * h + k;
+          acc = fma(B[cc * 16 + (rr ^ cc)], xv[k], acc);
+        }
+      }
+    }
+    out[bj] = acc + __shfl_xor_sync(0xffffffffu, acc, 16);
+  }
+}
+
+// One CTA per patch.  A producer warp streams the patch's packed separator
+// factor (forward order, then backward by column) through a `stages`-deep
+// ring of 32 KB shared-memory slots with cp.async.bulk + mbarrier; eight
+// consumer warps run the sub-block GEMVs.  Output: the separator solution.
 __global__ void __launch_bounds__(kSolveThreads)
     k_patch_solve(PatchArgs a, int stages, const double* __restrict__ rt, double* __restrict__ corr,
                   const double* __restrict__ tiles, const int32_t* __restrict__ pdofs,
-                  const int32_t* __restrict__ col_start, const int32_t* __restrict__ tile_row) {
+                  const int32_t* __restrict__ col_start, const int32_t* __restrict__ tile_row,
+                  const int32_t* __restrict__ tile_mask, const int32_t* __restrict__ tile_poff) {
   extern __shared__ __align__(128) double sm[];
   double* ring = sm;                          // stages x TT
   double* y = ring + size_t(stages) * TT;     // mpad
@@ -434,8 +516,9 @@ __global__ void __launch_bounds__(kSolveThreads)
       auto issue = [&](int t) {
         const int s = q % stages;
         if (q >= stages) mbar_wait(&empty[s], ((q / stages) - 1) & 1);
-        mbar_arrive_expect_tx(&full[s], TT * sizeof(double));
-        bulk_g2s(ring + size_t(s) * TT, tb + size_t(t) * TT, TT * sizeof(double), &full[s]);
+        const uint32_t bytes = uint32_t(__popc(tile_mask[t])) * SB * sizeof(double);
+        mbar_arrive_expect_tx(&full[s], bytes);
+        bulk_g2s(ring + size_t(s) * TT, tb + size_t(tile_poff[t]) * SB, bytes, &full[s]);
         ++q;
       };
       for (int t = 0; t < a.ntiles; ++t) issue(t);
@@ -449,6 +532,7 @@ __global__ void __launch_bounds__(kSolveThreads)
   }
 
   constexpr int NC = 32 * kSolveConsumers;
+  const int rl = lane & 15, h = lane >> 4;
   // ---- phase A: gather the Schur-reduced separator RHS (the interior elimination
   // was folded into the S^T cell kernel: bhat is patch independent) ----------------
   const int32_t* pdI = pdofs + size_t(j) * a.m;
@@ -460,24 +544,20 @@ __global__ void __launch_bounds__(kSolveThreads)
   // parity can never be two phases ahead of its waiter.
   // ---- phase B: forward substitution over tile columns (y <- L_G^{-1} y) ----------------
   int q = 0;  // stream position, mirrors the producer
+  double o[4];
   for (int K = 0; K < a.nT; ++K) {
     const int t0 = col_start[K], cnt = col_start[K + 1] - t0;
     double* yK = y + K * T;
     if (warp == q % stages) {
       const int s = q % stages;
       mbar_wait(&full[s], (q / stages) & 1);
-      const double* Li = ring + size_t(s) * TT;  // L_KK^{-1} (lower, zero above)
-      double v0 = 0.0, v1 = 0.0;
-#pragma unroll 8
-      for (int c = 0; c < T; ++c) {
-        const double yc = yK[c];
-        v0 = fma(Li[tsw(lane, c)], yc, v0);
-        v1 = fma(Li[tsw(lane + 32, c)], yc, v1);
-      }
+      packed_fwd(ring + size_t(s) * TT, tile_mask[t0], yK, lane, o);  // L_KK^{-1} y_K
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
-      yK[lane] = v0;
-      yK[lane + 32] = v1;
+      if (h == 0) {
+#pragma unroll
+        for (int bi = 0; bi < 4; ++bi) yK[16 * bi + rl] = o[bi];
+      }
     }
     ++q;
     named_sync(1, NC);
@@ -485,19 +565,14 @@ __global__ void __launch_bounds__(kSolveThreads)
       const int s = q % stages;
       if (s != warp) continue;
       mbar_wait(&full[s], (q / stages) & 1);
-      const double* Lt = ring + size_t(s) * TT;
-      double v0 = 0.0, v1 = 0.0;
-#pragma unroll 8
-      for (int c = 0; c < T; ++c) {
-        const double yc = yK[c];
-        v0 = fma(Lt[tsw(lane, c)], yc, v0);
-        v1 = fma(Lt[tsw(lane + 32, c)], yc, v1);
-      }
+      packed_fwd(ring + size_t(s) * TT, tile_mask[t0 + i], yK, lane, o);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
-      double* yI = y + tile_row[t0 + i] * T;
-      yI[lane] -= v0;
-      yI[lane + 32] -= v1;
+      if (h == 0) {
+        double* yI = y + tile_row[t0 + i] * T;
+#pragma unroll
+        for (int bi = 0; bi < 4; ++bi) yI[16 * bi + rl] -= o[bi];
+      }
     }
     named_sync(1, NC);
   }
@@ -505,24 +580,21 @@ __global__ void __launch_bounds__(kSolveThreads)
   // ---- phase C: backward substitution (x <- L_G^{-T} y), columns descending ---------------
   for (int K = a.nT - 1; K >= 0; --K) {
     const int t0 = col_start[K], cnt = col_start[K + 1] - t0;
-    double a0 = 0.0, a1 = 0.0;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
     for (int i = 1; i < cnt; ++i, ++q) {
       const int s = q % stages;
       if (s != warp) continue;
       mbar_wait(&full[s], (q / stages) & 1);
-      const double* Lt = ring + size_t(s) * TT;
-      const double* xI = y + tile_row[t0 + i] * T;
-#pragma unroll 8
-      for (int r = 0; r < T; ++r) {
-        const double xr = xI[r];
-        a0 = fma(Lt[tsw(r, lane)], xr, a0);
-        a1 = fma(Lt[tsw(r, lane + 32)], xr, a1);
-      }
+      packed_bwd(ring + size_t(s) * TT, tile_mask[t0 + i], y + tile_row[t0 + i] * T, lane, o);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
+#pragma unroll
+      for (int bj = 0; bj < 4; ++bj) acc[bj] += o[bj];
     }
-    part[warp * T + lane] = a0;
-    part[warp * T + lane + 32] = a1;
+    if (h == 0) {
+#pragma unroll
+      for (int bj = 0; bj < 4; ++bj) part[warp * T + 16 * bj + rl] = acc[bj];
+    }
     named_sync(1, NC);
     if (warp == q % stages) {
       double* yK = y + K * T;
@@ -536,18 +608,13 @@ __global__ void __launch_bounds__(kSolveThreads)
       __syncwarp();
       const int s = q % stages;
       mbar_wait(&full[s], (q / stages) & 1);
-      const double* Li = ring + size_t(s) * TT;  // x_K = L_KK^{-T} y_K
-      double v0 = 0.0, v1 = 0.0;
-#pragma unroll 8
-      for (int r = 0; r < T; ++r) {
-        const double yr = yK[r];
-        v0 = fma(Li[tsw(r, lane)], yr, v0);
-        v1 = fma(Li[tsw(r, lane + 32)], yr, v1);
-      }
+      packed_bwd(ring + size_t(s) * TT, tile_mask[t0], yK, lane, o);  // x_K = L_KK^{-T} y_K
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
-      yK[lane] = v0;
-      yK[lane + 32] = v1;
+      if (h == 0) {
+#pragma unroll
+        for (int bj = 0; bj < 4; ++bj) yK[16 * bj + rl] = o[bj];
+      }
     }
     ++q;
     named_sync(1, NC);
@@ -636,7 +703,14 @@ void launch_patch_solve(Context& c, const double* r_modal) {
   }
   KernelTimer timer(c, 0);
   k_patch_solve<<<c.npatch, kSolveThreads, smem, c.stream>>>(a, stages, r_modal, c.corr.p, c.tiles.p, c.pdofs.p,
-                                                              c.col_start.p, c.tile_row.p);
+                                                              c.col_start.p, c.tile_row.p, c.tile_mask.p,
+                                                              c.tile_poff.p);
+  FDM_LAUNCH_CHECK(c);
+}
+
+void launch_patch_pack(Context& c) {
+  KernelTimer timer(c, 1);
+  k_patch_pack<<<c.npatch, 256, TT * sizeof(double), c.stream>>>(c.L.ntiles, c.tile_mask.p, c.tile_poff.p, c.tiles.p);
   FDM_LAUNCH_CHECK(c);
 }
 

@@ -180,7 +180,7 @@ void analyze_patches(Context& c, int npatch, const int32_t* vertex, const int64_
   std::vector<uint8_t> tmark(size_t(L.nT) * L.nT, 0);
   const char* dbg_env = std::getenv("FDMGPU_DEBUG");
   const bool dbg = dbg_env && dbg_env[0] == '1';
-  std::vector<uint8_t> m32(dbg ? size_t(L.mpad / 32) * (L.mpad / 32) : 0), m16(dbg ? size_t(L.mpad / 16) * (L.mpad / 16) : 0);
+  std::vector<uint8_t> m32(dbg ? size_t(L.mpad / 32) * (L.mpad / 32) : 0), m16(size_t(L.mpad / 16) * (L.mpad / 16), 0);
   int64_t nnz_sep = 0;
   int stamp = 0;
   // All structural neighbours (any position) of position k in the canonical
@@ -246,10 +246,8 @@ void analyze_patches(Context& c, int npatch, const int32_t* vertex, const int64_
         if (k >= L.nI && jj >= L.nI) {
           tmark[size_t((k - L.nI) / T) * L.nT + (jj - L.nI) / T] = 1;
           ++nnz_sep;
-          if (dbg) {
-            m32[size_t((k - L.nI) / 32) * (L.mpad / 32) + (jj - L.nI) / 32] = 1;
-            m16[size_t((k - L.nI) / 16) * (L.mpad / 16) + (jj - L.nI) / 16] = 1;
-          }
+          m16[size_t((k - L.nI) / 16) * (L.mpad / 16) + (jj - L.nI) / 16] = 1;
+          if (dbg) m32[size_t((k - L.nI) / 32) * (L.mpad / 32) + (jj - L.nI) / 32] = 1;
         }
       }
     }
@@ -317,6 +315,23 @@ void analyze_patches(Context& c, int npatch, const int32_t* vertex, const int64_
   }
   L.col_start.push_back(int32_t(L.tile_row.size()));
   L.ntiles = int(L.tile_row.size());
+  // 16x16 sub-block masks (bit bi*4 + bj) for the packed solve stream:
+  // off-diagonal tiles keep the sub-blocks the symbolic factor touches,
+  // diagonal tiles (they hold L_KK^{-1}) keep their whole lower triangle.
+  const int nb16 = L.mpad / 16;
+  L.tile_mask.assign(L.ntiles, 0);
+  L.tile_poff.assign(L.ntiles + 1, 0);
+  for (int t = 0; t < L.ntiles; ++t) {
+    const int I = L.tile_row[t], K = L.tile_col[t];
+    int mask = 0;
+    for (int bi = 0; bi < 4; ++bi)
+      for (int bj = 0; bj < 4; ++bj) {
+        const bool on = I == K ? bi >= bj : m16[size_t(4 * I + bi) * nb16 + (4 * K + bj)] != 0;
+        if (on) mask |= 1 << (bi * 4 + bj);
+      }
+    L.tile_mask[t] = mask;
+    L.tile_poff[t + 1] = L.tile_poff[t] + __builtin_popcount(unsigned(mask));
+  }
   L.pair_ptr.push_back(0);
   for (int t = 0; t < L.ntiles; ++t) {
     const int I = L.tile_row[t], K = L.tile_col[t];
