@@ -232,21 +232,36 @@ struct TileAcc {
   }
 };
 
-__device__ __forceinline__ void tile_gemm_abt(const double* __restrict__ A, const double* __restrict__ B, TileAcc& acc) {
+__device__ __forceinline__ void tile_gemm_abt(const double* __restrict__ A, const double* __restrict__ B, TileAcc& acc,
+                                              int maskA = 0xffff, int maskB = 0xffff) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int r0 = 32 * (w >> 2) + (lane >> 2), c0 = 16 * (w & 3) + (lane >> 2), kl = lane & 3;
-#pragma unroll 4
-  for (int k0 = 0; k0 < T; k0 += 4) {
-    const int k = k0 + kl;
-    double av[4], bv[2];
+  const int wr = w >> 2, wc = w & 3;
+  const int r0 = 32 * wr + (lane >> 2), c0 = 16 * wc + (lane >> 2), kl = lane & 3;
+  // 16-wide k panels q where this warp's A rows (sub-block rows 2wr, 2wr+1)
+  // and B rows (sub-block row wc) hold structural nonzeros (warp uniform).
+  int qmask = 0;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) av[i] = A[tsw(r0 + 8 * i, k)];
+  for (int q = 0; q < 4; ++q) {
+    const bool a_on = ((maskA >> ((2 * wr) * 4 + q)) | (maskA >> ((2 * wr + 1) * 4 + q))) & 1;
+    const bool b_on = (maskB >> (wc * 4 + q)) & 1;
+    if (a_on && b_on) qmask |= 1 << q;
+  }
+#pragma unroll 1
+  for (int q = 0; q < 4; ++q) {
+    if (!((qmask >> q) & 1)) continue;
 #pragma unroll
-    for (int jj = 0; jj < 2; ++jj) bv[jj] = B[tsw(c0 + 8 * jj, k)];
+    for (int k0 = 16 * q; k0 < 16 * q + 16; k0 += 4) {
+      const int k = k0 + kl;
+      double av[4], bv[2];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < 4; ++i) av[i] = A[tsw(r0 + 8 * i, k)];
 #pragma unroll
-      for (int jj = 0; jj < 2; ++jj) dmma884(acc.v[i][jj][0], acc.v[i][jj][1], av[i], bv[jj]);
+      for (int jj = 0; jj < 2; ++jj) bv[jj] = B[tsw(c0 + 8 * jj, k)];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj) dmma884(acc.v[i][jj][0], acc.v[i][jj][1], av[i], bv[jj]);
+    }
   }
 }
 
@@ -303,6 +318,7 @@ __global__ void __launch_bounds__(kUpdThreads) k_patch_update(PatchArgs a, int K
                                                                 const int32_t* __restrict__ pair_ptr,
                                                                 const int32_t* __restrict__ pair_a,
                                                                 const int32_t* __restrict__ pair_b,
+                                                                const int32_t* __restrict__ tile_mask,
                                                                 double* __restrict__ tiles) {
   extern __shared__ __align__(128) double sm[];
   double* buf = sm;                                   // [2 stages][A,B][TT]
@@ -328,7 +344,7 @@ __global__ void __launch_bounds__(kUpdThreads) k_patch_update(PatchArgs a, int K
   for (int i = 0; i < np; ++i) {
     const int s = i & 1;
     mbar_wait(&full[s], (i >> 1) & 1);
-    tile_gemm_abt(buf + (2 * s) * TT, buf + (2 * s + 1) * TT, acc);
+    tile_gemm_abt(buf + (2 * s) * TT, buf + (2 * s + 1) * TT, acc, tile_mask[pair_a[p0 + i]], tile_mask[pair_b[p0 + i]]);
     __syncthreads();
     if (tid == 0 && i + 2 < np) {
       mbar_arrive_expect_tx(&full[s], 2 * TT * sizeof(double));
@@ -365,6 +381,7 @@ __global__ void __launch_bounds__(kUpdThreads) k_patch_update(PatchArgs a, int K
 
 // L(I,K) = C(I,K) L_KK^{-T} for the off-diagonal tiles of column K.
 __global__ void __launch_bounds__(kUpdThreads) k_patch_trsm(PatchArgs a, int K, const int32_t* __restrict__ col_start,
+                                                              const int32_t* __restrict__ tile_mask,
                                                               double* __restrict__ tiles) {
   extern __shared__ __align__(128) double sm[];
   double* Cs = sm;
@@ -386,7 +403,7 @@ __global__ void __launch_bounds__(kUpdThreads) k_patch_trsm(PatchArgs a, int K, 
   }
   mbar_wait(&full[0], 0);
   TileAcc acc = {};
-  tile_gemm_abt(Cs, Ls, acc);
+  tile_gemm_abt(Cs, Ls, acc, tile_mask[t], tile_mask[t0]);
   double* out = base + size_t(t) * TT;
 #pragma unroll
   for (int i = 0; i < 4; ++i)
@@ -662,7 +679,7 @@ void launch_patch_update(Context& c, int K) {
   dim3 grid(c.L.col_start[K + 1] - c.L.col_start[K], c.npatch);
   KernelTimer timer(c, 1);
   k_patch_update<<<grid, kUpdThreads, smem, c.stream>>>(a, K, c.col_start.p, c.tile_row.p, c.pair_ptr.p,
-                                                         c.pair_a.p, c.pair_b.p, c.tiles.p);
+                                                         c.pair_a.p, c.pair_b.p, c.tile_mask.p, c.tiles.p);
   FDM_LAUNCH_CHECK(c);
 }
 
@@ -678,7 +695,7 @@ void launch_patch_trsm(Context& c, int K) {
   }
   dim3 grid(cnt, c.npatch);
   KernelTimer timer(c, 1);
-  k_patch_trsm<<<grid, kUpdThreads, smem, c.stream>>>(a, K, c.col_start.p, c.tiles.p);
+  k_patch_trsm<<<grid, kUpdThreads, smem, c.stream>>>(a, K, c.col_start.p, c.tile_mask.p, c.tiles.p);
   FDM_LAUNCH_CHECK(c);
 }
 
