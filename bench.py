@@ -118,13 +118,6 @@ class ClockSampler:
                 "source": "nvml" if self._nvml else "nvidia-smi"}
 
 
-def dist_env():
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return rank, world, local
-
-
 def cpu_sample(config, steps, warmup, threads, sample_patches):
     """CPU restatement of the reference on the host cores: S^T, the patch
     solves of `sample_patches` patches (parallel_for over `threads`), S."""
@@ -167,6 +160,8 @@ def cpu_sample(config, steps, warmup, threads, sample_patches):
 
 
 def run_reference(args):
+    from paper_2107_14758_b200.replicas import dist_env
+
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
@@ -189,13 +184,11 @@ def run_ours(args):
     import torch
 
     import paper_2107_14758_b200 as pkg
+    from paper_2107_14758_b200 import replicas
 
-    rank, world, local = dist_env()
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl")
+    rank, world, local = replicas.dist_env()
     torch.cuda.set_device(local)
+    replicas.init("nccl")
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream(dev)
 
@@ -224,8 +217,7 @@ def run_ours(args):
     torch.cuda.synchronize()
 
     # ---- timed region: K relaxation applies, device-resident vectors ----
-    if world > 1:
-        torch.distributed.barrier()
+    replicas.barrier()
     torch.cuda.synchronize()
     launches0 = sol.launch_count()
     sol.kernel_timing(True)
@@ -241,12 +233,9 @@ def run_ours(args):
     solve_ms, solve_n = sol.kernel_time("patch_solve")
     tr_ms, tr_n = sol.kernel_time("transform")
     sol.kernel_timing(False)
-    if world > 1:
-        t = torch.tensor([ms], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = replicas.max_over_ranks(ms, dev)
     ms_per_step = ms / args.steps
-    value = world * prob.nfree / (ms_per_step * 1e-3) / 1e9
+    value = replicas.whole_job_rate(prob.nfree, world, ms_per_step * 1e-3) / 1e9
 
     # ---- e2e through the C ABI with host buffers (H2D + D2H inside) ----
     h_in = torch.from_numpy(prob.rhs()).pin_memory().numpy()
@@ -260,10 +249,7 @@ def run_ours(args):
     ee1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = ee0.elapsed_time(ee1) / args.steps
-    if world > 1:
-        t = torch.tensor([e2e_ms], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+    e2e_ms = replicas.max_over_ranks(e2e_ms, dev)
 
     # ---- PCG solve (for context: iteration count, time) ----
     pcg = None
@@ -326,9 +312,8 @@ def run_ours(args):
         except Exception as e:  # reported, not fatal for the GPU line
             result["cpu_baseline"] = {"value": None, "unit": "GDOF/s", "cores": os.cpu_count(), "kind": "port",
                                       "sample": f"failed: {e}"}
-    if world > 1:
-        torch.distributed.barrier()
-        torch.distributed.destroy_process_group()
+    replicas.barrier()
+    replicas.finalize()
     if rank == 0:
         print(json.dumps(result), flush=True)
     return 0
