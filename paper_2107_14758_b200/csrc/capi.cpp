@@ -465,6 +465,7 @@ fdmgpu_status fdmgpu_set_patches(fdmgpu_handle h, int32_t npatch, const int32_t*
     c.entries.upload(L.entries, c.stream);
     c.tile_mask.upload(L.tile_mask, c.stream);
     c.tile_poff.upload(L.tile_poff, c.stream);
+    c.active.upload(L.active, c.stream);
     if (L.pair_a.empty()) {
       c.pair_a.alloc(1);
       c.pair_b.alloc(1);

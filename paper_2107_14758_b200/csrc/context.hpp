@@ -68,6 +68,7 @@ struct PatchLayout {
   std::vector<int32_t> pair_ptr, pair_a, pair_b;       // left-looking update pairs per tile
   std::vector<int32_t> entries;      // structural nonzeros of S_G: tile << 12 | col << 6 | row
   std::vector<int32_t> tile_mask, tile_poff;  // packed 16x16 sub-blocks per tile (solve stream)
+  std::vector<int32_t> active, active_ptr;    // per column: tiles the update kernel must visit
   int64_t nnz_L = 0, flops_ref = 0, tile_gemms = 0;          // order in use
   int64_t nnz_L_reference = 0, flops_reference = 0;         // reference patch_ordering
 };
@@ -107,7 +108,7 @@ struct Context {
   int npatch = 0;
   PatchLayout L;
   DevArray<int32_t> pdofs, lat, pos_of_lat, pcells, pg_ptr, pg_idx;
-  DevArray<int32_t> tile_row, tile_col, col_start, pair_ptr, pair_a, pair_b, entries, tile_mask, tile_poff;
+  DevArray<int32_t> tile_row, tile_col, col_start, pair_ptr, pair_a, pair_b, entries, tile_mask, tile_poff, active;
   DevArray<double> corr, tiles, nK;
   std::vector<int32_t> h_pdofs, h_pcells;
   bool have_patches = false, factored = false;

@@ -265,43 +265,55 @@ __device__ __forceinline__ void tile_gemm_abt(const double* __restrict__ A, cons
   }
 }
 
-// POTRF + triangular inverse of the 64x64 tile in Dm (column-major, ld 65),
-// writes L^{-1} (lower, diag included) swizzled into `out`.
+// POTRF + triangular inverse of the 64x64 SPD tile in Dm (column-major, ld 65),
+// 256 threads; writes L^{-1} (lower, diag included) swizzled into `out`.
+// Cholesky: right-looking with the unscaled pivot column, one barrier per
+// step (column j-1 is scaled while step j updates the trailing matrix).
+// Inverse: each warp owns 8 columns of L^{-1}; 4 lanes per column split the
+// dot products of the row-by-row forward substitution (warp-synchronous).
 __device__ void diag_factor_invert(double* Dm, double* Wm, double* out, const PatchArgs& a, int K, int patch) {
   constexpr int LD = T + 1;
   const int tid = threadIdx.x;
-  for (int jc = 0; jc < T; ++jc) {
-    if (tid == 0) {
-      double d = Dm[jc * LD + jc];
-      if (!(d > 0.0)) {
-        const int pos = K * T + jc;
-        if (pos < a.m) record_pivot_error(a.err, patch, a.nI + pos);
-        d = 1.0;
-      }
-      Dm[jc * LD + jc] = sqrt(d);
+  const int mc = tid >> 2, mr = tid & 3;  // thread owns column mc, rows mr + 4i
+  for (int j = 0; j <= T; ++j) {
+    if (j > 0 && tid > j - 1 && tid < T) {  // finish column j-1: L(:, j-1) = D(:, j-1) / sqrt(d)
+      const double d = Dm[(j - 1) * LD + (j - 1)];
+      Dm[(j - 1) * LD + tid] *= rsqrt(d > 0.0 ? d : 1.0);
     }
-    __syncthreads();
-    const double piv = Dm[jc * LD + jc];
-    for (int r = jc + 1 + tid; r < T; r += blockDim.x) Dm[jc * LD + r] /= piv;
-    __syncthreads();
-    for (int e = tid; e < TT; e += blockDim.x) {
-      const int r = e % T, cc = e / T;
-      if (cc > jc && r >= cc) Dm[cc * LD + r] -= Dm[jc * LD + r] * Dm[jc * LD + cc];
+    if (j > 0 && tid == 0 && !(Dm[(j - 1) * LD + (j - 1)] > 0.0)) {
+      const int pos = K * T + (j - 1);
+      if (pos < a.m) record_pivot_error(a.err, patch, a.nI + pos);
+    }
+    if (j < T && mc > j) {  // trailing update with the unscaled column j: D(r,c) -= D(r,j) D(c,j) / d
+      double d = Dm[j * LD + j];
+      if (!(d > 0.0)) d = 1.0;
+      const double dcj = Dm[j * LD + mc] / d;
+      for (int r = mc + ((mr - mc) & 3); r < T; r += 4) Dm[mc * LD + r] -= Dm[j * LD + r] * dcj;
     }
     __syncthreads();
   }
-  // Row-sequential inverse: Linv(r, cc) = (delta - sum_{k=cc}^{r-1} L(r,k) Linv(k,cc)) / L(r,r);
-  // 4 threads per column split the k-sum.
-  const int col = tid >> 2, part = tid & 3;
+  // diagonal: L(j,j) = sqrt(d); reciprocals for the inverse
+  double* rdiag = Wm + T * LD;  // T extra doubles after Wm
+  if (tid < T) {
+    const double d = Dm[tid * LD + tid];
+    const double l = sqrt(d > 0.0 ? d : 1.0);
+    Dm[tid * LD + tid] = l;
+    rdiag[tid] = 1.0 / l;
+  }
+  __syncthreads();
+  // Inverse: W(r, c) = (delta_rc - sum_{k=c}^{r-1} L(r,k) W(k,c)) / L(r,r), rows ascending.
+  const int warp = tid >> 5, lane = tid & 31;
+  const int c = 8 * warp + (lane >> 2), part = lane & 3;
   for (int r = 0; r < T; ++r) {
     double s = 0.0;
-    if (col <= r)
-      for (int k = col + part; k < r; k += 4) s = fma(Dm[k * LD + r], Wm[col * LD + k], s);
+    if (r > c)
+      for (int k = c + part; k < r; k += 4) s = fma(Dm[k * LD + r], Wm[c * LD + k], s);
     s += __shfl_xor_sync(0xffffffffu, s, 1);
     s += __shfl_xor_sync(0xffffffffu, s, 2);
-    if (part == 0 && col <= r) Wm[col * LD + r] = ((r == col ? 1.0 : 0.0) - s) / Dm[r * LD + r];
-    __syncthreads();
+    if (part == 0 && r >= c) Wm[c * LD + r] = ((r == c ? 1.0 : 0.0) - s) * rdiag[r];
+    __syncwarp();
   }
+  __syncthreads();
   for (int e = tid; e < TT; e += blockDim.x) {
     const int r = e % T, cc = e / T;
     out[tsw(r, cc)] = r >= cc ? Wm[cc * LD + r] : 0.0;
@@ -313,7 +325,7 @@ constexpr int kUpdThreads = 256;
 // Left-looking update of tile column K: C(I,K) = A(I,K) - sum_J L(I,J) L(K,J)^T
 // for every stored tile (I,K); the CTA owning the diagonal tile then factors
 // and inverts it.  Operand tiles arrive by TMA bulk copy, double-buffered.
-__global__ void __launch_bounds__(kUpdThreads) k_patch_update(PatchArgs a, int K, const int32_t* __restrict__ col_start,
+__global__ void __launch_bounds__(kUpdThreads) k_patch_update(PatchArgs a, int K, const int32_t* __restrict__ active,
                                                                 const int32_t* __restrict__ tile_row,
                                                                 const int32_t* __restrict__ pair_ptr,
                                                                 const int32_t* __restrict__ pair_a,
@@ -323,7 +335,7 @@ __global__ void __launch_bounds__(kUpdThreads) k_patch_update(PatchArgs a, int K
   extern __shared__ __align__(128) double sm[];
   double* buf = sm;                                   // [2 stages][A,B][TT]
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + 4 * TT);
-  const int t = col_start[K] + blockIdx.x, j = blockIdx.y;
+  const int t = active[blockIdx.x], j = blockIdx.y;  // tiles of column K with work
   const int I = tile_row[t];
   double* base = tiles + size_t(j) * a.ntiles * TT;
   const int p0 = pair_ptr[t], np = pair_ptr[t + 1] - p0;
@@ -426,25 +438,32 @@ constexpr int SB = 256;                                    // doubles per packed
 // zeros of the factor, which the factorisation produces as exact 0.0.
 __global__ void k_patch_pack(int ntiles, const int32_t* __restrict__ mask, const int32_t* __restrict__ poff,
                              double* __restrict__ tiles) {
-  extern __shared__ __align__(16) double tile[];
+  extern __shared__ __align__(16) double tile[];  // 2 x TT (double buffer)
+  __shared__ int bits[16];
   double* base = tiles + size_t(blockIdx.x) * ntiles * TT;
-  for (int t = 0; t < ntiles; ++t) {
+  auto load = [&](int t, double* dst) {
     const double2* src = reinterpret_cast<const double2*>(base + size_t(t) * TT);
-    for (int e = threadIdx.x; e < TT / 2; e += blockDim.x) reinterpret_cast<double2*>(tile)[e] = src[e];
-    __syncthreads();
+    for (int e = threadIdx.x; e < TT / 2; e += blockDim.x) reinterpret_cast<double2*>(dst)[e] = src[e];
+  };
+  load(0, tile);
+  for (int t = 0; t < ntiles; ++t) {
+    double* cur = tile + (t & 1) * TT;
     const int m = mask[t];
+    if (threadIdx.x == 0) {
+      int n = 0;
+      for (int b2 = 0; b2 < 16; ++b2)
+        if ((m >> b2) & 1) bits[n++] = b2;
+    }
+    __syncthreads();  // cur loaded, bits ready, previous writes done
+    // Prefetch t+1: its source region starts at (t+1)*TT >= the end of tile t's
+    // packed destination, so the in-place compaction never overwrites unread data.
+    if (t + 1 < ntiles) load(t + 1, tile + ((t + 1) & 1) * TT);
     const int cnt = __popc(m);
     double* dst = base + size_t(poff[t]) * SB;
     for (int d = threadIdx.x; d < cnt * SB; d += blockDim.x) {
-      const int q = d / SB, w = d % SB;
-      int bit = -1, seen = -1;
-      for (int b2 = 0; b2 < 16 && seen < q; ++b2)
-        if ((m >> b2) & 1) {
-          ++seen;
-          bit = b2;
-        }
+      const int bit = bits[d / SB], w = d % SB;
       const int bi = bit >> 2, bj = bit & 3, cc = w >> 4, rr = (w & 15) ^ cc;
-      dst[d] = tile[tsw(16 * bi + rr, 16 * bj + cc)];
+      dst[d] = cur[tsw(16 * bi + rr, 16 * bj + cc)];
     }
     __syncthreads();
   }
@@ -676,9 +695,10 @@ void launch_patch_update(Context& c, int K) {
     FDM_CUDA(cudaFuncSetAttribute(k_patch_update, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     attr = true;
   }
-  dim3 grid(c.L.col_start[K + 1] - c.L.col_start[K], c.npatch);
+  const int na = c.L.active_ptr[K + 1] - c.L.active_ptr[K];
+  dim3 grid(na, c.npatch);
   KernelTimer timer(c, 1);
-  k_patch_update<<<grid, kUpdThreads, smem, c.stream>>>(a, K, c.col_start.p, c.tile_row.p, c.pair_ptr.p,
+  k_patch_update<<<grid, kUpdThreads, smem, c.stream>>>(a, K, c.active.p + c.L.active_ptr[K], c.tile_row.p, c.pair_ptr.p,
                                                          c.pair_a.p, c.pair_b.p, c.tile_mask.p, c.tiles.p);
   FDM_LAUNCH_CHECK(c);
 }
@@ -727,7 +747,12 @@ void launch_patch_solve(Context& c, const double* r_modal) {
 
 void launch_patch_pack(Context& c) {
   KernelTimer timer(c, 1);
-  k_patch_pack<<<c.npatch, 256, TT * sizeof(double), c.stream>>>(c.L.ntiles, c.tile_mask.p, c.tile_poff.p, c.tiles.p);
+  static bool attr = false;
+  if (!attr) {
+    FDM_CUDA(cudaFuncSetAttribute(k_patch_pack, cudaFuncAttributeMaxDynamicSharedMemorySize, int(2 * TT * sizeof(double))));
+    attr = true;
+  }
+  k_patch_pack<<<c.npatch, 512, 2 * TT * sizeof(double), c.stream>>>(c.L.ntiles, c.tile_mask.p, c.tile_poff.p, c.tiles.p);
   FDM_LAUNCH_CHECK(c);
 }
 

@@ -346,6 +346,14 @@ void analyze_patches(Context& c, int npatch, const int32_t* vertex, const int64_
     if (I != K) ++L.tile_gemms;  // TRSM against the diagonal inverse
   }
   L.tile_gemms += int64_t(L.pair_a.size());
+  // Update launches only visit tiles with work: the diagonal tile (factor +
+  // invert) and off-diagonal tiles with at least one update pair.
+  L.active_ptr.assign(1, 0);
+  for (int K = 0; K < L.nT; ++K) {
+    for (int t = L.col_start[K]; t < L.col_start[K + 1]; ++t)
+      if (L.tile_row[t] == K || L.pair_ptr[t + 1] > L.pair_ptr[t]) L.active.push_back(t);
+    L.active_ptr.push_back(int32_t(L.active.size()));
+  }
 
   // Structural nonzeros of the separator Schur complement S_G = A~_GG -
   // A~_GI D^-1 A~_IG (lower triangle), packed (tile << 12 | col << 6 | row):
