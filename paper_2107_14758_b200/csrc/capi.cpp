@@ -150,7 +150,76 @@ std::pair<double, double> tridiag_extremes(const std::vector<double>& dg, const 
   return {kth(0), kth(n - 1)};
 }
 
-// pcg (src/krylov.cpp:29-83) on device vectors; x must not alias b.
+// Builds the device-resident PCG loop (kernels/pcg.cu) as one CUDA graph:
+// WHILE(cont){ A p, p.Ap, alpha, x/r update, |r|, IF(continue){ z = Pinv r,
+// r.z, beta, p update } }.  Vectors: r = w0, z = w1, p = w2, Ap = w8, x = w9.
+void build_pcg_graph(Context& c, int precond, double omega) {
+  if (c.pcg_exec) {
+    cudaGraphExecDestroy(c.pcg_exec);
+    c.pcg_exec = nullptr;
+  }
+  prepare_buffers(c);
+  const bool timing = c.timing;
+  c.timing = false;  // no event records inside the captured graph
+  c.capturing = true;
+  double* r = c.w[0].p;
+  double* z = c.w[1].p;
+  double* p = c.w[2].p;
+  double* Ap = c.w[8].p;
+  double* x = c.w[9].p;
+  PcgDev* st = c.pcg_state.p;
+  cudaGraph_t g = nullptr, tmp = nullptr;
+  FDM_CUDA(cudaGraphCreate(&g, 0));
+  cudaGraphConditionalHandle hw, hi;
+  FDM_CUDA(cudaGraphConditionalHandleCreate(&hw, g, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams wp = {};
+  wp.type = cudaGraphNodeTypeConditional;
+  wp.conditional.handle = hw;
+  wp.conditional.type = cudaGraphCondTypeWhile;
+  wp.conditional.size = 1;
+  cudaGraphNode_t wn;
+  FDM_CUDA(cudaGraphAddNode(&wn, g, nullptr, 0, &wp));
+  cudaGraph_t body = wp.conditional.phGraph_out[0];
+  FDM_CUDA(cudaGraphConditionalHandleCreate(&hi, body, 0, 0));
+  FDM_CUDA(cudaStreamBeginCaptureToGraph(c.stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+  op_A(c, p, Ap);
+  launch_dot_partials(c, c.ndof, p, Ap, 0);
+  launch_dot_finish(c, 0, &st->pAp);
+  launch_pcg_alpha(c, st, c.pcg_alphas.p, hw);
+  launch_pcg_update_xr(c, st, p, Ap, x, r);
+  launch_dot_partials(c, c.ndof, r, r, 0);
+  launch_dot_finish(c, 0, &st->res);
+  launch_pcg_residual(c, st, c.pcg_res.p, hw, hi);
+  cudaStreamCaptureStatus cs;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t nd = 0;
+  FDM_CUDA(cudaStreamGetCaptureInfo(c.stream, &cs, nullptr, nullptr, &deps, &nd));
+  std::vector<cudaGraphNode_t> dv(deps, deps + nd);
+  FDM_CUDA(cudaStreamEndCapture(c.stream, &tmp));
+  cudaGraphNodeParams ip = {};
+  ip.type = cudaGraphNodeTypeConditional;
+  ip.conditional.handle = hi;
+  ip.conditional.type = cudaGraphCondTypeIf;
+  ip.conditional.size = 1;
+  cudaGraphNode_t in;
+  FDM_CUDA(cudaGraphAddNode(&in, body, dv.data(), dv.size(), &ip));
+  cudaGraph_t ibody = ip.conditional.phGraph_out[0];
+  FDM_CUDA(cudaStreamBeginCaptureToGraph(c.stream, ibody, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+  op_precond(c, precond, omega, r, z);
+  launch_dot_partials(c, c.ndof, r, z, 0);
+  launch_dot_finish(c, 0, &st->rz_new);
+  launch_pcg_beta(c, st, c.pcg_betas.p);
+  launch_pcg_update_p(c, st, z, p);
+  FDM_CUDA(cudaStreamEndCapture(c.stream, &tmp));
+  FDM_CUDA(cudaGraphInstantiate(&c.pcg_exec, g, 0));
+  FDM_CUDA(cudaGraphDestroy(g));
+  c.timing = timing;
+  c.capturing = false;
+  c.pcg_precond = precond;
+  c.pcg_omega = omega;
+}
+
+// pcg (src/krylov.cpp:29-83), device resident: x must not alias b.
 void run_pcg(Context& c, const double* b, double* x, double rtol, int maxit, int precond, double omega,
              fdmgpu_krylov_report* rep, std::vector<double>* residuals) {
   const auto t0 = std::chrono::steady_clock::now();
@@ -158,51 +227,54 @@ void run_pcg(Context& c, const double* b, double* x, double rtol, int maxit, int
   double* r = c.w[0].p;
   double* z = c.w[1].p;
   double* p = c.w[2].p;
-  double* Ap = c.w[8].p;
-  FDM_CUDA(cudaMemsetAsync(x, 0, c.ndof * sizeof(double), c.stream));
+  double* xi = c.w[9].p;
   const double bnorm = std::sqrt(host_dot(c, b, b));
   if (residuals) residuals->clear();
-  if (bnorm == 0.0) {
-    R.converged = 1;
-    R.kappa = 1.0;
+  FDM_CUDA(cudaMemsetAsync(xi, 0, c.ndof * sizeof(double), c.stream));
+  if (bnorm == 0.0 || maxit <= 0) {
+    if (x != xi) FDM_CUDA(cudaMemcpyAsync(x, xi, c.ndof * sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
+    FDM_CUDA(cudaStreamSynchronize(c.stream));
+    R.converged = bnorm == 0.0;
+    R.kappa = bnorm == 0.0 ? 1.0 : 0.0;
     *rep = R;
     return;
   }
   copy_dev(c, r, b);
   op_precond(c, precond, omega, r, z);
   copy_dev(c, p, z);
-  double rz = host_dot(c, r, z);
-  std::vector<double> alphas, betas;
-  for (int k = 0; k < maxit; ++k) {
-    op_A(c, p, Ap);
-    const double pAp = host_dot(c, p, Ap);
-    if (!(pAp > 0.0))
-      throw Error(FDMGPU_INDEFINITE, "pcg: indefinite operator at iteration " + std::to_string(k + 1));
-    const double alpha = rz / pAp;
-    launch_axpby(c, c.ndof, alpha, p, 1.0, x, x);
-    launch_axpby(c, c.ndof, -alpha, Ap, 1.0, r, r);
-    alphas.push_back(alpha);
-    const double res = std::sqrt(host_dot(c, r, r)) / bnorm;
-    if (residuals) residuals->push_back(res);
-    R.final_residual = res;
-    R.iterations = k + 1;
-    if (res <= rtol) {
-      R.converged = 1;
-      break;
-    }
-    op_precond(c, precond, omega, r, z);
-    const double rz_new = host_dot(c, r, z);
-    const double beta = rz_new / rz;
-    betas.push_back(beta);
-    rz = rz_new;
-    launch_axpby(c, c.ndof, 1.0, z, beta, p, p);
+  const double rz = host_dot(c, r, z);
+  if (!c.pcg_state.p) c.pcg_state.alloc(1);
+  if (c.pcg_cap < maxit) {
+    c.pcg_cap = std::max(maxit, 256);
+    c.pcg_alphas.alloc(c.pcg_cap);
+    c.pcg_betas.alloc(c.pcg_cap);
+    c.pcg_res.alloc(c.pcg_cap);
+    c.pcg_precond = -1;  // buffers moved: rebuild
   }
+  if (!c.pcg_exec || c.pcg_precond != precond || c.pcg_omega != omega) build_pcg_graph(c, precond, omega);
+  pcg_state_init(c, c.pcg_state.p, bnorm, rtol, rz, maxit);
+  FDM_CUDA(cudaGraphLaunch(c.pcg_exec, c.stream));
+  c.launches += 1;
+  int k = 0, status = 0;
+  pcg_state_read(c, c.pcg_state.p, &k, &status);
+  const int na = status == 2 ? k : k;  // alphas written for iterations 0..k-1 (k on indefinite: none at k)
+  std::vector<double> alphas(na), betas(std::max(na - 1, 0)), res(k);
+  if (na) FDM_CUDA(cudaMemcpy(alphas.data(), c.pcg_alphas.p, na * sizeof(double), cudaMemcpyDeviceToHost));
+  if (na > 1) FDM_CUDA(cudaMemcpy(betas.data(), c.pcg_betas.p, (na - 1) * sizeof(double), cudaMemcpyDeviceToHost));
+  if (k) FDM_CUDA(cudaMemcpy(res.data(), c.pcg_res.p, k * sizeof(double), cudaMemcpyDeviceToHost));
+  if (status == 2) throw Error(FDMGPU_INDEFINITE, "pcg: indefinite operator at iteration " + std::to_string(k + 1));
+  if (x != xi) FDM_CUDA(cudaMemcpyAsync(x, xi, c.ndof * sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
+  FDM_CUDA(cudaStreamSynchronize(c.stream));
+  if (residuals) *residuals = res;
+  R.iterations = k;
+  R.converged = status == 1;
+  R.final_residual = k ? res[k - 1] : 0.0;
   std::vector<double> td, to;
-  for (size_t k = 0; k < alphas.size(); ++k) {
-    double dk = 1.0 / alphas[k];
-    if (k > 0) dk += betas[k - 1] / alphas[k - 1];
+  for (size_t i = 0; i < alphas.size(); ++i) {
+    double dk = 1.0 / alphas[i];
+    if (i > 0) dk += betas[i - 1] / alphas[i - 1];
     td.push_back(dk);
-    if (k + 1 < alphas.size()) to.push_back(std::sqrt(betas[k]) / alphas[k]);
+    if (i + 1 < alphas.size()) to.push_back(std::sqrt(betas[i]) / alphas[i]);
   }
   auto [lmin, lmax] = tridiag_extremes(td, to);
   R.lambda_min = lmin;
@@ -631,7 +703,7 @@ fdmgpu_status fdmgpu_calibrate_damping(fdmgpu_handle h, int32_t lanczos_steps, u
   return fdmgpu::guarded(h, [&](Context& c) {
     c.check_ready(true, true, true);
     double* b = c.w[11].p;
-    double* x = c.w[9].p;
+    double* x = c.w[10].p;
     fdmgpu_krylov_report rep{};
     // estimate_damping (src/schwarz.cpp:97-119): CG-Lanczos of the smoother.
     auto hb = fdmgpu::random_free(c, seed);

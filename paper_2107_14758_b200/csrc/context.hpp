@@ -73,6 +73,12 @@ struct PatchLayout {
   int64_t nnz_L_reference = 0, flops_reference = 0;         // reference patch_ordering
 };
 
+// Device-resident PCG scalars (kernels/pcg.cu).
+struct PcgDev {
+  double bnorm, rtol, rz, rz_new, pAp, alpha, beta, res;
+  int k, maxit, status;  // status: 0 running, 1 converged, 2 indefinite at iteration k+1, 3 maxit
+};
+
 struct Context {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -126,14 +132,24 @@ struct Context {
   std::vector<double> h_red;
   double omega = 1.0, lambda_min = 0.0, lambda_max = 0.0;
 
+  // device PCG: one CUDA graph with a WHILE node (rebuilt when the
+  // preconditioner, omega or the coefficient capacity changes)
+  DevArray<PcgDev> pcg_state;
+  DevArray<double> pcg_alphas, pcg_betas, pcg_res;
+  cudaGraphExec_t pcg_exec = nullptr;
+  int pcg_precond = -1, pcg_cap = 0;
+  double pcg_omega = 0.0;
+
   // optional per-kernel CUDA-event timing (fdmgpu_kernel_timing)
   bool timing = false;
+  bool capturing = false;  // inside a CUDA-graph capture: launches are recorded, not counted
   bool force_staged = false;
   int sep_order = 0;  // 0 plane-by-plane facets (default), 1 reference patch_ordering (FDMGPU_SEP_ORDER)  // FDMGPU_FORCE_STAGED=1: staged cell kernels for every p (tests)
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tev[4];
 
   void check_ready(bool need_patches, bool need_factor, bool need_coarse) const;
   ~Context() {
+    if (pcg_exec) cudaGraphExecDestroy(pcg_exec);
     for (auto& v : tev)
       for (auto& [a, b] : v) {
         cudaEventDestroy(a);
@@ -181,5 +197,15 @@ void launch_restrict(Context& c, const double* fine, double* coarse);
 void launch_coarse_solve(Context& c, const double* rc, double* zc);
 void launch_prolong_add(Context& c, const double* coarse, double* fine);
 constexpr int kRedBlocks = 296;  // fixed reduction grid: deterministic partial sums
+void launch_dot_finish(Context& c, int k, double* dst);
+void pcg_state_init(Context& c, void* st, double bnorm, double rtol, double rz, int maxit);
+void pcg_state_read(Context& c, const void* st, int* k, int* status);
+void launch_pcg_alpha(Context& c, void* st, double* alphas, cudaGraphConditionalHandle hw);
+void launch_pcg_update_xr(Context& c, const void* st, const double* p, const double* Ap, double* x, double* r);
+void launch_pcg_residual(Context& c, void* st, double* residuals, cudaGraphConditionalHandle hw,
+                         cudaGraphConditionalHandle hi);
+void launch_pcg_beta(Context& c, void* st, double* betas);
+void launch_pcg_update_p(Context& c, const void* st, const double* z, double* p);
+void prepare_buffers(Context& c);
 
 }  // namespace fdmgpu

@@ -430,6 +430,19 @@ void launch_cells_quadrature(Context& c, const double* x) {
 
 namespace fdmgpu {
 
+// Allocate lazily-sized scratch before a CUDA-graph capture.
+void prepare_buffers(Context& c) {
+  if (!cells_fit_smem(c)) {
+    const size_t total = size_t(c.ncells) * c.npc;
+    if (c.E2.n < total) c.E2.alloc(total);
+  }
+  const bool kron_fits = sizeof(double) * (2 * size_t(c.n1) * c.n1 + 4 * size_t(c.npc)) <= 227 * 1024;
+  if (!(c.all_cartesian && kron_fits) && c.dim == 3 && c.q > 0) {
+    const size_t need = size_t(c.ncells) * 3 * c.n1 * c.q * c.q;
+    if (c.Qbuf.n < need) c.Qbuf.alloc(need);
+  }
+}
+
 void launch_cells_transform(Context& c, int dir, const double* in, int flags, const double* aux) {
   if (cells_fit_smem(c))
     launch_cells_transform_fused(c, dir, in, flags, aux);

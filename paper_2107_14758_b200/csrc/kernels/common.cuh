@@ -12,7 +12,7 @@ namespace fdmgpu {
 
 #define FDM_LAUNCH_CHECK(ctx)                 \
   do {                                        \
-    ++(ctx).launches;                         \
+    if (!(ctx).capturing) ++(ctx).launches;   \
     FDM_CUDA(cudaGetLastError());             \
   } while (0)
 

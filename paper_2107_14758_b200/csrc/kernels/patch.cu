@@ -321,6 +321,7 @@ __device__ void diag_factor_invert(double* Dm, double* Wm, double* out, const Pa
 }
 
 constexpr int kUpdThreads = 256;
+constexpr int kUpdStages = 3;  // TMA pipeline depth (2 operand tiles per stage, 64 KB)
 
 // Left-looking update of tile column K: C(I,K) = A(I,K) - sum_J L(I,J) L(K,J)^T
 // for every stored tile (I,K); the CTA owning the diagonal tile then factors
@@ -334,34 +335,33 @@ __global__ void __launch_bounds__(kUpdThreads) k_patch_update(PatchArgs a, int K
                                                                 double* __restrict__ tiles) {
   extern __shared__ __align__(128) double sm[];
   double* buf = sm;                                   // [2 stages][A,B][TT]
-  uint64_t* full = reinterpret_cast<uint64_t*>(sm + 4 * TT);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + 2 * kUpdStages * TT);
   const int t = active[blockIdx.x], j = blockIdx.y;  // tiles of column K with work
   const int I = tile_row[t];
   double* base = tiles + size_t(j) * a.ntiles * TT;
   const int p0 = pair_ptr[t], np = pair_ptr[t + 1] - p0;
   const int tid = threadIdx.x;
   if (tid == 0) {
-    mbar_init(&full[0], 1);
-    mbar_init(&full[1], 1);
+    for (int s = 0; s < kUpdStages; ++s) mbar_init(&full[s], 1);
     mbar_fence_init();
   }
   __syncthreads();
   if (tid == 0)
-    for (int s = 0; s < 2 && s < np; ++s) {
+    for (int s = 0; s < kUpdStages && s < np; ++s) {
       mbar_arrive_expect_tx(&full[s], 2 * TT * sizeof(double));
       bulk_g2s(buf + (2 * s) * TT, base + size_t(pair_a[p0 + s]) * TT, TT * sizeof(double), &full[s]);
       bulk_g2s(buf + (2 * s + 1) * TT, base + size_t(pair_b[p0 + s]) * TT, TT * sizeof(double), &full[s]);
     }
   TileAcc acc = {};
   for (int i = 0; i < np; ++i) {
-    const int s = i & 1;
-    mbar_wait(&full[s], (i >> 1) & 1);
+    const int s = i % kUpdStages;
+    mbar_wait(&full[s], (i / kUpdStages) & 1);
     tile_gemm_abt(buf + (2 * s) * TT, buf + (2 * s + 1) * TT, acc, tile_mask[pair_a[p0 + i]], tile_mask[pair_b[p0 + i]]);
     __syncthreads();
-    if (tid == 0 && i + 2 < np) {
+    if (tid == 0 && i + kUpdStages < np) {
       mbar_arrive_expect_tx(&full[s], 2 * TT * sizeof(double));
-      bulk_g2s(buf + (2 * s) * TT, base + size_t(pair_a[p0 + i + 2]) * TT, TT * sizeof(double), &full[s]);
-      bulk_g2s(buf + (2 * s + 1) * TT, base + size_t(pair_b[p0 + i + 2]) * TT, TT * sizeof(double), &full[s]);
+      bulk_g2s(buf + (2 * s) * TT, base + size_t(pair_a[p0 + i + kUpdStages]) * TT, TT * sizeof(double), &full[s]);
+      bulk_g2s(buf + (2 * s + 1) * TT, base + size_t(pair_b[p0 + i + kUpdStages]) * TT, TT * sizeof(double), &full[s]);
     }
   }
   double* ct = base + size_t(t) * TT;
@@ -689,7 +689,7 @@ void launch_patch_assemble(Context& c) {
 
 void launch_patch_update(Context& c, int K) {
   PatchArgs a = make_args(c);
-  const size_t smem = sizeof(double) * 4 * TT + 64;
+  const size_t smem = sizeof(double) * 2 * kUpdStages * TT + 64;
   static bool attr = false;
   if (!attr) {
     FDM_CUDA(cudaFuncSetAttribute(k_patch_update, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
