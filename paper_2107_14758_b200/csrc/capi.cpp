@@ -162,6 +162,12 @@ void build_pcg_graph(Context& c, int precond, double omega) {
   const bool timing = c.timing;
   c.timing = false;  // no event records inside the captured graph
   c.capturing = true;
+  // Capture on a private stream (the handle's stream may be the legacy default
+  // stream, which cannot be captured); the graph is launched on c.stream.
+  if (!c.cap_stream) FDM_CUDA(cudaStreamCreateWithFlags(&c.cap_stream, cudaStreamNonBlocking));
+  FDM_CUDA(cudaStreamSynchronize(c.stream));
+  cudaStream_t user_stream = c.stream;
+  c.stream = c.cap_stream;
   double* r = c.w[0].p;
   double* z = c.w[1].p;
   double* p = c.w[2].p;
@@ -215,6 +221,7 @@ void build_pcg_graph(Context& c, int precond, double omega) {
   FDM_CUDA(cudaGraphDestroy(g));
   c.timing = timing;
   c.capturing = false;
+  c.stream = user_stream;
   c.pcg_precond = precond;
   c.pcg_omega = omega;
 }

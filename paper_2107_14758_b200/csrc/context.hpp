@@ -137,6 +137,7 @@ struct Context {
   DevArray<PcgDev> pcg_state;
   DevArray<double> pcg_alphas, pcg_betas, pcg_res;
   cudaGraphExec_t pcg_exec = nullptr;
+  cudaStream_t cap_stream = nullptr;  // private stream for graph captures
   int pcg_precond = -1, pcg_cap = 0;
   double pcg_omega = 0.0;
 
@@ -150,6 +151,7 @@ struct Context {
   void check_ready(bool need_patches, bool need_factor, bool need_coarse) const;
   ~Context() {
     if (pcg_exec) cudaGraphExecDestroy(pcg_exec);
+    if (cap_stream) cudaStreamDestroy(cap_stream);
     for (auto& v : tev)
       for (auto& [a, b] : v) {
         cudaEventDestroy(a);

@@ -181,6 +181,7 @@ void analyze_patches(Context& c, int npatch, const int32_t* vertex, const int64_
   const char* dbg_env = std::getenv("FDMGPU_DEBUG");
   const bool dbg = dbg_env && dbg_env[0] == '1';
   std::vector<uint8_t> m32(dbg ? size_t(L.mpad / 32) * (L.mpad / 32) : 0), m16(size_t(L.mpad / 16) * (L.mpad / 16), 0);
+  std::vector<uint8_t> m8(dbg ? size_t(L.mpad / 8) * (L.mpad / 8) : 0);
   int64_t nnz_sep = 0;
   int stamp = 0;
   // All structural neighbours (any position) of position k in the canonical
@@ -247,7 +248,10 @@ void analyze_patches(Context& c, int npatch, const int32_t* vertex, const int64_
           tmark[size_t((k - L.nI) / T) * L.nT + (jj - L.nI) / T] = 1;
           ++nnz_sep;
           m16[size_t((k - L.nI) / 16) * (L.mpad / 16) + (jj - L.nI) / 16] = 1;
-          if (dbg) m32[size_t((k - L.nI) / 32) * (L.mpad / 32) + (jj - L.nI) / 32] = 1;
+          if (dbg) {
+            m32[size_t((k - L.nI) / 32) * (L.mpad / 32) + (jj - L.nI) / 32] = 1;
+            m8[size_t((k - L.nI) / 8) * (L.mpad / 8) + (jj - L.nI) / 8] = 1;
+          }
         }
       }
     }
@@ -295,7 +299,9 @@ void analyze_patches(Context& c, int npatch, const int32_t* vertex, const int64_
   }
   for (int K = 0; K < L.nT; ++K) tmark[size_t(K) * L.nT + K] = 1;
   if (dbg) {
-    int64_t t64 = 0, t32 = 0, t16 = 0;
+    int64_t t64 = 0, t32 = 0, t16 = 0, t8 = 0;
+    for (auto v : m8) t8 += v;
+    std::fprintf(stderr, "[fdmgpu] blocks8 %lld (%.3f)\n", (long long)t8, double(nnz_sep + L.m) / (t8 * 64.0));
     for (auto v : tmark) t64 += v;
     for (auto v : m32) t32 += v;
     for (auto v : m16) t16 += v;

@@ -172,6 +172,17 @@ def test_not_spd_reports_pivot(pkg, torch):
     sol.factor()
 
 
+def test_pcg_on_callers_default_stream(pkg, torch):
+    # the handle runs on torch's (legacy default) stream; the PCG graph is
+    # captured on a private stream and launched on the caller's
+    prob = pkg.Problem(2, 3, 3)
+    sol = pkg.Solver(prob, stream=torch.cuda.current_stream())
+    sol.factor()
+    sol.calibrate_damping()
+    _, rep = sol.pcg(torch.from_numpy(prob.rhs()).cuda())
+    assert rep["converged"] and rep["iterations"] == 13
+
+
 def test_launch_evidence(pkg, torch):
     prob = pkg.Problem(2, 3, 3)
     sol = pkg.Solver(prob)
