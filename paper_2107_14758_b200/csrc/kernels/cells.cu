@@ -34,15 +34,22 @@ namespace {
 
 enum : int { kSchur = 1, kRecon = 2 };
 
-// out[.., k, ..] = alpha * sum_j M1[k + n1 j] in1[.., j, ..] (+ beta * same with M2/in2)
-__device__ __forceinline__ void contract(int n1, int npc, int stride, const double* __restrict__ M1,
+// out[.., k, ..] = alpha * sum_j M1[k + n1 j] in1[.., j, ..] (+ beta * same with M2/in2).
+// N1C > 0 makes the tile edge a compile-time constant (index math becomes
+// shifts / multiplies and the j loop unrolls); N1C = 0 is the generic path.
+template <int N1C>
+__device__ __forceinline__ void contract(int n1_rt, int npc, int axis, const double* __restrict__ M1,
                                          const double* __restrict__ in1, double alpha, const double* __restrict__ M2,
                                          const double* __restrict__ in2, double beta, double* __restrict__ out) {
+  const int n1 = N1C > 0 ? N1C : n1_rt;
+  const int stride = axis == 0 ? 1 : (axis == 1 ? n1 : n1 * n1);
   for (int o = threadIdx.x; o < npc; o += blockDim.x) {
     const int k = (o / stride) % n1;
     const int base = o - k * stride;
     double s1 = 0.0, s2 = 0.0;
-    for (int j = 0; j < n1; ++j) {
+#pragma unroll
+    for (int j = 0; j < (N1C > 0 ? N1C : 64); ++j) {
+      if (N1C == 0 && j >= n1) break;
       s1 = fma(M1[k + n1 * j], in1[base + j * stride], s1);
       if (M2) s2 = fma(M2[k + n1 * j], in2[base + j * stride], s2);
     }
@@ -59,10 +66,12 @@ struct CellFdm {
 };
 
 // lattice index of interior point number ii (each coordinate in 1..p-1)
+template <int N1C>
 __device__ __forceinline__ int interior_lat(const CellFdm& f, int ii, int* x) {
-  const int pm = f.p - 1;
+  const int n1 = N1C > 0 ? N1C : f.n1;
+  const int pm = n1 - 2;
   int lin = 0, stride = 1;
-  for (int a = 0; a < f.dim; ++a, stride *= f.n1) {
+  for (int a = 0; a < f.dim; ++a, stride *= n1) {
     x[a] = 1 + ii % pm;
     ii /= pm;
     lin += x[a] * stride;
@@ -70,10 +79,11 @@ __device__ __forceinline__ int interior_lat(const CellFdm& f, int ii, int* x) {
   return lin;
 }
 
+template <int N1C>
 __device__ void compute_invD(const CellFdm& f) {
   for (int ii = threadIdx.x; ii < f.ni; ii += blockDim.x) {
     int x[3];
-    interior_lat(f, ii, x);
+    interior_lat<N1C>(f, ii, x);
     double s = 0.0;
     for (int q = 0; q < f.dim; ++q) {
       double prod = f.mu[q];
@@ -85,8 +95,10 @@ __device__ void compute_invD(const CellFdm& f) {
 }
 
 // u[facet point] -= sum_x A~_{f x} u[x] / D_x for the 2 dim faces of the cell.
+template <int N1C>
 __device__ void schur_faces(const CellFdm& f, double* u) {
-  const int pm = f.p - 1;
+  const int n1c = N1C > 0 ? N1C : f.n1;
+  const int pm = n1c - 2;
   int nt = 1;
   for (int a = 1; a < f.dim; ++a) nt *= pm;
   for (int idx = threadIdx.x; idx < 2 * f.dim * nt; idx += blockDim.x) {
@@ -101,7 +113,7 @@ __device__ void schur_faces(const CellFdm& f, double* u) {
       coef *= f.Bt[x[b] * (f.n1 + 1)];
     }
     int stride_a = 1, lin0 = 0, ii0 = 0, istride_a = 1;
-    for (int b = 0, s = 1, is = 1; b < f.dim; ++b, s *= f.n1, is *= pm) {
+    for (int b = 0, s = 1, is = 1; b < f.dim; ++b, s *= n1c, is *= pm) {
       if (b == a) {
         stride_a = s;
         istride_a = is;
@@ -111,18 +123,22 @@ __device__ void schur_faces(const CellFdm& f, double* u) {
       }
     }
     double acc = 0.0;
-    for (int xa = 1; xa < f.p; ++xa)
-      acc = fma(f.At[e + f.n1 * xa] * u[lin0 + xa * stride_a], f.invD[ii0 + (xa - 1) * istride_a], acc);
+#pragma unroll
+    for (int xa = 1; xa < (N1C > 0 ? N1C - 1 : 64); ++xa) {
+      if (N1C == 0 && xa >= f.p) break;
+      acc = fma(f.At[e + n1c * xa] * u[lin0 + xa * stride_a], f.invD[ii0 + (xa - 1) * istride_a], acc);
+    }
     u[lin0 + e * stride_a] -= coef * acc;
   }
 }
 
 // u[x] = (nK * b[x] - sum_{a, e} A~_{x, f(a,e)} u[f(a,e)]) / D_x for every interior x.
+template <int N1C>
 __device__ void recon_interior(const CellFdm& f, double* u, const double* __restrict__ rb,
                                const int32_t* __restrict__ cd, double nK) {
   for (int ii = threadIdx.x; ii < f.ni; ii += blockDim.x) {
     int x[3];
-    const int lin = interior_lat(f, ii, x);
+    const int lin = interior_lat<N1C>(f, ii, x);
     double v = nK * rb[cd[lin]];
     for (int a = 0, s = 1; a < f.dim; ++a, s *= f.n1) {
       double coef = f.mu[a];
@@ -155,6 +171,7 @@ __device__ void load_cell_fdm(CellFdm& f, double* smem_tables, int dim, int n1, 
   f.invD = bt + n1 * n1;
 }
 
+template <int N1C>
 __global__ void k_cells_transform(int dim, int n1, int npc, int dir, int flags, const double* __restrict__ in,
                                   const double* __restrict__ aux, double* __restrict__ E,
                                   const int32_t* __restrict__ cdofs, const double* __restrict__ inv_mult,
@@ -183,18 +200,17 @@ __global__ void k_cells_transform(int dim, int n1, int npc, int dir, int flags, 
   }
   __syncthreads();
   if (flags) {
-    compute_invD(f);
+    compute_invD<N1C>(f);
     __syncthreads();
   }
   if (flags & kRecon) {
-    recon_interior(f, b0, aux, cd, nK[c]);
+    recon_interior<N1C>(f, b0, aux, cd, nK[c]);
     __syncthreads();
   }
   double* src = b0;
   double* dst = b1;
-  int stride = 1;
-  for (int a = 0; a < dim; ++a, stride *= n1) {
-    contract(n1, npc, stride, Ms, src, 1.0, nullptr, nullptr, 0.0, dst);
+  for (int a = 0; a < dim; ++a) {
+    contract<N1C>(n1, npc, a, Ms, src, 1.0, nullptr, nullptr, 0.0, dst);
     __syncthreads();
     double* t = src;
     src = dst;
@@ -205,7 +221,7 @@ __global__ void k_cells_transform(int dim, int n1, int npc, int dir, int flags, 
     __syncthreads();
   }
   if (flags & kSchur) {
-    schur_faces(f, src);
+    schur_faces<N1C>(f, src);
     __syncthreads();
   }
   double* e = E + size_t(c) * npc;
@@ -230,7 +246,7 @@ __global__ void k_cells_schur(int dim, int n1, int npc, const double* __restrict
     u[l] = cons[g] ? 0.0 : in[g];
   }
   __syncthreads();
-  compute_invD(f);
+  compute_invD<0>(f);
   __syncthreads();
   // keep the interior values, zero everything else, then subtract at facets
   for (int l = threadIdx.x; l < npc; l += blockDim.x) {
@@ -239,7 +255,7 @@ __global__ void k_cells_schur(int dim, int n1, int npc, const double* __restrict
     if (!interior) u[l] = 0.0;
   }
   __syncthreads();
-  schur_faces(f, u);
+  schur_faces<0>(f, u);
   __syncthreads();
   double* e = E + size_t(c) * npc;
   for (int l = threadIdx.x; l < npc; l += blockDim.x) {
@@ -263,18 +279,19 @@ __global__ void k_cells_recon(int dim, int n1, int npc, double* __restrict__ z, 
   const int32_t* cd = cdofs + size_t(c) * npc;
   for (int l = threadIdx.x; l < npc; l += blockDim.x) u[l] = z[cd[l]];
   __syncthreads();
-  compute_invD(f);
+  compute_invD<0>(f);
   __syncthreads();
-  recon_interior(f, u, rb, cd, nK[c]);
+  recon_interior<0>(f, u, rb, cd, nK[c]);
   __syncthreads();
   for (int ii = threadIdx.x; ii < f.ni; ii += blockDim.x) {
     int x[3];
-    const int lin = interior_lat(f, ii, x);
+    const int lin = interior_lat<0>(f, ii, x);
     z[cd[lin]] = u[lin];
   }
 }
 
 // Cartesian stiffness: y_K = sum_a mu_a (A on axis a, B elsewhere) u_K.
+template <int N1C>
 __global__ void k_cells_stiffness(int dim, int n1, int npc, const double* __restrict__ x, double* __restrict__ E,
                                   const int32_t* __restrict__ cdofs, const uint8_t* __restrict__ cons,
                                   const double* __restrict__ mu, const double* __restrict__ Ahat,
@@ -298,23 +315,23 @@ __global__ void k_cells_stiffness(int dim, int n1, int npc, const double* __rest
   }
   const double m0 = mu[size_t(c) * dim], m1 = mu[size_t(c) * dim + 1], m2 = dim == 3 ? mu[size_t(c) * dim + 2] : 0.0;
   __syncthreads();
-  contract(n1, npc, 1, Bs, u, 1.0, nullptr, nullptr, 0.0, t0);  // B_x u
-  contract(n1, npc, 1, As, u, 1.0, nullptr, nullptr, 0.0, t1);  // A_x u
+  contract<N1C>(n1, npc, 0, Bs, u, 1.0, nullptr, nullptr, 0.0, t0);  // B_x u
+  contract<N1C>(n1, npc, 0, As, u, 1.0, nullptr, nullptr, 0.0, t1);  // A_x u
   __syncthreads();
   double* e = E + size_t(c) * npc;
   if (dim == 2) {
     // mu0 B_y A_x u + mu1 A_y B_x u
-    contract(n1, npc, n1, Bs, t1, m0, As, t0, m1, u);
+    contract<N1C>(n1, npc, 1, Bs, t1, m0, As, t0, m1, u);
     __syncthreads();
     for (int l = threadIdx.x; l < npc; l += blockDim.x) e[l] = u[l];
     return;
   }
   // P = mu0 B_y A_x u + mu1 A_y B_x u  (into u),  Q = B_y B_x u
-  contract(n1, npc, n1, Bs, t1, m0, As, t0, m1, u);
-  contract(n1, npc, n1, Bs, t0, 1.0, nullptr, nullptr, 0.0, q);
+  contract<N1C>(n1, npc, 1, Bs, t1, m0, As, t0, m1, u);
+  contract<N1C>(n1, npc, 1, Bs, t0, 1.0, nullptr, nullptr, 0.0, q);
   __syncthreads();
   // y = B_z P + mu2 A_z Q
-  contract(n1, npc, n1 * n1, Bs, u, 1.0, As, q, m2, t0);
+  contract<N1C>(n1, npc, 2, Bs, u, 1.0, As, q, m2, t0);
   __syncthreads();
   for (int l = threadIdx.x; l < npc; l += blockDim.x) e[l] = t0[l];
 }
@@ -352,12 +369,21 @@ int cell_threads(const Context& c) { return c.npc >= 1024 ? 512 : 256; }
 
 void launch_cells_transform_fused(Context& c, int dir, const double* in, int flags, const double* aux) {
   const size_t smem = sizeof(double) * (size_t(c.n1) * c.n1 + 2 * size_t(c.npc)) + (flags ? fdm_tables_bytes(c) : 0);
-  set_smem(k_cells_transform, smem);
-  KernelTimer timer(c, 2);
-  k_cells_transform<<<c.ncells, cell_threads(c), smem, c.stream>>>(
-      c.dim, c.n1, c.npc, dir, flags, in, aux, c.E.p, dir == 0 ? c.cell_dofs.p : c.cell_modes.p, c.inv_mult.p,
-      c.constrained.p, c.mode_sign.p, dir == 0 ? c.St.p : c.S.p, c.mu.p, c.At.p, c.Bt.p, c.nK.p);
-  FDM_LAUNCH_CHECK(c);
+  auto go = [&](auto kernel) {
+    set_smem(kernel, smem);
+    KernelTimer timer(c, 2);
+    kernel<<<c.ncells, cell_threads(c), smem, c.stream>>>(
+        c.dim, c.n1, c.npc, dir, flags, in, aux, c.E.p, dir == 0 ? c.cell_dofs.p : c.cell_modes.p, c.inv_mult.p,
+        c.constrained.p, c.mode_sign.p, dir == 0 ? c.St.p : c.S.p, c.mu.p, c.At.p, c.Bt.p, c.nK.p);
+    FDM_LAUNCH_CHECK(c);
+  };
+  switch (c.n1) {
+    case 4: go(k_cells_transform<4>); break;
+    case 6: go(k_cells_transform<6>); break;
+    case 8: go(k_cells_transform<8>); break;
+    case 16: go(k_cells_transform<16>); break;
+    default: go(k_cells_transform<0>);
+  }
 }
 
 void launch_cells_schur_fused(Context& c, const double* in) {
@@ -388,11 +414,20 @@ void launch_gather(Context& c, int mode, const double* E, const double* x, doubl
 
 void launch_cells_stiffness_kron(Context& c, const double* x) {
   const size_t smem = sizeof(double) * (2 * size_t(c.n1) * c.n1 + 4 * size_t(c.npc));
-  set_smem(k_cells_stiffness, smem);
-  KernelTimer timer(c, 3);
-  k_cells_stiffness<<<c.ncells, cell_threads(c), smem, c.stream>>>(c.dim, c.n1, c.npc, x, c.E.p, c.cell_dofs.p,
-                                                                   c.constrained.p, c.mu.p, c.Ahat.p, c.Bhat.p);
-  FDM_LAUNCH_CHECK(c);
+  auto go = [&](auto kernel) {
+    set_smem(kernel, smem);
+    KernelTimer timer(c, 3);
+    kernel<<<c.ncells, cell_threads(c), smem, c.stream>>>(c.dim, c.n1, c.npc, x, c.E.p, c.cell_dofs.p,
+                                                          c.constrained.p, c.mu.p, c.Ahat.p, c.Bhat.p);
+    FDM_LAUNCH_CHECK(c);
+  };
+  switch (c.n1) {
+    case 4: go(k_cells_stiffness<4>); break;
+    case 6: go(k_cells_stiffness<6>); break;
+    case 8: go(k_cells_stiffness<8>); break;
+    case 16: go(k_cells_stiffness<16>); break;
+    default: go(k_cells_stiffness<0>);
+  }
 }
 
 }  // namespace fdmgpu
