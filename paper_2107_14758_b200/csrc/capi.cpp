@@ -544,6 +544,9 @@ fdmgpu_status fdmgpu_set_patches(fdmgpu_handle h, int32_t npatch, const int32_t*
     c.entries.upload(L.entries, c.stream);
     c.tile_mask.upload(L.tile_mask, c.stream);
     c.tile_poff.upload(L.tile_poff, c.stream);
+    c.tile_mask8.upload(L.tile_mask8, c.stream);
+    c.tile_poff8.upload(L.tile_poff8, c.stream);
+    c.tile_hdr.upload(L.tile_hdr, c.stream);
     c.active.upload(L.active, c.stream);
     if (L.pair_a.empty()) {
       c.pair_a.alloc(1);
@@ -635,7 +638,7 @@ fdmgpu_status fdmgpu_get_layout(fdmgpu_handle h, fdmgpu_layout* out) {
     L.nnz_L_reference = c.L.nnz_L_reference;
     L.flops_reference = c.L.flops_reference;
     L.separator_order = c.sep_order;
-    L.stream_bytes = int64_t(c.L.tile_poff.back()) * 256 * 8 * c.npatch;
+    L.stream_bytes = int64_t(c.L.tile_poff8.back()) * 8 * c.npatch;
     *out = L;
   });
 }

@@ -67,7 +67,10 @@ struct PatchLayout {
   std::vector<int32_t> tile_row, tile_col, col_start;  // tile pattern, column-major order
   std::vector<int32_t> pair_ptr, pair_a, pair_b;       // left-looking update pairs per tile
   std::vector<int32_t> entries;      // structural nonzeros of S_G: tile << 12 | col << 6 | row
-  std::vector<int32_t> tile_mask, tile_poff;  // packed 16x16 sub-blocks per tile (solve stream)
+  std::vector<int32_t> tile_mask, tile_poff;  // 16x16 sub-blocks the factorisation touches per tile
+  std::vector<int64_t> tile_mask8;            // 8x8 sub-blocks per tile kept in the solve stream
+  std::vector<int32_t> tile_poff8;            // stream record offset (doubles): header + sub-blocks
+  std::vector<uint8_t> tile_hdr;              // 128-byte record header per tile
   std::vector<int32_t> active, active_ptr;    // per column: tiles the update kernel must visit
   int64_t nnz_L = 0, flops_ref = 0, tile_gemms = 0;          // order in use
   int64_t nnz_L_reference = 0, flops_reference = 0;         // reference patch_ordering
@@ -114,7 +117,9 @@ struct Context {
   int npatch = 0;
   PatchLayout L;
   DevArray<int32_t> pdofs, lat, pos_of_lat, pcells, pg_ptr, pg_idx;
-  DevArray<int32_t> tile_row, tile_col, col_start, pair_ptr, pair_a, pair_b, entries, tile_mask, tile_poff, active;
+  DevArray<int32_t> tile_row, tile_col, col_start, pair_ptr, pair_a, pair_b, entries, tile_mask, tile_poff, active, tile_poff8;
+  DevArray<int64_t> tile_mask8;
+  DevArray<uint8_t> tile_hdr;
   DevArray<double> corr, tiles, nK;
   std::vector<int32_t> h_pdofs, h_pcells;
   bool have_patches = false, factored = false;
@@ -144,8 +149,8 @@ struct Context {
   // optional per-kernel CUDA-event timing (fdmgpu_kernel_timing)
   bool timing = false;
   bool capturing = false;  // inside a CUDA-graph capture: launches are recorded, not counted
-  bool force_staged = false;
-  int sep_order = 0;  // 0 plane-by-plane facets (default), 1 reference patch_ordering (FDMGPU_SEP_ORDER)  // FDMGPU_FORCE_STAGED=1: staged cell kernels for every p (tests)
+  bool force_staged = false;  // FDMGPU_FORCE_STAGED=1: staged cell kernels for every p (tests)
+  int sep_order = 0;  // 0 plane-by-plane facets (default), 1 reference patch_ordering (FDMGPU_SEP_ORDER)
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tev[4];
 
   void check_ready(bool need_patches, bool need_factor, bool need_coarse) const;

@@ -429,17 +429,20 @@ __global__ void __launch_bounds__(kUpdThreads) k_patch_trsm(PatchArgs a, int K, 
 // ---- K3: patch relaxation solve -------------------------------------------------
 constexpr int kSolveConsumers = 8;                         // consumer warps
 constexpr int kSolveThreads = 32 * (kSolveConsumers + 1);  // + 1 TMA producer warp
-constexpr int SB = 256;                                    // doubles per packed 16x16 sub-block
+constexpr int SB = 256;
+constexpr int SB8 = 64;   // doubles per packed 8x8 sub-block (solve stream)
+constexpr int kHdr = 16;  // doubles of the per-tile stream header (128 block-index bytes)
+constexpr int kSlot = TT + kHdr;  // ring slot: the densest possible record
 
 // Packed solve stream.  After factorisation every 64x64 tile is compacted to
 // its structurally nonzero 16x16 sub-blocks (mask bit bi*4 + bj, packed in bit
 // order; element (r, c) of a sub-block at c*16 + (r ^ c), conflict free for
 // both row and column sweeps).  Exact: the dropped sub-blocks are structural
 // zeros of the factor, which the factorisation produces as exact 0.0.
-__global__ void k_patch_pack(int ntiles, const int32_t* __restrict__ mask, const int32_t* __restrict__ poff,
-                             double* __restrict__ tiles) {
+__global__ void k_patch_pack(int ntiles, const int64_t* __restrict__ mask8, const int32_t* __restrict__ poff8,
+                             const uint8_t* __restrict__ hdr, double* __restrict__ tiles) {
   extern __shared__ __align__(16) double tile[];  // 2 x TT (double buffer)
-  __shared__ int bits[16];
+  __shared__ int bits[64];
   double* base = tiles + size_t(blockIdx.x) * ntiles * TT;
   auto load = [&](int t, double* dst) {
     const double2* src = reinterpret_cast<const double2*>(base + size_t(t) * TT);
@@ -448,99 +451,160 @@ __global__ void k_patch_pack(int ntiles, const int32_t* __restrict__ mask, const
   load(0, tile);
   for (int t = 0; t < ntiles; ++t) {
     double* cur = tile + (t & 1) * TT;
-    const int m = mask[t];
-    if (threadIdx.x == 0) {
-      int n = 0;
-      for (int b2 = 0; b2 < 16; ++b2)
-        if ((m >> b2) & 1) bits[n++] = b2;
-    }
+    const unsigned long long m = static_cast<unsigned long long>(mask8[t]);
+    if (threadIdx.x < 64 && ((m >> threadIdx.x) & 1ull))
+      bits[__popcll(m & ((1ull << threadIdx.x) - 1ull))] = int(threadIdx.x);
     __syncthreads();  // cur loaded, bits ready, previous writes done
     // Prefetch t+1: its source region starts at (t+1)*TT >= the end of tile t's
     // packed destination, so the in-place compaction never overwrites unread data.
     if (t + 1 < ntiles) load(t + 1, tile + ((t + 1) & 1) * TT);
-    const int cnt = __popc(m);
-    double* dst = base + size_t(poff[t]) * SB;
-    for (int d = threadIdx.x; d < cnt * SB; d += blockDim.x) {
-      const int bit = bits[d / SB], w = d % SB;
-      const int bi = bit >> 2, bj = bit & 3, cc = w >> 4, rr = (w & 15) ^ cc;
-      dst[d] = cur[tsw(16 * bi + rr, 16 * bj + cc)];
+    const int cnt = __popcll(m);
+    double* dst = base + size_t(poff8[t]);
+    if (threadIdx.x < kHdr) dst[threadIdx.x] = reinterpret_cast<const double*>(hdr + size_t(t) * 8 * kHdr)[threadIdx.x];
+    dst += kHdr;
+    for (int d = threadIdx.x; d < cnt * SB8; d += blockDim.x) {
+      const int bit = bits[d >> 6], w = d & 63;
+      const int bi = bit >> 3, bj = bit & 7, rr = w >> 3, cc = 2 * (((w >> 1) & 3) ^ ((rr >> 1) & 3)) + (w & 1);
+      dst[d] = cur[tsw(8 * bi + rr, 8 * bj + cc)];
     }
     __syncthreads();
   }
 }
 
-// out[bi] (rows 16 bi + (lane & 15)) = sum over the tile's sub-blocks of
-// block-row bi of L_sub * x[16 bj ..]; half-warps split the 16 columns.
-__device__ __forceinline__ void packed_fwd(const double* __restrict__ slot, int mask, const double* __restrict__ x,
-                                           int lane, double out[4]) {
-  const int rr = lane & 15, h = lane >> 4;
-  int q = 0;
+// Packed 8x8 sub-block layout: row-major, element (r, c) at
+// r*8 + 2*((c >> 1) ^ ((r >> 1) & 3)) + (c & 1).  Lane (r = lane & 7,
+// g = lane >> 3) owns block-columns g and 7 - g (balanced on the triangular
+// diagonal tiles) and reads row r of a sub-block as four 16-byte loads,
+// conflict free per quarter-warp.  Both solve directions use this lane map:
+//   forward  (y_I -= L_IK y_K): 8 row sums per lane, closed by two shuffles;
+//   backward (u_K -= L_IK^T y_I): 16 column partials per lane accumulated over
+//            the tiles of a column, reduced across the 8 row lanes once.
+// Absent sub-blocks read a shared zero block instead of branching, so every
+// tile is one straight-line sequence of independent loads and FMA chains.
+__device__ __forceinline__ void ld_row8(const double* __restrict__ B, int r, double v[8]) {
+  const double2* row = reinterpret_cast<const double2*>(B + r * 8);
 #pragma unroll
-  for (int bi = 0; bi < 4; ++bi) {
-    double acc = 0.0;
-#pragma unroll
-    for (int bj = 0; bj < 4; ++bj) {
-      if ((mask >> (bi * 4 + bj)) & 1) {
-        const double* B = slot + q * SB;
-        const double* xv = x + 16 * bj + 8 * h;
-        ++q;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const int cc = 8 * h + k;
-          acc = fma(B[cc * 16 + (rr ^ cc)], xv[k], acc);
-        }
-      }
-    }
-    out[bi] = acc + __shfl_xor_sync(0xffffffffu, acc, 16);
+  for (int j = 0; j < 4; ++j) {
+    const double2 t = row[j ^ ((r >> 1) & 3)];
+    v[2 * j] = t.x;
+    v[2 * j + 1] = t.y;
   }
 }
 
-// out[bj] (columns 16 bj + (lane & 15)) = sum over block-column bj of L_sub^T x[16 bi ..].
-__device__ __forceinline__ void packed_bwd(const double* __restrict__ slot, int mask, const double* __restrict__ x,
-                                           int lane, double out[4]) {
-  const int cc = lane & 15, h = lane >> 4;
+// Sub-block (bi, bj) of a stream record: header byte -> packed index.
+__device__ __forceinline__ const double* rec_block(const double* rec, const double* zblk, unsigned long long hw,
+                                                   int e) {
+  const unsigned idx = unsigned(hw >> (8 * e)) & 0xffu;
+  return idx == 0xffu ? zblk : rec + kHdr + idx * SB8;
+}
+
+// Forward, rows map: lane (r, g) owns block-rows g and 7 - g (two sub-block
+// rows of 8 doubles each per block-column) and the whole x = y_K in
+// registers, so its two output rows need no cross-lane reduction.
+__device__ __forceinline__ void tile_fwd(const double* __restrict__ rec, const double* __restrict__ zblk, int r, int g,
+                                         const double (&x)[64], double& o0, double& o1) {
+  const unsigned long long* hrow = reinterpret_cast<const unsigned long long*>(rec);  // [bi][bj] bytes
 #pragma unroll
-  for (int bj = 0; bj < 4; ++bj) {
-    double acc = 0.0;
+  for (int jj = 0; jj < 2; ++jj) {
+    const unsigned long long hw = hrow[jj ? 7 - g : g];
+    double a0 = 0.0, a1 = 0.0;
 #pragma unroll
-    for (int bi = 0; bi < 4; ++bi) {
-      const int bit = bi * 4 + bj;
-      if ((mask >> bit) & 1) {
-        const double* B = slot + __popc(mask & ((1 << bit) - 1)) * SB;
-        const double* xv = x + 16 * bi + 8 * h;
+    for (int bj = 0; bj < 8; ++bj) {
+      double v[8];
+      ld_row8(rec_block(rec, zblk, hw, bj), r, v);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const int rr = 8 * h + k;
-          acc = fma(B[cc * 16 + (rr ^ cc)], xv[k], acc);
-        }
+      for (int k = 0; k < 8; k += 2) {
+        a0 = fma(v[k], x[8 * bj + k], a0);
+        a1 = fma(v[k + 1], x[8 * bj + k + 1], a1);
       }
     }
-    out[bj] = acc + __shfl_xor_sync(0xffffffffu, acc, 16);
+    (jj ? o1 : o0) = a0 + a1;
+  }
+}
+
+// Backward, columns map: acc[jj][k] += sum_bi L_tile(8 bi + r, 8 bj + k) * yv[bi]
+// for the lane's block-columns bj = g, 7 - g;  yv[bi] = x[8 bi + r].
+__device__ __forceinline__ void tile_bwd(const double* __restrict__ rec, const double* __restrict__ zblk, int r, int g,
+                                         const double yv[8], double (&acc)[2][8]) {
+  const unsigned long long* hcol = reinterpret_cast<const unsigned long long*>(rec) + 8;  // [bj][bi] bytes
+#pragma unroll
+  for (int jj = 0; jj < 2; ++jj) {
+    const unsigned long long hw = hcol[jj ? 7 - g : g];
+#pragma unroll
+    for (int bi = 0; bi < 8; ++bi) {
+      double v[8];
+      ld_row8(rec_block(rec, zblk, hw, bi), r, v);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc[jj][k] = fma(v[k], yv[bi], acc[jj][k]);
+    }
+  }
+}
+
+// Sum acc over the 8 row lanes sharing g (recursive halving, 14 shuffles).
+// The lane ends with columns c and c + 1 of the 64-column tile.
+__device__ __forceinline__ void reduce_cols(const double (&acc)[2][8], int lane, double& s0, double& s1, int& c) {
+  double w8[8], w4[4];
+  {
+    const bool up = lane & 4;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const double lo = acc[0][i], hi = acc[1][i];
+      w8[i] = (up ? hi : lo) + __shfl_xor_sync(0xffffffffu, up ? lo : hi, 4);
+    }
+  }
+  {
+    const bool up = lane & 2;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      w4[i] = (up ? w8[i + 4] : w8[i]) + __shfl_xor_sync(0xffffffffu, up ? w8[i] : w8[i + 4], 2);
+  }
+  const bool up = lane & 1;
+  s0 = (up ? w4[2] : w4[0]) + __shfl_xor_sync(0xffffffffu, up ? w4[0] : w4[2], 1);
+  s1 = (up ? w4[3] : w4[1]) + __shfl_xor_sync(0xffffffffu, up ? w4[1] : w4[3], 1);
+  const int g = lane >> 3, jj = (lane >> 2) & 1, k = 4 * ((lane >> 1) & 1) + 2 * (lane & 1);
+  c = 8 * (jj ? 7 - g : g) + k;
+}
+
+__device__ __forceinline__ void load_x(const double* __restrict__ x, double (&xr)[64]) {
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const double2 t = reinterpret_cast<const double2*>(x)[j];
+    xr[2 * j] = t.x;
+    xr[2 * j + 1] = t.y;
   }
 }
 
 // One CTA per patch.  A producer warp streams the patch's packed separator
-// factor (forward order, then backward by column) through a `stages`-deep
-// ring of 32 KB shared-memory slots with cp.async.bulk + mbarrier; eight
-// consumer warps run the sub-block GEMVs.  Output: the separator solution.
+// factor records (forward order, then backward by column) into a byte ring
+// of shared memory with cp.async.bulk; kRingEntries mbarrier pairs track the
+// records in flight, so the prefetch depth is set by bytes (~9 average
+// records in ~200 KB), not by the largest record.  Stream position q goes to
+// consumer warp q % 8 and ring entry q % 16: each entry is only ever waited
+// on by one warp, in order, so an mbarrier can never be two phases ahead of
+// its waiter.  The producer frees ring bytes in stream order (the oldest
+// record first).  Output: the separator solution.
+constexpr int kRingEntries = 16;
+
 __global__ void __launch_bounds__(kSolveThreads)
-    k_patch_solve(PatchArgs a, int stages, const double* __restrict__ rt, double* __restrict__ corr,
+    k_patch_solve(PatchArgs a, int ring_len, const double* __restrict__ rt, double* __restrict__ corr,
                   const double* __restrict__ tiles, const int32_t* __restrict__ pdofs,
                   const int32_t* __restrict__ col_start, const int32_t* __restrict__ tile_row,
-                  const int32_t* __restrict__ tile_mask, const int32_t* __restrict__ tile_poff) {
+                  const int32_t* __restrict__ rec_off) {
   extern __shared__ __align__(128) double sm[];
-  double* ring = sm;                          // stages x TT
-  double* y = ring + size_t(stages) * TT;     // mpad
+  double* ring = sm;                          // ring_len doubles
+  double* y = ring + ring_len;                // mpad
   double* part = y + a.mpad;                  // kSolveConsumers x T
-  uint64_t* full = reinterpret_cast<uint64_t*>(part + kSolveConsumers * T);
-  uint64_t* empty = full + stages;
+  double* zblk = part + kSolveConsumers * T;  // SB8 zeros (absent sub-blocks)
+  uint64_t* full = reinterpret_cast<uint64_t*>(zblk + SB8);
+  uint64_t* empty = full + kRingEntries;
+  int* slot_off = reinterpret_cast<int*>(empty + kRingEntries);  // ring offset of entry e's record
   const int j = blockIdx.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const double* tb = tiles + size_t(j) * a.ntiles * TT;
   if (tid == 0) {
-    for (int s = 0; s < stages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+    for (int e = 0; e < kRingEntries; ++e) {
+      mbar_init(&full[e], 1);
+      mbar_init(&empty[e], 1);
     }
     mbar_fence_init();
   }
@@ -548,13 +612,37 @@ __global__ void __launch_bounds__(kSolveThreads)
 
   if (warp == kSolveConsumers) {
     if (lane == 0) {
-      int q = 0;
+      int q = 0, qt = 0, head = 0;  // next position, oldest unreleased position, ring head
+      auto release_oldest = [&]() {
+        mbar_wait(&empty[qt & (kRingEntries - 1)], (qt / kRingEntries) & 1);
+        ++qt;
+      };
       auto issue = [&](int t) {
-        const int s = q % stages;
-        if (q >= stages) mbar_wait(&empty[s], ((q / stages) - 1) & 1);
-        const uint32_t bytes = uint32_t(__popc(tile_mask[t])) * SB * sizeof(double);
-        mbar_arrive_expect_tx(&full[s], bytes);
-        bulk_g2s(ring + size_t(s) * TT, tb + size_t(tile_poff[t]) * SB, bytes, &full[s]);
+        const int len = rec_off[t + 1] - rec_off[t];
+        while (q - qt >= kRingEntries) release_oldest();
+        for (;;) {  // find room at head (or at 0 after a wrap) by freeing the oldest records
+          if (qt == q) {
+            if (head + len > ring_len) head = 0;
+            break;
+          }
+          const int tail = slot_off[qt & (kRingEntries - 1)];
+          if (tail < head) {  // in flight: [tail, head)
+            if (head + len <= ring_len) break;
+            if (len <= tail) {
+              head = 0;
+              break;
+            }
+          } else if (tail > head && head + len <= tail) {  // in flight: [tail, end) + [0, head)
+            break;
+          }
+          release_oldest();
+        }
+        const int e = q & (kRingEntries - 1);
+        slot_off[e] = head;
+        const uint32_t bytes = uint32_t(len) * sizeof(double);
+        mbar_arrive_expect_tx(&full[e], bytes);
+        bulk_g2s(ring + head, tb + rec_off[t], bytes, &full[e]);
+        head += len;
         ++q;
       };
       for (int t = 0; t < a.ntiles; ++t) issue(t);
@@ -568,71 +656,88 @@ __global__ void __launch_bounds__(kSolveThreads)
   }
 
   constexpr int NC = 32 * kSolveConsumers;
-  const int rl = lane & 15, h = lane >> 4;
+  const int rl = lane & 7, g = lane >> 3;
+  // record of stream position q, after its bytes landed
+  auto acquire = [&](int q) {
+    const int e = q & (kRingEntries - 1);
+    mbar_wait(&full[e], (q / kRingEntries) & 1);
+    return ring + slot_off[e];
+  };
+  auto release = [&](int q) {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[q & (kRingEntries - 1)]);
+  };
   // ---- phase A: gather the Schur-reduced separator RHS (the interior elimination
   // was folded into the S^T cell kernel: bhat is patch independent) ----------------
   const int32_t* pdI = pdofs + size_t(j) * a.m;
   for (int r = tid; r < a.mpad; r += NC) y[r] = r < a.m ? rt[pdI[r]] : 0.0;
+  for (int r = tid; r < SB8; r += NC) zblk[r] = 0.0;
   named_sync(1, NC);
 
-  // Ring slot s = q % stages is owned by consumer warp s (stages <= 8), so
-  // every slot's fills are waited on by one warp, in order: the mbarrier
-  // parity can never be two phases ahead of its waiter.
   // ---- phase B: forward substitution over tile columns (y <- L_G^{-1} y) ----------------
   int q = 0;  // stream position, mirrors the producer
-  double o[4];
+  double o0, o1;
+  double xr[64];
   for (int K = 0; K < a.nT; ++K) {
     const int t0 = col_start[K], cnt = col_start[K + 1] - t0;
     double* yK = y + K * T;
-    if (warp == q % stages) {
-      const int s = q % stages;
-      mbar_wait(&full[s], (q / stages) & 1);
-      packed_fwd(ring + size_t(s) * TT, tile_mask[t0], yK, lane, o);  // L_KK^{-1} y_K
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-      if (h == 0) {
-#pragma unroll
-        for (int bi = 0; bi < 4; ++bi) yK[16 * bi + rl] = o[bi];
-      }
+    if (warp == (q & 7)) {
+      load_x(yK, xr);
+      const double* rec = acquire(q);
+      tile_fwd(rec, zblk, rl, g, xr, o0, o1);  // L_KK^{-1} y_K
+      release(q);
+      yK[8 * g + rl] = o0;
+      yK[8 * (7 - g) + rl] = o1;
     }
     ++q;
     named_sync(1, NC);
-    for (int i = 1; i < cnt; ++i, ++q) {
-      const int s = q % stages;
-      if (s != warp) continue;
-      mbar_wait(&full[s], (q / stages) & 1);
-      packed_fwd(ring + size_t(s) * TT, tile_mask[t0 + i], yK, lane, o);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-      if (h == 0) {
-        double* yI = y + tile_row[t0 + i] * T;
-#pragma unroll
-        for (int bi = 0; bi < 4; ++bi) yI[16 * bi + rl] -= o[bi];
-      }
+    int i = 1 + ((warp - q) & 7);  // this warp's first tile of the column
+    if (i < cnt) load_x(yK, xr);
+    for (; i < cnt; i += 8) {
+      const int qi = q + i - 1;
+      const double* rec = acquire(qi);
+      tile_fwd(rec, zblk, rl, g, xr, o0, o1);
+      release(qi);
+      double* yI = y + tile_row[t0 + i] * T;
+      yI[8 * g + rl] -= o0;
+      yI[8 * (7 - g) + rl] -= o1;
     }
+    q += cnt - 1;
     named_sync(1, NC);
   }
 
   // ---- phase C: backward substitution (x <- L_G^{-T} y), columns descending ---------------
+  double acc[2][8];
   for (int K = a.nT - 1; K >= 0; --K) {
     const int t0 = col_start[K], cnt = col_start[K + 1] - t0;
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int i = 1; i < cnt; ++i, ++q) {
-      const int s = q % stages;
-      if (s != warp) continue;
-      mbar_wait(&full[s], (q / stages) & 1);
-      packed_bwd(ring + size_t(s) * TT, tile_mask[t0 + i], y + tile_row[t0 + i] * T, lane, o);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
+    int i = 1 + ((warp - q) & 7);
+    if (i < cnt) {
 #pragma unroll
-      for (int bj = 0; bj < 4; ++bj) acc[bj] += o[bj];
-    }
-    if (h == 0) {
+      for (int jj = 0; jj < 2; ++jj)
 #pragma unroll
-      for (int bj = 0; bj < 4; ++bj) part[warp * T + 16 * bj + rl] = acc[bj];
+        for (int k = 0; k < 8; ++k) acc[jj][k] = 0.0;
+      for (; i < cnt; i += 8) {
+        const int qi = q + i - 1;
+        const double* yI = y + tile_row[t0 + i] * T;
+        double yv[8];
+#pragma unroll
+        for (int bi = 0; bi < 8; ++bi) yv[bi] = yI[8 * bi + rl];
+        const double* rec = acquire(qi);
+        tile_bwd(rec, zblk, rl, g, yv, acc);
+        release(qi);
+      }
+      double s0, s1;
+      int c;
+      reduce_cols(acc, lane, s0, s1, c);
+      part[warp * T + c] = s0;
+      part[warp * T + c + 1] = s1;
+    } else {
+      part[warp * T + lane] = 0.0;
+      part[warp * T + lane + 32] = 0.0;
     }
+    q += cnt - 1;
     named_sync(1, NC);
-    if (warp == q % stages) {
+    if (warp == (q & 7)) {
       double* yK = y + K * T;
       double u0 = yK[lane], u1 = yK[lane + 32];
       for (int w = 0; w < kSolveConsumers; ++w) {
@@ -642,15 +747,21 @@ __global__ void __launch_bounds__(kSolveThreads)
       yK[lane] = u0;
       yK[lane + 32] = u1;
       __syncwarp();
-      const int s = q % stages;
-      mbar_wait(&full[s], (q / stages) & 1);
-      packed_bwd(ring + size_t(s) * TT, tile_mask[t0], yK, lane, o);  // x_K = L_KK^{-T} y_K
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-      if (h == 0) {
+      double yv[8];
 #pragma unroll
-        for (int bj = 0; bj < 4; ++bj) yK[16 * bj + rl] = o[bj];
-      }
+      for (int bi = 0; bi < 8; ++bi) yv[bi] = yK[8 * bi + rl];
+#pragma unroll
+      for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc[jj][k] = 0.0;
+      const double* rec = acquire(q);
+      tile_bwd(rec, zblk, rl, g, yv, acc);  // x_K = L_KK^{-T} y_K
+      release(q);
+      double s0, s1;
+      int c;
+      reduce_cols(acc, lane, s0, s1, c);
+      yK[c] = s0;
+      yK[c + 1] = s1;
     }
     ++q;
     named_sync(1, NC);
@@ -719,29 +830,32 @@ void launch_patch_trsm(Context& c, int K) {
   FDM_LAUNCH_CHECK(c);
 }
 
-static int solve_stages(const Context& c, size_t* smem_out) {
-  const size_t fixed = sizeof(double) * (size_t(c.L.mpad) + kSolveConsumers * T);
+// Ring size (doubles) of the separator solve: all shared memory left after
+// the separator vector, the backward partials, the zero block and the barriers.
+static int solve_ring(const Context& c, size_t* smem_out) {
   const size_t budget = 227 * 1024;
-  int stages = kSolveConsumers;  // one ring slot per consumer warp at most
-  while (stages > 2 && fixed + stages * (sizeof(double) * TT + 16) > budget) --stages;
-  *smem_out = fixed + stages * sizeof(double) * TT + 2 * stages * sizeof(uint64_t);
-  if (*smem_out > budget) throw Error(FDMGPU_UNSUPPORTED, "separator too large for the shared-memory solve");
-  return stages;
+  const size_t fixed = sizeof(double) * (size_t(c.L.mpad) + kSolveConsumers * T + SB8) +
+                       2 * kRingEntries * sizeof(uint64_t) + kRingEntries * sizeof(int);
+  int max_rec = 0;
+  for (int t = 0; t < c.L.ntiles; ++t) max_rec = std::max(max_rec, c.L.tile_poff8[t + 1] - c.L.tile_poff8[t]);
+  const int ring = fixed < budget ? int(((budget - fixed) / sizeof(double)) & ~size_t(15)) : 0;
+  if (ring < max_rec) throw Error(FDMGPU_UNSUPPORTED, "separator too large for the shared-memory solve");
+  *smem_out = fixed + size_t(ring) * sizeof(double);
+  return ring;
 }
 
 void launch_patch_solve(Context& c, const double* r_modal) {
   PatchArgs a = make_args(c);
   size_t smem = 0;
-  const int stages = solve_stages(c, &smem);
+  const int ring = solve_ring(c, &smem);
   static bool attr = false;
   if (!attr) {
     FDM_CUDA(cudaFuncSetAttribute(k_patch_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr = true;
   }
   KernelTimer timer(c, 0);
-  k_patch_solve<<<c.npatch, kSolveThreads, smem, c.stream>>>(a, stages, r_modal, c.corr.p, c.tiles.p, c.pdofs.p,
-                                                              c.col_start.p, c.tile_row.p, c.tile_mask.p,
-                                                              c.tile_poff.p);
+  k_patch_solve<<<c.npatch, kSolveThreads, smem, c.stream>>>(a, ring, r_modal, c.corr.p, c.tiles.p, c.pdofs.p,
+                                                              c.col_start.p, c.tile_row.p, c.tile_poff8.p);
   FDM_LAUNCH_CHECK(c);
 }
 
@@ -752,7 +866,7 @@ void launch_patch_pack(Context& c) {
     FDM_CUDA(cudaFuncSetAttribute(k_patch_pack, cudaFuncAttributeMaxDynamicSharedMemorySize, int(2 * TT * sizeof(double))));
     attr = true;
   }
-  k_patch_pack<<<c.npatch, 512, 2 * TT * sizeof(double), c.stream>>>(c.L.ntiles, c.tile_mask.p, c.tile_poff.p, c.tiles.p);
+  k_patch_pack<<<c.npatch, 512, 2 * TT * sizeof(double), c.stream>>>(c.L.ntiles, c.tile_mask8.p, c.tile_poff8.p, c.tile_hdr.p, c.tiles.p);
   FDM_LAUNCH_CHECK(c);
 }
 

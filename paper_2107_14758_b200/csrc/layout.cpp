@@ -181,7 +181,7 @@ void analyze_patches(Context& c, int npatch, const int32_t* vertex, const int64_
   const char* dbg_env = std::getenv("FDMGPU_DEBUG");
   const bool dbg = dbg_env && dbg_env[0] == '1';
   std::vector<uint8_t> m32(dbg ? size_t(L.mpad / 32) * (L.mpad / 32) : 0), m16(size_t(L.mpad / 16) * (L.mpad / 16), 0);
-  std::vector<uint8_t> m8(dbg ? size_t(L.mpad / 8) * (L.mpad / 8) : 0);
+  std::vector<uint8_t> m8(size_t(L.mpad / 8) * (L.mpad / 8), 0);
   int64_t nnz_sep = 0;
   int stamp = 0;
   // All structural neighbours (any position) of position k in the canonical
@@ -248,10 +248,8 @@ void analyze_patches(Context& c, int npatch, const int32_t* vertex, const int64_
           tmark[size_t((k - L.nI) / T) * L.nT + (jj - L.nI) / T] = 1;
           ++nnz_sep;
           m16[size_t((k - L.nI) / 16) * (L.mpad / 16) + (jj - L.nI) / 16] = 1;
-          if (dbg) {
-            m32[size_t((k - L.nI) / 32) * (L.mpad / 32) + (jj - L.nI) / 32] = 1;
-            m8[size_t((k - L.nI) / 8) * (L.mpad / 8) + (jj - L.nI) / 8] = 1;
-          }
+          m8[size_t((k - L.nI) / 8) * (L.mpad / 8) + (jj - L.nI) / 8] = 1;
+          if (dbg) m32[size_t((k - L.nI) / 32) * (L.mpad / 32) + (jj - L.nI) / 32] = 1;
         }
       }
     }
@@ -337,6 +335,35 @@ void analyze_patches(Context& c, int npatch, const int32_t* vertex, const int64_
       }
     L.tile_mask[t] = mask;
     L.tile_poff[t + 1] = L.tile_poff[t] + __builtin_popcount(unsigned(mask));
+  }
+  // 8x8 sub-block masks (bit bi*8 + bj) of the packed solve stream, same rule.
+  const int nb8 = L.mpad / 8;
+  L.tile_mask8.assign(L.ntiles, 0);
+  L.tile_poff8.assign(L.ntiles + 1, 0);
+  L.tile_hdr.assign(size_t(L.ntiles) * 128, 0);
+  for (int t = 0; t < L.ntiles; ++t) {
+    const int I = L.tile_row[t], K = L.tile_col[t];
+    uint64_t mask = 0;
+    for (int bi = 0; bi < 8; ++bi)
+      for (int bj = 0; bj < 8; ++bj) {
+        const bool on = I == K ? bi >= bj : m8[size_t(8 * I + bi) * nb8 + (8 * K + bj)] != 0;
+        if (on) mask |= uint64_t(1) << (bi * 8 + bj);
+      }
+    L.tile_mask8[t] = int64_t(mask);
+    // stream record: 16-double header (block index per sub-block, row-major
+    // then column-major, 0xff = structurally zero) + the present sub-blocks
+    uint8_t* hr = &L.tile_hdr[size_t(t) * 128];
+    int q = 0;
+    for (int b = 0; b < 64; ++b) {
+      const uint8_t v = (mask >> b) & 1 ? uint8_t(q++) : uint8_t(0xff);
+      hr[b] = v;                              // [bi*8 + bj]
+      hr[64 + (b & 7) * 8 + (b >> 3)] = v;    // [bj*8 + bi]
+    }
+    L.tile_poff8[t + 1] = L.tile_poff8[t] + 16 + 64 * q;
+    // the in-place compaction (k_patch_pack) needs every packed prefix to end
+    // before the next unpacked tile starts
+    if (int64_t(L.tile_poff8[t + 1]) > int64_t(t + 1) * T * T)
+      throw Error(FDMGPU_UNSUPPORTED, "separator factor too dense for the packed solve stream");
   }
   L.pair_ptr.push_back(0);
   for (int t = 0; t < L.ntiles; ++t) {
