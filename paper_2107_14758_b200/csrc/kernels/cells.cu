@@ -57,6 +57,20 @@ __device__ __forceinline__ void contract(int n1_rt, int npc, int axis, const dou
   }
 }
 
+struct PosId {
+  __device__ __forceinline__ int operator()(int o) const { return o; }
+};
+
+// Shared-memory layout of the line-blocked n1 = 16 kernels: 16-double rows
+// with their 16-byte chunks XOR-swizzled by the row index, so a thread
+// reading a whole row (4 x double2 per 8 lanes) and 16 threads writing one
+// element each of a row are both bank-conflict free.
+struct Pos16 {
+  __device__ __forceinline__ int operator()(int o) const {
+    return (o & ~15) | ((((o >> 1) & 7) ^ ((o >> 4) & 7)) << 1) | (o & 1);
+  }
+};
+
 struct CellFdm {
   int dim, n1, p, ni;     // ni = (p-1)^dim interior points
   const double* At;       // shared-memory copies, (p+1)^2 column-major
@@ -95,8 +109,8 @@ __device__ void compute_invD(const CellFdm& f) {
 }
 
 // u[facet point] -= sum_x A~_{f x} u[x] / D_x for the 2 dim faces of the cell.
-template <int N1C>
-__device__ void schur_faces(const CellFdm& f, double* u) {
+template <int N1C, class Pos = PosId>
+__device__ void schur_faces(const CellFdm& f, double* u, Pos P = Pos()) {
   const int n1c = N1C > 0 ? N1C : f.n1;
   const int pm = n1c - 2;
   int nt = 1;
@@ -126,16 +140,16 @@ __device__ void schur_faces(const CellFdm& f, double* u) {
 #pragma unroll
     for (int xa = 1; xa < (N1C > 0 ? N1C - 1 : 64); ++xa) {
       if (N1C == 0 && xa >= f.p) break;
-      acc = fma(f.At[e + n1c * xa] * u[lin0 + xa * stride_a], f.invD[ii0 + (xa - 1) * istride_a], acc);
+      acc = fma(f.At[e + n1c * xa] * u[P(lin0 + xa * stride_a)], f.invD[ii0 + (xa - 1) * istride_a], acc);
     }
-    u[lin0 + e * stride_a] -= coef * acc;
+    u[P(lin0 + e * stride_a)] -= coef * acc;
   }
 }
 
 // u[x] = (nK * b[x] - sum_{a, e} A~_{x, f(a,e)} u[f(a,e)]) / D_x for every interior x.
-template <int N1C>
+template <int N1C, class Pos = PosId>
 __device__ void recon_interior(const CellFdm& f, double* u, const double* __restrict__ rb,
-                               const int32_t* __restrict__ cd, double nK) {
+                               const int32_t* __restrict__ cd, double nK, Pos P = Pos()) {
   for (int ii = threadIdx.x; ii < f.ni; ii += blockDim.x) {
     int x[3];
     const int lin = interior_lat<N1C>(f, ii, x);
@@ -145,10 +159,10 @@ __device__ void recon_interior(const CellFdm& f, double* u, const double* __rest
       for (int b = 0; b < f.dim; ++b)
         if (b != a) coef *= f.Bt[x[b] * (f.n1 + 1)];
       const int base = lin - x[a] * s;
-      const double fsum = f.At[x[a] + f.n1 * 0] * u[base] + f.At[x[a] + f.n1 * f.p] * u[base + f.p * s];
+      const double fsum = f.At[x[a] + f.n1 * 0] * u[P(base)] + f.At[x[a] + f.n1 * f.p] * u[P(base + f.p * s)];
       v -= coef * fsum;
     }
-    u[lin] = v * f.invD[ii];
+    u[P(lin)] = v * f.invD[ii];
   }
 }
 
@@ -336,6 +350,167 @@ __global__ void k_cells_stiffness(int dim, int n1, int npc, const double* __rest
   for (int l = threadIdx.x; l < npc; l += blockDim.x) e[l] = t0[l];
 }
 
+// ---- line-blocked n1 = 16, dim = 3 kernels (p = 15: C3, C4) ------------------
+// Every 1D contraction is a pass over the 256 lines of the current fastest
+// axis: thread r loads line r into registers (16 doubles), the CTA syncs, and
+// the thread writes out(k, r) = sum_j M(k, j) x_j to element r + 256 k, i.e.
+// the contracted index becomes the slowest one.  Three passes cycle the axes
+// back to the original order, each pass reads and writes the tile in place
+// (one 32 KB buffer per field), rows of M come from shared memory by
+// broadcast, and the FMA:load ratio is 16:1 instead of 1:2.
+constexpr int kL16 = 16, kNpc16 = 4096, kLines16 = 256;
+
+__device__ __forceinline__ void load_line16(const double* __restrict__ b, int r, double (&x)[16]) {
+  const double2* row = reinterpret_cast<const double2*>(b + 16 * r);
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const double2 t = row[c ^ (r & 7)];
+    x[2 * c] = t.x;
+    x[2 * c + 1] = t.y;
+  }
+}
+
+// sum_j Mrow[j] x[j] with Mrow 16 contiguous doubles (broadcast reads)
+__device__ __forceinline__ double dot16(const double* __restrict__ Mrow, const double (&x)[16]) {
+  const double2* m = reinterpret_cast<const double2*>(Mrow);
+  double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const double2 mm = m[c];
+    a0 = fma(mm.x, x[2 * c], a0);
+    a1 = fma(mm.y, x[2 * c + 1], a1);
+  }
+  return a0 + a1;
+}
+
+// Mt[j + 16 k] = M[k + 16 j]: row k of M contiguous
+__device__ __forceinline__ void load_rows16(double* __restrict__ Mt, const double* __restrict__ M) {
+  for (int i = threadIdx.x; i < kL16 * kL16; i += blockDim.x) Mt[(i >> 4) + 16 * (i & 15)] = M[i];
+}
+
+__global__ void __launch_bounds__(kLines16) k_cells_transform16(int dir, int flags, const double* __restrict__ in,
+                                                                 const double* __restrict__ aux, double* __restrict__ E,
+                                                                 const int32_t* __restrict__ cdofs,
+                                                                 const double* __restrict__ inv_mult,
+                                                                 const uint8_t* __restrict__ cons,
+                                                                 const double* __restrict__ sign,
+                                                                 const double* __restrict__ M, const double* __restrict__ mu,
+                                                                 const double* __restrict__ At,
+                                                                 const double* __restrict__ Bt,
+                                                                 const double* __restrict__ nK) {
+  extern __shared__ __align__(16) double sm[];
+  double* Mt = sm;               // 256
+  double* b = Mt + kL16 * kL16;  // 4096, Pos16 layout
+  double* tables = b + kNpc16;   // At, Bt, invD (only with flags)
+  const Pos16 P;
+  const int c = blockIdx.x, r = threadIdx.x;
+  load_rows16(Mt, M);
+  CellFdm f;
+  if (flags) load_cell_fdm(f, tables, 3, kL16, c, mu, At, Bt);
+  const int32_t* cd = cdofs + size_t(c) * kNpc16;
+#pragma unroll 4
+  for (int l = r; l < kNpc16; l += kLines16) {
+    const int g = cd[l];
+    double v = cons[g] ? 0.0 : in[g];
+    if (dir == 0)
+      v *= inv_mult[g];
+    else if (sign)
+      v *= sign[size_t(c) * kNpc16 + l];
+    b[P(l)] = v;
+  }
+  __syncthreads();
+  if (flags) {
+    compute_invD<kL16>(f);
+    __syncthreads();
+  }
+  if (flags & kRecon) {
+    recon_interior<kL16>(f, b, aux, cd, nK[c], P);
+    __syncthreads();
+  }
+  for (int pass = 0; pass < 3; ++pass) {
+    double x[16];
+    load_line16(b, r, x);
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kL16; ++k) b[P(r + kLines16 * k)] = dot16(Mt + 16 * k, x);
+    __syncthreads();
+  }
+  if (dir == 0 && sign) {
+    for (int l = r; l < kNpc16; l += kLines16) b[P(l)] *= sign[size_t(c) * kNpc16 + l];
+    __syncthreads();
+  }
+  if (flags & kSchur) {
+    schur_faces<kL16>(f, b, P);
+    __syncthreads();
+  }
+  double* e = E + size_t(c) * kNpc16;
+  for (int l = r; l < kNpc16; l += kLines16) e[l] = b[P(l)];
+}
+
+// Cartesian stiffness y_K = mu0 Bz By Ax u + mu1 Bz Ay Bx u + mu2 Az By Bx u in
+// three line passes over two in-place buffers:
+//   (Bx u, Ax u) -> (P = mu0 By Ax u + mu1 Ay Bx u, Q = By Bx u) -> y = Bz P + mu2 Az Q.
+__global__ void __launch_bounds__(kLines16) k_cells_stiffness16(const double* __restrict__ x, double* __restrict__ E,
+                                                                 const int32_t* __restrict__ cdofs,
+                                                                 const uint8_t* __restrict__ cons,
+                                                                 const double* __restrict__ mu,
+                                                                 const double* __restrict__ Ahat,
+                                                                 const double* __restrict__ Bhat) {
+  extern __shared__ __align__(16) double sm[];
+  double* As = sm;              // rows of A
+  double* Bs = As + kL16 * kL16;
+  double* b0 = Bs + kL16 * kL16;
+  double* b1 = b0 + kNpc16;
+  const Pos16 P;
+  const int c = blockIdx.x, r = threadIdx.x;
+  load_rows16(As, Ahat);
+  load_rows16(Bs, Bhat);
+  const int32_t* cd = cdofs + size_t(c) * kNpc16;
+#pragma unroll 4
+  for (int l = r; l < kNpc16; l += kLines16) {
+    const int g = cd[l];
+    b0[P(l)] = cons[g] ? 0.0 : x[g];
+  }
+  const double m0 = mu[size_t(c) * 3], m1 = mu[size_t(c) * 3 + 1], m2 = mu[size_t(c) * 3 + 2];
+  __syncthreads();
+  {
+    double u[16];
+    load_line16(b0, r, u);
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kL16; ++k) {
+      const int o = P(r + kLines16 * k);
+      b0[o] = dot16(Bs + 16 * k, u);
+      b1[o] = dot16(As + 16 * k, u);
+    }
+    __syncthreads();
+  }
+  {
+    double t0[16], t1[16];
+    load_line16(b0, r, t0);
+    load_line16(b1, r, t1);
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kL16; ++k) {
+      const int o = P(r + kLines16 * k);
+      b0[o] = m0 * dot16(Bs + 16 * k, t1) + m1 * dot16(As + 16 * k, t0);
+      b1[o] = dot16(Bs + 16 * k, t0);
+    }
+    __syncthreads();
+  }
+  {
+    double pp[16], qq[16];
+    load_line16(b0, r, pp);
+    load_line16(b1, r, qq);
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kL16; ++k) b0[P(r + kLines16 * k)] = dot16(Bs + 16 * k, pp) + m2 * dot16(As + 16 * k, qq);
+    __syncthreads();
+  }
+  double* e = E + size_t(c) * kNpc16;
+  for (int l = r; l < kNpc16; l += kLines16) e[l] = b0[P(l)];
+}
+
 // mode 0: apply_St (sum, project); 1: apply_S (sum * inv_mult, project);
 // 2: operator (sum; constrained rows y_i = x_i); 3: x + sum (project).
 __global__ void k_gather(int64_t ndof, int mode, const double* __restrict__ E, const int32_t* __restrict__ ptr,
@@ -368,6 +543,16 @@ int cell_threads(const Context& c) { return c.npc >= 1024 ? 512 : 256; }
 }  // namespace
 
 void launch_cells_transform_fused(Context& c, int dir, const double* in, int flags, const double* aux) {
+  if (c.n1 == kL16 && c.dim == 3) {
+    const size_t smem16 = sizeof(double) * (kL16 * kL16 + size_t(kNpc16)) + (flags ? fdm_tables_bytes(c) : 0);
+    set_smem(k_cells_transform16, smem16);
+    KernelTimer timer(c, 2);
+    k_cells_transform16<<<c.ncells, kLines16, smem16, c.stream>>>(
+        dir, flags, in, aux, c.E.p, dir == 0 ? c.cell_dofs.p : c.cell_modes.p, c.inv_mult.p, c.constrained.p,
+        c.mode_sign.p, dir == 0 ? c.St.p : c.S.p, c.mu.p, c.At.p, c.Bt.p, c.nK.p);
+    FDM_LAUNCH_CHECK(c);
+    return;
+  }
   const size_t smem = sizeof(double) * (size_t(c.n1) * c.n1 + 2 * size_t(c.npc)) + (flags ? fdm_tables_bytes(c) : 0);
   auto go = [&](auto kernel) {
     set_smem(kernel, smem);
@@ -413,6 +598,15 @@ void launch_gather(Context& c, int mode, const double* E, const double* x, doubl
 }
 
 void launch_cells_stiffness_kron(Context& c, const double* x) {
+  if (c.n1 == kL16 && c.dim == 3) {
+    const size_t smem16 = sizeof(double) * (2 * kL16 * kL16 + 2 * size_t(kNpc16));
+    set_smem(k_cells_stiffness16, smem16);
+    KernelTimer timer(c, 3);
+    k_cells_stiffness16<<<c.ncells, kLines16, smem16, c.stream>>>(x, c.E.p, c.cell_dofs.p, c.constrained.p, c.mu.p,
+                                                                   c.Ahat.p, c.Bhat.p);
+    FDM_LAUNCH_CHECK(c);
+    return;
+  }
   const size_t smem = sizeof(double) * (2 * size_t(c.n1) * c.n1 + 4 * size_t(c.npc));
   auto go = [&](auto kernel) {
     set_smem(kernel, smem);
