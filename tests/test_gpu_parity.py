@@ -20,7 +20,7 @@ pytestmark = pytest.mark.gpu
 TOL_RELAX = 1e-11
 TOL_TRANSFORM = 1e-12
 
-CASES = [(1, 0, 0), (2, 0, 0), (2, 3, 3), (1, 4, 5), (4, 4, 5), (3, 3, 5), (4, 0, 3)]
+CASES = [(1, 0, 0), (2, 0, 0), (2, 3, 3), (1, 4, 5), (4, 4, 5), (3, 3, 5), (4, 0, 3), (3, 2, 15), (4, 3, 15)]
 
 
 @pytest.fixture(scope="module")
