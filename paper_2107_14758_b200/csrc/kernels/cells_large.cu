@@ -136,78 +136,133 @@ __global__ void k_cell_recon_g(int dim, int n1, int npc, int ncells, double* __r
 }
 
 // ---- trilinear true-form operator, 3D -----------------------------------------
+// Every contraction is a small GEMM on shared-memory operands.  mgemm blocks
+// the M x N outputs RM x RN per thread (rows and columns strided by the block
+// counts, so a warp's lanes read consecutive elements) and evaluates NO
+// output fields that share operands in one k loop; `step` does the loads and
+// FMAs of one k for all fields.
+template <int RM, int RN, int NO, class Step, class Out>
+__device__ __forceinline__ void mgemm(int M, int N, int K, Step step, Out out) {
+  const int nbm = (M + RM - 1) / RM, nbn = (N + RN - 1) / RN;
+  for (int blk = threadIdx.x; blk < nbm * nbn; blk += blockDim.x) {
+    const int bm = blk / nbn, bn = blk - bm * nbn;
+    int mi[RM], nj[RN];
+#pragma unroll
+    for (int i = 0; i < RM; ++i) mi[i] = min(bm + i * nbm, M - 1);
+#pragma unroll
+    for (int j = 0; j < RN; ++j) nj[j] = min(bn + j * nbn, N - 1);
+    double acc[NO][RM][RN];
+#pragma unroll
+    for (int o = 0; o < NO; ++o)
+#pragma unroll
+      for (int i = 0; i < RM; ++i)
+#pragma unroll
+        for (int j = 0; j < RN; ++j) acc[o][i][j] = 0.0;
+#pragma unroll 4
+    for (int k = 0; k < K; ++k) step(k, mi, nj, acc);
+#pragma unroll
+    for (int o = 0; o < NO; ++o)
+#pragma unroll
+      for (int i = 0; i < RM; ++i)
+#pragma unroll
+        for (int j = 0; j < RN; ++j)
+          if (bm + i * nbm < M && bn + j * nbn < N) out(o, bm + i * nbm, bn + j * nbn, acc[o][i][j]);
+  }
+}
+
+constexpr int kQR = 2;  // register block (rows and columns) of the quadrature GEMMs
+
 // Stage 1: per (cell, z-level kz): t0 = V_x u, t1 = D_x u, then
 // T[c][0] = V_y t0 (-> d/dz path), T[c][1] = D_y t0 (d/dy), T[c][2] = V_y t1 (d/dx);
-// layout T[c][f][kz][qy][qx].
-__global__ void k_quad_stage1(int n1, int q, const double* __restrict__ x, const int32_t* __restrict__ cdofs,
-                              const uint8_t* __restrict__ cons, const double* __restrict__ Vq,
-                              const double* __restrict__ Dq, double* __restrict__ T) {
+// layout T[c][f][kz][qy][qx].  V, D: q x n1 column-major (V[qx + q i]).
+__global__ void __launch_bounds__(256, 3) k_quad_stage1(int n1, int q, const double* __restrict__ x,
+                                                         const int32_t* __restrict__ cdofs,
+                                                         const uint8_t* __restrict__ cons,
+                                                         const double* __restrict__ Vq,
+                                                         const double* __restrict__ Dq, double* __restrict__ T) {
   extern __shared__ double sm[];
-  double* V = sm;              // q x n1, V[qi + q j]
+  double* V = sm;                  // q x n1
   double* D = V + q * n1;
-  double* u = D + q * n1;      // n1 x n1 slab, u[i + n1 j]
-  double* t0 = u + n1 * n1;    // q x n1, t0[qx + q j]
+  double* u = D + q * n1;          // u[i + (n1 + 1) j]
+  double* t0 = u + (n1 + 1) * n1;  // t0[qx + q j]
   double* t1 = t0 + q * n1;
   const int c = blockIdx.x / n1, kz = blockIdx.x % n1;
-  const int npc = n1 * n1 * n1, q2 = q * q;
+  const int npc = n1 * n1 * n1, q2 = q * q, su = n1 + 1;
   for (int i = threadIdx.x; i < q * n1; i += blockDim.x) {
     V[i] = Vq[i];
     D[i] = Dq[i];
   }
   const int32_t* cd = cdofs + size_t(c) * npc + size_t(kz) * n1 * n1;
-  for (int l = threadIdx.x; l < n1 * n1; l += blockDim.x) {
-    const int g = cd[l];
-    u[l] = cons[g] ? 0.0 : x[g];
-  }
+  staged_copy<4>(
+      n1 * n1, [&](int l) { const int g = cd[l]; return cons[g] ? 0.0 : x[g]; },
+      [&](int l, double v) { u[l % n1 + su * (l / n1)] = v; });
   __syncthreads();
-  for (int o = threadIdx.x; o < q * n1; o += blockDim.x) {
-    const int qx = o % q, j = o / q;
-    double s0 = 0.0, s1 = 0.0;
-    for (int i = 0; i < n1; ++i) {
-      const double ui = u[i + n1 * j];
-      s0 = fma(V[qx + q * i], ui, s0);
-      s1 = fma(D[qx + q * i], ui, s1);
-    }
-    t0[o] = s0;
-    t1[o] = s1;
-  }
+  mgemm<kQR, kQR, 2>(
+      n1, q, n1,
+      [&](int i, const int* mj, const int* nq, auto& acc) {
+        double a[kQR], bv[kQR], bd[kQR];
+#pragma unroll
+        for (int r = 0; r < kQR; ++r) a[r] = u[i + su * mj[r]];
+#pragma unroll
+        for (int r = 0; r < kQR; ++r) {
+          bv[r] = V[nq[r] + q * i];
+          bd[r] = D[nq[r] + q * i];
+        }
+#pragma unroll
+        for (int r = 0; r < kQR; ++r)
+#pragma unroll
+          for (int s2 = 0; s2 < kQR; ++s2) {
+            acc[0][r][s2] = fma(a[r], bv[s2], acc[0][r][s2]);
+            acc[1][r][s2] = fma(a[r], bd[s2], acc[1][r][s2]);
+          }
+      },
+      [&](int o, int j, int qx, double v) { (o ? t1 : t0)[qx + q * j] = v; });
   __syncthreads();
   double* out = T + size_t(c) * 3 * n1 * q2 + size_t(kz) * q2;
-  for (int o = threadIdx.x; o < q2; o += blockDim.x) {
-    const int qx = o % q, qy = o / q;
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-    for (int j = 0; j < n1; ++j) {
-      const double v = V[qy + q * j], d = D[qy + q * j];
-      a0 = fma(v, t0[qx + q * j], a0);
-      a1 = fma(d, t0[qx + q * j], a1);
-      a2 = fma(v, t1[qx + q * j], a2);
-    }
-    out[o] = a0;
-    out[size_t(n1) * q2 + o] = a1;
-    out[2 * size_t(n1) * q2 + o] = a2;
-  }
+  mgemm<kQR, kQR, 3>(
+      q, q, n1,
+      [&](int j, const int* my, const int* nx, auto& acc) {
+        double av[kQR], ad[kQR], b0[kQR], b1[kQR];
+#pragma unroll
+        for (int r = 0; r < kQR; ++r) {
+          av[r] = V[my[r] + q * j];
+          ad[r] = D[my[r] + q * j];
+          b0[r] = t0[nx[r] + q * j];
+          b1[r] = t1[nx[r] + q * j];
+        }
+#pragma unroll
+        for (int r = 0; r < kQR; ++r)
+#pragma unroll
+          for (int s2 = 0; s2 < kQR; ++s2) {
+            acc[0][r][s2] = fma(av[r], b0[s2], acc[0][r][s2]);
+            acc[1][r][s2] = fma(ad[r], b0[s2], acc[1][r][s2]);
+            acc[2][r][s2] = fma(av[r], b1[s2], acc[2][r][s2]);
+          }
+      },
+      [&](int o, int qy, int qx, double v) { out[size_t(o) * n1 * q2 + qx + q * qy] = v; });
 }
 
-constexpr int kQuadCols = 64;
-
-// Stage 2: per quadrature column (qx, qy): gradients g = (V_z T2, V_z T1, D_z T0),
-// f = w kappa G g with G = det J^{-1} J^{-T} of the trilinear map, then the
-// z-projection back into T in place: T0 <- V_z^T f_x, T1 <- V_z^T f_y, T2 <- D_z^T f_z.
-__global__ void k_quad_stage2(int n1, int q, double* __restrict__ T, const double* __restrict__ Vq,
-                              const double* __restrict__ Dq, const double* __restrict__ wq,
-                              const double* __restrict__ xyz, const double* __restrict__ kappa,
-                              const double* __restrict__ qpts) {
+// Stage 2: per (cell, qy): interpolate the three fields to the quadrature
+// points along z, g = (V_z T2, V_z T1, D_z T0) = (du/dxi, du/deta, du/dzeta);
+// f = w kappa G g with G = det J^{-1} J^{-T} of the trilinear map (Jacobian
+// from the 8 cell corners, src/geometry.cpp:33-43); project back in place:
+// T0 <- V_z^T f_x, T1 <- V_z^T f_y, T2 <- D_z^T f_z.
+__global__ void __launch_bounds__(256, 3) k_quad_stage2(int n1, int q, double* __restrict__ T,
+                                                         const double* __restrict__ Vq,
+                                                         const double* __restrict__ Dq,
+                                                         const double* __restrict__ wq,
+                                                         const double* __restrict__ xyz,
+                                                         const double* __restrict__ kappa,
+                                                         const double* __restrict__ qpts) {
   extern __shared__ double sm[];
   double* V = sm;
   double* D = V + q * n1;
-  double* W = D + q * n1;           // q weights, q points
-  double* X = W + 2 * q;            // 24 corner coordinates
-  double* col = X + 24;             // [3 * n1][kQuadCols]
-  double* fs = col + 3 * n1 * kQuadCols;  // [3 * q][kQuadCols]
+  double* W = D + q * n1;      // q weights, q points
+  double* X = W + 2 * q;       // 24 corner coordinates, X[3 b + r]
+  double* C = X + 24;          // C[f][kz][qx] (stride q)
+  double* G = C + 3 * n1 * q;  // g / f [field][qz][qx]
+  const int c = blockIdx.x / q, qy = blockIdx.x % q;
   const int q2 = q * q;
-  const int chunks = (q2 + kQuadCols - 1) / kQuadCols;
-  const int c = blockIdx.x / chunks;
-  const int cc = (blockIdx.x % chunks) * kQuadCols + threadIdx.x;
   for (int i = threadIdx.x; i < q * n1; i += blockDim.x) {
     V[i] = Vq[i];
     D[i] = Dq[i];
@@ -217,77 +272,134 @@ __global__ void k_quad_stage2(int n1, int q, double* __restrict__ T, const doubl
     W[q + i] = qpts[i];
   }
   for (int i = threadIdx.x; i < 24; i += blockDim.x) X[i] = xyz[size_t(c) * 24 + i];
+  double* base = T + size_t(c) * 3 * n1 * q2 + size_t(qy) * q;
+  staged_copy<8>(
+      3 * n1 * q, [&](int i) { const int fk = i / q; return base[size_t(fk) * q2 + (i - fk * q)]; },
+      [&](int i, double v) { C[i] = v; });
   __syncthreads();
-  if (cc >= q2) return;
-  const int tid = threadIdx.x;
-  const int qx = cc % q, qy = cc / q;
-  double* base = T + size_t(c) * 3 * n1 * q2 + cc;
-  for (int f = 0; f < 3; ++f)
-    for (int k = 0; k < n1; ++k) col[(f * n1 + k) * kQuadCols + tid] = base[(size_t(f) * n1 + k) * q2];
-  const double kap = kappa[c];
-  const double xh0 = W[q + qx], xh1 = W[q + qy];
-  for (int qz = 0; qz < q; ++qz) {
-    double g0 = 0.0, g1 = 0.0, g2 = 0.0;
-    for (int k = 0; k < n1; ++k) {
-      const double v = V[qz + q * k], d = D[qz + q * k];
-      g0 = fma(v, col[(2 * n1 + k) * kQuadCols + tid], g0);
-      g1 = fma(v, col[(1 * n1 + k) * kQuadCols + tid], g1);
-      g2 = fma(d, col[(0 * n1 + k) * kQuadCols + tid], g2);
-    }
-    // Jacobian of the trilinear map (src/geometry.cpp:33-43), J[r][a]
-    const double xh[3] = {xh0, xh1, W[q + qz]};
-    double J[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
-    for (int b = 0; b < 8; ++b) {
-      double dphi[3];
-      for (int a = 0; a < 3; ++a) {
-        double gg = 1.0;
-        for (int e = 0; e < 3; ++e) {
-          const bool hi = (b >> e) & 1;
-          gg *= (e == a) ? (hi ? 0.5 : -0.5) : (hi ? 0.5 * (1.0 + xh[e]) : 0.5 * (1.0 - xh[e]));
+  mgemm<kQR, kQR, 3>(
+      q, q, n1,
+      [&](int k, const int* mz, const int* nx, auto& acc) {
+        double av[kQR], ad[kQR], c0[kQR], c1[kQR], c2[kQR];
+#pragma unroll
+        for (int r = 0; r < kQR; ++r) {
+          av[r] = V[mz[r] + q * k];
+          ad[r] = D[mz[r] + q * k];
+          c0[r] = C[k * q + nx[r]];
+          c1[r] = C[(n1 + k) * q + nx[r]];
+          c2[r] = C[(2 * n1 + k) * q + nx[r]];
         }
-        dphi[a] = gg;
+#pragma unroll
+        for (int r = 0; r < kQR; ++r)
+#pragma unroll
+          for (int s2 = 0; s2 < kQR; ++s2) {
+            acc[0][r][s2] = fma(av[r], c2[s2], acc[0][r][s2]);
+            acc[1][r][s2] = fma(av[r], c1[s2], acc[1][r][s2]);
+            acc[2][r][s2] = fma(ad[r], c0[s2], acc[2][r][s2]);
+          }
+      },
+      [&](int o, int qz, int qx, double v) { G[o * q2 + qz * q + qx] = v; });
+  __syncthreads();
+  // Jacobian columns of the trilinear map x = sum_b N_b(xi) X_b at (xi_x, xi_y, xi_z),
+  // xi_y fixed per block:  col0 depends on (xi_y, xi_z), col2 on (xi_x, xi_y),
+  // col1 = h0(xi_z) al(xi_x) + h1(xi_z) be(xi_x) -- tables in shared memory.
+  {
+    double* J0 = C;             // [qz][3]   (C is free after the interpolation)
+    double* J2 = J0 + 3 * q;    // [qx][3]
+    double* AL = J2 + 3 * q;    // [qx][3]
+    double* BE = AL + 3 * q;    // [qx][3]
+    const double ey = W[q + qy];
+    const double hy[2] = {0.5 * (1.0 - ey), 0.5 * (1.0 + ey)};
+    for (int i = threadIdx.x; i < q; i += blockDim.x) {
+      const double t = W[q + i];
+      const double h[2] = {0.5 * (1.0 - t), 0.5 * (1.0 + t)};
+      for (int r = 0; r < 3; ++r) {
+        double j0 = 0.0, j2 = 0.0, al = 0.0, be = 0.0;
+        for (int u = 0; u < 2; ++u)
+          for (int v = 0; v < 2; ++v) {
+            // d/dxi_x at (xi_y = ey, xi_z = t): corners b = 1 + 2u + 4v minus b = 2u + 4v
+            j0 += hy[u] * h[v] * 0.5 * (X[3 * (1 + 2 * u + 4 * v) + r] - X[3 * (2 * u + 4 * v) + r]);
+            // d/dxi_z at (xi_x = t, xi_y = ey): corners b = u + 2v + 4 minus b = u + 2v
+            j2 += h[u] * hy[v] * 0.5 * (X[3 * (u + 2 * v + 4) + r] - X[3 * (u + 2 * v) + r]);
+          }
+        for (int u = 0; u < 2; ++u) {  // d/dxi_y at xi_x = t, split by the xi_z corner layer
+          al += h[u] * 0.5 * (X[3 * (u + 2) + r] - X[3 * u + r]);
+          be += h[u] * 0.5 * (X[3 * (u + 6) + r] - X[3 * (u + 4) + r]);
+        }
+        J0[3 * i + r] = j0;
+        J2[3 * i + r] = j2;
+        AL[3 * i + r] = al;
+        BE[3 * i + r] = be;
       }
-      for (int r = 0; r < 3; ++r)
-        for (int a = 0; a < 3; ++a) J[r][a] += dphi[a] * X[3 * b + r];
     }
-    const double det = J[0][0] * (J[1][1] * J[2][2] - J[1][2] * J[2][1]) -
-                       J[0][1] * (J[1][0] * J[2][2] - J[1][2] * J[2][0]) +
-                       J[0][2] * (J[1][0] * J[2][1] - J[1][1] * J[2][0]);
-    double inv[3][3];
-    for (int i = 0; i < 3; ++i)
-      for (int j = 0; j < 3; ++j) {
-        const int i1 = (j + 1) % 3, i2 = (j + 2) % 3, j1 = (i + 1) % 3, j2 = (i + 2) % 3;
-        inv[i][j] = (J[i1][j1] * J[i2][j2] - J[i1][j2] * J[i2][j1]) / det;
+    __syncthreads();
+    const double kap = kappa[c], wy = W[qy];
+    for (int pnt = threadIdx.x; pnt < q2; pnt += blockDim.x) {
+      const int qz = pnt / q, qx = pnt - qz * q;
+      const double tz = W[q + qz];
+      const double hz0 = 0.5 * (1.0 - tz), hz1 = 0.5 * (1.0 + tz);
+      double J[3][3];
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        J[r][0] = J0[3 * qz + r];
+        J[r][1] = hz0 * AL[3 * qx + r] + hz1 * BE[3 * qx + r];
+        J[r][2] = J2[3 * qx + r];
       }
-    double G[3][3];
-    for (int a = 0; a < 3; ++a)
-      for (int b = 0; b < 3; ++b) G[a][b] = det * (inv[a][0] * inv[b][0] + inv[a][1] * inv[b][1] + inv[a][2] * inv[b][2]);
-    const double w = W[qx] * W[qy] * W[qz] * kap;
-    const double g[3] = {g0, g1, g2};
-    for (int a = 0; a < 3; ++a) fs[(a * q + qz) * kQuadCols + tid] = w * (G[a][0] * g[0] + G[a][1] * g[1] + G[a][2] * g[2]);
-  }
-  for (int k = 0; k < n1; ++k) {
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-    for (int qz = 0; qz < q; ++qz) {
-      const double v = V[qz + q * k], d = D[qz + q * k];
-      a0 = fma(v, fs[(0 * q + qz) * kQuadCols + tid], a0);
-      a1 = fma(v, fs[(1 * q + qz) * kQuadCols + tid], a1);
-      a2 = fma(d, fs[(2 * q + qz) * kQuadCols + tid], a2);
+      // adj[i][j] = det * (J^{-1})[i][j]
+      double adj[3][3];
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          const int i1 = (j + 1) % 3, i2 = (j + 2) % 3, j1 = (i + 1) % 3, j2 = (i + 2) % 3;
+          adj[i][j] = J[i1][j1] * J[i2][j2] - J[i1][j2] * J[i2][j1];
+        }
+      const double det = J[0][0] * adj[0][0] + J[0][1] * adj[1][0] + J[0][2] * adj[2][0];
+      // f = w kappa det J^{-1} J^{-T} g = (w kappa / det) adj (adj^T g)
+      const double g[3] = {G[pnt], G[q2 + pnt], G[2 * q2 + pnt]};
+      double hv[3];
+#pragma unroll
+      for (int r = 0; r < 3; ++r) hv[r] = adj[0][r] * g[0] + adj[1][r] * g[1] + adj[2][r] * g[2];
+      const double sc = W[qx] * wy * W[qz] * kap / det;
+#pragma unroll
+      for (int a2 = 0; a2 < 3; ++a2) G[a2 * q2 + pnt] = sc * (adj[a2][0] * hv[0] + adj[a2][1] * hv[1] + adj[a2][2] * hv[2]);
     }
-    base[(size_t(0) * n1 + k) * q2] = a0;  // x-gradient path
-    base[(size_t(1) * n1 + k) * q2] = a1;  // y
-    base[(size_t(2) * n1 + k) * q2] = a2;  // z
   }
+  __syncthreads();
+  mgemm<kQR, kQR, 3>(
+      n1, q, q,
+      [&](int qz, const int* mk, const int* nx, auto& acc) {
+        double av[kQR], ad[kQR], f0[kQR], f1[kQR], f2[kQR];
+#pragma unroll
+        for (int r = 0; r < kQR; ++r) {
+          av[r] = V[qz + q * mk[r]];
+          ad[r] = D[qz + q * mk[r]];
+          f0[r] = G[qz * q + nx[r]];
+          f1[r] = G[q2 + qz * q + nx[r]];
+          f2[r] = G[2 * q2 + qz * q + nx[r]];
+        }
+#pragma unroll
+        for (int r = 0; r < kQR; ++r)
+#pragma unroll
+          for (int s2 = 0; s2 < kQR; ++s2) {
+            acc[0][r][s2] = fma(av[r], f0[s2], acc[0][r][s2]);
+            acc[1][r][s2] = fma(av[r], f1[s2], acc[1][r][s2]);
+            acc[2][r][s2] = fma(ad[r], f2[s2], acc[2][r][s2]);
+          }
+      },
+      [&](int o, int k, int qx, double v) { base[size_t(o * n1 + k) * q2 + qx] = v; });
 }
 
 // Stage 3: per (cell, kz): b0 = V_y^T T0, b12 = D_y^T T1 + V_y^T T2,
 // E = D_x^T b0 + V_x^T b12.
-__global__ void k_quad_stage3(int n1, int q, const double* __restrict__ T, const double* __restrict__ Vq,
-                              const double* __restrict__ Dq, double* __restrict__ E) {
+__global__ void __launch_bounds__(256, 3) k_quad_stage3(int n1, int q, const double* __restrict__ T,
+                                                         const double* __restrict__ Vq,
+                                                         const double* __restrict__ Dq, double* __restrict__ E) {
   extern __shared__ double sm[];
   double* V = sm;
   double* D = V + q * n1;
-  double* b0 = D + q * n1;   // q x n1: b0[qx + q j]
+  double* P = D + q * n1;      // 3 planes [f][qy][qx]
+  double* b0 = P + 3 * q * q;  // b0[qx + q j]
   double* b12 = b0 + q * n1;
   const int c = blockIdx.x / n1, kz = blockIdx.x % n1;
   const int q2 = q * q;
@@ -295,28 +407,280 @@ __global__ void k_quad_stage3(int n1, int q, const double* __restrict__ T, const
     V[i] = Vq[i];
     D[i] = Dq[i];
   }
-  __syncthreads();
   const double* in = T + size_t(c) * 3 * n1 * q2 + size_t(kz) * q2;
-  for (int o = threadIdx.x; o < q * n1; o += blockDim.x) {
-    const int qx = o % q, j = o / q;
-    double s0 = 0.0, s12 = 0.0;
-    for (int qy = 0; qy < q; ++qy) {
-      const double v = V[qy + q * j], d = D[qy + q * j];
-      s0 = fma(v, in[qx + q * qy], s0);
-      s12 = fma(d, in[size_t(n1) * q2 + qx + q * qy], s12);
-      s12 = fma(v, in[2 * size_t(n1) * q2 + qx + q * qy], s12);
-    }
-    b0[o] = s0;
-    b12[o] = s12;
-  }
+  staged_copy<8>(
+      3 * q2, [&](int i) { const int f = i / q2; return in[size_t(f) * n1 * q2 + (i - f * q2)]; },
+      [&](int i, double v) { P[i] = v; });
+  __syncthreads();
+  mgemm<kQR, kQR, 2>(
+      n1, q, q,
+      [&](int qy, const int* mj, const int* nx, auto& acc) {
+        double av[kQR], ad[kQR], p0[kQR], p1[kQR], p2[kQR];
+#pragma unroll
+        for (int r = 0; r < kQR; ++r) {
+          av[r] = V[qy + q * mj[r]];
+          ad[r] = D[qy + q * mj[r]];
+          p0[r] = P[qy * q + nx[r]];
+          p1[r] = P[q2 + qy * q + nx[r]];
+          p2[r] = P[2 * q2 + qy * q + nx[r]];
+        }
+#pragma unroll
+        for (int r = 0; r < kQR; ++r)
+#pragma unroll
+          for (int s2 = 0; s2 < kQR; ++s2) {
+            acc[0][r][s2] = fma(av[r], p0[s2], acc[0][r][s2]);
+            acc[1][r][s2] = fma(ad[r], p1[s2], acc[1][r][s2]);
+            acc[1][r][s2] = fma(av[r], p2[s2], acc[1][r][s2]);
+          }
+      },
+      [&](int o, int j, int qx, double v) { (o ? b12 : b0)[qx + q * j] = v; });
   __syncthreads();
   double* out = E + size_t(c) * n1 * n1 * n1 + size_t(kz) * n1 * n1;
-  for (int o = threadIdx.x; o < n1 * n1; o += blockDim.x) {
-    const int i = o % n1, j = o / n1;
-    double s = 0.0;
-    for (int qx = 0; qx < q; ++qx) s = fma(D[qx + q * i], b0[qx + q * j], fma(V[qx + q * i], b12[qx + q * j], s));
-    out[o] = s;
+  mgemm<kQR, kQR, 1>(
+      n1, n1, q,
+      [&](int qx, const int* mj, const int* ni, auto& acc) {
+        double a0[kQR], a12[kQR], bd[kQR], bv[kQR];
+#pragma unroll
+        for (int r = 0; r < kQR; ++r) {
+          a0[r] = b0[qx + q * mj[r]];
+          a12[r] = b12[qx + q * mj[r]];
+          bd[r] = D[qx + q * ni[r]];
+          bv[r] = V[qx + q * ni[r]];
+        }
+#pragma unroll
+        for (int r = 0; r < kQR; ++r)
+#pragma unroll
+          for (int s2 = 0; s2 < kQR; ++s2) acc[0][r][s2] = fma(a0[r], bd[s2], fma(a12[r], bv[s2], acc[0][r][s2]));
+      },
+      [&](int, int j, int i, double v) { out[i + n1 * j] = v; });
+}
+
+// ---- p = 31 (n1 = 32), 3D: slab-blocked transform ------------------------------
+// A 32^3 tile (256 KB) does not fit in shared memory, so the transform runs as
+//   T1  per (cell, 8 z-slabs): gather (+ FDM interior rebuild for S), contract
+//       x and y in shared memory (line passes as in the p = 15 kernels: thread
+//       per 32-point line in registers, contracted index written slowest, two
+//       passes cycle back), store the slabs to the E-vector;
+//   T2  per (cell, 8 y-planes): thread per z-line straight from E into
+//       registers, contract z, mode signs, interior elimination at the z- and
+//       x-faces (x-face sums are warp reductions: lanes run along x), store;
+//   T3  (S^T only) interior elimination at the y-faces, thread per y-line.
+// Interior-mode diagonal D = sum_q mu_q prod_b (A~ | B~)_{x_b x_b} is formed
+// from the 1D diagonals (separable), in the order of compute_invD.
+constexpr int kL32 = 32, kSlab32 = 1024, kNpc32 = 32768;
+
+__device__ __forceinline__ int pos32(int o) {
+  return (o & ~31) | ((((o >> 1) & 15) ^ ((o >> 5) & 7)) << 1) | (o & 1);
+}
+
+__device__ __forceinline__ void load_line32(const double* __restrict__ b, int r, double (&x)[32]) {
+  const double2* row = reinterpret_cast<const double2*>(b + 32 * r);
+#pragma unroll
+  for (int c = 0; c < 16; ++c) {
+    const double2 t = row[c ^ (r & 7)];
+    x[2 * c] = t.x;
+    x[2 * c + 1] = t.y;
   }
+}
+
+__device__ __forceinline__ double dot32(const double* __restrict__ Mrow, const double (&x)[32]) {
+  const double2* m = reinterpret_cast<const double2*>(Mrow);
+  double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+  for (int c = 0; c < 16; ++c) {
+    const double2 mm = m[c];
+    a0 = fma(mm.x, x[2 * c], a0);
+    a1 = fma(mm.y, x[2 * c + 1], a1);
+  }
+  return a0 + a1;
+}
+
+// 1D tables of the FDM interior algebra: diagonals of A~ / B~, the face rows
+// and columns of A~ (element (i, j) of the n1 x n1 column-major A~ is At[i + n1 j]).
+struct Fdm32 {
+  double ad[kL32], bd[kL32];  // A~_ii, B~_ii
+  double ac0[kL32], acp[kL32];  // A~_{i,0}, A~_{i,p}   (rebuild)
+  double ar0[kL32], arp[kL32];  // A~_{0,j}, A~_{p,j}   (elimination)
+};
+
+__device__ __forceinline__ void load_fdm32(Fdm32* t, const double* __restrict__ At, const double* __restrict__ Bt) {
+  for (int i = threadIdx.x; i < kL32; i += blockDim.x) {
+    t->ad[i] = At[i * (kL32 + 1)];
+    t->bd[i] = Bt[i * (kL32 + 1)];
+    t->ac0[i] = At[i];
+    t->acp[i] = At[i + kL32 * (kL32 - 1)];
+    t->ar0[i] = At[kL32 * i];
+    t->arp[i] = At[kL32 - 1 + kL32 * i];
+  }
+}
+
+__device__ __forceinline__ double diag32(const Fdm32& t, const double* mu, int x, int y, int z) {
+  double s = 0.0;
+  s += mu[0] * t.bd[z] * t.bd[y] * t.ad[x];
+  s += mu[1] * t.bd[z] * t.ad[y] * t.bd[x];
+  s += mu[2] * t.ad[z] * t.bd[y] * t.bd[x];
+  return s;
+}
+
+__device__ __forceinline__ void load_rows32(double* __restrict__ Mt, const double* __restrict__ M) {
+  for (int i = threadIdx.x; i < kL32 * kL32; i += blockDim.x) Mt[(i >> 5) + 32 * (i & 31)] = M[i];
+}
+
+__global__ void __launch_bounds__(256) k_cells_t1_32(int dir, int flags, const double* __restrict__ in,
+                                                      const double* __restrict__ aux, double* __restrict__ E,
+                                                      const int32_t* __restrict__ cdofs,
+                                                      const double* __restrict__ inv_mult,
+                                                      const uint8_t* __restrict__ cons,
+                                                      const double* __restrict__ sign, const double* __restrict__ M,
+                                                      const double* __restrict__ mu, const double* __restrict__ At,
+                                                      const double* __restrict__ Bt, const double* __restrict__ nK) {
+  extern __shared__ __align__(16) double sm[];
+  double* Mt = sm;                    // 1024
+  double* slab = Mt + kL32 * kL32;    // 8 x 1024, pos32 layout
+  double* zf = slab + 8 * kSlab32;    // 2 x 1024 (z = 0, z = p face planes; rebuild only)
+  Fdm32* t = reinterpret_cast<Fdm32*>(zf + 2 * kSlab32);
+  const int c = blockIdx.x >> 2, z0 = 8 * (blockIdx.x & 3);
+  const int tid = threadIdx.x;
+  const bool recon = dir == 1 && (flags & 2);
+  load_rows32(Mt, M);
+  if (recon) load_fdm32(t, At, Bt);
+  const int32_t* cd = cdofs + size_t(c) * kNpc32;
+  auto fetch = [&](int l) {
+    const int g = cd[l];
+    double v = cons[g] ? 0.0 : in[g];
+    if (dir == 0)
+      v *= inv_mult[g];
+    else if (sign)
+      v *= sign[size_t(c) * kNpc32 + l];
+    return v;
+  };
+#pragma unroll 4
+  for (int i = tid; i < 8 * kSlab32; i += 256) slab[(i & ~1023) + pos32(i & 1023)] = fetch(z0 * kSlab32 + i);
+  if (recon)
+    for (int i = tid; i < 2 * kSlab32; i += 256) zf[i] = fetch((i >> 10) * (kL32 - 1) * kSlab32 + (i & 1023));
+  __syncthreads();
+  if (recon) {
+    const double m[3] = {mu[size_t(c) * 3], mu[size_t(c) * 3 + 1], mu[size_t(c) * 3 + 2]};
+    const double nk = nK[c];
+    constexpr int pm = kL32 - 2;
+    for (int i = tid; i < 8 * pm * pm; i += 256) {
+      const int s = i / (pm * pm), z = z0 + s;
+      if (z == 0 || z == kL32 - 1) continue;
+      const int y = 1 + (i / pm) % pm, x = 1 + i % pm;
+      double* sl = slab + s * kSlab32;
+      const int o = x + 32 * y;
+      double v = nk * aux[cd[size_t(z) * kSlab32 + o]];
+      // faces along x, y (this slab) and z (the face planes), as recon_interior
+      const double cx = m[0] * t->bd[y] * t->bd[z];
+      v -= cx * (t->ac0[x] * sl[pos32(0 + 32 * y)] + t->acp[x] * sl[pos32(kL32 - 1 + 32 * y)]);
+      const double cy = m[1] * t->bd[x] * t->bd[z];
+      v -= cy * (t->ac0[y] * sl[pos32(x)] + t->acp[y] * sl[pos32(x + 32 * (kL32 - 1))]);
+      const double cz = m[2] * t->bd[x] * t->bd[y];
+      v -= cz * (t->ac0[z] * zf[o] + t->acp[z] * zf[kSlab32 + o]);
+      sl[pos32(o)] = v * (1.0 / diag32(*t, m, x, y, z));
+    }
+    __syncthreads();
+  }
+  double* sl = slab + (tid >> 5) * kSlab32;
+  const int r = tid & 31;
+  for (int pass = 0; pass < 2; ++pass) {
+    double x[32];
+    load_line32(sl, r, x);
+    __syncthreads();
+#pragma unroll 4
+    for (int k = 0; k < kL32; ++k) sl[pos32(r + 32 * k)] = dot32(Mt + 32 * k, x);
+    __syncthreads();
+  }
+  double* e = E + size_t(c) * kNpc32 + size_t(z0) * kSlab32;
+  for (int i = tid; i < 8 * kSlab32; i += 256) e[i] = slab[(i & ~1023) + pos32(i & 1023)];
+}
+
+__global__ void __launch_bounds__(256) k_cells_t2_32(int dir, int flags, double* __restrict__ E,
+                                                      const double* __restrict__ sign, const double* __restrict__ M,
+                                                      const double* __restrict__ mu, const double* __restrict__ At,
+                                                      const double* __restrict__ Bt) {
+  extern __shared__ __align__(16) double sm[];
+  double* Mt = sm;  // 1024
+  Fdm32* t = reinterpret_cast<Fdm32*>(Mt + kL32 * kL32);
+  const int c = blockIdx.x >> 2;
+  const int tid = threadIdx.x, x = tid & 31, y = 8 * (blockIdx.x & 3) + (tid >> 5);
+  const bool schur = dir == 0 && (flags & 1);
+  load_rows32(Mt, M);
+  if (schur) load_fdm32(t, At, Bt);
+  double* col = E + size_t(c) * kNpc32 + 32 * y + x;
+  double u[32];
+#pragma unroll
+  for (int z = 0; z < kL32; ++z) u[z] = col[size_t(z) * kSlab32];
+  __syncthreads();
+  double v[32];
+#pragma unroll
+  for (int k = 0; k < kL32; ++k) v[k] = dot32(Mt + 32 * k, u);
+  if (dir == 0 && sign) {
+    const double* sg = sign + size_t(c) * kNpc32 + 32 * y + x;
+#pragma unroll
+    for (int k = 0; k < kL32; ++k) v[k] *= sg[size_t(k) * kSlab32];
+  }
+  if (schur) {
+    const double m[3] = {mu[size_t(c) * 3], mu[size_t(c) * 3 + 1], mu[size_t(c) * 3 + 2]};
+    const bool yi = y > 0 && y < kL32 - 1, xi = x > 0 && x < kL32 - 1;
+    // w_z = v_z / D(x, y, z) on interior points (0 elsewhere)
+    double w[32];
+#pragma unroll
+    for (int z = 0; z < kL32; ++z)
+      w[z] = (xi && yi && z > 0 && z < kL32 - 1) ? v[z] * (1.0 / diag32(*t, m, x, y, z)) : 0.0;
+    // x faces (e, y, z): sum over the lanes (x) of A~_{e x} w
+    if (yi) {
+#pragma unroll
+      for (int z = 1; z < kL32 - 1; ++z) {
+        double s0 = t->ar0[x] * w[z], sp = t->arp[x] * w[z];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+          sp += __shfl_xor_sync(0xffffffffu, sp, o);
+        }
+        const double cx = m[0] * t->bd[y] * t->bd[z];
+        if (x == 0) v[z] -= cx * s0;
+        if (x == kL32 - 1) v[z] -= cx * sp;
+      }
+    }
+    // z faces (x, y, e): sum along the thread's own z-line
+    if (xi && yi) {
+      double s0 = 0.0, sp = 0.0;
+#pragma unroll
+      for (int z = 1; z < kL32 - 1; ++z) {
+        s0 = fma(t->ar0[z], w[z], s0);
+        sp = fma(t->arp[z], w[z], sp);
+      }
+      const double cz = m[2] * t->bd[x] * t->bd[y];
+      v[0] -= cz * s0;
+      v[kL32 - 1] -= cz * sp;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < kL32; ++k) col[size_t(k) * kSlab32] = v[k];
+}
+
+// y faces (x, e, z) for x, z interior: thread per y-line.
+__global__ void __launch_bounds__(256) k_cells_t3_32(double* __restrict__ E, const double* __restrict__ mu,
+                                                      const double* __restrict__ At, const double* __restrict__ Bt) {
+  __shared__ Fdm32 t;
+  const int c = blockIdx.x >> 2;
+  const int tid = threadIdx.x, x = tid & 31, z = 8 * (blockIdx.x & 3) + (tid >> 5);
+  load_fdm32(&t, At, Bt);
+  __syncthreads();
+  if (x == 0 || x == kL32 - 1 || z == 0 || z == kL32 - 1) return;
+  const double m[3] = {mu[size_t(c) * 3], mu[size_t(c) * 3 + 1], mu[size_t(c) * 3 + 2]};
+  double* row = E + size_t(c) * kNpc32 + size_t(z) * kSlab32 + x;
+  double s0 = 0.0, sp = 0.0;
+#pragma unroll 6
+  for (int y = 1; y < kL32 - 1; ++y) {
+    const double w = row[32 * y] * (1.0 / diag32(t, m, x, y, z));
+    s0 = fma(t.ar0[y], w, s0);
+    sp = fma(t.arp[y], w, sp);
+  }
+  const double cy = m[1] * t.bd[x] * t.bd[z];
+  row[0] -= cy * s0;
+  row[32 * (kL32 - 1)] -= cy * sp;
 }
 
 unsigned grid_for(int64_t total) {
@@ -409,18 +773,19 @@ void launch_cells_quadrature(Context& c, const double* x) {
   const size_t need = size_t(c.ncells) * 3 * n1 * q * q;
   if (c.Qbuf.n < need) c.Qbuf.alloc(need);
   KernelTimer timer(c, 3);
-  const size_t s1 = sizeof(double) * (2 * q * n1 + n1 * n1 + 2 * q * n1);
+  const size_t s1 = sizeof(double) * (4 * size_t(q) * n1 + size_t(n1 + 1) * n1);
+  const size_t s2 = sizeof(double) * (2 * size_t(q) * n1 + 2 * q + 24 + 3 * size_t(n1) * q + 3 * size_t(q) * q);
+  const size_t s3 = sizeof(double) * (4 * size_t(q) * n1 + 3 * size_t(q) * q);
+  if (s1 > 227 * 1024 || s2 > 227 * 1024 || s3 > 227 * 1024)
+    throw Error(FDMGPU_UNSUPPORTED, "true-form quadrature operator: p too large");
   FDM_CUDA(cudaFuncSetAttribute(k_quad_stage1, cudaFuncAttributeMaxDynamicSharedMemorySize, int(s1)));
   k_quad_stage1<<<c.ncells * n1, 256, s1, c.stream>>>(n1, q, x, c.cell_dofs.p, c.constrained.p, c.Vq.p, c.Dq.p,
                                                        c.Qbuf.p);
   FDM_LAUNCH_CHECK(c);
-  const int chunks = (q * q + kQuadCols - 1) / kQuadCols;
-  const size_t s2 = sizeof(double) * (2 * q * n1 + 2 * q + 24 + 3 * size_t(n1) * kQuadCols + 3 * size_t(q) * kQuadCols);
   FDM_CUDA(cudaFuncSetAttribute(k_quad_stage2, cudaFuncAttributeMaxDynamicSharedMemorySize, int(s2)));
-  k_quad_stage2<<<c.ncells * chunks, kQuadCols, s2, c.stream>>>(n1, q, c.Qbuf.p, c.Vq.p, c.Dq.p, c.wq.p, c.xyz.p,
-                                                                c.kappa.p, c.qpts.p);
+  k_quad_stage2<<<c.ncells * q, 256, s2, c.stream>>>(n1, q, c.Qbuf.p, c.Vq.p, c.Dq.p, c.wq.p, c.xyz.p, c.kappa.p,
+                                                      c.qpts.p);
   FDM_LAUNCH_CHECK(c);
-  const size_t s3 = sizeof(double) * (4 * q * n1);
   FDM_CUDA(cudaFuncSetAttribute(k_quad_stage3, cudaFuncAttributeMaxDynamicSharedMemorySize, int(s3)));
   k_quad_stage3<<<c.ncells * n1, 256, s3, c.stream>>>(n1, q, c.Qbuf.p, c.Vq.p, c.Dq.p, c.E.p);
   FDM_LAUNCH_CHECK(c);
@@ -443,9 +808,34 @@ void prepare_buffers(Context& c) {
   }
 }
 
+// p = 31 slab path (T1, T2, T3 above)
+static void launch_cells_transform_32(Context& c, int dir, const double* in, int flags, const double* aux) {
+  const double* M = dir == 0 ? c.St.p : c.S.p;
+  const int32_t* cd = dir == 0 ? c.cell_dofs.p : c.cell_modes.p;
+  const size_t s1 = sizeof(double) * (kL32 * kL32 + 10 * kSlab32) + sizeof(Fdm32);
+  const size_t s2 = sizeof(double) * kL32 * kL32 + sizeof(Fdm32);
+  static bool attr = false;
+  if (!attr) {
+    FDM_CUDA(cudaFuncSetAttribute(k_cells_t1_32, cudaFuncAttributeMaxDynamicSharedMemorySize, int(s1)));
+    attr = true;
+  }
+  KernelTimer timer(c, 2);
+  k_cells_t1_32<<<c.ncells * 4, 256, s1, c.stream>>>(dir, flags, in, aux, c.E.p, cd, c.inv_mult.p, c.constrained.p,
+                                                     c.mode_sign.p, M, c.mu.p, c.At.p, c.Bt.p, c.nK.p);
+  FDM_LAUNCH_CHECK(c);
+  k_cells_t2_32<<<c.ncells * 4, 256, s2, c.stream>>>(dir, flags, c.E.p, c.mode_sign.p, M, c.mu.p, c.At.p, c.Bt.p);
+  FDM_LAUNCH_CHECK(c);
+  if (dir == 0 && (flags & 1)) {
+    k_cells_t3_32<<<c.ncells * 4, 256, 0, c.stream>>>(c.E.p, c.mu.p, c.At.p, c.Bt.p);
+    FDM_LAUNCH_CHECK(c);
+  }
+}
+
 void launch_cells_transform(Context& c, int dir, const double* in, int flags, const double* aux) {
   if (cells_fit_smem(c))
     launch_cells_transform_fused(c, dir, in, flags, aux);
+  else if (c.n1 == kL32 && c.dim == 3 && !c.force_staged)
+    launch_cells_transform_32(c, dir, in, flags, aux);
   else
     launch_cells_transform_staged(c, dir, in, flags, aux);
 }

@@ -78,6 +78,25 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// Global -> shared staging with U loads in flight per thread (a plain loop
+// issues load, wait, store one element at a time).
+template <int U, class Ld, class St>
+__device__ __forceinline__ void staged_copy(int n, Ld ld, St st) {
+  for (int i0 = threadIdx.x; i0 < n; i0 += U * blockDim.x) {
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = i0 + u * blockDim.x;
+      v[u] = i < n ? ld(i) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = i0 + u * blockDim.x;
+      if (i < n) st(i, v[u]);
+    }
+  }
+}
+
 // Named barrier over `count` threads (multiple of 32).
 __device__ __forceinline__ void named_sync(int id, int count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");

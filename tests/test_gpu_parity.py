@@ -198,3 +198,25 @@ def test_smoke(torch):
     import __graft_entry__
 
     __graft_entry__.smoke()
+
+
+def test_p31_slab_path(pkg, oracle, torch):
+    # p = 31 (C5 shape, one patch): the slab-blocked transforms (T1/T2/T3) and the
+    # register-blocked quadrature operator against the oracle; the fused FDM
+    # interior elimination/rebuild inside smooth against the staged per-axis path
+    prob = pkg.Problem(5, 2, 31)
+    sol = pkg.Solver(prob)
+    sol.factor()
+    r = prob.rhs()
+    ref = oracle.Problem(5, 2, 31, build_global=True, threads=os.cpu_count())
+    assert rel(sol.apply_St(r), ref.apply_St(r)) <= TOL_TRANSFORM
+    assert rel(sol.apply_S(r), ref.apply_S(r)) <= TOL_TRANSFORM
+    assert rel(sol.apply_A(r), ref.apply_A(r)) <= TOL_TRANSFORM
+    z = sol.smooth(r)
+    os.environ["FDMGPU_FORCE_STAGED"] = "1"
+    try:
+        staged = pkg.Solver(prob)
+    finally:
+        del os.environ["FDMGPU_FORCE_STAGED"]
+    staged.factor()
+    assert rel(z, staged.smooth(r)) <= TOL_RELAX
