@@ -267,56 +267,106 @@ __device__ __forceinline__ void tile_gemm_abt(const double* __restrict__ A, cons
 
 // POTRF + triangular inverse of the 64x64 SPD tile in Dm (column-major, ld 65),
 // 256 threads; writes L^{-1} (lower, diag included) swizzled into `out`.
-// Cholesky: right-looking with the unscaled pivot column, one barrier per
-// step (column j-1 is scaled while step j updates the trailing matrix).
-// Inverse: each warp owns 8 columns of L^{-1}; 4 lanes per column split the
-// dot products of the row-by-row forward substitution (warp-synchronous).
+// Rank-4 blocked and register resident: thread t owns column c = t / 4, rows
+// r = 4 i + t % 4 (i < 16).  Per 4-column panel the owner warp factors the
+// panel in shared memory (Lp keeps all 16 panels, row-major by 4), one
+// barrier, then every thread applies the rank-4 update to its registers.
+// The inverse W = L^{-1} runs 4 rows at a time per column, warp local: the
+// column's 4 lanes finalise one row each (shuffles), then fold the block into
+// their running sums of the rows below (rotated so indices stay static).
 __device__ void diag_factor_invert(double* Dm, double* Wm, double* out, const PatchArgs& a, int K, int patch) {
   constexpr int LD = T + 1;
-  const int tid = threadIdx.x;
-  const int mc = tid >> 2, mr = tid & 3;  // thread owns column mc, rows mr + 4i
-  for (int j = 0; j <= T; ++j) {
-    if (j > 0 && tid > j - 1 && tid < T) {  // finish column j-1: L(:, j-1) = D(:, j-1) / sqrt(d)
-      const double d = Dm[(j - 1) * LD + (j - 1)];
-      Dm[(j - 1) * LD + tid] *= rsqrt(d > 0.0 ? d : 1.0);
-    }
-    if (j > 0 && tid == 0 && !(Dm[(j - 1) * LD + (j - 1)] > 0.0)) {
-      const int pos = K * T + (j - 1);
-      if (pos < a.m) record_pivot_error(a.err, patch, a.nI + pos);
-    }
-    if (j < T && mc > j) {  // trailing update with the unscaled column j: D(r,c) -= D(r,j) D(c,j) / d
-      double d = Dm[j * LD + j];
-      if (!(d > 0.0)) d = 1.0;
-      const double dcj = Dm[j * LD + mc] / d;
-      for (int r = mc + ((mr - mc) & 3); r < T; r += 4) Dm[mc * LD + r] -= Dm[j * LD + r] * dcj;
+  double* Lp = Wm + T * LD;        // [16][T][4]
+  double* rdiag = Lp + 16 * T * 4;  // [T]
+  const int tid = threadIdx.x, lane = tid & 31, c = tid >> 2, rq = tid & 3, warp = tid >> 5;
+  double v[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = Dm[c * LD + 4 * i + rq];
+#pragma unroll 1
+  for (int jb = 0; jb < 16; ++jb) {
+    const int j0 = 4 * jb;
+    double* P = Lp + size_t(jb) * T * 4;
+    if (warp == (jb >> 1)) {  // owner warp: columns j0..j0+3 are lanes 16 (jb & 1) .. + 15
+      if ((c >> 2) == jb) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) P[(4 * i + rq) * 4 + (c - j0)] = v[i];
+      }
+      __syncwarp();
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) {
+        const int j = j0 + jj;
+        double d = P[j * 4 + jj];
+        if (lane == 0 && !(d > 0.0)) {
+          const int pos = K * T + j;
+          if (pos < a.m) record_pivot_error(a.err, patch, a.nI + pos);
+        }
+        if (!(d > 0.0)) d = 1.0;
+        const double s = rsqrt(d);
+        __syncwarp();
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r = lane + 32 * h;
+          if (r > j) P[r * 4 + jj] *= s;
+          if (r == j) P[r * 4 + jj] = d * s;
+        }
+        if (lane == 0) rdiag[j] = s;
+        __syncwarp();
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r = lane + 32 * h;
+#pragma unroll
+          for (int j2 = jj + 1; j2 < 4; ++j2)
+            if (r >= j0 + j2) P[r * 4 + j2] -= P[r * 4 + jj] * P[(j0 + j2) * 4 + jj];
+        }
+        __syncwarp();
+      }
     }
     __syncthreads();
+    if (c >= j0 + 4) {  // rank-4 update of the thread's column (all rows; the upper part is unused)
+      const double4 lc = *reinterpret_cast<const double4*>(P + c * 4);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const double4 lr = *reinterpret_cast<const double4*>(P + (4 * i + rq) * 4);
+        v[i] = fma(-lr.x, lc.x, fma(-lr.y, lc.y, fma(-lr.z, lc.z, fma(-lr.w, lc.w, v[i]))));
+      }
+    }
   }
-  // diagonal: L(j,j) = sqrt(d); reciprocals for the inverse
-  double* rdiag = Wm + T * LD;  // T extra doubles after Wm
-  if (tid < T) {
-    const double d = Dm[tid * LD + tid];
-    const double l = sqrt(d > 0.0 ? d : 1.0);
-    Dm[tid * LD + tid] = l;
-    rdiag[tid] = 1.0 / l;
-  }
-  __syncthreads();
-  // Inverse: W(r, c) = (delta_rc - sum_{k=c}^{r-1} L(r,k) W(k,c)) / L(r,r), rows ascending.
-  const int warp = tid >> 5, lane = tid & 31;
-  const int c = 8 * warp + (lane >> 2), part = lane & 3;
-  for (int r = 0; r < T; ++r) {
-    double s = 0.0;
-    if (r > c)
-      for (int k = c + part; k < r; k += 4) s = fma(Dm[k * LD + r], Wm[c * LD + k], s);
-    s += __shfl_xor_sync(0xffffffffu, s, 1);
-    s += __shfl_xor_sync(0xffffffffu, s, 2);
-    if (part == 0 && r >= c) Wm[c * LD + r] = ((r == c ? 1.0 : 0.0) - s) * rdiag[r];
-    __syncwarp();
+  // inverse: W(k, c) = (delta_kc - sum_{c <= m < k} L(k, m) W(m, c)) / L(k, k)
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = 0.0;  // running sums of rows 4 (kb + i) + rq
+#pragma unroll 1
+  for (int kb = 0; kb < 16; ++kb) {
+    const double* P = Lp + size_t(kb) * T * 4;
+    double wv[4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const int k = 4 * kb + m;
+      double sum = v[0];
+#pragma unroll
+      for (int m2 = 0; m2 < m; ++m2) sum = fma(P[k * 4 + m2], wv[m2], sum);
+      const double my = ((k == c ? 1.0 : 0.0) - sum) * rdiag[k];
+      wv[m] = __shfl_sync(0xffffffffu, my, (lane & ~3) | m);
+    }
+    double mine = wv[0];
+#pragma unroll
+    for (int m = 1; m < 4; ++m) mine = rq == m ? wv[m] : mine;
+    Dm[c * LD + 4 * kb + rq] = mine;  // Dm is free: L lives in Lp
+#pragma unroll
+    for (int i = 1; i < 16; ++i) {
+      const int r = 4 * (kb + i) + rq;
+      if (r < T) {
+        const double4 l = *reinterpret_cast<const double4*>(P + r * 4);
+        v[i] = fma(l.x, wv[0], fma(l.y, wv[1], fma(l.z, wv[2], fma(l.w, wv[3], v[i]))));
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 15; ++i) v[i] = v[i + 1];
+    v[15] = 0.0;
   }
   __syncthreads();
   for (int e = tid; e < TT; e += blockDim.x) {
     const int r = e % T, cc = e / T;
-    out[tsw(r, cc)] = r >= cc ? Wm[cc * LD + r] : 0.0;
+    out[tsw(r, cc)] = r >= cc ? Dm[cc * LD + r] : 0.0;
   }
 }
 
