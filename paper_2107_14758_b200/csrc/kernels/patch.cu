@@ -554,22 +554,24 @@ __device__ __forceinline__ const double* rec_block(const double* rec, const doub
 __device__ __forceinline__ void tile_fwd(const double* __restrict__ rec, const double* __restrict__ zblk, int r, int g,
                                          const double (&x)[64], double& o0, double& o1) {
   const unsigned long long* hrow = reinterpret_cast<const unsigned long long*>(rec);  // [bi][bj] bytes
+  const unsigned long long hw0 = hrow[g], hw1 = hrow[7 - g];
+  double a[2][4];  // 4 independent chains per output row (both rows interleaved)
 #pragma unroll
-  for (int jj = 0; jj < 2; ++jj) {
-    const unsigned long long hw = hrow[jj ? 7 - g : g];
-    double a0 = 0.0, a1 = 0.0;
+  for (int jj = 0; jj < 2; ++jj)
 #pragma unroll
-    for (int bj = 0; bj < 8; ++bj) {
+    for (int k = 0; k < 4; ++k) a[jj][k] = 0.0;
+#pragma unroll
+  for (int bj = 0; bj < 8; ++bj) {
+#pragma unroll
+    for (int jj = 0; jj < 2; ++jj) {
       double v[8];
-      ld_row8(rec_block(rec, zblk, hw, bj), r, v);
+      ld_row8(rec_block(rec, zblk, jj ? hw1 : hw0, bj), r, v);
 #pragma unroll
-      for (int k = 0; k < 8; k += 2) {
-        a0 = fma(v[k], x[8 * bj + k], a0);
-        a1 = fma(v[k + 1], x[8 * bj + k + 1], a1);
-      }
+      for (int k = 0; k < 8; ++k) a[jj][k & 3] = fma(v[k], x[8 * bj + k], a[jj][k & 3]);
     }
-    (jj ? o1 : o0) = a0 + a1;
   }
+  o0 = (a[0][0] + a[0][1]) + (a[0][2] + a[0][3]);
+  o1 = (a[1][0] + a[1][1]) + (a[1][2] + a[1][3]);
 }
 
 // Backward, columns map: acc[jj][k] += sum_bi L_tile(8 bi + r, 8 bj + k) * yv[bi]
