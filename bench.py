@@ -262,6 +262,14 @@ def run_ours(args):
                "solve_s": rep["wall_time"], "calibrate_s": cal_s, "omega": cal["omega"]}
 
     hbm_peak, peak_src = measured_peaks()
+    traffic = None  # ncu dram bytes per launch (profiles/ncu_traffic.json, committed from a --set full capture)
+    try:
+        tr = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")))
+        ent = tr.get(str(args.config))
+        if ent and ent.get("kernel") == "k_patch_solve":
+            traffic = float(ent["dram_bytes_read"] + ent["dram_bytes_write"])
+    except (OSError, ValueError, KeyError):
+        traffic = None
     nnz_total = L["nnz_L_reference"] * L["npatch"]  # reference patch_ordering factor (SURVEY.md Bytes_relax)
     # separator columns of the factor the kernel streams (order in use; interior columns are never stored)
     nnz_sep = (L["nnz_L"] - (prob.dim + 1) * L["n_interior"]) * L["npatch"]
@@ -280,7 +288,7 @@ def run_ours(args):
                    "separator_dofs": L["n_interface"], "parallelism": "replicas" if world > 1 else "single",
                    "l2": f"inputs larger than L2: 2 x {L['stream_bytes'] / 1e9:.2f} GB packed patch factor streamed per step"},
         "roofline": {"kernel": "k_patch_solve", "bound": "hbm", "achieved": achieved, "peak": hbm_peak,
-                     "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": None,
+                     "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": traffic,
                      "peak_source": peak_src, "kernel_ms": kern_ms, "algorithmic_bytes": kern_bytes,
                      "share_of_step": solve_ms / ms if ms > 0 else None,
                      "bytes_def": "16 B x separator nnz(L_j) of the factor in use (fwd + bwd; plane-by-plane "
