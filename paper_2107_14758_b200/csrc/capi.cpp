@@ -547,6 +547,8 @@ fdmgpu_status fdmgpu_set_patches(fdmgpu_handle h, int32_t npatch, const int32_t*
     c.tile_mask8.upload(L.tile_mask8, c.stream);
     c.tile_poff8.upload(L.tile_poff8, c.stream);
     c.tile_hdr.upload(L.tile_hdr, c.stream);
+    c.lead_diag.upload(L.lead_diag, c.stream);
+    c.lead_trsm.upload(L.lead_trsm, c.stream);
     c.active.upload(L.active, c.stream);
     if (L.pair_a.empty()) {
       c.pair_a.alloc(1);
@@ -604,7 +606,8 @@ fdmgpu_status fdmgpu_factor(fdmgpu_handle h) {
     const unsigned long long none = ~0ULL;
     FDM_CUDA(cudaMemcpyAsync(c.d_err.p, &none, sizeof(none), cudaMemcpyHostToDevice, c.stream));
     fdmgpu::launch_patch_assemble(c);
-    for (int K = 0; K < c.L.nT; ++K) {
+    fdmgpu::launch_patch_lead(c);
+    for (int K = c.L.lead_cols; K < c.L.nT; ++K) {
       fdmgpu::launch_patch_update(c, K);
       fdmgpu::launch_patch_trsm(c, K);
     }

@@ -70,6 +70,8 @@ struct PatchLayout {
   std::vector<int32_t> tile_mask, tile_poff;  // 16x16 sub-blocks the factorisation touches per tile
   std::vector<int64_t> tile_mask8;            // 8x8 sub-blocks per tile kept in the solve stream
   std::vector<int32_t> tile_poff8;            // stream record offset (doubles): header + sub-blocks
+  int lead_cols = 0;                          // leading tile columns without updates (batched)
+  std::vector<int32_t> lead_diag, lead_trsm;  // their diagonal tiles; (tile, diagonal tile) pairs
   std::vector<uint8_t> tile_hdr;              // 128-byte record header per tile
   std::vector<int32_t> active, active_ptr;    // per column: tiles the update kernel must visit
   int64_t nnz_L = 0, flops_ref = 0, tile_gemms = 0;          // order in use
@@ -117,7 +119,7 @@ struct Context {
   int npatch = 0;
   PatchLayout L;
   DevArray<int32_t> pdofs, lat, pos_of_lat, pcells, pg_ptr, pg_idx;
-  DevArray<int32_t> tile_row, tile_col, col_start, pair_ptr, pair_a, pair_b, entries, tile_mask, tile_poff, active, tile_poff8;
+  DevArray<int32_t> tile_row, tile_col, col_start, pair_ptr, pair_a, pair_b, entries, tile_mask, tile_poff, active, tile_poff8, lead_diag, lead_trsm;
   DevArray<int64_t> tile_mask8;
   DevArray<uint8_t> tile_hdr;
   DevArray<double> corr, tiles, nK;
@@ -195,6 +197,7 @@ void launch_cells_quadrature(Context& c, const double* x);           // writes c
 void launch_patch_assemble(Context& c);
 void launch_patch_update(Context& c, int K);
 void launch_patch_trsm(Context& c, int K);
+void launch_patch_lead(Context& c);
 void launch_patch_pack(Context& c);
 void launch_patch_solve(Context& c, const double* r_modal);          // writes c.corr
 void launch_patch_gather(Context& c, double* z_modal);

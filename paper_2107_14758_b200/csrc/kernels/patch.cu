@@ -384,10 +384,11 @@ __global__ void __launch_bounds__(kUpdThreads) k_patch_update(PatchArgs a, int K
                                                                 const int32_t* __restrict__ tile_mask,
                                                                 double* __restrict__ tiles) {
   extern __shared__ __align__(128) double sm[];
-  double* buf = sm;                                   // [2 stages][A,B][TT]
-  uint64_t* full = reinterpret_cast<uint64_t*>(sm + 2 * kUpdStages * TT);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm);  // kUpdStages barriers
+  double* buf = sm + 16;                              // [stages][A,B][TT] (128-byte aligned)
   const int t = active[blockIdx.x], j = blockIdx.y;  // tiles of column K with work
   const int I = tile_row[t];
+  if (K < 0) K = I;  // batched leading columns: diagonal tiles without updates
   double* base = tiles + size_t(j) * a.ntiles * TT;
   const int p0 = pair_ptr[t], np = pair_ptr[t + 1] - p0;
   const int tid = threadIdx.x;
@@ -443,14 +444,16 @@ __global__ void __launch_bounds__(kUpdThreads) k_patch_update(PatchArgs a, int K
 
 // L(I,K) = C(I,K) L_KK^{-T} for the off-diagonal tiles of column K.
 __global__ void __launch_bounds__(kUpdThreads) k_patch_trsm(PatchArgs a, int K, const int32_t* __restrict__ col_start,
+                                                              const int32_t* __restrict__ lead,
                                                               const int32_t* __restrict__ tile_mask,
                                                               double* __restrict__ tiles) {
   extern __shared__ __align__(128) double sm[];
   double* Cs = sm;
   double* Ls = sm + TT;
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + 2 * TT);
-  const int t0 = col_start[K];
-  const int t = t0 + 1 + blockIdx.x, j = blockIdx.y;
+  // K < 0: batched leading columns, (tile, diagonal tile) pairs in `lead`
+  const int t0 = K >= 0 ? col_start[K] : lead[2 * blockIdx.x + 1];
+  const int t = K >= 0 ? t0 + 1 + blockIdx.x : lead[2 * blockIdx.x], j = blockIdx.y;
   double* base = tiles + size_t(j) * a.ntiles * TT;
   const int tid = threadIdx.x;
   if (tid == 0) {
@@ -852,7 +855,7 @@ void launch_patch_assemble(Context& c) {
 
 void launch_patch_update(Context& c, int K) {
   PatchArgs a = make_args(c);
-  const size_t smem = sizeof(double) * 2 * kUpdStages * TT + 64;
+  const size_t smem = sizeof(double) * (16 + 2 * kUpdStages * TT);
   static bool attr = false;
   if (!attr) {
     FDM_CUDA(cudaFuncSetAttribute(k_patch_update, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
@@ -864,6 +867,34 @@ void launch_patch_update(Context& c, int K) {
   k_patch_update<<<grid, kUpdThreads, smem, c.stream>>>(a, K, c.active.p + c.L.active_ptr[K], c.tile_row.p, c.pair_ptr.p,
                                                          c.pair_a.p, c.pair_b.p, c.tile_mask.p, c.tiles.p);
   FDM_LAUNCH_CHECK(c);
+}
+
+// Leading tile columns whose tiles receive no updates (the first separator
+// plane: its facets share no cell) are independent: factor all their diagonal
+// tiles in one launch (only the diagonal work area: 2 CTAs per SM), then all
+// their off-diagonal tiles in one triangular-solve launch.
+void launch_patch_lead(Context& c) {
+  if (c.L.lead_cols == 0) return;
+  PatchArgs a = make_args(c);
+  const size_t smem_d = sizeof(double) * (16 + 2 * size_t(T + 1) * T + 16 * T * 4 + T);
+  const size_t smem_t = sizeof(double) * 2 * TT + 64;
+  static bool attr = false;
+  if (!attr) {
+    FDM_CUDA(cudaFuncSetAttribute(k_patch_update, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(sizeof(double) * (16 + 2 * kUpdStages * TT))));
+    FDM_CUDA(cudaFuncSetAttribute(k_patch_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_t)));
+    attr = true;
+  }
+  KernelTimer timer(c, 1);
+  k_patch_update<<<dim3(c.L.lead_cols, c.npatch), kUpdThreads, smem_d, c.stream>>>(
+      a, -1, c.lead_diag.p, c.tile_row.p, c.pair_ptr.p, c.pair_a.p, c.pair_b.p, c.tile_mask.p, c.tiles.p);
+  FDM_LAUNCH_CHECK(c);
+  const int nt = int(c.L.lead_trsm.size() / 2);
+  if (nt > 0) {
+    k_patch_trsm<<<dim3(nt, c.npatch), kUpdThreads, smem_t, c.stream>>>(a, -1, c.col_start.p, c.lead_trsm.p,
+                                                                         c.tile_mask.p, c.tiles.p);
+    FDM_LAUNCH_CHECK(c);
+  }
 }
 
 void launch_patch_trsm(Context& c, int K) {
@@ -878,7 +909,7 @@ void launch_patch_trsm(Context& c, int K) {
   }
   dim3 grid(cnt, c.npatch);
   KernelTimer timer(c, 1);
-  k_patch_trsm<<<grid, kUpdThreads, smem, c.stream>>>(a, K, c.col_start.p, c.tile_mask.p, c.tiles.p);
+  k_patch_trsm<<<grid, kUpdThreads, smem, c.stream>>>(a, K, c.col_start.p, nullptr, c.tile_mask.p, c.tiles.p);
   FDM_LAUNCH_CHECK(c);
 }
 

@@ -387,6 +387,22 @@ void analyze_patches(Context& c, int npatch, const int32_t* vertex, const int64_
       if (L.tile_row[t] == K || L.pair_ptr[t + 1] > L.pair_ptr[t]) L.active.push_back(t);
     L.active_ptr.push_back(int32_t(L.active.size()));
   }
+  // leading columns with no updates at all (factorised in one batch, launch_patch_lead)
+  L.lead_cols = 0;
+  while (L.lead_cols < L.nT) {
+    const int K = L.lead_cols, t0 = L.col_start[K];
+    if (L.active_ptr[K + 1] - L.active_ptr[K] != 1 || L.pair_ptr[t0 + 1] > L.pair_ptr[t0]) break;
+    ++L.lead_cols;
+  }
+  L.lead_diag.clear();
+  L.lead_trsm.clear();
+  for (int K = 0; K < L.lead_cols; ++K) {
+    L.lead_diag.push_back(L.col_start[K]);
+    for (int t = L.col_start[K] + 1; t < L.col_start[K + 1]; ++t) {
+      L.lead_trsm.push_back(t);
+      L.lead_trsm.push_back(L.col_start[K]);
+    }
+  }
 
   // Structural nonzeros of the separator Schur complement S_G = A~_GG -
   // A~_GI D^-1 A~_IG (lower triangle), packed (tile << 12 | col << 6 | row):
