@@ -108,6 +108,18 @@ __device__ void compute_invD(const CellFdm& f) {
   }
 }
 
+// 1 / D_x from the interior point's coordinates (same product order as compute_invD);
+// used when f.invD is null (the p = 15 kernels keep the table out of shared memory).
+__device__ __forceinline__ double inv_diag(const CellFdm& f, const int* x) {
+  double s = 0.0;
+  for (int q = 0; q < f.dim; ++q) {
+    double prod = f.mu[q];
+    for (int b = f.dim - 1; b >= 0; --b) prod *= (b == q ? f.At : f.Bt)[x[b] * (f.n1 + 1)];
+    s += prod;
+  }
+  return 1.0 / s;
+}
+
 // u[facet point] -= sum_x A~_{f x} u[x] / D_x for the 2 dim faces of the cell.
 template <int N1C, class Pos = PosId>
 __device__ void schur_faces(const CellFdm& f, double* u, Pos P = Pos()) {
@@ -140,7 +152,14 @@ __device__ void schur_faces(const CellFdm& f, double* u, Pos P = Pos()) {
 #pragma unroll
     for (int xa = 1; xa < (N1C > 0 ? N1C - 1 : 64); ++xa) {
       if (N1C == 0 && xa >= f.p) break;
-      acc = fma(f.At[e + n1c * xa] * u[P(lin0 + xa * stride_a)], f.invD[ii0 + (xa - 1) * istride_a], acc);
+      double id;
+      if (f.invD) {
+        id = f.invD[ii0 + (xa - 1) * istride_a];
+      } else {
+        x[a] = xa;
+        id = inv_diag(f, x);
+      }
+      acc = fma(f.At[e + n1c * xa] * u[P(lin0 + xa * stride_a)], id, acc);
     }
     u[P(lin0 + e * stride_a)] -= coef * acc;
   }
@@ -162,7 +181,7 @@ __device__ void recon_interior(const CellFdm& f, double* u, const double* __rest
       const double fsum = f.At[x[a] + f.n1 * 0] * u[P(base)] + f.At[x[a] + f.n1 * f.p] * u[P(base + f.p * s)];
       v -= coef * fsum;
     }
-    u[P(lin)] = v * f.invD[ii];
+    u[P(lin)] = v * (f.invD ? f.invD[ii] : inv_diag(f, x));
   }
 }
 
@@ -388,7 +407,7 @@ __device__ __forceinline__ void load_rows16(double* __restrict__ Mt, const doubl
   for (int i = threadIdx.x; i < kL16 * kL16; i += blockDim.x) Mt[(i >> 4) + 16 * (i & 15)] = M[i];
 }
 
-__global__ void __launch_bounds__(kLines16) k_cells_transform16(int dir, int flags, const double* __restrict__ in,
+__global__ void __launch_bounds__(kLines16, 4) k_cells_transform16(int dir, int flags, const double* __restrict__ in,
                                                                  const double* __restrict__ aux, double* __restrict__ E,
                                                                  const int32_t* __restrict__ cdofs,
                                                                  const double* __restrict__ inv_mult,
@@ -401,28 +420,35 @@ __global__ void __launch_bounds__(kLines16) k_cells_transform16(int dir, int fla
   extern __shared__ __align__(16) double sm[];
   double* Mt = sm;               // 256
   double* b = Mt + kL16 * kL16;  // 4096, Pos16 layout
-  double* tables = b + kNpc16;   // At, Bt, invD (only with flags)
+  double* tables = b + kNpc16;   // At, Bt (only with flags; 1/D computed on the fly)
   const Pos16 P;
   const int c = blockIdx.x, r = threadIdx.x;
   load_rows16(Mt, M);
   CellFdm f;
-  if (flags) load_cell_fdm(f, tables, 3, kL16, c, mu, At, Bt);
+  if (flags) {
+    load_cell_fdm(f, tables, 3, kL16, c, mu, At, Bt);
+    f.invD = nullptr;
+  }
   const int32_t* cd = cdofs + size_t(c) * kNpc16;
-#pragma unroll 4
-  for (int l = r; l < kNpc16; l += kLines16) {
-    const int g = cd[l];
-    double v = cons[g] ? 0.0 : in[g];
-    if (dir == 0)
-      v *= inv_mult[g];
-    else if (sign)
-      v *= sign[size_t(c) * kNpc16 + l];
-    b[P(l)] = v;
+  // gather: all map loads first, then the independent value loads (no branch on
+  // the constraint flag, so in[g], cons[g] and the weight load in parallel)
+#pragma unroll 1
+  for (int h = 0; h < 2; ++h) {
+    int gi[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) gi[u] = cd[r + kLines16 * (8 * h + u)];
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int l = r + kLines16 * (8 * h + u), g = gi[u];
+      const double xv = in[g];
+      const double w = dir == 0 ? inv_mult[g] : (sign ? sign[size_t(c) * kNpc16 + l] : 1.0);
+      v[u] = cons[g] ? 0.0 : xv * w;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) b[P(r + kLines16 * (8 * h + u))] = v[u];
   }
   __syncthreads();
-  if (flags) {
-    compute_invD<kL16>(f);
-    __syncthreads();
-  }
   if (flags & kRecon) {
     recon_interior<kL16>(f, b, aux, cd, nK[c], P);
     __syncthreads();
@@ -466,10 +492,19 @@ __global__ void __launch_bounds__(kLines16) k_cells_stiffness16(const double* __
   load_rows16(As, Ahat);
   load_rows16(Bs, Bhat);
   const int32_t* cd = cdofs + size_t(c) * kNpc16;
-#pragma unroll 4
-  for (int l = r; l < kNpc16; l += kLines16) {
-    const int g = cd[l];
-    b0[P(l)] = cons[g] ? 0.0 : x[g];
+#pragma unroll 1
+  for (int h = 0; h < 2; ++h) {
+    int gi[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) gi[u] = cd[r + kLines16 * (8 * h + u)];
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const double xv = x[gi[u]];
+      v[u] = cons[gi[u]] ? 0.0 : xv;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) b0[P(r + kLines16 * (8 * h + u))] = v[u];
   }
   const double m0 = mu[size_t(c) * 3], m1 = mu[size_t(c) * 3 + 1], m2 = mu[size_t(c) * 3 + 2];
   __syncthreads();
@@ -544,7 +579,7 @@ int cell_threads(const Context& c) { return c.npc >= 1024 ? 512 : 256; }
 
 void launch_cells_transform_fused(Context& c, int dir, const double* in, int flags, const double* aux) {
   if (c.n1 == kL16 && c.dim == 3) {
-    const size_t smem16 = sizeof(double) * (kL16 * kL16 + size_t(kNpc16)) + (flags ? fdm_tables_bytes(c) : 0);
+    const size_t smem16 = sizeof(double) * (kL16 * kL16 + size_t(kNpc16) + (flags ? 2 * kL16 * kL16 : 0));
     set_smem(k_cells_transform16, smem16);
     KernelTimer timer(c, 2);
     k_cells_transform16<<<c.ncells, kLines16, smem16, c.stream>>>(
