@@ -136,110 +136,100 @@ __global__ void k_cell_recon_g(int dim, int n1, int npc, int ncells, double* __r
 }
 
 // ---- trilinear true-form operator, 3D -----------------------------------------
-// Every contraction is a small GEMM on shared-memory operands.  mgemm blocks
-// the M x N outputs RM x RN per thread (rows and columns strided by the block
-// counts, so a warp's lanes read consecutive elements) and evaluates NO
-// output fields that share operands in one k loop; `step` does the loads and
-// FMAs of one k for all fields.
-template <int RM, int RN, int NO, class Step, class Out>
-__device__ __forceinline__ void mgemm(int M, int N, int K, Step step, Out out) {
-  const int nbm = (M + RM - 1) / RM, nbn = (N + RN - 1) / RN;
-  for (int blk = threadIdx.x; blk < nbm * nbn; blk += blockDim.x) {
-    const int bm = blk / nbn, bn = blk - bm * nbn;
-    int mi[RM], nj[RN];
-#pragma unroll
-    for (int i = 0; i < RM; ++i) mi[i] = min(bm + i * nbm, M - 1);
-#pragma unroll
-    for (int j = 0; j < RN; ++j) nj[j] = min(bn + j * nbn, N - 1);
-    double acc[NO][RM][RN];
-#pragma unroll
-    for (int o = 0; o < NO; ++o)
-#pragma unroll
-      for (int i = 0; i < RM; ++i)
-#pragma unroll
-        for (int j = 0; j < RN; ++j) acc[o][i][j] = 0.0;
+// Every contraction is a small GEMM on shared-memory operands, run on the FP64
+// tensor pipe (mma.sync m8n8k4 f64 -> DMMA): dims padded to multiples of 8
+// (q = 33 -> 40) with zero rows/columns, each warp task an 8 x 16 output block
+// (one A fragment, two B fragments per k-step).  Operand strides are chosen
+// so fragment loads touch every bank pair exactly twice (two wavefronts).
+constexpr int kQP = 40;  // padded quadrature count (q <= 40)
+
+template <class FA, class FB, class FO>
+__device__ __forceinline__ void dgemm_tc(int M, int N, int K, FA A, FB B, FO O) {
+  // M, N multiples of 8, K multiple of 4
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int tm = M >> 3, tn = (N + 15) >> 4;
+  const int ar = lane >> 2, ak = lane & 3;
+  for (int task = warp; task < tm * tn; task += nw) {
+    const int m0 = 8 * (task / tn), n0 = 16 * (task % tn);
+    const bool two = n0 + 8 < N;
+    double d[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll 4
-    for (int k = 0; k < K; ++k) step(k, mi, nj, acc);
-#pragma unroll
-    for (int o = 0; o < NO; ++o)
-#pragma unroll
-      for (int i = 0; i < RM; ++i)
-#pragma unroll
-        for (int j = 0; j < RN; ++j)
-          if (bm + i * nbm < M && bn + j * nbn < N) out(o, bm + i * nbm, bn + j * nbn, acc[o][i][j]);
+    for (int k0 = 0; k0 < K; k0 += 4) {
+      const double a = A(m0 + ar, k0 + ak);
+      const double b0 = B(k0 + ak, n0 + ar);
+      const double b1 = two ? B(k0 + ak, n0 + 8 + ar) : 0.0;
+      dmma884(d[0][0], d[0][1], a, b0);
+      dmma884(d[1][0], d[1][1], a, b1);
+    }
+    const int r = m0 + ar, c = n0 + 2 * ak;
+    O(r, c, d[0][0]);
+    O(r, c + 1, d[0][1]);
+    if (two) {
+      O(r, c + 8, d[1][0]);
+      O(r, c + 9, d[1][1]);
+    }
   }
 }
 
-constexpr int kQR = 2;  // register block (rows and columns) of the quadrature GEMMs
+// V, D padded: Vp[qx + kQP i] (zero for qx >= q)
+__device__ __forceinline__ void load_vd_padded(double* Vp, double* Dp, const double* __restrict__ Vq,
+                                               const double* __restrict__ Dq, int q, int n1, int n1p) {
+  for (int i = threadIdx.x; i < kQP * n1p; i += blockDim.x) {
+    const int qx = i % kQP, j = i / kQP;
+    const bool in = qx < q && j < n1;
+    Vp[i] = in ? Vq[qx + q * j] : 0.0;
+    Dp[i] = in ? Dq[qx + q * j] : 0.0;
+  }
+}
+
+__host__ __device__ __forceinline__ int pad8(int n) { return (n + 7) & ~7; }
+__host__ __device__ __forceinline__ int pad4(int n) { return (n + 3) & ~3; }
 
 // Stage 1: per (cell, z-level kz): t0 = V_x u, t1 = D_x u, then
 // T[c][0] = V_y t0 (-> d/dz path), T[c][1] = D_y t0 (d/dy), T[c][2] = V_y t1 (d/dx);
-// layout T[c][f][kz][qy][qx].  V, D: q x n1 column-major (V[qx + q i]).
-__global__ void __launch_bounds__(256, 3) k_quad_stage1(int n1, int q, const double* __restrict__ x,
-                                                         const int32_t* __restrict__ cdofs,
-                                                         const uint8_t* __restrict__ cons,
-                                                         const double* __restrict__ Vq,
-                                                         const double* __restrict__ Dq, double* __restrict__ T) {
-  extern __shared__ double sm[];
-  double* V = sm;                  // q x n1
-  double* D = V + q * n1;
-  double* u = D + q * n1;          // u[i + (n1 + 1) j]
-  double* t0 = u + (n1 + 1) * n1;  // t0[qx + q j]
-  double* t1 = t0 + q * n1;
+// layout T[c][f][kz][qy][qx].
+__global__ void __launch_bounds__(256) k_quad_stage1(int n1, int q, const double* __restrict__ x,
+                                                      const int32_t* __restrict__ cdofs,
+                                                      const uint8_t* __restrict__ cons, const double* __restrict__ Vq,
+                                                      const double* __restrict__ Dq, double* __restrict__ T) {
+  extern __shared__ __align__(16) double sm[];
+  const int n1p = pad8(n1), n1k = pad4(n1), su = n1k + 4;
+  double* Vp = sm;                  // kQP x n1p
+  double* Dp = Vp + kQP * n1p;
+  double* u = Dp + kQP * n1p;       // u[j * su + i], zero padded to n1p x n1k
+  double* t0 = u + su * n1p;        // t0[j * kQP + qx]
+  double* t1 = t0 + kQP * n1p;
   const int c = blockIdx.x / n1, kz = blockIdx.x % n1;
-  const int npc = n1 * n1 * n1, q2 = q * q, su = n1 + 1;
-  for (int i = threadIdx.x; i < q * n1; i += blockDim.x) {
-    V[i] = Vq[i];
-    D[i] = Dq[i];
-  }
-  const int32_t* cd = cdofs + size_t(c) * npc + size_t(kz) * n1 * n1;
-  staged_copy<4>(
-      n1 * n1, [&](int l) { const int g = cd[l]; return cons[g] ? 0.0 : x[g]; },
-      [&](int l, double v) { u[l % n1 + su * (l / n1)] = v; });
+  const int npc = n1 * n1 * n1, q2 = q * q;
+  load_vd_padded(Vp, Dp, Vq, Dq, q, n1, n1p);
+  for (int i = threadIdx.x; i < su * n1p; i += blockDim.x) u[i] = 0.0;
   __syncthreads();
-  mgemm<kQR, kQR, 2>(
-      n1, q, n1,
-      [&](int i, const int* mj, const int* nq, auto& acc) {
-        double a[kQR], bv[kQR], bd[kQR];
-#pragma unroll
-        for (int r = 0; r < kQR; ++r) a[r] = u[i + su * mj[r]];
-#pragma unroll
-        for (int r = 0; r < kQR; ++r) {
-          bv[r] = V[nq[r] + q * i];
-          bd[r] = D[nq[r] + q * i];
-        }
-#pragma unroll
-        for (int r = 0; r < kQR; ++r)
-#pragma unroll
-          for (int s2 = 0; s2 < kQR; ++s2) {
-            acc[0][r][s2] = fma(a[r], bv[s2], acc[0][r][s2]);
-            acc[1][r][s2] = fma(a[r], bd[s2], acc[1][r][s2]);
-          }
-      },
-      [&](int o, int j, int qx, double v) { (o ? t1 : t0)[qx + q * j] = v; });
+  const int32_t* cd = cdofs + size_t(c) * npc + size_t(kz) * n1 * n1;
+#pragma unroll 4
+  for (int l = threadIdx.x; l < n1 * n1; l += blockDim.x) {
+    const int g = cd[l];
+    const double xv = x[g];
+    u[(l / n1) * su + l % n1] = cons[g] ? 0.0 : xv;
+  }
+  __syncthreads();
+  auto Au = [&](int j, int i) { return u[j * su + i]; };
+  dgemm_tc(n1p, kQP, n1k, Au, [&](int i, int qx) { return Vp[qx + kQP * i]; },
+           [&](int j, int qx, double v) { t0[j * kQP + qx] = v; });
+  dgemm_tc(n1p, kQP, n1k, Au, [&](int i, int qx) { return Dp[qx + kQP * i]; },
+           [&](int j, int qx, double v) { t1[j * kQP + qx] = v; });
   __syncthreads();
   double* out = T + size_t(c) * 3 * n1 * q2 + size_t(kz) * q2;
-  mgemm<kQR, kQR, 3>(
-      q, q, n1,
-      [&](int j, const int* my, const int* nx, auto& acc) {
-        double av[kQR], ad[kQR], b0[kQR], b1[kQR];
-#pragma unroll
-        for (int r = 0; r < kQR; ++r) {
-          av[r] = V[my[r] + q * j];
-          ad[r] = D[my[r] + q * j];
-          b0[r] = t0[nx[r] + q * j];
-          b1[r] = t1[nx[r] + q * j];
-        }
-#pragma unroll
-        for (int r = 0; r < kQR; ++r)
-#pragma unroll
-          for (int s2 = 0; s2 < kQR; ++s2) {
-            acc[0][r][s2] = fma(av[r], b0[s2], acc[0][r][s2]);
-            acc[1][r][s2] = fma(ad[r], b0[s2], acc[1][r][s2]);
-            acc[2][r][s2] = fma(av[r], b1[s2], acc[2][r][s2]);
-          }
-      },
-      [&](int o, int qy, int qx, double v) { out[size_t(o) * n1 * q2 + qx + q * qy] = v; });
+  auto AV = [&](int qy, int j) { return Vp[qy + kQP * j]; };
+  auto B0 = [&](int j, int qx) { return t0[j * kQP + qx]; };
+  dgemm_tc(kQP, kQP, n1k, AV, B0, [&](int qy, int qx, double v) {
+    if (qy < q && qx < q) out[qx + q * qy] = v;
+  });
+  dgemm_tc(kQP, kQP, n1k, [&](int qy, int j) { return Dp[qy + kQP * j]; }, B0, [&](int qy, int qx, double v) {
+    if (qy < q && qx < q) out[size_t(n1) * q2 + qx + q * qy] = v;
+  });
+  dgemm_tc(kQP, kQP, n1k, AV, [&](int j, int qx) { return t1[j * kQP + qx]; }, [&](int qy, int qx, double v) {
+    if (qy < q && qx < q) out[2 * size_t(n1) * q2 + qx + q * qy] = v;
+  });
 }
 
 // Stage 2: per (cell, qy): interpolate the three fields to the quadrature
@@ -247,26 +237,26 @@ __global__ void __launch_bounds__(256, 3) k_quad_stage1(int n1, int q, const dou
 // f = w kappa G g with G = det J^{-1} J^{-T} of the trilinear map (Jacobian
 // from the 8 cell corners, src/geometry.cpp:33-43); project back in place:
 // T0 <- V_z^T f_x, T1 <- V_z^T f_y, T2 <- D_z^T f_z.
-__global__ void __launch_bounds__(256, 3) k_quad_stage2(int n1, int q, double* __restrict__ T,
-                                                         const double* __restrict__ Vq,
-                                                         const double* __restrict__ Dq,
-                                                         const double* __restrict__ wq,
-                                                         const double* __restrict__ xyz,
-                                                         const double* __restrict__ kappa,
-                                                         const double* __restrict__ qpts) {
-  extern __shared__ double sm[];
-  double* V = sm;
-  double* D = V + q * n1;
-  double* W = D + q * n1;      // q weights, q points
-  double* X = W + 2 * q;       // 24 corner coordinates, X[3 b + r]
-  double* C = X + 24;          // C[f][kz][qx] (stride q)
-  double* G = C + 3 * n1 * q;  // g / f [field][qz][qx]
+__global__ void __launch_bounds__(256) k_quad_stage2(int n1, int q, double* __restrict__ T,
+                                                      const double* __restrict__ Vq, const double* __restrict__ Dq,
+                                                      const double* __restrict__ wq, const double* __restrict__ xyz,
+                                                      const double* __restrict__ kappa,
+                                                      const double* __restrict__ qpts) {
+  extern __shared__ __align__(16) double sm[];
+  const int n1p = pad8(n1), n1k = pad4(n1);
+  double* Vp = sm;
+  double* Dp = Vp + kQP * n1p;
+  double* C = Dp + kQP * n1p;         // C[f][kz < n1k][qx] (stride kQP, zero padded)
+  double* G = C + 3 * n1k * kQP;      // g / f [field][qz][qx] (kQP x kQP, zero padded)
+  double* W = G + 3 * kQP * kQP;      // q weights, q points
+  double* X = W + 2 * q;              // 24 corner coordinates, X[3 b + r]
+  double* J0 = X + 24;                // Jacobian tables [q][3] x 4
+  double* J2 = J0 + 3 * q;
+  double* AL = J2 + 3 * q;
+  double* BE = AL + 3 * q;
   const int c = blockIdx.x / q, qy = blockIdx.x % q;
   const int q2 = q * q;
-  for (int i = threadIdx.x; i < q * n1; i += blockDim.x) {
-    V[i] = Vq[i];
-    D[i] = Dq[i];
-  }
+  load_vd_padded(Vp, Dp, Vq, Dq, q, n1, n1p);
   for (int i = threadIdx.x; i < q; i += blockDim.x) {
     W[i] = wq[i];
     W[q + i] = qpts[i];
@@ -274,40 +264,16 @@ __global__ void __launch_bounds__(256, 3) k_quad_stage2(int n1, int q, double* _
   for (int i = threadIdx.x; i < 24; i += blockDim.x) X[i] = xyz[size_t(c) * 24 + i];
   double* base = T + size_t(c) * 3 * n1 * q2 + size_t(qy) * q;
   staged_copy<8>(
-      3 * n1 * q, [&](int i) { const int fk = i / q; return base[size_t(fk) * q2 + (i - fk * q)]; },
+      3 * n1k * kQP,
+      [&](int i) {
+        const int fk = i / kQP, qx = i - fk * kQP, f = fk / n1k, k = fk - f * n1k;
+        return (qx < q && k < n1) ? base[size_t(f * n1 + k) * q2 + qx] : 0.0;
+      },
       [&](int i, double v) { C[i] = v; });
   __syncthreads();
-  mgemm<kQR, kQR, 3>(
-      q, q, n1,
-      [&](int k, const int* mz, const int* nx, auto& acc) {
-        double av[kQR], ad[kQR], c0[kQR], c1[kQR], c2[kQR];
-#pragma unroll
-        for (int r = 0; r < kQR; ++r) {
-          av[r] = V[mz[r] + q * k];
-          ad[r] = D[mz[r] + q * k];
-          c0[r] = C[k * q + nx[r]];
-          c1[r] = C[(n1 + k) * q + nx[r]];
-          c2[r] = C[(2 * n1 + k) * q + nx[r]];
-        }
-#pragma unroll
-        for (int r = 0; r < kQR; ++r)
-#pragma unroll
-          for (int s2 = 0; s2 < kQR; ++s2) {
-            acc[0][r][s2] = fma(av[r], c2[s2], acc[0][r][s2]);
-            acc[1][r][s2] = fma(av[r], c1[s2], acc[1][r][s2]);
-            acc[2][r][s2] = fma(ad[r], c0[s2], acc[2][r][s2]);
-          }
-      },
-      [&](int o, int qz, int qx, double v) { G[o * q2 + qz * q + qx] = v; });
-  __syncthreads();
-  // Jacobian columns of the trilinear map x = sum_b N_b(xi) X_b at (xi_x, xi_y, xi_z),
-  // xi_y fixed per block:  col0 depends on (xi_y, xi_z), col2 on (xi_x, xi_y),
-  // col1 = h0(xi_z) al(xi_x) + h1(xi_z) be(xi_x) -- tables in shared memory.
+  // Jacobian columns of x = sum_b N_b(xi) X_b:  col0 depends on (xi_y, xi_z),
+  // col2 on (xi_x, xi_y), col1 = h0(xi_z) al(xi_x) + h1(xi_z) be(xi_x).
   {
-    double* J0 = C;             // [qz][3]   (C is free after the interpolation)
-    double* J2 = J0 + 3 * q;    // [qx][3]
-    double* AL = J2 + 3 * q;    // [qx][3]
-    double* BE = AL + 3 * q;    // [qx][3]
     const double ey = W[q + qy];
     const double hy[2] = {0.5 * (1.0 - ey), 0.5 * (1.0 + ey)};
     for (int i = threadIdx.x; i < q; i += blockDim.x) {
@@ -317,12 +283,10 @@ __global__ void __launch_bounds__(256, 3) k_quad_stage2(int n1, int q, double* _
         double j0 = 0.0, j2 = 0.0, al = 0.0, be = 0.0;
         for (int u = 0; u < 2; ++u)
           for (int v = 0; v < 2; ++v) {
-            // d/dxi_x at (xi_y = ey, xi_z = t): corners b = 1 + 2u + 4v minus b = 2u + 4v
             j0 += hy[u] * h[v] * 0.5 * (X[3 * (1 + 2 * u + 4 * v) + r] - X[3 * (2 * u + 4 * v) + r]);
-            // d/dxi_z at (xi_x = t, xi_y = ey): corners b = u + 2v + 4 minus b = u + 2v
             j2 += h[u] * hy[v] * 0.5 * (X[3 * (u + 2 * v + 4) + r] - X[3 * (u + 2 * v) + r]);
           }
-        for (int u = 0; u < 2; ++u) {  // d/dxi_y at xi_x = t, split by the xi_z corner layer
+        for (int u = 0; u < 2; ++u) {
           al += h[u] * 0.5 * (X[3 * (u + 2) + r] - X[3 * u + r]);
           be += h[u] * 0.5 * (X[3 * (u + 6) + r] - X[3 * (u + 4) + r]);
         }
@@ -332,127 +296,100 @@ __global__ void __launch_bounds__(256, 3) k_quad_stage2(int n1, int q, double* _
         BE[3 * i + r] = be;
       }
     }
-    __syncthreads();
-    const double kap = kappa[c], wy = W[qy];
-    for (int pnt = threadIdx.x; pnt < q2; pnt += blockDim.x) {
-      const int qz = pnt / q, qx = pnt - qz * q;
-      const double tz = W[q + qz];
-      const double hz0 = 0.5 * (1.0 - tz), hz1 = 0.5 * (1.0 + tz);
-      double J[3][3];
-#pragma unroll
-      for (int r = 0; r < 3; ++r) {
-        J[r][0] = J0[3 * qz + r];
-        J[r][1] = hz0 * AL[3 * qx + r] + hz1 * BE[3 * qx + r];
-        J[r][2] = J2[3 * qx + r];
-      }
-      // adj[i][j] = det * (J^{-1})[i][j]
-      double adj[3][3];
-#pragma unroll
-      for (int i = 0; i < 3; ++i)
-#pragma unroll
-        for (int j = 0; j < 3; ++j) {
-          const int i1 = (j + 1) % 3, i2 = (j + 2) % 3, j1 = (i + 1) % 3, j2 = (i + 2) % 3;
-          adj[i][j] = J[i1][j1] * J[i2][j2] - J[i1][j2] * J[i2][j1];
-        }
-      const double det = J[0][0] * adj[0][0] + J[0][1] * adj[1][0] + J[0][2] * adj[2][0];
-      // f = w kappa det J^{-1} J^{-T} g = (w kappa / det) adj (adj^T g)
-      const double g[3] = {G[pnt], G[q2 + pnt], G[2 * q2 + pnt]};
-      double hv[3];
-#pragma unroll
-      for (int r = 0; r < 3; ++r) hv[r] = adj[0][r] * g[0] + adj[1][r] * g[1] + adj[2][r] * g[2];
-      const double sc = W[qx] * wy * W[qz] * kap / det;
-#pragma unroll
-      for (int a2 = 0; a2 < 3; ++a2) G[a2 * q2 + pnt] = sc * (adj[a2][0] * hv[0] + adj[a2][1] * hv[1] + adj[a2][2] * hv[2]);
+  }
+  const int kq2 = kQP * kQP;
+  auto AVz = [&](int qz, int k) { return Vp[qz + kQP * k]; };
+  dgemm_tc(kQP, kQP, n1k, AVz, [&](int k, int qx) { return C[(2 * n1k + k) * kQP + qx]; },
+           [&](int qz, int qx, double v) { G[qz * kQP + qx] = v; });
+  dgemm_tc(kQP, kQP, n1k, AVz, [&](int k, int qx) { return C[(n1k + k) * kQP + qx]; },
+           [&](int qz, int qx, double v) { G[kq2 + qz * kQP + qx] = v; });
+  dgemm_tc(kQP, kQP, n1k, [&](int qz, int k) { return Dp[qz + kQP * k]; }, [&](int k, int qx) { return C[k * kQP + qx]; },
+           [&](int qz, int qx, double v) { G[2 * kq2 + qz * kQP + qx] = v; });
+  __syncthreads();
+  const double kap = kappa[c], wy = W[qy];
+  for (int pnt = threadIdx.x; pnt < kq2; pnt += blockDim.x) {
+    const int qz = pnt / kQP, qx = pnt - qz * kQP;
+    if (qz >= q || qx >= q) {
+      G[pnt] = G[kq2 + pnt] = G[2 * kq2 + pnt] = 0.0;
+      continue;
     }
+    const double tz = W[q + qz];
+    const double hz0 = 0.5 * (1.0 - tz), hz1 = 0.5 * (1.0 + tz);
+    double J[3][3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      J[r][0] = J0[3 * qz + r];
+      J[r][1] = hz0 * AL[3 * qx + r] + hz1 * BE[3 * qx + r];
+      J[r][2] = J2[3 * qx + r];
+    }
+    double adj[3][3];  // det * J^{-1}
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        const int i1 = (j + 1) % 3, i2 = (j + 2) % 3, j1 = (i + 1) % 3, j2 = (i + 2) % 3;
+        adj[i][j] = J[i1][j1] * J[i2][j2] - J[i1][j2] * J[i2][j1];
+      }
+    const double det = J[0][0] * adj[0][0] + J[0][1] * adj[1][0] + J[0][2] * adj[2][0];
+    const double g[3] = {G[pnt], G[kq2 + pnt], G[2 * kq2 + pnt]};
+    double hv[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) hv[r] = adj[0][r] * g[0] + adj[1][r] * g[1] + adj[2][r] * g[2];
+    const double sc = W[qx] * wy * W[qz] * kap / det;
+#pragma unroll
+    for (int a2 = 0; a2 < 3; ++a2) G[a2 * kq2 + pnt] = sc * (adj[a2][0] * hv[0] + adj[a2][1] * hv[1] + adj[a2][2] * hv[2]);
   }
   __syncthreads();
-  mgemm<kQR, kQR, 3>(
-      n1, q, q,
-      [&](int qz, const int* mk, const int* nx, auto& acc) {
-        double av[kQR], ad[kQR], f0[kQR], f1[kQR], f2[kQR];
-#pragma unroll
-        for (int r = 0; r < kQR; ++r) {
-          av[r] = V[qz + q * mk[r]];
-          ad[r] = D[qz + q * mk[r]];
-          f0[r] = G[qz * q + nx[r]];
-          f1[r] = G[q2 + qz * q + nx[r]];
-          f2[r] = G[2 * q2 + qz * q + nx[r]];
-        }
-#pragma unroll
-        for (int r = 0; r < kQR; ++r)
-#pragma unroll
-          for (int s2 = 0; s2 < kQR; ++s2) {
-            acc[0][r][s2] = fma(av[r], f0[s2], acc[0][r][s2]);
-            acc[1][r][s2] = fma(av[r], f1[s2], acc[1][r][s2]);
-            acc[2][r][s2] = fma(ad[r], f2[s2], acc[2][r][s2]);
-          }
-      },
-      [&](int o, int k, int qx, double v) { base[size_t(o * n1 + k) * q2 + qx] = v; });
+  const int Kq = (q + 3) & ~3;  // projection over qz (rows >= q are zero)
+  auto BVk = [&](int k, int qz) { return Vp[qz + kQP * k]; };
+  dgemm_tc(n1p, kQP, Kq, BVk, [&](int qz, int qx) { return G[qz * kQP + qx]; }, [&](int k, int qx, double v) {
+    if (qx < q && k < n1) base[size_t(k) * q2 + qx] = v;
+  });
+  dgemm_tc(n1p, kQP, Kq, BVk, [&](int qz, int qx) { return G[kq2 + qz * kQP + qx]; }, [&](int k, int qx, double v) {
+    if (qx < q && k < n1) base[size_t(n1 + k) * q2 + qx] = v;
+  });
+  dgemm_tc(n1p, kQP, Kq, [&](int k, int qz) { return Dp[qz + kQP * k]; },
+           [&](int qz, int qx) { return G[2 * kq2 + qz * kQP + qx]; }, [&](int k, int qx, double v) {
+             if (qx < q && k < n1) base[size_t(2 * n1 + k) * q2 + qx] = v;
+           });
 }
 
 // Stage 3: per (cell, kz): b0 = V_y^T T0, b12 = D_y^T T1 + V_y^T T2,
 // E = D_x^T b0 + V_x^T b12.
-__global__ void __launch_bounds__(256, 3) k_quad_stage3(int n1, int q, const double* __restrict__ T,
-                                                         const double* __restrict__ Vq,
-                                                         const double* __restrict__ Dq, double* __restrict__ E) {
-  extern __shared__ double sm[];
-  double* V = sm;
-  double* D = V + q * n1;
-  double* P = D + q * n1;      // 3 planes [f][qy][qx]
-  double* b0 = P + 3 * q * q;  // b0[qx + q j]
-  double* b12 = b0 + q * n1;
+__global__ void __launch_bounds__(256) k_quad_stage3(int n1, int q, const double* __restrict__ T,
+                                                      const double* __restrict__ Vq, const double* __restrict__ Dq,
+                                                      double* __restrict__ E) {
+  extern __shared__ __align__(16) double sm[];
+  const int Kq = (q + 3) & ~3, n1p = pad8(n1);
+  double* Vp = sm;
+  double* Dp = Vp + kQP * n1p;
+  double* P = Dp + kQP * n1p;        // 3 planes [f][qy < Kq][qx < kQP], zero padded
+  double* b0 = P + 3 * Kq * kQP;     // b0[j * kQP + qx]
+  double* b12 = b0 + kQP * n1p;
   const int c = blockIdx.x / n1, kz = blockIdx.x % n1;
-  const int q2 = q * q;
-  for (int i = threadIdx.x; i < q * n1; i += blockDim.x) {
-    V[i] = Vq[i];
-    D[i] = Dq[i];
-  }
+  const int q2 = q * q, pl = Kq * kQP;
+  load_vd_padded(Vp, Dp, Vq, Dq, q, n1, n1p);
   const double* in = T + size_t(c) * 3 * n1 * q2 + size_t(kz) * q2;
   staged_copy<8>(
-      3 * q2, [&](int i) { const int f = i / q2; return in[size_t(f) * n1 * q2 + (i - f * q2)]; },
+      3 * pl,
+      [&](int i) {
+        const int f = i / pl, e = i - f * pl, qy = e / kQP, qx = e - qy * kQP;
+        return (qy < q && qx < q) ? in[size_t(f) * n1 * q2 + qy * q + qx] : 0.0;
+      },
       [&](int i, double v) { P[i] = v; });
   __syncthreads();
-  mgemm<kQR, kQR, 2>(
-      n1, q, q,
-      [&](int qy, const int* mj, const int* nx, auto& acc) {
-        double av[kQR], ad[kQR], p0[kQR], p1[kQR], p2[kQR];
-#pragma unroll
-        for (int r = 0; r < kQR; ++r) {
-          av[r] = V[qy + q * mj[r]];
-          ad[r] = D[qy + q * mj[r]];
-          p0[r] = P[qy * q + nx[r]];
-          p1[r] = P[q2 + qy * q + nx[r]];
-          p2[r] = P[2 * q2 + qy * q + nx[r]];
-        }
-#pragma unroll
-        for (int r = 0; r < kQR; ++r)
-#pragma unroll
-          for (int s2 = 0; s2 < kQR; ++s2) {
-            acc[0][r][s2] = fma(av[r], p0[s2], acc[0][r][s2]);
-            acc[1][r][s2] = fma(ad[r], p1[s2], acc[1][r][s2]);
-            acc[1][r][s2] = fma(av[r], p2[s2], acc[1][r][s2]);
-          }
-      },
-      [&](int o, int j, int qx, double v) { (o ? b12 : b0)[qx + q * j] = v; });
+  dgemm_tc(n1p, kQP, Kq, [&](int j, int qy) { return Vp[qy + kQP * j]; }, [&](int qy, int qx) { return P[qy * kQP + qx]; },
+           [&](int j, int qx, double v) { b0[j * kQP + qx] = v; });
+  dgemm_tc(n1p, kQP, 2 * Kq, [&](int j, int k) { return k < Kq ? Dp[k + kQP * j] : Vp[k - Kq + kQP * j]; },
+           [&](int k, int qx) { return P[pl + k * kQP + qx]; },  // T1 rows then T2 rows (contiguous)
+           [&](int j, int qx, double v) { b12[j * kQP + qx] = v; });
   __syncthreads();
   double* out = E + size_t(c) * n1 * n1 * n1 + size_t(kz) * n1 * n1;
-  mgemm<kQR, kQR, 1>(
-      n1, n1, q,
-      [&](int qx, const int* mj, const int* ni, auto& acc) {
-        double a0[kQR], a12[kQR], bd[kQR], bv[kQR];
-#pragma unroll
-        for (int r = 0; r < kQR; ++r) {
-          a0[r] = b0[qx + q * mj[r]];
-          a12[r] = b12[qx + q * mj[r]];
-          bd[r] = D[qx + q * ni[r]];
-          bv[r] = V[qx + q * ni[r]];
-        }
-#pragma unroll
-        for (int r = 0; r < kQR; ++r)
-#pragma unroll
-          for (int s2 = 0; s2 < kQR; ++s2) acc[0][r][s2] = fma(a0[r], bd[s2], fma(a12[r], bv[s2], acc[0][r][s2]));
-      },
-      [&](int, int j, int i, double v) { out[i + n1 * j] = v; });
+  dgemm_tc(n1p, n1p, 2 * Kq, [&](int j, int k) { return k < Kq ? b0[j * kQP + k] : b12[j * kQP + k - Kq]; },
+           [&](int k, int i) { return k < Kq ? Dp[k + kQP * i] : Vp[k - Kq + kQP * i]; },
+           [&](int j, int i, double v) {
+             if (i < n1 && j < n1) out[i + n1 * j] = v;
+           });
 }
 
 // ---- p = 31 (n1 = 32), 3D: slab-blocked transform ------------------------------
@@ -773,10 +710,12 @@ void launch_cells_quadrature(Context& c, const double* x) {
   const size_t need = size_t(c.ncells) * 3 * n1 * q * q;
   if (c.Qbuf.n < need) c.Qbuf.alloc(need);
   KernelTimer timer(c, 3);
-  const size_t s1 = sizeof(double) * (4 * size_t(q) * n1 + size_t(n1 + 1) * n1);
-  const size_t s2 = sizeof(double) * (2 * size_t(q) * n1 + 2 * q + 24 + 3 * size_t(n1) * q + 3 * size_t(q) * q);
-  const size_t s3 = sizeof(double) * (4 * size_t(q) * n1 + 3 * size_t(q) * q);
-  if (s1 > 227 * 1024 || s2 > 227 * 1024 || s3 > 227 * 1024)
+  const int Kq = (q + 3) & ~3, n1p = pad8(n1), n1k = pad4(n1);
+  const size_t s1 = sizeof(double) * (4 * size_t(kQP) * n1p + size_t(n1k + 4) * n1p);
+  const size_t s2 = sizeof(double) * (2 * size_t(kQP) * n1p + 3 * size_t(n1k) * kQP + 3 * size_t(kQP) * kQP + 2 * q + 24 +
+                                      12 * size_t(q));
+  const size_t s3 = sizeof(double) * (4 * size_t(kQP) * n1p + 3 * size_t(Kq) * kQP);
+  if (q > kQP || s1 > 227 * 1024 || s2 > 227 * 1024 || s3 > 227 * 1024)
     throw Error(FDMGPU_UNSUPPORTED, "true-form quadrature operator: p too large");
   FDM_CUDA(cudaFuncSetAttribute(k_quad_stage1, cudaFuncAttributeMaxDynamicSharedMemorySize, int(s1)));
   k_quad_stage1<<<c.ncells * n1, 256, s1, c.stream>>>(n1, q, x, c.cell_dofs.p, c.constrained.p, c.Vq.p, c.Dq.p,
