@@ -1,3 +1,5 @@
+#include <algorithm>
+#include <cstdlib>
 // Vertex-star patch kernels: batched numeric factorisation (K2), the
 // patch relaxation solve (K3) and the deterministic patch owner-gather.
 //
@@ -276,7 +278,7 @@ __device__ __forceinline__ void tile_gemm_abt(const double* __restrict__ A, cons
 // their running sums of the rows below (rotated so indices stay static).
 __device__ void diag_factor_invert(double* Dm, double* Wm, double* out, const PatchArgs& a, int K, int patch) {
   constexpr int LD = T + 1;
-  double* Lp = Wm + T * LD;        // [16][T][4]
+  double* Lp = Wm;                 // [16][T][4]
   double* rdiag = Lp + 16 * T * 4;  // [T]
   const int tid = threadIdx.x, lane = tid & 31, c = tid >> 2, rq = tid & 3, warp = tid >> 5;
   double v[16];
@@ -376,15 +378,15 @@ constexpr int kUpdStages = 3;  // TMA pipeline depth (2 operand tiles per stage,
 // Left-looking update of tile column K: C(I,K) = A(I,K) - sum_J L(I,J) L(K,J)^T
 // for every stored tile (I,K); the CTA owning the diagonal tile then factors
 // and inverts it.  Operand tiles arrive by TMA bulk copy, double-buffered.
-__global__ void __launch_bounds__(kUpdThreads) k_patch_update(PatchArgs a, int K, const int32_t* __restrict__ active,
+__global__ void __launch_bounds__(kUpdThreads, 3) k_patch_update(PatchArgs a, int K, const int32_t* __restrict__ active,
                                                                 const int32_t* __restrict__ tile_row,
                                                                 const int32_t* __restrict__ pair_ptr,
                                                                 const int32_t* __restrict__ pair_a,
                                                                 const int32_t* __restrict__ pair_b,
                                                                 const int32_t* __restrict__ tile_mask,
-                                                                double* __restrict__ tiles) {
+                                                                double* __restrict__ tiles, int nst) {
   extern __shared__ __align__(128) double sm[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(sm);  // kUpdStages barriers
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm);  // nst (<= 3) barriers
   double* buf = sm + 16;                              // [stages][A,B][TT] (128-byte aligned)
   const int t = active[blockIdx.x], j = blockIdx.y;  // tiles of column K with work
   const int I = tile_row[t];
@@ -393,26 +395,26 @@ __global__ void __launch_bounds__(kUpdThreads) k_patch_update(PatchArgs a, int K
   const int p0 = pair_ptr[t], np = pair_ptr[t + 1] - p0;
   const int tid = threadIdx.x;
   if (tid == 0) {
-    for (int s = 0; s < kUpdStages; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < nst; ++s) mbar_init(&full[s], 1);
     mbar_fence_init();
   }
   __syncthreads();
   if (tid == 0)
-    for (int s = 0; s < kUpdStages && s < np; ++s) {
+    for (int s = 0; s < nst && s < np; ++s) {
       mbar_arrive_expect_tx(&full[s], 2 * TT * sizeof(double));
       bulk_g2s(buf + (2 * s) * TT, base + size_t(pair_a[p0 + s]) * TT, TT * sizeof(double), &full[s]);
       bulk_g2s(buf + (2 * s + 1) * TT, base + size_t(pair_b[p0 + s]) * TT, TT * sizeof(double), &full[s]);
     }
   TileAcc acc = {};
   for (int i = 0; i < np; ++i) {
-    const int s = i % kUpdStages;
-    mbar_wait(&full[s], (i / kUpdStages) & 1);
+    const int s = i % nst;
+    mbar_wait(&full[s], (i / nst) & 1);
     tile_gemm_abt(buf + (2 * s) * TT, buf + (2 * s + 1) * TT, acc, tile_mask[pair_a[p0 + i]], tile_mask[pair_b[p0 + i]]);
     __syncthreads();
-    if (tid == 0 && i + kUpdStages < np) {
+    if (tid == 0 && i + nst < np) {
       mbar_arrive_expect_tx(&full[s], 2 * TT * sizeof(double));
-      bulk_g2s(buf + (2 * s) * TT, base + size_t(pair_a[p0 + i + kUpdStages]) * TT, TT * sizeof(double), &full[s]);
-      bulk_g2s(buf + (2 * s + 1) * TT, base + size_t(pair_b[p0 + i + kUpdStages]) * TT, TT * sizeof(double), &full[s]);
+      bulk_g2s(buf + (2 * s) * TT, base + size_t(pair_a[p0 + i + nst]) * TT, TT * sizeof(double), &full[s]);
+      bulk_g2s(buf + (2 * s + 1) * TT, base + size_t(pair_b[p0 + i + nst]) * TT, TT * sizeof(double), &full[s]);
     }
   }
   double* ct = base + size_t(t) * TT;
@@ -437,7 +439,6 @@ __global__ void __launch_bounds__(kUpdThreads) k_patch_update(PatchArgs a, int K
         const int r = acc.row(i), cc = acc.col(jj, e);
         Dm[cc * LD + r] = ct[tsw(r, cc)] - acc.v[i][jj][e];
       }
-  for (int e = tid; e < T * LD; e += blockDim.x) Wm[e] = 0.0;
   __syncthreads();
   diag_factor_invert(Dm, Wm, ct, a, K, j);
 }
@@ -855,17 +856,29 @@ void launch_patch_assemble(Context& c) {
 
 void launch_patch_update(Context& c, int K) {
   PatchArgs a = make_args(c);
-  const size_t smem = sizeof(double) * (16 + 2 * kUpdStages * TT);
   static bool attr = false;
   if (!attr) {
-    FDM_CUDA(cudaFuncSetAttribute(k_patch_update, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    FDM_CUDA(cudaFuncSetAttribute(k_patch_update, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(sizeof(double) * (16 + 2 * kUpdStages * TT))));
     attr = true;
   }
   const int na = c.L.active_ptr[K + 1] - c.L.active_ptr[K];
+  // Light columns (few tile GEMMs per output tile): one operand stage, so two
+  // CTAs fit per SM and overlap each other's TMA latency; heavy columns keep
+  // the 3-stage pipeline.
+  int npmax = 0;
+  for (int i = c.L.active_ptr[K]; i < c.L.active_ptr[K + 1]; ++i) {
+    const int t = c.L.active[i];
+    npmax = std::max(npmax, c.L.pair_ptr[t + 1] - c.L.pair_ptr[t]);
+  }
+  static const int light = getenv("FDMGPU_UPD_LIGHT") ? atoi(getenv("FDMGPU_UPD_LIGHT")) : 1 << 30;
+  const int nst = npmax <= light ? 1 : kUpdStages;
+  const size_t diag_area = size_t(T + 1) * T + 16 * T * 4 + T;  // Dm, Lp, rdiag
+  const size_t smem = sizeof(double) * (16 + std::max(size_t(2 * nst * TT), diag_area));
   dim3 grid(na, c.npatch);
   KernelTimer timer(c, 1);
   k_patch_update<<<grid, kUpdThreads, smem, c.stream>>>(a, K, c.active.p + c.L.active_ptr[K], c.tile_row.p, c.pair_ptr.p,
-                                                         c.pair_a.p, c.pair_b.p, c.tile_mask.p, c.tiles.p);
+                                                         c.pair_a.p, c.pair_b.p, c.tile_mask.p, c.tiles.p, nst);
   FDM_LAUNCH_CHECK(c);
 }
 
@@ -876,7 +889,7 @@ void launch_patch_update(Context& c, int K) {
 void launch_patch_lead(Context& c) {
   if (c.L.lead_cols == 0) return;
   PatchArgs a = make_args(c);
-  const size_t smem_d = sizeof(double) * (16 + 2 * size_t(T + 1) * T + 16 * T * 4 + T);
+  const size_t smem_d = sizeof(double) * (16 + size_t(T + 1) * T + 16 * T * 4 + T);
   const size_t smem_t = sizeof(double) * 2 * TT + 64;
   static bool attr = false;
   if (!attr) {
@@ -887,7 +900,7 @@ void launch_patch_lead(Context& c) {
   }
   KernelTimer timer(c, 1);
   k_patch_update<<<dim3(c.L.lead_cols, c.npatch), kUpdThreads, smem_d, c.stream>>>(
-      a, -1, c.lead_diag.p, c.tile_row.p, c.pair_ptr.p, c.pair_a.p, c.pair_b.p, c.tile_mask.p, c.tiles.p);
+      a, -1, c.lead_diag.p, c.tile_row.p, c.pair_ptr.p, c.pair_a.p, c.pair_b.p, c.tile_mask.p, c.tiles.p, 1);
   FDM_LAUNCH_CHECK(c);
   const int nt = int(c.L.lead_trsm.size() / 2);
   if (nt > 0) {
