@@ -495,23 +495,32 @@ constexpr int kSlot = TT + kHdr;  // ring slot: the densest possible record
 // zeros of the factor, which the factorisation produces as exact 0.0.
 __global__ void k_patch_pack(int ntiles, const int64_t* __restrict__ mask8, const int32_t* __restrict__ poff8,
                              const uint8_t* __restrict__ hdr, double* __restrict__ tiles) {
-  extern __shared__ __align__(16) double tile[];  // 2 x TT (double buffer)
+  extern __shared__ __align__(128) double tile[];  // 2 x TT (double buffer, filled by TMA)
   __shared__ int bits[64];
+  __shared__ __align__(8) uint64_t bar[2];
   double* base = tiles + size_t(blockIdx.x) * ntiles * TT;
-  auto load = [&](int t, double* dst) {
-    const double2* src = reinterpret_cast<const double2*>(base + size_t(t) * TT);
-    for (int e = threadIdx.x; e < TT / 2; e += blockDim.x) reinterpret_cast<double2*>(dst)[e] = src[e];
+  auto load = [&](int t) {  // one thread
+    mbar_arrive_expect_tx(&bar[t & 1], TT * sizeof(double));
+    bulk_g2s(tile + (t & 1) * TT, base + size_t(t) * TT, TT * sizeof(double), &bar[t & 1]);
   };
-  load(0, tile);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) load(0);
   for (int t = 0; t < ntiles; ++t) {
-    double* cur = tile + (t & 1) * TT;
+    // Prefetch t+1 (its buffer was released by the barrier ending t-1).  Its
+    // source region starts at (t+1)*TT >= the end of tile t's packed
+    // destination, so the in-place compaction never overwrites unread data.
+    if (threadIdx.x == 0 && t + 1 < ntiles) load(t + 1);
+    const double* cur = tile + (t & 1) * TT;
     const unsigned long long m = static_cast<unsigned long long>(mask8[t]);
     if (threadIdx.x < 64 && ((m >> threadIdx.x) & 1ull))
       bits[__popcll(m & ((1ull << threadIdx.x) - 1ull))] = int(threadIdx.x);
-    __syncthreads();  // cur loaded, bits ready, previous writes done
-    // Prefetch t+1: its source region starts at (t+1)*TT >= the end of tile t's
-    // packed destination, so the in-place compaction never overwrites unread data.
-    if (t + 1 < ntiles) load(t + 1, tile + ((t + 1) & 1) * TT);
+    mbar_wait(&bar[t & 1], (t >> 1) & 1);
+    __syncthreads();  // bits ready
     const int cnt = __popcll(m);
     double* dst = base + size_t(poff8[t]);
     if (threadIdx.x < kHdr) dst[threadIdx.x] = reinterpret_cast<const double*>(hdr + size_t(t) * 8 * kHdr)[threadIdx.x];
