@@ -1,4 +1,4 @@
-"""Scratch: time the patch solve alone (patch_apply) for debug grid/stage overrides."""
+"""Scratch: time the patch solve kernel alone (patch_apply, CUDA events via kernel_timing)."""
 import os, sys
 sys.path.insert(0, "/root/repo")
 import torch
