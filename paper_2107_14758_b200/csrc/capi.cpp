@@ -365,6 +365,8 @@ fdmgpu_status fdmgpu_create(fdmgpu_handle* out, int32_t dim, int32_t p, int32_t 
     FDM_CUDA(cudaSetDevice(cc.device));
     FDM_CUDA(cudaStreamCreateWithFlags(&cc.stream, cudaStreamNonBlocking));
     cc.own_stream = true;
+    const char* pd = std::getenv("FDMGPU_PDL");
+    cc.pdl = !(pd && pd[0] == '0');
     const char* fs = std::getenv("FDMGPU_FORCE_STAGED");
     cc.force_staged = fs && fs[0] == '1';
     const char* so = std::getenv("FDMGPU_SEP_ORDER");

@@ -152,6 +152,7 @@ struct Context {
   bool timing = false;
   bool capturing = false;  // inside a CUDA-graph capture: launches are recorded, not counted
   bool force_staged = false;  // FDMGPU_FORCE_STAGED=1: staged cell kernels for every p (tests)
+  bool pdl = true;            // programmatic dependent launch in the relaxation chain (FDMGPU_PDL=0 disables)
   int sep_order = 0;  // 0 plane-by-plane facets (default), 1 reference patch_ordering (FDMGPU_SEP_ORDER)
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tev[4];
 

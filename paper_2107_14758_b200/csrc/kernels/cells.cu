@@ -423,6 +423,7 @@ __global__ void __launch_bounds__(kLines16, 4) k_cells_transform16(int dir, int 
   double* tables = b + kNpc16;   // At, Bt (only with flags; 1/D computed on the fly)
   const Pos16 P;
   const int c = blockIdx.x, r = threadIdx.x;
+  pdl_trigger();
   load_rows16(Mt, M);
   CellFdm f;
   if (flags) {
@@ -430,6 +431,7 @@ __global__ void __launch_bounds__(kLines16, 4) k_cells_transform16(int dir, int 
     f.invD = nullptr;
   }
   const int32_t* cd = cdofs + size_t(c) * kNpc16;
+  pdl_wait();  // `in` / `aux` come from the previous kernel
   // gather: all map loads first, then the independent value loads (no branch on
   // the constraint flag, so in[g], cons[g] and the weight load in parallel)
 #pragma unroll 1
@@ -552,6 +554,8 @@ __global__ void k_gather(int64_t ndof, int mode, const double* __restrict__ E, c
                          const int32_t* __restrict__ idx, const double* __restrict__ inv_mult,
                          const uint8_t* __restrict__ cons, const double* __restrict__ x, double* __restrict__ out) {
   const int64_t g = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  pdl_trigger();
+  pdl_wait();
   if (g >= ndof) return;
   double s = 0.0;
   for (int q = ptr[g]; q < ptr[g + 1]; ++q) s += E[idx[q]];
@@ -582,9 +586,9 @@ void launch_cells_transform_fused(Context& c, int dir, const double* in, int fla
     const size_t smem16 = sizeof(double) * (kL16 * kL16 + size_t(kNpc16) + (flags ? 2 * kL16 * kL16 : 0));
     set_smem(k_cells_transform16, smem16);
     KernelTimer timer(c, 2);
-    k_cells_transform16<<<c.ncells, kLines16, smem16, c.stream>>>(
-        dir, flags, in, aux, c.E.p, dir == 0 ? c.cell_dofs.p : c.cell_modes.p, c.inv_mult.p, c.constrained.p,
-        c.mode_sign.p, dir == 0 ? c.St.p : c.S.p, c.mu.p, c.At.p, c.Bt.p, c.nK.p);
+    launch_pdl(c.pdl && !c.timing, k_cells_transform16, dim3(c.ncells), dim3(kLines16), smem16, c.stream, dir, flags, in,
+               aux, c.E.p, dir == 0 ? c.cell_dofs.p : c.cell_modes.p, c.inv_mult.p, c.constrained.p, c.mode_sign.p,
+               dir == 0 ? c.St.p : c.S.p, c.mu.p, c.At.p, c.Bt.p, c.nK.p);
     FDM_LAUNCH_CHECK(c);
     return;
   }
@@ -626,9 +630,8 @@ void launch_gather(Context& c, int mode, const double* E, const double* x, doubl
   const bool modes = (mode == 0 || mode == 3) && !c.modes_alias;
   const int threads = 256;
   const int64_t blocks = (c.ndof + threads - 1) / threads;
-  k_gather<<<unsigned(blocks), threads, 0, c.stream>>>(c.ndof, mode, E, modes ? c.gm_ptr.p : c.g_ptr.p,
-                                                       modes ? c.gm_idx.p : c.g_idx.p, c.inv_mult.p, c.constrained.p,
-                                                       x, out);
+  launch_pdl(c.pdl && !c.timing, k_gather, dim3(unsigned(blocks)), dim3(threads), 0, c.stream, c.ndof, mode, E,
+             modes ? c.gm_ptr.p : c.g_ptr.p, modes ? c.gm_idx.p : c.g_idx.p, c.inv_mult.p, c.constrained.p, x, out);
   FDM_LAUNCH_CHECK(c);
 }
 

@@ -666,6 +666,7 @@ __global__ void __launch_bounds__(kSolveThreads)
   const int j = blockIdx.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const double* tb = tiles + size_t(j) * a.ntiles * TT;
+  pdl_trigger();
   if (tid == 0) {
     for (int e = 0; e < kRingEntries; ++e) {
       mbar_init(&full[e], 1);
@@ -722,6 +723,7 @@ __global__ void __launch_bounds__(kSolveThreads)
 
   constexpr int NC = 32 * kSolveConsumers;
   const int rl = lane & 7, g = lane >> 3;
+  pdl_wait();  // the separator RHS comes from the previous kernel (the factor stream does not)
   // record of stream position q, after its bytes landed
   auto acquire = [&](int q) {
     const int e = q & (kRingEntries - 1);
@@ -841,6 +843,8 @@ __global__ void __launch_bounds__(kSolveThreads)
 // (src/schwarz.cpp:49-53 order, no atomics).
 __global__ void k_patch_gather(int64_t ndof, const double* __restrict__ corr, const int32_t* __restrict__ ptr,
                                const int32_t* __restrict__ idx, double* __restrict__ z) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t g = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (g >= ndof) return;
   double s = 0.0;
@@ -959,8 +963,9 @@ void launch_patch_solve(Context& c, const double* r_modal) {
     attr = true;
   }
   KernelTimer timer(c, 0);
-  k_patch_solve<<<c.npatch, kSolveThreads, smem, c.stream>>>(a, ring, r_modal, c.corr.p, c.tiles.p, c.pdofs.p,
-                                                              c.col_start.p, c.tile_row.p, c.tile_poff8.p);
+  launch_pdl(c.pdl && !c.timing, k_patch_solve, dim3(c.npatch), dim3(kSolveThreads), smem, c.stream, a, ring, r_modal,
+             c.corr.p, (const double*)c.tiles.p, (const int32_t*)c.pdofs.p, (const int32_t*)c.col_start.p,
+             (const int32_t*)c.tile_row.p, (const int32_t*)c.tile_poff8.p);
   FDM_LAUNCH_CHECK(c);
 }
 
@@ -978,7 +983,8 @@ void launch_patch_pack(Context& c) {
 void launch_patch_gather(Context& c, double* z_modal) {
   const int threads = 256;
   const int64_t blocks = (c.ndof + threads - 1) / threads;
-  k_patch_gather<<<unsigned(blocks), threads, 0, c.stream>>>(c.ndof, c.corr.p, c.pg_ptr.p, c.pg_idx.p, z_modal);
+  launch_pdl(c.pdl && !c.timing, k_patch_gather, dim3(unsigned(blocks)), dim3(threads), 0, c.stream, c.ndof,
+             (const double*)c.corr.p, (const int32_t*)c.pg_ptr.p, (const int32_t*)c.pg_idx.p, z_modal);
   FDM_LAUNCH_CHECK(c);
 }
 
