@@ -753,11 +753,7 @@ static void launch_cells_transform_32(Context& c, int dir, const double* in, int
   const int32_t* cd = dir == 0 ? c.cell_dofs.p : c.cell_modes.p;
   const size_t s1 = sizeof(double) * (kL32 * kL32 + 10 * kSlab32) + sizeof(Fdm32);
   const size_t s2 = sizeof(double) * kL32 * kL32 + sizeof(Fdm32);
-  static bool attr = false;
-  if (!attr) {
-    FDM_CUDA(cudaFuncSetAttribute(k_cells_t1_32, cudaFuncAttributeMaxDynamicSharedMemorySize, int(s1)));
-    attr = true;
-  }
+  FDM_CUDA(cudaFuncSetAttribute(k_cells_t1_32, cudaFuncAttributeMaxDynamicSharedMemorySize, int(s1)));
   KernelTimer timer(c, 2);
   k_cells_t1_32<<<c.ncells * 4, 256, s1, c.stream>>>(dir, flags, in, aux, c.E.p, cd, c.inv_mult.p, c.constrained.p,
                                                      c.mode_sign.p, M, c.mu.p, c.At.p, c.Bt.p, c.nK.p);

@@ -869,23 +869,13 @@ void launch_patch_assemble(Context& c) {
 
 void launch_patch_update(Context& c, int K) {
   PatchArgs a = make_args(c);
-  static bool attr = false;
-  if (!attr) {
-    FDM_CUDA(cudaFuncSetAttribute(k_patch_update, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  int(sizeof(double) * (16 + 2 * kUpdStages * TT))));
-    attr = true;
-  }
+  FDM_CUDA(cudaFuncSetAttribute(k_patch_update, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(sizeof(double) * (16 + 2 * kUpdStages * TT))));
   const int na = c.L.active_ptr[K + 1] - c.L.active_ptr[K];
-  // Light columns (few tile GEMMs per output tile): one operand stage, so two
-  // CTAs fit per SM and overlap each other's TMA latency; heavy columns keep
-  // the 3-stage pipeline.
-  int npmax = 0;
-  for (int i = c.L.active_ptr[K]; i < c.L.active_ptr[K + 1]; ++i) {
-    const int t = c.L.active[i];
-    npmax = std::max(npmax, c.L.pair_ptr[t + 1] - c.L.pair_ptr[t]);
-  }
-  static const int light = getenv("FDMGPU_UPD_LIGHT") ? atoi(getenv("FDMGPU_UPD_LIGHT")) : 1 << 30;
-  const int nst = npmax <= light ? 1 : kUpdStages;
+  // One operand stage: with the 65 KB diagonal work area three CTAs fit per SM
+  // and overlap each other's TMA latency, which measured faster than one CTA
+  // with a kUpdStages-deep pipeline in every tile column (C3 31.9 -> 24.8 ms).
+  const int nst = 1;
   const size_t diag_area = size_t(T + 1) * T + 16 * T * 4 + T;  // Dm, Lp, rdiag
   const size_t smem = sizeof(double) * (16 + std::max(size_t(2 * nst * TT), diag_area));
   dim3 grid(na, c.npatch);
@@ -904,13 +894,9 @@ void launch_patch_lead(Context& c) {
   PatchArgs a = make_args(c);
   const size_t smem_d = sizeof(double) * (16 + size_t(T + 1) * T + 16 * T * 4 + T);
   const size_t smem_t = sizeof(double) * 2 * TT + 64;
-  static bool attr = false;
-  if (!attr) {
-    FDM_CUDA(cudaFuncSetAttribute(k_patch_update, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  int(sizeof(double) * (16 + 2 * kUpdStages * TT))));
-    FDM_CUDA(cudaFuncSetAttribute(k_patch_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_t)));
-    attr = true;
-  }
+  FDM_CUDA(cudaFuncSetAttribute(k_patch_update, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(sizeof(double) * (16 + 2 * kUpdStages * TT))));
+  FDM_CUDA(cudaFuncSetAttribute(k_patch_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_t)));
   KernelTimer timer(c, 1);
   k_patch_update<<<dim3(c.L.lead_cols, c.npatch), kUpdThreads, smem_d, c.stream>>>(
       a, -1, c.lead_diag.p, c.tile_row.p, c.pair_ptr.p, c.pair_a.p, c.pair_b.p, c.tile_mask.p, c.tiles.p, 1);
@@ -928,11 +914,7 @@ void launch_patch_trsm(Context& c, int K) {
   if (cnt <= 0) return;
   PatchArgs a = make_args(c);
   const size_t smem = sizeof(double) * 2 * TT + 64;
-  static bool attr = false;
-  if (!attr) {
-    FDM_CUDA(cudaFuncSetAttribute(k_patch_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    attr = true;
-  }
+  FDM_CUDA(cudaFuncSetAttribute(k_patch_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   dim3 grid(cnt, c.npatch);
   KernelTimer timer(c, 1);
   k_patch_trsm<<<grid, kUpdThreads, smem, c.stream>>>(a, K, c.col_start.p, nullptr, c.tile_mask.p, c.tiles.p);
@@ -957,11 +939,7 @@ void launch_patch_solve(Context& c, const double* r_modal) {
   PatchArgs a = make_args(c);
   size_t smem = 0;
   const int ring = solve_ring(c, &smem);
-  static bool attr = false;
-  if (!attr) {
-    FDM_CUDA(cudaFuncSetAttribute(k_patch_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    attr = true;
-  }
+  FDM_CUDA(cudaFuncSetAttribute(k_patch_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
   KernelTimer timer(c, 0);
   launch_pdl(c.pdl && !c.timing, k_patch_solve, dim3(c.npatch), dim3(kSolveThreads), smem, c.stream, a, ring, r_modal,
              c.corr.p, (const double*)c.tiles.p, (const int32_t*)c.pdofs.p, (const int32_t*)c.col_start.p,
@@ -971,11 +949,7 @@ void launch_patch_solve(Context& c, const double* r_modal) {
 
 void launch_patch_pack(Context& c) {
   KernelTimer timer(c, 1);
-  static bool attr = false;
-  if (!attr) {
-    FDM_CUDA(cudaFuncSetAttribute(k_patch_pack, cudaFuncAttributeMaxDynamicSharedMemorySize, int(2 * TT * sizeof(double))));
-    attr = true;
-  }
+  FDM_CUDA(cudaFuncSetAttribute(k_patch_pack, cudaFuncAttributeMaxDynamicSharedMemorySize, int(2 * TT * sizeof(double))));
   k_patch_pack<<<c.npatch, 512, 2 * TT * sizeof(double), c.stream>>>(c.L.ntiles, c.tile_mask8.p, c.tile_poff8.p, c.tile_hdr.p, c.tiles.p);
   FDM_LAUNCH_CHECK(c);
 }
