@@ -319,12 +319,11 @@ void analyze_patches(Context& c, int npatch, const int32_t* vertex, const int64_
   }
   L.col_start.push_back(int32_t(L.tile_row.size()));
   L.ntiles = int(L.tile_row.size());
-  // 16x16 sub-block masks (bit bi*4 + bj) for the packed solve stream:
-  // off-diagonal tiles keep the sub-blocks the symbolic factor touches,
-  // diagonal tiles (they hold L_KK^{-1}) keep their whole lower triangle.
+  // 16x16 sub-block masks (bit bi*4 + bj) used by the factor GEMMs to skip
+  // structurally zero k panels: off-diagonal tiles mark the sub-blocks the
+  // symbolic factor touches, diagonal tiles (L_KK^{-1}) their lower triangle.
   const int nb16 = L.mpad / 16;
   L.tile_mask.assign(L.ntiles, 0);
-  L.tile_poff.assign(L.ntiles + 1, 0);
   for (int t = 0; t < L.ntiles; ++t) {
     const int I = L.tile_row[t], K = L.tile_col[t];
     int mask = 0;
@@ -334,7 +333,6 @@ void analyze_patches(Context& c, int npatch, const int32_t* vertex, const int64_
         if (on) mask |= 1 << (bi * 4 + bj);
       }
     L.tile_mask[t] = mask;
-    L.tile_poff[t + 1] = L.tile_poff[t] + __builtin_popcount(unsigned(mask));
   }
   // 8x8 sub-block masks (bit bi*8 + bj) of the packed solve stream, same rule.
   const int nb8 = L.mpad / 8;
