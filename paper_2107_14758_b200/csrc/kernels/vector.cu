@@ -44,8 +44,18 @@ __global__ void k_dot_partials(int64_t n, const double* __restrict__ x, const do
 __global__ void k_restrict(const int32_t* __restrict__ ptr, const int32_t* __restrict__ col,
                            const double* __restrict__ val, const double* __restrict__ fine, double* __restrict__ rc) {
   const int i = blockIdx.x;
-  double s = 0.0;
-  for (int q = ptr[i] + threadIdx.x; q < ptr[i + 1]; q += blockDim.x) s = fma(val[q], fine[col[q]], s);
+  // four independent chains: the fine[col[q]] gathers of a thread overlap
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  const int q1 = ptr[i + 1], st = blockDim.x;
+  int q = ptr[i] + threadIdx.x;
+  for (; q + 3 * st < q1; q += 4 * st) {
+    s0 = fma(val[q], fine[col[q]], s0);
+    s1 = fma(val[q + st], fine[col[q + st]], s1);
+    s2 = fma(val[q + 2 * st], fine[col[q + 2 * st]], s2);
+    s3 = fma(val[q + 3 * st], fine[col[q + 3 * st]], s3);
+  }
+  for (; q < q1; q += st) s0 = fma(val[q], fine[col[q]], s0);
+  double s = (s0 + s1) + (s2 + s3);
   s = block_sum<256>(s);
   if (threadIdx.x == 0) rc[i] = s;
 }
