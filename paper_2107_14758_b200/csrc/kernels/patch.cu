@@ -679,6 +679,11 @@ __global__ void __launch_bounds__(kSolveThreads)
   if (warp == kSolveConsumers) {
     if (lane == 0) {
       int q = 0, qt = 0, head = 0;  // next position, oldest unreleased position, ring head
+      // L2 policy: forward-sweep records evict_last, backward-sweep records
+      // (read once more, last) evict_first, so the most recently streamed
+      // forward records -- the first ones the backward sweep reads -- stay in L2
+      // (measured: solve 1.284 -> 1.261 ms at C3).
+      const uint64_t pol_keep = policy_evict_last(), pol_stream = policy_evict_first();
       auto release_oldest = [&]() {
         mbar_wait(&empty[qt & (kRingEntries - 1)], (qt / kRingEntries) & 1);
         ++qt;
@@ -707,7 +712,8 @@ __global__ void __launch_bounds__(kSolveThreads)
         slot_off[e] = head;
         const uint32_t bytes = uint32_t(len) * sizeof(double);
         mbar_arrive_expect_tx(&full[e], bytes);
-        bulk_g2s(ring + head, tb + rec_off[t], bytes, &full[e]);
+        bulk_g2s_hint(ring + head, tb + rec_off[t], bytes, &full[e],
+                      q < a.ntiles ? pol_keep : pol_stream);
         head += len;
         ++q;
       };
