@@ -394,11 +394,13 @@ __global__ void __launch_bounds__(kUpdThreads, 3) k_patch_update(PatchArgs a, in
   double* base = tiles + size_t(j) * a.ntiles * TT;
   const int p0 = pair_ptr[t], np = pair_ptr[t + 1] - p0;
   const int tid = threadIdx.x;
+  pdl_trigger();
   if (tid == 0) {
     for (int s = 0; s < nst; ++s) mbar_init(&full[s], 1);
     mbar_fence_init();
   }
   __syncthreads();
+  pdl_wait();  // operands of column K-1 come from the previous launch
   if (tid == 0)
     for (int s = 0; s < nst && s < np; ++s) {
       mbar_arrive_expect_tx(&full[s], 2 * TT * sizeof(double));
@@ -457,11 +459,13 @@ __global__ void __launch_bounds__(kUpdThreads) k_patch_trsm(PatchArgs a, int K, 
   const int t = K >= 0 ? t0 + 1 + blockIdx.x : lead[2 * blockIdx.x], j = blockIdx.y;
   double* base = tiles + size_t(j) * a.ntiles * TT;
   const int tid = threadIdx.x;
+  pdl_trigger();
   if (tid == 0) {
     mbar_init(&full[0], 1);
     mbar_fence_init();
   }
   __syncthreads();
+  pdl_wait();
   if (tid == 0) {
     mbar_arrive_expect_tx(&full[0], 2 * TT * sizeof(double));
     bulk_g2s(Cs, base + size_t(t) * TT, TT * sizeof(double), &full[0]);
@@ -886,8 +890,10 @@ void launch_patch_update(Context& c, int K) {
   const size_t smem = sizeof(double) * (16 + std::max(size_t(2 * nst * TT), diag_area));
   dim3 grid(na, c.npatch);
   KernelTimer timer(c, 1);
-  k_patch_update<<<grid, kUpdThreads, smem, c.stream>>>(a, K, c.active.p + c.L.active_ptr[K], c.tile_row.p, c.pair_ptr.p,
-                                                         c.pair_a.p, c.pair_b.p, c.tile_mask.p, c.tiles.p, nst);
+  launch_pdl(c.pdl && !c.timing, k_patch_update, grid, dim3(kUpdThreads), smem, c.stream, a, K,
+             (const int32_t*)(c.active.p + c.L.active_ptr[K]), (const int32_t*)c.tile_row.p,
+             (const int32_t*)c.pair_ptr.p, (const int32_t*)c.pair_a.p, (const int32_t*)c.pair_b.p,
+             (const int32_t*)c.tile_mask.p, c.tiles.p, nst);
   FDM_LAUNCH_CHECK(c);
 }
 
@@ -923,7 +929,8 @@ void launch_patch_trsm(Context& c, int K) {
   FDM_CUDA(cudaFuncSetAttribute(k_patch_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   dim3 grid(cnt, c.npatch);
   KernelTimer timer(c, 1);
-  k_patch_trsm<<<grid, kUpdThreads, smem, c.stream>>>(a, K, c.col_start.p, nullptr, c.tile_mask.p, c.tiles.p);
+  launch_pdl(c.pdl && !c.timing, k_patch_trsm, grid, dim3(kUpdThreads), smem, c.stream, a, K,
+             (const int32_t*)c.col_start.p, (const int32_t*)nullptr, (const int32_t*)c.tile_mask.p, c.tiles.p);
   FDM_LAUNCH_CHECK(c);
 }
 
