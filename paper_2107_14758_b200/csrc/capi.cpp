@@ -612,7 +612,7 @@ fdmgpu_status fdmgpu_factor(fdmgpu_handle h) {
       fdmgpu::launch_patch_update(c, K);
       fdmgpu::launch_patch_trsm(c, K);
     }
-    fdmgpu::launch_patch_pack(c);  // dense tiles -> packed 16x16 sub-blocks for the solve stream
+    fdmgpu::launch_patch_pack(c);  // dense tiles -> packed 8x8 sub-block records for the solve stream
     unsigned long long e = 0;
     FDM_CUDA(cudaMemcpyAsync(&e, c.d_err.p, sizeof(e), cudaMemcpyDeviceToHost, c.stream));
     FDM_CUDA(cudaStreamSynchronize(c.stream));

@@ -487,16 +487,15 @@ __global__ void __launch_bounds__(kUpdThreads) k_patch_trsm(PatchArgs a, int K, 
 // ---- K3: patch relaxation solve -------------------------------------------------
 constexpr int kSolveConsumers = 8;                         // consumer warps
 constexpr int kSolveThreads = 32 * (kSolveConsumers + 1);  // + 1 TMA producer warp
-constexpr int SB = 256;
 constexpr int SB8 = 64;   // doubles per packed 8x8 sub-block (solve stream)
 constexpr int kHdr = 16;  // doubles of the per-tile stream header (128 block-index bytes)
 constexpr int kSlot = TT + kHdr;  // ring slot: the densest possible record
 
-// Packed solve stream.  After factorisation every 64x64 tile is compacted to
-// its structurally nonzero 16x16 sub-blocks (mask bit bi*4 + bj, packed in bit
-// order; element (r, c) of a sub-block at c*16 + (r ^ c), conflict free for
-// both row and column sweeps).  Exact: the dropped sub-blocks are structural
-// zeros of the factor, which the factorisation produces as exact 0.0.
+// Packed solve stream.  After factorisation every 64x64 tile is compacted in
+// place into one record: the 128-byte block-index header (tile_hdr) and the
+// structurally nonzero 8x8 sub-blocks (mask bit bi*8 + bj, packed in bit
+// order; sub-block layout below).  Exact: the dropped sub-blocks are
+// structural zeros of the factor, which the factorisation produces as exact 0.0.
 __global__ void k_patch_pack(int ntiles, const int64_t* __restrict__ mask8, const int32_t* __restrict__ poff8,
                              const uint8_t* __restrict__ hdr, double* __restrict__ tiles) {
   extern __shared__ __align__(128) double tile[];  // 2 x TT (double buffer, filled by TMA)
