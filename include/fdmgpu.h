@@ -134,6 +134,16 @@ fdmgpu_status fdmgpu_set_patches(fdmgpu_handle h, int32_t npatch, const int32_t*
 fdmgpu_status fdmgpu_set_coarse(fdmgpu_handle h, int32_t ndof_c, const double* coarse_inverse,
                                 const int64_t* P_ptr, const int32_t* P_col, const double* P_val);
 
+/* Optional: the cell structure of the same prolongation, so P and P^T run as
+ * cell-wise sum-factorised kernels instead of the CSR:
+ * coarse_cell_dofs (ncells x 2^d, corner bit a = side along axis a, as the
+ * reference's q_space(p = 1) cell_dofs), the coarse constrained flags, and the
+ * Q1 hats at the fine GLL nodes, phat[(p+1) x 2] column-major -- the entries
+ * build_prolongation (src/schwarz.cpp:139-165) sums.  Same operator; sums in
+ * a different order (results equal to rounding). */
+fdmgpu_status fdmgpu_set_coarse_cells(fdmgpu_handle h, const int32_t* coarse_cell_dofs,
+                                      const uint8_t* coarse_constrained, const double* phat);
+
 /* Batched numeric factorisation of every patch matrix A~_j under its
  * patch ordering (replaces cholesky(), src/cholesky.cpp:9-87, inside
  * build_patch_solver, src/schwarz.cpp:84-93).  Returns FDMGPU_NOT_SPD with

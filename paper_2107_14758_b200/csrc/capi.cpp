@@ -601,6 +601,52 @@ fdmgpu_status fdmgpu_set_coarse(fdmgpu_handle h, int32_t ndof_c, const double* c
   });
 }
 
+fdmgpu_status fdmgpu_set_coarse_cells(fdmgpu_handle h, const int32_t* coarse_cell_dofs,
+                                      const uint8_t* coarse_constrained, const double* phat) {
+  return fdmgpu::guarded(h, [&](Context& c) {
+    if (!c.have_coarse || !c.have_maps) throw Error(FDMGPU_INVALID_ARGUMENT, "set_coarse_cells: set maps and coarse first");
+    if (!coarse_cell_dofs || !coarse_constrained || !phat)
+      throw Error(FDMGPU_INVALID_ARGUMENT, "set_coarse_cells: null array");
+    const int ncorner = 1 << c.dim;
+    const size_t nslots = size_t(c.ncells) * ncorner;
+    // coarse gather: per free coarse DOF its (cell, corner) slots, ascending
+    std::vector<int32_t> cptr(c.nc + 1, 0), cidx;
+    for (size_t e = 0; e < nslots; ++e) {
+      const int j = coarse_cell_dofs[e];
+      if (j < 0 || j >= c.nc) throw Error(FDMGPU_INVALID_ARGUMENT, "set_coarse_cells: coarse DOF out of range");
+      if (!coarse_constrained[j]) ++cptr[j + 1];
+    }
+    for (int j = 0; j < c.nc; ++j) cptr[j + 1] += cptr[j];
+    cidx.resize(cptr[c.nc]);
+    std::vector<int32_t> pos(cptr.begin(), cptr.end() - 1);
+    for (size_t e = 0; e < nslots; ++e) {
+      const int j = coarse_cell_dofs[e];
+      if (!coarse_constrained[j]) cidx[pos[j]++] = int32_t(e);
+    }
+    // prolongation owner: the first (lowest) cell holding a free fine DOF writes it
+    std::vector<uint8_t> owner(size_t(c.ncells) * c.npc, 0), seen(size_t(c.ndof), 0);
+    for (size_t e = 0; e < owner.size(); ++e) {
+      const int g = c.h_cell_dofs[e];
+      if (!c.h_constrained[g] && !seen[g]) {
+        seen[g] = 1;
+        owner[e] = 1;
+      }
+    }
+    std::vector<int32_t> ccd(coarse_cell_dofs, coarse_cell_dofs + nslots);
+    for (size_t e = 0; e < nslots; ++e)
+      if (coarse_constrained[ccd[e]]) ccd[e] = -1;  // constrained coarse DOFs carry no prolongation
+    c.ccd.upload(ccd, c.stream);
+    c.cg_ptr.upload(cptr, c.stream);
+    c.cg_idx.upload(cidx, c.stream);
+    c.powner.upload(owner, c.stream);
+    c.phat.upload(phat, size_t(c.n1) * 2, c.stream);
+    c.cellsum.alloc(nslots);
+    FDM_CUDA(cudaStreamSynchronize(c.stream));
+    const char* tr = std::getenv("FDMGPU_TRANSFER");  // "csr": keep the CSR transfer (tests)
+    c.have_coarse_cells = !(tr && std::string(tr) == "csr");
+  });
+}
+
 fdmgpu_status fdmgpu_factor(fdmgpu_handle h) {
   return fdmgpu::guarded(h, [&](Context& c) {
     c.check_ready(true, false, false);

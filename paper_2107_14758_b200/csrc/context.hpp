@@ -132,6 +132,12 @@ struct Context {
   DevArray<double> cinv, P_val, PT_val, rc, zc;
   DevArray<int32_t> P_ptr, P_col, PT_ptr, PT_col;
   bool have_coarse = false;
+  // cell-wise transfer (fdmgpu_set_coarse_cells): coarse cell maps, coarse
+  // gather CSR over (cell, corner) slots, prolongation owner flags, Q1 hats
+  DevArray<int32_t> ccd, cg_ptr, cg_idx;
+  DevArray<uint8_t> powner;
+  DevArray<double> phat, cellsum;
+  bool have_coarse_cells = false;
 
   // work vectors (ndof)
   DevArray<double> w[12];

@@ -165,6 +165,8 @@ int fdmhost_attach(void* ph, int device, int sep_order, fdmgpu_handle* out) {
   if ((st = fdmgpu_set_coarse(h, C.ndof, C.inverse.data(), C.P_ptr.data(), C.P_col.data(), C.P_val.data())) !=
       FDMGPU_OK)
     return fail(st);
+  if ((st = fdmgpu_set_coarse_cells(h, C.cell_dofs.data(), C.constrained.data(), C.phat.data())) != FDMGPU_OK)
+    return fail(st);
   *out = h;
   return FDMGPU_OK;
 }

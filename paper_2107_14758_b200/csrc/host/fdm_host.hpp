@@ -124,6 +124,9 @@ struct Coarse {
   std::vector<int64_t> P_ptr;   // prolongation CSR, fine rows
   std::vector<int32_t> P_col;
   std::vector<double> P_val;
+  std::vector<int32_t> cell_dofs;     // coarse (p = 1) cell maps, ncells x 2^d
+  std::vector<uint8_t> constrained;   // coarse constrained flags
+  std::vector<double> phat;           // (p+1) x 2 Q1 hats at the fine nodes, column-major
 };
 Coarse build_coarse(const Mesh& m, const Space& fine, const Basis1D& fb);
 

@@ -557,6 +557,11 @@ Coarse build_coarse(const Mesh& m, const Space& fine, const Basis1D& fb) {
         if (v != 0.0) rows[fi][cj] += v;
       }
     }
+  C.cell_dofs.assign(cs.cell_dofs.begin(), cs.cell_dofs.end());
+  C.constrained.assign(cs.constrained.begin(), cs.constrained.end());
+  C.phat.resize(size_t(n1) * 2);
+  for (int l = 0; l < n1; ++l)
+    for (int j = 0; j < 2; ++j) C.phat[l + size_t(n1) * j] = ph(l, j);
   C.P_ptr.assign(1, 0);
   for (int i = 0; i < fine.ndof; ++i) {
     for (const auto& [cj, v] : rows[i]) {

@@ -220,3 +220,23 @@ def test_p31_slab_path(pkg, oracle, torch):
         del os.environ["FDMGPU_FORCE_STAGED"]
     staged.factor()
     assert rel(z, staged.smooth(r)) <= TOL_RELAX
+
+
+@pytest.mark.parametrize("cfg", [(2, 0, 0), (1, 0, 0), (5, 3, 4)])
+def test_cellwise_transfer_matches_csr(pkg, torch, cfg):
+    # the sum-factorised restriction / prolongation (fdmgpu_set_coarse_cells)
+    # against the CSR of build_prolongation (src/schwarz.cpp:139-165)
+    prob = pkg.Problem(*cfg)
+    sols = []
+    for mode in ("cells", "csr"):
+        if mode == "csr":
+            os.environ["FDMGPU_TRANSFER"] = "csr"
+        try:
+            s = pkg.Solver(prob)
+        finally:
+            os.environ.pop("FDMGPU_TRANSFER", None)
+        s.factor()
+        s.omega = 0.3
+        sols.append(s)
+    r = prob.rhs()
+    assert rel(sols[0].vcycle(r), sols[1].vcycle(r)) <= 1e-13
