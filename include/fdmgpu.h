@@ -124,7 +124,9 @@ fdmgpu_status fdmgpu_set_cell_coeffs(fdmgpu_handle h, const uint8_t* kind, const
 /* PatchSolver::Patch lists (src/schwarz.cpp:62-83): for patch j, the vertex,
  * its ascending star_dofs dofs[ptr[j]..ptr[j+1]) (src/discretization.cpp:
  * 266-297), the patch_ordering permutation perm (local indices,
- * src/ordering.cpp:17-45) and its 2^dim star cells (ascending ids). */
+ * src/ordering.cpp:17-45) and its 2^dim star cells (ascending ids; a
+ * boundary-vertex star -- SolverConfig::skip_boundary_patches = false, the
+ * reference default -- has fewer cells and pads with -1). */
 fdmgpu_status fdmgpu_set_patches(fdmgpu_handle h, int32_t npatch, const int32_t* vertex, const int64_t* ptr,
                                  const int32_t* dofs, const int32_t* perm, const int32_t* star_cells);
 

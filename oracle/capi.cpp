@@ -65,6 +65,66 @@ void* oracle_create(int config, int n, int p, int build_global, int threads) {
   return rc ? nullptr : c;
 }
 
+// [ext] external mesh: vertices (nv x 3), cells (nc x 2^dim), facet tags
+// (cell, local facet 2*axis + (side > 0), 0/1/2 = interior/dirichlet/neumann).
+void* oracle_create_mesh(int dim, int nv, const double* vertices, int nc, const int* cells, int ntag,
+                         const int* tag_cell, const int* tag_lf, const int* tag_kind, int p, uint64_t seed,
+                         int build_global, int threads) {
+  Ctx* c = nullptr;
+  int rc = guard([&] {
+    Mesh m;
+    m.dim = dim;
+    for (int v = 0; v < nv; ++v) m.vertices.push_back({vertices[3 * v], vertices[3 * v + 1], vertices[3 * v + 2]});
+    const int ncorner = 1 << dim;
+    for (int k = 0; k < nc; ++k) m.cells.emplace_back(cells + size_t(k) * ncorner, cells + size_t(k + 1) * ncorner);
+    m.finalize();
+    for (int k = 0; k < ntag; ++k) {  // src/mesh.cpp:399-407
+      const int lf = tag_lf[k], axis = lf / 2, side = (lf % 2) ? 1 : -1;
+      int fi = -1;
+      for (int f = 0; f < int(m.facets.size()) && fi < 0; ++f)
+        for (int r = 0; r < m.facets[f].ncells(); ++r)
+          if (m.facets[f].cell[r] == tag_cell[k] && m.facets[f].axis[r] == axis && m.facets[f].side[r] == side) fi = f;
+      if (fi < 0) throw std::runtime_error("load_mesh: facet_tags entry names a missing facet");
+      m.facets[fi].tag = static_cast<FacetTag>(tag_kind[k]);
+    }
+    auto ctx = std::make_unique<Ctx>();
+    ctx->pb = make_problem_from_mesh(std::move(m), p, seed);
+    ctx->cfg.skip_boundary_patches = true;
+    ctx->cfg.threads = threads;
+    ctx->A = std::make_shared<GlobalOperator>(poisson_operator(ctx->pb->disc, ctx->pb->bundle));
+    ctx->sys = std::make_shared<TransformedSystem>(transformed_poisson(ctx->pb->disc, ctx->pb->bundle, true, build_global != 0));
+    ctx->pl = patch_list(ctx->pb->disc, ctx->cfg);
+    ctx->ps.ndof = ctx->pb->disc.ndof;
+    ctx->ps.threads = threads;
+    ctx->ps.patches.resize(ctx->pl.vertex.size());
+    for (size_t j = 0; j < ctx->pl.vertex.size(); ++j) {
+      ctx->ps.patches[j].vertex = ctx->pl.vertex[j];
+      ctx->ps.patches[j].dofs = ctx->pl.dofs[j];
+    }
+    c = ctx.release();
+  });
+  return rc ? nullptr : c;
+}
+
+// [ext] SolverConfig::skip_boundary_patches (include/fdmstar/schwarz.hpp:24);
+// the handles start with true (the configs); false = the reference default.
+int oracle_set_skip_boundary_patches(void* h, int skip) {
+  return guard([&] {
+    Ctx* ctx = static_cast<Ctx*>(h);
+    ctx->cfg.skip_boundary_patches = skip != 0;
+    ctx->pl = patch_list(ctx->pb->disc, ctx->cfg);
+    ctx->ps = PatchSolver();
+    ctx->tl.reset();
+    ctx->ps.ndof = ctx->pb->disc.ndof;
+    ctx->ps.threads = ctx->cfg.threads;
+    ctx->ps.patches.resize(ctx->pl.vertex.size());
+    for (size_t j = 0; j < ctx->pl.vertex.size(); ++j) {
+      ctx->ps.patches[j].vertex = ctx->pl.vertex[j];
+      ctx->ps.patches[j].dofs = ctx->pl.dofs[j];
+    }
+  });
+}
+
 void oracle_destroy(void* h) { delete static_cast<Ctx*>(h); }
 
 // out[0..9] = dim, p, ncells, ndof, nfree, npatches, nvertices, dofs_per_cell, sum n_j, config

@@ -73,4 +73,20 @@ std::unique_ptr<Problem> make_problem(int config, int n_override, int p_override
   return pb;
 }
 
+std::unique_ptr<Problem> make_problem_from_mesh(Mesh mesh, int p, uint64_t seed) {
+  auto pb = std::make_unique<Problem>();
+  pb->config = 0;
+  pb->p = p;
+  pb->mesh = std::move(mesh);
+  pb->disc = q_space(pb->mesh, p);
+  pb->disc.mesh = &pb->mesh;
+  pb->bundle = make_bundle(p);
+  std::mt19937_64 rng(seed);
+  std::uniform_real_distribution<double> uni(-1.0, 1.0);
+  pb->rhs.resize(pb->disc.ndof);
+  for (auto& v : pb->rhs) v = uni(rng);
+  pb->disc.project_free(pb->rhs);
+  return pb;
+}
+
 }  // namespace oracle

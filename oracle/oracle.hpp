@@ -347,5 +347,9 @@ struct Problem {
 // Builds mesh + space + RHS for config id (1..5); `n_override`/`p_override`
 // (>0) give reduced variants with the same generators.
 std::unique_ptr<Problem> make_problem(int config, int n_override = 0, int p_override = 0);
+// [ext] Problem on an external mesh (the reference's load_mesh data: vertices,
+// cells, facet tags applied as src/mesh.cpp:399-407 does); Q_p space, RHS
+// U[-1,1] from std::mt19937_64(seed) over all DOFs, project_free.
+std::unique_ptr<Problem> make_problem_from_mesh(Mesh mesh, int p, uint64_t seed);
 
 }  // namespace oracle

@@ -38,6 +38,10 @@ def lib():
         L.oracle_last_error.restype = C.c_char_p
         L.oracle_create.restype = C.c_void_p
         L.oracle_create.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int]
+        L.oracle_create_mesh.restype = C.c_void_p
+        L.oracle_set_skip_boundary_patches.argtypes = [C.c_void_p, C.c_int]
+        L.oracle_create_mesh.argtypes = [C.c_int, C.c_int, _d, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p,
+                                         C.c_void_p, C.c_int, C.c_uint64, C.c_int, C.c_int]
         L.oracle_destroy.argtypes = [C.c_void_p]
         L.oracle_info.argtypes = [C.c_void_p, _i64]
         L.oracle_get_rhs.argtypes = [C.c_void_p, _d]
@@ -187,17 +191,39 @@ def estimate_damping_dense(A, P):
 class Problem:
     """One synthetic configuration (1..5), optionally reduced (n cells/axis, degree p)."""
 
-    def __init__(self, config, n=0, p=0, build_global=True, threads=1):
+    def __init__(self, config, n=0, p=0, build_global=True, threads=1, _handle=None, skip_boundary_patches=True):
         L = lib()
-        self.h = L.oracle_create(config, n, p, 1 if build_global else 0, threads)
+        self.h = _handle if _handle is not None else L.oracle_create(config, n, p, 1 if build_global else 0, threads)
         if not self.h:
             raise OracleError(L.oracle_last_error().decode())
+        if not skip_boundary_patches:  # [ext] the reference default (src/schwarz.cpp:71-81)
+            _chk(L.oracle_set_skip_boundary_patches(self.h, 0))
         info = np.zeros(10, np.int64)
         _chk(L.oracle_info(self.h, info))
         (self.dim, self.p, self.ncells, self.ndof, self.nfree, self.npatches, self.nvertices,
          self.npc, self.sum_nj, self.config) = (int(v) for v in info)
         self.threads = threads
         self._twolevel = False
+
+    TAGS = {"interior": 0, "dirichlet": 1, "neumann": 2}
+
+    @classmethod
+    def from_mesh(cls, dim, vertices, cells, p, facet_tags=(), seed=0, build_global=True, threads=1,
+                  skip_boundary_patches=True):
+        """[ext] Problem on an external mesh (load_mesh data), RHS U[-1,1] from seed."""
+        v = np.zeros((len(vertices), 3))
+        v[:, :dim] = np.asarray(vertices, np.float64)[:, :dim]
+        c = np.ascontiguousarray(np.asarray(cells, np.int32))
+        tc = np.array([t[0] for t in facet_tags], np.int32)
+        tl = np.array([t[1] for t in facet_tags], np.int32)
+        tk = np.array([cls.TAGS[t[2]] for t in facet_tags], np.int32)
+        addr = lambda a: a.ctypes.data if len(a) else None
+        h = lib().oracle_create_mesh(int(dim), len(v), np.ascontiguousarray(v), len(c), c.ctypes.data, len(tc),
+                                     addr(tc), addr(tl), addr(tk), int(p), int(seed), 1 if build_global else 0, threads)
+        if not h:
+            raise OracleError(lib().oracle_last_error().decode())
+        return cls(0, p=p, build_global=build_global, threads=threads, _handle=h,
+                   skip_boundary_patches=skip_boundary_patches)
 
     def __del__(self):
         if getattr(self, "h", None) and _lib is not None:

@@ -72,6 +72,13 @@ def lib():
         L.fdmhost_problem_create.restype = _vp
         L.fdmhost_problem_create.argtypes = [C.c_int, C.c_int, C.c_int]
         L.fdmhost_problem_destroy.argtypes = [_vp]
+        L.fdmhost_problem_from_mesh_file.restype = _vp
+        L.fdmhost_problem_from_mesh_file.argtypes = [C.c_char_p, C.c_int, C.c_uint64]
+        L.fdmhost_problem_from_mesh.restype = _vp
+        L.fdmhost_problem_from_mesh.argtypes = [C.c_int, C.c_int, _vp, C.c_int, _vp, C.c_int, _vp, _vp, _vp, C.c_int,
+                                                C.c_uint64]
+        L.fdmhost_save_mesh.argtypes = [_vp, C.c_char_p]
+        L.fdmhost_problem_set_skip_boundary_patches.argtypes = [_vp, C.c_int]
         L.fdmhost_problem_info.argtypes = [_vp, _vp]
         L.fdmhost_get_rhs.argtypes = [_vp, _vp]
         L.fdmhost_get_maps.argtypes = [_vp] * 7
@@ -115,16 +122,55 @@ class Problem:
     """One synthetic configuration (BASELINE.json configs 1..5), optionally
     reduced to n cells per axis / degree p, built by the host setup mirror."""
 
-    def __init__(self, config: int, n: int = 0, p: int = 0):
+    def __init__(self, config: int, n: int = 0, p: int = 0, _handle=None, skip_boundary_patches=True):
         L = lib()
-        self.h = L.fdmhost_problem_create(config, n, p)
+        self.h = _handle if _handle is not None else L.fdmhost_problem_create(config, n, p)
         if not self.h:
             raise FdmGpuError(1, L.fdmhost_last_error().decode())
+        if not skip_boundary_patches:
+            _host_chk(L.fdmhost_problem_set_skip_boundary_patches(self.h, 0))
+        self.skip_boundary_patches = bool(skip_boundary_patches)
         info = np.zeros(15, np.int64)
         _host_chk(L.fdmhost_problem_info(self.h, _ptr(info)))
         (self.dim, self.p, self.ncells, self.ndof, self.nfree, self.npatches, self.nvertices, self.npc,
          self.sum_nj, self.ncoarse, self.P_nnz, self.q, self.config, self.n, cart) = (int(v) for v in info)
         self.all_cartesian = bool(cart)
+
+    # ---- external meshes (the reference's mesh file format, src/mesh.cpp:354-434) ----
+    TAGS = {"interior": 0, "dirichlet": 1, "neumann": 2}
+
+    @classmethod
+    def from_mesh_file(cls, path, p, seed=0, skip_boundary_patches=True):
+        """Q_p problem on a mesh file written by the reference's save_mesh (JSON:
+        dim, vertices, cells, facet_tags); unit coefficient, RHS U[-1,1] from
+        std::mt19937_64(seed), zero on Dirichlet DOFs.  Raises FdmGpuError with
+        the reference's load_mesh messages.  skip_boundary_patches=False adds the
+        boundary-vertex stars (SolverConfig's default, src/schwarz.cpp:71-81)."""
+        h = lib().fdmhost_problem_from_mesh_file(os.fsencode(path), int(p), int(seed))
+        if not h:
+            raise FdmGpuError(1, lib().fdmhost_last_error().decode())
+        return cls(0, _handle=h, skip_boundary_patches=skip_boundary_patches)
+
+    @classmethod
+    def from_mesh(cls, dim, vertices, cells, p, facet_tags=(), seed=0, skip_boundary_patches=True):
+        """Same from arrays: vertices (nv x dim), cells (nc x 2^dim, the reference's
+        corner order), facet_tags [(cell, local_facet, 'dirichlet'|'neumann'|'interior')]."""
+        v = np.zeros((len(vertices), 3))
+        v[:, :dim] = np.asarray(vertices, np.float64)[:, :dim]
+        c = np.ascontiguousarray(np.asarray(cells, np.int32))
+        tc = np.array([t[0] for t in facet_tags], np.int32)
+        tl = np.array([t[1] for t in facet_tags], np.int32)
+        tk = np.array([cls.TAGS[t[2]] for t in facet_tags], np.int32)
+        h = lib().fdmhost_problem_from_mesh(int(dim), len(v), _ptr(np.ascontiguousarray(v)), len(c), _ptr(c), len(tc),
+                                            _ptr(tc) if len(tc) else None, _ptr(tl) if len(tl) else None,
+                                            _ptr(tk) if len(tk) else None, int(p), int(seed))
+        if not h:
+            raise FdmGpuError(1, lib().fdmhost_last_error().decode())
+        return cls(0, _handle=h, skip_boundary_patches=skip_boundary_patches)
+
+    def save_mesh(self, path):
+        """Write the mesh in the reference's JSON format (save_mesh)."""
+        _host_chk(lib().fdmhost_save_mesh(self.h, os.fsencode(path)))
 
     def __del__(self):
         if getattr(self, "h", None) and _lib is not None:

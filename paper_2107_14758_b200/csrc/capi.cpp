@@ -29,17 +29,20 @@ void Context::check_ready(bool need_patches, bool need_factor, bool need_coarse)
 namespace {
 
 // Gather CSR: for each DOF, its (cell, lattice) slots in ascending cell order.
+// skip_absent: entries -1 (absent positions of boundary stars) are left out.
 void build_gather(const std::vector<int32_t>& map, int64_t ndof, std::vector<int32_t>& ptr,
-                  std::vector<int32_t>& idx) {
+                  std::vector<int32_t>& idx, bool skip_absent = false) {
   ptr.assign(ndof + 1, 0);
   for (int32_t g : map) {
+    if (skip_absent && g == -1) continue;
     if (g < 0 || g >= ndof) throw Error(FDMGPU_INVALID_ARGUMENT, "cell map entry out of range");
     ++ptr[g + 1];
   }
   for (int64_t i = 0; i < ndof; ++i) ptr[i + 1] += ptr[i];
-  idx.assign(map.size(), 0);
+  idx.assign(ptr[ndof], 0);
   std::vector<int32_t> pos(ptr.begin(), ptr.end() - 1);
-  for (size_t e = 0; e < map.size(); ++e) idx[pos[map[e]]++] = int32_t(e);
+  for (size_t e = 0; e < map.size(); ++e)
+    if (map[e] >= 0) idx[pos[map[e]]++] = int32_t(e);
 }
 
 double host_dot(Context& c, const double* x, const double* y) {
@@ -532,7 +535,10 @@ fdmgpu_status fdmgpu_set_patches(fdmgpu_handle h, int32_t npatch, const int32_t*
     for (int j = 0; j < npatch; ++j) {
       std::copy(c.h_pdofs.begin() + size_t(j) * L.n + L.nI, c.h_pdofs.begin() + size_t(j + 1) * L.n,
                 sep.begin() + size_t(j) * m);
-      for (int k = 0; k < (1 << c.dim); ++k) nK[c.h_pcells[size_t(j) * (1 << c.dim) + k]] += 1.0;
+      for (int k = 0; k < (1 << c.dim); ++k) {
+        const int K = c.h_pcells[size_t(j) * (1 << c.dim) + k];
+        if (K >= 0) nK[K] += 1.0;
+      }
     }
     c.pdofs.upload(sep, c.stream);
     c.nK.upload(nK, c.stream);
@@ -559,7 +565,7 @@ fdmgpu_status fdmgpu_set_patches(fdmgpu_handle h, int32_t npatch, const int32_t*
       c.pair_b.upload(L.pair_b, c.stream);
     }
     std::vector<int32_t> pptr, pidx;
-    fdmgpu::build_gather(sep, c.ndof, pptr, pidx);  // ascending (patch, position) per separator DOF
+    fdmgpu::build_gather(sep, c.ndof, pptr, pidx, true);  // ascending (patch, position) per separator DOF
     c.pg_ptr.upload(pptr, c.stream);
     c.pg_idx.upload(pidx, c.stream);
     c.corr.alloc(size_t(npatch) * m);
@@ -573,10 +579,11 @@ fdmgpu_status fdmgpu_set_patches(fdmgpu_handle h, int32_t npatch, const int32_t*
 fdmgpu_status fdmgpu_set_coarse(fdmgpu_handle h, int32_t ndof_c, const double* cinv, const int64_t* P_ptr,
                                 const int32_t* P_col, const double* P_val) {
   return fdmgpu::guarded(h, [&](Context& c) {
-    if (ndof_c < 1 || !cinv || !P_ptr || !P_col || !P_val) throw Error(FDMGPU_INVALID_ARGUMENT, "set_coarse: bad args");
+    if (ndof_c < 1 || !cinv || !P_ptr) throw Error(FDMGPU_INVALID_ARGUMENT, "set_coarse: bad args");
+    const int64_t nnz = P_ptr[c.ndof];  // 0 when every coarse DOF is constrained
+    if (nnz > 0 && (!P_col || !P_val)) throw Error(FDMGPU_INVALID_ARGUMENT, "set_coarse: bad args");
     c.nc = ndof_c;
     c.cinv.upload(cinv, size_t(ndof_c) * ndof_c, c.stream);
-    const int64_t nnz = P_ptr[c.ndof];
     std::vector<int32_t> ptr(c.ndof + 1), tptr(ndof_c + 1, 0), tcol(nnz);
     std::vector<double> tval(nnz);
     for (int64_t i = 0; i <= c.ndof; ++i) ptr[i] = int32_t(P_ptr[i]);

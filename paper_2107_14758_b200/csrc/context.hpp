@@ -62,6 +62,7 @@ struct DevArray {
 struct PatchLayout {
   int n = 0, nI = 0, m = 0, mpad = 0, nT = 0, ntiles = 0;
   int span = 0;                      // 2p+1 lattice points per axis
+  int ragged = 0;                    // boundary stars embedded in the template (absent positions)
   std::vector<int32_t> lat;          // n: packed patch-lattice coords P (elimination order)
   std::vector<int32_t> pos_of_lat;   // span^d: elimination position or -1
   std::vector<int32_t> tile_row, tile_col, col_start;  // tile pattern, column-major order

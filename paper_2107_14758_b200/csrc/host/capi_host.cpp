@@ -40,6 +40,61 @@ void* fdmhost_problem_create(int config, int n, int p) {
   return out;
 }
 
+// Problem on a mesh file in the reference's JSON format (load_mesh,
+// src/mesh.cpp:375-434); Q_p space, unit coefficient, RHS U[-1,1] from seed.
+void* fdmhost_problem_from_mesh_file(const char* path, int p, uint64_t seed) {
+  Problem* out = nullptr;
+  if (guard([&] { out = make_problem_from_mesh(load_mesh(path), p, seed).release(); })) return nullptr;
+  return out;
+}
+
+// Same from arrays: vertices (nv x 3), cells (nc x 2^dim), facet tags
+// (cell, local facet 2*axis + (side > 0), tag 0/1/2 = interior/dirichlet/neumann).
+void* fdmhost_problem_from_mesh(int dim, int nv, const double* vertices, int nc, const int32_t* cells, int ntag,
+                                const int32_t* tag_cell, const int32_t* tag_local_facet, const int32_t* tag_kind,
+                                int p, uint64_t seed) {
+  Problem* out = nullptr;
+  if (guard([&] {
+        if (dim < 2 || dim > 3 || nv < 1 || nc < 1 || !vertices || !cells)
+          throw std::invalid_argument("problem_from_mesh: bad mesh arrays");
+        Mesh m;
+        m.dim = dim;
+        for (int v = 0; v < nv; ++v) m.vertices.push_back({vertices[3 * v], vertices[3 * v + 1], vertices[3 * v + 2]});
+        const int ncorner = 1 << dim;
+        for (int c = 0; c < nc; ++c) {
+          m.cells.emplace_back(cells + size_t(c) * ncorner, cells + size_t(c + 1) * ncorner);
+          for (int v : m.cells.back())
+            if (v < 0 || v >= nv) throw std::invalid_argument("problem_from_mesh: cell vertex out of range");
+        }
+        m.finalize();
+        if (ntag > 0) {
+          for (int k = 0; k < ntag; ++k)
+            if (tag_kind[k] < 0 || tag_kind[k] > 2) throw std::invalid_argument("problem_from_mesh: bad facet tag");
+          apply_facet_tags(m, std::vector<int>(tag_cell, tag_cell + ntag),
+                           std::vector<int>(tag_local_facet, tag_local_facet + ntag),
+                           std::vector<int>(tag_kind, tag_kind + ntag));
+        }
+        check_orientation(m);
+        out = make_problem_from_mesh(std::move(m), p, seed).release();
+      }))
+    return nullptr;
+  return out;
+}
+
+int fdmhost_save_mesh(void* ph, const char* path) {
+  return guard([&] { save_mesh(static_cast<Problem*>(ph)->mesh, path); });
+}
+
+// SolverConfig::skip_boundary_patches (include/fdmstar/schwarz.hpp:24): the
+// problems are built with true (the configs' setting); false adds the
+// boundary-vertex stars as the reference default does (src/schwarz.cpp:71-81).
+int fdmhost_problem_set_skip_boundary_patches(void* ph, int skip) {
+  return guard([&] {
+    Problem& P = *static_cast<Problem*>(ph);
+    P.patches = vertex_patches(P.space, skip != 0);
+  });
+}
+
 void fdmhost_problem_destroy(void* ph) { delete static_cast<Problem*>(ph); }
 
 // out: dim, p, ncells, ndof, nfree, npatch, nvertices, npc, sum n_j, ncoarse,

@@ -14,6 +14,8 @@
 #include <map>
 #include <memory>
 #include <string>
+#include <random>
+#include <string>
 #include <vector>
 
 namespace fdmgpu::host {
@@ -56,6 +58,7 @@ Basis1D make_bundle(int p);  // src/assembly.cpp:37-54 (CG family)
 struct Facet {
   std::array<int, 2> cell{-1, -1}, axis{-1, -1}, side{0, 0};
   bool flip = false, oriented = true;
+  int tag = 0;  // 0 interior, 1 dirichlet, 2 neumann (FacetTag, include/fdmstar/mesh.hpp)
   std::vector<int> vertices;
   int ncells() const { return cell[1] >= 0 ? 2 : 1; }
 };
@@ -69,8 +72,16 @@ struct Mesh {
   int num_cells() const { return int(cells.size()); }
   int num_vertices() const { return int(vertices.size()); }
   double coeff(int c) const { return kappa.empty() ? 1.0 : kappa[c]; }
-  void finalize();  // src/mesh.cpp:33-91
+  void finalize();  // src/mesh.cpp:33-91 (boundary facets tagged dirichlet)
+  int find_facet(int cell, int axis, int side) const;  // -1 if absent
 };
+void jacobian(const Mesh& m, int cell, const double* xh, double* J);
+// Mesh files (src/mesh.cpp:354-434): the reference's JSON document.
+Mesh load_mesh(const std::string& path);
+void save_mesh(const Mesh& m, const std::string& path);
+void apply_facet_tags(Mesh& m, const std::vector<int>& cell, const std::vector<int>& local_facet,
+                      const std::vector<int>& tag);
+void check_orientation(const Mesh& m);
 Mesh cartesian_mesh(int dim, const std::vector<int>& counts, const std::vector<double>& lengths);
 Mesh tensor_grid_mesh(int dim, const std::vector<std::vector<double>>& coords);
 std::vector<char> boundary_vertices(const Mesh& m);
@@ -145,5 +156,8 @@ struct Problem {
   Coarse coarse;
 };
 std::unique_ptr<Problem> make_problem(int config, int n_override, int p_override);
+// Space, RHS (U[-1,1], or N(0,1) when `normal`, from `rng`), cell data, patches, coarse level.
+void finish_problem(Problem& pb, std::mt19937_64& rng, bool normal);
+std::unique_ptr<Problem> make_problem_from_mesh(Mesh mesh, int p, uint64_t seed);
 
 }  // namespace fdmgpu::host

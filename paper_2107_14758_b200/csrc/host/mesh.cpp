@@ -63,21 +63,6 @@ double det3(const double* J, int d) {  // J row-major d x d
 }
 
 // Jacobian of the multilinear map at xhat (src/geometry.cpp:33-43), row-major.
-void jacobian(const Mesh& m, int cell, const double* xh, double* J) {
-  const int d = m.dim;
-  for (int k = 0; k < d * d; ++k) J[k] = 0.0;
-  for (int b = 0; b < (1 << d); ++b) {
-    const auto& v = m.vertices[m.cells[cell][b]];
-    for (int a = 0; a < d; ++a) {
-      double g = 1.0;
-      for (int e = 0; e < d; ++e) {
-        const bool hi = (b >> e) & 1;
-        g *= (e == a) ? (hi ? 0.5 : -0.5) : (hi ? 0.5 * (1.0 + xh[e]) : 0.5 * (1.0 - xh[e]));
-      }
-      for (int r = 0; r < d; ++r) J[r * d + a] += g * v[r];
-    }
-  }
-}
 
 // G = det * J^{-1} J^{-T} (row-major d x d), via the adjugate.
 void metric(const double* J, int d, double& det, double* G) {
@@ -104,6 +89,22 @@ void metric(const double* J, int d, double& det, double* G) {
 }
 
 }  // namespace
+
+void jacobian(const Mesh& m, int cell, const double* xh, double* J) {
+  const int d = m.dim;
+  for (int k = 0; k < d * d; ++k) J[k] = 0.0;
+  for (int b = 0; b < (1 << d); ++b) {
+    const auto& v = m.vertices[m.cells[cell][b]];
+    for (int a = 0; a < d; ++a) {
+      double g = 1.0;
+      for (int e = 0; e < d; ++e) {
+        const bool hi = (b >> e) & 1;
+        g *= (e == a) ? (hi ? 0.5 : -0.5) : (hi ? 0.5 * (1.0 + xh[e]) : 0.5 * (1.0 - xh[e]));
+      }
+      for (int r = 0; r < d; ++r) J[r * d + a] += g * v[r];
+    }
+  }
+}
 
 void Mesh::finalize() {
   facets.clear();
@@ -143,6 +144,8 @@ void Mesh::finalize() {
         }
       }
   }
+  for (auto& f : facets)
+    if (f.ncells() == 1 && f.tag == 0) f.tag = 1;  // src/mesh.cpp:82
   vertex_cells.assign(num_vertices(), {});
   for (int c = 0; c < num_cells(); ++c)
     for (int v : cells[c]) vertex_cells[v].push_back(c);
@@ -333,7 +336,9 @@ Space q_space(const Mesh& m, int p) {
       }
       s.multiplicity[dof] += 1.0;
       for (int k = 0; k < nif; ++k)
-        if (m.facets[cf[K][2 * iax[k] + (isd[k] > 0)]].ncells() == 1) s.constrained[dof] = 1;
+        if (m.facets[cf[K][2 * iax[k] + (isd[k] > 0)]].ncells() == 1 &&
+            m.facets[cf[K][2 * iax[k] + (isd[k] > 0)]].tag == 1)
+          s.constrained[dof] = 1;  // src/discretization.cpp:221-226 (Dirichlet facets)
       s.label_cls[dof] = cls;
       s.label_entity[dof] = entity;
       for (int a = 0; a < d; ++a) {
@@ -417,7 +422,7 @@ Patches vertex_patches(const Space& s, bool skip_boundary) {
   for (int j = 0; j < np; ++j)
     for (int k = 0; k < (1 << m.dim); ++k)
       if (P.cells[size_t(j) * (1 << m.dim) + k] >= 0) cell_patches[P.cells[size_t(j) * (1 << m.dim) + k]].push_back(j);
-  P.colour.assign(np, -1);
+  P.colour.assign(P.vertex.size(), -1);
   for (int j = 0; j < np; ++j) {
     std::set<int> used;
     for (int k = 0; k < (1 << m.dim); ++k) {

@@ -55,34 +55,39 @@ std::unique_ptr<Problem> make_problem(int config, int n_override, int p_override
           for (int a = 0; a < d; ++a) pb->mesh.vertices[v][a] += 0.1 * h * uni(rng);
     }
   }
-  pb->basis = make_bundle(pb->p);
-  pb->space = q_space(pb->mesh, pb->p);
-  pb->space.mesh = &pb->mesh;
-  pb->rhs.resize(pb->space.ndof);
-  if (config == 3) {
-    std::normal_distribution<double> nd(0.0, 1.0);
-    for (auto& v : pb->rhs) v = nd(rng);
-  } else {
-    for (auto& v : pb->rhs) v = uni(rng);
-  }
-  for (int i = 0; i < pb->space.ndof; ++i)
-    if (pb->space.constrained[i]) pb->rhs[i] = 0.0;
-  const int nc = pb->mesh.num_cells(), ncorner = 1 << d;
-  pb->cell_kind.resize(nc);
-  pb->cell_mu.resize(size_t(nc) * d);
-  pb->cell_xyz.resize(size_t(nc) * ncorner * 3);
-  pb->cell_kappa.resize(nc);
-  for (int c = 0; c < nc; ++c) {
-    CellCoeffs cc = cell_coeffs(pb->mesh, c, pb->basis);
-    pb->cell_kind[c] = uint8_t(cc.kind);
-    for (int a = 0; a < d; ++a) pb->cell_mu[size_t(c) * d + a] = cc.mu[a];
-    for (int b = 0; b < ncorner; ++b)
-      for (int r = 0; r < 3; ++r) pb->cell_xyz[(size_t(c) * ncorner + b) * 3 + r] = pb->mesh.vertices[pb->mesh.cells[c][b]][r];
-    pb->cell_kappa[c] = pb->mesh.coeff(c);
-  }
-  pb->patches = vertex_patches(pb->space, /*skip_boundary=*/true);
-  pb->coarse = build_coarse(pb->mesh, pb->space, pb->basis);
+  finish_problem(*pb, rng, config == 3);
   return pb;
+}
+
+void finish_problem(Problem& pb, std::mt19937_64& rng, bool normal) {
+  std::uniform_real_distribution<double> uni(-1.0, 1.0);
+  pb.basis = make_bundle(pb.p);
+  pb.space = q_space(pb.mesh, pb.p);
+  pb.space.mesh = &pb.mesh;
+  pb.rhs.resize(pb.space.ndof);
+  if (normal) {
+    std::normal_distribution<double> nd(0.0, 1.0);
+    for (auto& v : pb.rhs) v = nd(rng);
+  } else {
+    for (auto& v : pb.rhs) v = uni(rng);
+  }
+  for (int i = 0; i < pb.space.ndof; ++i)
+    if (pb.space.constrained[i]) pb.rhs[i] = 0.0;
+  const int d = pb.dim, nc = pb.mesh.num_cells(), ncorner = 1 << d;
+  pb.cell_kind.resize(nc);
+  pb.cell_mu.resize(size_t(nc) * d);
+  pb.cell_xyz.resize(size_t(nc) * ncorner * 3);
+  pb.cell_kappa.resize(nc);
+  for (int c = 0; c < nc; ++c) {
+    CellCoeffs cc = cell_coeffs(pb.mesh, c, pb.basis);
+    pb.cell_kind[c] = uint8_t(cc.kind);
+    for (int a = 0; a < d; ++a) pb.cell_mu[size_t(c) * d + a] = cc.mu[a];
+    for (int b = 0; b < ncorner; ++b)
+      for (int r = 0; r < 3; ++r) pb.cell_xyz[(size_t(c) * ncorner + b) * 3 + r] = pb.mesh.vertices[pb.mesh.cells[c][b]][r];
+    pb.cell_kappa[c] = pb.mesh.coeff(c);
+  }
+  pb.patches = vertex_patches(pb.space, /*skip_boundary=*/true);
+  pb.coarse = build_coarse(pb.mesh, pb.space, pb.basis);
 }
 
 }  // namespace fdmgpu::host

@@ -30,6 +30,7 @@ struct PatchArgs {
   const int32_t* lat;
   const int32_t* pos_of_lat;
   const int32_t* pcells;
+  const int32_t* psep;  // npatch x m separator DOFs, -1 = absent (boundary star)
   const double* mu;
   const double* At;
   const double* Bt;
@@ -51,6 +52,7 @@ PatchArgs make_args(Context& c) {
   a.lat = c.lat.p;
   a.pos_of_lat = c.pos_of_lat.p;
   a.pcells = c.pcells.p;
+  a.psep = c.pdofs.p;
   a.mu = c.mu.p;
   a.At = c.At.p;
   a.Bt = c.Bt.p;
@@ -105,7 +107,8 @@ __device__ __forceinline__ double facet_coupling(const PatchArgs& a, const doubl
 }
 
 // Entry (r, c) of the separator Schur complement S_G, r,c in [0, m).
-__device__ double schur_entry(const PatchArgs& a, const double* __restrict__ mu_patch, int r, int c,
+// smask: star slots holding a cell (boundary stars miss some).
+__device__ double schur_entry(const PatchArgs& a, const double* __restrict__ mu_patch, int smask, int r, int c,
                               const double* At, const double* Bt) {
   int P[3] = {0, 0, 0}, Q[3] = {0, 0, 0};
   unpack(a.lat[a.nI + r], P);
@@ -125,6 +128,7 @@ __device__ double schur_entry(const PatchArgs& a, const double* __restrict__ mu_
       for (int s0 = lo[0]; s0 <= hi[0]; ++s0) {
         const int s[3] = {s0, s1, s2};
         const int slot = s0 | (s1 << 1) | (s2 << 2);
+        if (!((smask >> slot) & 1)) continue;
         const double* mus = mu_patch + slot * a.dim;
         int lr[3] = {0, 0, 0}, lc[3] = {0, 0, 0};
         for (int b = 0; b < a.dim; ++b) {
@@ -186,17 +190,26 @@ __global__ void k_patch_assemble(PatchArgs a, int nentries, const int32_t* __res
     At[i] = a.At[i];
     Bt[i] = a.Bt[i];
   }
+  int smask = 0;
+  for (int s = 0; s < ncorner; ++s) smask |= (a.pcells[size_t(j) * ncorner + s] >= 0) << s;
   for (int i = threadIdx.x; i < ncorner * a.dim; i += blockDim.x) {
-    const int s = i / a.dim, q = i % a.dim;
-    mup[i] = a.mu[size_t(a.pcells[size_t(j) * ncorner + s]) * a.dim + q];
+    const int s = i / a.dim, q = i % a.dim, K = a.pcells[size_t(j) * ncorner + s];
+    mup[i] = K >= 0 ? a.mu[size_t(K) * a.dim + q] : 0.0;
   }
   __syncthreads();
   double* base = tiles + size_t(j) * a.ntiles * TT;
+  const int32_t* sep = a.psep + size_t(j) * a.m;
+  const bool whole = smask == (1 << ncorner) - 1;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nentries; e += gridDim.x * blockDim.x) {
     const int code = entries[e];
     const int t = code >> 12, cc = (code >> 6) & 63, rr = code & 63;
     const int r = tile_row[t] * T + rr, c = tile_col[t] * T + cc;
-    base[size_t(t) * TT + tsw(rr, cc)] = schur_entry(a, mup, r, c, At, Bt);
+    double v;
+    if (!whole && (sep[r] < 0 || sep[c] < 0))
+      v = r == c ? 1.0 : 0.0;  // absent position of a boundary star: decoupled identity row
+    else
+      v = schur_entry(a, mup, smask, r, c, At, Bt);
+    base[size_t(t) * TT + tsw(rr, cc)] = v;
   }
 }
 
@@ -208,8 +221,10 @@ __global__ void k_patch_pad_check(PatchArgs a, double* __restrict__ tiles, int l
   for (int r = a.m + threadIdx.x; r < a.mpad; r += blockDim.x) dt[tsw(r % T, r % T)] = 1.0;
   const int ncorner = 1 << a.dim;
   double mup[24];
-  for (int i = 0; i < ncorner * a.dim; ++i)
-    mup[i] = a.mu[size_t(a.pcells[size_t(j) * ncorner + i / a.dim]) * a.dim + i % a.dim];
+  for (int i = 0; i < ncorner * a.dim; ++i) {
+    const int K = a.pcells[size_t(j) * ncorner + i / a.dim];
+    mup[i] = K >= 0 ? a.mu[size_t(K) * a.dim + i % a.dim] : 0.0;
+  }
   for (int k = threadIdx.x; k < a.nI; k += blockDim.x) {
     int P[3] = {0, 0, 0}, s[3] = {0, 0, 0}, l[3] = {0, 0, 0};
     unpack(a.lat[k], P);
@@ -218,6 +233,7 @@ __global__ void k_patch_pad_check(PatchArgs a, double* __restrict__ tiles, int l
       l[b] = P[b] - s[b] * a.p;
     }
     const int slot = s[0] | (s[1] << 1) | (s[2] << 2);
+    if (a.pcells[size_t(j) * ncorner + slot] < 0) continue;  // missing cell of a boundary star
     if (!(diag_interior(a, mup + slot * a.dim, l, a.At, a.Bt) > 0.0)) record_pivot_error(a.err, j, k);
   }
 }
@@ -746,7 +762,7 @@ __global__ void __launch_bounds__(kSolveThreads)
   // ---- phase A: gather the Schur-reduced separator RHS (the interior elimination
   // was folded into the S^T cell kernel: bhat is patch independent) ----------------
   const int32_t* pdI = pdofs + size_t(j) * a.m;
-  for (int r = tid; r < a.mpad; r += NC) y[r] = r < a.m ? rt[pdI[r]] : 0.0;
+  for (int r = tid; r < a.mpad; r += NC) y[r] = (r < a.m && pdI[r] >= 0) ? rt[pdI[r]] : 0.0;
   for (int r = tid; r < SB8; r += NC) zblk[r] = 0.0;
   named_sync(1, NC);
 

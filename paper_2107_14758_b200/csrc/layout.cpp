@@ -38,9 +38,19 @@ inline void unpack(int32_t v, int* P) {
 }  // namespace
 
 // Builds c.L, c.h_pdofs, c.h_pcells from the patch lists.
+//
+// Boundary stars (SolverConfig::skip_boundary_patches = false, the reference
+// default, src/schwarz.cpp:71-81) have fewer than 2^d cells and lose their
+// constrained DOFs; they are embedded in the same (2p-1)^d template: missing
+// cells leave their slot empty (-1), absent positions get pdofs = -1 and an
+// identity row in the separator factor, so every patch shares one symbolic
+// layout.  The reference eliminates only the DOFs a star has; a decoupled
+// identity row changes no other entry of the factor, so the solution is the
+// same up to rounding.
 void analyze_patches(Context& c, int npatch, const int32_t* vertex, const int64_t* ptr, const int32_t* dofs,
                      const int32_t* perm, const int32_t* star_cells) {
   const int d = c.dim, p = c.p, n1 = p + 1, ncorner = 1 << d;
+  if (p < 2 || p > 31) throw Error(FDMGPU_UNSUPPORTED, "patch layout needs 2 <= p <= 31");
   PatchLayout& L = c.L;
   L = PatchLayout();
   L.span = 2 * p + 1;
@@ -52,25 +62,64 @@ void analyze_patches(Context& c, int npatch, const int32_t* vertex, const int64_
   L.n = expect_n;
   L.nI = expect_nI;
   L.m = L.n - L.nI;
-  c.h_pdofs.assign(size_t(npatch) * L.n, 0);
+  c.h_pdofs.assign(size_t(npatch) * L.n, -1);
   c.h_pcells.assign(size_t(npatch) * ncorner, -1);
-  std::vector<int32_t> where(c.ndof, -1), touched;
-  std::vector<int32_t> lat0;
-  for (int j = 0; j < npatch; ++j) {
+  std::vector<int32_t> where(c.ndof, -1), touched, inpatch(c.ndof, -1);
+  auto corner_lin = [&](int cb) {
+    int l = 0, stride = 1;
+    for (int a = 0; a < d; ++a, stride *= n1) l += ((cb >> a) & 1) * p * stride;
+    return l;
+  };
+  auto is_full = [&](int j) {
+    if (ptr[j + 1] - ptr[j] != L.n) return false;
+    for (int k = 0; k < ncorner; ++k)
+      if (star_cells[size_t(j) * ncorner + k] < 0) return false;
+    return true;
+  };
+  // Lattice code of every DOF of patch j, in its own elimination order, and
+  // the slot of each star cell.  The corner of cell K at the patch vertex:
+  // for a full star, the corner holding the vertex DOF (eliminated last);
+  // otherwise the corner that maps all of K's patch DOFs into [1, 2p-1]^d,
+  // axes the present DOFs leave free taking side 0 (a star cell adjacent to
+  // another across axis a always holds free DOFs of their shared facet, so
+  // such a choice never puts two cells in one slot).
+  auto map_patch = [&](int j, std::vector<int32_t>& latj) {
     const int64_t b = ptr[j], nj = ptr[j + 1] - ptr[j];
-    if (nj != L.n)
+    if (nj < 1 || nj > L.n)
       throw Error(FDMGPU_UNSUPPORTED, "patch " + std::to_string(j) + " (vertex " + std::to_string(vertex[j]) +
-                                          ") has " + std::to_string(nj) + " DOFs, expected (2p-1)^d = " +
-                                          std::to_string(L.n) + " (boundary or non-lattice star)");
-    const int gv = dofs[b + perm[b + nj - 1]];  // the vertex DOF is eliminated last
+                                          ") has " + std::to_string(nj) + " DOFs, at most (2p-1)^d = " +
+                                          std::to_string(L.n) + " fit the star lattice");
+    const bool full = is_full(j);
+    for (int64_t k = 0; k < nj; ++k) {
+      const int g = dofs[b + k];
+      if (g < 0 || g >= c.ndof) throw Error(FDMGPU_INVALID_ARGUMENT, "set_patches: DOF out of range");
+      inpatch[g] = j;
+    }
+    const int gv = dofs[b + perm[b + nj - 1]];
     for (int k = 0; k < ncorner; ++k) {
       const int K = star_cells[size_t(j) * ncorner + k];
-      if (K < 0 || K >= c.ncells) throw Error(FDMGPU_UNSUPPORTED, "patch star is not 2^d cells");
+      if (K < 0) continue;
+      if (K >= c.ncells) throw Error(FDMGPU_UNSUPPORTED, "patch star cell out of range");
+      const int32_t* cd = c.h_cell_dofs.data() + size_t(K) * c.npc;
       int bits = -1;
-      for (int cb = 0; cb < ncorner && bits < 0; ++cb) {
-        int l = 0, stride = 1;
-        for (int a = 0; a < d; ++a, stride *= n1) l += ((cb >> a) & 1) * p * stride;
-        if (c.h_cell_dofs[size_t(K) * c.npc + l] == gv) bits = cb;
+      if (full) {
+        for (int cb = 0; cb < ncorner && bits < 0; ++cb)
+          if (cd[corner_lin(cb)] == gv) bits = cb;
+      } else {
+        int need0 = 0, need1 = 0;  // axes on which K's patch DOFs force the corner side
+        int l[3] = {0, 0, 0};
+        for (int lin = 0; lin < c.npc; ++lin) {
+          if (inpatch[cd[lin]] == j)
+            for (int a = 0; a < d; ++a) {
+              if (l[a] == 0) need0 |= 1 << a;
+              if (l[a] == p) need1 |= 1 << a;
+            }
+          for (int a = 0; a < d; ++a) {
+            if (++l[a] <= p) break;
+            l[a] = 0;
+          }
+        }
+        if (!(need0 & need1)) bits = need1;
       }
       if (bits < 0) throw Error(FDMGPU_UNSUPPORTED, "star cell does not contain the patch vertex");
       const int slot = (~bits) & (ncorner - 1);
@@ -85,7 +134,7 @@ void analyze_patches(Context& c, int npatch, const int32_t* vertex, const int64_
           in = in && P[a] >= 1 && P[a] <= 2 * p - 1;
         }
         if (in) {
-          const int g = c.h_cell_dofs[size_t(K) * c.npc + lin];
+          const int g = cd[lin];
           const int32_t code = pack(P);
           if (where[g] == -1) {
             where[g] = code;
@@ -100,20 +149,55 @@ void analyze_patches(Context& c, int npatch, const int32_t* vertex, const int64_
         }
       }
     }
-    std::vector<int32_t> latj(L.n);
-    for (int k = 0; k < L.n; ++k) {
-      const int g = dofs[b + perm[b + k]];
-      c.h_pdofs[size_t(j) * L.n + k] = g;
-      latj[k] = where[g];
+    latj.assign(nj, -1);
+    for (int64_t k = 0; k < nj; ++k) {
+      latj[k] = where[dofs[b + perm[b + k]]];
       if (latj[k] < 0) throw Error(FDMGPU_UNSUPPORTED, "patch DOF outside its star lattice");
     }
     for (int g : touched) where[g] = -1;
     touched.clear();
-    if (j == 0)
-      lat0 = latj;
-    else if (latj != lat0)
+    return full;
+  };
+  // Canonical template: the elimination order of the first full star (all
+  // full stars must share it); with no full star, a synthetic order with the
+  // interiors first, then facets, edges and the vertex, each lexicographic.
+  std::vector<int32_t> lat0, latj;
+  int j0 = -1;
+  for (int j = 0; j < npatch && j0 < 0; ++j)
+    if (is_full(j)) j0 = j;
+  if (j0 >= 0) {
+    map_patch(j0, lat0);
+    std::fill(c.h_pcells.begin() + size_t(j0) * ncorner, c.h_pcells.begin() + size_t(j0 + 1) * ncorner, -1);
+  } else {
+    for (int cls = 0; cls <= d; ++cls) {  // number of coordinates at the vertex plane P_a = p
+      int P[3] = {0, 0, 0};
+      for (int lin = 0; lin < L.n; ++lin) {
+        int t = lin, cnt = 0;
+        for (int a = 0; a < d; ++a) {
+          P[a] = 1 + t % (2 * p - 1);
+          t /= 2 * p - 1;
+          cnt += P[a] == p;
+        }
+        if (cnt == cls) lat0.push_back(pack(P));
+      }
+    }
+  }
+  auto key = [](int32_t code) { return (code & 63) | (((code >> 8) & 63) << 6) | (((code >> 16) & 63) << 12); };
+  std::vector<int32_t> pos0(size_t(1) << 18, -1);  // 2p - 1 <= 63
+  for (int k = 0; k < L.n; ++k) pos0[key(lat0[k])] = k;
+  L.ragged = 0;
+  for (int j = 0; j < npatch; ++j) {
+    const int64_t b = ptr[j];
+    const bool full = map_patch(j, latj);
+    if (full && latj != lat0)
       throw Error(FDMGPU_UNSUPPORTED, "patch " + std::to_string(j) +
                                           " does not share the canonical elimination order (non-lattice mesh)");
+    if (!full) ++L.ragged;
+    for (size_t k = 0; k < latj.size(); ++k) {
+      const int t = pos0[key(latj[k])];
+      if (t < 0) throw Error(FDMGPU_UNSUPPORTED, "patch DOF outside its star lattice");
+      c.h_pdofs[size_t(j) * L.n + t] = dofs[b + perm[b + k]];
+    }
   }
   // Internal separator elimination order.  Default (sep_order 0, "plane"):
   // the facet groups plane by plane -- the facets of one plane never share a
