@@ -374,6 +374,13 @@ fdmgpu_status fdmgpu_create(fdmgpu_handle* out, int32_t dim, int32_t p, int32_t 
     cc.force_staged = fs && fs[0] == '1';
     const char* so = std::getenv("FDMGPU_SEP_ORDER");
     cc.sep_order = (so && std::string(so) == "reference") ? 1 : 0;
+    // Separator solve split: the last partial wave of patches runs on clusters
+    // of solve_cs CTAs (default 2; FDMGPU_SOLVE_CS=1 keeps one CTA per patch,
+    // FDMGPU_SOLVE_TAIL=0 splits every patch).
+    const char* cs = std::getenv("FDMGPU_SOLVE_CS");
+    if (cs && cs[0] >= '1' && cs[0] <= '4' && cs[1] == 0) cc.solve_cs = cs[0] - '0';
+    const char* st = std::getenv("FDMGPU_SOLVE_TAIL");
+    cc.solve_tail = !(st && st[0] == '0');
     cc.E.alloc(size_t(cc.ncells) * cc.npc);
     for (auto& v : cc.w) v.alloc(cc.ndof);
     cc.red.alloc(4 * fdmgpu::kRedBlocks);

@@ -125,6 +125,10 @@ struct Context {
   DevArray<uint8_t> tile_hdr;
   DevArray<double> corr, tiles, nK;
   std::vector<int32_t> h_pdofs, h_pcells;
+  int solve_cs = 2;                      // CTAs per split patch in the separator solve (FDMGPU_SOLVE_CS)
+  bool solve_tail = true;                // cluster-split only the last partial wave (FDMGPU_SOLVE_TAIL)
+  int cl_cs = 0;                         // cluster size cl_list / cl_col were built for
+  DevArray<int32_t> cl_list, cl_col;     // per-rank tile lists of the cluster solve
   bool have_patches = false, factored = false;
   DevArray<unsigned long long> d_err;
 

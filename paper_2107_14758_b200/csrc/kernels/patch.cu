@@ -673,7 +673,7 @@ __global__ void __launch_bounds__(kSolveThreads)
     k_patch_solve(PatchArgs a, int ring_len, const double* __restrict__ rt, double* __restrict__ corr,
                   const double* __restrict__ tiles, const int32_t* __restrict__ pdofs,
                   const int32_t* __restrict__ col_start, const int32_t* __restrict__ tile_row,
-                  const int32_t* __restrict__ rec_off) {
+                  const int32_t* __restrict__ rec_off, int j0) {
   extern __shared__ __align__(128) double sm[];
   double* ring = sm;                          // ring_len doubles
   double* y = ring + ring_len;                // mpad
@@ -682,7 +682,7 @@ __global__ void __launch_bounds__(kSolveThreads)
   uint64_t* full = reinterpret_cast<uint64_t*>(zblk + SB8);
   uint64_t* empty = full + kRingEntries;
   int* slot_off = reinterpret_cast<int*>(empty + kRingEntries);  // ring offset of entry e's record
-  const int j = blockIdx.x;
+  const int j = j0 + blockIdx.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const double* tb = tiles + size_t(j) * a.ntiles * TT;
   pdl_trigger();
@@ -864,6 +864,259 @@ __global__ void __launch_bounds__(kSolveThreads)
   for (int r = tid; r < a.m; r += NC) cj[r] = y[r];
 }
 
+// Cluster variant: one patch per cluster of CS CTAs (SMs).  Tile row I of
+// the separator factor belongs to CTA I % CS, which streams exactly the
+// records of its rows (forward, then backward by column) through its own
+// ring, keeps y_I, and solves the diagonal tiles of its rows.
+//   forward  column K: the owner of K solves y_K = L_KK^{-1} y_K and
+//            broadcasts it with st.async into every CTA's y (completing
+//            fbar[K] there); each CTA then applies its tiles (I, K).
+//   backward column K: each CTA sums L_IK^T x_I over its tiles into one
+//            64-vector and st.asyncs it into slot `rank` of the owner's psum
+//            (completing pbar[K]); the owner subtracts the CS partials in
+//            rank order, solves x_K = L_KK^{-T} u and broadcasts x_K (bbar[K]).
+// Every barrier is used for exactly one phase; a partial for column K is
+// sent only after x_{K+1} arrived, i.e. after every owner consumed the psum
+// slot's previous use.  Same arithmetic per tile as k_patch_solve; only the
+// order of the backward partial sums differs (rounding level).  This spreads
+// one patch's dependency chain over CS SMs: a lone patch is latency bound
+// (0.38 ms at C3), so the last partial wave of single-CTA patches wastes HBM
+// bandwidth that CS-way patches recover.
+template <int CS>
+__global__ void __launch_bounds__(kSolveThreads)
+    k_patch_solve_cl(PatchArgs a, int ring_len, const double* __restrict__ rt, double* __restrict__ corr,
+                     const double* __restrict__ tiles, const int32_t* __restrict__ pdofs,
+                     const int32_t* __restrict__ tile_row, const int32_t* __restrict__ rec_off,
+                     const int32_t* __restrict__ cl_list, const int32_t* __restrict__ cl_col, int j0) {
+  extern __shared__ __align__(128) double sm[];
+  double* ring = sm;                              // ring_len doubles
+  double* y = ring + ring_len;                    // mpad (owned rows; broadcast y_K / x_K)
+  double* part = y + a.mpad;                      // 2 x kSolveConsumers x T
+  double* psum = part + 2 * kSolveConsumers * T;  // CS x T backward partials (owner side)
+  double* zblk = psum + CS * T;                   // SB8 zeros
+  uint64_t* full = reinterpret_cast<uint64_t*>(zblk + SB8);
+  uint64_t* empty = full + kRingEntries;
+  uint64_t* fbar = empty + kRingEntries;  // nT
+  uint64_t* bbar = fbar + a.nT;           // nT
+  uint64_t* pbar = bbar + a.nT;           // nT
+  int* slot_off = reinterpret_cast<int*>(pbar + a.nT);
+  const int rank = int(cluster_ctarank());
+  const int j = j0 + blockIdx.x / CS;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const double* tb = tiles + size_t(j) * a.ntiles * TT;
+  const int32_t* col = cl_col + rank * (a.nT + 1);
+  pdl_trigger();
+  if (tid < kRingEntries) {
+    mbar_init(&full[tid], 1);
+    mbar_init(&empty[tid], 1);
+  }
+  for (int K = tid; K < a.nT; K += blockDim.x) {
+    mbar_init(&fbar[K], 1);
+    mbar_init(&bbar[K], 1);
+    mbar_init(&pbar[K], 1);
+    mbar_arrive_expect_tx(&fbar[K], T * sizeof(double));
+    mbar_arrive_expect_tx(&bbar[K], T * sizeof(double));
+    if (K % CS == rank) mbar_arrive_expect_tx(&pbar[K], CS * T * sizeof(double));
+  }
+  mbar_fence_init();
+  cluster_sync_all();
+
+  if (warp == kSolveConsumers) {
+    if (lane == 0) {
+      int q = 0, qt = 0, head = 0;
+      const uint64_t pol_keep = policy_evict_last(), pol_stream = policy_evict_first();
+      auto release_oldest = [&]() {
+        mbar_wait(&empty[qt & (kRingEntries - 1)], (qt / kRingEntries) & 1);
+        ++qt;
+      };
+      auto issue = [&](int t, uint64_t pol) {
+        const int len = rec_off[t + 1] - rec_off[t];
+        while (q - qt >= kRingEntries) release_oldest();
+        for (;;) {
+          if (qt == q) {
+            if (head + len > ring_len) head = 0;
+            break;
+          }
+          const int tail = slot_off[qt & (kRingEntries - 1)];
+          if (tail < head) {
+            if (head + len <= ring_len) break;
+            if (len <= tail) {
+              head = 0;
+              break;
+            }
+          } else if (tail > head && head + len <= tail) {
+            break;
+          }
+          release_oldest();
+        }
+        const int e = q & (kRingEntries - 1);
+        slot_off[e] = head;
+        const uint32_t bytes = uint32_t(len) * sizeof(double);
+        mbar_arrive_expect_tx(&full[e], bytes);
+        bulk_g2s_hint(ring + head, tb + rec_off[t], bytes, &full[e], pol);
+        head += len;
+        ++q;
+      };
+      for (int i = col[0]; i < col[a.nT]; ++i) issue(cl_list[i], pol_keep);
+      for (int K = a.nT - 1; K >= 0; --K) {
+        const int s0 = col[K], s1 = col[K + 1], own = (K % CS == rank) ? 1 : 0;
+        for (int i = s0 + own; i < s1; ++i) issue(cl_list[i], pol_stream);
+        if (own) issue(cl_list[s0], pol_stream);
+      }
+    }
+  } else {
+    constexpr int NC = 32 * kSolveConsumers;
+    const int rl = lane & 7, g = lane >> 3;
+    auto acquire = [&](int q) {
+      const int e = q & (kRingEntries - 1);
+      mbar_wait(&full[e], (q / kRingEntries) & 1);
+      return ring + slot_off[e];
+    };
+    auto release = [&](int q) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[q & (kRingEntries - 1)]);
+    };
+    pdl_wait();
+    // ---- phase A: this CTA's rows of the Schur-reduced separator RHS
+    const int32_t* pdI = pdofs + size_t(j) * a.m;
+    for (int r = tid; r < a.mpad; r += NC)
+      if ((r / T) % CS == rank) y[r] = (r < a.m && pdI[r] >= 0) ? rt[pdI[r]] : 0.0;
+    for (int r = tid; r < SB8; r += NC) zblk[r] = 0.0;
+    named_sync(1, NC);
+
+    // ---- phase B: forward substitution
+    int q = 0;
+    double o0, o1;
+    double xr[64];
+    for (int K = 0; K < a.nT; ++K) {
+      const int s0 = col[K], own = (K % CS == rank) ? 1 : 0, noff = col[K + 1] - s0 - own;
+      double* yK = y + K * T;
+      if (own) {
+        if (warp == (q & 7)) {
+          load_x(yK, xr);
+          const double* rec = acquire(q);
+          tile_fwd(rec, zblk, rl, g, xr, o0, o1);
+          release(q);
+#pragma unroll
+          for (int d = 0; d < CS; ++d) {
+            const uint32_t bar = dsmem_addr(&fbar[K], d);
+            st_async_f64(dsmem_addr(yK + 8 * g + rl, d), o0, bar);
+            st_async_f64(dsmem_addr(yK + 8 * (7 - g) + rl, d), o1, bar);
+          }
+        }
+        ++q;
+      }
+      int i = (warp - q) & 7;
+      if (i < noff) {
+        mbar_wait(&fbar[K], 0);
+        load_x(yK, xr);
+      }
+      for (; i < noff; i += 8) {
+        const int qi = q + i;
+        const double* rec = acquire(qi);
+        tile_fwd(rec, zblk, rl, g, xr, o0, o1);
+        release(qi);
+        double* yI = y + tile_row[cl_list[s0 + own + i]] * T;
+        yI[8 * g + rl] -= o0;
+        yI[8 * (7 - g) + rl] -= o1;
+      }
+      q += noff;
+      named_sync(1, NC);
+    }
+
+    // ---- phase C: backward substitution, columns descending
+    double acc[2][8];
+    for (int K = a.nT - 1; K >= 0; --K) {
+      const int s0 = col[K], own = (K % CS == rank) ? 1 : 0, noff = col[K + 1] - s0 - own;
+      double* pw = part + ((K & 1) * kSolveConsumers + warp) * T;
+      int i = (warp - q) & 7;
+      if (i < noff) {
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+          for (int k = 0; k < 8; ++k) acc[jj][k] = 0.0;
+        for (; i < noff; i += 8) {
+          const int qi = q + i, I = tile_row[cl_list[s0 + own + i]];
+          mbar_wait(&bbar[I], 0);
+          const double* yI = y + I * T;
+          double yv[8];
+#pragma unroll
+          for (int bi = 0; bi < 8; ++bi) yv[bi] = yI[8 * bi + rl];
+          const double* rec = acquire(qi);
+          tile_bwd(rec, zblk, rl, g, yv, acc);
+          release(qi);
+        }
+        double s0v, s1v;
+        int c;
+        reduce_cols(acc, lane, s0v, s1v, c);
+        pw[c] = s0v;
+        pw[c + 1] = s1v;
+      } else {
+        pw[lane] = 0.0;
+        pw[lane + 32] = 0.0;
+      }
+      q += noff;
+      named_sync(1, NC);
+      if (warp == (q & 7)) {
+        const double* pk = part + (K & 1) * kSolveConsumers * T;
+        double u0 = 0.0, u1 = 0.0;
+#pragma unroll
+        for (int w = 0; w < kSolveConsumers; ++w) {
+          u0 += pk[w * T + lane];
+          u1 += pk[w * T + lane + 32];
+        }
+        if (K + 1 < a.nT) mbar_wait(&bbar[K + 1], 0);  // the owner's psum slot is free again
+        const int dst = K % CS;
+        const uint32_t pb = dsmem_addr(&pbar[K], dst);
+        st_async_f64(dsmem_addr(psum + rank * T + lane, dst), u0, pb);
+        st_async_f64(dsmem_addr(psum + rank * T + lane + 32, dst), u1, pb);
+        if (own) {
+          mbar_wait(&pbar[K], 0);
+          const double* yK = y + K * T;
+          double v0 = yK[lane], v1 = yK[lane + 32];
+#pragma unroll
+          for (int cc = 0; cc < CS; ++cc) {
+            v0 -= psum[cc * T + lane];
+            v1 -= psum[cc * T + lane + 32];
+          }
+          double yv[8];
+#pragma unroll
+          for (int bi = 0; bi < 8; ++bi) {
+            const double t0 = __shfl_sync(0xffffffffu, v0, 8 * (bi & 3) + rl);
+            const double t1 = __shfl_sync(0xffffffffu, v1, 8 * (bi & 3) + rl);
+            yv[bi] = bi < 4 ? t0 : t1;
+          }
+#pragma unroll
+          for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+            for (int k = 0; k < 8; ++k) acc[jj][k] = 0.0;
+          const double* rec = acquire(q);
+          tile_bwd(rec, zblk, rl, g, yv, acc);
+          release(q);
+          double s0v, s1v;
+          int c;
+          reduce_cols(acc, lane, s0v, s1v, c);
+#pragma unroll
+          for (int d = 0; d < CS; ++d)
+            st_async_f64x2(dsmem_addr(y + K * T + c, d), s0v, s1v, dsmem_addr(&bbar[K], d));
+        }
+      }
+      q += own;
+    }
+
+    // ---- phase D: every broadcast landed; write this CTA's rows of x_G
+    for (int K = tid; K < a.nT; K += NC) {
+      mbar_wait(&fbar[K], 0);
+      mbar_wait(&bbar[K], 0);
+    }
+    named_sync(1, NC);
+    double* cj = corr + size_t(j) * a.m;
+    for (int r = tid; r < a.m; r += NC)
+      if ((r / T) % CS == rank) cj[r] = y[r];
+  }
+  cluster_sync_all();  // no CTA leaves while a peer may still write into it
+}
+
 // z[g] = sum of patch corrections of DOF g in ascending patch order
 // (src/schwarz.cpp:49-53 order, no atomics).
 __global__ void k_patch_gather(int64_t ndof, const double* __restrict__ corr, const int32_t* __restrict__ ptr,
@@ -949,6 +1202,42 @@ void launch_patch_trsm(Context& c, int K) {
   FDM_LAUNCH_CHECK(c);
 }
 
+// Cluster solve (k_patch_solve_cl): per-rank tile lists, built once per CS.
+static void build_cluster_lists(Context& c, int cs) {
+  if (c.cl_cs == cs) return;
+  const auto& L = c.L;
+  std::vector<int32_t> list, colp(size_t(cs) * (L.nT + 1));
+  for (int r = 0; r < cs; ++r) {
+    colp[size_t(r) * (L.nT + 1)] = int32_t(list.size());
+    for (int K = 0; K < L.nT; ++K) {
+      for (int t = L.col_start[K]; t < L.col_start[K + 1]; ++t)
+        if (L.tile_row[t] % cs == r) list.push_back(t);  // the diagonal tile (row K) comes first
+      colp[size_t(r) * (L.nT + 1) + K + 1] = int32_t(list.size());
+    }
+  }
+  c.cl_list.upload(list, c.stream);
+  c.cl_col.upload(colp, c.stream);
+  c.cl_cs = cs;
+}
+
+template <int CS>
+static void launch_solve_cl(Context& c, const PatchArgs& a, const double* r_modal, int j0) {
+  const size_t budget = 227 * 1024;
+  const size_t fixed = sizeof(double) * (size_t(c.L.mpad) + 2 * kSolveConsumers * T + CS * T + SB8) +
+                       2 * kRingEntries * sizeof(uint64_t) + 3 * size_t(c.L.nT) * sizeof(uint64_t) +
+                       kRingEntries * sizeof(int);
+  int max_rec = 0;
+  for (int t = 0; t < c.L.ntiles; ++t) max_rec = std::max(max_rec, c.L.tile_poff8[t + 1] - c.L.tile_poff8[t]);
+  const int ring = fixed < budget ? int(((budget - fixed) / sizeof(double)) & ~size_t(15)) : 0;
+  if (ring < max_rec) throw Error(FDMGPU_UNSUPPORTED, "separator too large for the shared-memory cluster solve");
+  const size_t smem = fixed + size_t(ring) * sizeof(double);
+  FDM_CUDA(cudaFuncSetAttribute(k_patch_solve_cl<CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+  launch_cluster(c.pdl && !c.timing, CS, k_patch_solve_cl<CS>, dim3((c.npatch - j0) * CS), dim3(kSolveThreads),
+                 smem, c.stream, a, ring, r_modal, c.corr.p, (const double*)c.tiles.p, (const int32_t*)c.pdofs.p,
+                 (const int32_t*)c.tile_row.p, (const int32_t*)c.tile_poff8.p, (const int32_t*)c.cl_list.p,
+                 (const int32_t*)c.cl_col.p, j0);
+}
+
 // Ring size (doubles) of the separator solve: all shared memory left after
 // the separator vector, the backward partials, the zero block and the barriers.
 static int solve_ring(const Context& c, size_t* smem_out) {
@@ -965,13 +1254,38 @@ static int solve_ring(const Context& c, size_t* smem_out) {
 
 void launch_patch_solve(Context& c, const double* r_modal) {
   PatchArgs a = make_args(c);
+  // Patches [0, nsolo): one CTA each; [nsolo, npatch): cluster-split
+  // (all of them when solve_tail is off).  The cluster part runs first: the
+  // single-CTA launch waits for it (PDL), so the next kernel sees both.
+  int nsolo = 0;
+  // Split only separators of >= 8 tile columns: below that the per-column
+  // cluster exchange costs more than the chain it shortens (C1/C2).
+  if (c.solve_cs > 1 && c.L.nT >= 8) {
+    int nsm = 0;
+    FDM_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c.device));
+    nsolo = c.solve_tail ? (c.npatch / nsm) * nsm : 0;
+    if (nsolo < c.npatch) {
+      build_cluster_lists(c, c.solve_cs);
+      KernelTimer timer(c, 0);
+      switch (c.solve_cs) {
+        case 2: launch_solve_cl<2>(c, a, r_modal, nsolo); break;
+        case 3: launch_solve_cl<3>(c, a, r_modal, nsolo); break;
+        case 4: launch_solve_cl<4>(c, a, r_modal, nsolo); break;
+        default: throw Error(FDMGPU_INVALID_ARGUMENT, "solve cluster size must be 1..4");
+      }
+      FDM_LAUNCH_CHECK(c);
+    }
+    if (nsolo == 0) return;
+  } else {
+    nsolo = c.npatch;
+  }
   size_t smem = 0;
   const int ring = solve_ring(c, &smem);
   FDM_CUDA(cudaFuncSetAttribute(k_patch_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
   KernelTimer timer(c, 0);
-  launch_pdl(c.pdl && !c.timing, k_patch_solve, dim3(c.npatch), dim3(kSolveThreads), smem, c.stream, a, ring, r_modal,
+  launch_pdl(c.pdl && !c.timing, k_patch_solve, dim3(nsolo), dim3(kSolveThreads), smem, c.stream, a, ring, r_modal,
              c.corr.p, (const double*)c.tiles.p, (const int32_t*)c.pdofs.p, (const int32_t*)c.col_start.p,
-             (const int32_t*)c.tile_row.p, (const int32_t*)c.tile_poff8.p);
+             (const int32_t*)c.tile_row.p, (const int32_t*)c.tile_poff8.p, 0);
   FDM_LAUNCH_CHECK(c);
 }
 

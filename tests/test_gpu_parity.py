@@ -320,3 +320,21 @@ def test_two_level_with_boundary_stars_reference_pins(pkg, oracle, torch):
         assert rep["iterations"] == rr["iterations"]
         its.append(rep["iterations"])
     assert max(its) - min(its) <= 2
+
+
+@pytest.mark.parametrize("cs,tail", [("1", "1"), ("2", "0"), ("3", "0"), ("4", "0"), ("2", "1")])
+def test_cluster_split_solve(pkg, oracle, torch, monkeypatch, cs, tail):
+    """k_patch_solve_cl: one patch spread over a cluster of 2-4 CTAs (DSMEM
+    exchange of y_K / x_K and the backward partials) against the oracle and the
+    single-CTA solve; 8 patches with 39 separator tile columns (p = 15)."""
+    monkeypatch.setenv("FDMGPU_SOLVE_CS", cs)
+    monkeypatch.setenv("FDMGPU_SOLVE_TAIL", tail)
+    prob = pkg.Problem(4, 3, 15)
+    sol = pkg.Solver(prob)
+    sol.factor()
+    ref = oracle.Problem(4, 3, 15, build_global=False, threads=os.cpu_count())
+    ref.factor()
+    rt = ref.apply_St(prob.rhs())
+    z = sol.patch_apply(rt)
+    assert rel(z, ref.patch_apply(rt)) <= TOL_RELAX
+    assert np.array_equal(z, sol.patch_apply(rt))  # deterministic
