@@ -375,7 +375,7 @@ fdmgpu_status fdmgpu_create(fdmgpu_handle* out, int32_t dim, int32_t p, int32_t 
     const char* so = std::getenv("FDMGPU_SEP_ORDER");
     cc.sep_order = (so && std::string(so) == "reference") ? 1 : 0;
     // Separator solve split: the last partial wave of patches runs on clusters
-    // of solve_cs CTAs (default 2; FDMGPU_SOLVE_CS=1 keeps one CTA per patch,
+    // of CTAs (FDMGPU_SOLVE_CS=2..4 fixes the size, 1 keeps one CTA per patch;
     // FDMGPU_SOLVE_TAIL=0 splits every patch).
     const char* cs = std::getenv("FDMGPU_SOLVE_CS");
     if (cs && cs[0] >= '1' && cs[0] <= '4' && cs[1] == 0) cc.solve_cs = cs[0] - '0';

@@ -125,10 +125,12 @@ struct Context {
   DevArray<uint8_t> tile_hdr;
   DevArray<double> corr, tiles, nK;
   std::vector<int32_t> h_pdofs, h_pcells;
-  int solve_cs = 2;                      // CTAs per split patch in the separator solve (FDMGPU_SOLVE_CS)
+  int solve_cs = 0;                      // CTAs per split patch (FDMGPU_SOLVE_CS; 0 = auto, 1 = no split)
   bool solve_tail = true;                // cluster-split only the last partial wave (FDMGPU_SOLVE_TAIL)
   int cl_cs = 0;                         // cluster size cl_list / cl_col were built for
   DevArray<int32_t> cl_list, cl_col;     // per-rank tile lists of the cluster solve
+  int cl_fit[5] = {-1, -1, -1, -1, -1};  // co-resident clusters per cluster size (memo)
+  DevArray<unsigned> tail_sync;          // finished split-tail CTAs, completed calls
   bool have_patches = false, factored = false;
   DevArray<unsigned long long> d_err;
 

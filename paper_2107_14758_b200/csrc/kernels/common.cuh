@@ -169,6 +169,21 @@ __device__ __forceinline__ void st_async_f64x2(uint32_t addr, double v0, double 
                : "memory");
 }
 
+// ---- device-scope flags in global memory ---------------------------------------
+__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// Spin until *p >= target (every calling thread acquires).
+__device__ __forceinline__ void wait_geq(const unsigned* p, unsigned target) {
+  while (int(ld_acquire(p) - target) < 0) {
+  }
+}
+
 // Launch with a 1D cluster of `csize` CTAs (and PDL when `pdl`).
 template <typename... KArgs, typename... Args>
 inline void launch_cluster(bool pdl, int csize, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,

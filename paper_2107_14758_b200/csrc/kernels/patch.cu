@@ -673,7 +673,8 @@ __global__ void __launch_bounds__(kSolveThreads)
     k_patch_solve(PatchArgs a, int ring_len, const double* __restrict__ rt, double* __restrict__ corr,
                   const double* __restrict__ tiles, const int32_t* __restrict__ pdofs,
                   const int32_t* __restrict__ col_start, const int32_t* __restrict__ tile_row,
-                  const int32_t* __restrict__ rec_off, int j0) {
+                  const int32_t* __restrict__ rec_off, int j0, unsigned* __restrict__ tail_sync,
+                  unsigned tail_ctas) {
   extern __shared__ __align__(128) double sm[];
   double* ring = sm;                          // ring_len doubles
   double* y = ring + ring_len;                // mpad
@@ -748,7 +749,11 @@ __global__ void __launch_bounds__(kSolveThreads)
 
   constexpr int NC = 32 * kSolveConsumers;
   const int rl = lane & 7, g = lane >> 3;
-  pdl_wait();  // the separator RHS comes from the previous kernel (the factor stream does not)
+  // The separator RHS comes from the kernel before.  With a split tail
+  // (tail_ctas > 0) that kernel is the tail solve, which already waited for
+  // the RHS producer before triggering this launch: no wait here, so both run
+  // side by side; instead CTA 0 holds this grid open until the tail is done.
+  if (tail_ctas == 0) pdl_wait();
   // record of stream position q, after its bytes landed
   auto acquire = [&](int q) {
     const int e = q & (kRingEntries - 1);
@@ -862,6 +867,12 @@ __global__ void __launch_bounds__(kSolveThreads)
   // ---- phase D: write the separator solution x_G (interiors are rebuilt per cell)
   double* cj = corr + size_t(j) * a.m;
   for (int r = tid; r < a.m; r += NC) cj[r] = y[r];
+  if (tail_ctas > 0 && blockIdx.x == 0 && tid == 0) {
+    // tail_sync[0]: finished tail CTAs (cumulative), [1]: calls completed
+    const unsigned E1 = __ldcg(tail_sync + 1) + 1u;
+    wait_geq(tail_sync, tail_ctas * E1);
+    atomicAdd(tail_sync + 1, 1u);
+  }
 }
 
 // Cluster variant: one patch per cluster of CS CTAs (SMs).  Tile row I of
@@ -887,7 +898,8 @@ __global__ void __launch_bounds__(kSolveThreads)
     k_patch_solve_cl(PatchArgs a, int ring_len, const double* __restrict__ rt, double* __restrict__ corr,
                      const double* __restrict__ tiles, const int32_t* __restrict__ pdofs,
                      const int32_t* __restrict__ tile_row, const int32_t* __restrict__ rec_off,
-                     const int32_t* __restrict__ cl_list, const int32_t* __restrict__ cl_col, int j0) {
+                     const int32_t* __restrict__ cl_list, const int32_t* __restrict__ cl_col, int j0,
+                     unsigned* __restrict__ tail_done) {
   extern __shared__ __align__(128) double sm[];
   double* ring = sm;                              // ring_len doubles
   double* y = ring + ring_len;                    // mpad (owned rows; broadcast y_K / x_K)
@@ -905,6 +917,9 @@ __global__ void __launch_bounds__(kSolveThreads)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const double* tb = tiles + size_t(j) * a.ntiles * TT;
   const int32_t* col = cl_col + rank * (a.nT + 1);
+  // Wait for the predecessor before letting the single-CTA solve launch: that
+  // launch then runs beside this one without waiting for it (see launch_patch_solve).
+  pdl_wait();
   pdl_trigger();
   if (tid < kRingEntries) {
     mbar_init(&full[tid], 1);
@@ -1115,6 +1130,10 @@ __global__ void __launch_bounds__(kSolveThreads)
       if ((r / T) % CS == rank) cj[r] = y[r];
   }
   cluster_sync_all();  // no CTA leaves while a peer may still write into it
+  if (tid == 0) {      // this CTA's rows of corr are written
+    __threadfence();
+    atomicAdd(tail_done, 1u);
+  }
 }
 
 // z[g] = sum of patch corrections of DOF g in ascending patch order
@@ -1221,7 +1240,7 @@ static void build_cluster_lists(Context& c, int cs) {
 }
 
 template <int CS>
-static void launch_solve_cl(Context& c, const PatchArgs& a, const double* r_modal, int j0) {
+static size_t solve_cl_smem(const Context& c, int* ring_out) {
   const size_t budget = 227 * 1024;
   const size_t fixed = sizeof(double) * (size_t(c.L.mpad) + 2 * kSolveConsumers * T + CS * T + SB8) +
                        2 * kRingEntries * sizeof(uint64_t) + 3 * size_t(c.L.nT) * sizeof(uint64_t) +
@@ -1230,12 +1249,53 @@ static void launch_solve_cl(Context& c, const PatchArgs& a, const double* r_moda
   for (int t = 0; t < c.L.ntiles; ++t) max_rec = std::max(max_rec, c.L.tile_poff8[t + 1] - c.L.tile_poff8[t]);
   const int ring = fixed < budget ? int(((budget - fixed) / sizeof(double)) & ~size_t(15)) : 0;
   if (ring < max_rec) throw Error(FDMGPU_UNSUPPORTED, "separator too large for the shared-memory cluster solve");
-  const size_t smem = fixed + size_t(ring) * sizeof(double);
+  *ring_out = ring;
+  return fixed + size_t(ring) * sizeof(double);
+}
+
+// Clusters of cs CTAs of the split solve that can be resident at once.
+static int max_active_clusters(Context& c, int cs) {
+  auto& memo = c.cl_fit[cs];
+  if (memo >= 0) return memo;
+  int ring = 0, n = 0;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = unsigned(cs);
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(kSolveThreads);
+  cfg.gridDim = dim3(cs);
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  switch (cs) {
+    case 3:
+      cfg.dynamicSmemBytes = solve_cl_smem<3>(c, &ring);
+      FDM_CUDA(cudaFuncSetAttribute(k_patch_solve_cl<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+      FDM_CUDA(cudaOccupancyMaxActiveClusters(&n, k_patch_solve_cl<3>, &cfg));
+      break;
+    case 4:
+      cfg.dynamicSmemBytes = solve_cl_smem<4>(c, &ring);
+      FDM_CUDA(cudaFuncSetAttribute(k_patch_solve_cl<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+      FDM_CUDA(cudaOccupancyMaxActiveClusters(&n, k_patch_solve_cl<4>, &cfg));
+      break;
+    default:
+      cfg.dynamicSmemBytes = solve_cl_smem<2>(c, &ring);
+      FDM_CUDA(cudaFuncSetAttribute(k_patch_solve_cl<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+      FDM_CUDA(cudaOccupancyMaxActiveClusters(&n, k_patch_solve_cl<2>, &cfg));
+  }
+  return memo = n;
+}
+
+template <int CS>
+static void launch_solve_cl(Context& c, const PatchArgs& a, const double* r_modal, int j0) {
+  int ring = 0;
+  const size_t smem = solve_cl_smem<CS>(c, &ring);
   FDM_CUDA(cudaFuncSetAttribute(k_patch_solve_cl<CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
   launch_cluster(c.pdl && !c.timing, CS, k_patch_solve_cl<CS>, dim3((c.npatch - j0) * CS), dim3(kSolveThreads),
                  smem, c.stream, a, ring, r_modal, c.corr.p, (const double*)c.tiles.p, (const int32_t*)c.pdofs.p,
                  (const int32_t*)c.tile_row.p, (const int32_t*)c.tile_poff8.p, (const int32_t*)c.cl_list.p,
-                 (const int32_t*)c.cl_col.p, j0);
+                 (const int32_t*)c.cl_col.p, j0, c.tail_sync.p);
 }
 
 // Ring size (doubles) of the separator solve: all shared memory left after
@@ -1254,26 +1314,50 @@ static int solve_ring(const Context& c, size_t* smem_out) {
 
 void launch_patch_solve(Context& c, const double* r_modal) {
   PatchArgs a = make_args(c);
-  // Patches [0, nsolo): one CTA each; [nsolo, npatch): cluster-split
-  // (all of them when solve_tail is off).  The cluster part runs first: the
-  // single-CTA launch waits for it (PDL), so the next kernel sees both.
+  // Patches [0, nsolo): one CTA each (full waves); [nsolo, npatch): the last
+  // partial wave, each patch split over several SMs (all patches when
+  // solve_tail is off).  The split launch goes first and triggers the
+  // single-CTA launch once all its CTAs run, so the two overlap; CTA 0 of the
+  // single-CTA grid waits for the split CTAs' completion count, so whatever
+  // waits for that grid sees both.
   int nsolo = 0;
+  unsigned tail_ctas = 0;
+  KernelTimer timer(c, 0);  // one interval for the whole separator solve (both launches)
   // Split only separators of >= 8 tile columns: below that the per-column
-  // cluster exchange costs more than the chain it shortens (C1/C2).
-  if (c.solve_cs > 1 && c.L.nT >= 8) {
+  // exchange costs more than the chain it shortens (C1/C2).
+  if (c.solve_cs != 1 && c.L.nT >= 8) {
     int nsm = 0;
     FDM_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c.device));
     nsolo = c.solve_tail ? (c.npatch / nsm) * nsm : 0;
-    if (nsolo < c.npatch) {
-      build_cluster_lists(c, c.solve_cs);
-      KernelTimer timer(c, 0);
-      switch (c.solve_cs) {
+    const int ntail = c.npatch - nsolo;
+    if (c.tail_sync.n == 0) {
+      c.tail_sync.alloc(2);
+      FDM_CUDA(cudaMemsetAsync(c.tail_sync.p, 0, c.tail_sync.bytes(), c.stream));
+    }
+    // Cluster size: 2 when the single-CTA launch runs beside the split one
+    // (the 94 split CTAs leave 54 SMs to it); with no full wave, the largest
+    // size whose clusters all fit at once (3-CTA clusters: 45, 4-CTA: 33 at
+    // 220 KB per CTA), since a lone patch speeds up with every SM it gets.
+    int cs = c.solve_cs;
+    if (cs == 0) {
+      cs = 2;
+      if (nsolo == 0)
+        for (int cand : {4, 3})
+          if (max_active_clusters(c, cand) >= ntail) {
+            cs = cand;
+            break;
+          }
+    }
+    if (ntail > 0 && cs >= 2) {
+      build_cluster_lists(c, cs);
+      switch (cs) {
         case 2: launch_solve_cl<2>(c, a, r_modal, nsolo); break;
         case 3: launch_solve_cl<3>(c, a, r_modal, nsolo); break;
         case 4: launch_solve_cl<4>(c, a, r_modal, nsolo); break;
         default: throw Error(FDMGPU_INVALID_ARGUMENT, "solve cluster size must be 1..4");
       }
       FDM_LAUNCH_CHECK(c);
+      tail_ctas = unsigned(ntail * cs);
     }
     if (nsolo == 0) return;
   } else {
@@ -1282,10 +1366,10 @@ void launch_patch_solve(Context& c, const double* r_modal) {
   size_t smem = 0;
   const int ring = solve_ring(c, &smem);
   FDM_CUDA(cudaFuncSetAttribute(k_patch_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-  KernelTimer timer(c, 0);
-  launch_pdl(c.pdl && !c.timing, k_patch_solve, dim3(nsolo), dim3(kSolveThreads), smem, c.stream, a, ring, r_modal,
+  // (PDL after a split tail even when timing: the overlap is part of the solve)
+  launch_pdl(c.pdl && (!c.timing || tail_ctas > 0), k_patch_solve, dim3(nsolo), dim3(kSolveThreads), smem, c.stream, a, ring, r_modal,
              c.corr.p, (const double*)c.tiles.p, (const int32_t*)c.pdofs.p, (const int32_t*)c.col_start.p,
-             (const int32_t*)c.tile_row.p, (const int32_t*)c.tile_poff8.p, 0);
+             (const int32_t*)c.tile_row.p, (const int32_t*)c.tile_poff8.p, 0, c.tail_sync.p, tail_ctas);
   FDM_LAUNCH_CHECK(c);
 }
 

@@ -32,15 +32,15 @@ import numpy as np
 cfg = sys.argv[1] if len(sys.argv) > 1 else "3"
 os.makedirs("/tmp/cs", exist_ok=True)
 res = {}
-VARIANTS = [(1, 1, 0, 0), (2, 1, 0, 0), (3, 1, 0, 0), (4, 1, 0, 0), (2, 0, 0, 0)]
-for vi, (cs, tail, la, sla) in enumerate(VARIANTS):
-    env = dict(os.environ, FDMGPU_SOLVE_CS=str(cs), FDMGPU_SOLVE_TAIL=str(tail), FDMGPU_SOLVE_LA=str(la),
-               FDMGPU_SOLO_LA=str(sla))
+# (cluster size of the split solve: 0 = auto, 1 = none; split only the tail)
+VARIANTS = [(1, 1), (0, 1), (2, 1), (3, 1), (4, 1), (2, 0)]
+for vi, (cs, tail) in enumerate(VARIANTS):
+    env = dict(os.environ, FDMGPU_SOLVE_CS=str(cs), FDMGPU_SOLVE_TAIL=str(tail))
     try:
         out = subprocess.run([sys.executable, __file__, cfg, f"/tmp/cs/z{vi}.npy"], env=env, capture_output=True,
                              text=True, timeout=120)
     except subprocess.TimeoutExpired:
-        print(cs, tail, la, sla, "TIMEOUT (hang)", flush=True)
+        print(cs, tail, "TIMEOUT (hang)", flush=True)
         continue
     if out.returncode != 0:
         print(cs, "FAILED", out.stderr[-2000:], flush=True)
@@ -48,4 +48,4 @@ for vi, (cs, tail, la, sla) in enumerate(VARIANTS):
     d = json.loads(out.stdout.strip().splitlines()[-1])
     z1 = np.load("/tmp/cs/z0.npy"); zc = np.load(f"/tmp/cs/z{vi}.npy")
     d["rel_vs_cs1"] = float(np.linalg.norm(zc - z1) / np.linalg.norm(z1))
-    print("config", cfg, "cs", cs, "tail", tail, "la", la, "solo_la", sla, json.dumps(d), flush=True)
+    print("config", cfg, "cs", cs, "tail", tail, json.dumps(d), flush=True)
