@@ -152,6 +152,13 @@ fdmgpu_status fdmgpu_set_coarse_cells(fdmgpu_handle h, const int32_t* coarse_cel
  * "cholesky: matrix not SPD at pivot k (patch j)" on a non-positive pivot. */
 fdmgpu_status fdmgpu_factor(fdmgpu_handle h);
 fdmgpu_status fdmgpu_get_layout(fdmgpu_handle h, fdmgpu_layout* out);
+/* The separator Schur complement S_G = A_BB - A_BI A_II^{-1} A_IB of patch j
+ * -- the matrix the batched factorisation factors (extract_submatrix of the
+ * transformed matrix, src/sparse.cpp:17-31, with the closed-form interior
+ * elimination applied) -- as a dense m x m column-major array in this
+ * handle's separator order (fdmgpu_get_patch_elimination_dofs positions
+ * n_I..n-1; absent positions of boundary stars hold identity rows). */
+fdmgpu_status fdmgpu_patch_schur(fdmgpu_handle h, int32_t j, double* out);
 /* Per-patch global DOFs in elimination order (npatch x n): dofs[perm[k]]. */
 fdmgpu_status fdmgpu_get_patch_elimination_dofs(fdmgpu_handle h, int32_t* out);
 

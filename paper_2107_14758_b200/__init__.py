@@ -79,6 +79,8 @@ def lib():
                                                 C.c_uint64]
         L.fdmhost_save_mesh.argtypes = [_vp, C.c_char_p]
         L.fdmhost_problem_set_skip_boundary_patches.argtypes = [_vp, C.c_int]
+        L.fdmhost_write_matrix_market.argtypes = [C.c_char_p, C.c_int64, C.c_int64, _vp, _vp, _vp, C.c_int]
+        L.fdmgpu_patch_schur.argtypes = [_vp, C.c_int32, _vp]
         L.fdmhost_problem_info.argtypes = [_vp, _vp]
         L.fdmhost_get_rhs.argtypes = [_vp, _vp]
         L.fdmhost_get_maps.argtypes = [_vp] * 7
@@ -116,6 +118,31 @@ def _host_chk(rc):
 
 def _ptr(a):
     return None if a is None else _vp(a.ctypes.data)
+
+
+def write_matrix_market(path, A, symmetric=False):
+    """write_matrix_market (src/sparse.cpp:33-52): A is a dense array or a scipy
+    sparse matrix; stored in column-major order (explicit entries of a sparse
+    matrix, nonzeros of a dense one); `symmetric` writes the lower triangle."""
+    if hasattr(A, "tocsc"):
+        M = A.tocsc()
+        M.sort_indices()
+        rows, cols = M.shape
+        colptr, rowidx, val = M.indptr, M.indices, M.data
+    else:
+        D = np.asarray(A, np.float64)
+        rows, cols = D.shape
+        nzr, nzc = np.nonzero(D.T)  # column-major: (column, row) pairs, rows ascending per column
+        colptr = np.zeros(cols + 1, np.int64)
+        np.add.at(colptr, nzr + 1, 1)
+        colptr = np.cumsum(colptr)
+        rowidx, val = nzc, D[nzc, nzr]
+    colptr = np.ascontiguousarray(colptr, np.int64)
+    rowidx = np.ascontiguousarray(rowidx, np.int32)
+    val = np.ascontiguousarray(val, np.float64)
+    _host_chk(lib().fdmhost_write_matrix_market(os.fsencode(path), rows, cols, _ptr(colptr),
+                                                _ptr(rowidx) if len(rowidx) else None,
+                                                _ptr(val) if len(val) else None, 1 if symmetric else 0))
 
 
 class Problem:
@@ -311,6 +338,18 @@ class Solver:
         out = np.zeros(L["npatch"] * L["n"], np.int32)
         self._chk(lib().fdmgpu_get_patch_elimination_dofs(self.h, _ptr(out)))
         return out.reshape(L["npatch"], L["n"])
+
+    def patch_schur(self, j):
+        """Separator Schur complement of patch j (dense m x m, this handle's separator order)."""
+        m = self.layout()["n_interface"]
+        out = np.zeros((m, m), order="F")
+        self._chk(lib().fdmgpu_patch_schur(self.h, int(j), _ptr(out)))
+        return out
+
+    def export_patch_matrix(self, j, path):
+        """Debug dump of patch j's separator Schur complement in MatrixMarket
+        (symmetric, lower triangle), as write_matrix_market writes it."""
+        write_matrix_market(path, self.patch_schur(j), symmetric=True)
 
     def launch_count(self):
         return int(lib().fdmgpu_launch_count(self.h))

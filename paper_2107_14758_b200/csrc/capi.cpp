@@ -707,6 +707,33 @@ fdmgpu_status fdmgpu_get_layout(fdmgpu_handle h, fdmgpu_layout* out) {
   });
 }
 
+fdmgpu_status fdmgpu_patch_schur(fdmgpu_handle h, int32_t j, double* out) {
+  return fdmgpu::guarded(h, [&](Context& c) {
+    c.check_ready(true, false, false);
+    if (j < 0 || j >= c.npatch || !out) throw Error(FDMGPU_INVALID_ARGUMENT, "patch_schur: bad patch index");
+    const auto& L = c.L;
+    const size_t tt = size_t(fdmgpu::kTile) * fdmgpu::kTile;
+    fdmgpu::DevArray<double> scratch;
+    scratch.alloc(size_t(L.ntiles) * tt);
+    fdmgpu::launch_patch_assemble_one(c, j, scratch.p);
+    std::vector<double> h_t(scratch.n);
+    FDM_CUDA(cudaMemcpyAsync(h_t.data(), scratch.p, scratch.bytes(), cudaMemcpyDeviceToHost, c.stream));
+    FDM_CUDA(cudaStreamSynchronize(c.stream));
+    const int m = L.m, T = fdmgpu::kTile;
+    std::fill(out, out + size_t(m) * m, 0.0);
+    for (int t = 0; t < L.ntiles; ++t)
+      for (int cc = 0; cc < T; ++cc)
+        for (int rr = 0; rr < T; ++rr) {
+          const int r = L.tile_row[t] * T + rr, col = L.tile_col[t] * T + cc;
+          if (r >= m || col >= m || col > r) continue;
+          const int swz = ((cc & 3) << 2) | ((cc >> 2) & 3);  // tile swizzle (kernels/common.cuh tsw)
+          const double v = h_t[size_t(t) * tt + size_t(cc) * T + (rr ^ swz)];
+          out[size_t(col) * m + r] = v;
+          out[size_t(r) * m + col] = v;
+        }
+  });
+}
+
 fdmgpu_status fdmgpu_get_patch_elimination_dofs(fdmgpu_handle h, int32_t* out) {
   return fdmgpu::guarded(h, [&](Context& c) {
     c.check_ready(true, false, false);

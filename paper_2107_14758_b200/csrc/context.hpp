@@ -209,6 +209,7 @@ void launch_gather(Context& c, int mode, const double* E, const double* x, doubl
 void launch_cells_stiffness(Context& c, const double* x);            // writes c.E
 void launch_cells_quadrature(Context& c, const double* x);           // writes c.E (true form)
 void launch_patch_assemble(Context& c);
+void launch_patch_assemble_one(Context& c, int j, double* out);  // S_G of patch j, tile layout
 void launch_patch_update(Context& c, int K);
 void launch_patch_trsm(Context& c, int K);
 void launch_patch_lead(Context& c);

@@ -7,7 +7,7 @@
 #include <exception>
 #include <string>
 
-#include "../../../include/fdmgpu.h"
+#include "../../../include/fdmhost.h"
 #include "fdm_host.hpp"
 
 using namespace fdmgpu::host;
@@ -92,6 +92,16 @@ int fdmhost_problem_set_skip_boundary_patches(void* ph, int skip) {
   return guard([&] {
     Problem& P = *static_cast<Problem*>(ph);
     P.patches = vertex_patches(P.space, skip != 0);
+  });
+}
+
+// write_matrix_market (src/sparse.cpp:33-52): CSC input, `symmetric` keeps row >= col.
+int fdmhost_write_matrix_market(const char* path, int64_t rows, int64_t cols, const int64_t* colptr,
+                                const int32_t* rowidx, const double* val, int symmetric) {
+  return guard([&] {
+    if (!path || rows < 0 || cols < 0 || !colptr || (colptr[cols] > 0 && (!rowidx || !val)))
+      throw std::invalid_argument("write_matrix_market: bad arguments");
+    write_matrix_market(path, rows, cols, colptr, rowidx, val, symmetric != 0);
   });
 }
 

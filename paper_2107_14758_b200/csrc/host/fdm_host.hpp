@@ -159,5 +159,8 @@ std::unique_ptr<Problem> make_problem(int config, int n_override, int p_override
 // Space, RHS (U[-1,1], or N(0,1) when `normal`, from `rng`), cell data, patches, coarse level.
 void finish_problem(Problem& pb, std::mt19937_64& rng, bool normal);
 std::unique_ptr<Problem> make_problem_from_mesh(Mesh mesh, int p, uint64_t seed);
+// write_matrix_market (src/sparse.cpp:33-52) for a CSC matrix (column-major, like SpMat).
+void write_matrix_market(const std::string& path, int64_t rows, int64_t cols, const int64_t* colptr,
+                         const int32_t* rowidx, const double* val, bool symmetric);
 
 }  // namespace fdmgpu::host

@@ -177,14 +177,15 @@ __device__ __forceinline__ void record_pivot_error(unsigned long long* err, int 
 
 // Separator Schur complement S_G on the structural nonzeros only (`entries`,
 // shared by all patches); all other stored tile entries were zeroed first.
+// (patches j0 + blockIdx.y; tiles indexed by blockIdx.y)
 __global__ void k_patch_assemble(PatchArgs a, int nentries, const int32_t* __restrict__ entries,
                                  const int32_t* __restrict__ tile_row, const int32_t* __restrict__ tile_col,
-                                 double* __restrict__ tiles) {
+                                 double* __restrict__ tiles, int j0) {
   extern __shared__ double sm[];
   double* At = sm;
   double* Bt = At + a.n1 * a.n1;
   double* mup = Bt + a.n1 * a.n1;  // 2^d x d
-  const int j = blockIdx.y;
+  const int j = j0 + blockIdx.y;
   const int ncorner = 1 << a.dim;
   for (int i = threadIdx.x; i < a.n1 * a.n1; i += blockDim.x) {
     At[i] = a.At[i];
@@ -197,7 +198,7 @@ __global__ void k_patch_assemble(PatchArgs a, int nentries, const int32_t* __res
     mup[i] = K >= 0 ? a.mu[size_t(K) * a.dim + q] : 0.0;
   }
   __syncthreads();
-  double* base = tiles + size_t(j) * a.ntiles * TT;
+  double* base = tiles + size_t(blockIdx.y) * a.ntiles * TT;
   const int32_t* sep = a.psep + size_t(j) * a.m;
   const bool whole = smask == (1 << ncorner) - 1;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nentries; e += gridDim.x * blockDim.x) {
@@ -1158,9 +1159,20 @@ void launch_patch_assemble(Context& c) {
   const size_t smem = sizeof(double) * (2 * size_t(c.n1) * c.n1 + 24);
   const int ne = int(c.L.entries.size());
   dim3 grid(unsigned((ne + 255) / 256 < 64 ? (ne + 255) / 256 : 64), c.npatch);
-  k_patch_assemble<<<grid, 256, smem, c.stream>>>(a, ne, c.entries.p, c.tile_row.p, c.tile_col.p, c.tiles.p);
+  k_patch_assemble<<<grid, 256, smem, c.stream>>>(a, ne, c.entries.p, c.tile_row.p, c.tile_col.p, c.tiles.p, 0);
   FDM_LAUNCH_CHECK(c);
   k_patch_pad_check<<<c.npatch, 256, 0, c.stream>>>(a, c.tiles.p, c.L.col_start[c.L.nT - 1]);
+  FDM_LAUNCH_CHECK(c);
+}
+
+// Separator Schur complement of one patch into `out` (ntiles x TT, zeroed here).
+void launch_patch_assemble_one(Context& c, int j, double* out) {
+  PatchArgs a = make_args(c);
+  FDM_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * size_t(c.L.ntiles) * TT, c.stream));
+  const size_t smem = sizeof(double) * (2 * size_t(c.n1) * c.n1 + 24);
+  const int ne = int(c.L.entries.size());
+  dim3 grid(unsigned((ne + 255) / 256 < 148 ? (ne + 255) / 256 : 148), 1);
+  k_patch_assemble<<<grid, 256, smem, c.stream>>>(a, ne, c.entries.p, c.tile_row.p, c.tile_col.p, out, j);
   FDM_LAUNCH_CHECK(c);
 }
 

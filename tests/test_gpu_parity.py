@@ -338,3 +338,40 @@ def test_cluster_split_solve(pkg, oracle, torch, monkeypatch, cs, tail):
     z = sol.patch_apply(rt)
     assert rel(z, ref.patch_apply(rt)) <= TOL_RELAX
     assert np.array_equal(z, sol.patch_apply(rt))  # deterministic
+
+
+@pytest.mark.parametrize("cfg,skip", [((4, 3, 5), True), ((5, 2, 4), False), ((1, 3, 5), False)])
+def test_patch_schur_matches_oracle(pkg, oracle, torch, tmp_path, cfg, skip):
+    """fdmgpu_patch_schur (the matrix the batched factorisation factors) against
+    the oracle's patch matrix (extract_submatrix of the assembled transformed
+    matrix) with its interior block eliminated; absent positions of boundary
+    stars are identity rows; the MatrixMarket dump reads back exactly."""
+    import scipy.io
+
+    prob = pkg.Problem(*cfg, skip_boundary_patches=skip)
+    sol = pkg.Solver(prob)
+    ref = oracle.Problem(*cfg, build_global=True, skip_boundary_patches=skip)
+    L = sol.layout()
+    el = sol.elimination_dofs()
+    pt = ref.patches()
+    for j in sorted({0, L["npatch"] // 2, L["npatch"] - 1}):
+        S = sol.patch_schur(j)
+        ptr, col, val = ref.patch_matrix(j)
+        n = len(ptr) - 1
+        A = np.zeros((n, n))
+        for r in range(n):
+            A[r, col[ptr[r]:ptr[r + 1]]] = val[ptr[r]:ptr[r + 1]]
+        dofs = pt["dofs"][pt["ptr"][j]:pt["ptr"][j + 1]]
+        pos = {int(g): i for i, g in enumerate(dofs)}
+        sep = el[j, L["n_interior"]:]
+        present = sep >= 0
+        isep = np.array([pos[int(g)] for g in sep[present]])
+        iint = np.setdiff1d(np.arange(n), isep)
+        Sref = A[np.ix_(isep, isep)] - A[np.ix_(isep, iint)] @ np.linalg.solve(A[np.ix_(iint, iint)], A[np.ix_(iint, isep)])
+        assert rel(S[np.ix_(present, present)], Sref) <= 1e-12
+        assert not S[np.ix_(~present, present)].any() and np.all(np.diag(S)[~present] == 1.0)
+    path = str(tmp_path / "s.mtx")
+    sol.export_patch_matrix(0, path)
+    R = scipy.io.mmread(path)
+    R = R.toarray() if hasattr(R, "toarray") else np.asarray(R)
+    assert np.array_equal(R, sol.patch_schur(0))
