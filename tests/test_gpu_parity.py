@@ -365,7 +365,7 @@ def test_patch_schur_matches_oracle(pkg, oracle, torch, tmp_path, cfg, skip):
         pos = {int(g): i for i, g in enumerate(dofs)}
         sep = el[j, L["n_interior"]:]
         present = sep >= 0
-        isep = np.array([pos[int(g)] for g in sep[present]])
+        isep = np.array([pos[int(g)] for g in sep[present]], dtype=np.int64)
         iint = np.setdiff1d(np.arange(n), isep)
         Sref = A[np.ix_(isep, isep)] - A[np.ix_(isep, iint)] @ np.linalg.solve(A[np.ix_(iint, iint)], A[np.ix_(iint, isep)])
         assert rel(S[np.ix_(present, present)], Sref) <= 1e-12
