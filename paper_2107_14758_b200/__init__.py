@@ -18,7 +18,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libfdmgpu.so")
+LIB_PATH = os.environ.get("FDMGPU_LIB") or os.path.join(_HERE, "lib", "libfdmgpu.so")  # override: A/B builds
 _lib = None
 
 OP_APPLY_ST, OP_APPLY_S, OP_PATCH, OP_SMOOTH, OP_A, OP_VCYCLE = range(6)
