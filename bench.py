@@ -286,7 +286,7 @@ def run_ours(args):
     # k_patch_solve_cl (one timed interval around both)
     kern_ms = solve_ms / n_timed
     nsm = torch.cuda.get_device_properties(dev).multi_processor_count
-    split = L["tile_cols"] >= 8 and L["npatch"] % nsm != 0 and os.environ.get("FDMGPU_SOLVE_CS") != "1"
+    split = L["tile_cols"] >= 16 and L["npatch"] % nsm != 0 and os.environ.get("FDMGPU_SOLVE_CS") != "1"
     solve_kernels = "k_patch_solve + k_patch_solve_cl (split tail, overlapped)" if split else "k_patch_solve"
     achieved = kern_bytes / (kern_ms * 1e-3) / 1e9
     relax_bytes = 8.0 * (2 * nnz_total + 2 * prob.sum_nj + 4 * prob.ndof)  # SURVEY.md §8(d) Bytes_relax

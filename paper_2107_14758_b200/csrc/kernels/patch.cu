@@ -1335,9 +1335,10 @@ void launch_patch_solve(Context& c, const double* r_modal) {
   int nsolo = 0;
   unsigned tail_ctas = 0;
   KernelTimer timer(c, 0);  // one interval for the whole separator solve (both launches)
-  // Split only separators of >= 8 tile columns: below that the per-column
-  // exchange costs more than the chain it shortens (C1/C2).
-  if (c.solve_cs != 1 && c.L.nT >= 8) {
+  // Split only separators of >= 16 tile columns: below that the per-column
+  // exchange costs more than the chain it shortens (C2, 8 columns: 41 us
+  // split vs 35 us whole).
+  if (c.solve_cs != 1 && c.L.nT >= 16) {
     int nsm = 0;
     FDM_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c.device));
     nsolo = c.solve_tail ? (c.npatch / nsm) * nsm : 0;
