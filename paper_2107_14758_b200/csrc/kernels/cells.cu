@@ -65,9 +65,14 @@ struct PosId {
 // with their 16-byte chunks XOR-swizzled by the row index, so a thread
 // reading a whole row (4 x double2 per 8 lanes) and 16 threads writing one
 // element each of a row are both bank-conflict free.
+// Element o of a 16^3 tile (axis 0 fastest) -> shared-memory slot: the
+// double pair (o >> 1) & 7 within each 16-double row is XORed with
+// (row ^ row >> 4) & 7, so both DMMA fragment accesses of the line passes are
+// conflict-free: reading 8 consecutive rows x 4 columns, and writing double
+// pairs of 8 rows 16 apart (the contracted index becomes the slowest).
 struct Pos16 {
   __device__ __forceinline__ int operator()(int o) const {
-    return (o & ~15) | ((((o >> 1) & 7) ^ ((o >> 4) & 7)) << 1) | (o & 1);
+    return (o & ~15) | ((((o >> 1) & 7) ^ (((o >> 4) ^ (o >> 8)) & 7)) << 1) | (o & 1);
   }
 };
 
@@ -369,42 +374,47 @@ __global__ void k_cells_stiffness(int dim, int n1, int npc, const double* __rest
   for (int l = threadIdx.x; l < npc; l += blockDim.x) e[l] = t0[l];
 }
 
-// ---- line-blocked n1 = 16, dim = 3 kernels (p = 15: C3, C4) ------------------
+// ---- n1 = 16, dim = 3 kernels (p = 15: C3, C4) -----------------------------------
 // Every 1D contraction is a pass over the 256 lines of the current fastest
-// axis: thread r loads line r into registers (16 doubles), the CTA syncs, and
-// the thread writes out(k, r) = sum_j M(k, j) x_j to element r + 256 k, i.e.
-// the contracted index becomes the slowest one.  Three passes cycle the axes
-// back to the original order, each pass reads and writes the tile in place
-// (one 32 KB buffer per field), rows of M come from shared memory by
-// broadcast, and the FMA:load ratio is 16:1 instead of 1:2.
+// axis, run as the GEMM OUT(16 x 256) = M(16 x 16) X(16 x 256) on the FP64
+// tensor pipe (DMMA m8n8k4): warp w owns lines 32w .. 32w+31 (4 n-tiles), M
+// is held as A fragments in registers for the whole kernel, the warp's X
+// fragments are read once per pass, and OUT(k, r) is written to element
+// r + 256 k, i.e. the contracted index becomes the slowest one, so three
+// passes cycle the axes back to the original order, in place (one 32 KB
+// buffer per field).
 constexpr int kL16 = 16, kNpc16 = 4096, kLines16 = 256;
-
-__device__ __forceinline__ void load_line16(const double* __restrict__ b, int r, double (&x)[16]) {
-  const double2* row = reinterpret_cast<const double2*>(b + 16 * r);
-#pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    const double2 t = row[c ^ (r & 7)];
-    x[2 * c] = t.x;
-    x[2 * c + 1] = t.y;
-  }
-}
-
-// sum_j Mrow[j] x[j] with Mrow 16 contiguous doubles (broadcast reads)
-__device__ __forceinline__ double dot16(const double* __restrict__ Mrow, const double (&x)[16]) {
-  const double2* m = reinterpret_cast<const double2*>(Mrow);
-  double a0 = 0.0, a1 = 0.0;
-#pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    const double2 mm = m[c];
-    a0 = fma(mm.x, x[2 * c], a0);
-    a1 = fma(mm.y, x[2 * c + 1], a1);
-  }
-  return a0 + a1;
-}
 
 // Mt[j + 16 k] = M[k + 16 j]: row k of M contiguous
 __device__ __forceinline__ void load_rows16(double* __restrict__ Mt, const double* __restrict__ M) {
   for (int i = threadIdx.x; i < kL16 * kL16; i += blockDim.x) Mt[(i >> 4) + 16 * (i & 15)] = M[i];
+}
+
+struct MFrag16 {
+  double a[2][4];  // [m-tile][k-tile]: M(8 mt + lane / 4, 4 kt + lane % 4)
+};
+__device__ __forceinline__ void mfrag16(MFrag16& f, const double* __restrict__ Mt) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int kt = 0; kt < 4; ++kt) f.a[mt][kt] = Mt[16 * (8 * mt + (lane >> 2)) + 4 * kt + (lane & 3)];
+}
+// X fragments of the warp's 32 lines: X(4 kt + lane % 4, line 8 nt + lane / 4)
+__device__ __forceinline__ void xfrag16(const double* __restrict__ b, double (&x)[4][4]) {
+  const Pos16 P;
+  const int lane = threadIdx.x & 31, r0 = 32 * (threadIdx.x >> 5) + (lane >> 2);
+#pragma unroll
+  for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+    for (int kt = 0; kt < 4; ++kt) x[kt][nt] = b[P(16 * (r0 + 8 * nt) + 4 * kt + (lane & 3))];
+}
+// OUT(8 mt + lane / 4, lines 8 nt + 2 (lane % 4) + {0, 1}) -> elements r + 256 k
+__device__ __forceinline__ void store16(double* __restrict__ b, int mt, int nt, double d0, double d1) {
+  const Pos16 P;
+  const int lane = threadIdx.x & 31;
+  const int k = 8 * mt + (lane >> 2), r = 32 * (threadIdx.x >> 5) + 8 * nt + 2 * (lane & 3);
+  *reinterpret_cast<double2*>(b + P(r + kLines16 * k)) = make_double2(d0, d1);
 }
 
 __global__ void __launch_bounds__(kLines16, 4) k_cells_transform16(int dir, int flags, const double* __restrict__ in,
@@ -455,12 +465,22 @@ __global__ void __launch_bounds__(kLines16, 4) k_cells_transform16(int dir, int 
     recon_interior<kL16>(f, b, aux, cd, nK[c], P);
     __syncthreads();
   }
+  MFrag16 fm;
+  mfrag16(fm, Mt);
+#pragma unroll 1
   for (int pass = 0; pass < 3; ++pass) {
-    double x[16];
-    load_line16(b, r, x);
+    double x[4][4];
+    xfrag16(b, x);
     __syncthreads();
 #pragma unroll
-    for (int k = 0; k < kL16; ++k) b[P(r + kLines16 * k)] = dot16(Mt + 16 * k, x);
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+        for (int kt = 0; kt < 4; ++kt) dmma884(d0, d1, fm.a[mt][kt], x[kt][nt]);
+        store16(b, mt, nt, d0, d1);
+      }
     __syncthreads();
   }
   if (dir == 0 && sign) {
@@ -478,7 +498,7 @@ __global__ void __launch_bounds__(kLines16, 4) k_cells_transform16(int dir, int 
 // Cartesian stiffness y_K = mu0 Bz By Ax u + mu1 Bz Ay Bx u + mu2 Az By Bx u in
 // three line passes over two in-place buffers:
 //   (Bx u, Ax u) -> (P = mu0 By Ax u + mu1 Ay Bx u, Q = By Bx u) -> y = Bz P + mu2 Az Q.
-__global__ void __launch_bounds__(kLines16) k_cells_stiffness16(const double* __restrict__ x, double* __restrict__ E,
+__global__ void __launch_bounds__(kLines16, 2) k_cells_stiffness16(const double* __restrict__ x, double* __restrict__ E,
                                                                  const int32_t* __restrict__ cdofs,
                                                                  const uint8_t* __restrict__ cons,
                                                                  const double* __restrict__ mu,
@@ -510,38 +530,66 @@ __global__ void __launch_bounds__(kLines16) k_cells_stiffness16(const double* __
   }
   const double m0 = mu[size_t(c) * 3], m1 = mu[size_t(c) * 3 + 1], m2 = mu[size_t(c) * 3 + 2];
   __syncthreads();
-  {
-    double u[16];
-    load_line16(b0, r, u);
+  MFrag16 fa, fb;
+  mfrag16(fa, As);
+  mfrag16(fb, Bs);
+  {  // (Bx u, Ax u)
+    double x[4][4];
+    xfrag16(b0, x);
     __syncthreads();
 #pragma unroll
-    for (int k = 0; k < kL16; ++k) {
-      const int o = P(r + kLines16 * k);
-      b0[o] = dot16(Bs + 16 * k, u);
-      b1[o] = dot16(As + 16 * k, u);
-    }
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        double p0 = 0.0, p1 = 0.0, q0 = 0.0, q1 = 0.0;
+#pragma unroll
+        for (int kt = 0; kt < 4; ++kt) {
+          dmma884(p0, p1, fb.a[mt][kt], x[kt][nt]);
+          dmma884(q0, q1, fa.a[mt][kt], x[kt][nt]);
+        }
+        store16(b0, mt, nt, p0, p1);
+        store16(b1, mt, nt, q0, q1);
+      }
     __syncthreads();
   }
-  {
-    double t0[16], t1[16];
-    load_line16(b0, r, t0);
-    load_line16(b1, r, t1);
+  {  // (P = mu0 By Ax u + mu1 Ay Bx u, Q = By Bx u)
+    double t0[4][4], t1[4][4];
+    xfrag16(b0, t0);
+    xfrag16(b1, t1);
     __syncthreads();
 #pragma unroll
-    for (int k = 0; k < kL16; ++k) {
-      const int o = P(r + kLines16 * k);
-      b0[o] = m0 * dot16(Bs + 16 * k, t1) + m1 * dot16(As + 16 * k, t0);
-      b1[o] = dot16(Bs + 16 * k, t0);
-    }
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        double p0 = 0.0, p1 = 0.0, q0 = 0.0, q1 = 0.0;
+#pragma unroll
+        for (int kt = 0; kt < 4; ++kt) {
+          dmma884(p0, p1, m0 * fb.a[mt][kt], t1[kt][nt]);
+          dmma884(p0, p1, m1 * fa.a[mt][kt], t0[kt][nt]);
+          dmma884(q0, q1, fb.a[mt][kt], t0[kt][nt]);
+        }
+        store16(b0, mt, nt, p0, p1);
+        store16(b1, mt, nt, q0, q1);
+      }
     __syncthreads();
   }
-  {
-    double pp[16], qq[16];
-    load_line16(b0, r, pp);
-    load_line16(b1, r, qq);
+  {  // y = Bz P + mu2 Az Q
+    double pp[4][4], qq[4][4];
+    xfrag16(b0, pp);
+    xfrag16(b1, qq);
     __syncthreads();
 #pragma unroll
-    for (int k = 0; k < kL16; ++k) b0[P(r + kLines16 * k)] = dot16(Bs + 16 * k, pp) + m2 * dot16(As + 16 * k, qq);
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        double y0 = 0.0, y1 = 0.0;
+#pragma unroll
+        for (int kt = 0; kt < 4; ++kt) {
+          dmma884(y0, y1, fb.a[mt][kt], pp[kt][nt]);
+          dmma884(y0, y1, m2 * fa.a[mt][kt], qq[kt][nt]);
+        }
+        store16(b0, mt, nt, y0, y1);
+      }
     __syncthreads();
   }
   double* e = E + size_t(c) * kNpc16;
@@ -555,13 +603,27 @@ __global__ void k_gather(int64_t ndof, int mode, const double* __restrict__ E, c
                          const uint8_t* __restrict__ cons, const double* __restrict__ x, double* __restrict__ out) {
   const int64_t g = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   pdl_trigger();
+  // The maps are static: load them (and the first two entry indices -- one
+  // for cell-interior DOFs, two on facets) while the predecessor finishes.
+  int q0 = 0, q1 = 0, i0 = 0, i1 = 0;
+  bool c = false;
+  double w = 1.0;
+  if (g < ndof) {
+    q0 = ptr[g];
+    q1 = ptr[g + 1];
+    c = cons[g];
+    if (mode == 1) w = inv_mult[g];
+    if (q1 > q0) i0 = idx[q0];
+    if (q1 > q0 + 1) i1 = idx[q0 + 1];
+  }
   pdl_wait();
   if (g >= ndof) return;
-  double s = 0.0;
-  for (int q = ptr[g]; q < ptr[g + 1]; ++q) s += E[idx[q]];
-  if (mode == 1) s *= inv_mult[g];
+  double s = q1 > q0 ? E[i0] : 0.0;
+  if (q1 > q0 + 1) s += E[i1];
+  for (int q = q0 + 2; q < q1; ++q) s += E[idx[q]];
+  s *= w;
   if (mode == 3) s += x[g];
-  if (cons[g]) s = (mode == 2) ? x[g] : 0.0;
+  if (c) s = (mode == 2) ? x[g] : 0.0;
   out[g] = s;
 }
 

@@ -1142,11 +1142,17 @@ __global__ void __launch_bounds__(kSolveThreads)
 __global__ void k_patch_gather(int64_t ndof, const double* __restrict__ corr, const int32_t* __restrict__ ptr,
                                const int32_t* __restrict__ idx, double* __restrict__ z) {
   pdl_trigger();
-  pdl_wait();
   const int64_t g = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  int q0 = 0, q1 = 0, i0 = 0;  // static map, loaded before the wait
+  if (g < ndof) {
+    q0 = ptr[g];
+    q1 = ptr[g + 1];
+    if (q1 > q0) i0 = idx[q0];
+  }
+  pdl_wait();
   if (g >= ndof) return;
-  double s = 0.0;
-  for (int q = ptr[g]; q < ptr[g + 1]; ++q) s += corr[idx[q]];
+  double s = q1 > q0 ? corr[i0] : 0.0;
+  for (int q = q0 + 1; q < q1; ++q) s += corr[idx[q]];
   z[g] = s;
 }
 
