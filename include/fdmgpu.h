@@ -93,6 +93,25 @@ fdmgpu_status fdmgpu_destroy(fdmgpu_handle h);
 fdmgpu_status fdmgpu_set_stream(fdmgpu_handle h, void* cuda_stream);
 fdmgpu_status fdmgpu_synchronize(fdmgpu_handle h);
 
+/* Linear elasticity, the SDC variant of the path (src/elasticity.cpp,
+ * include/fdmstar/elasticity.hpp): turns a handle created for the vector Q_p
+ * space (ndof = dim x scalar DOFs, vector_q_space's component-major
+ * numbering, src/discretization.cpp:313-318) into the device half of
+ * build_elasticity_twolevel (src/elasticity.cpp:204-229).  Call right after
+ * fdmgpu_create.  The setters then take: set_mesh_maps -- component 0's cell
+ * maps with multiplicity / constrained over all ndof; set_cell_coeffs -- the
+ * geometric mu^K (Cartesian cells only, kappa NULL); set_patches -- the
+ * vector star lists of build_patch_solver (all components) and their
+ * patch_ordering; set_coarse -- the vector Q1 coarse inverse and
+ * prolongation; set_coarse_cells -- component 0's coarse cell maps and the
+ * vector coarse constrained flags.  FDMGPU_OP_A applies the true form
+ * elasticity_primal_operator (src/elasticity.cpp:69-120), the relaxation the
+ * SDC surrogate sdc_transformed (src/elasticity.cpp:122-167): per component
+ * the scalar path with coefficients sdc_axis_coefficients(ci) * mu^K.
+ * C = bundle.C (V^T W D on GL(p+1), src/assembly.cpp:49-52), (p+1)^2
+ * column-major.  mu, lambda: the Lame parameters. */
+fdmgpu_status fdmgpu_set_elasticity(fdmgpu_handle h, double mu, double lambda, const double* C);
+
 /* FdmBasis (include/fdmstar/fdm_basis.hpp:21-32) and the reference interval
  * (reference_interval.hpp:15-27).  All (p+1)^2 arrays column-major:
  * S, A_t = S^T A S, B_t = S^T B S (values + structural 0/1 patterns), lambda

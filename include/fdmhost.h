@@ -26,6 +26,13 @@ const char* fdmhost_last_error(void);
 /* One of the BASELINE.json configurations 1..5, optionally reduced to n cells
  * per axis / degree p (0 = the config's value). */
 void* fdmhost_problem_create(int config, int n, int p);
+/* Linear elasticity (src/elasticity.cpp): the reference's Table-2 problem
+ * (tests/test_elasticity.cpp:24-30, 162-185) in dim = 2|3 -- unit square /
+ * cube, n cells per axis, x = 0 Dirichlet, other boundary facets Neumann --
+ * with vector Q_p, Lame mu / lambda, body force -0.02 e_{dim-1}, the SDC
+ * relaxation and a vector Q1 coarse level.  skip_boundary_patches: the
+ * reference default is 0. */
+void* fdmhost_elastic_create(int dim, int n, int p, double mu, double lambda, int skip_boundary_patches);
 /* Q_p problem on a mesh file in the reference's JSON format (load_mesh,
  * src/mesh.cpp:375-434), RHS U[-1,1] from std::mt19937_64(seed). */
 void* fdmhost_problem_from_mesh_file(const char* path, int p, uint64_t seed);
@@ -47,8 +54,10 @@ int fdmhost_write_matrix_market(const char* path, int64_t rows, int64_t cols, co
                                 const int32_t* rowidx, const double* val, int symmetric);
 void fdmhost_problem_destroy(void* problem);
 
-/* out[15]: dim, p, ncells, ndof, nfree, npatch, nvertices, dofs per cell,
- * sum n_j, coarse ndof, P nnz, quadrature points, config, n, all Cartesian. */
+/* out[16]: dim, p, ncells, ndof, nfree, npatch, nvertices, dofs per cell,
+ * sum n_j, coarse ndof, P nnz, quadrature points, config, n, all Cartesian,
+ * components (1 scalar, dim elasticity; ndof / nfree / sum n_j / coarse ndof
+ * count all components, cell maps are component 0's). */
 int fdmhost_problem_info(void* problem, int64_t* out);
 int fdmhost_get_rhs(void* problem, double* out);
 int fdmhost_get_maps(void* problem, int32_t* cell_dofs, int32_t* cell_modes, uint8_t* constrained,

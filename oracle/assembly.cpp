@@ -17,6 +17,16 @@ static Vec gather(const Vec& x, const std::vector<int>& dofs) {
 static void scatter_add(Vec& y, const std::vector<int>& dofs, const Vec& v) {
   for (size_t i = 0; i < dofs.size(); ++i) y[dofs[i]] += v[i];
 }
+// concat_dofs (src/assembly.cpp:16-23): cell DOFs of all components, component-major.
+static std::vector<int> concat_dofs(const Discretization& d, int c) {
+  if (d.ncomp == 1) return d.cell_dofs[c];
+  std::vector<int> out;
+  for (int ci = 0; ci < d.ncomp; ++ci) {
+    const auto v = d.comp_dofs(ci, c);
+    out.insert(out.end(), v.begin(), v.end());
+  }
+  return out;
+}
 
 Bundle1D make_bundle(int degree) {  // src/assembly.cpp:37-54, CG family
   Bundle1D b;
@@ -43,7 +53,7 @@ Vec GlobalOperator::apply(const Vec& x) const {  // src/assembly.cpp:56-88
   Vec y(d.ndof, 0.0);
   for (int c = 0; c < d.mesh->num_cells(); ++c) {
     const CellTerm& term = cells[c];
-    const auto& dofs = d.cell_dofs[c];
+    const auto dofs = concat_dofs(d, c);
     if (term.sumfact)
       scatter_add(y, dofs, sumfact_cell_apply(*bundle, d.dim(), term.G, gather(xp, dofs)));
     else if (term.dense.r > 0) {
@@ -53,6 +63,8 @@ Vec GlobalOperator::apply(const Vec& x) const {  // src/assembly.cpp:56-88
       scatter_add(y, dofs, v);
     }
     if (term.has_kron) scatter_add(y, dofs, kron_apply(term.kron, gather(xp, dofs)));
+    for (const auto& b : term.kron_blocks)
+      scatter_add(y, d.comp_dofs(b.ci, c), kron_apply(b.op, gather(xp, d.comp_dofs(b.cj, c))));
   }
   for (int i = 0; i < d.ndof; ++i)
     if (d.constrained[i]) y[i] = x[i];
@@ -72,8 +84,9 @@ Csr GlobalOperator::assemble() const {  // src/assembly.cpp:90-129
   for (int c = 0; c < d.mesh->num_cells(); ++c) {
     const CellTerm& term = cells[c];
     if (term.sumfact) throw std::invalid_argument("assemble: sum-factorised cell terms are matrix-free only");
-    if (term.dense.r > 0) add_block(d.cell_dofs[c], d.cell_dofs[c], term.dense);
+    if (term.dense.r > 0) add_block(concat_dofs(d, c), concat_dofs(d, c), term.dense);
     if (term.has_kron) add_block(d.cell_dofs[c], d.cell_dofs[c], kron_materialize(term.kron));
+    for (const auto& b : term.kron_blocks) add_block(d.comp_dofs(b.ci, c), d.comp_dofs(b.cj, c), kron_materialize(b.op));
   }
   for (int i = 0; i < d.ndof; ++i)
     if (d.constrained[i]) t.push_back({i, i, 1.0});
@@ -304,6 +317,11 @@ static void for_each_cell_entry(const FdmBasis& f, int d, int p, const Vec& mu, 
   }
 }
 
+void cell_transformed_entries(const FdmBasis& f, int d, int p, const Vec& mu,
+                              const std::function<void(int, int, double)>& fn) {
+  for_each_cell_entry(f, d, p, mu, fn);
+}
+
 TransformedSystem transformed_poisson(const Discretization& disc, const Bundle1D& bundle, bool eliminate,
                                       bool build_global) {  // src/assembly.cpp:245-291
   TransformedSystem sys;
@@ -361,12 +379,13 @@ Vec TransformedSystem::apply_S(const Vec& modes) const {  // src/assembly.cpp:30
   d.project_free(x);
   Vec y(d.ndof, 0.0);
   std::vector<int> dims(d.dim(), d.degree + 1);
+  for (int ci = 0; ci < d.ncomp; ++ci)
   for (int c = 0; c < d.mesh->num_cells(); ++c) {
-    Vec v = gather(x, d.cell_modes[c]);
+    Vec v = gather(x, d.comp_modes(ci, c));
     const Vec s = mode_signs(c);
     for (size_t i = 0; i < v.size(); ++i) v[i] *= s[i];
     for (int a = 0; a < d.dim(); ++a) v = apply_axis(S, v, dims, a);
-    scatter_add(y, d.cell_dofs[c], v);
+    scatter_add(y, d.comp_dofs(ci, c), v);
   }
   for (int i = 0; i < d.ndof; ++i) y[i] *= inv_multiplicity[i];
   d.project_free(y);
@@ -381,12 +400,13 @@ Vec TransformedSystem::apply_St(const Vec& nodal) const {  // src/assembly.cpp:3
   Vec y(d.ndof, 0.0);
   std::vector<int> dims(d.dim(), d.degree + 1);
   const Mat St = S.transpose();
+  for (int ci = 0; ci < d.ncomp; ++ci)
   for (int c = 0; c < d.mesh->num_cells(); ++c) {
-    Vec v = gather(x, d.cell_dofs[c]);
+    Vec v = gather(x, d.comp_dofs(ci, c));
     for (int a = 0; a < d.dim(); ++a) v = apply_axis(St, v, dims, a);
     const Vec s = mode_signs(c);
     for (size_t i = 0; i < v.size(); ++i) v[i] *= s[i];
-    scatter_add(y, d.cell_modes[c], v);
+    scatter_add(y, d.comp_modes(ci, c), v);
   }
   d.project_free(y);
   return y;

@@ -1,0 +1,262 @@
+// TEST INFRASTRUCTURE ONLY — extern "C" surface of the oracle's elasticity
+// restatement (oracle/elasticity.cpp) for the Python tests and bench.py's
+// CPU legs.  Problem: the reference's Table-2 "table" mesh generalised to
+// dim = 2|3 (tests/test_elasticity.cpp:24-30: cartesian_mesh on the unit
+// square/cube, every boundary facet Neumann, x = 0 Dirichlet), vector Q_p
+// space, body force f = -0.02 e_{dim-1} (tests/test_elasticity.cpp:170-172).
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <memory>
+#include <random>
+#include <string>
+
+#include "oracle.hpp"
+
+using namespace oracle;
+
+namespace {
+thread_local std::string g_err;
+
+struct ECtx {
+  Mesh mesh;
+  Discretization disc;
+  Bundle1D bundle;
+  double mu = 1.0, lambda = 0.0;
+  SolverConfig cfg;
+  std::shared_ptr<GlobalOperator> A;
+  std::unique_ptr<TwoLevel> tl;
+  Vec rhs;
+};
+
+template <class Fn>
+int guard(Fn&& fn) {
+  try {
+    fn();
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+ECtx* E(void* h) { return static_cast<ECtx*>(h); }
+}  // namespace
+
+extern "C" {
+
+const char* oracle_elastic_last_error() { return g_err.c_str(); }
+
+// skip_boundary: SolverConfig::skip_boundary_patches (reference default 0).
+void* oracle_elastic_create(int dim, int n, int p, double mu, double lambda, int skip_boundary, int threads) {
+  ECtx* out = nullptr;
+  guard([&] {
+    auto c = std::make_unique<ECtx>();
+    c->mesh = cartesian_mesh(dim, std::vector<int>(dim, n), std::vector<double>(dim, 1.0));
+    tag_boundary(c->mesh, [](const std::array<double, 3>&) { return true; }, FacetTag::Neumann);
+    tag_boundary(c->mesh, [](const std::array<double, 3>& x) { return std::abs(x[0]) < 1e-12; }, FacetTag::Dirichlet);
+    c->disc = vector_q_space(c->mesh, p);
+    c->disc.mesh = &c->mesh;
+    c->bundle = make_bundle(p);
+    c->mu = mu;
+    c->lambda = lambda;
+    c->cfg.skip_boundary_patches = skip_boundary != 0;
+    c->cfg.threads = threads;
+    c->A = std::make_shared<GlobalOperator>(elasticity_primal_operator(c->disc, c->bundle, mu, lambda));
+    const int d = dim;
+    c->rhs = vector_load(c->disc, c->bundle, [d](const std::array<double, 3>&) {
+      std::array<double, 3> f{0.0, 0.0, 0.0};
+      f[d - 1] = -0.02;
+      return f;
+    });
+    c->disc.project_free(c->rhs);  // zero_constrained
+    out = c.release();
+  });
+  return out;
+}
+
+void oracle_elastic_destroy(void* h) { delete E(h); }
+
+// out: dim, p, ncells, ndof (all components), scalar block size, nfree, dofs per cell (one component)
+int oracle_elastic_info(void* h, int64_t* out) {
+  return guard([&] {
+    const auto& d = E(h)->disc;
+    int64_t v[7] = {d.dim(), d.degree, E(h)->mesh.num_cells(), d.ndof, d.nsc, d.num_free(), d.dofs_per_cell};
+    std::memcpy(out, v, sizeof(v));
+  });
+}
+
+int oracle_elastic_rhs(void* h, double* out) {
+  return guard([&] { std::memcpy(out, E(h)->rhs.data(), E(h)->rhs.size() * 8); });
+}
+
+// random_free of tests/test_elasticity.cpp:13-20 (U[-1,1] from mt19937_64(seed), project_free)
+int oracle_elastic_random_free(void* h, uint64_t seed, double* out) {
+  return guard([&] {
+    const auto& d = E(h)->disc;
+    std::mt19937_64 rng(seed);
+    std::uniform_real_distribution<double> uni(-1, 1);
+    Vec x(d.ndof);
+    for (auto& v : x) v = uni(rng);
+    d.project_free(x);
+    std::memcpy(out, x.data(), x.size() * 8);
+  });
+}
+
+// Component-0 cell maps (ncells x (p+1)^d), constrained / multiplicity (ndof).
+int oracle_elastic_maps(void* h, int32_t* cell_dofs, uint8_t* constrained, double* multiplicity) {
+  return guard([&] {
+    const auto& d = E(h)->disc;
+    for (size_t c = 0; c < d.cell_dofs.size(); ++c)
+      for (int l = 0; l < d.dofs_per_cell; ++l) cell_dofs[c * d.dofs_per_cell + l] = d.cell_dofs[c][l];
+    for (int i = 0; i < d.ndof; ++i) {
+      constrained[i] = uint8_t(d.constrained[i]);
+      multiplicity[i] = d.multiplicity[i];
+    }
+  });
+}
+
+int oracle_elastic_apply_A(void* h, const double* in, double* out) {
+  return guard([&] {
+    Vec x(in, in + E(h)->disc.ndof);
+    Vec y = E(h)->A->apply(x);
+    std::memcpy(out, y.data(), y.size() * 8);
+  });
+}
+
+// build_elasticity_twolevel (src/elasticity.cpp:204-229); calibrate = 0 keeps omega = 1.
+int oracle_elastic_build(void* h, int calibrate) {
+  return guard([&] {
+    ECtx* c = E(h);
+    c->tl = std::make_unique<TwoLevel>(
+        build_elasticity_twolevel(c->disc, c->bundle, c->A, c->mu, c->lambda, c->cfg, calibrate != 0));
+  });
+}
+
+// out: omega, lambda_min, lambda_max, coarse ndof, patches, sum n_j
+int oracle_elastic_twolevel_info(void* h, double* out) {
+  return guard([&] {
+    const auto& tl = *E(h)->tl;
+    out[0] = tl.omega;
+    out[1] = tl.lambda_min;
+    out[2] = tl.lambda_max;
+    out[3] = tl.coarse->n;
+    out[4] = double(tl.patches.patches.size());
+    double s = 0;
+    for (const auto& p : tl.patches.patches) s += double(p.dofs.size());
+    out[5] = s;
+  });
+}
+
+int oracle_elastic_set_omega(void* h, double w) {
+  return guard([&] { E(h)->tl->omega = w; });
+}
+
+// which: 0 apply_St, 1 apply_S, 2 PatchSolver::apply, 3 smooth, 4 V-cycle
+int oracle_elastic_op(void* h, int which, const double* in, double* out) {
+  return guard([&] {
+    ECtx* c = E(h);
+    Vec x(in, in + c->disc.ndof), y;
+    const auto& tl = *c->tl;
+    switch (which) {
+      case 0: y = tl.sys->apply_St(x); break;
+      case 1: y = tl.sys->apply_S(x); break;
+      case 2: y = tl.patches.apply(x); break;
+      case 3: y = tl.smooth(x); break;
+      case 4: y = tl.apply(x); break;
+      default: throw std::invalid_argument("oracle_elastic_op: which 0..4");
+    }
+    std::memcpy(out, y.data(), y.size() * 8);
+  });
+}
+
+// Patch lists: ptr (npatch+1), dofs (sum n_j), vertex (npatch).
+int oracle_elastic_patches(void* h, int64_t* ptr, int32_t* dofs, int32_t* vertex) {
+  return guard([&] {
+    const auto& ps = E(h)->tl->patches.patches;
+    ptr[0] = 0;
+    for (size_t j = 0; j < ps.size(); ++j) {
+      ptr[j + 1] = ptr[j] + int64_t(ps[j].dofs.size());
+      std::memcpy(dofs + ptr[j], ps[j].dofs.data(), ps[j].dofs.size() * 4);
+      vertex[j] = ps[j].vertex;
+    }
+  });
+}
+
+// Dense assembled operator (row-major ndof^2): which 0 = the true form,
+// 1 = its diagonal (ci == cj) Kronecker blocks only, the SDC matrix of
+// tests/test_elasticity.cpp:115-121.
+int oracle_elastic_assemble_dense(void* h, int which, double* out) {
+  return guard([&] {
+    ECtx* c = E(h);
+    GlobalOperator op = *c->A;
+    if (which == 1)
+      for (auto& t : op.cells) {
+        std::vector<GlobalOperator::CellTerm::KronBlock> keep;
+        for (auto& b : t.kron_blocks)
+          if (b.ci == b.cj) keep.push_back(b);
+        t.kron_blocks = keep;
+      }
+    const Csr A = op.assemble();
+    const int n = c->disc.ndof;
+    std::memset(out, 0, size_t(n) * n * 8);
+    for (int i = 0; i < n; ++i)
+      for (int64_t q = A.ptr[i]; q < A.ptr[i + 1]; ++q) out[size_t(i) * n + A.col[q]] = A.val[q];
+  });
+}
+
+// Kronecker cell blocks materialised (kron) and the dense quadrature cell
+// matrix (quad) of `cell`, both (d nloc)^2 column-major, component-major.
+int oracle_elastic_cell_matrices(void* h, int cell, double* kron, double* quad) {
+  return guard([&] {
+    ECtx* c = E(h);
+    const int d = c->disc.dim(), nloc = c->disc.dofs_per_cell, N = d * nloc;
+    std::memset(kron, 0, size_t(N) * N * 8);
+    for (const auto& b : c->A->cells[cell].kron_blocks) {
+      const Mat K = kron_materialize(b.op);
+      for (int j = 0; j < nloc; ++j)
+        for (int i = 0; i < nloc; ++i) kron[size_t(b.ci * nloc + i) + size_t(N) * (b.cj * nloc + j)] = K(i, j);
+    }
+    const Mat Q = elasticity_primal_cell(c->mesh, cell, c->bundle, c->mu, c->lambda);
+    std::memcpy(quad, Q.a.data(), Q.a.size() * 8);
+  });
+}
+
+// pcg (src/krylov.cpp:29-83) with A = the true form and precond 0 identity,
+// 1 smooth, 2 V-cycle.  report: iterations, converged, kappa, lambda_min, lambda_max.
+int oracle_elastic_pcg(void* h, const double* b, double* x, double rtol, int maxit, int precond, double* report,
+                       double* residuals) {
+  return guard([&] {
+    ECtx* c = E(h);
+    Vec bb(b, b + c->disc.ndof);
+    auto A = c->A;
+    LinOp Aop = [A](const Vec& v) { return A->apply(v); };
+    LinOp P;
+    const TwoLevel* tl = c->tl.get();
+    if (precond == 0)
+      P = [](const Vec& v) { return v; };
+    else if (precond == 1)
+      P = [tl](const Vec& v) { return tl->smooth(v); };
+    else
+      P = tl->applier();
+    auto [xx, rep] = pcg(Aop, P, bb, rtol, maxit);
+    std::memcpy(x, xx.data(), xx.size() * 8);
+    report[0] = rep.iterations;
+    report[1] = rep.converged;
+    report[2] = rep.kappa;
+    report[3] = rep.lambda_min;
+    report[4] = rep.lambda_max;
+    for (size_t k = 0; k < rep.residuals.size(); ++k) residuals[k] = rep.residuals[k];
+  });
+}
+
+// sdc_axis_coefficients (src/elasticity.cpp:7-11)
+int oracle_sdc_axis_coefficients(int comp, int dim, double mu, double lambda, double* out) {
+  return guard([&] {
+    const Vec c = sdc_axis_coefficients(comp, dim, mu, lambda);
+    std::memcpy(out, c.data(), c.size() * 8);
+  });
+}
+
+}  // extern "C"

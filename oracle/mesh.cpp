@@ -441,6 +441,7 @@ Discretization q_space(const Mesh& mesh, int p) {
       }
     }
   }
+  disc.nsc = disc.ndof;
   return disc;
 }
 
@@ -448,8 +449,9 @@ std::vector<int> Discretization::star_dofs(int v) const {
   const auto& star_cells = mesh->vertex_cells[v];
   std::set<int> star(star_cells.begin(), star_cells.end());
   std::vector<int> out;
+  for (int ci = 0; ci < ncomp; ++ci)
   for (int K : star_cells)
-    for (int dof : cell_dofs[K]) {
+    for (int dof : comp_dofs(ci, K)) {
       if (constrained[dof]) continue;
       bool in = false;
       switch (owner_kind[dof]) {
@@ -473,6 +475,54 @@ std::vector<int> Discretization::star_dofs(int v) const {
   std::sort(out.begin(), out.end());
   out.erase(std::unique(out.begin(), out.end()), out.end());
   return out;
+}
+
+std::vector<int> Discretization::comp_dofs(int ci, int cell) const {
+  std::vector<int> out = cell_dofs[cell];
+  if (ci > 0)
+    for (auto& v : out) v += ci * nsc;
+  return out;
+}
+
+std::vector<int> Discretization::comp_modes(int ci, int cell) const {
+  std::vector<int> out = cell_modes[cell];
+  if (ci > 0)
+    for (auto& v : out) v += ci * nsc;
+  return out;
+}
+
+// vector_q_space (src/discretization.cpp:313-318): mesh.dim identical CG
+// components.  build_discretization numbers each component with its own
+// first-touch map after the previous ones (src/discretization.cpp:86-258), so
+// component ci repeats component 0's numbering shifted by ci * nsc.
+Discretization vector_q_space(const Mesh& mesh, int p) {
+  Discretization d = q_space(mesh, p);
+  const int n = d.ndof, nc = mesh.dim;
+  d.ncomp = nc;
+  d.nsc = n;
+  auto rep = [&](auto& v) {
+    auto base = v;
+    for (int ci = 1; ci < nc; ++ci) v.insert(v.end(), base.begin(), base.end());
+  };
+  rep(d.labels);
+  rep(d.multiplicity);
+  rep(d.constrained);
+  rep(d.owner_kind);
+  rep(d.owner_id);
+  d.ndof = n * nc;
+  return d;
+}
+
+void tag_boundary(Mesh& mesh, const std::function<bool(const std::array<double, 3>&)>& pred,
+                  FacetTag tag) {  // src/mesh.cpp:323-332
+  for (auto& f : mesh.facets) {
+    if (f.ncells() != 1) continue;
+    std::array<double, 3> c{0.0, 0.0, 0.0};
+    for (int v : f.vertices)
+      for (int r = 0; r < 3; ++r) c[r] += mesh.vertices[v][r];
+    for (int r = 0; r < 3; ++r) c[r] /= double(f.vertices.size());
+    if (pred(c)) f.tag = tag;
+  }
 }
 
 }  // namespace oracle

@@ -194,8 +194,16 @@ std::array<double, 3> cell_map(const Mesh& mesh, int cell, const Vec& xhat);  //
 CellGeometry cell_geometry(const Mesh& mesh, int cell, const QuadratureRule& rule);  // src/geometry.cpp:45-104
 
 enum class Owner { Cell, Facet, Edge, Vertex };
-struct Discretization {  // include/fdmstar/discretization.hpp:20-58 (scalar CG component)
+struct Discretization {  // include/fdmstar/discretization.hpp:20-58 (identical CG components)
   const Mesh* mesh = nullptr;
+  // Components (vector_q_space, src/discretization.cpp:313-318): build_discretization
+  // numbers component ci after components 0..ci-1 with its own first-touch map
+  // (src/discretization.cpp:86-258), so with identical components the DOFs of
+  // component ci are those of component 0 shifted by ci * nsc.  cell_dofs /
+  // cell_modes hold component 0; the per-DOF arrays below span all ndof.
+  int ncomp = 1, nsc = 0;
+  std::vector<int> comp_dofs(int ci, int cell) const;
+  std::vector<int> comp_modes(int ci, int cell) const;
   int degree = 0;
   int dofs_per_cell = 0;
   std::vector<std::vector<int>> cell_dofs, cell_modes;
@@ -213,6 +221,7 @@ struct Discretization {  // include/fdmstar/discretization.hpp:20-58 (scalar CG 
   void project_free(Vec& x) const;
 };
 Discretization q_space(const Mesh& mesh, int p);  // src/discretization.cpp:70-264,299-304
+Discretization vector_q_space(const Mesh& mesh, int p);  // src/discretization.cpp:313-318
 
 struct Bundle1D {  // include/fdmstar/assembly.hpp:19-25
   int degree = 0;
@@ -231,6 +240,12 @@ struct GlobalOperator {  // include/fdmstar/assembly.hpp:31-52 (cell terms only)
     // [ext] sum-factorised trilinear quadrature apply (replaces `dense` when set)
     bool sumfact = false;
     Vec G;  // per quadrature point: w*kappa*G (d*d, row-major), q^d points
+    // vector spaces: (ci, cj, op) blocks, y_ci += op x_cj (include/fdmstar/assembly.hpp:40-44)
+    struct KronBlock {
+      int ci = 0, cj = 0;
+      KronOperator op;
+    };
+    std::vector<KronBlock> kron_blocks;
   };
   std::vector<CellTerm> cells;
   const Bundle1D* bundle = nullptr;
@@ -251,12 +266,17 @@ struct TransformedSystem {  // include/fdmstar/assembly.hpp:57-70
   Csr At;
   Vec inv_multiplicity;
   std::vector<Vec> cell_mu;  // mu^K (times kappa_K) per cell, kept for patch-only assembly
+  std::vector<std::vector<Vec>> comp_mu;  // vector (SDC) systems: per component, coeff * mu^K per cell
   Vec apply_S(const Vec& modes) const;   // src/assembly.cpp:308-324
   Vec apply_St(const Vec& nodal) const;  // src/assembly.cpp:326-342
   Vec mode_signs(int cell) const;        // src/assembly.cpp:293-306
 };
 TransformedSystem transformed_poisson(const Discretization& disc, const Bundle1D& bundle,
                                       bool eliminate = true, bool build_global = true);  // src/assembly.cpp:245-291
+// Entries (lattice row, lattice col, value) of one cell block sum_a mu_a (x)_b (b==a ? A_t : B_t)
+// on its structural pattern (src/assembly.cpp:263-270).
+void cell_transformed_entries(const FdmBasis& f, int d, int p, const Vec& mu,
+                              const std::function<void(int, int, double)>& fn);
 // Patch matrix A~_j assembled from the star cells only (equal to
 // extract_submatrix(At, dofs), src/sparse.cpp:20-31, without the global matrix).
 Csr patch_matrix(const TransformedSystem& sys, const Bundle1D& bundle, int v, const std::vector<int>& dofs);
@@ -325,12 +345,28 @@ struct DampingEstimate {
 DampingEstimate estimate_damping(const LinOp& P, const LinOp& A, int n, const SolverConfig& config,
                                  const Discretization* disc);  // src/schwarz.cpp:97-119
 void calibrate_damping(TwoLevel& tl, const Discretization& disc, const SolverConfig& config);  // src/schwarz.cpp:167-228
-Csr build_prolongation(const Discretization& fine, const Discretization& coarse, const Mat& phat);  // src/schwarz.cpp:139-165
+Csr build_prolongation(const Discretization& fine, const Discretization& coarse, const Mat& phat);  // src/schwarz.cpp:139-165 (all components)
 TwoLevel build_poisson_twolevel(const Discretization& disc, const Bundle1D& bundle,
                                 std::shared_ptr<const GlobalOperator> A, const SolverConfig& config,
                                 bool calibrate = true);  // src/schwarz.cpp:230-252
 
 void parallel_for(int n, int threads, const std::function<void(int)>& fn);  // src/schwarz.cpp:16-29
+
+// ---- elasticity (src/elasticity.cpp, include/fdmstar/elasticity.hpp) --------
+Vec sdc_axis_coefficients(int comp, int dim, double mu, double lambda);  // src/elasticity.cpp:7-11
+Mat elasticity_primal_cell(const Mesh& mesh, int cell, const Bundle1D& bundle, double mu,
+                           double lambda);  // src/elasticity.cpp:15-67
+GlobalOperator elasticity_primal_operator(const Discretization& disc, const Bundle1D& bundle, double mu,
+                                          double lambda);  // src/elasticity.cpp:69-120
+TransformedSystem sdc_transformed(const Discretization& disc, const Bundle1D& bundle, double mu,
+                                  double lambda);  // src/elasticity.cpp:122-167
+Vec vector_load(const Discretization& disc, const Bundle1D& bundle,
+                const std::function<std::array<double, 3>(const std::array<double, 3>&)>& f);  // src/elasticity.cpp:169-202
+TwoLevel build_elasticity_twolevel(const Discretization& disc, const Bundle1D& bundle,
+                                   std::shared_ptr<const GlobalOperator> A, double mu, double lambda,
+                                   const SolverConfig& config, bool calibrate = true);  // src/elasticity.cpp:204-229
+// tag_boundary (src/mesh.cpp:323-332): boundary facets whose vertex centroid satisfies pred.
+void tag_boundary(Mesh& mesh, const std::function<bool(const std::array<double, 3>&)>& pred, FacetTag tag);
 
 // ---- [ext] synthetic configurations C1..C5 -----------------
 struct ConfigSpec {

@@ -391,3 +391,126 @@ class Problem:
         out = np.zeros(self.npc)
         _chk(lib().oracle_cell_sumfact_apply(self.h, cell, np.ascontiguousarray(u, np.float64), out))
         return out
+
+
+# ---- elasticity (oracle/elasticity.cpp, src/elasticity.cpp) -------------------
+def _elastic_lib():
+    L = lib()
+    if not getattr(L, "_elastic_ready", False):
+        L.oracle_elastic_last_error.restype = C.c_char_p
+        L.oracle_elastic_create.restype = C.c_void_p
+        L.oracle_elastic_create.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, C.c_int]
+        L.oracle_elastic_destroy.argtypes = [C.c_void_p]
+        L.oracle_elastic_info.argtypes = [C.c_void_p, _i64]
+        L.oracle_elastic_rhs.argtypes = [C.c_void_p, _d]
+        L.oracle_elastic_random_free.argtypes = [C.c_void_p, C.c_uint64, _d]
+        L.oracle_elastic_maps.argtypes = [C.c_void_p, _i32, _u8, _d]
+        L.oracle_elastic_apply_A.argtypes = [C.c_void_p, _d, _d]
+        L.oracle_elastic_build.argtypes = [C.c_void_p, C.c_int]
+        L.oracle_elastic_twolevel_info.argtypes = [C.c_void_p, _d]
+        L.oracle_elastic_set_omega.argtypes = [C.c_void_p, C.c_double]
+        L.oracle_elastic_op.argtypes = [C.c_void_p, C.c_int, _d, _d]
+        L.oracle_elastic_patches.argtypes = [C.c_void_p, _i64, _i32, _i32]
+        L.oracle_elastic_assemble_dense.argtypes = [C.c_void_p, C.c_int, _d]
+        L.oracle_elastic_cell_matrices.argtypes = [C.c_void_p, C.c_int, _d, _d]
+        L.oracle_elastic_pcg.argtypes = [C.c_void_p, _d, _d, C.c_double, C.c_int, C.c_int, _d, _d]
+        L.oracle_sdc_axis_coefficients.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, _d]
+        L._elastic_ready = True
+    return L
+
+
+def _echk(rc):
+    if rc != 0:
+        raise OracleError(_elastic_lib().oracle_elastic_last_error().decode())
+
+
+def sdc_axis_coefficients(comp, dim, mu, lam):
+    out = np.zeros(dim)
+    _echk(_elastic_lib().oracle_sdc_axis_coefficients(comp, dim, mu, lam, out))
+    return out
+
+
+class ElasticProblem:
+    """Vector Q_p linear elasticity on the reference's Table-2 'table' mesh
+    (unit square/cube, x = 0 Dirichlet, other boundary facets Neumann), with
+    the SDC/FDM two-level solver of build_elasticity_twolevel."""
+
+    OPS = {"apply_St": 0, "apply_S": 1, "patch": 2, "smooth": 3, "vcycle": 4}
+
+    def __init__(self, dim, n, p, mu=1.0, lam=0.0, skip_boundary_patches=False, threads=1):
+        L = _elastic_lib()
+        self.h = L.oracle_elastic_create(dim, n, p, mu, lam, 1 if skip_boundary_patches else 0, threads)
+        if not self.h:
+            raise OracleError(L.oracle_elastic_last_error().decode())
+        info = np.zeros(7, np.int64)
+        _echk(L.oracle_elastic_info(self.h, info))
+        self.dim, self.p, self.ncells, self.ndof, self.nsc, self.nfree, self.npc = (int(v) for v in info)
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.oracle_elastic_destroy(self.h)
+            self.h = None
+
+    def rhs(self):
+        out = np.zeros(self.ndof)
+        _echk(_elastic_lib().oracle_elastic_rhs(self.h, out))
+        return out
+
+    def random_free(self, seed):
+        out = np.zeros(self.ndof)
+        _echk(_elastic_lib().oracle_elastic_random_free(self.h, seed, out))
+        return out
+
+    def maps(self):
+        cd = np.zeros(self.ncells * self.npc, np.int32)
+        con, mult = np.zeros(self.ndof, np.uint8), np.zeros(self.ndof)
+        _echk(_elastic_lib().oracle_elastic_maps(self.h, cd, con, mult))
+        return dict(cell_dofs=cd.reshape(self.ncells, self.npc), constrained=con, multiplicity=mult)
+
+    def apply_A(self, x):
+        out = np.zeros(self.ndof)
+        _echk(_elastic_lib().oracle_elastic_apply_A(self.h, np.ascontiguousarray(x, np.float64), out))
+        return out
+
+    def build(self, calibrate=True):
+        _echk(_elastic_lib().oracle_elastic_build(self.h, 1 if calibrate else 0))
+
+    def twolevel_info(self):
+        out = np.zeros(6)
+        _echk(_elastic_lib().oracle_elastic_twolevel_info(self.h, out))
+        return dict(omega=out[0], lambda_min=out[1], lambda_max=out[2], ncoarse=int(out[3]), npatches=int(out[4]),
+                    sum_nj=int(out[5]))
+
+    def set_omega(self, w):
+        _echk(_elastic_lib().oracle_elastic_set_omega(self.h, float(w)))
+
+    def op(self, name, x):
+        out = np.zeros(self.ndof)
+        _echk(_elastic_lib().oracle_elastic_op(self.h, self.OPS[name], np.ascontiguousarray(x, np.float64), out))
+        return out
+
+    def patches(self):
+        info = self.twolevel_info()
+        ptr = np.zeros(info["npatches"] + 1, np.int64)
+        dofs, vert = np.zeros(info["sum_nj"], np.int32), np.zeros(info["npatches"], np.int32)
+        _echk(_elastic_lib().oracle_elastic_patches(self.h, ptr, dofs, vert))
+        return dict(ptr=ptr, dofs=dofs, vertex=vert)
+
+    def assemble_dense(self, sdc_only=False):
+        out = np.zeros(self.ndof * self.ndof)
+        _echk(_elastic_lib().oracle_elastic_assemble_dense(self.h, 1 if sdc_only else 0, out))
+        return out.reshape(self.ndof, self.ndof)
+
+    def cell_matrices(self, cell):
+        N = self.dim * self.npc
+        kron, quad = np.zeros(N * N), np.zeros(N * N)
+        _echk(_elastic_lib().oracle_elastic_cell_matrices(self.h, cell, kron, quad))
+        return kron.reshape(N, N, order="F"), quad.reshape(N, N, order="F")
+
+    def pcg(self, b, rtol=1e-8, maxit=600, precond=2):
+        x, rep, res = np.zeros(self.ndof), np.zeros(5), np.zeros(max(maxit, 1))
+        _echk(_elastic_lib().oracle_elastic_pcg(self.h, np.ascontiguousarray(b, np.float64), x, rtol, maxit, precond,
+                                                rep, res))
+        it = int(rep[0])
+        return x, dict(iterations=it, converged=bool(rep[1]), kappa=rep[2], lambda_min=rep[3], lambda_max=rep[4],
+                       residuals=res[:it].copy())

@@ -72,6 +72,8 @@ def lib():
         L.fdmhost_problem_create.restype = _vp
         L.fdmhost_problem_create.argtypes = [C.c_int, C.c_int, C.c_int]
         L.fdmhost_problem_destroy.argtypes = [_vp]
+        L.fdmhost_elastic_create.restype = _vp
+        L.fdmhost_elastic_create.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_int]
         L.fdmhost_problem_from_mesh_file.restype = _vp
         L.fdmhost_problem_from_mesh_file.argtypes = [C.c_char_p, C.c_int, C.c_uint64]
         L.fdmhost_problem_from_mesh.restype = _vp
@@ -154,14 +156,29 @@ class Problem:
         self.h = _handle if _handle is not None else L.fdmhost_problem_create(config, n, p)
         if not self.h:
             raise FdmGpuError(1, L.fdmhost_last_error().decode())
-        if not skip_boundary_patches:
+        if skip_boundary_patches is False:
             _host_chk(L.fdmhost_problem_set_skip_boundary_patches(self.h, 0))
-        self.skip_boundary_patches = bool(skip_boundary_patches)
-        info = np.zeros(15, np.int64)
+        self.skip_boundary_patches = skip_boundary_patches is not False
+        info = np.zeros(16, np.int64)
         _host_chk(L.fdmhost_problem_info(self.h, _ptr(info)))
         (self.dim, self.p, self.ncells, self.ndof, self.nfree, self.npatches, self.nvertices, self.npc,
-         self.sum_nj, self.ncoarse, self.P_nnz, self.q, self.config, self.n, cart) = (int(v) for v in info)
+         self.sum_nj, self.ncoarse, self.P_nnz, self.q, self.config, self.n, cart, self.ncomp) = (int(v) for v in info)
         self.all_cartesian = bool(cart)
+
+    @classmethod
+    def elasticity(cls, dim, n, p, mu=1.0, lam=0.0, skip_boundary_patches=False):
+        """Linear elasticity (src/elasticity.cpp) on the reference's Table-2 problem
+        (tests/test_elasticity.cpp:24-30, 162-185) in dim = 2|3: unit square/cube
+        with n cells per axis, x = 0 Dirichlet, other boundary facets Neumann,
+        vector Q_p, Lame mu / lam, body force -0.02 e_{dim-1}.  The Solver then
+        runs build_elasticity_twolevel's path: true-form operator, SDC/FDM
+        relaxation per component, vector Q1 coarse space.  skip_boundary_patches
+        defaults to the reference's SolverConfig default (False)."""
+        h = lib().fdmhost_elastic_create(int(dim), int(n), int(p), float(mu), float(lam),
+                                         1 if skip_boundary_patches else 0)
+        if not h:
+            raise FdmGpuError(1, lib().fdmhost_last_error().decode())
+        return cls(0, _handle=h, skip_boundary_patches=True if skip_boundary_patches else None)
 
     # ---- external meshes (the reference's mesh file format, src/mesh.cpp:354-434) ----
     TAGS = {"interior": 0, "dirichlet": 1, "neumann": 2}

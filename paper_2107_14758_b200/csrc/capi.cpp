@@ -60,7 +60,16 @@ void copy_dev(Context& c, double* dst, const double* src) {
 }
 
 // ---- device operators ----------------------------------------------------------
+// Vector (elasticity SDC) handles run the block-diagonal operators component
+// by component on their scalar sub-contexts (contiguous component blocks).
+template <class Fn>
+void per_component(Context& c, const double* in, double* out, Fn&& fn) {
+  for (int ci = 0; ci < c.ncomp; ++ci) fn(c.sub(ci), in + ci * c.nsc, out + ci * c.nsc);
+}
+
 void op_transform(Context& c, int dir, const double* in, double* out) {
+  if (c.ncomp > 1)
+    return per_component(c, in, out, [&](Context& s, const double* i, double* o) { op_transform(s, dir, i, o); });
   launch_cells_transform(c, dir, in, 0, nullptr);
   launch_gather(c, dir, c.E.p, nullptr, out);
 }
@@ -68,6 +77,7 @@ void op_transform(Context& c, int dir, const double* in, double* out) {
 // PatchSolver::apply on a modal vector (src/schwarz.cpp:41-54): Schur-reduced
 // separator RHS, batched separator solves, patch sum, interior rebuild.
 void op_patch(Context& c, const double* in, double* out) {
+  if (c.ncomp > 1) return per_component(c, in, out, [](Context& s, const double* i, double* o) { op_patch(s, i, o); });
   launch_cells_schur(c, in);
   launch_gather(c, 3, c.E.p, in, c.w[6].p);
   launch_patch_solve(c, c.w[6].p);
@@ -78,6 +88,7 @@ void op_patch(Context& c, const double* in, double* out) {
 // TwoLevel::smooth (src/schwarz.cpp:121-123) = S * PatchSolver(S^T r), with
 // the interior elimination fused into the two cell transforms.
 void op_smooth(Context& c, const double* r, double* z) {
+  if (c.ncomp > 1) return per_component(c, r, z, [](Context& s, const double* i, double* o) { op_smooth(s, i, o); });
   launch_cells_transform(c, 0, r, 1, nullptr);  // S^T r, minus each cell's interior-elimination share
   launch_gather(c, 0, c.E.p, nullptr, c.w[6].p);
   launch_patch_solve(c, c.w[6].p);               // separator solves
@@ -87,8 +98,31 @@ void op_smooth(Context& c, const double* r, double* z) {
 }
 
 void op_A(Context& c, const double* x, double* y) {  // src/assembly.cpp:56-88
+  if (c.ncomp > 1) {  // elasticity_primal_operator (src/elasticity.cpp:69-120): all blocks in one cell pass
+    launch_cells_elastic(c, x);
+    for (int ci = 0; ci < c.ncomp; ++ci)
+      launch_gather(c.sub(ci), 2, c.E.p + size_t(ci) * c.ncells * c.npc, x + ci * c.nsc, y + ci * c.nsc);
+    return;
+  }
   launch_cells_stiffness(c, x);
   launch_gather(c, 2, c.E.p, x, y);
+}
+
+// Coarse transfer: component-wise cell kernels on vector handles with cell
+// transfer data, else the handle's own (CSR or cell) path.
+void transfer_restrict(Context& c, const double* fine, double* coarse) {
+  if (c.ncomp > 1 && c.have_coarse_cells) {
+    for (int ci = 0; ci < c.ncomp; ++ci) launch_restrict(c.sub(ci), fine + ci * c.nsc, coarse + ci * c.ncs);
+    return;
+  }
+  launch_restrict(c, fine, coarse);
+}
+void transfer_prolong_add(Context& c, const double* coarse, double* fine) {
+  if (c.ncomp > 1 && c.have_coarse_cells) {
+    for (int ci = 0; ci < c.ncomp; ++ci) launch_prolong_add(c.sub(ci), coarse + ci * c.ncs, fine + ci * c.nsc);
+    return;
+  }
+  launch_prolong_add(c, coarse, fine);
 }
 
 void op_vcycle(Context& c, double omega, const double* r, double* z) {  // src/schwarz.cpp:125-133
@@ -99,9 +133,9 @@ void op_vcycle(Context& c, double omega, const double* r, double* z) {  // src/s
   launch_axpby(c, c.ndof, omega, t1, 0.0, t1, z);  // z = omega * smooth(r)
   op_A(c, z, t2);
   launch_axpby(c, c.ndof, 1.0, r, -1.0, t2, t3);  // r1 = r - A z
-  launch_restrict(c, t3, c.rc.p);
+  transfer_restrict(c, t3, c.rc.p);
   launch_coarse_solve(c, c.rc.p, c.zc.p);
-  launch_prolong_add(c, c.zc.p, z);  // z += P A_c^{-1} P^T r1
+  transfer_prolong_add(c, c.zc.p, z);  // z += P A_c^{-1} P^T r1
   op_A(c, z, t2);
   launch_axpby(c, c.ndof, 1.0, r, -1.0, t2, t3);  // r2 = r - A z
   op_smooth(c, t3, t1);
@@ -162,6 +196,7 @@ void build_pcg_graph(Context& c, int precond, double omega) {
     c.pcg_exec = nullptr;
   }
   prepare_buffers(c);
+  for (Context* s : c.comp) prepare_buffers(*s);
   const bool timing = c.timing;
   c.timing = false;  // no event records inside the captured graph
   c.capturing = true;
@@ -324,13 +359,33 @@ fdmgpu_status guarded(fdmgpu_handle h, Fn&& fn) {
   }
 }
 
+// Forwards a public call to every component sub-handle; a failure is
+// re-thrown with the sub-handle's status and message.
+template <class Fn>
+void forward(Context& c, Fn&& fn) {
+  for (int ci = 0; ci < int(c.comp.size()); ++ci) {
+    Context& s = c.sub(ci);
+    const fdmgpu_status st = fn(reinterpret_cast<fdmgpu_handle>(&s), ci);
+    if (st != FDMGPU_OK) throw Error(st, s.err);
+  }
+}
+
 }  // namespace
 }  // namespace fdmgpu
 
 using fdmgpu::Context;
+
 using fdmgpu::Error;
 
 struct fdmgpu_context : fdmgpu::Context {};
+
+namespace fdmgpu {
+void destroy_sub(Context* s) {
+  s->stream = nullptr;  // the parent's stream
+  s->own_stream = false;
+  delete reinterpret_cast<fdmgpu_context*>(s);
+}
+}  // namespace fdmgpu
 
 extern "C" {
 
@@ -411,6 +466,37 @@ fdmgpu_status fdmgpu_set_stream(fdmgpu_handle h, void* stream) {
     if (c.own_stream) cudaStreamDestroy(c.stream);
     c.stream = static_cast<cudaStream_t>(stream);
     c.own_stream = false;
+    for (Context* sc : c.comp) sc->stream = c.stream;
+  });
+}
+
+/* Linear elasticity (src/elasticity.cpp): turns a fresh handle into a vector
+ * handle with dim identical components and the SDC relaxation. */
+fdmgpu_status fdmgpu_set_elasticity(fdmgpu_handle h, double mu, double lambda, const double* C) {
+  return fdmgpu::guarded(h, [&](Context& c) {
+    if (c.have_maps || !c.comp.empty()) throw Error(FDMGPU_INVALID_ARGUMENT, "set_elasticity: call right after fdmgpu_create");
+    if (!C) throw Error(FDMGPU_INVALID_ARGUMENT, "set_elasticity: null C");
+    if (!(mu > 0.0) || !(lambda >= 0.0) || std::isinf(lambda))
+      throw Error(FDMGPU_INVALID_ARGUMENT, "elasticity_primal_operator: lambda must be finite");
+    if (c.ndof % c.dim != 0) throw Error(FDMGPU_INVALID_ARGUMENT, "set_elasticity: ndof must be dim x scalar DOFs");
+    c.ncomp = c.dim;
+    c.nsc = c.ndof / c.dim;
+    c.lame_mu = mu;
+    c.lame_lambda = lambda;
+    c.Cm.upload(C, size_t(c.n1) * c.n1, c.stream);
+    c.E.alloc(size_t(c.ncomp) * c.ncells * c.npc);
+    for (int ci = 0; ci < c.ncomp; ++ci) {
+      fdmgpu_handle sh = nullptr;
+      const fdmgpu_status st = fdmgpu_create(&sh, c.dim, c.p, c.ncells, c.nsc, c.device);
+      if (st != FDMGPU_OK) throw Error(st, "set_elasticity: component handle");
+      FDM_CUDA(cudaStreamSynchronize(sh->stream));
+      cudaStreamDestroy(sh->stream);
+      sh->own_stream = false;
+      sh->stream = c.stream;
+      sh->sep_order = c.sep_order;
+      c.comp.push_back(sh);
+    }
+    FDM_CUDA(cudaStreamSynchronize(c.stream));
   });
 }
 
@@ -452,6 +538,9 @@ fdmgpu_status fdmgpu_set_basis(fdmgpu_handle h, const double* S, const double* l
       c.wq.upload(wq, q, c.stream);
     }
     FDM_CUDA(cudaStreamSynchronize(c.stream));
+    fdmgpu::forward(c, [&](fdmgpu_handle sh, int) {
+      return fdmgpu_set_basis(sh, S, lambda, A_t, B_t, A_t_pattern, B_t_pattern, A_hat, B_hat, q, q_points, wq, Vq, Dq);
+    });
     c.have_basis = true;
   });
 }
@@ -461,6 +550,36 @@ fdmgpu_status fdmgpu_set_mesh_maps(fdmgpu_handle h, const int32_t* cell_dofs, co
   return fdmgpu::guarded(h, [&](Context& c) {
     if (!cell_dofs || !multiplicity || !constrained) throw Error(FDMGPU_INVALID_ARGUMENT, "set_mesh_maps: null array");
     const size_t nm = size_t(c.ncells) * c.npc;
+    if (c.ncomp > 1) {
+      // Vector handle: component-0 cell maps, per-DOF arrays over all components
+      // (identical blocks); each component handle gets the scalar maps.
+      if (mode_signs || (cell_modes && !std::equal(cell_dofs, cell_dofs + nm, cell_modes)))
+        throw Error(FDMGPU_UNSUPPORTED, "set_mesh_maps: elasticity needs unflipped lattice meshes");
+      for (int ci = 1; ci < c.ncomp; ++ci)
+        for (int64_t i = 0; i < c.nsc; ++i)
+          if (constrained[ci * c.nsc + i] != constrained[i] || multiplicity[ci * c.nsc + i] != multiplicity[i])
+            throw Error(FDMGPU_INVALID_ARGUMENT, "set_mesh_maps: components must share one scalar space");
+      for (size_t k = 0; k < nm; ++k)
+        if (cell_dofs[k] < 0 || cell_dofs[k] >= c.nsc) throw Error(FDMGPU_INVALID_ARGUMENT, "set_mesh_maps: DOF out of range");
+      c.h_cell_dofs.assign(cell_dofs, cell_dofs + nm);
+      c.h_cell_modes = c.h_cell_dofs;
+      c.h_constrained.assign(constrained, constrained + c.ndof);
+      std::vector<double> inv(c.ndof);
+      for (int64_t i = 0; i < c.ndof; ++i) {
+        if (!(multiplicity[i] > 0)) throw Error(FDMGPU_INVALID_ARGUMENT, "set_mesh_maps: multiplicity must be > 0");
+        inv[i] = 1.0 / multiplicity[i];
+      }
+      c.cell_dofs.upload(c.h_cell_dofs, c.stream);
+      c.cell_modes.upload(c.h_cell_dofs, c.stream);
+      c.inv_mult.upload(inv, c.stream);
+      c.constrained.upload(c.h_constrained, c.stream);
+      FDM_CUDA(cudaStreamSynchronize(c.stream));
+      fdmgpu::forward(c, [&](fdmgpu_handle sh, int) {
+        return fdmgpu_set_mesh_maps(sh, cell_dofs, nullptr, nullptr, multiplicity, constrained);
+      });
+      c.have_maps = true;
+      return;
+    }
     c.h_cell_dofs.assign(cell_dofs, cell_dofs + nm);
     c.h_cell_modes.assign(cell_modes ? cell_modes : cell_dofs, (cell_modes ? cell_modes : cell_dofs) + nm);
     c.modes_alias = c.h_cell_modes == c.h_cell_dofs;
@@ -501,6 +620,33 @@ fdmgpu_status fdmgpu_set_cell_coeffs(fdmgpu_handle h, const uint8_t* kind, const
                                      const double* kappa) {
   return fdmgpu::guarded(h, [&](Context& c) {
     if (!kind || !mu) throw Error(FDMGPU_INVALID_ARGUMENT, "set_cell_coeffs: null array");
+    if (c.ncomp > 1) {
+      // elasticity_primal_operator's Kronecker path (src/elasticity.cpp:83-119):
+      // Cartesian cells, no kappa; component ci's SDC coefficients are
+      // sdc_axis_coefficients(ci) * mu^K (src/elasticity.cpp:141-151).
+      for (int k = 0; k < c.ncells; ++k)
+        if (kind[k] != 0) throw Error(FDMGPU_UNSUPPORTED, "elasticity: non-Cartesian cells need the dense quadrature form");
+      if (kappa)
+        for (int k = 0; k < c.ncells; ++k)
+          if (kappa[k] != 1.0) throw Error(FDMGPU_INVALID_ARGUMENT, "elasticity: per-cell kappa is not part of the operator");
+      c.all_cartesian = true;
+      c.kind.upload(kind, c.ncells, c.stream);
+      c.h_mu.assign(mu, mu + size_t(c.ncells) * c.dim);
+      c.mu.upload(c.h_mu, c.stream);
+      FDM_CUDA(cudaStreamSynchronize(c.stream));
+      fdmgpu::forward(c, [&](fdmgpu_handle sh, int ci) {
+        std::vector<double> m(c.h_mu.size());
+        for (int k = 0; k < c.ncells; ++k)
+          for (int a = 0; a < c.dim; ++a) {
+            const double coeff = c.lame_mu + (a == ci ? c.lame_mu + c.lame_lambda : 0.0);
+            m[size_t(k) * c.dim + a] = coeff * c.h_mu[size_t(k) * c.dim + a];
+          }
+        return fdmgpu_set_cell_coeffs(sh, kind, m.data(), xyz, nullptr);
+      });
+      c.have_coeffs = true;
+      c.factored = false;
+      return;
+    }
     c.all_cartesian = true;
     for (int k = 0; k < c.ncells; ++k) c.all_cartesian = c.all_cartesian && kind[k] == 0;
     if (!c.all_cartesian && !xyz)
@@ -524,6 +670,41 @@ fdmgpu_status fdmgpu_set_patches(fdmgpu_handle h, int32_t npatch, const int32_t*
     c.check_ready(false, false, false);
     if (npatch < 1 || !vertex || !ptr || !dofs || !perm || !star_cells)
       throw Error(FDMGPU_INVALID_ARGUMENT, "set_patches: bad arguments");
+    if (c.ncomp > 1) {
+      // Vector stars (star_dofs over all components, src/discretization.cpp:
+      // 266-297): the SDC patch matrix is block diagonal over components, so
+      // component ci solves its own star with the order patch_ordering gives
+      // its DOFs inside the vector order.
+      std::vector<std::vector<int64_t>> cptr(c.ncomp, std::vector<int64_t>(1, 0));
+      std::vector<std::vector<int32_t>> cdofs(c.ncomp), cperm(c.ncomp);
+      std::vector<int32_t> local;
+      for (int j = 0; j < npatch; ++j) {
+        const int64_t b = ptr[j], e = ptr[j + 1];
+        local.assign(size_t(e - b), -1);
+        std::vector<int32_t> cnt(c.ncomp, 0);
+        for (int64_t k = b; k < e; ++k) {
+          const int32_t g = dofs[k];
+          if (g < 0 || g >= c.ndof) throw Error(FDMGPU_INVALID_ARGUMENT, "set_patches: DOF out of range");
+          const int ci = int(g / c.nsc);
+          local[k - b] = cnt[ci]++;
+          cdofs[ci].push_back(int32_t(g - ci * c.nsc));
+        }
+        for (int64_t k = b; k < e; ++k) {
+          const int32_t q = perm[k];
+          if (q < 0 || q >= e - b) throw Error(FDMGPU_INVALID_ARGUMENT, "set_patches: bad permutation");
+          cperm[int(dofs[b + q] / c.nsc)].push_back(local[q]);
+        }
+        for (int ci = 0; ci < c.ncomp; ++ci) cptr[ci].push_back(int64_t(cdofs[ci].size()));
+      }
+      fdmgpu::forward(c, [&](fdmgpu_handle sh, int ci) {
+        sh->sep_order = c.sep_order;
+        return fdmgpu_set_patches(sh, npatch, vertex, cptr[ci].data(), cdofs[ci].data(), cperm[ci].data(), star_cells);
+      });
+      c.npatch = npatch;
+      c.have_patches = true;
+      c.factored = false;
+      return;
+    }
     if (c.mode_sign.p || !c.modes_alias)
       throw Error(FDMGPU_UNSUPPORTED, "set_patches: facet mode flips (2D non-lattice meshes) are not supported");
     fdmgpu::analyze_patches(c, npatch, vertex, ptr, dofs, perm, star_cells);
@@ -621,6 +802,20 @@ fdmgpu_status fdmgpu_set_coarse_cells(fdmgpu_handle h, const int32_t* coarse_cel
     if (!c.have_coarse || !c.have_maps) throw Error(FDMGPU_INVALID_ARGUMENT, "set_coarse_cells: set maps and coarse first");
     if (!coarse_cell_dofs || !coarse_constrained || !phat)
       throw Error(FDMGPU_INVALID_ARGUMENT, "set_coarse_cells: null array");
+    if (c.ncomp > 1) {
+      // Vector Q1 coarse space: component blocks of nc / ncomp coarse DOFs,
+      // prolongation per component (build_prolongation, src/schwarz.cpp:145-158).
+      if (c.nc % c.ncomp) throw Error(FDMGPU_INVALID_ARGUMENT, "set_coarse_cells: coarse ndof must be ncomp x scalar");
+      c.ncs = c.nc / c.ncomp;
+      fdmgpu::forward(c, [&](fdmgpu_handle sh, int) {
+        sh->nc = c.ncs;
+        sh->have_coarse = true;  // transfer data only: the coarse solve stays on the vector handle
+        return fdmgpu_set_coarse_cells(sh, coarse_cell_dofs, coarse_constrained, phat);
+      });
+      const char* tr = std::getenv("FDMGPU_TRANSFER");
+      c.have_coarse_cells = !(tr && std::string(tr) == "csr");
+      return;
+    }
     const int ncorner = 1 << c.dim;
     const size_t nslots = size_t(c.ncells) * ncorner;
     // coarse gather: per free coarse DOF its (cell, corner) slots, ascending
@@ -664,6 +859,12 @@ fdmgpu_status fdmgpu_set_coarse_cells(fdmgpu_handle h, const int32_t* coarse_cel
 fdmgpu_status fdmgpu_factor(fdmgpu_handle h) {
   return fdmgpu::guarded(h, [&](Context& c) {
     c.check_ready(true, false, false);
+    if (c.ncomp > 1) {
+      c.factored = false;
+      fdmgpu::forward(c, [](fdmgpu_handle sh, int) { return fdmgpu_factor(sh); });
+      c.factored = true;
+      return;
+    }
     const unsigned long long none = ~0ULL;
     FDM_CUDA(cudaMemcpyAsync(c.d_err.p, &none, sizeof(none), cudaMemcpyHostToDevice, c.stream));
     fdmgpu::launch_patch_assemble(c);
@@ -687,6 +888,22 @@ fdmgpu_status fdmgpu_factor(fdmgpu_handle h) {
 fdmgpu_status fdmgpu_get_layout(fdmgpu_handle h, fdmgpu_layout* out) {
   return fdmgpu::guarded(h, [&](Context& c) {
     c.check_ready(true, false, false);
+    if (c.ncomp > 1) {  // per-component layout; byte totals over all components
+      fdmgpu_layout L{};
+      fdmgpu::forward(c, [&](fdmgpu_handle sh, int ci) {
+        fdmgpu_layout Li{};
+        const fdmgpu_status st = fdmgpu_get_layout(sh, &Li);
+        if (ci == 0)
+          L = Li;
+        else {
+          L.factor_bytes += Li.factor_bytes;
+          L.stream_bytes += Li.stream_bytes;
+        }
+        return st;
+      });
+      *out = L;
+      return;
+    }
     fdmgpu_layout L{};
     L.npatch = c.npatch;
     L.n = c.L.n;
@@ -710,6 +927,7 @@ fdmgpu_status fdmgpu_get_layout(fdmgpu_handle h, fdmgpu_layout* out) {
 fdmgpu_status fdmgpu_patch_schur(fdmgpu_handle h, int32_t j, double* out) {
   return fdmgpu::guarded(h, [&](Context& c) {
     c.check_ready(true, false, false);
+    if (c.ncomp > 1) throw Error(FDMGPU_UNSUPPORTED, "patch_schur: scalar handles only");
     if (j < 0 || j >= c.npatch || !out) throw Error(FDMGPU_INVALID_ARGUMENT, "patch_schur: bad patch index");
     const auto& L = c.L;
     const size_t tt = size_t(fdmgpu::kTile) * fdmgpu::kTile;
@@ -737,6 +955,7 @@ fdmgpu_status fdmgpu_patch_schur(fdmgpu_handle h, int32_t j, double* out) {
 fdmgpu_status fdmgpu_get_patch_elimination_dofs(fdmgpu_handle h, int32_t* out) {
   return fdmgpu::guarded(h, [&](Context& c) {
     c.check_ready(true, false, false);
+    if (c.ncomp > 1) throw Error(FDMGPU_UNSUPPORTED, "patch elimination dofs: scalar handles only");
     std::memcpy(out, c.h_pdofs.data(), c.h_pdofs.size() * sizeof(int32_t));
   });
 }
@@ -876,12 +1095,18 @@ fdmgpu_status fdmgpu_get_omega(fdmgpu_handle h, double* omega) {
   return fdmgpu::guarded(h, [&](Context& c) { *omega = c.omega; });
 }
 
-int64_t fdmgpu_launch_count(fdmgpu_handle h) { return h ? h->launches : -1; }
+int64_t fdmgpu_launch_count(fdmgpu_handle h) {
+  if (!h) return -1;
+  int64_t n = h->launches;
+  for (Context* s : h->comp) n += s->launches;
+  return n;
+}
 
 fdmgpu_status fdmgpu_set_separator_order(fdmgpu_handle h, int32_t order) {
   return fdmgpu::guarded(h, [&](Context& c) {
     if (order != 0 && order != 1) throw Error(FDMGPU_INVALID_ARGUMENT, "separator order: 0 plane, 1 reference");
     c.sep_order = order;
+    for (Context* s : c.comp) s->sep_order = order;
   });
 }
 
@@ -896,6 +1121,7 @@ fdmgpu_status fdmgpu_kernel_timing(fdmgpu_handle h, int32_t enable) {
       v.clear();
     }
     c.timing = enable != 0;
+    fdmgpu::forward(c, [&](fdmgpu_handle sh, int) { return fdmgpu_kernel_timing(sh, enable); });
   });
 }
 
@@ -904,13 +1130,19 @@ fdmgpu_status fdmgpu_kernel_time(fdmgpu_handle h, int32_t which, double* total_m
     if (which < 0 || which > 3) throw Error(FDMGPU_INVALID_ARGUMENT, "kernel_time: class 0..3");
     FDM_CUDA(cudaStreamSynchronize(c.stream));
     double t = 0.0;
-    for (auto& [a, b] : c.tev[which]) {
-      float ms = 0.f;
-      FDM_CUDA(cudaEventElapsedTime(&ms, a, b));
-      t += ms;
-    }
+    int64_t n = 0;
+    auto add = [&](Context& cc) {
+      for (auto& [a, b] : cc.tev[which]) {
+        float ms = 0.f;
+        FDM_CUDA(cudaEventElapsedTime(&ms, a, b));
+        t += ms;
+      }
+      n += int64_t(cc.tev[which].size());
+    };
+    add(c);
+    for (Context* s : c.comp) add(*s);
     *total_ms = t;
-    *launches = int64_t(c.tev[which].size());
+    *launches = n;
   });
 }
 

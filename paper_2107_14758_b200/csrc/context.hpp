@@ -85,6 +85,9 @@ struct PcgDev {
   int k, maxit, status;  // status: 0 running, 1 converged, 2 indefinite at iteration k+1, 3 maxit
 };
 
+struct Context;
+void destroy_sub(Context* s);  // capi.cpp: frees a component sub-handle
+
 struct Context {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -94,6 +97,20 @@ struct Context {
 
   int dim = 3, p = 1, n1 = 2, npc = 8, ncells = 0;
   int64_t ndof = 0;
+
+  // Vector (linear-elasticity SDC) handles, fdmgpu_set_elasticity: ncomp = dim
+  // identical Q_p components, component ci's DOFs = component 0's + ci * nsc
+  // (src/discretization.cpp:86-258).  The SDC relaxation is block diagonal over
+  // components (src/elasticity.cpp:122-167), so each component runs on its
+  // own scalar sub-context (its own coefficients c_ci * mu^K, factors and
+  // buffers, this handle's stream); this context owns the true-form vector
+  // operator (kernels/elastic.cu), the vector coarse level and the PCG loop.
+  int ncomp = 1;
+  int64_t nsc = 0;
+  double lame_mu = 0.0, lame_lambda = 0.0;
+  DevArray<double> Cm;                 // bundle.C = V^T W D on GL(p+1) (src/assembly.cpp:49-52)
+  std::vector<Context*> comp;          // owned sub-contexts (ncomp > 1)
+  int ncs = 0;                         // scalar coarse block size
 
   // basis
   DevArray<double> S, St, Ahat, Bhat, At, Bt, Vq, Dq, wq, qpts, Qbuf;
@@ -170,7 +187,18 @@ struct Context {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tev[4];
 
   void check_ready(bool need_patches, bool need_factor, bool need_coarse) const;
+  // Component sub-context ci, synchronised with this handle's launch state
+  // (stream -- swapped during graph capture --, capture / timing / PDL flags).
+  Context& sub(int ci) {
+    Context& s = *comp[ci];
+    s.stream = stream;
+    s.capturing = capturing;
+    s.timing = timing;
+    s.pdl = pdl;
+    return s;
+  }
   ~Context() {
+    for (Context* s : comp) destroy_sub(s);
     if (pcg_exec) cudaGraphExecDestroy(pcg_exec);
     if (cap_stream) cudaStreamDestroy(cap_stream);
     for (auto& v : tev)
@@ -208,6 +236,8 @@ void launch_cells_recon(Context& c, double* z, const double* rb);
 void launch_gather(Context& c, int mode, const double* E, const double* x, double* out);
 void launch_cells_stiffness(Context& c, const double* x);            // writes c.E
 void launch_cells_quadrature(Context& c, const double* x);           // writes c.E (true form)
+void launch_cells_elastic(Context& c, const double* x);              // writes c.E (ncomp blocks, elasticity)
+size_t elastic_smem_bytes(const Context& c);
 void launch_patch_assemble(Context& c);
 void launch_patch_assemble_one(Context& c, int j, double* out);  // S_G of patch j, tile layout
 void launch_patch_update(Context& c, int K);

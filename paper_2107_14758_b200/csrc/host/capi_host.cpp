@@ -40,6 +40,15 @@ void* fdmhost_problem_create(int config, int n, int p) {
   return out;
 }
 
+// Linear elasticity (make_elastic_problem): the reference's Table-2 problem
+// in dim = 2|3 with n cells per axis, vector Q_p, Lame mu / lambda.
+void* fdmhost_elastic_create(int dim, int n, int p, double mu, double lambda, int skip_boundary_patches) {
+  Problem* out = nullptr;
+  if (guard([&] { out = make_elastic_problem(dim, n, p, mu, lambda, skip_boundary_patches != 0).release(); }))
+    return nullptr;
+  return out;
+}
+
 // Problem on a mesh file in the reference's JSON format (load_mesh,
 // src/mesh.cpp:375-434); Q_p space, unit coefficient, RHS U[-1,1] from seed.
 void* fdmhost_problem_from_mesh_file(const char* path, int p, uint64_t seed) {
@@ -91,7 +100,7 @@ int fdmhost_save_mesh(void* ph, const char* path) {
 int fdmhost_problem_set_skip_boundary_patches(void* ph, int skip) {
   return guard([&] {
     Problem& P = *static_cast<Problem*>(ph);
-    P.patches = vertex_patches(P.space, skip != 0);
+    rebuild_patches(P, skip != 0);
   });
 }
 
@@ -108,16 +117,17 @@ int fdmhost_write_matrix_market(const char* path, int64_t rows, int64_t cols, co
 void fdmhost_problem_destroy(void* ph) { delete static_cast<Problem*>(ph); }
 
 // out: dim, p, ncells, ndof, nfree, npatch, nvertices, npc, sum n_j, ncoarse,
-//      P nnz, q, config, n (cells per axis), all_cartesian
+//      P nnz, q, config, n (cells per axis), all_cartesian, ncomp
 int fdmhost_problem_info(void* ph, int64_t* out) {
   return guard([&] {
     const Problem& P = *static_cast<Problem*>(ph);
     bool cart = true;
     for (auto k : P.cell_kind) cart = cart && k == 0;
-    const int64_t v[15] = {P.dim, P.p, P.mesh.num_cells(), P.space.ndof, P.space.num_free(),
+    const int64_t v[16] = {P.dim, P.p, P.mesh.num_cells(), int64_t(P.ncomp) * P.space.ndof,
+                           int64_t(P.ncomp) * P.space.num_free(),
                            int64_t(P.patches.vertex.size()), P.mesh.num_vertices(), P.space.npc,
                            P.patches.ptr.back(), P.coarse.ndof, int64_t(P.coarse.P_col.size()), P.basis.q,
-                           P.config, P.n, cart ? 1 : 0};
+                           P.config, P.n, cart ? 1 : 0, P.ncomp};
     std::memcpy(out, v, sizeof(v));
   });
 }
@@ -129,13 +139,17 @@ int fdmhost_get_rhs(void* ph, double* out) {
 int fdmhost_get_maps(void* ph, int32_t* cell_dofs, int32_t* cell_modes, uint8_t* constrained, double* multiplicity,
                      int32_t* label_cls, int32_t* label_entity) {
   return guard([&] {
-    const Space& s = static_cast<Problem*>(ph)->space;
-    put(cell_dofs, s.cell_dofs);
+    const Problem& P = *static_cast<Problem*>(ph);
+    const Space& s = P.space;
+    put(cell_dofs, s.cell_dofs);  // component 0 for vector problems
     put(cell_modes, s.cell_modes);
-    put(constrained, s.constrained);
-    put(multiplicity, s.multiplicity);
-    put(label_cls, s.label_cls);
-    put(label_entity, s.label_entity);
+    for (int ci = 0; ci < P.ncomp; ++ci) {  // per-DOF arrays over all components
+      const size_t o = size_t(ci) * s.ndof;
+      if (constrained) put(constrained + o, s.constrained);
+      if (multiplicity) put(multiplicity + o, s.multiplicity);
+      if (label_cls) put(label_cls + o, s.label_cls);
+      if (label_entity) put(label_entity + o, s.label_entity);
+    }
   });
 }
 
@@ -198,7 +212,8 @@ int fdmhost_get_coarse(void* ph, double* inverse, int64_t* P_ptr, int32_t* P_col
 int fdmhost_attach(void* ph, int device, int sep_order, fdmgpu_handle* out) {
   Problem& P = *static_cast<Problem*>(ph);
   fdmgpu_handle h = nullptr;
-  fdmgpu_status st = fdmgpu_create(&h, P.dim, P.p, P.mesh.num_cells(), P.space.ndof, device);
+  const int64_t ndof = int64_t(P.ncomp) * P.space.ndof;
+  fdmgpu_status st = fdmgpu_create(&h, P.dim, P.p, P.mesh.num_cells(), ndof, device);
   if (st != FDMGPU_OK) {
     g_err = h ? fdmgpu_last_error(h) : "fdmgpu_create failed (no CUDA device?)";
     return st;
@@ -209,18 +224,26 @@ int fdmhost_attach(void* ph, int device, int sep_order, fdmgpu_handle* out) {
     return int(s);
   };
   if (sep_order >= 0 && (st = fdmgpu_set_separator_order(h, sep_order)) != FDMGPU_OK) return fail(st);
+  if (P.ncomp > 1 && (st = fdmgpu_set_elasticity(h, P.lame_mu, P.lame_lambda, P.Cmat.data())) != FDMGPU_OK)
+    return fail(st);
   const Basis1D& b = P.basis;
   if ((st = fdmgpu_set_basis(h, b.S.a.data(), b.lambda.data(), b.A_t.a.data(), b.B_t.a.data(), b.A_nz.data(),
                              b.B_nz.data(), b.A_hat.a.data(), b.B_hat.a.data(), b.q, b.qp.data(), b.wq.data(),
                              b.Vq.a.data(), b.Dq.a.data())) != FDMGPU_OK)
     return fail(st);
   const Space& s = P.space;
+  std::vector<double> mult(s.multiplicity);
+  std::vector<uint8_t> con(s.constrained);
+  for (int ci = 1; ci < P.ncomp; ++ci) {  // vector_q_space: identical component blocks
+    mult.insert(mult.end(), s.multiplicity.begin(), s.multiplicity.end());
+    con.insert(con.end(), s.constrained.begin(), s.constrained.end());
+  }
   if ((st = fdmgpu_set_mesh_maps(h, s.cell_dofs.data(), s.cell_modes.data(),
-                                 s.mode_sign.empty() ? nullptr : s.mode_sign.data(), s.multiplicity.data(),
-                                 s.constrained.data())) != FDMGPU_OK)
+                                 s.mode_sign.empty() ? nullptr : s.mode_sign.data(), mult.data(), con.data())) !=
+      FDMGPU_OK)
     return fail(st);
   if ((st = fdmgpu_set_cell_coeffs(h, P.cell_kind.data(), P.cell_mu.data(), P.cell_xyz.data(),
-                                   P.cell_kappa.data())) != FDMGPU_OK)
+                                   P.ncomp > 1 ? nullptr : P.cell_kappa.data())) != FDMGPU_OK)
     return fail(st);
   const Patches& pt = P.patches;
   if ((st = fdmgpu_set_patches(h, int32_t(pt.vertex.size()), pt.vertex.data(), pt.ptr.data(), pt.dofs.data(),

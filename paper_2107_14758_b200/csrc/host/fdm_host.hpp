@@ -140,6 +140,8 @@ struct Coarse {
   std::vector<double> phat;           // (p+1) x 2 Q1 hats at the fine nodes, column-major
 };
 Coarse build_coarse(const Mesh& m, const Space& fine, const Basis1D& fb);
+// Row-major inverse of a dense SPD matrix through its Cholesky factor.
+std::vector<double> dense_spd_inverse(const std::vector<double>& A, int n);
 
 // ---- synthetic configurations C1..C5 ------------------------
 struct Problem {
@@ -154,11 +156,31 @@ struct Problem {
   std::vector<double> cell_kappa;   // ncells
   Patches patches;
   Coarse coarse;
+  // Linear elasticity (make_elastic_problem): ncomp = dim identical
+  // components of `space` (vector_q_space, src/discretization.cpp:313-318);
+  // rhs, patches and coarse are then the vector ones.
+  int ncomp = 1;
+  double lame_mu = 0.0, lame_lambda = 0.0;
+  std::vector<double> Cmat;  // bundle.C = V^T W D on GL(p+1), (p+1)^2 column-major
+  bool skip_boundary = true;
 };
 std::unique_ptr<Problem> make_problem(int config, int n_override, int p_override);
 // Space, RHS (U[-1,1], or N(0,1) when `normal`, from `rng`), cell data, patches, coarse level.
 void finish_problem(Problem& pb, std::mt19937_64& rng, bool normal);
 std::unique_ptr<Problem> make_problem_from_mesh(Mesh mesh, int p, uint64_t seed);
+
+// ---- linear elasticity (src/elasticity.cpp) ------------------------------------
+// The reference's Table-2 problem generalised to dim = 2|3
+// (tests/test_elasticity.cpp:24-30, 162-185): unit square/cube with n cells per
+// axis, every boundary facet Neumann except x = 0 (Dirichlet), vector Q_p,
+// body force -0.02 e_{dim-1} (vector_load, src/elasticity.cpp:169-202),
+// Lame parameters mu, lambda; vector Q1 coarse level with the true form.
+std::unique_ptr<Problem> make_elastic_problem(int dim, int n, int p, double mu, double lambda, bool skip_boundary);
+// Vector star lists (star_dofs over all components, src/discretization.cpp:
+// 266-297) and their patch_ordering, from the scalar ones.
+Patches vector_patches(const Space& s, const Patches& scalar, int ncomp);
+// The patch lists of `pb` for skip_boundary (scalar or vector).
+void rebuild_patches(Problem& pb, bool skip_boundary);
 // write_matrix_market (src/sparse.cpp:33-52) for a CSC matrix (column-major, like SpMat).
 void write_matrix_market(const std::string& path, int64_t rows, int64_t cols, const int64_t* colptr,
                          const int32_t* rowidx, const double* val, bool symmetric);

@@ -438,6 +438,49 @@ Patches vertex_patches(const Space& s, bool skip_boundary) {
   return P;
 }
 
+// Dense Cholesky (natural ordering, as cholesky(A, natural_ordering) on the
+// assembled coarse matrix, src/schwarz.cpp:242-243) and the explicit inverse
+// (row-major n x n); the coarse problems are at most a few thousand DOFs.
+std::vector<double> dense_spd_inverse(const std::vector<double>& A, int nc) {
+  std::vector<double> L(size_t(nc) * nc, 0.0);  // row-major lower factor
+  for (int j = 0; j < nc; ++j) {
+    const double* Lj = &L[size_t(j) * nc];
+    double dd = A[size_t(j) * nc + j];
+    for (int k = 0; k < j; ++k) dd -= Lj[k] * Lj[k];
+    if (!(dd > 0.0)) throw std::runtime_error("cholesky: coarse matrix not SPD at pivot " + std::to_string(j));
+    L[size_t(j) * nc + j] = std::sqrt(dd);
+    for (int i = j + 1; i < nc; ++i) {
+      const double* Li = &L[size_t(i) * nc];
+      double s = A[size_t(i) * nc + j];
+      for (int k = 0; k < j; ++k) s -= Li[k] * Lj[k];
+      L[size_t(i) * nc + j] = s / Lj[j];
+    }
+  }
+  // W[e][i] = (L^{-1})(i, e): forward substitution per unit vector.
+  std::vector<double> W(size_t(nc) * nc, 0.0);
+  for (int e = 0; e < nc; ++e) {
+    double* x = &W[size_t(e) * nc];
+    for (int i = e; i < nc; ++i) {
+      const double* Li = &L[size_t(i) * nc];
+      double s = i == e ? 1.0 : 0.0;
+      for (int k = e; k < i; ++k) s -= Li[k] * x[k];
+      x[i] = s / Li[i];
+    }
+  }
+  // A^{-1} = L^{-T} L^{-1}: entry (i, j) = sum_k W[i][k] W[j][k].
+  std::vector<double> inv(size_t(nc) * nc, 0.0);
+  for (int i = 0; i < nc; ++i)
+    for (int j = 0; j <= i; ++j) {
+      const double* wi = &W[size_t(i) * nc];
+      const double* wj = &W[size_t(j) * nc];
+      double s = 0.0;
+      for (int k = i; k < nc; ++k) s += wi[k] * wj[k];
+      inv[size_t(i) * nc + j] = s;
+      inv[size_t(j) * nc + i] = s;
+    }
+  return inv;
+}
+
 Coarse build_coarse(const Mesh& m, const Space& fine, const Basis1D& fb) {
   const int d = m.dim;
   Space cs = q_space(m, 1);
@@ -512,36 +555,7 @@ Coarse build_coarse(const Mesh& m, const Space& fine, const Basis1D& fb) {
   }
   for (int i = 0; i < nc; ++i)
     if (cs.constrained[i]) A[size_t(i) * nc + i] = 1.0;
-  // Dense Cholesky and explicit inverse (the coarse problem is <= 729 DOFs).
-  std::vector<double> L(size_t(nc) * nc, 0.0);
-  for (int j = 0; j < nc; ++j) {
-    double dd = A[size_t(j) * nc + j];
-    for (int k = 0; k < j; ++k) dd -= L[size_t(j) * nc + k] * L[size_t(j) * nc + k];
-    if (!(dd > 0.0)) throw std::runtime_error("cholesky: coarse matrix not SPD at pivot " + std::to_string(j));
-    L[size_t(j) * nc + j] = std::sqrt(dd);
-    for (int i = j + 1; i < nc; ++i) {
-      double s = A[size_t(i) * nc + j];
-      for (int k = 0; k < j; ++k) s -= L[size_t(i) * nc + k] * L[size_t(j) * nc + k];
-      L[size_t(i) * nc + j] = s / L[size_t(j) * nc + j];
-    }
-  }
-  C.inverse.assign(size_t(nc) * nc, 0.0);
-  std::vector<double> col(nc);
-  for (int e = 0; e < nc; ++e) {
-    std::fill(col.begin(), col.end(), 0.0);
-    col[e] = 1.0;
-    for (int i = 0; i < nc; ++i) {
-      double s = col[i];
-      for (int k = 0; k < i; ++k) s -= L[size_t(i) * nc + k] * col[k];
-      col[i] = s / L[size_t(i) * nc + i];
-    }
-    for (int i = nc - 1; i >= 0; --i) {
-      double s = col[i];
-      for (int k = i + 1; k < nc; ++k) s -= L[size_t(k) * nc + i] * col[k];
-      col[i] = s / L[size_t(i) * nc + i];
-    }
-    for (int i = 0; i < nc; ++i) C.inverse[size_t(i) * nc + e] = col[i];
-  }
+  C.inverse = dense_spd_inverse(A, nc);
   // Prolongation: Q1 hats at the fine GLL nodes, summed over cells, divided
   // by the fine multiplicity; constrained rows / columns dropped.
   const int p = fb.p, n1 = p + 1;
