@@ -404,6 +404,130 @@ def run_ours(args):
     return 0
 
 
+def elastic_flops(prob):
+    """kron_apply count of elasticity_primal_operator (src/elasticity.cpp:83-119): per cell d^2 diagonal-block
+    terms + 2 d (d-1) cross-block terms, each d contractions of 2 (p+1)^(d+1) flop."""
+    d, n1 = prob.dim, prob.p + 1
+    return 2.0 * n1 ** (d + 1) * d * (d * d + 2 * d * (d - 1)) * prob.ncells
+
+
+def run_elastic(args):
+    """Linear-elasticity workload: the SDC/FDM relaxation of build_elasticity_twolevel on the
+    reference's Table-2 problem in 3D (--elastic DIM,N,P,LAMBDA).  Same timing rules as the main line."""
+    import numpy as np
+    import torch
+
+    import paper_2107_14758_b200 as pkg
+
+    dim, n, p, lam = (float(v) for v in args.elastic.split(","))
+    dim, n, p = int(dim), int(n), int(p)
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.current_stream(dev)
+    t0 = time.perf_counter()
+    prob = pkg.Problem.elasticity(dim, n, p, 1.0, lam)
+    sol = pkg.Solver(prob, device=0, stream=stream)
+    setup_s = time.perf_counter() - t0
+    L = sol.layout()
+
+    def ev_time(fn, reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record(stream)
+        for _ in range(reps):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps
+
+    factor_ms = min(ev_time(sol.factor, 1) for _ in range(2))
+    r = torch.from_numpy(prob.rhs()).to(dev)
+    z = torch.empty_like(r)
+    for _ in range(args.warmup):
+        sol.smooth(r, z)
+    l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
+    working_set = 2 * L["stream_bytes"] + 4 * 8 * prob.ndof
+    flush = working_set < 2 * l2_bytes
+    flush_buf = torch.empty(512 << 20, dtype=torch.uint8, device=dev) if flush else None
+    launches0 = sol.launch_count()
+    with ClockSampler(0) as clk:
+        if flush:
+            ms = 0.0
+            for _ in range(args.steps):
+                flush_buf.zero_()
+                ms += ev_time(lambda: sol.smooth(r, z), 1)
+        else:
+            ms = ev_time(lambda: sol.smooth(r, z), args.steps) * args.steps
+    gpu_launches = sol.launch_count() - launches0
+    ms_per_step = ms / args.steps
+    n_op = max(5, min(args.steps, 50))
+    for _ in range(3):
+        sol.apply_A(r, z)
+    a_ms = ev_time(lambda: sol.apply_A(r, z), n_op)
+    sol.kernel_timing(True)
+    for _ in range(n_op):
+        sol.apply_A(r, z)
+    torch.cuda.synchronize()
+    ak_ms, ak_n = sol.kernel_time("stiffness")
+    sol.kernel_timing(False)
+    h_in = torch.from_numpy(prob.rhs()).pin_memory().numpy()
+    h_out = torch.empty(prob.ndof, dtype=torch.float64).pin_memory().numpy()
+    sol.apply(pkg.OP_SMOOTH, h_in, h_out)
+    e2e_ms = ev_time(lambda: sol.apply(pkg.OP_SMOOTH, h_in, h_out), args.steps)
+    t = time.perf_counter()
+    cal = sol.calibrate_damping()
+    cal_s = time.perf_counter() - t
+    x, rep = sol.pcg(r, rtol=1e-8, maxit=600)
+    flops = elastic_flops(prob)
+    hbm_peak, peak_src = measured_peaks()
+    result = {
+        "metric": "Elasticity SDC relaxation apply GDOF/s (FP64)", "value": prob.nfree / (ms_per_step * 1e-3) / 1e9,
+        "unit": "GDOF/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"elasticity (Table-2 problem, tests/test_elasticity.cpp:157-185) dim {dim}, {n}^{dim} "
+                               f"cells, vector Q{p}, mu 1, lambda {lam:g}, boundary stars included",
+                   "ndof": prob.ndof, "nfree": prob.nfree, "patches": L["npatch"], "components": prob.ncomp,
+                   "l2": "L2 flushed before every step" if flush else
+                         f"inputs larger than L2: 2 x {L['stream_bytes'] / 1e9:.2f} GB packed factors per step"},
+        "residual_roofline": {"kernel": "k_cells_elastic (+ per-component k_gather)", "bound": "fp64",
+                              "op_ms": a_ms, "kernel_ms": ak_ms / max(ak_n, 1), "flops": flops,
+                              "achieved_TFLOPs": flops / (ak_ms / max(ak_n, 1) * 1e-3) / 1e12,
+                              "peak": FP64_PEAK_TFLOPS,
+                              "frac": flops / (ak_ms / max(ak_n, 1) * 1e-3) / 1e12 / FP64_PEAK_TFLOPS,
+                              "flops_def": "kron_apply count: d^2 + 2d(d-1) Kronecker terms x d contractions x "
+                                           "2 (p+1)^(d+1) flop per cell"},
+        "factor_ms": factor_ms,
+        "e2e": {"value": prob.nfree / (e2e_ms * 1e-3) / 1e9, "unit": "GDOF/s", "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": 8 * prob.ndof, "d2h_bytes_per_step": 8 * prob.ndof},
+        "gpu_launches": gpu_launches, "clocks": clk.summary(), "setup_s": setup_s, "peak_source": peak_src,
+        "pcg": {"iterations": rep["iterations"], "converged": rep["converged"], "kappa": rep["kappa"],
+                "solve_s": rep["wall_time"], "calibrate_s": cal_s, "omega": cal["omega"]},
+    }
+    if not args.no_cpu:
+        from oracle import oracle as O
+
+        # bounded CPU sample: the oracle's elasticity path (global SDC assembly, vector patch
+        # factors) on the 3D problem with 3^3 cells at the same p, timed smooth
+        try:
+            threads = os.cpu_count() or 1
+            ref = O.ElasticProblem(dim, 3, p, 1.0, lam, threads=threads)
+            ref.build(calibrate=False)
+            rr = ref.rhs()
+            ts = []
+            for _ in range(3):
+                t = time.perf_counter()
+                ref.op("smooth", rr)
+                ts.append(time.perf_counter() - t)
+            result["cpu_baseline"] = {"value": ref.nfree / statistics.median(ts) / 1e9, "unit": "GDOF/s",
+                                      "cores": threads, "kind": "port",
+                                      "sample": f"oracle elasticity smooth on dim {dim}, 3^{dim} cells, Q{p} "
+                                                f"(parallel_for over patches, {threads} threads), median of 3"}
+        except Exception as e:
+            result["cpu_baseline"] = {"value": None, "sample": f"failed: {e}"}
+    print(json.dumps(result), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -414,10 +538,13 @@ def main():
     ap.add_argument("--cpu-sample-patches", type=int, default=16)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-pcg", action="store_true")
+    ap.add_argument("--elastic", default=None, help="DIM,N,P,LAMBDA: linear-elasticity workload (SURVEY.md 8(f)3)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         return run_reference(args)
+    if args.elastic:
+        return run_elastic(args)
     return run_ours(args)
 
 

@@ -596,6 +596,241 @@ __global__ void __launch_bounds__(kLines16, 2) k_cells_stiffness16(const double*
   for (int l = r; l < kNpc16; l += kLines16) e[l] = b0[P(l)];
 }
 
+// ---- vector elasticity, n1 = 16, dim = 3 (kernels/elastic.cu has the generic path) ----
+// elasticity_primal_operator's Kronecker blocks (src/elasticity.cpp:83-119) on
+// the FP64 tensor pipe with the line-pass scheme above.  Output component i
+// accumulates in registers: every third pass leaves its result in the same
+// fragment positions (element r + 256 k of the original lattice order), so
+// y_i never touches shared memory and is stored once.  Per (i, j) block the
+// input tile x_j is gathered into b0 and run through three passes over two
+// buffers: the diagonal block as k_cells_stiffness16 with mu'_a = c_ia mu_a;
+// a cross block's two terms (C on i, C^T on j | C^T on i, C on j; B on the
+// third axis k) share the B pass when it comes first (k = 0) or combine before
+// the last pass when it comes last (k = 2).
+__device__ __forceinline__ void gather16(double* __restrict__ b, const double* __restrict__ x,
+                                         const int32_t* __restrict__ cd, const uint8_t* __restrict__ cons,
+                                         int64_t off) {
+  const Pos16 P;
+  const int r = threadIdx.x;
+#pragma unroll 1
+  for (int h = 0; h < 2; ++h) {
+    int64_t gi[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) gi[u] = cd[r + kLines16 * (8 * h + u)] + off;
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const double xv = x[gi[u]];
+      v[u] = cons[gi[u]] ? 0.0 : xv;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) b[P(r + kLines16 * (8 * h + u))] = v[u];
+  }
+}
+
+// OUT = a * M . T (one product per output tile)
+__device__ __forceinline__ void mm16(double& d0, double& d1, const MFrag16& f, double a, const double (&t)[4][4],
+                                     int mt, int nt) {
+#pragma unroll
+  for (int kt = 0; kt < 4; ++kt) dmma884(d0, d1, a * f.a[mt][kt], t[kt][nt]);
+}
+
+// Cross block (i, j) with B on axis K, accumulated into acc: three passes
+// (axis 0, 1, 2) over b0 / b1; Ms holds the rows of A, B, C, C^T.
+template <int K>
+__device__ __forceinline__ void elastic_cross16(const double* __restrict__ Ms, double* __restrict__ b0,
+                                                double* __restrict__ b1, int i, int j, double al, double be,
+                                                double (&acc)[2][4][2]) {
+  // factor of term 1 (C on i, C^T on j) / term 2 (C^T on i, C on j) on axis a; B = 1, C = 2, C^T = 3
+  auto f1 = [&](int a) { return a == i ? 2 : (a == j ? 3 : 1); };
+  auto f2 = [&](int a) { return a == i ? 3 : (a == j ? 2 : 1); };
+  {  // pass 1 (axis 0): K = 0 -> B x once, else (F1_0 x, F2_0 x)
+    double t[4][4];
+    xfrag16(b0, t);
+    __syncthreads();
+    MFrag16 g;
+    mfrag16(g, Ms + 256 * f1(0));
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        double p0 = 0.0, p1 = 0.0;
+        mm16(p0, p1, g, 1.0, t, mt, nt);
+        store16(b0, mt, nt, p0, p1);
+      }
+    if (K != 0) {
+      mfrag16(g, Ms + 256 * f2(0));
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) {
+          double q0 = 0.0, q1 = 0.0;
+          mm16(q0, q1, g, 1.0, t, mt, nt);
+          store16(b1, mt, nt, q0, q1);
+        }
+    }
+    __syncthreads();
+  }
+  {  // pass 2 (axis 1)
+    double t0[4][4], t1[4][4];
+    xfrag16(b0, t0);
+    if (K != 0) xfrag16(b1, t1);
+    __syncthreads();
+    MFrag16 g1, g2;
+    mfrag16(g1, Ms + 256 * f1(1));
+    mfrag16(g2, Ms + 256 * f2(1));
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        double p0 = 0.0, p1 = 0.0, q0 = 0.0, q1 = 0.0;
+        if (K == 0) {  // shared B x: two outputs
+          mm16(p0, p1, g1, al, t0, mt, nt);
+          mm16(q0, q1, g2, be, t0, mt, nt);
+          store16(b0, mt, nt, p0, p1);
+          store16(b1, mt, nt, q0, q1);
+        } else if (K == 2) {  // both end with B: combine now
+          mm16(p0, p1, g1, al, t0, mt, nt);
+          mm16(p0, p1, g2, be, t1, mt, nt);
+          store16(b0, mt, nt, p0, p1);
+        } else {
+          mm16(p0, p1, g1, al, t0, mt, nt);
+          mm16(q0, q1, g2, be, t1, mt, nt);
+          store16(b0, mt, nt, p0, p1);
+          store16(b1, mt, nt, q0, q1);
+        }
+      }
+    __syncthreads();
+  }
+  {  // pass 3 (axis 2) into the accumulator
+    double t0[4][4];
+    xfrag16(b0, t0);
+    MFrag16 g;
+    mfrag16(g, Ms + 256 * f1(2));
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) mm16(acc[mt][nt][0], acc[mt][nt][1], g, 1.0, t0, mt, nt);
+    if (K != 2) {
+      xfrag16(b1, t0);
+      mfrag16(g, Ms + 256 * f2(2));
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) mm16(acc[mt][nt][0], acc[mt][nt][1], g, 1.0, t0, mt, nt);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kLines16, 1) k_cells_elastic16(const double* __restrict__ x, double* __restrict__ E,
+                                                               int ncells, int64_t nsc,
+                                                               const int32_t* __restrict__ cdofs,
+                                                               const uint8_t* __restrict__ cons,
+                                                               const double* __restrict__ mu, double lmu, double llam,
+                                                               const double* __restrict__ Ahat,
+                                                               const double* __restrict__ Bhat,
+                                                               const double* __restrict__ Cm) {
+  extern __shared__ __align__(16) double sm[];
+  double* Ms = sm;                    // rows of A, B, C, C^T
+  double* b0 = Ms + 4 * kL16 * kL16;  // 4096, Pos16 layout
+  double* b1 = b0 + kNpc16;
+  const int c = blockIdx.x, lane = threadIdx.x & 31;
+  load_rows16(Ms, Ahat);
+  load_rows16(Ms + 256, Bhat);
+  load_rows16(Ms + 512, Cm);
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) Ms[768 + i] = Cm[i];  // rows of C^T = columns of C
+  const int32_t* cd = cdofs + size_t(c) * kNpc16;
+  double m[3];
+  for (int a = 0; a < 3; ++a) m[a] = mu[size_t(c) * 3 + a];
+  pdl_wait();
+#pragma unroll 1
+  for (int i = 0; i < 3; ++i) {
+    double acc[2][4][2];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+#pragma unroll 1
+    for (int j = 0; j < 3; ++j) {
+      __syncthreads();  // previous block's last fragment reads of b0 / b1 are done
+      gather16(b0, x, cd, cons, j * nsc);
+      __syncthreads();
+      if (j == i) {  // diagonal block: sum_a mu'_a A_a (x) B (x) B, mu'_a = (mu + (mu + lambda) [a == i]) mu_a
+        const double m0 = (llam * (i == 0) + lmu * (1 + (i == 0))) * m[0];
+        const double m1 = (llam * (i == 1) + lmu * (1 + (i == 1))) * m[1];
+        const double m2 = (llam * (i == 2) + lmu * (1 + (i == 2))) * m[2];
+        MFrag16 fa, fb;
+        mfrag16(fa, Ms);
+        mfrag16(fb, Ms + 256);
+        {
+          double t[4][4];
+          xfrag16(b0, t);
+          __syncthreads();
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt) {
+              double p0 = 0.0, p1 = 0.0, q0 = 0.0, q1 = 0.0;
+              mm16(p0, p1, fb, 1.0, t, mt, nt);
+              mm16(q0, q1, fa, 1.0, t, mt, nt);
+              store16(b0, mt, nt, p0, p1);
+              store16(b1, mt, nt, q0, q1);
+            }
+          __syncthreads();
+        }
+        {
+          double t0[4][4], t1[4][4];
+          xfrag16(b0, t0);
+          xfrag16(b1, t1);
+          __syncthreads();
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt) {
+              double p0 = 0.0, p1 = 0.0, q0 = 0.0, q1 = 0.0;
+              mm16(p0, p1, fb, m0, t1, mt, nt);
+              mm16(p0, p1, fa, m1, t0, mt, nt);
+              mm16(q0, q1, fb, 1.0, t0, mt, nt);
+              store16(b0, mt, nt, p0, p1);
+              store16(b1, mt, nt, q0, q1);
+            }
+          __syncthreads();
+        }
+        {
+          double t0[4][4], t1[4][4];
+          xfrag16(b0, t0);
+          xfrag16(b1, t1);
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt) {
+              mm16(acc[mt][nt][0], acc[mt][nt][1], fb, 1.0, t0, mt, nt);
+              mm16(acc[mt][nt][0], acc[mt][nt][1], fa, m2, t1, mt, nt);
+            }
+        }
+        continue;
+      }
+      // cross block (i, j): alpha (C on i, C^T on j) + beta (C^T on i, C on j), B on the third axis
+      const double s = sqrt(m[i] * m[j]);
+      switch (3 - i - j) {
+        case 0: elastic_cross16<0>(Ms, b0, b1, i, j, lmu * s, llam * s, acc); break;
+        case 1: elastic_cross16<1>(Ms, b0, b1, i, j, lmu * s, llam * s, acc); break;
+        default: elastic_cross16<2>(Ms, b0, b1, i, j, lmu * s, llam * s, acc); break;
+      }
+    }
+    // y_i: element r + 256 k of the lattice order, straight from the accumulator
+    double* e = E + (size_t(i) * ncells + c) * kNpc16;
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        const int kk = 8 * mt + (lane >> 2), r = 32 * (threadIdx.x >> 5) + 8 * nt + 2 * (lane & 3);
+        *reinterpret_cast<double2*>(e + r + kLines16 * kk) = make_double2(acc[mt][nt][0], acc[mt][nt][1]);
+      }
+  }
+  pdl_trigger();
+}
+
 // mode 0: apply_St (sum, project); 1: apply_S (sum * inv_mult, project);
 // 2: operator (sum; constrained rows y_i = x_i); 3: x + sum (project).
 __global__ void k_gather(int64_t ndof, int mode, const double* __restrict__ E, const int32_t* __restrict__ ptr,
@@ -695,6 +930,18 @@ void launch_gather(Context& c, int mode, const double* E, const double* x, doubl
   launch_pdl(c.pdl && !c.timing, k_gather, dim3(unsigned(blocks)), dim3(threads), 0, c.stream, c.ndof, mode, E,
              modes ? c.gm_ptr.p : c.g_ptr.p, modes ? c.gm_idx.p : c.g_idx.p, c.inv_mult.p, c.constrained.p, x, out);
   FDM_LAUNCH_CHECK(c);
+}
+
+bool launch_cells_elastic16(Context& c, const double* x) {
+  if (c.n1 != kL16 || c.dim != 3) return false;
+  const size_t smem = sizeof(double) * (4 * kL16 * kL16 + 2 * size_t(kNpc16));
+  set_smem(k_cells_elastic16, smem);
+  KernelTimer timer(c, 3);
+  launch_pdl(c.pdl && !c.timing, k_cells_elastic16, dim3(c.ncells), dim3(kLines16), smem, c.stream, x, c.E.p,
+             c.ncells, c.nsc, c.cell_dofs.p, c.constrained.p, c.mu.p, c.lame_mu, c.lame_lambda, c.Ahat.p, c.Bhat.p,
+             c.Cm.p);
+  FDM_LAUNCH_CHECK(c);
+  return true;
 }
 
 void launch_cells_stiffness_kron(Context& c, const double* x) {

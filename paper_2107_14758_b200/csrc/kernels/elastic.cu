@@ -136,7 +136,10 @@ size_t elastic_smem_bytes(const Context& c) {
   return sizeof(double) * (4 * size_t(c.n1) * c.n1 + size_t(c.dim + 3) * c.npc);
 }
 
+bool launch_cells_elastic16(Context& c, const double* x);  // cells.cu: n1 = 16, dim = 3 on the DMMA pipe
+
 void launch_cells_elastic(Context& c, const double* x) {
+  if (!c.force_staged && launch_cells_elastic16(c, x)) return;
   const size_t smem = elastic_smem_bytes(c);
   auto go = [&](auto kernel) {
     set_smem(kernel, smem);
