@@ -100,8 +100,7 @@ void op_smooth(Context& c, const double* r, double* z) {
 void op_A(Context& c, const double* x, double* y) {  // src/assembly.cpp:56-88
   if (c.ncomp > 1) {  // elasticity_primal_operator (src/elasticity.cpp:69-120): all blocks in one cell pass
     launch_cells_elastic(c, x);
-    for (int ci = 0; ci < c.ncomp; ++ci)
-      launch_gather(c.sub(ci), 2, c.E.p + size_t(ci) * c.ncells * c.npc, x + ci * c.nsc, y + ci * c.nsc);
+    launch_gather_vec(c, 2, c.E.p, x, y);
     return;
   }
   launch_cells_stiffness(c, x);

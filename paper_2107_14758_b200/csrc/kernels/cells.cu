@@ -628,6 +628,24 @@ __device__ __forceinline__ void gather16(double* __restrict__ b, const double* _
   }
 }
 
+// Rows of a 16 x 16 matrix at a padded stride of 20 doubles: the A-fragment
+// loads (8 rows x 4 columns per warp) of the per-pass fragment reloads are
+// then conflict-free (row starts 20 words apart cover all 16 bank pairs).
+constexpr int kRow20 = 20, kMat20 = 16 * kRow20;
+__device__ __forceinline__ void load_rows20(double* __restrict__ Mt, const double* __restrict__ M, bool transpose) {
+  for (int i = threadIdx.x; i < kL16 * kL16; i += blockDim.x) {
+    const int r = i & 15, c = i >> 4;  // M column-major: M(r, c) = M[r + 16 c]
+    Mt[(transpose ? c : r) * kRow20 + (transpose ? r : c)] = M[i];
+  }
+}
+__device__ __forceinline__ void mfrag20(MFrag16& f, const double* __restrict__ Mt) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int kt = 0; kt < 4; ++kt) f.a[mt][kt] = Mt[kRow20 * (8 * mt + (lane >> 2)) + 4 * kt + (lane & 3)];
+}
+
 // OUT = a * M . T (one product per output tile)
 __device__ __forceinline__ void mm16(double& d0, double& d1, const MFrag16& f, double a, const double (&t)[4][4],
                                      int mt, int nt) {
@@ -649,7 +667,7 @@ __device__ __forceinline__ void elastic_cross16(const double* __restrict__ Ms, d
     xfrag16(b0, t);
     __syncthreads();
     MFrag16 g;
-    mfrag16(g, Ms + 256 * f1(0));
+    mfrag20(g, Ms + kMat20 * f1(0));
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
@@ -659,7 +677,7 @@ __device__ __forceinline__ void elastic_cross16(const double* __restrict__ Ms, d
         store16(b0, mt, nt, p0, p1);
       }
     if (K != 0) {
-      mfrag16(g, Ms + 256 * f2(0));
+      mfrag20(g, Ms + kMat20 * f2(0));
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
@@ -677,8 +695,8 @@ __device__ __forceinline__ void elastic_cross16(const double* __restrict__ Ms, d
     if (K != 0) xfrag16(b1, t1);
     __syncthreads();
     MFrag16 g1, g2;
-    mfrag16(g1, Ms + 256 * f1(1));
-    mfrag16(g2, Ms + 256 * f2(1));
+    mfrag20(g1, Ms + kMat20 * f1(1));
+    mfrag20(g2, Ms + kMat20 * f2(1));
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
@@ -706,14 +724,14 @@ __device__ __forceinline__ void elastic_cross16(const double* __restrict__ Ms, d
     double t0[4][4];
     xfrag16(b0, t0);
     MFrag16 g;
-    mfrag16(g, Ms + 256 * f1(2));
+    mfrag20(g, Ms + kMat20 * f1(2));
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
       for (int nt = 0; nt < 4; ++nt) mm16(acc[mt][nt][0], acc[mt][nt][1], g, 1.0, t0, mt, nt);
     if (K != 2) {
       xfrag16(b1, t0);
-      mfrag16(g, Ms + 256 * f2(2));
+      mfrag20(g, Ms + kMat20 * f2(2));
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
@@ -731,14 +749,14 @@ __global__ void __launch_bounds__(kLines16, 1) k_cells_elastic16(const double* _
                                                                const double* __restrict__ Bhat,
                                                                const double* __restrict__ Cm) {
   extern __shared__ __align__(16) double sm[];
-  double* Ms = sm;                    // rows of A, B, C, C^T
-  double* b0 = Ms + 4 * kL16 * kL16;  // 4096, Pos16 layout
+  double* Ms = sm;               // rows of A, B, C, C^T (stride kRow20)
+  double* b0 = Ms + 4 * kMat20;  // 4096, Pos16 layout
   double* b1 = b0 + kNpc16;
   const int c = blockIdx.x, lane = threadIdx.x & 31;
-  load_rows16(Ms, Ahat);
-  load_rows16(Ms + 256, Bhat);
-  load_rows16(Ms + 512, Cm);
-  for (int i = threadIdx.x; i < 256; i += blockDim.x) Ms[768 + i] = Cm[i];  // rows of C^T = columns of C
+  load_rows20(Ms, Ahat, false);
+  load_rows20(Ms + kMat20, Bhat, false);
+  load_rows20(Ms + 2 * kMat20, Cm, false);
+  load_rows20(Ms + 3 * kMat20, Cm, true);  // C^T
   const int32_t* cd = cdofs + size_t(c) * kNpc16;
   double m[3];
   for (int a = 0; a < 3; ++a) m[a] = mu[size_t(c) * 3 + a];
@@ -760,8 +778,8 @@ __global__ void __launch_bounds__(kLines16, 1) k_cells_elastic16(const double* _
         const double m1 = (llam * (i == 1) + lmu * (1 + (i == 1))) * m[1];
         const double m2 = (llam * (i == 2) + lmu * (1 + (i == 2))) * m[2];
         MFrag16 fa, fb;
-        mfrag16(fa, Ms);
-        mfrag16(fb, Ms + 256);
+        mfrag20(fa, Ms);
+        mfrag20(fb, Ms + kMat20);
         {
           double t[4][4];
           xfrag16(b0, t);
@@ -833,9 +851,14 @@ __global__ void __launch_bounds__(kLines16, 1) k_cells_elastic16(const double* _
 
 // mode 0: apply_St (sum, project); 1: apply_S (sum * inv_mult, project);
 // 2: operator (sum; constrained rows y_i = x_i); 3: x + sum (project).
+// VEC: vector (elasticity) handles, all components in one grid -- DOF g is
+// scalar DOF g mod nsc of component g / nsc, whose E block starts at
+// (g / nsc) * eoff; the gather maps are the (shared) scalar ones.
+template <bool VEC>
 __global__ void k_gather(int64_t ndof, int mode, const double* __restrict__ E, const int32_t* __restrict__ ptr,
                          const int32_t* __restrict__ idx, const double* __restrict__ inv_mult,
-                         const uint8_t* __restrict__ cons, const double* __restrict__ x, double* __restrict__ out) {
+                         const uint8_t* __restrict__ cons, const double* __restrict__ x, double* __restrict__ out,
+                         int64_t nsc, int64_t eoff) {
   const int64_t g = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   pdl_trigger();
   // The maps are static: load them (and the first two entry indices -- one
@@ -844,8 +867,14 @@ __global__ void k_gather(int64_t ndof, int mode, const double* __restrict__ E, c
   bool c = false;
   double w = 1.0;
   if (g < ndof) {
-    q0 = ptr[g];
-    q1 = ptr[g + 1];
+    int64_t gl = g;
+    if (VEC) {
+      const int64_t comp = g / nsc;
+      gl = g - comp * nsc;
+      E += comp * eoff;
+    }
+    q0 = ptr[gl];
+    q1 = ptr[gl + 1];
     c = cons[g];
     if (mode == 1) w = inv_mult[g];
     if (q1 > q0) i0 = idx[q0];
@@ -927,14 +956,24 @@ void launch_gather(Context& c, int mode, const double* E, const double* x, doubl
   const bool modes = (mode == 0 || mode == 3) && !c.modes_alias;
   const int threads = 256;
   const int64_t blocks = (c.ndof + threads - 1) / threads;
-  launch_pdl(c.pdl && !c.timing, k_gather, dim3(unsigned(blocks)), dim3(threads), 0, c.stream, c.ndof, mode, E,
-             modes ? c.gm_ptr.p : c.g_ptr.p, modes ? c.gm_idx.p : c.g_idx.p, c.inv_mult.p, c.constrained.p, x, out);
+  launch_pdl(c.pdl && !c.timing, k_gather<false>, dim3(unsigned(blocks)), dim3(threads), 0, c.stream, c.ndof, mode, E,
+             modes ? c.gm_ptr.p : c.g_ptr.p, modes ? c.gm_idx.p : c.g_idx.p, c.inv_mult.p, c.constrained.p, x, out,
+             c.ndof, int64_t(0));
+  FDM_LAUNCH_CHECK(c);
+}
+
+void launch_gather_vec(Context& c, int mode, const double* E, const double* x, double* out) {
+  const Context& s = *c.comp[0];  // the components share the scalar gather maps
+  const int threads = 256;
+  const int64_t blocks = (c.ndof + threads - 1) / threads;
+  launch_pdl(c.pdl && !c.timing, k_gather<true>, dim3(unsigned(blocks)), dim3(threads), 0, c.stream, c.ndof, mode, E,
+             s.g_ptr.p, s.g_idx.p, c.inv_mult.p, c.constrained.p, x, out, c.nsc, int64_t(c.ncells) * c.npc);
   FDM_LAUNCH_CHECK(c);
 }
 
 bool launch_cells_elastic16(Context& c, const double* x) {
   if (c.n1 != kL16 || c.dim != 3) return false;
-  const size_t smem = sizeof(double) * (4 * kL16 * kL16 + 2 * size_t(kNpc16));
+  const size_t smem = sizeof(double) * (4 * kMat20 + 2 * size_t(kNpc16));
   set_smem(k_cells_elastic16, smem);
   KernelTimer timer(c, 3);
   launch_pdl(c.pdl && !c.timing, k_cells_elastic16, dim3(c.ncells), dim3(kLines16), smem, c.stream, x, c.E.p,
