@@ -12,6 +12,8 @@
 #include <random>
 #include <string>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "context.hpp"
 
 namespace fdmgpu {
@@ -337,6 +339,13 @@ std::vector<double> random_free(Context& c, uint64_t seed) {
     if (c.h_constrained[i]) b[i] = 0.0;
   return b;
 }
+
+// NVTX range around one public call (visible to ncu --nvtx / nsys when a tool
+// is attached; a no-op otherwise).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 template <class Fn>
 fdmgpu_status guarded(fdmgpu_handle h, Fn&& fn) {
@@ -666,6 +675,7 @@ fdmgpu_status fdmgpu_set_cell_coeffs(fdmgpu_handle h, const uint8_t* kind, const
 fdmgpu_status fdmgpu_set_patches(fdmgpu_handle h, int32_t npatch, const int32_t* vertex, const int64_t* ptr,
                                  const int32_t* dofs, const int32_t* perm, const int32_t* star_cells) {
   return fdmgpu::guarded(h, [&](Context& c) {
+    fdmgpu::NvtxRange nvtx_("fdmgpu_set_patches");
     c.check_ready(false, false, false);
     if (npatch < 1 || !vertex || !ptr || !dofs || !perm || !star_cells)
       throw Error(FDMGPU_INVALID_ARGUMENT, "set_patches: bad arguments");
@@ -857,6 +867,7 @@ fdmgpu_status fdmgpu_set_coarse_cells(fdmgpu_handle h, const int32_t* coarse_cel
 
 fdmgpu_status fdmgpu_factor(fdmgpu_handle h) {
   return fdmgpu::guarded(h, [&](Context& c) {
+    fdmgpu::NvtxRange nvtx_("fdmgpu_factor");
     c.check_ready(true, false, false);
     if (c.ncomp > 1) {
       c.factored = false;
@@ -961,6 +972,7 @@ fdmgpu_status fdmgpu_get_patch_elimination_dofs(fdmgpu_handle h, int32_t* out) {
 
 fdmgpu_status fdmgpu_apply(fdmgpu_handle h, int32_t op, double omega, const double* in, double* out, int32_t host) {
   return fdmgpu::guarded(h, [&](Context& c) {
+    fdmgpu::NvtxRange nvtx_("fdmgpu_apply");
     if (!in || !out) throw Error(FDMGPU_INVALID_ARGUMENT, "apply: null vector");
     const bool needs_factor = op == FDMGPU_OP_PATCH || op == FDMGPU_OP_SMOOTH || op == FDMGPU_OP_VCYCLE;
     c.check_ready(needs_factor, needs_factor, op == FDMGPU_OP_VCYCLE);
@@ -1009,6 +1021,7 @@ fdmgpu_status fdmgpu_vcycle(fdmgpu_handle h, double omega, const double* r, doub
 fdmgpu_status fdmgpu_pcg(fdmgpu_handle h, const double* b, double* x, double rtol, int32_t maxit, int32_t precond,
                          fdmgpu_krylov_report* report, double* residuals) {
   return fdmgpu::guarded(h, [&](Context& c) {
+    fdmgpu::NvtxRange nvtx_("fdmgpu_pcg");
     if (!b || !x || !report || maxit < 0 || b == x) throw Error(FDMGPU_INVALID_ARGUMENT, "pcg: bad arguments");
     c.check_ready(precond > 0, precond > 0, precond == 2);
     std::vector<double> res;
@@ -1020,6 +1033,7 @@ fdmgpu_status fdmgpu_pcg(fdmgpu_handle h, const double* b, double* x, double rto
 fdmgpu_status fdmgpu_calibrate_damping(fdmgpu_handle h, int32_t lanczos_steps, uint32_t seed, int32_t formula,
                                        double* omega, double* lambda_min, double* lambda_max) {
   return fdmgpu::guarded(h, [&](Context& c) {
+    fdmgpu::NvtxRange nvtx_("fdmgpu_calibrate_damping");
     c.check_ready(true, true, true);
     double* b = c.w[11].p;
     double* x = c.w[10].p;
