@@ -186,6 +186,18 @@ fdmgpu_status fdmgpu_get_patch_elimination_dofs(fdmgpu_handle h, int32_t* out);
  * means `in` / `out` are host pointers (copied inside, synchronous). */
 fdmgpu_status fdmgpu_apply(fdmgpu_handle h, int32_t op, double omega, const double* in, double* out,
                            int32_t host);
+/* Asynchronous host-buffer form of fdmgpu_apply for a stream of independent
+ * vectors (many right-hand sides, serving): copies host_in (pinned) in on a
+ * copy stream, runs op on the handle stream, copies the result out to
+ * host_out (pinned) on a second copy stream, and returns at once, so the
+ * copies of one call overlap the compute of its neighbours.  Two staging
+ * slots: a call waits (on the device) for the slot used two calls earlier.
+ * Host buffers must stay untouched until fdmgpu_synchronize returns, which
+ * waits for every call in flight.  Same results as fdmgpu_apply. */
+fdmgpu_status fdmgpu_apply_async(fdmgpu_handle h, int32_t op, double omega, const double* host_in, double* host_out);
+/* Device-side join: the handle stream waits for every fdmgpu_apply_async copy-out in flight
+ * (work enqueued on it afterwards -- e.g. a timing event -- runs after them). */
+fdmgpu_status fdmgpu_async_join(fdmgpu_handle h);
 fdmgpu_status fdmgpu_transform(fdmgpu_handle h, int32_t dir, const double* in, double* out); /* 0 S^T, 1 S */
 fdmgpu_status fdmgpu_patch_solve(fdmgpu_handle h, const double* r_modal, double* z_modal);
 fdmgpu_status fdmgpu_smooth(fdmgpu_handle h, const double* r, double* z);

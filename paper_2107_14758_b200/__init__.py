@@ -98,6 +98,8 @@ def lib():
         L.fdmgpu_get_layout.argtypes = [_vp, C.POINTER(Layout)]
         L.fdmgpu_get_patch_elimination_dofs.argtypes = [_vp, _vp]
         L.fdmgpu_apply.argtypes = [_vp, C.c_int32, C.c_double, _vp, _vp, C.c_int32]
+        L.fdmgpu_apply_async.argtypes = [_vp, C.c_int32, C.c_double, _vp, _vp]
+        L.fdmgpu_async_join.argtypes = [_vp]
         L.fdmgpu_pcg.argtypes = [_vp, _vp, _vp, C.c_double, C.c_int32, C.c_int32, C.POINTER(KrylovReport), _vp]
         L.fdmgpu_calibrate_damping.argtypes = [_vp, C.c_int32, C.c_uint32, C.c_int32, C.POINTER(C.c_double),
                                                C.POINTER(C.c_double), C.POINTER(C.c_double)]
@@ -398,6 +400,19 @@ class Solver:
         if sync:
             self.synchronize()
         return out
+
+    def apply_async(self, op, host_in, host_out, omega=0.0):
+        """fdmgpu_apply_async: host_in / host_out pinned float64 arrays (e.g.
+        torch.empty(n, dtype=torch.float64).pin_memory().numpy()), left untouched
+        until synchronize(); copies overlap the compute of neighbouring calls."""
+        assert host_in.dtype == np.float64 and host_out.dtype == np.float64
+        assert host_in.flags.c_contiguous and host_out.flags.c_contiguous
+        assert host_in.size == self.ndof and host_out.size == self.ndof
+        self._chk(lib().fdmgpu_apply_async(self.h, op, omega, _ptr(host_in), _ptr(host_out)))
+
+    def async_join(self):
+        """fdmgpu_async_join: the library stream waits for all apply_async copy-outs."""
+        self._chk(lib().fdmgpu_async_join(self.h))
 
     def apply_St(self, x, out=None):
         return self.apply(OP_APPLY_ST, x, out)

@@ -509,7 +509,11 @@ fdmgpu_status fdmgpu_set_elasticity(fdmgpu_handle h, double mu, double lambda, c
 }
 
 fdmgpu_status fdmgpu_synchronize(fdmgpu_handle h) {
-  return fdmgpu::guarded(h, [](Context& c) { FDM_CUDA(cudaStreamSynchronize(c.stream)); });
+  return fdmgpu::guarded(h, [](Context& c) {
+    FDM_CUDA(cudaStreamSynchronize(c.stream));
+    if (c.h2d_stream) FDM_CUDA(cudaStreamSynchronize(c.h2d_stream));
+    if (c.d2h_stream) FDM_CUDA(cudaStreamSynchronize(c.d2h_stream));
+  });
 }
 
 fdmgpu_status fdmgpu_set_basis(fdmgpu_handle h, const double* S, const double* lambda, const double* A_t,
@@ -999,6 +1003,57 @@ fdmgpu_status fdmgpu_apply(fdmgpu_handle h, int32_t op, double omega, const doub
       FDM_CUDA(cudaMemcpyAsync(out, dout, bytes, cudaMemcpyDeviceToHost, c.stream));
       FDM_CUDA(cudaStreamSynchronize(c.stream));
     }
+  });
+}
+
+fdmgpu_status fdmgpu_apply_async(fdmgpu_handle h, int32_t op, double omega, const double* host_in, double* host_out) {
+  return fdmgpu::guarded(h, [&](Context& c) {
+    fdmgpu::NvtxRange nvtx_("fdmgpu_apply_async");
+    if (!host_in || !host_out) throw Error(FDMGPU_INVALID_ARGUMENT, "apply_async: null vector");
+    const bool needs_factor = op == FDMGPU_OP_PATCH || op == FDMGPU_OP_SMOOTH || op == FDMGPU_OP_VCYCLE;
+    c.check_ready(needs_factor, needs_factor, op == FDMGPU_OP_VCYCLE);
+    if (op < FDMGPU_OP_APPLY_ST || op > FDMGPU_OP_VCYCLE) throw Error(FDMGPU_INVALID_ARGUMENT, "apply: unknown operator id");
+    if (!c.h2d_stream) {
+      FDM_CUDA(cudaStreamCreateWithFlags(&c.h2d_stream, cudaStreamNonBlocking));
+      FDM_CUDA(cudaStreamCreateWithFlags(&c.d2h_stream, cudaStreamNonBlocking));
+      for (int k = 0; k < 2; ++k) {
+        for (cudaEvent_t* e : {&c.ev_in[k], &c.ev_comp[k], &c.ev_out[k]})
+          FDM_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+        c.stage_in[k].alloc(c.ndof);
+        c.stage_out[k].alloc(c.ndof);
+      }
+    }
+    const int s = c.async_slot;
+    c.async_slot ^= 1;
+    const size_t bytes = c.ndof * sizeof(double);
+    // copy-in once this slot's previous input has been consumed
+    FDM_CUDA(cudaStreamWaitEvent(c.h2d_stream, c.ev_comp[s], 0));
+    FDM_CUDA(cudaMemcpyAsync(c.stage_in[s].p, host_in, bytes, cudaMemcpyHostToDevice, c.h2d_stream));
+    FDM_CUDA(cudaEventRecord(c.ev_in[s], c.h2d_stream));
+    // compute once the input is in and this slot's previous output has been copied out
+    FDM_CUDA(cudaStreamWaitEvent(c.stream, c.ev_in[s], 0));
+    FDM_CUDA(cudaStreamWaitEvent(c.stream, c.ev_out[s], 0));
+    const double* din = c.stage_in[s].p;
+    double* dout = c.stage_out[s].p;
+    switch (op) {
+      case FDMGPU_OP_APPLY_ST: fdmgpu::op_transform(c, 0, din, dout); break;
+      case FDMGPU_OP_APPLY_S: fdmgpu::op_transform(c, 1, din, dout); break;
+      case FDMGPU_OP_PATCH: fdmgpu::op_patch(c, din, dout); break;
+      case FDMGPU_OP_SMOOTH: fdmgpu::op_smooth(c, din, dout); break;
+      case FDMGPU_OP_A: fdmgpu::op_A(c, din, dout); break;
+      default: fdmgpu::op_vcycle(c, omega, din, dout); break;
+    }
+    FDM_CUDA(cudaEventRecord(c.ev_comp[s], c.stream));
+    FDM_CUDA(cudaStreamWaitEvent(c.d2h_stream, c.ev_comp[s], 0));
+    FDM_CUDA(cudaMemcpyAsync(host_out, dout, bytes, cudaMemcpyDeviceToHost, c.d2h_stream));
+    FDM_CUDA(cudaEventRecord(c.ev_out[s], c.d2h_stream));
+  });
+}
+
+fdmgpu_status fdmgpu_async_join(fdmgpu_handle h) {
+  return fdmgpu::guarded(h, [&](Context& c) {
+    for (int k = 0; k < 2; ++k)
+      if (c.ev_out[k]) FDM_CUDA(cudaStreamWaitEvent(c.stream, c.ev_out[k], 0));
   });
 }
 

@@ -178,6 +178,13 @@ struct Context {
   int pcg_precond = -1, pcg_cap = 0;
   double pcg_omega = 0.0;
 
+  // asynchronous host-buffer applies (fdmgpu_apply_async): copy-in / copy-out
+  // streams, two staging slots, per-slot events
+  cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
+  DevArray<double> stage_in[2], stage_out[2];
+  cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_comp[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
+  int async_slot = 0;
+
   // optional per-kernel CUDA-event timing (fdmgpu_kernel_timing)
   bool timing = false;
   bool capturing = false;  // inside a CUDA-graph capture: launches are recorded, not counted
@@ -200,6 +207,11 @@ struct Context {
   ~Context() {
     for (Context* s : comp) destroy_sub(s);
     if (pcg_exec) cudaGraphExecDestroy(pcg_exec);
+    for (int k = 0; k < 2; ++k)
+      for (cudaEvent_t e : {ev_in[k], ev_comp[k], ev_out[k]})
+        if (e) cudaEventDestroy(e);
+    if (h2d_stream) cudaStreamDestroy(h2d_stream);
+    if (d2h_stream) cudaStreamDestroy(d2h_stream);
     if (cap_stream) cudaStreamDestroy(cap_stream);
     for (auto& v : tev)
       for (auto& [a, b] : v) {

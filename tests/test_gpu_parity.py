@@ -375,3 +375,21 @@ def test_patch_schur_matches_oracle(pkg, oracle, torch, tmp_path, cfg, skip):
     R = scipy.io.mmread(path)
     R = R.toarray() if hasattr(R, "toarray") else np.asarray(R)
     assert np.array_equal(R, sol.patch_schur(0))
+
+
+@pytest.mark.parametrize("cfg", [(2, 3, 5), (3, 2, 15)])
+def test_apply_async_matches_sync(pkg, torch, cfg):
+    """fdmgpu_apply_async (copy streams, two staging slots) returns what the
+    synchronous host-buffer call returns, bitwise, for a stream of distinct inputs."""
+    prob = pkg.Problem(*cfg)
+    sol = pkg.Solver(prob)
+    sol.factor()
+    rng = np.random.default_rng(7)
+    ins = [torch.from_numpy(rng.standard_normal(prob.ndof)).pin_memory().numpy() for _ in range(5)]
+    outs = [torch.empty(prob.ndof, dtype=torch.float64).pin_memory().numpy() for _ in range(5)]
+    for op in (pkg.OP_SMOOTH, pkg.OP_A):
+        for x, y in zip(ins, outs):
+            sol.apply_async(op, x, y)
+        sol.synchronize()
+        for x, y in zip(ins, outs):
+            assert np.array_equal(y, sol.apply(op, x)), op
