@@ -149,3 +149,43 @@ def test_elastic_table2_counts_on_gpu(pkg):
     for got, exp in zip(its, TABLE2_EXPECTED):
         assert int(0.8 * exp) <= got <= int(1.2 * exp) + 1, its
     assert its == sorted(its) and its[-1] >= 10 * its[0]
+
+
+@pytest.mark.gpu
+def test_elastic_deterministic_and_async(pkg):
+    """Two applies give bitwise-identical results (owner gathers, no atomics), and
+    the asynchronous host-buffer path returns the synchronous results."""
+    import torch
+
+    prob = pkg.Problem.elasticity(3, 2, 7, 1.0, 3.0)
+    sol = pkg.Solver(prob)
+    sol.factor()
+    r = prob.rhs() + np.random.default_rng(1).standard_normal(prob.ndof) * (prob.maps()["constrained"] == 0)
+    for fn in (sol.smooth, sol.apply_A):
+        assert np.array_equal(fn(r), fn(r))
+    h_in = torch.from_numpy(r).pin_memory().numpy()
+    outs = [torch.empty(prob.ndof, dtype=torch.float64).pin_memory().numpy() for _ in range(3)]
+    for o in outs:
+        sol.apply_async(pkg.OP_SMOOTH, h_in, o)
+    sol.synchronize()
+    ref = sol.smooth(r)
+    for o in outs:
+        assert np.array_equal(o, ref)
+
+
+@pytest.mark.gpu
+def test_elastic_handle_errors(pkg):
+    """Vector handles reject what the device path does not cover, with status codes."""
+    prob = pkg.Problem.elasticity(2, 3, 3, 1.0, 1.0)
+    sol = pkg.Solver(prob)
+    g = prob.geometry()
+    with pytest.raises(pkg.FdmGpuError) as e:  # kappa is not part of the elasticity operator
+        sol.set_cell_coeffs(g["mu"], kappa=np.full(prob.ncells, 2.0))
+    assert e.value.status == 1
+    with pytest.raises(pkg.FdmGpuError) as e:  # non-Cartesian cells need the dense quadrature form
+        sol.set_cell_coeffs(g["mu"], kind=np.full(prob.ncells, 2, np.uint8))
+    assert e.value.status == 6
+    with pytest.raises(pkg.FdmGpuError) as e:  # scalar-only debug view
+        sol.factor()
+        sol.patch_schur(0)
+    assert e.value.status == 6
