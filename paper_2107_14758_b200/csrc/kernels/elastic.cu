@@ -27,6 +27,28 @@ template <int N1C>
 __device__ __forceinline__ void contract_axis(int n1_rt, int npc, int axis, const double* __restrict__ M,
                                               const double* __restrict__ in, double* __restrict__ out, double coeff,
                                               bool accumulate) {
+  if constexpr (N1C > 0) {
+    // Thread t owns output index k = t mod n1 on the contracted axis for the whole
+    // pass (blockDim is a multiple of n1), so row k of M sits in registers and
+    // every output costs n1 loads of `in` (lanes sharing a line broadcast).
+    static_assert(256 % N1C == 0, "block size must be a multiple of n1");
+    const int stride = axis == 0 ? 1 : (axis == 1 ? N1C : N1C * N1C);
+    const int k = threadIdx.x % N1C;
+    double mk[N1C];
+#pragma unroll
+    for (int l = 0; l < N1C; ++l) mk[l] = M[k + N1C * l];
+    for (int mm = threadIdx.x / N1C; mm < npc / N1C; mm += blockDim.x / N1C) {
+      const int lo = mm % stride, hi = mm / stride;
+      const int base = lo + hi * stride * N1C;
+      double s = 0.0;
+#pragma unroll
+      for (int l = 0; l < N1C; ++l) s = fma(mk[l], in[base + l * stride], s);
+      const int o = base + k * stride;
+      out[o] = accumulate ? fma(coeff, s, out[o]) : coeff * s;
+    }
+    __syncthreads();
+    return;
+  }
   const int n1 = N1C > 0 ? N1C : n1_rt;
   const int stride = axis == 0 ? 1 : (axis == 1 ? n1 : n1 * n1);
   for (int o = threadIdx.x; o < npc; o += blockDim.x) {
@@ -44,9 +66,9 @@ __device__ __forceinline__ void contract_axis(int n1_rt, int npc, int axis, cons
 }
 
 // One Kronecker term: Y (+)= coeff * (F_{d-1} (x) ... (x) F_0) X.  Passes run
-// axis 0 first (the order of kron_apply, src/kron.cpp:40-55); every output
-// entry is owned by the same thread in every pass, so the final accumulate
-// needs no extra barrier.
+// axis 0 first (the order of kron_apply, src/kron.cpp:40-55).  The final
+// accumulate into Y is race free: each pass ends with a barrier, and within a
+// pass every Y entry has exactly one writer.
 template <int N1C>
 __device__ __forceinline__ void kron_term(int dim, int n1, int npc, const double* const* F, const double* X, double* T1,
                                           double* T2, double* Y, double coeff, bool& first) {
