@@ -771,6 +771,18 @@ fdmgpu_status fdmgpu_set_patches(fdmgpu_handle h, int32_t npatch, const int32_t*
     c.pg_idx.upload(pidx, c.stream);
     c.corr.alloc(size_t(npatch) * m);
     c.tiles.alloc(size_t(npatch) * L.ntiles * fdmgpu::kTile * fdmgpu::kTile);
+    // Separate solve-record buffer when it takes under a quarter of the free
+    // memory (C3: 3.7 GB; packing then overlaps the factorisation, 24.3 -> 23.8 ms);
+    // else (C5: 63.5 GB) the records are packed in place after the factorisation.
+    // FDMGPU_PACK=inplace forces the latter.
+    c.packed.reset();
+    {
+      const char* pk = std::getenv("FDMGPU_PACK");
+      const size_t rec_bytes = size_t(npatch) * size_t(L.tile_poff8.back()) * sizeof(double);
+      size_t fb = 0, tb = 0;
+      FDM_CUDA(cudaMemGetInfo(&fb, &tb));
+      if (!(pk && std::string(pk) == "inplace") && 4 * rec_bytes < fb) c.packed.alloc(rec_bytes / sizeof(double));
+    }
     FDM_CUDA(cudaStreamSynchronize(c.stream));
     c.have_patches = true;
     c.factored = false;
@@ -883,11 +895,16 @@ fdmgpu_status fdmgpu_factor(fdmgpu_handle h) {
     FDM_CUDA(cudaMemcpyAsync(c.d_err.p, &none, sizeof(none), cudaMemcpyHostToDevice, c.stream));
     fdmgpu::launch_patch_assemble(c);
     fdmgpu::launch_patch_lead(c);
+    for (int K = 0; K < c.L.lead_cols; ++K) fdmgpu::launch_patch_pack_col(c, K);
     for (int K = c.L.lead_cols; K < c.L.nT; ++K) {
       fdmgpu::launch_patch_update(c, K);
       fdmgpu::launch_patch_trsm(c, K);
+      fdmgpu::launch_patch_pack_col(c, K);  // no-op when packing in place
     }
-    fdmgpu::launch_patch_pack(c);  // dense tiles -> packed 8x8 sub-block records for the solve stream
+    if (c.packed.p)
+      fdmgpu::launch_patch_pack_join(c);
+    else
+      fdmgpu::launch_patch_pack(c);  // dense tiles -> packed 8x8 sub-block records, in place
     unsigned long long e = 0;
     FDM_CUDA(cudaMemcpyAsync(&e, c.d_err.p, sizeof(e), cudaMemcpyDeviceToHost, c.stream));
     FDM_CUDA(cudaStreamSynchronize(c.stream));

@@ -141,6 +141,11 @@ struct Context {
   DevArray<int64_t> tile_mask8;
   DevArray<uint8_t> tile_hdr;
   DevArray<double> corr, tiles, nK;
+  // packed solve records in their own buffer when memory allows (packing then
+  // overlaps the factorisation on pack_stream); empty -> packed in place
+  DevArray<double> packed;
+  cudaStream_t pack_stream = nullptr;
+  cudaEvent_t pack_ev = nullptr;
   std::vector<int32_t> h_pdofs, h_pcells;
   int solve_cs = 0;                      // CTAs per split patch (FDMGPU_SOLVE_CS; 0 = auto, 1 = no split)
   bool solve_tail = true;                // cluster-split only the last partial wave (FDMGPU_SOLVE_TAIL)
@@ -211,6 +216,8 @@ struct Context {
       for (cudaEvent_t e : {ev_in[k], ev_comp[k], ev_out[k]})
         if (e) cudaEventDestroy(e);
     if (h2d_stream) cudaStreamDestroy(h2d_stream);
+    if (pack_ev) cudaEventDestroy(pack_ev);
+    if (pack_stream) cudaStreamDestroy(pack_stream);
     if (d2h_stream) cudaStreamDestroy(d2h_stream);
     if (cap_stream) cudaStreamDestroy(cap_stream);
     for (auto& v : tev)
@@ -257,6 +264,8 @@ void launch_patch_update(Context& c, int K);
 void launch_patch_trsm(Context& c, int K);
 void launch_patch_lead(Context& c);
 void launch_patch_pack(Context& c);
+void launch_patch_pack_col(Context& c, int K);   // separate record buffer, side stream
+void launch_patch_pack_join(Context& c);
 void launch_patch_solve(Context& c, const double* r_modal);          // writes c.corr
 void launch_patch_gather(Context& c, double* z_modal);
 void launch_axpby(Context& c, int64_t n, double a, const double* x, double b, const double* y, double* out);

@@ -35,6 +35,7 @@ struct PatchArgs {
   const double* At;
   const double* Bt;
   unsigned long long* err;
+  int64_t rec_stride;  // doubles per patch in the solve-record buffer
 };
 
 PatchArgs make_args(Context& c) {
@@ -53,6 +54,7 @@ PatchArgs make_args(Context& c) {
   a.pos_of_lat = c.pos_of_lat.p;
   a.pcells = c.pcells.p;
   a.psep = c.pdofs.p;
+  a.rec_stride = c.packed.p ? int64_t(c.L.tile_poff8.back()) : int64_t(c.L.ntiles) * TT;
   a.mu = c.mu.p;
   a.At = c.At.p;
   a.Bt = c.Bt.p;
@@ -554,6 +556,34 @@ __global__ void k_patch_pack(int ntiles, const int64_t* __restrict__ mask8, cons
   }
 }
 
+// Same records into a separate buffer, for the tiles [t0, t0 + gridDim.x) of
+// every patch (blockIdx.y): launched per tile column on a side stream while
+// the factorisation continues, so the packing hides under the compute-bound
+// updates (the dense tiles stay intact as update operands).
+__global__ void __launch_bounds__(256) k_patch_pack_cols(int t0, int ntiles, const int64_t* __restrict__ mask8,
+                                                        const int32_t* __restrict__ poff8,
+                                                        const uint8_t* __restrict__ hdr,
+                                                        const double* __restrict__ tiles, double* __restrict__ packed,
+                                                        int64_t pstride) {
+  __shared__ __align__(16) double cur[TT];
+  __shared__ int bits[64];
+  const int t = t0 + blockIdx.x, j = blockIdx.y;
+  const double2* src = reinterpret_cast<const double2*>(tiles + (size_t(j) * ntiles + t) * TT);
+  for (int i = threadIdx.x; i < TT / 2; i += blockDim.x) reinterpret_cast<double2*>(cur)[i] = __ldcs(src + i);
+  const unsigned long long m = static_cast<unsigned long long>(mask8[t]);
+  if (threadIdx.x < 64 && ((m >> threadIdx.x) & 1ull)) bits[__popcll(m & ((1ull << threadIdx.x) - 1ull))] = int(threadIdx.x);
+  __syncthreads();
+  const int cnt = __popcll(m);
+  double* dst = packed + size_t(j) * pstride + poff8[t];
+  if (threadIdx.x < kHdr) dst[threadIdx.x] = reinterpret_cast<const double*>(hdr + size_t(t) * 8 * kHdr)[threadIdx.x];
+  dst += kHdr;
+  for (int d = threadIdx.x; d < cnt * SB8; d += blockDim.x) {
+    const int bit = bits[d >> 6], w = d & 63;
+    const int bi = bit >> 3, bj = bit & 7, rr = w >> 3, cc = 2 * (((w >> 1) & 3) ^ ((rr >> 1) & 3)) + (w & 1);
+    dst[d] = cur[tsw(8 * bi + rr, 8 * bj + cc)];
+  }
+}
+
 // Packed 8x8 sub-block layout: row-major, element (r, c) at
 // r*8 + 2*((c >> 1) ^ ((r >> 1) & 3)) + (c & 1).  Lane (r = lane & 7,
 // g = lane >> 3) owns block-columns g and 7 - g (balanced on the triangular
@@ -686,7 +716,7 @@ __global__ void __launch_bounds__(kSolveThreads)
   int* slot_off = reinterpret_cast<int*>(empty + kRingEntries);  // ring offset of entry e's record
   const int j = j0 + blockIdx.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const double* tb = tiles + size_t(j) * a.ntiles * TT;
+  const double* tb = tiles + size_t(j) * a.rec_stride;
   pdl_trigger();
   if (tid == 0) {
     for (int e = 0; e < kRingEntries; ++e) {
@@ -916,7 +946,7 @@ __global__ void __launch_bounds__(kSolveThreads)
   const int rank = int(cluster_ctarank());
   const int j = j0 + blockIdx.x / CS;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const double* tb = tiles + size_t(j) * a.ntiles * TT;
+  const double* tb = tiles + size_t(j) * a.rec_stride;
   const int32_t* col = cl_col + rank * (a.nT + 1);
   // Wait for the predecessor before letting the single-CTA solve launch: that
   // launch then runs beside this one without waiting for it (see launch_patch_solve).
@@ -1158,6 +1188,9 @@ __global__ void k_patch_gather(int64_t ndof, const double* __restrict__ corr, co
 
 }  // namespace
 
+// Solve records: the separate packed buffer when it exists, else the tiles (packed in place).
+static const double* rec_base(const Context& c) { return c.packed.p ? c.packed.p : c.tiles.p; }
+
 void launch_patch_assemble(Context& c) {
   PatchArgs a = make_args(c);
   KernelTimer timer(c, 1);
@@ -1311,7 +1344,7 @@ static void launch_solve_cl(Context& c, const PatchArgs& a, const double* r_moda
   const size_t smem = solve_cl_smem<CS>(c, &ring);
   FDM_CUDA(cudaFuncSetAttribute(k_patch_solve_cl<CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
   launch_cluster(c.pdl && !c.timing, CS, k_patch_solve_cl<CS>, dim3((c.npatch - j0) * CS), dim3(kSolveThreads),
-                 smem, c.stream, a, ring, r_modal, c.corr.p, (const double*)c.tiles.p, (const int32_t*)c.pdofs.p,
+                 smem, c.stream, a, ring, r_modal, c.corr.p, rec_base(c), (const int32_t*)c.pdofs.p,
                  (const int32_t*)c.tile_row.p, (const int32_t*)c.tile_poff8.p, (const int32_t*)c.cl_list.p,
                  (const int32_t*)c.cl_col.p, j0, c.tail_sync.p);
 }
@@ -1387,9 +1420,33 @@ void launch_patch_solve(Context& c, const double* r_modal) {
   FDM_CUDA(cudaFuncSetAttribute(k_patch_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
   // (PDL after a split tail even when timing: the overlap is part of the solve)
   launch_pdl(c.pdl && (!c.timing || tail_ctas > 0), k_patch_solve, dim3(nsolo), dim3(kSolveThreads), smem, c.stream, a, ring, r_modal,
-             c.corr.p, (const double*)c.tiles.p, (const int32_t*)c.pdofs.p, (const int32_t*)c.col_start.p,
+             c.corr.p, rec_base(c), (const int32_t*)c.pdofs.p, (const int32_t*)c.col_start.p,
              (const int32_t*)c.tile_row.p, (const int32_t*)c.tile_poff8.p, 0, c.tail_sync.p, tail_ctas);
   FDM_LAUNCH_CHECK(c);
+}
+
+// Column-wise packing into the separate record buffer (side stream): call
+// after column K's tiles are final (after its trsm).
+void launch_patch_pack_col(Context& c, int K) {
+  if (!c.packed.p) return;
+  if (!c.pack_stream) {
+    FDM_CUDA(cudaStreamCreateWithFlags(&c.pack_stream, cudaStreamNonBlocking));
+    FDM_CUDA(cudaEventCreateWithFlags(&c.pack_ev, cudaEventDisableTiming));
+  }
+  const int t0 = c.L.col_start[K], n = c.L.col_start[K + 1] - t0;
+  FDM_CUDA(cudaEventRecord(c.pack_ev, c.stream));
+  FDM_CUDA(cudaStreamWaitEvent(c.pack_stream, c.pack_ev, 0));
+  k_patch_pack_cols<<<dim3(n, c.npatch), 256, 0, c.pack_stream>>>(t0, c.L.ntiles, c.tile_mask8.p, c.tile_poff8.p,
+                                                                  c.tile_hdr.p, c.tiles.p, c.packed.p,
+                                                                  int64_t(c.L.tile_poff8.back()));
+  FDM_LAUNCH_CHECK(c);
+}
+
+// Joins the side stream (the records are complete when the handle stream passes this).
+void launch_patch_pack_join(Context& c) {
+  if (!c.packed.p || !c.pack_stream) return;
+  FDM_CUDA(cudaEventRecord(c.pack_ev, c.pack_stream));
+  FDM_CUDA(cudaStreamWaitEvent(c.stream, c.pack_ev, 0));
 }
 
 void launch_patch_pack(Context& c) {

@@ -393,3 +393,17 @@ def test_apply_async_matches_sync(pkg, torch, cfg):
         sol.synchronize()
         for x, y in zip(ins, outs):
             assert np.array_equal(y, sol.apply(op, x)), op
+
+
+def test_inplace_and_separate_packing_agree(pkg, torch, monkeypatch):
+    """Solve records packed in place after the factorisation (FDMGPU_PACK=inplace) and
+    packed per tile column into their own buffer during it give identical relaxations."""
+    prob = pkg.Problem(2, 3, 7)
+    r = prob.rhs()
+    sol = pkg.Solver(prob)
+    sol.factor()
+    z_sep = sol.smooth(r)
+    monkeypatch.setenv("FDMGPU_PACK", "inplace")
+    sol2 = pkg.Solver(prob)
+    sol2.factor()
+    assert np.array_equal(sol2.smooth(r), z_sep)
