@@ -416,6 +416,20 @@ def run_ours(args):
         except Exception as e:  # reported, not fatal for the GPU line
             result["cpu_baseline"] = {"value": None, "unit": "GDOF/s", "cores": os.cpu_count(), "kind": "port",
                                       "sample": f"failed: {e}"}
+    if rank == 0 and not args.no_elastic:
+        # the widened row, reported beside the headline: 3D elasticity,
+        # 8^3 cells, vector Q15 (bench.py --elastic 3,8,15,1 gives the full line)
+        try:
+            del sol
+            torch.cuda.empty_cache()
+            e = elastic_measure("3,8,15,1", min(args.steps, 20), args.warmup, True)
+            result["elasticity"] = {
+                "workload": e["config"]["workload"], "value": e["value"], "unit": e["unit"],
+                "ms_per_step": e["ms_per_step"], "apply_A_kernel_ms": e["residual_roofline"]["kernel_ms"],
+                "apply_A_fp64_frac": e["residual_roofline"]["frac"], "factor_ms": e["factor_ms"],
+                "pcg_iterations": e["pcg"]["iterations"], "e2e": e["e2e"]["value"]}
+        except Exception as ex:  # reported, not fatal for the headline line
+            result["elasticity"] = {"failed": str(ex)}
     replicas.barrier()
     replicas.finalize()
     if rank == 0:
@@ -433,12 +447,22 @@ def elastic_flops(prob):
 def run_elastic(args):
     """Linear-elasticity workload: the SDC/FDM relaxation of build_elasticity_twolevel on the
     reference's Table-2 problem in 3D (--elastic DIM,N,P,LAMBDA).  Same timing rules as the main line."""
+    print(json.dumps(elastic_measure(args.elastic, args.steps, args.warmup, args.no_cpu)), flush=True)
+    return 0
+
+
+def elastic_measure(spec, steps, warmup, no_cpu):
     import numpy as np
     import torch
 
     import paper_2107_14758_b200 as pkg
 
-    dim, n, p, lam = (float(v) for v in args.elastic.split(","))
+    class _A:
+        pass
+
+    args = _A()
+    args.steps, args.warmup, args.no_cpu = steps, max(warmup, 3), no_cpu
+    dim, n, p, lam = (float(v) for v in spec.split(","))
     dim, n, p = int(dim), int(n), int(p)
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
@@ -555,8 +579,7 @@ def run_elastic(args):
                                                 f"(parallel_for over patches, {threads} threads), median of 3"}
         except Exception as e:
             result["cpu_baseline"] = {"value": None, "sample": f"failed: {e}"}
-    print(json.dumps(result), flush=True)
-    return 0
+    return result
 
 
 def main():
@@ -570,6 +593,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-pcg", action="store_true")
     ap.add_argument("--elastic", default=None, help="DIM,N,P,LAMBDA: linear-elasticity workload (SURVEY.md 8(f)3)")
+    ap.add_argument("--no-elastic", action="store_true", help="skip the elasticity sub-line of the default run")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
