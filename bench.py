@@ -416,7 +416,7 @@ def run_ours(args):
         except Exception as e:  # reported, not fatal for the GPU line
             result["cpu_baseline"] = {"value": None, "unit": "GDOF/s", "cores": os.cpu_count(), "kind": "port",
                                       "sample": f"failed: {e}"}
-    if rank == 0 and not args.no_elastic:
+    if rank == 0 and world == 1 and not args.no_elastic:
         # the widened row, reported beside the headline: 3D elasticity,
         # 8^3 cells, vector Q15 (bench.py --elastic 3,8,15,1 gives the full line)
         try:
