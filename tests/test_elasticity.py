@@ -163,6 +163,11 @@ def test_elastic_deterministic_and_async(pkg):
     r = prob.rhs() + np.random.default_rng(1).standard_normal(prob.ndof) * (prob.maps()["constrained"] == 0)
     for fn in (sol.smooth, sol.apply_A):
         assert np.array_equal(fn(r), fn(r))
+    # symmetric operator and relaxation, adjoint transforms (full vector space)
+    y = np.random.default_rng(2).standard_normal(prob.ndof) * (prob.maps()["constrained"] == 0)
+    for fn in (sol.apply_A, sol.smooth):
+        assert abs(y @ fn(r) - r @ fn(y)) <= 1e-12 * abs(y @ fn(r))
+    assert abs(y @ sol.apply_S(r) - sol.apply_St(y) @ r) <= 1e-12 * np.linalg.norm(y) * np.linalg.norm(r)
     h_in = torch.from_numpy(r).pin_memory().numpy()
     outs = [torch.empty(prob.ndof, dtype=torch.float64).pin_memory().numpy() for _ in range(3)]
     for o in outs:

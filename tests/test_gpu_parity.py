@@ -157,6 +157,9 @@ def test_c3_relaxation_properties(c3, torch):
     assert np.array_equal(sol.smooth(x), Px)  # deterministic, bitwise
     A_x = sol.apply_A(x)
     assert abs(y @ A_x - x @ sol.apply_A(y)) <= 1e-12 * abs(y @ A_x)
+    # S / S^T adjointness (tests/test_assembly.cpp:186-193): y^T S x = (S^T y)^T x
+    Sx, Sty = sol.apply_S(x), sol.apply_St(y)
+    assert abs(y @ Sx - Sty @ x) <= 1e-12 * np.linalg.norm(y) * np.linalg.norm(Sx)
 
 
 def test_not_spd_reports_pivot(pkg, torch):
