@@ -66,6 +66,11 @@ Vec GlobalOperator::apply(const Vec& x) const {  // src/assembly.cpp:56-88
     for (const auto& b : term.kron_blocks)
       scatter_add(y, d.comp_dofs(b.ci, c), kron_apply(b.op, gather(xp, d.comp_dofs(b.cj, c))));
   }
+  for (const auto& ft : facets) {  // src/assembly.cpp:71-83
+    const Facet& f = d.mesh->facets[ft.facet];
+    for (const auto& b : ft.blocks)
+      scatter_add(y, d.cell_dofs[f.cell[b.r]], kron_apply(b.op, gather(xp, d.cell_dofs[f.cell[b.s]])));
+  }
   for (int i = 0; i < d.ndof; ++i)
     if (d.constrained[i]) y[i] = x[i];
   return y;
@@ -87,6 +92,11 @@ Csr GlobalOperator::assemble() const {  // src/assembly.cpp:90-129
     if (term.dense.r > 0) add_block(concat_dofs(d, c), concat_dofs(d, c), term.dense);
     if (term.has_kron) add_block(d.cell_dofs[c], d.cell_dofs[c], kron_materialize(term.kron));
     for (const auto& b : term.kron_blocks) add_block(d.comp_dofs(b.ci, c), d.comp_dofs(b.cj, c), kron_materialize(b.op));
+  }
+  for (const auto& ft : facets) {  // src/assembly.cpp:109-124
+    const Facet& f = d.mesh->facets[ft.facet];
+    for (const auto& b : ft.blocks)
+      add_block(d.cell_dofs[f.cell[b.r]], d.cell_dofs[f.cell[b.s]], kron_materialize(b.op));
   }
   for (int i = 0; i < d.ndof; ++i)
     if (d.constrained[i]) t.push_back({i, i, 1.0});

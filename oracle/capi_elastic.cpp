@@ -260,3 +260,170 @@ int oracle_sdc_axis_coefficients(int comp, int dim, double mu, double lambda, do
 }
 
 }  // extern "C"
+
+// ---- SIPG DG (oracle/sipg.cpp) -------------------------------------------------
+namespace {
+struct DCtx {
+  Mesh mesh;
+  Discretization disc;
+  Bundle1D bundle;
+  double eta = 0.0;
+  SolverConfig cfg;
+  std::shared_ptr<GlobalOperator> A;
+  std::shared_ptr<TransformedSystem> sys;
+  std::unique_ptr<TwoLevel> tl;
+  std::shared_ptr<Discretization> coarse_disc;
+  Vec rhs;
+};
+DCtx* D(void* h) { return static_cast<DCtx*>(h); }
+}  // namespace
+
+extern "C" {
+
+double oracle_sipg_default_eta(int p, int d) { return sipg_default_eta(p, d); }
+
+// Nodal facet matrices of reference_operators(p, kind): dirichlet (p+1)^2, interior (2p+2)^2, column-major;
+// traces: values / normal derivatives (2 x (p+1), column-major).
+int oracle_sipg_facet_matrices(int p, int kind, double mu0, double mu1, double eta, int side0, int side1,
+                               double* dirichlet, double* interior, double* tvals, double* tders) {
+  return guard([&] {
+    const ReferenceInterval ref = reference_operators(p, static_cast<BasisKind>(kind));
+    const Mat E = sipg_facet_dirichlet(ref, mu0, eta, side0);
+    const Mat Ei = sipg_facet_interior(ref, mu0, mu1, eta, side0, side1);
+    std::memcpy(dirichlet, E.a.data(), E.a.size() * 8);
+    std::memcpy(interior, Ei.a.data(), Ei.a.size() * 8);
+    std::memcpy(tvals, ref.trace_values.a.data(), ref.trace_values.a.size() * 8);
+    std::memcpy(tders, ref.trace_normal_derivs.a.data(), ref.trace_normal_derivs.a.size() * 8);
+  });
+}
+
+// dq_space on cartesian_mesh(dim, n^dim, unit), SIPG with eta (< 0: sipg_default_eta),
+// all boundary facets Dirichlet; rhs = load_vector(f = 1).
+void* oracle_dg_create(int dim, int n, int p, double eta, int skip_boundary, int threads) {
+  DCtx* out = nullptr;
+  guard([&] {
+    auto c = std::make_unique<DCtx>();
+    c->mesh = cartesian_mesh(dim, std::vector<int>(dim, n), std::vector<double>(dim, 1.0));
+    c->disc = dq_space(c->mesh, p);
+    c->disc.mesh = &c->mesh;
+    c->bundle = make_bundle_dg(p);
+    c->eta = eta < 0 ? sipg_default_eta(p, dim) : eta;
+    c->cfg.skip_boundary_patches = skip_boundary != 0;
+    c->cfg.threads = threads;
+    c->A = std::make_shared<GlobalOperator>(dg_poisson_operator(c->disc, c->bundle, c->eta));
+    c->sys = std::make_shared<TransformedSystem>(transformed_dg_poisson(c->disc, c->bundle, c->eta));
+    c->rhs = load_vector(c->disc, c->bundle, [](const std::array<double, 3>&) { return 1.0; });
+    out = c.release();
+  });
+  return out;
+}
+
+void oracle_dg_destroy(void* h) { delete D(h); }
+
+// out: dim, p, ncells, ndof, dofs per cell
+int oracle_dg_info(void* h, int64_t* out) {
+  return guard([&] {
+    const auto& d = D(h)->disc;
+    int64_t v[5] = {d.dim(), d.degree, D(h)->mesh.num_cells(), d.ndof, d.dofs_per_cell};
+    std::memcpy(out, v, sizeof(v));
+  });
+}
+
+int oracle_dg_rhs(void* h, double* out) {
+  return guard([&] { std::memcpy(out, D(h)->rhs.data(), D(h)->rhs.size() * 8); });
+}
+
+// which 0: true-form operator, 1: transformed matrix At; dense row-major, and the
+// stored entries per row of At (explicit zeros count, as Eigen stores them).
+int oracle_dg_dense(void* h, int which, double* out, int32_t* at_row_nnz, int32_t* label_cls) {
+  return guard([&] {
+    DCtx* c = D(h);
+    const Csr M = which == 0 ? c->A->assemble() : c->sys->At;
+    const int n = c->disc.ndof;
+    std::memset(out, 0, size_t(n) * n * 8);
+    for (int i = 0; i < n; ++i)
+      for (int64_t q = M.ptr[i]; q < M.ptr[i + 1]; ++q) out[size_t(i) * n + M.col[q]] = M.val[q];
+    for (int i = 0; i < n; ++i) {
+      at_row_nnz[i] = int32_t(c->sys->At.ptr[i + 1] - c->sys->At.ptr[i]);
+      label_cls[i] = int32_t(c->disc.labels[i].cls);
+    }
+  });
+}
+
+int oracle_dg_apply(void* h, int which, const double* in, double* out) {  // 0 A, 1 S^T, 2 S
+  return guard([&] {
+    DCtx* c = D(h);
+    Vec x(in, in + c->disc.ndof), y;
+    y = which == 0 ? c->A->apply(x) : which == 1 ? c->sys->apply_St(x) : c->sys->apply_S(x);
+    std::memcpy(out, y.data(), y.size() * 8);
+  });
+}
+
+// x = S At^{-1} S^T b with a natural-order Cholesky of At (tests/test_sipg.cpp:139-143).
+int oracle_dg_fdm_solve(void* h, const double* b, double* x) {
+  return guard([&] {
+    DCtx* c = D(h);
+    const CholFactor F = cholesky(c->sys->At, natural_ordering(c->disc.ndof));
+    Vec bb(b, b + c->disc.ndof);
+    const Vec y = c->sys->apply_S(F.solve(c->sys->apply_St(bb)));
+    std::memcpy(x, y.data(), y.size() * 8);
+  });
+}
+
+// Vertex-star patch of vertex v: its size and the nnz of its Cholesky factor under
+// patch_ordering (tests/test_sipg.cpp:150-167); v < 0 picks the first interior vertex.
+int oracle_dg_patch(void* h, int v, int64_t* out) {
+  return guard([&] {
+    DCtx* c = D(h);
+    if (v < 0)
+      for (int u = 0; u < c->mesh.num_vertices() && v < 0; ++u)
+        if (int(c->mesh.vertex_cells[u].size()) == (1 << c->mesh.dim)) v = u;
+    const std::vector<int> dofs = c->disc.star_dofs(v);
+    std::vector<DofLabel> labels;
+    for (int d : dofs) labels.push_back(c->disc.labels[d]);
+    const CholFactor F = cholesky(extract_submatrix(c->sys->At, dofs), patch_ordering(labels));
+    out[0] = int64_t(dofs.size());
+    out[1] = F.nnz();
+  });
+}
+
+// The DG two-level solver of tests/test_sipg.cpp:184-197: PatchSolver on At,
+// Q1 continuous Poisson coarse level, build_prolongation from it, damping.
+int oracle_dg_build(void* h, int calibrate) {
+  return guard([&] {
+    DCtx* c = D(h);
+    auto tl = std::make_unique<TwoLevel>();
+    auto A = c->A;
+    tl->A = [A](const Vec& x) { return A->apply(x); };
+    tl->sys = c->sys;
+    tl->patches = build_patch_solver(c->disc, *c->sys, c->bundle, c->cfg);
+    c->coarse_disc = std::make_shared<Discretization>(q_space(c->mesh, 1));
+    const Bundle1D cb = make_bundle(1);
+    const GlobalOperator cop = poisson_operator(*c->coarse_disc, cb);
+    tl->coarse = std::make_shared<CholFactor>(cholesky(cop.assemble(), natural_ordering(c->coarse_disc->ndof)));
+    Mat V, Dm;
+    cb.ref.eval(c->bundle.ref.nodes, V, Dm);
+    tl->prolong = build_prolongation(c->disc, *c->coarse_disc, V);
+    if (calibrate) calibrate_damping(*tl, c->disc, c->cfg);
+    c->tl = std::move(tl);
+  });
+}
+
+// report: iterations, converged, kappa, omega, npatches
+int oracle_dg_pcg(void* h, const double* b, double* x, double rtol, int maxit, double* report) {
+  return guard([&] {
+    DCtx* c = D(h);
+    Vec bb(b, b + c->disc.ndof);
+    auto A = c->A;
+    LinOp Aop = [A](const Vec& v) { return A->apply(v); };
+    auto [xx, rep] = pcg(Aop, c->tl->applier(), bb, rtol, maxit);
+    std::memcpy(x, xx.data(), xx.size() * 8);
+    report[0] = rep.iterations;
+    report[1] = rep.converged;
+    report[2] = rep.kappa;
+    report[3] = c->tl->omega;
+    report[4] = double(c->tl->patches.patches.size());
+  });
+}
+
+}  // extern "C"

@@ -491,6 +491,14 @@ FdmBasis fdm_basis(const ReferenceInterval& ref) {
     for (int i = 0; i <= p; ++i) dot += fdm.S(i, j) * fdm.S(p - i, j);
     fdm.parity[j] = (dot >= 0.0) ? 1.0 : -1.0;
   }
+  // deriv_traces = trace_normal_derivs * S (src/fdm_basis.cpp:78)
+  fdm.deriv_traces = Mat(2, p + 1);
+  for (int e = 0; e < 2; ++e)
+    for (int c = 0; c <= p; ++c) {
+      double acc = 0.0;
+      for (int k = 0; k <= p; ++k) acc += ref.trace_normal_derivs(e, k) * fdm.S(k, c);
+      fdm.deriv_traces(e, c) = acc;
+    }
   return fdm;
 }
 

@@ -292,7 +292,14 @@ void Discretization::project_free(Vec& x) const {
     if (constrained[d]) x[d] = 0.0;
 }
 
-Discretization q_space(const Mesh& mesh, int p) {
+static Discretization q_space_impl(const Mesh& mesh, int p, bool dg);
+Discretization q_space(const Mesh& mesh, int p) { return q_space_impl(mesh, p, false); }
+// dq_space (src/discretization.cpp:306-311): every axis DG, so no slot is
+// shared (cg_count = 0: one new DOF per cell slot, no strong Dirichlet rows);
+// labels still classify by interface slots.
+Discretization dq_space(const Mesh& mesh, int p) { return q_space_impl(mesh, p, true); }
+
+static Discretization q_space_impl(const Mesh& mesh, int p, bool dg) {
   Discretization disc;
   disc.mesh = &mesh;
   disc.degree = p;
@@ -321,7 +328,7 @@ Discretization q_space(const Mesh& mesh, int p) {
       int owner_id = K;
       std::tuple<int, int, int> key{0, 0, 0};
       bool is_shared = false;
-      const int cg_count = n_iface;
+      const int cg_count = dg ? 0 : n_iface;
       const auto& cg_axes = iface_axis;
       const auto& cg_sides = iface_side;
       bool mode_flip = false;

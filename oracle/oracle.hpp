@@ -112,6 +112,7 @@ struct FdmBasis {  // include/fdmstar/fdm_basis.hpp:21-32
   Vec lambda;
   PatMat A_t, B_t;
   Vec parity;
+  Mat deriv_traces;  // 2 x (p+1): outward normal derivative of each mode at the ends (src/fdm_basis.cpp:78)
 };
 FdmBasis fdm_basis(const ReferenceInterval& ref);  // src/fdm_basis.cpp:10-87
 
@@ -222,6 +223,7 @@ struct Discretization {  // include/fdmstar/discretization.hpp:20-58 (identical 
 };
 Discretization q_space(const Mesh& mesh, int p);  // src/discretization.cpp:70-264,299-304
 Discretization vector_q_space(const Mesh& mesh, int p);  // src/discretization.cpp:313-318
+Discretization dq_space(const Mesh& mesh, int p);         // src/discretization.cpp:306-311 (discontinuous)
 
 struct Bundle1D {  // include/fdmstar/assembly.hpp:19-25
   int degree = 0;
@@ -230,6 +232,8 @@ struct Bundle1D {  // include/fdmstar/assembly.hpp:19-25
   Mat C;
 };
 Bundle1D make_bundle(int degree);  // src/assembly.cpp:37-54 (CG family)
+Bundle1D make_bundle_dg(int degree);  // src/assembly.cpp:37-54 (DG family: GL-nodal, FDM basis in GL representation)
+FdmBasis to_gl_representation(const FdmBasis& fdm, const ReferenceInterval& gll);  // src/fdm_basis.cpp:89-101
 
 struct GlobalOperator {  // include/fdmstar/assembly.hpp:31-52 (cell terms only)
   const Discretization* disc = nullptr;
@@ -248,6 +252,16 @@ struct GlobalOperator {  // include/fdmstar/assembly.hpp:31-52 (cell terms only)
     std::vector<KronBlock> kron_blocks;
   };
   std::vector<CellTerm> cells;
+  // facet terms (include/fdmstar/assembly.hpp:40-45): y_{cell r} += op x_{cell s}
+  struct FacetTerm {
+    int facet = -1;
+    struct Block {
+      int r = 0, s = 0;
+      KronOperator op;
+    };
+    std::vector<Block> blocks;
+  };
+  std::vector<FacetTerm> facets;
   const Bundle1D* bundle = nullptr;
   Vec apply(const Vec& x) const;   // src/assembly.cpp:56-88
   Csr assemble() const;            // src/assembly.cpp:90-129
@@ -365,6 +379,19 @@ Vec vector_load(const Discretization& disc, const Bundle1D& bundle,
 TwoLevel build_elasticity_twolevel(const Discretization& disc, const Bundle1D& bundle,
                                    std::shared_ptr<const GlobalOperator> A, double mu, double lambda,
                                    const SolverConfig& config, bool calibrate = true);  // src/elasticity.cpp:204-229
+// ---- SIPG discontinuous Galerkin (src/sipg.cpp), Cartesian facets -----------
+double sipg_default_eta(int p, int d);                                                        // src/sipg.cpp:7
+Mat sipg_facet_dirichlet(const ReferenceInterval& ref, double mu_e, double eta, int side);     // src/sipg.cpp:20-25
+Mat sipg_facet_interior(const ReferenceInterval& ref, double mu0, double mu1, double eta, int side0,
+                        int side1);                                                           // src/sipg.cpp:27-45
+PatMat sipg_facet_dirichlet_t(const FdmBasis& fdm, double mu_e, double eta, int side);        // src/sipg.cpp:47-62
+PatMat sipg_facet_interior_t(const FdmBasis& fdm, double mu0, double mu1, double eta, int side0, int side1,
+                             int block_r, int block_s);                                       // src/sipg.cpp:64-87
+GlobalOperator dg_poisson_operator(const Discretization& disc, const Bundle1D& bundle,
+                                   double eta);  // src/sipg.cpp:176-250 (Kronecker path)
+TransformedSystem transformed_dg_poisson(const Discretization& disc, const Bundle1D& bundle,
+                                         double eta);  // src/sipg.cpp:252-364 (Cartesian, unflipped)
+
 // tag_boundary (src/mesh.cpp:323-332): boundary facets whose vertex centroid satisfies pred.
 void tag_boundary(Mesh& mesh, const std::function<bool(const std::array<double, 3>&)>& pred, FacetTag tag);
 

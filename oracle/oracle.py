@@ -514,3 +514,93 @@ class ElasticProblem:
         it = int(rep[0])
         return x, dict(iterations=it, converged=bool(rep[1]), kappa=rep[2], lambda_min=rep[3], lambda_max=rep[4],
                        residuals=res[:it].copy())
+
+
+# ---- SIPG DG (oracle/sipg.cpp, src/sipg.cpp) ---------------------------------------
+def _dg_lib():
+    L = _elastic_lib()
+    if not getattr(L, "_dg_ready", False):
+        L.oracle_sipg_default_eta.restype = C.c_double
+        L.oracle_sipg_default_eta.argtypes = [C.c_int, C.c_int]
+        L.oracle_sipg_facet_matrices.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, C.c_int,
+                                                 C.c_int, _d, _d, _d, _d]
+        L.oracle_dg_create.restype = C.c_void_p
+        L.oracle_dg_create.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int]
+        L.oracle_dg_destroy.argtypes = [C.c_void_p]
+        L.oracle_dg_info.argtypes = [C.c_void_p, _i64]
+        L.oracle_dg_rhs.argtypes = [C.c_void_p, _d]
+        L.oracle_dg_dense.argtypes = [C.c_void_p, C.c_int, _d, _i32, _i32]
+        L.oracle_dg_apply.argtypes = [C.c_void_p, C.c_int, _d, _d]
+        L.oracle_dg_fdm_solve.argtypes = [C.c_void_p, _d, _d]
+        L.oracle_dg_patch.argtypes = [C.c_void_p, C.c_int, _i64]
+        L.oracle_dg_build.argtypes = [C.c_void_p, C.c_int]
+        L.oracle_dg_pcg.argtypes = [C.c_void_p, _d, _d, C.c_double, C.c_int, _d]
+        L._dg_ready = True
+    return L
+
+
+def sipg_default_eta(p, d):
+    return _dg_lib().oracle_sipg_default_eta(p, d)
+
+
+def sipg_facet_matrices(p, kind, mu0, mu1, eta, side0, side1):
+    n = p + 1
+    E, Ei, tv, td = np.zeros(n * n), np.zeros(4 * n * n), np.zeros(2 * n), np.zeros(2 * n)
+    _echk(_dg_lib().oracle_sipg_facet_matrices(p, kind, mu0, mu1, eta, side0, side1, E, Ei, tv, td))
+    f = lambda a, r, c: a.reshape(r, c, order="F")
+    return f(E, n, n), f(Ei, 2 * n, 2 * n), f(tv, 2, n), f(td, 2, n)
+
+
+class DGProblem:
+    """SIPG Poisson on dq_space(cartesian_mesh(dim, n^dim), p), all boundary facets
+    Dirichlet (weak), with the transformed system and the DG two-level solver."""
+
+    def __init__(self, dim, n, p, eta=-1.0, skip_boundary_patches=False, threads=1):
+        L = _dg_lib()
+        self.h = L.oracle_dg_create(dim, n, p, eta, 1 if skip_boundary_patches else 0, threads)
+        if not self.h:
+            raise OracleError(L.oracle_elastic_last_error().decode())
+        info = np.zeros(5, np.int64)
+        _echk(L.oracle_dg_info(self.h, info))
+        self.dim, self.p, self.ncells, self.ndof, self.npc = (int(v) for v in info)
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.oracle_dg_destroy(self.h)
+            self.h = None
+
+    def rhs(self):
+        out = np.zeros(self.ndof)
+        _echk(_dg_lib().oracle_dg_rhs(self.h, out))
+        return out
+
+    def dense(self, transformed=False):
+        n = self.ndof
+        out, nnz, cls = np.zeros(n * n), np.zeros(n, np.int32), np.zeros(n, np.int32)
+        _echk(_dg_lib().oracle_dg_dense(self.h, 1 if transformed else 0, out, nnz, cls))
+        return out.reshape(n, n), nnz, cls
+
+    def apply(self, which, x):
+        out = np.zeros(self.ndof)
+        _echk(_dg_lib().oracle_dg_apply(self.h, {"A": 0, "St": 1, "S": 2}[which],
+                                        np.ascontiguousarray(x, np.float64), out))
+        return out
+
+    def fdm_solve(self, b):
+        out = np.zeros(self.ndof)
+        _echk(_dg_lib().oracle_dg_fdm_solve(self.h, np.ascontiguousarray(b, np.float64), out))
+        return out
+
+    def patch(self, v=-1):
+        out = np.zeros(2, np.int64)
+        _echk(_dg_lib().oracle_dg_patch(self.h, v, out))
+        return dict(n=int(out[0]), nnz=int(out[1]))
+
+    def build(self, calibrate=True):
+        _echk(_dg_lib().oracle_dg_build(self.h, 1 if calibrate else 0))
+
+    def pcg(self, b, rtol=1e-8, maxit=200):
+        x, rep = np.zeros(self.ndof), np.zeros(5)
+        _echk(_dg_lib().oracle_dg_pcg(self.h, np.ascontiguousarray(b, np.float64), x, rtol, maxit, rep))
+        return x, dict(iterations=int(rep[0]), converged=bool(rep[1]), kappa=rep[2], omega=rep[3],
+                       npatches=int(rep[4]))
