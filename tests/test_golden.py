@@ -54,3 +54,34 @@ def test_oracle_reproduces_golden(oracle, path):
     assert close(tl["omega"], g["damping"]["omega"], 1e-10)
     _, rep = pb.pcg(r)
     assert rep["iterations"] == g["pcg"]["iterations"]
+
+
+def test_elastic_table2_golden(oracle):
+    import json
+    import os
+
+    import numpy as np
+
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "variants", "elastic_table2.json")))
+    for lam, its, om in zip(g["lambdas"], g["iterations"], g["omega"]):
+        e = oracle.ElasticProblem(2, 8, 3, 1.0, lam)
+        e.build()
+        _, rep = e.pcg(e.rhs(), 1e-8, 600)
+        assert rep["iterations"] == its
+        assert abs(e.twolevel_info()["omega"] - om) <= 1e-10 * om
+    assert abs(np.linalg.norm(e.rhs()) - g["rhs_norm"]) <= 1e-14 * g["rhs_norm"]
+
+
+def test_dg_two_level_golden(oracle):
+    import json
+    import os
+
+    import numpy as np
+
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "variants", "dg_two_level.json")))
+    d = oracle.DGProblem(2, 4, 4)
+    d.build()
+    x, rep = d.pcg(d.rhs(), 1e-8, 200)
+    assert rep["iterations"] == g["iterations"] and rep["npatches"] == g["npatches"]
+    assert abs(rep["omega"] - g["omega"]) <= 1e-10 * g["omega"]
+    assert abs(np.linalg.norm(x) - g["x_norm"]) <= 1e-9 * g["x_norm"]
