@@ -1,22 +1,25 @@
 #!/usr/bin/env python3
 """Benchmark of the B200 vertex-star FDM Schwarz relaxation (BASELINE.json metric).
 
-Workload (config.workload): BASELINE.json config C3 — 3D Poisson on the unit
-cube, Cartesian 8x8x8 hex mesh, Q15 on GLL nodes, 343 interior vertex-star
-patches.  One step = one relaxation apply TwoLevel::smooth
-(src/schwarz.cpp:121-123): S^T transform, 343 patch solves, S transform.
-`value` = free DOFs relaxed per second over the whole job (GDOF/s), inputs
-resident in HBM; `e2e` = the same through the C-ABI host-buffer call
-(fdmgpu_apply(..., host=1)) with the H2D copy of r and the D2H copy of z
-inside the timed region.  The patch factorisation time (the metric's second
-half) and a PCG solve are reported beside it.
+Workload (config.workload): BASELINE.json config C5, the largest configuration
+and the one that fits one GPU (83.9 GB of patch factors in 180 GB HBM) -- 3D
+Poisson on the unit cube, 8x8x8 hexes with interior vertices perturbed by
++-0.1h (seed 4), Q31 on GLL nodes, 343 interior vertex-star patches of
+226,981 DOFs, 15.07 M free DOFs.  One step = one relaxation apply
+TwoLevel::smooth (src/schwarz.cpp:121-123): S^T transform, 343 patch solves,
+S transform.  `value` = free DOFs relaxed per second over the whole job
+(GDOF/s), inputs resident in HBM; `e2e` = the same through the C-ABI
+host-buffer call (fdmgpu_apply_async) with the H2D copy of r and the D2H copy
+of z of every step inside the timed region.  The patch factorisation time
+(the metric's second half) and a PCG solve are reported beside it, and C3
+(8^3 Cartesian, Q15) as a sub-result.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3] [--impl reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 5] [--impl reference]
 
 --impl reference times the CPU restatement of the reference (oracle/, the
 reference itself cannot be compiled here: Eigen3 is absent) on the host
-cores: S^T and S over all cells plus CholFactor::solve on a bounded sample of
-patches, scaled to all patches (see cpu_baseline.sample).
+cores: S^T and S over all cells plus PatchSolver::apply on a bounded sample of
+patches (one per core), scaled to all patches (see cpu_baseline.sample).
 Multi-GPU (torchrun): one independent replica per rank ("replicas only",
 weak scaling, no collective); value = sum of all ranks' DOFs / max time.
 """
@@ -118,9 +121,37 @@ class ClockSampler:
                 "source": "nvml" if self._nvml else "nvidia-smi"}
 
 
+def host_info():
+    """CPU model, logical cores and RAM of the box."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    ram = None
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemTotal"):
+                ram = round(int(line.split()[1]) / 1024 ** 2, 1)
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count(), "ram_gib": ram}
+
+
+P31_FACTORED = 4  # C5: patches factored on the CPU (143 s each); the other timed patches solve with copies
+
+
 def cpu_sample(config, steps, warmup, threads, sample_patches):
-    """CPU restatement of the reference on the host cores: S^T, the patch
-    solves of `sample_patches` patches (parallel_for over `threads`), S."""
+    """CPU restatement of the reference (oracle/) on the host cores, one bounded
+    sample of the relaxation apply TwoLevel::smooth per step: apply_St and apply_S
+    over all cells (serial, as src/assembly.cpp:308-342) plus PatchSolver::apply
+    (src/schwarz.cpp:41-54, parallel_for over `threads`) on k of the npatch
+    patches, its time scaled by npatch / k.  Both bench arms call this with the
+    same arguments."""
     import numpy as np
     from oracle import oracle as O
 
@@ -129,7 +160,18 @@ def cpu_sample(config, steps, warmup, threads, sample_patches):
     npatch = ref.npatches
     k = min(sample_patches, npatch)
     idx = np.linspace(0, npatch - 1, k).round().astype(np.int32)
-    ref.factor(idx, threads=threads)
+    copies = ""
+    if ref.p >= 31 and k > P31_FACTORED:
+        # p = 31: one factorisation is 8.66e10 multiply-adds (~143 s on one core);
+        # factor P31_FACTORED of the sampled patches, the others solve with copies
+        # of those factors (same structure and bytes streamed per solve)
+        ref.factor(idx[:P31_FACTORED], threads=P31_FACTORED)
+        for i in range(P31_FACTORED, k):
+            ref.copy_factor(int(idx[i % P31_FACTORED]), int(idx[i]))
+        copies = (f"; {P31_FACTORED} of them factored on the CPU, the other {k - P31_FACTORED} solve with copies "
+                  f"of those factors (identical structure, same bytes per solve)")
+    else:
+        ref.factor(idx, threads=threads)
     setup_s = time.perf_counter() - t0
     r = ref.rhs()
     times = []
@@ -151,12 +193,23 @@ def cpu_sample(config, steps, warmup, threads, sample_patches):
         "unit": "GDOF/s",
         "cores": threads,
         "kind": "port",
-        "sample": (f"oracle (plain-C++ restatement; reference needs Eigen3, absent) on config C{config}: apply_St + "
-                   f"apply_S over all {ref.ncells} cells and CholFactor::solve on {k} of {npatch} patches "
-                   f"(parallel_for, {threads} threads), patch time scaled by {npatch}/{k}; median of {steps}"),
+        "sample": (f"oracle (plain-C++ restatement; the reference needs Eigen3, absent) on config C{config}: apply_St "
+                   f"+ apply_S over all {ref.ncells} cells and PatchSolver::apply on {k} of {npatch} patches "
+                   f"(parallel_for, {threads} threads{copies}), patch time scaled by {npatch}/{k}; median of "
+                   f"{steps} steps after {warmup} warm-up"),
         "ms_per_step": t_step * 1e3,
+        "ms_min": min(times) * 1e3,
+        "ms_max": max(times) * 1e3,
         "setup_s": setup_s,
+        "host": host_info(),
     }
+
+
+def config_dict(config):
+    """The `config` object both arms print (identical, so the driver's same_config holds)."""
+    l2 = ("L2 flushed before every step (512 MB write outside the per-step events)" if config in (1, 2) else
+          "inputs larger than L2: the packed patch factor streamed per step is GBs (>> 126 MB L2)")
+    return {"workload": WORKLOADS[config], "config": config, "l2": l2}
 
 
 def run_reference(args):
@@ -166,13 +219,15 @@ def run_reference(args):
     if rank != 0:
         return 0
     threads = os.cpu_count() or 1
-    cb = cpu_sample(args.config, args.steps, args.warmup, threads, args.cpu_sample_patches)
+    cb = cpu_sample(args.config, args.steps, args.warmup, threads, args.cpu_sample_patches or threads)
     line = {
         "impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "GDOF/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": cb["ms_per_step"], "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOADS[args.config], "config": args.config},
+        "config": config_dict(args.config),
         "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "cpu_spread_ms": {"min": cb["ms_min"], "median": cb["ms_per_step"], "max": cb["ms_max"]},
+        "host": cb["host"], "setup_s": cb["setup_s"],
         "e2e": {"value": cb["value"], "unit": "GDOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -203,6 +258,71 @@ def transform_roofline(prob, ms, hbm_peak):
     t_floor = max(byts / (hbm_peak * 1e9), flops / (FP64_PEAK_TFLOPS * 1e12))
     return {"ms": ms, "flops": flops, "bytes": byts, "achieved_TFLOPs": flops / (ms * 1e-3) / 1e12,
             "achieved_GBps": byts / (ms * 1e-3) / 1e9, "frac": t_floor / (ms * 1e-3), "op": "apply_St"}
+
+
+CPU_STEPS = 5  # CPU-leg samples in the GPU arm (median of 5 after 1 warm-up)
+
+
+def solve_kernel_bytes(L, prob):
+    """Algorithmic bytes of one separator solve launch (k_patch_solve + split tail):
+    16 B x separator nnz(L_j) of the factor in use (fwd + bwd) + 20 B x m per patch."""
+    nnz_sep = (L["nnz_L"] - (prob.dim + 1) * L["n_interior"]) * L["npatch"]
+    return 16.0 * nnz_sep + 2 * 8.0 * L["npatch"] * L["n_interface"] + 4.0 * L["npatch"] * L["n_interface"]
+
+
+def sub_measure(config, steps, warmup, stream, device):
+    """Secondary configuration beside the headline (same timing rules, device-resident
+    vectors, inputs larger than L2): relaxation rate, separator-solve roofline,
+    factorisation time and a PCG solve."""
+    import torch
+
+    import paper_2107_14758_b200 as pkg
+
+    prob = pkg.Problem(config)
+    sol = pkg.Solver(prob, device=device, stream=stream)
+    L = sol.layout()
+    fac = []
+    for _ in range(2):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record(stream)
+        sol.factor()
+        b.record(stream)
+        torch.cuda.synchronize()
+        fac.append(a.elapsed_time(b))
+    r = torch.from_numpy(prob.rhs()).to(torch.device("cuda", device))
+    z = torch.empty_like(r)
+    for _ in range(max(warmup, 3)):
+        sol.smooth(r, z)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(steps):
+        sol.smooth(r, z)
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / steps
+    sol.kernel_timing(True)
+    n = min(steps, 20)
+    for _ in range(n):
+        sol.smooth(r, z)
+    torch.cuda.synchronize()
+    solve_ms = sol.kernel_time("patch_solve")[0] / n
+    sol.kernel_timing(False)
+    hbm_peak, _ = measured_peaks()
+    kb = solve_kernel_bytes(L, prob)
+    cal = sol.calibrate_damping()
+    _, rep = sol.pcg(r, rtol=1e-8, maxit=200)
+    fac_flops = 2.0 * L["flops_ref"] * L["npatch"]
+    return {"workload": WORKLOADS[config], "value": prob.nfree / (ms * 1e-3) / 1e9, "unit": "GDOF/s",
+            "ms_per_step": ms, "steps": steps,
+            "roofline": {"kernel": "k_patch_solve (+ split tail)", "achieved": kb / (solve_ms * 1e-3) / 1e9,
+                         "peak": hbm_peak, "unit": "GB/s", "frac": kb / (solve_ms * 1e-3) / 1e9 / hbm_peak,
+                         "kernel_ms": solve_ms, "algorithmic_bytes": kb},
+            "factor_ms": min(fac),
+            "factor_fp64_frac": fac_flops / (min(fac) * 1e-3) / 1e12 / FP64_PEAK_TFLOPS,
+            "pcg": {"iterations": rep["iterations"], "converged": rep["converged"], "omega": cal["omega"],
+                    "solve_s": rep["wall_time"]}}
 
 
 def run_ours(args):
@@ -355,8 +475,7 @@ def run_ours(args):
         traffic = None
     nnz_total = L["nnz_L_reference"] * L["npatch"]  # reference patch_ordering factor (SURVEY.md Bytes_relax)
     # separator columns of the factor the kernel streams (order in use; interior columns are never stored)
-    nnz_sep = (L["nnz_L"] - (prob.dim + 1) * L["n_interior"]) * L["npatch"]
-    kern_bytes = 16.0 * nnz_sep + 2 * 8.0 * L["npatch"] * L["n_interface"] + 4.0 * L["npatch"] * L["n_interface"]
+    kern_bytes = solve_kernel_bytes(L, prob)
     # per step: the separator solve is one launch of k_patch_solve plus, for the
     # last partial wave of patches, one overlapping launch of the cluster-split
     # k_patch_solve_cl (one timed interval around both)
@@ -372,10 +491,10 @@ def run_ours(args):
         "metric": METRIC, "value": value, "unit": "GDOF/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOADS[args.config], "config": args.config, "ndof": prob.ndof,
-                   "nfree": prob.nfree, "patches": L["npatch"], "patch_dofs": L["n"],
-                   "separator_dofs": L["n_interface"], "parallelism": "replicas" if world > 1 else "single",
-                   "l2": l2_note},
+        "config": config_dict(args.config),
+        "sizes": {"ndof": prob.ndof, "nfree": prob.nfree, "patches": L["npatch"], "patch_dofs": L["n"],
+                  "separator_dofs": L["n_interface"], "parallelism": "replicas" if world > 1 else "single",
+                  "l2": l2_note},
         "roofline": {"kernel": solve_kernels, "bound": "hbm", "achieved": achieved, "peak": hbm_peak,
                      "unit": "GB/s", "frac": achieved / hbm_peak, "frac_nominal_8TBps": achieved / 8000.0,
                      "traffic": traffic,
@@ -384,11 +503,11 @@ def run_ours(args):
                      "bytes_def": "16 B x separator nnz(L_j) of the factor in use (fwd + bwd; plane-by-plane "
                                   "separator order) + separator RHS gather / solution write, per launch, all patches",
                      "stored_bytes_per_pass": L["stream_bytes"]},
-        "relaxation_roofline": {"bytes": relax_bytes, "achieved_GBps": relax_bytes / (ms_per_step * 1e-3) / 1e9,
-                                "frac": relax_bytes / (ms_per_step * 1e-3) / 1e9 / hbm_peak,
-                                "bytes_def": "SURVEY.md 8(d): 8*(2*NNZ + 2*sum n_j + 4*ndof), NNZ of the reference "
-                                             "patch_ordering factor (reference-equivalent: this path streams fewer "
-                                             "bytes, so frac can exceed the kernel's)"},
+        "relaxation_reference_equivalent": {
+            "bytes": relax_bytes, "rate_GBps": relax_bytes / (ms_per_step * 1e-3) / 1e9,
+            "note": "not a roofline fraction: SURVEY.md 8(d) Bytes_relax = 8*(2*NNZ + 2*sum n_j + 4*ndof) with NNZ of "
+                    "the reference patch_ordering factor, divided by this path's step, which streams a smaller "
+                    "factor (plane-by-plane separator order, interior columns eliminated in the cell kernels)"},
         "residual_roofline": residual_roofline(prob, a_ms, hbm_peak),
         "transform_roofline": transform_roofline(prob, st_ms, hbm_peak),
         "factor_ms": factor_ms,
@@ -409,10 +528,21 @@ def run_ours(args):
         "setup_s": setup_s,
         "pcg": pcg,
     }
+    if rank == 0 and world == 1 and args.config == 5 and not args.no_sub:
+        # C3 (8^3 Cartesian, Q15) kept beside the C5 headline
+        try:
+            del sol
+            torch.cuda.empty_cache()
+            result["sub_results"] = {"C3": sub_measure(3, min(args.steps, 50), args.warmup, stream, local)}
+        except Exception as ex:  # reported, not fatal for the headline line
+            result["sub_results"] = {"C3": {"failed": str(ex)}}
     if rank == 0 and not args.no_cpu:
         try:
-            cb = cpu_sample(args.config, 3, 1, os.cpu_count() or 1, args.cpu_sample_patches)
+            threads = os.cpu_count() or 1
+            cb = cpu_sample(args.config, CPU_STEPS, 1, threads, args.cpu_sample_patches or threads)
             result["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            result["cpu_spread_ms"] = {"min": cb["ms_min"], "median": cb["ms_per_step"], "max": cb["ms_max"]}
+            result["host"] = cb["host"]
         except Exception as e:  # reported, not fatal for the GPU line
             result["cpu_baseline"] = {"value": None, "unit": "GDOF/s", "cores": os.cpu_count(), "kind": "port",
                                       "sample": f"failed: {e}"}
@@ -420,7 +550,7 @@ def run_ours(args):
         # the widened row, reported beside the headline: 3D elasticity,
         # 8^3 cells, vector Q15 (bench.py --elastic 3,8,15,1 gives the full line)
         try:
-            del sol
+            sol = None
             torch.cuda.empty_cache()
             e = elastic_measure("3,8,15,1", min(args.steps, 20), args.warmup, True)
             result["elasticity"] = {
@@ -587,9 +717,10 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", type=int, default=3, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--config", type=int, default=5, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-sample-patches", type=int, default=16)
+    ap.add_argument("--cpu-sample-patches", type=int, default=0, help="patches in the CPU sample (0: one per core)")
+    ap.add_argument("--no-sub", action="store_true", help="skip the C3 sub-result of the default C5 run")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-pcg", action="store_true")
     ap.add_argument("--elastic", default=None, help="DIM,N,P,LAMBDA: linear-elasticity workload (SURVEY.md 8(f)3)")

@@ -178,6 +178,14 @@ fdmgpu_status fdmgpu_get_layout(fdmgpu_handle h, fdmgpu_layout* out);
  * handle's separator order (fdmgpu_get_patch_elimination_dofs positions
  * n_I..n-1; absent positions of boundary stars hold identity rows). */
 fdmgpu_status fdmgpu_patch_schur(fdmgpu_handle h, int32_t j, double* out);
+/* Debug / parity entry, the twin of fdmgpu_patch_schur: x_j = A~_j^{-1} r_j
+ * for patch j alone -- CholFactor::solve of patches[j].factor
+ * (src/cholesky.cpp:89-110) as PatchSolver::apply calls it
+ * (src/schwarz.cpp:41-54) -- with r_j / x_j host arrays in the order of
+ * patches[j].dofs (ascending star_dofs ids, src/discretization.cpp:266-297),
+ * length n_j.  Runs the batched device solve and keeps patch j's
+ * correction only (cost of one relaxation's patch stage). */
+fdmgpu_status fdmgpu_patch_solve_one(fdmgpu_handle h, int32_t j, const double* rhs, double* out);
 /* Per-patch global DOFs in elimination order (npatch x n): dofs[perm[k]]. */
 fdmgpu_status fdmgpu_get_patch_elimination_dofs(fdmgpu_handle h, int32_t* out);
 

@@ -268,6 +268,21 @@ int oracle_factor_patches(void* h, const int32_t* idx, int n, int threads) {
   });
 }
 
+// Timing harness only (bench.py cpu legs): patch dst gets a copy of patch
+// src's factor.  All interior stars share one structure and size, so a solve
+// with the copy streams the same bytes as a solve with dst's own factor would
+// (the values are src's); used where factoring every timed patch is too slow
+// (C5: 143 s per patch).
+int oracle_copy_factor(void* h, int src, int dst) {
+  return guard([&] {
+    Ctx* c = static_cast<Ctx*>(h);
+    auto& P = c->ps.patches;
+    if (P.at(src).factor.n != int(P.at(dst).dofs.size()))
+      throw std::invalid_argument("copy_factor: patch sizes differ or source not factored");
+    P.at(dst).factor = P.at(src).factor;
+  });
+}
+
 // out: nnz(L_j), flops (reference counter), n_j
 int oracle_patch_factor_info(void* h, int j, int64_t* out) {
   return guard([&] {

@@ -55,6 +55,7 @@ def lib():
             getattr(L, nm).argtypes = [C.c_void_p, _d, _d]
         L.oracle_factor_patches.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int]
         L.oracle_patch_factor_info.argtypes = [C.c_void_p, C.c_int, _i64]
+        L.oracle_copy_factor.argtypes = [C.c_void_p, C.c_int, C.c_int]
         L.oracle_patch_factor_get.argtypes = [C.c_void_p, C.c_int, _i64, _i32, _d]
         L.oracle_patch_matrix.argtypes = [C.c_void_p, C.c_int, _i64, C.c_void_p, C.c_void_p, C.c_void_p]
         L.oracle_patch_solve_one.argtypes = [C.c_void_p, C.c_int, _d, _d]
@@ -310,6 +311,10 @@ class Problem:
         else:
             a = np.ascontiguousarray(idx, np.int32)
             _chk(lib().oracle_factor_patches(self.h, a.ctypes.data_as(C.c_void_p), len(a), threads))
+
+    def copy_factor(self, src, dst):
+        """Timing harness only: patch dst solves with a copy of patch src's factor."""
+        _chk(lib().oracle_copy_factor(self.h, int(src), int(dst)))
 
     def factor_info(self, j):
         out = np.zeros(3, np.int64)

@@ -83,6 +83,9 @@ def lib():
         L.fdmhost_problem_set_skip_boundary_patches.argtypes = [_vp, C.c_int]
         L.fdmhost_write_matrix_market.argtypes = [C.c_char_p, C.c_int64, C.c_int64, _vp, _vp, _vp, C.c_int]
         L.fdmgpu_patch_schur.argtypes = [_vp, C.c_int32, _vp]
+        L.fdmgpu_patch_solve_one.argtypes = [_vp, C.c_int32, _vp, _vp]
+        L.fdmgpu_set_separator_order.argtypes = [_vp, C.c_int32]
+        L.fdmgpu_set_patches.argtypes = [_vp, C.c_int32, _vp, _vp, _vp, _vp, _vp]
         L.fdmhost_problem_info.argtypes = [_vp, _vp]
         L.fdmhost_get_rhs.argtypes = [_vp, _vp]
         L.fdmhost_get_maps.argtypes = [_vp] * 7
@@ -347,6 +350,18 @@ class Solver:
         mu = np.ascontiguousarray(mu, np.float64)
         self._chk(lib().fdmgpu_set_cell_coeffs(self.h, _ptr(kind), _ptr(mu), _ptr(xyz), _ptr(kap)))
 
+    def set_patches(self, separator_order=None, patches=None):
+        """Re-feed the patch lists (fdmgpu_set_patches; invalidates the factor),
+        optionally under another separator order ("plane" | "reference") or
+        from explicit lists (dict as Problem.patches() returns)."""
+        if separator_order is not None:
+            self._chk(lib().fdmgpu_set_separator_order(self.h, {"plane": 0, "reference": 1}[separator_order]))
+        pt = self.problem.patches() if patches is None else patches
+        arrs = [np.ascontiguousarray(pt["vertex"], np.int32), np.ascontiguousarray(pt["ptr"], np.int64),
+                np.ascontiguousarray(pt["dofs"], np.int32), np.ascontiguousarray(pt["perm"], np.int32),
+                np.ascontiguousarray(pt["cells"], np.int32)]
+        self._chk(lib().fdmgpu_set_patches(self.h, len(arrs[0]), *(_ptr(a) for a in arrs)))
+
     def layout(self):
         L = Layout()
         self._chk(lib().fdmgpu_get_layout(self.h, C.byref(L)))
@@ -363,6 +378,14 @@ class Solver:
         m = self.layout()["n_interface"]
         out = np.zeros((m, m), order="F")
         self._chk(lib().fdmgpu_patch_schur(self.h, int(j), _ptr(out)))
+        return out
+
+    def patch_solve_one(self, j, rj):
+        """x_j = A~_j^{-1} r_j for patch j alone (CholFactor::solve, src/cholesky.cpp:89-110);
+        rj / x_j in the order of the patch's ascending star_dofs."""
+        rj = np.ascontiguousarray(rj, np.float64)
+        out = np.zeros_like(rj)
+        self._chk(lib().fdmgpu_patch_solve_one(self.h, int(j), _ptr(rj), _ptr(out)))
         return out
 
     def export_patch_matrix(self, j, path):

@@ -57,6 +57,17 @@ double host_dot(Context& c, const double* x, const double* y) {
   return s;
 }
 
+// Drops the captured PCG graph: it holds the device pointers and the kernel
+// path of the state it was captured on, so every setter that reallocates or
+// re-selects device state must call this (the next pcg re-captures).
+void invalidate_graph(Context& c) {
+  if (c.pcg_exec) {
+    cudaGraphExecDestroy(c.pcg_exec);
+    c.pcg_exec = nullptr;
+  }
+  c.pcg_precond = -1;
+}
+
 void copy_dev(Context& c, double* dst, const double* src) {
   FDM_CUDA(cudaMemcpyAsync(dst, src, c.ndof * sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
 }
@@ -482,6 +493,7 @@ fdmgpu_status fdmgpu_set_stream(fdmgpu_handle h, void* stream) {
  * handle with dim identical components and the SDC relaxation. */
 fdmgpu_status fdmgpu_set_elasticity(fdmgpu_handle h, double mu, double lambda, const double* C) {
   return fdmgpu::guarded(h, [&](Context& c) {
+    fdmgpu::invalidate_graph(c);
     if (c.have_maps || !c.comp.empty()) throw Error(FDMGPU_INVALID_ARGUMENT, "set_elasticity: call right after fdmgpu_create");
     if (!C) throw Error(FDMGPU_INVALID_ARGUMENT, "set_elasticity: null C");
     if (!(mu > 0.0) || !(lambda >= 0.0) || std::isinf(lambda))
@@ -522,6 +534,7 @@ fdmgpu_status fdmgpu_set_basis(fdmgpu_handle h, const double* S, const double* l
                                const double* wq, const double* Vq, const double* Dq) {
   (void)lambda;
   return fdmgpu::guarded(h, [&](Context& c) {
+    fdmgpu::invalidate_graph(c);
     if (!S || !A_t || !B_t || !A_t_pattern || !B_t_pattern || !A_hat || !B_hat)
       throw Error(FDMGPU_INVALID_ARGUMENT, "set_basis: null array");
     const int n1 = c.n1, nn = n1 * n1;
@@ -560,6 +573,7 @@ fdmgpu_status fdmgpu_set_basis(fdmgpu_handle h, const double* S, const double* l
 fdmgpu_status fdmgpu_set_mesh_maps(fdmgpu_handle h, const int32_t* cell_dofs, const int32_t* cell_modes,
                                    const double* mode_signs, const double* multiplicity, const uint8_t* constrained) {
   return fdmgpu::guarded(h, [&](Context& c) {
+    fdmgpu::invalidate_graph(c);
     if (!cell_dofs || !multiplicity || !constrained) throw Error(FDMGPU_INVALID_ARGUMENT, "set_mesh_maps: null array");
     const size_t nm = size_t(c.ncells) * c.npc;
     if (c.ncomp > 1) {
@@ -631,6 +645,7 @@ fdmgpu_status fdmgpu_set_mesh_maps(fdmgpu_handle h, const int32_t* cell_dofs, co
 fdmgpu_status fdmgpu_set_cell_coeffs(fdmgpu_handle h, const uint8_t* kind, const double* mu, const double* xyz,
                                      const double* kappa) {
   return fdmgpu::guarded(h, [&](Context& c) {
+    fdmgpu::invalidate_graph(c);
     if (!kind || !mu) throw Error(FDMGPU_INVALID_ARGUMENT, "set_cell_coeffs: null array");
     if (c.ncomp > 1) {
       // elasticity_primal_operator's Kronecker path (src/elasticity.cpp:83-119):
@@ -679,6 +694,7 @@ fdmgpu_status fdmgpu_set_cell_coeffs(fdmgpu_handle h, const uint8_t* kind, const
 fdmgpu_status fdmgpu_set_patches(fdmgpu_handle h, int32_t npatch, const int32_t* vertex, const int64_t* ptr,
                                  const int32_t* dofs, const int32_t* perm, const int32_t* star_cells) {
   return fdmgpu::guarded(h, [&](Context& c) {
+    fdmgpu::invalidate_graph(c);
     fdmgpu::NvtxRange nvtx_("fdmgpu_set_patches");
     c.check_ready(false, false, false);
     if (npatch < 1 || !vertex || !ptr || !dofs || !perm || !star_cells)
@@ -722,6 +738,10 @@ fdmgpu_status fdmgpu_set_patches(fdmgpu_handle h, int32_t npatch, const int32_t*
       throw Error(FDMGPU_UNSUPPORTED, "set_patches: facet mode flips (2D non-lattice meshes) are not supported");
     fdmgpu::analyze_patches(c, npatch, vertex, ptr, dofs, perm, star_cells);
     c.npatch = npatch;
+    // split-tail solve state belongs to the previous tile pattern / patch count
+    c.cl_cs = 0;
+    for (int& f : c.cl_fit) f = -1;
+    c.tail_sync.reset();
     const auto& L = c.L;
     const size_t tile_bytes = size_t(npatch) * L.ntiles * fdmgpu::kTile * fdmgpu::kTile * sizeof(double);
     size_t free_b = 0, total_b = 0;
@@ -792,6 +812,7 @@ fdmgpu_status fdmgpu_set_patches(fdmgpu_handle h, int32_t npatch, const int32_t*
 fdmgpu_status fdmgpu_set_coarse(fdmgpu_handle h, int32_t ndof_c, const double* cinv, const int64_t* P_ptr,
                                 const int32_t* P_col, const double* P_val) {
   return fdmgpu::guarded(h, [&](Context& c) {
+    fdmgpu::invalidate_graph(c);
     if (ndof_c < 1 || !cinv || !P_ptr) throw Error(FDMGPU_INVALID_ARGUMENT, "set_coarse: bad args");
     const int64_t nnz = P_ptr[c.ndof];  // 0 when every coarse DOF is constrained
     if (nnz > 0 && (!P_col || !P_val)) throw Error(FDMGPU_INVALID_ARGUMENT, "set_coarse: bad args");
@@ -824,6 +845,7 @@ fdmgpu_status fdmgpu_set_coarse(fdmgpu_handle h, int32_t ndof_c, const double* c
 fdmgpu_status fdmgpu_set_coarse_cells(fdmgpu_handle h, const int32_t* coarse_cell_dofs,
                                       const uint8_t* coarse_constrained, const double* phat) {
   return fdmgpu::guarded(h, [&](Context& c) {
+    fdmgpu::invalidate_graph(c);
     if (!c.have_coarse || !c.have_maps) throw Error(FDMGPU_INVALID_ARGUMENT, "set_coarse_cells: set maps and coarse first");
     if (!coarse_cell_dofs || !coarse_constrained || !phat)
       throw Error(FDMGPU_INVALID_ARGUMENT, "set_coarse_cells: null array");
@@ -983,6 +1005,58 @@ fdmgpu_status fdmgpu_patch_schur(fdmgpu_handle h, int32_t j, double* out) {
   });
 }
 
+fdmgpu_status fdmgpu_patch_solve_one(fdmgpu_handle h, int32_t j, const double* rhs, double* out) {
+  return fdmgpu::guarded(h, [&](Context& c) {
+    fdmgpu::NvtxRange nvtx_("fdmgpu_patch_solve_one");
+    c.check_ready(true, true, false);
+    if (c.ncomp > 1) throw Error(FDMGPU_UNSUPPORTED, "patch_solve_one: scalar handles only");
+    if (j < 0 || j >= c.npatch || !rhs || !out) throw Error(FDMGPU_INVALID_ARGUMENT, "patch_solve_one: bad arguments");
+    const int n = c.L.n, ncorner = 1 << c.dim;
+    std::vector<int32_t> dofs;
+    for (int k = 0; k < n; ++k)
+      if (c.h_pdofs[size_t(j) * n + k] >= 0) dofs.push_back(c.h_pdofs[size_t(j) * n + k]);
+    std::sort(dofs.begin(), dofs.end());  // star_dofs order (ascending global ids)
+    std::vector<double> r(c.ndof, 0.0);
+    for (size_t k = 0; k < dofs.size(); ++k) r[dofs[k]] = rhs[k];
+    // only patch j's cells carry its interior block
+    std::vector<double> ind(c.ncells, 0.0);
+    for (int k = 0; k < ncorner; ++k) {
+      const int K = c.h_pcells[size_t(j) * ncorner + k];
+      if (K >= 0) ind[K] = 1.0;
+    }
+    fdmgpu::DevArray<double> nk1;
+    nk1.upload(ind, c.stream);
+    double* rin = c.w[9].p;
+    double* zout = c.w[10].p;
+    FDM_CUDA(cudaMemcpyAsync(rin, r.data(), c.ndof * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+    // PatchSolver::apply restricted to patch j: every patch solves, then all
+    // corrections but patch j's are dropped before the patch sum
+    fdmgpu::launch_cells_schur(c, rin);
+    fdmgpu::launch_gather(c, 3, c.E.p, rin, c.w[6].p);
+    fdmgpu::launch_patch_solve(c, c.w[6].p);
+    const size_t m = size_t(c.L.m);
+    if (j > 0) FDM_CUDA(cudaMemsetAsync(c.corr.p, 0, size_t(j) * m * sizeof(double), c.stream));
+    if (j + 1 < c.npatch)
+      FDM_CUDA(cudaMemsetAsync(c.corr.p + size_t(j + 1) * m, 0, size_t(c.npatch - j - 1) * m * sizeof(double), c.stream));
+    fdmgpu::launch_patch_gather(c, zout);
+    std::swap(c.nK.p, nk1.p);
+    std::swap(c.nK.n, nk1.n);
+    try {
+      fdmgpu::launch_cells_recon(c, zout, rin);
+      FDM_CUDA(cudaStreamSynchronize(c.stream));
+    } catch (...) {
+      std::swap(c.nK.p, nk1.p);
+      std::swap(c.nK.n, nk1.n);
+      throw;
+    }
+    std::swap(c.nK.p, nk1.p);
+    std::swap(c.nK.n, nk1.n);
+    std::vector<double> z(c.ndof);
+    FDM_CUDA(cudaMemcpy(z.data(), zout, c.ndof * sizeof(double), cudaMemcpyDeviceToHost));
+    for (size_t k = 0; k < dofs.size(); ++k) out[k] = z[dofs[k]];
+  });
+}
+
 fdmgpu_status fdmgpu_get_patch_elimination_dofs(fdmgpu_handle h, int32_t* out) {
   return fdmgpu::guarded(h, [&](Context& c) {
     c.check_ready(true, false, false);
@@ -1030,15 +1104,25 @@ fdmgpu_status fdmgpu_apply_async(fdmgpu_handle h, int32_t op, double omega, cons
     const bool needs_factor = op == FDMGPU_OP_PATCH || op == FDMGPU_OP_SMOOTH || op == FDMGPU_OP_VCYCLE;
     c.check_ready(needs_factor, needs_factor, op == FDMGPU_OP_VCYCLE);
     if (op < FDMGPU_OP_APPLY_ST || op > FDMGPU_OP_VCYCLE) throw Error(FDMGPU_INVALID_ARGUMENT, "apply: unknown operator id");
-    if (!c.h2d_stream) {
-      FDM_CUDA(cudaStreamCreateWithFlags(&c.h2d_stream, cudaStreamNonBlocking));
-      FDM_CUDA(cudaStreamCreateWithFlags(&c.d2h_stream, cudaStreamNonBlocking));
-      for (int k = 0; k < 2; ++k) {
-        for (cudaEvent_t* e : {&c.ev_in[k], &c.ev_comp[k], &c.ev_out[k]})
-          FDM_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
-        c.stage_in[k].alloc(c.ndof);
-        c.stage_out[k].alloc(c.ndof);
+    if (!c.async_ready) {
+      // all-or-nothing setup: a failure part way leaves nothing half-initialised
+      try {
+        if (!c.h2d_stream) FDM_CUDA(cudaStreamCreateWithFlags(&c.h2d_stream, cudaStreamNonBlocking));
+        if (!c.d2h_stream) FDM_CUDA(cudaStreamCreateWithFlags(&c.d2h_stream, cudaStreamNonBlocking));
+        for (int k = 0; k < 2; ++k) {
+          for (cudaEvent_t* e : {&c.ev_in[k], &c.ev_comp[k], &c.ev_out[k]})
+            if (!*e) FDM_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+          if (c.stage_in[k].n != size_t(c.ndof)) c.stage_in[k].alloc(c.ndof);
+          if (c.stage_out[k].n != size_t(c.ndof)) c.stage_out[k].alloc(c.ndof);
+        }
+      } catch (...) {
+        for (int k = 0; k < 2; ++k) {
+          c.stage_in[k].reset();
+          c.stage_out[k].reset();
+        }
+        throw;
       }
+      c.async_ready = true;
     }
     const int s = c.async_slot;
     c.async_slot ^= 1;

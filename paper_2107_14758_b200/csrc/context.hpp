@@ -189,6 +189,7 @@ struct Context {
   DevArray<double> stage_in[2], stage_out[2];
   cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_comp[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
   int async_slot = 0;
+  bool async_ready = false;  // streams, events and both staging slots all created
 
   // optional per-kernel CUDA-event timing (fdmgpu_kernel_timing)
   bool timing = false;

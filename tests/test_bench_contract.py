@@ -23,6 +23,21 @@ def test_reference_arm_json_line():
     cb = line["cpu_baseline"]
     assert cb["kind"] in ("port", "reference") and cb["cores"] >= 1 and cb["value"] == line["value"]
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["d2h_bytes_per_step"] == 0
+    # the GPU arm prints the same config object (the driver's same_config)
+    sys.path.insert(0, ROOT)
+    import bench
+
+    assert line["config"] == bench.config_dict(2)
+    assert line["host"]["nproc"] == os.cpu_count() and line["cpu_spread_ms"]["min"] <= line["ms_per_step"]
+
+
+def test_default_headline_is_c5():
+    sys.path.insert(0, ROOT)
+    import bench
+
+    src = open(os.path.join(ROOT, "bench.py")).read()
+    assert '"--config", type=int, default=5' in src
+    assert bench.config_dict(5)["workload"].startswith("C5")
 
 
 def test_product_does_not_import_oracle():

@@ -301,3 +301,18 @@ def test_patch_factor_structure(oracle, cfg, n, p, nj, nnz, madds):
     info = pb.factor_info(0)
     assert (info["n"], info["nnz"], info["flops"]) == (nj, nnz, madds)
     assert list(pb.group_offsets(0))[0] == 0
+
+
+@pytest.mark.parametrize("p", [2, 3, 4, 5, 6])
+def test_sumfact_apply_pinned_to_dense_quadrature(oracle, p):
+    """[ext] pin of the oracle's sum-factorised trilinear apply (used for C5,
+    where the dense 8.6 GB/cell matrix is infeasible) against its restatement
+    of the reference's dense cell_matrix_quadrature (src/assembly.cpp:198-228)
+    on perturbed hexes, in the style of tests/test_assembly.cpp:54-95."""
+    pb = oracle.Problem(5, 3, p, build_global=False)  # 3^3 cells, 8 perturbed interior vertices
+    rng = np.random.default_rng(p)
+    for cell in range(pb.ncells):
+        A = pb.cell_matrix_quadrature(cell)
+        u = rng.uniform(-1, 1, pb.npc)
+        y = pb.cell_sumfact_apply(cell, u)
+        assert np.linalg.norm(y - A @ u) <= 1e-12 * np.linalg.norm(A @ u), (cell, p)
