@@ -38,7 +38,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "Schwarz relaxation apply GDOF/s (FP64) + % HBM roofline; patch factorization time"
-FP64_PEAK_TFLOPS = 37.0  # measured: tools/probe/fp64_peak.cu (DMMA 37.0 / DFMA 36.5 TFLOP/s) on this pool
+# measured: tools/probe/fp64_peak.cu on this pool, DMMA 37.09 / DFMA 36.54 TFLOP/s at 1965 MHz
+# (profiles/r2a_fp64_peak.txt, with the clocks sampled during the run); MEASURED_PEAKS.json has no FP64 entry
+FP64_PEAK_TFLOPS = 37.0
 WORKLOADS = {
     1: "C1: 2D Poisson 8x8 quads, Q7 GLL, 49 vertex-star patches",
     2: "C2: 3D Poisson 4^3 hexes, Q7 GLL, 27 vertex-star patches",

@@ -82,6 +82,8 @@ def test_zero_in_zero_out(pair):
     assert np.linalg.norm(sol.smooth(z)) == 0.0 and np.linalg.norm(sol.patch_apply(z)) == 0.0
 
 
+GOLDEN = {os.path.basename(p): p for p in glob.glob(os.path.join(os.path.dirname(__file__), "golden", "*.json"))}
+
 # ---- full-size configurations against the in-process oracle (whole vectors) --------
 FULL_ORACLE = [(3, 0, 0), (4, 0, 0), (5, 0, 3)]
 
@@ -100,7 +102,7 @@ def full_pair(request, pkg, oracle, torch):
 def test_full_size_vectors_match_oracle(full_pair, torch):
     """BASELINE.json configs C3, C4 and C5's mesh at p = 3, at full size: every
     operator, the patch solve, the relaxation and the V-cycle compared as whole
-    vectors (rel-l2), and PCG to the iteration at a common omega (the damping
+    vectors (rel-l2), and PCG to the iteration at the golden calibrated omega (the damping
     calibration itself is pinned by test_full_size_against_golden)."""
     prob, sol, ref = full_pair
     r = prob.rhs()
@@ -111,7 +113,9 @@ def test_full_size_vectors_match_oracle(full_pair, torch):
     assert rel(sol.patch_apply(rt), ref.patch_apply(rt)) <= TOL_RELAX
     assert rel(sol.smooth(r), ref.smooth(r)) <= TOL_RELAX
     ref.build_twolevel(calibrate=False)
-    w = 0.25
+    name = "c%d.json" % prob.config if prob.p == {3: 15, 4: 15, 5: 31}[prob.config] else "c%d_0_%d.json" % (
+        prob.config, prob.p)
+    w = json.load(open(GOLDEN[name]))["damping"]["omega"]  # the calibrated omega (pinned by the golden test)
     ref.set_omega(w)
     sol.omega = w
     assert rel(sol.vcycle(r), ref.vcycle(r)) <= TOL_RELAX
