@@ -112,6 +112,32 @@ fdmgpu_status fdmgpu_synchronize(fdmgpu_handle h);
  * column-major.  mu, lambda: the Lame parameters. */
 fdmgpu_status fdmgpu_set_elasticity(fdmgpu_handle h, double mu, double lambda, const double* C);
 
+/* Symmetric interior-penalty DG, the SIPG variant of the path (src/sipg.cpp,
+ * include/fdmstar/sipg.hpp; the two-level DG solver of
+ * tests/test_sipg.cpp:184-197).  Turns a fresh scalar handle for
+ * dq_space(mesh, p) (all DOFs cell-local: cell_dofs per cell, multiplicity 1,
+ * nothing constrained) into the device half of that solver; call before
+ * fdmgpu_set_patches.  Cartesian cells.  Inputs:
+ *   eta                 the penalty (sipg_default_eta = (p+1)(p+d), src/sipg.cpp:7);
+ *   deriv_traces        FdmBasis::deriv_traces of the DG bundle (2 x (p+1), col-major);
+ *   trace_values,       the GL-nodal reference interval's endpoint traces
+ *   trace_normal_derivs (reference_interval.hpp:22-23, 2 x (p+1), col-major);
+ *   facets              mesh.facets: cells (nf x 2, -1 = none), normal axis,
+ *                       sides (nf x 2, -1/+1), tag (0 interior, 1 Dirichlet, 2 Neumann);
+ *   cell_vertices       mesh.cells (ncells x 2^dim corner vertex ids, tensor order).
+ * The setters then take: set_basis -- the DG bundle (S in GL representation,
+ * A_t / B_t, A_hat / B_hat the GL-nodal stiffness / mass); set_patches -- the
+ * DG vertex stars of build_patch_solver ((2p+2)^d DOFs each, whole cells) and
+ * their patch_ordering; set_coarse -- the Q1 coarse inverse and
+ * build_prolongation(dq_space, q_space(mesh, 1)).  FDMGPU_OP_A is then
+ * dg_poisson_operator (src/sipg.cpp:176-250), the relaxation the patches of
+ * transformed_dg_poisson (src/sipg.cpp:252-364), whose factors keep every
+ * patch DOF (no interior elimination). */
+fdmgpu_status fdmgpu_set_sipg(fdmgpu_handle h, double eta, const double* deriv_traces, const double* trace_values,
+                              const double* trace_normal_derivs, int32_t nfacets, const int32_t* facet_cells,
+                              const int32_t* facet_axis, const int32_t* facet_sides, const uint8_t* facet_tags,
+                              const int32_t* cell_vertices);
+
 /* FdmBasis (include/fdmstar/fdm_basis.hpp:21-32) and the reference interval
  * (reference_interval.hpp:15-27).  All (p+1)^2 arrays column-major:
  * S, A_t = S^T A S, B_t = S^T B S (values + structural 0/1 patterns), lambda

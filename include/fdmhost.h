@@ -33,6 +33,11 @@ void* fdmhost_problem_create(int config, int n, int p);
  * relaxation and a vector Q1 coarse level.  skip_boundary_patches: the
  * reference default is 0. */
 void* fdmhost_elastic_create(int dim, int n, int p, double mu, double lambda, int skip_boundary_patches);
+/* Symmetric interior-penalty DG (src/sipg.cpp): dq_space(cartesian_mesh(dim,
+ * n^dim, unit), p), every boundary facet weak Dirichlet, penalty eta (< 0:
+ * sipg_default_eta), RHS load_vector(f = 1), DG vertex stars
+ * (skip_boundary_patches: the reference default is 0), Q1 coarse level. */
+void* fdmhost_dg_create(int dim, int n, int p, double eta, int skip_boundary_patches);
 /* Q_p problem on a mesh file in the reference's JSON format (load_mesh,
  * src/mesh.cpp:375-434), RHS U[-1,1] from std::mt19937_64(seed). */
 void* fdmhost_problem_from_mesh_file(const char* path, int p, uint64_t seed);

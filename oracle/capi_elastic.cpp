@@ -409,6 +409,47 @@ int oracle_dg_build(void* h, int calibrate) {
   });
 }
 
+// After oracle_dg_build: which 0 PatchSolver::apply (modal in, modal out),
+// 1 TwoLevel::smooth, 2 TwoLevel::apply (V-cycle at the solver's omega).
+int oracle_dg_op(void* h, int which, const double* in, double* out) {
+  return guard([&] {
+    DCtx* c = D(h);
+    if (!c->tl) throw std::invalid_argument("oracle_dg_op: build first");
+    Vec x(in, in + c->disc.ndof), y;
+    y = which == 0 ? c->tl->patches.apply(x) : which == 1 ? c->tl->smooth(x) : c->tl->apply(x);
+    std::memcpy(out, y.data(), y.size() * 8);
+  });
+}
+
+int oracle_dg_set_omega(void* h, double w) {
+  return guard([&] {
+    if (!D(h)->tl) throw std::invalid_argument("oracle_dg_set_omega: build first");
+    D(h)->tl->omega = w;
+  });
+}
+
+// Patch lists of the built solver: npatch (count only when ptr is null), then
+// vertex, ptr (npatch+1), dofs, factor nnz per patch.
+int oracle_dg_patches(void* h, int64_t* count, int32_t* vertex, int64_t* ptr, int32_t* dofs, int64_t* nnz) {
+  return guard([&] {
+    DCtx* c = D(h);
+    if (!c->tl) throw std::invalid_argument("oracle_dg_patches: build first");
+    const auto& P = c->tl->patches.patches;
+    count[0] = int64_t(P.size());
+    int64_t tot = 0;
+    for (const auto& q : P) tot += int64_t(q.dofs.size());
+    count[1] = tot;
+    if (!ptr) return;
+    ptr[0] = 0;
+    for (size_t j = 0; j < P.size(); ++j) {
+      vertex[j] = P[j].vertex;
+      ptr[j + 1] = ptr[j] + int64_t(P[j].dofs.size());
+      std::memcpy(dofs + ptr[j], P[j].dofs.data(), P[j].dofs.size() * 4);
+      nnz[j] = P[j].factor.nnz();
+    }
+  });
+}
+
 // report: iterations, converged, kappa, omega, npatches
 int oracle_dg_pcg(void* h, const double* b, double* x, double rtol, int maxit, double* report) {
   return guard([&] {

@@ -540,6 +540,9 @@ def _dg_lib():
         L.oracle_dg_patch.argtypes = [C.c_void_p, C.c_int, _i64]
         L.oracle_dg_build.argtypes = [C.c_void_p, C.c_int]
         L.oracle_dg_pcg.argtypes = [C.c_void_p, _d, _d, C.c_double, C.c_int, _d]
+        L.oracle_dg_op.argtypes = [C.c_void_p, C.c_int, _d, _d]
+        L.oracle_dg_set_omega.argtypes = [C.c_void_p, C.c_double]
+        L.oracle_dg_patches.argtypes = [C.c_void_p] * 6
         L._dg_ready = True
     return L
 
@@ -603,6 +606,29 @@ class DGProblem:
 
     def build(self, calibrate=True):
         _echk(_dg_lib().oracle_dg_build(self.h, 1 if calibrate else 0))
+
+    def op(self, which, x):
+        """After build(): "patch" (PatchSolver::apply, modal), "smooth", "vcycle"."""
+        out = np.zeros(self.ndof)
+        _echk(_dg_lib().oracle_dg_op(self.h, {"patch": 0, "smooth": 1, "vcycle": 2}[which],
+                                     np.ascontiguousarray(x, np.float64), out))
+        return out
+
+    def set_omega(self, w):
+        _echk(_dg_lib().oracle_dg_set_omega(self.h, float(w)))
+
+    def patches(self):
+        """After build(): vertex, ptr, dofs and factor nnz of every patch."""
+        cnt = np.zeros(2, np.int64)
+        L = _dg_lib()
+        _echk(L.oracle_dg_patches(self.h, cnt.ctypes.data_as(C.c_void_p), None, None, None, None))
+        npch, tot = int(cnt[0]), int(cnt[1])
+        vert, ptr = np.zeros(npch, np.int32), np.zeros(npch + 1, np.int64)
+        dofs, nnz = np.zeros(tot, np.int32), np.zeros(npch, np.int64)
+        _echk(L.oracle_dg_patches(self.h, cnt.ctypes.data_as(C.c_void_p), vert.ctypes.data_as(C.c_void_p),
+                                  ptr.ctypes.data_as(C.c_void_p), dofs.ctypes.data_as(C.c_void_p),
+                                  nnz.ctypes.data_as(C.c_void_p)))
+        return dict(vertex=vert, ptr=ptr, dofs=dofs, nnz=nnz)
 
     def pcg(self, b, rtol=1e-8, maxit=200):
         x, rep = np.zeros(self.ndof), np.zeros(5)

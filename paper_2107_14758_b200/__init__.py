@@ -74,6 +74,8 @@ def lib():
         L.fdmhost_problem_destroy.argtypes = [_vp]
         L.fdmhost_elastic_create.restype = _vp
         L.fdmhost_elastic_create.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_int]
+        L.fdmhost_dg_create.restype = _vp
+        L.fdmhost_dg_create.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_int]
         L.fdmhost_problem_from_mesh_file.restype = _vp
         L.fdmhost_problem_from_mesh_file.argtypes = [C.c_char_p, C.c_int, C.c_uint64]
         L.fdmhost_problem_from_mesh.restype = _vp
@@ -184,6 +186,26 @@ class Problem:
         if not h:
             raise FdmGpuError(1, lib().fdmhost_last_error().decode())
         return cls(0, _handle=h, skip_boundary_patches=True if skip_boundary_patches else None)
+
+    @classmethod
+    def sipg(cls, dim, n, p, eta=-1.0, skip_boundary_patches=False):
+        """Symmetric interior-penalty DG Poisson (src/sipg.cpp) on dq_space of the
+        unit square / cube with n cells per axis, every boundary facet weak
+        Dirichlet, penalty eta (< 0: sipg_default_eta = (p+1)(p+d)), RHS
+        load_vector(f = 1).  The Solver then runs the two-level DG solver of
+        tests/test_sipg.cpp:184-197: dg_poisson_operator as A, vertex-star
+        patches of transformed_dg_poisson ((2p+2)^d DOFs) as the relaxation,
+        continuous Q1 coarse level.  skip_boundary_patches defaults to the
+        reference's SolverConfig default (False)."""
+        h = lib().fdmhost_dg_create(int(dim), int(n), int(p), float(eta), 1 if skip_boundary_patches else 0)
+        if not h:
+            raise FdmGpuError(1, lib().fdmhost_last_error().decode())
+        pb = cls(0, _handle=h, skip_boundary_patches=True if skip_boundary_patches else None)
+        pb.dg = True
+        pb.skip_boundary_patches = bool(skip_boundary_patches)
+        return pb
+
+    dg = False
 
     # ---- external meshes (the reference's mesh file format, src/mesh.cpp:354-434) ----
     TAGS = {"interior": 0, "dirichlet": 1, "neumann": 2}

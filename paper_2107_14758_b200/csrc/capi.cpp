@@ -19,6 +19,8 @@
 namespace fdmgpu {
 void analyze_patches(Context& c, int npatch, const int32_t* vertex, const int64_t* ptr, const int32_t* dofs,
                      const int32_t* perm, const int32_t* star_cells);
+void analyze_dg_patches(Context& c, int npatch, const int32_t* vertex, const int64_t* ptr, const int32_t* dofs,
+                        const int32_t* perm, const int32_t* star_cells);
 
 void Context::check_ready(bool need_patches, bool need_factor, bool need_coarse) const {
   if (!have_basis || !have_maps || !have_coeffs)
@@ -91,6 +93,11 @@ void op_transform(Context& c, int dir, const double* in, double* out) {
 // separator RHS, batched separator solves, patch sum, interior rebuild.
 void op_patch(Context& c, const double* in, double* out) {
   if (c.ncomp > 1) return per_component(c, in, out, [](Context& s, const double* i, double* o) { op_patch(s, i, o); });
+  if (c.dg) {  // SIPG: the patches hold every DOF of their cells, no interior elimination
+    launch_patch_solve(c, in);
+    launch_patch_gather(c, out);
+    return;
+  }
   launch_cells_schur(c, in);
   launch_gather(c, 3, c.E.p, in, c.w[6].p);
   launch_patch_solve(c, c.w[6].p);
@@ -102,6 +109,15 @@ void op_patch(Context& c, const double* in, double* out) {
 // the interior elimination fused into the two cell transforms.
 void op_smooth(Context& c, const double* r, double* z) {
   if (c.ncomp > 1) return per_component(c, r, z, [](Context& s, const double* i, double* o) { op_smooth(s, i, o); });
+  if (c.dg) {  // S * PatchSolver(S^T r) on the transformed DG system
+    launch_cells_transform(c, 0, r, 0, nullptr);
+    launch_gather(c, 0, c.E.p, nullptr, c.w[6].p);
+    launch_patch_solve(c, c.w[6].p);
+    launch_patch_gather(c, c.w[7].p);
+    launch_cells_transform(c, 1, c.w[7].p, 0, nullptr);
+    launch_gather(c, 1, c.E.p, nullptr, z);
+    return;
+  }
   launch_cells_transform(c, 0, r, 1, nullptr);  // S^T r, minus each cell's interior-elimination share
   launch_gather(c, 0, c.E.p, nullptr, c.w[6].p);
   launch_patch_solve(c, c.w[6].p);               // separator solves
@@ -117,6 +133,7 @@ void op_A(Context& c, const double* x, double* y) {  // src/assembly.cpp:56-88
     return;
   }
   launch_cells_stiffness(c, x);
+  if (c.dg) launch_dg_facets(c, x);  // dg_poisson_operator's facet terms (src/sipg.cpp:192-248)
   launch_gather(c, 2, c.E.p, x, y);
 }
 
@@ -520,6 +537,47 @@ fdmgpu_status fdmgpu_set_elasticity(fdmgpu_handle h, double mu, double lambda, c
   });
 }
 
+/* Symmetric interior-penalty DG (src/sipg.cpp): marks a fresh scalar handle
+ * as the dq_space SIPG problem -- penalty eta, the FDM modes' derivative
+ * traces, the GL nodal traces, the facet list -- before set_patches. */
+fdmgpu_status fdmgpu_set_sipg(fdmgpu_handle h, double eta, const double* deriv_traces, const double* trace_values,
+                              const double* trace_normal_derivs, int32_t nfacets, const int32_t* facet_cells,
+                              const int32_t* facet_axis, const int32_t* facet_sides, const uint8_t* facet_tags,
+                              const int32_t* cell_vertices) {
+  return fdmgpu::guarded(h, [&](Context& c) {
+    fdmgpu::invalidate_graph(c);
+    if (c.ncomp > 1 || c.have_patches) throw Error(FDMGPU_INVALID_ARGUMENT, "set_sipg: call on a scalar handle before set_patches");
+    if (!deriv_traces || !trace_values || !trace_normal_derivs || nfacets < 0 || (nfacets > 0 && (!facet_cells || !facet_axis || !facet_sides || !facet_tags)) || !cell_vertices)
+      throw Error(FDMGPU_INVALID_ARGUMENT, "set_sipg: null array");
+    if (!(eta > 0.0)) throw Error(FDMGPU_INVALID_ARGUMENT, "sipg: penalty eta must be positive");
+    const int twod = 2 * c.dim, ncorner = 1 << c.dim;
+    std::vector<int32_t> nbr(size_t(c.ncells) * twod, -1);
+    std::vector<uint8_t> tag(size_t(c.ncells) * twod, 2);  // a facet slot no facet claims: no term
+    for (int f = 0; f < nfacets; ++f) {
+      const int ax = facet_axis[f];
+      if (ax < 0 || ax >= c.dim || facet_tags[f] > 2) throw Error(FDMGPU_INVALID_ARGUMENT, "set_sipg: bad facet");
+      for (int r = 0; r < 2; ++r) {
+        const int K = facet_cells[2 * f + r];
+        if (K < 0) continue;
+        if (K >= c.ncells) throw Error(FDMGPU_INVALID_ARGUMENT, "set_sipg: facet cell out of range");
+        const int slot = 2 * ax + (facet_sides[2 * f + r] > 0 ? 1 : 0);
+        nbr[size_t(K) * twod + slot] = facet_cells[2 * f + 1 - r];
+        tag[size_t(K) * twod + slot] = facet_cells[2 * f + 1 - r] >= 0 ? 0 : facet_tags[f];
+      }
+    }
+    c.dg = true;
+    c.eta = eta;
+    const size_t nt = size_t(2) * c.n1;
+    c.dtr.upload(deriv_traces, nt, c.stream);
+    c.tv.upload(trace_values, nt, c.stream);
+    c.tnd.upload(trace_normal_derivs, nt, c.stream);
+    c.fnbr.upload(nbr, c.stream);
+    c.ftag.upload(tag, c.stream);
+    c.h_cell_vertices.assign(cell_vertices, cell_vertices + size_t(c.ncells) * ncorner);
+    FDM_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
 fdmgpu_status fdmgpu_synchronize(fdmgpu_handle h) {
   return fdmgpu::guarded(h, [](Context& c) {
     FDM_CUDA(cudaStreamSynchronize(c.stream));
@@ -736,7 +794,10 @@ fdmgpu_status fdmgpu_set_patches(fdmgpu_handle h, int32_t npatch, const int32_t*
     }
     if (c.mode_sign.p || !c.modes_alias)
       throw Error(FDMGPU_UNSUPPORTED, "set_patches: facet mode flips (2D non-lattice meshes) are not supported");
-    fdmgpu::analyze_patches(c, npatch, vertex, ptr, dofs, perm, star_cells);
+    if (c.dg)
+      fdmgpu::analyze_dg_patches(c, npatch, vertex, ptr, dofs, perm, star_cells);
+    else
+      fdmgpu::analyze_patches(c, npatch, vertex, ptr, dofs, perm, star_cells);
     c.npatch = npatch;
     // split-tail solve state belongs to the previous tile pattern / patch count
     c.cl_cs = 0;
@@ -915,7 +976,10 @@ fdmgpu_status fdmgpu_factor(fdmgpu_handle h) {
     }
     const unsigned long long none = ~0ULL;
     FDM_CUDA(cudaMemcpyAsync(c.d_err.p, &none, sizeof(none), cudaMemcpyHostToDevice, c.stream));
-    fdmgpu::launch_patch_assemble(c);
+    if (c.dg)
+      fdmgpu::launch_dg_patch_assemble(c);
+    else
+      fdmgpu::launch_patch_assemble(c);
     fdmgpu::launch_patch_lead(c);
     for (int K = 0; K < c.L.lead_cols; ++K) fdmgpu::launch_patch_pack_col(c, K);
     for (int K = c.L.lead_cols; K < c.L.nT; ++K) {

@@ -112,6 +112,18 @@ struct Context {
   std::vector<Context*> comp;          // owned sub-contexts (ncomp > 1)
   int ncs = 0;                         // scalar coarse block size
 
+  // Symmetric interior-penalty DG (fdmgpu_set_sipg, src/sipg.cpp): dq_space
+  // DOFs (all cell-local), the SIPG true form (cell Kronecker terms + facet
+  // penalty terms, dg_poisson_operator :176-250) as FDMGPU_OP_A, the
+  // transformed DG matrix (transformed_dg_poisson :252-364) in the patches,
+  // which keep every DOF of their 2^d cells (no interior elimination).
+  bool dg = false;
+  double eta = 0.0;
+  DevArray<double> dtr, tv, tnd;          // 2 x (p+1): FDM-mode derivative traces, GL nodal traces / normal derivs
+  DevArray<int32_t> fnbr;                 // ncells x 2d: neighbour across local facet (axis, side), -1 none
+  DevArray<uint8_t> ftag;                 // ncells x 2d: 0 interior, 1 dirichlet, 2 neumann
+  std::vector<int32_t> h_cell_vertices;   // ncells x 2^d mesh corners (tensor order)
+
   // basis
   DevArray<double> S, St, Ahat, Bhat, At, Bt, Vq, Dq, wq, qpts, Qbuf;
   std::vector<double> h_At, h_Bt;
@@ -260,6 +272,8 @@ void launch_cells_quadrature(Context& c, const double* x);           // writes c
 void launch_cells_elastic(Context& c, const double* x);              // writes c.E (ncomp blocks, elasticity)
 size_t elastic_smem_bytes(const Context& c);
 void launch_patch_assemble(Context& c);
+void launch_dg_patch_assemble(Context& c);                            // kernels/sipg.cu
+void launch_dg_facets(Context& c, const double* x);                    // adds the SIPG facet terms to c.E
 void launch_patch_assemble_one(Context& c, int j, double* out);  // S_G of patch j, tile layout
 void launch_patch_update(Context& c, int K);
 void launch_patch_trsm(Context& c, int K);

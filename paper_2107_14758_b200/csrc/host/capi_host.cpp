@@ -49,6 +49,14 @@ void* fdmhost_elastic_create(int dim, int n, int p, double mu, double lambda, in
   return out;
 }
 
+// Symmetric interior-penalty DG (make_dg_problem): dq_space on the unit
+// square / cube with n cells per axis, weak Dirichlet, penalty eta.
+void* fdmhost_dg_create(int dim, int n, int p, double eta, int skip_boundary_patches) {
+  Problem* out = nullptr;
+  if (guard([&] { out = make_dg_problem(dim, n, p, eta, skip_boundary_patches != 0).release(); })) return nullptr;
+  return out;
+}
+
 // Problem on a mesh file in the reference's JSON format (load_mesh,
 // src/mesh.cpp:375-434); Q_p space, unit coefficient, RHS U[-1,1] from seed.
 void* fdmhost_problem_from_mesh_file(const char* path, int p, uint64_t seed) {
@@ -227,6 +235,24 @@ int fdmhost_attach(void* ph, int device, int sep_order, fdmgpu_handle* out) {
   if (P.ncomp > 1 && (st = fdmgpu_set_elasticity(h, P.lame_mu, P.lame_lambda, P.Cmat.data())) != FDMGPU_OK)
     return fail(st);
   const Basis1D& b = P.basis;
+  if (P.dg) {  // SIPG: penalty, traces, facet list, cell corners (fdmgpu_set_sipg)
+    const auto& F = P.mesh.facets;
+    const int nf = int(F.size());
+    std::vector<int32_t> fc(2 * size_t(nf)), fa(nf), fs(2 * size_t(nf)), cv;
+    std::vector<uint8_t> ft(nf);
+    for (int f = 0; f < nf; ++f) {
+      for (int r = 0; r < 2; ++r) {
+        fc[2 * f + r] = F[f].cell[r];
+        fs[2 * f + r] = F[f].side[r];
+      }
+      fa[f] = F[f].axis[0];
+      ft[f] = uint8_t(F[f].tag);
+    }
+    for (const auto& cell : P.mesh.cells) cv.insert(cv.end(), cell.begin(), cell.end());
+    if ((st = fdmgpu_set_sipg(h, P.eta, b.dtr.a.data(), b.tv.a.data(), b.tnd.a.data(), nf, fc.data(), fa.data(),
+                              fs.data(), ft.data(), cv.data())) != FDMGPU_OK)
+      return fail(st);
+  }
   if ((st = fdmgpu_set_basis(h, b.S.a.data(), b.lambda.data(), b.A_t.a.data(), b.B_t.a.data(), b.A_nz.data(),
                              b.B_nz.data(), b.A_hat.a.data(), b.B_hat.a.data(), b.q, b.qp.data(), b.wq.data(),
                              b.Vq.a.data(), b.Dq.a.data())) != FDMGPU_OK)

@@ -51,8 +51,15 @@ struct Basis1D {
   int q = 0;
   Dense Vq, Dq;       // q x (p+1)
   Vec wq, qp;
+  // DG family (make_bundle_dg): nodes / A_hat / B_hat / S of the GL-nodal
+  // interval, the FDM modes' outward derivative traces (fdm.deriv_traces) and
+  // the nodal traces (trace_values, trace_normal_derivs), all 2 x (p+1)
+  bool dg = false;
+  Dense dtr, tv, tnd;
 };
-Basis1D make_bundle(int p);  // src/assembly.cpp:37-54 (CG family)
+Basis1D make_bundle(int p);     // src/assembly.cpp:37-54 (CG family)
+Basis1D make_bundle_dg(int p);  // src/assembly.cpp:37-54 (DG family), to_gl_representation (src/fdm_basis.cpp:89-101)
+double sipg_default_eta(int p, int d);  // src/sipg.cpp:7
 
 // ---- mesh (src/mesh.cpp), geometry (src/geometry.cpp) ------------------------
 struct Facet {
@@ -111,7 +118,9 @@ struct Space {
   int num_free() const;
   std::vector<int32_t> star_dofs(int v) const;  // src/discretization.cpp:266-297
 };
-Space q_space(const Mesh& m, int p);
+// dg = true: dq_space (src/discretization.cpp:306-311), all DOFs cell-local,
+// no strong Dirichlet marking, labels by interface-slot class as the CG ones.
+Space q_space(const Mesh& m, int p, bool dg = false);
 
 // patch_ordering (src/ordering.cpp:17-45): interiors, then facet / edge groups
 // by entity id, vertex last; ties on the position in `dofs`.
@@ -163,11 +172,20 @@ struct Problem {
   double lame_mu = 0.0, lame_lambda = 0.0;
   std::vector<double> Cmat;  // bundle.C = V^T W D on GL(p+1), (p+1)^2 column-major
   bool skip_boundary = true;
+  // SIPG DG (make_dg_problem): dq_space, penalty eta
+  bool dg = false;
+  double eta = 0.0;
 };
 std::unique_ptr<Problem> make_problem(int config, int n_override, int p_override);
 // Space, RHS (U[-1,1], or N(0,1) when `normal`, from `rng`), cell data, patches, coarse level.
 void finish_problem(Problem& pb, std::mt19937_64& rng, bool normal);
 std::unique_ptr<Problem> make_problem_from_mesh(Mesh mesh, int p, uint64_t seed);
+
+// ---- symmetric interior-penalty DG (src/sipg.cpp) -------------------------------
+// SIPG Poisson on dq_space(cartesian_mesh(dim, n^dim, unit), p), every boundary
+// facet weak Dirichlet, eta < 0 -> sipg_default_eta; RHS load_vector(f = 1);
+// DG vertex stars and the continuous Q1 coarse level (tests/test_sipg.cpp:184-197).
+std::unique_ptr<Problem> make_dg_problem(int dim, int n, int p, double eta, bool skip_boundary);
 
 // ---- linear elasticity (src/elasticity.cpp) ------------------------------------
 // The reference's Table-2 problem generalised to dim = 2|3

@@ -226,7 +226,7 @@ int Space::num_free() const {
   return n;
 }
 
-Space q_space(const Mesh& m, int p) {
+Space q_space(const Mesh& m, int p, bool dg) {
   Space s;
   s.mesh = &m;
   s.p = p;
@@ -284,7 +284,23 @@ Space q_space(const Mesh& m, int p) {
       int entity = K;
       int mode_dof = -1;
       double msign = 1.0;
-      if (nif == 0) {
+      if (dg) {
+        // dq_space (src/discretization.cpp:306-311): every slot is cell-local
+        // (owner the cell), classified like the CG slots for patch_ordering
+        dof = new_dof(0, K);
+        if (nif == 1) {
+          cls = 1;
+          entity = cf[K][2 * iax[0] + (isd[0] > 0)];
+        } else if (nif == 2 && d == 3) {
+          const int afree = 3 - iax[0] - iax[1];
+          const int v0 = m.cells[K][bits], v1 = m.cells[K][bits | (1 << afree)];
+          cls = 2;
+          entity = edge_id.at({std::min(v0, v1), std::max(v0, v1)});
+        } else if (nif > 0) {
+          cls = 3;
+          entity = m.cells[K][bits];
+        }
+      } else if (nif == 0) {
         dof = new_dof(0, K);
       } else if (nif == 1) {
         const int a = iax[0];
@@ -335,7 +351,7 @@ Space q_space(const Mesh& m, int p) {
         sign[slot] = msign;  // placeholder, fixed by the caller with the basis parity
       }
       s.multiplicity[dof] += 1.0;
-      for (int k = 0; k < nif; ++k)
+      for (int k = 0; k < nif && !dg; ++k)
         if (m.facets[cf[K][2 * iax[k] + (isd[k] > 0)]].ncells() == 1 &&
             m.facets[cf[K][2 * iax[k] + (isd[k] > 0)]].tag == 1)
           s.constrained[dof] = 1;  // src/discretization.cpp:221-226 (Dirichlet facets)

@@ -20,6 +20,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <functional>
 #include <unordered_map>
 
 #include "context.hpp"
@@ -36,6 +37,194 @@ inline void unpack(int32_t v, int* P) {
 }
 
 }  // namespace
+
+// Symbolic factorisation (etree + column counts, src/cholesky.cpp:18-31) of
+// the canonical patch pattern `neigh` (all structural neighbours of an
+// elimination position) and everything the batched kernels derive from it:
+// the dense-tile pattern of the columns from L.nI on (the factor the device
+// stores), 16x16 / 8x8 sub-block masks, the packed solve-record offsets and
+// headers, the left-looking tile-update pairs, the update-free leading
+// columns, and the structural nonzeros of the stored block after eliminating
+// positions [0, L.nI) (the entries the assembly kernels evaluate).
+void symbolic_tiles(PatchLayout& L, const std::function<void(int, std::vector<int>&)>& neigh) {
+  const int T = kTile;
+  L.nT = (L.m + T - 1) / T;
+  L.mpad = L.nT * T;
+  std::vector<int> parent(L.n, -1), flag(L.n, -1), colcount(L.n, 1), row;
+  std::vector<uint8_t> tmark(size_t(L.nT) * L.nT, 0);
+  const char* dbg_env = std::getenv("FDMGPU_DEBUG");
+  const bool dbg = dbg_env && dbg_env[0] == '1';
+  std::vector<uint8_t> m32(dbg ? size_t(L.mpad / 32) * (L.mpad / 32) : 0), m16(size_t(L.mpad / 16) * (L.mpad / 16), 0);
+  std::vector<uint8_t> m8(size_t(L.mpad / 8) * (L.mpad / 8), 0);
+  int64_t nnz_sep = 0;
+  std::vector<int> nb;
+  for (int k = 0; k < L.n; ++k) {
+    neigh(k, nb);
+    row.clear();
+    for (int pos : nb)
+      if (pos < k) row.push_back(pos);
+    flag[k] = k;
+    for (int j0 : row) {
+      for (int jj = j0; jj < k && flag[jj] != k; jj = parent[jj]) {
+        if (parent[jj] == -1) parent[jj] = k;
+        ++colcount[jj];
+        flag[jj] = k;
+        if (k >= L.nI && jj >= L.nI) {
+          tmark[size_t((k - L.nI) / T) * L.nT + (jj - L.nI) / T] = 1;
+          ++nnz_sep;
+          m16[size_t((k - L.nI) / 16) * (L.mpad / 16) + (jj - L.nI) / 16] = 1;
+          m8[size_t((k - L.nI) / 8) * (L.mpad / 8) + (jj - L.nI) / 8] = 1;
+          if (dbg) m32[size_t((k - L.nI) / 32) * (L.mpad / 32) + (jj - L.nI) / 32] = 1;
+        }
+      }
+    }
+  }
+  for (int k = 0; k < L.n; ++k) {
+    L.nnz_L += colcount[k];
+    L.flops_ref += int64_t(colcount[k]) * (colcount[k] - 1) / 2;
+  }
+  L.nnz_L_reference = L.nnz_L;
+  L.flops_reference = L.flops_ref;
+  for (int K = 0; K < L.nT; ++K) tmark[size_t(K) * L.nT + K] = 1;
+  if (dbg) {
+    int64_t t64 = 0, t32 = 0, t16 = 0, t8 = 0;
+    for (auto v : m8) t8 += v;
+    std::fprintf(stderr, "[fdmgpu] blocks8 %lld (%.3f)\n", (long long)t8, double(nnz_sep + L.m) / (t8 * 64.0));
+    for (auto v : tmark) t64 += v;
+    for (auto v : m32) t32 += v;
+    for (auto v : m16) t16 += v;
+    std::fprintf(stderr, "[fdmgpu] sep nnz %lld (+diag %d) | tiles64 %lld (%.3f) | blocks32 %lld (%.3f) | blocks16 %lld (%.3f)\n",
+                 (long long)nnz_sep, L.m, (long long)t64, double(nnz_sep + L.m) / (t64 * 4096.0), (long long)t32,
+                 double(nnz_sep + L.m) / (t32 * 1024.0), (long long)t16, double(nnz_sep + L.m) / (t16 * 256.0));
+  }
+  std::vector<int32_t> tidx(size_t(L.nT) * L.nT, -1);
+  for (int K = 0; K < L.nT; ++K) {
+    L.col_start.push_back(int32_t(L.tile_row.size()));
+    for (int I = K; I < L.nT; ++I)
+      if (tmark[size_t(I) * L.nT + K]) {
+        tidx[size_t(I) * L.nT + K] = int32_t(L.tile_row.size());
+        L.tile_row.push_back(I);
+        L.tile_col.push_back(K);
+      }
+  }
+  L.col_start.push_back(int32_t(L.tile_row.size()));
+  L.ntiles = int(L.tile_row.size());
+  // 16x16 sub-block masks (bit bi*4 + bj) used by the factor GEMMs to skip
+  // structurally zero k panels: off-diagonal tiles mark the sub-blocks the
+  // symbolic factor touches, diagonal tiles (L_KK^{-1}) their lower triangle.
+  const int nb16 = L.mpad / 16;
+  L.tile_mask.assign(L.ntiles, 0);
+  for (int t = 0; t < L.ntiles; ++t) {
+    const int I = L.tile_row[t], K = L.tile_col[t];
+    int mask = 0;
+    for (int bi = 0; bi < 4; ++bi)
+      for (int bj = 0; bj < 4; ++bj) {
+        const bool on = I == K ? bi >= bj : m16[size_t(4 * I + bi) * nb16 + (4 * K + bj)] != 0;
+        if (on) mask |= 1 << (bi * 4 + bj);
+      }
+    L.tile_mask[t] = mask;
+  }
+  // 8x8 sub-block masks (bit bi*8 + bj) of the packed solve stream, same rule.
+  const int nb8 = L.mpad / 8;
+  L.tile_mask8.assign(L.ntiles, 0);
+  L.tile_poff8.assign(L.ntiles + 1, 0);
+  L.tile_hdr.assign(size_t(L.ntiles) * 128, 0);
+  for (int t = 0; t < L.ntiles; ++t) {
+    const int I = L.tile_row[t], K = L.tile_col[t];
+    uint64_t mask = 0;
+    for (int bi = 0; bi < 8; ++bi)
+      for (int bj = 0; bj < 8; ++bj) {
+        const bool on = I == K ? bi >= bj : m8[size_t(8 * I + bi) * nb8 + (8 * K + bj)] != 0;
+        if (on) mask |= uint64_t(1) << (bi * 8 + bj);
+      }
+    L.tile_mask8[t] = int64_t(mask);
+    // stream record: 16-double header (block index per sub-block, row-major
+    // then column-major, 0xff = structurally zero) + the present sub-blocks
+    uint8_t* hr = &L.tile_hdr[size_t(t) * 128];
+    int q = 0;
+    for (int b = 0; b < 64; ++b) {
+      const uint8_t v = (mask >> b) & 1 ? uint8_t(q++) : uint8_t(0xff);
+      hr[b] = v;                              // [bi*8 + bj]
+      hr[64 + (b & 7) * 8 + (b >> 3)] = v;    // [bj*8 + bi]
+    }
+    L.tile_poff8[t + 1] = L.tile_poff8[t] + 16 + 64 * q;
+    // the in-place compaction (k_patch_pack) needs every packed prefix to end
+    // before the next unpacked tile starts
+    if (int64_t(L.tile_poff8[t + 1]) > int64_t(t + 1) * T * T)
+      throw Error(FDMGPU_UNSUPPORTED, "separator factor too dense for the packed solve stream");
+  }
+  L.pair_ptr.push_back(0);
+  for (int t = 0; t < L.ntiles; ++t) {
+    const int I = L.tile_row[t], K = L.tile_col[t];
+    for (int J = 0; J < K; ++J) {
+      const int a = tidx[size_t(I) * L.nT + J], bb = tidx[size_t(K) * L.nT + J];
+      if (a >= 0 && bb >= 0) {
+        L.pair_a.push_back(a);
+        L.pair_b.push_back(bb);
+      }
+    }
+    L.pair_ptr.push_back(int32_t(L.pair_a.size()));
+    if (I != K) ++L.tile_gemms;  // TRSM against the diagonal inverse
+  }
+  L.tile_gemms += int64_t(L.pair_a.size());
+  // Update launches only visit tiles with work: the diagonal tile (factor +
+  // invert) and off-diagonal tiles with at least one update pair.
+  L.active_ptr.assign(1, 0);
+  for (int K = 0; K < L.nT; ++K) {
+    for (int t = L.col_start[K]; t < L.col_start[K + 1]; ++t)
+      if (L.tile_row[t] == K || L.pair_ptr[t + 1] > L.pair_ptr[t]) L.active.push_back(t);
+    L.active_ptr.push_back(int32_t(L.active.size()));
+  }
+  // leading columns with no updates at all (factorised in one batch, launch_patch_lead)
+  L.lead_cols = 0;
+  while (L.lead_cols < L.nT) {
+    const int K = L.lead_cols, t0 = L.col_start[K];
+    if (L.active_ptr[K + 1] - L.active_ptr[K] != 1 || L.pair_ptr[t0 + 1] > L.pair_ptr[t0]) break;
+    ++L.lead_cols;
+  }
+  L.lead_diag.clear();
+  L.lead_trsm.clear();
+  for (int K = 0; K < L.lead_cols; ++K) {
+    L.lead_diag.push_back(L.col_start[K]);
+    for (int t = L.col_start[K] + 1; t < L.col_start[K + 1]; ++t) {
+      L.lead_trsm.push_back(t);
+      L.lead_trsm.push_back(L.col_start[K]);
+    }
+  }
+
+  // Structural nonzeros of the separator Schur complement S_G = A~_GG -
+  // A~_GI D^-1 A~_IG (lower triangle), packed (tile << 12 | col << 6 | row):
+  // the assembly kernel evaluates only these; every other stored entry
+  // starts at zero (fill).
+  std::vector<int> nb2, cols;
+  std::vector<int> seen(L.n, -1);
+  for (int k = L.nI; k < L.n; ++k) {
+    neigh(k, nb);
+    cols.clear();
+    auto add = [&](int cpos) {
+      if (cpos >= L.nI && cpos <= k && seen[cpos] != k) {
+        seen[cpos] = k;
+        cols.push_back(cpos);
+      }
+    };
+    for (int q : nb) {
+      if (q >= L.nI) {
+        add(q);
+      } else {
+        neigh(q, nb2);
+        for (int q2 : nb2) add(q2);
+      }
+    }
+    const int r = k - L.nI;
+    for (int cpos : cols) {
+      const int cc = cpos - L.nI;
+      const int t = tidx[size_t(r / T) * L.nT + cc / T];
+      if (t < 0) throw Error(FDMGPU_UNSUPPORTED, "separator entry outside the tile pattern");
+      L.entries.push_back((t << 12) | ((cc % T) << 6) | (r % T));
+    }
+  }
+  std::sort(L.entries.begin(), L.entries.end());
+}
 
 // Builds c.L, c.h_pdofs, c.h_pcells from the patch lists.
 //
@@ -252,21 +441,12 @@ void analyze_patches(Context& c, int npatch, const int32_t* vertex, const int64_
   }
 
   // ---- symbolic factorisation of the canonical patch (src/cholesky.cpp:18-31)
-  const int T = kTile;
-  L.nT = (L.m + T - 1) / T;
-  L.mpad = L.nT * T;
   std::vector<std::vector<int>> Acols(n1);
   for (int i = 0; i < n1; ++i)
     for (int jj = 0; jj < n1; ++jj)
       if (c.h_Anz[i + size_t(n1) * jj] || c.h_Bnz[i + size_t(n1) * jj]) Acols[i].push_back(jj);
   auto has = [&](const std::vector<uint8_t>& nz, int i, int jj) { return nz[i + size_t(n1) * jj] != 0; };
-  std::vector<int> parent(L.n, -1), flag(L.n, -1), colcount(L.n, 1), mark(L.n, -1), row;
-  std::vector<uint8_t> tmark(size_t(L.nT) * L.nT, 0);
-  const char* dbg_env = std::getenv("FDMGPU_DEBUG");
-  const bool dbg = dbg_env && dbg_env[0] == '1';
-  std::vector<uint8_t> m32(dbg ? size_t(L.mpad / 32) * (L.mpad / 32) : 0), m16(size_t(L.mpad / 16) * (L.mpad / 16), 0);
-  std::vector<uint8_t> m8(size_t(L.mpad / 8) * (L.mpad / 8), 0);
-  int64_t nnz_sep = 0;
+  std::vector<int> mark(L.n, -1);
   int stamp = 0;
   // All structural neighbours (any position) of position k in the canonical
   // patch matrix: union of the Kronecker patterns of the cells containing it.
@@ -316,34 +496,8 @@ void analyze_patches(Context& c, int npatch, const int32_t* vertex, const int64_
               }
         }
   };
+  symbolic_tiles(L, neigh);
   std::vector<int> nb;
-  for (int k = 0; k < L.n; ++k) {
-    neigh(k, nb);
-    row.clear();
-    for (int pos : nb)
-      if (pos < k) row.push_back(pos);
-    flag[k] = k;
-    for (int j0 : row) {
-      for (int jj = j0; jj < k && flag[jj] != k; jj = parent[jj]) {
-        if (parent[jj] == -1) parent[jj] = k;
-        ++colcount[jj];
-        flag[jj] = k;
-        if (k >= L.nI && jj >= L.nI) {
-          tmark[size_t((k - L.nI) / T) * L.nT + (jj - L.nI) / T] = 1;
-          ++nnz_sep;
-          m16[size_t((k - L.nI) / 16) * (L.mpad / 16) + (jj - L.nI) / 16] = 1;
-          m8[size_t((k - L.nI) / 8) * (L.mpad / 8) + (jj - L.nI) / 8] = 1;
-          if (dbg) m32[size_t((k - L.nI) / 32) * (L.mpad / 32) + (jj - L.nI) / 32] = 1;
-        }
-      }
-    }
-  }
-  for (int k = 0; k < L.n; ++k) {
-    L.nnz_L += colcount[k];
-    L.flops_ref += int64_t(colcount[k]) * (colcount[k] - 1) / 2;
-  }
-  L.nnz_L_reference = L.nnz_L;
-  L.flops_reference = L.flops_ref;
   if (lat_ref != L.lat) {
     // Column counts under the reference patch_ordering (SURVEY.md Appendix A
     // figures, reported beside the ones of the order in use).
@@ -379,145 +533,6 @@ void analyze_patches(Context& c, int npatch, const int32_t* vertex, const int64_
     }
     set_lat(lat_use);
   }
-  for (int K = 0; K < L.nT; ++K) tmark[size_t(K) * L.nT + K] = 1;
-  if (dbg) {
-    int64_t t64 = 0, t32 = 0, t16 = 0, t8 = 0;
-    for (auto v : m8) t8 += v;
-    std::fprintf(stderr, "[fdmgpu] blocks8 %lld (%.3f)\n", (long long)t8, double(nnz_sep + L.m) / (t8 * 64.0));
-    for (auto v : tmark) t64 += v;
-    for (auto v : m32) t32 += v;
-    for (auto v : m16) t16 += v;
-    std::fprintf(stderr, "[fdmgpu] sep nnz %lld (+diag %d) | tiles64 %lld (%.3f) | blocks32 %lld (%.3f) | blocks16 %lld (%.3f)\n",
-                 (long long)nnz_sep, L.m, (long long)t64, double(nnz_sep + L.m) / (t64 * 4096.0), (long long)t32,
-                 double(nnz_sep + L.m) / (t32 * 1024.0), (long long)t16, double(nnz_sep + L.m) / (t16 * 256.0));
-  }
-  std::vector<int32_t> tidx(size_t(L.nT) * L.nT, -1);
-  for (int K = 0; K < L.nT; ++K) {
-    L.col_start.push_back(int32_t(L.tile_row.size()));
-    for (int I = K; I < L.nT; ++I)
-      if (tmark[size_t(I) * L.nT + K]) {
-        tidx[size_t(I) * L.nT + K] = int32_t(L.tile_row.size());
-        L.tile_row.push_back(I);
-        L.tile_col.push_back(K);
-      }
-  }
-  L.col_start.push_back(int32_t(L.tile_row.size()));
-  L.ntiles = int(L.tile_row.size());
-  // 16x16 sub-block masks (bit bi*4 + bj) used by the factor GEMMs to skip
-  // structurally zero k panels: off-diagonal tiles mark the sub-blocks the
-  // symbolic factor touches, diagonal tiles (L_KK^{-1}) their lower triangle.
-  const int nb16 = L.mpad / 16;
-  L.tile_mask.assign(L.ntiles, 0);
-  for (int t = 0; t < L.ntiles; ++t) {
-    const int I = L.tile_row[t], K = L.tile_col[t];
-    int mask = 0;
-    for (int bi = 0; bi < 4; ++bi)
-      for (int bj = 0; bj < 4; ++bj) {
-        const bool on = I == K ? bi >= bj : m16[size_t(4 * I + bi) * nb16 + (4 * K + bj)] != 0;
-        if (on) mask |= 1 << (bi * 4 + bj);
-      }
-    L.tile_mask[t] = mask;
-  }
-  // 8x8 sub-block masks (bit bi*8 + bj) of the packed solve stream, same rule.
-  const int nb8 = L.mpad / 8;
-  L.tile_mask8.assign(L.ntiles, 0);
-  L.tile_poff8.assign(L.ntiles + 1, 0);
-  L.tile_hdr.assign(size_t(L.ntiles) * 128, 0);
-  for (int t = 0; t < L.ntiles; ++t) {
-    const int I = L.tile_row[t], K = L.tile_col[t];
-    uint64_t mask = 0;
-    for (int bi = 0; bi < 8; ++bi)
-      for (int bj = 0; bj < 8; ++bj) {
-        const bool on = I == K ? bi >= bj : m8[size_t(8 * I + bi) * nb8 + (8 * K + bj)] != 0;
-        if (on) mask |= uint64_t(1) << (bi * 8 + bj);
-      }
-    L.tile_mask8[t] = int64_t(mask);
-    // stream record: 16-double header (block index per sub-block, row-major
-    // then column-major, 0xff = structurally zero) + the present sub-blocks
-    uint8_t* hr = &L.tile_hdr[size_t(t) * 128];
-    int q = 0;
-    for (int b = 0; b < 64; ++b) {
-      const uint8_t v = (mask >> b) & 1 ? uint8_t(q++) : uint8_t(0xff);
-      hr[b] = v;                              // [bi*8 + bj]
-      hr[64 + (b & 7) * 8 + (b >> 3)] = v;    // [bj*8 + bi]
-    }
-    L.tile_poff8[t + 1] = L.tile_poff8[t] + 16 + 64 * q;
-    // the in-place compaction (k_patch_pack) needs every packed prefix to end
-    // before the next unpacked tile starts
-    if (int64_t(L.tile_poff8[t + 1]) > int64_t(t + 1) * T * T)
-      throw Error(FDMGPU_UNSUPPORTED, "separator factor too dense for the packed solve stream");
-  }
-  L.pair_ptr.push_back(0);
-  for (int t = 0; t < L.ntiles; ++t) {
-    const int I = L.tile_row[t], K = L.tile_col[t];
-    for (int J = 0; J < K; ++J) {
-      const int a = tidx[size_t(I) * L.nT + J], bb = tidx[size_t(K) * L.nT + J];
-      if (a >= 0 && bb >= 0) {
-        L.pair_a.push_back(a);
-        L.pair_b.push_back(bb);
-      }
-    }
-    L.pair_ptr.push_back(int32_t(L.pair_a.size()));
-    if (I != K) ++L.tile_gemms;  // TRSM against the diagonal inverse
-  }
-  L.tile_gemms += int64_t(L.pair_a.size());
-  // Update launches only visit tiles with work: the diagonal tile (factor +
-  // invert) and off-diagonal tiles with at least one update pair.
-  L.active_ptr.assign(1, 0);
-  for (int K = 0; K < L.nT; ++K) {
-    for (int t = L.col_start[K]; t < L.col_start[K + 1]; ++t)
-      if (L.tile_row[t] == K || L.pair_ptr[t + 1] > L.pair_ptr[t]) L.active.push_back(t);
-    L.active_ptr.push_back(int32_t(L.active.size()));
-  }
-  // leading columns with no updates at all (factorised in one batch, launch_patch_lead)
-  L.lead_cols = 0;
-  while (L.lead_cols < L.nT) {
-    const int K = L.lead_cols, t0 = L.col_start[K];
-    if (L.active_ptr[K + 1] - L.active_ptr[K] != 1 || L.pair_ptr[t0 + 1] > L.pair_ptr[t0]) break;
-    ++L.lead_cols;
-  }
-  L.lead_diag.clear();
-  L.lead_trsm.clear();
-  for (int K = 0; K < L.lead_cols; ++K) {
-    L.lead_diag.push_back(L.col_start[K]);
-    for (int t = L.col_start[K] + 1; t < L.col_start[K + 1]; ++t) {
-      L.lead_trsm.push_back(t);
-      L.lead_trsm.push_back(L.col_start[K]);
-    }
-  }
-
-  // Structural nonzeros of the separator Schur complement S_G = A~_GG -
-  // A~_GI D^-1 A~_IG (lower triangle), packed (tile << 12 | col << 6 | row):
-  // the assembly kernel evaluates only these; every other stored entry
-  // starts at zero (fill).
-  std::vector<int> nb2, cols;
-  std::vector<int> seen(L.n, -1);
-  for (int k = L.nI; k < L.n; ++k) {
-    neigh(k, nb);
-    cols.clear();
-    auto add = [&](int cpos) {
-      if (cpos >= L.nI && cpos <= k && seen[cpos] != k) {
-        seen[cpos] = k;
-        cols.push_back(cpos);
-      }
-    };
-    for (int q : nb) {
-      if (q >= L.nI) {
-        add(q);
-      } else {
-        neigh(q, nb2);
-        for (int q2 : nb2) add(q2);
-      }
-    }
-    const int r = k - L.nI;
-    for (int cpos : cols) {
-      const int cc = cpos - L.nI;
-      const int t = tidx[size_t(r / T) * L.nT + cc / T];
-      if (t < 0) throw Error(FDMGPU_UNSUPPORTED, "separator entry outside the tile pattern");
-      L.entries.push_back((t << 12) | ((cc % T) << 6) | (r % T));
-    }
-  }
-  std::sort(L.entries.begin(), L.entries.end());
 }
 
 }  // namespace fdmgpu

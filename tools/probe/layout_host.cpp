@@ -1,0 +1,73 @@
+// Host-only layout statistics (no GPU): runs the library's shared symbolic
+// analysis (fdmgpu::analyze_patches / symbolic_tiles) on a configuration and
+// prints the separator factor structure: tiles, nnz, stored solve-record
+// bytes, tile GEMM pairs, and the padding of the 8x8 sub-block records.
+//   g++ -O2 -std=c++20 -I include -I paper_2107_14758_b200/csrc tools/probe/layout_host.cpp \
+//       -L paper_2107_14758_b200/lib -lfdmgpu -Wl,-rpath,$PWD/paper_2107_14758_b200/lib -o /tmp/layout_host
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "context.hpp"
+#include "fdmhost.h"
+
+namespace fdmgpu {
+void analyze_patches(Context& c, int npatch, const int32_t* vertex, const int64_t* ptr, const int32_t* dofs,
+                     const int32_t* perm, const int32_t* star_cells);
+}
+
+int main(int argc, char** argv) {
+  const int config = argc > 1 ? std::atoi(argv[1]) : 3, n = argc > 2 ? std::atoi(argv[2]) : 0,
+            p = argc > 3 ? std::atoi(argv[3]) : 0, order = argc > 4 ? std::atoi(argv[4]) : 0;
+  void* pb = fdmhost_problem_create(config, n, p);
+  if (!pb) {
+    std::fprintf(stderr, "%s\n", fdmhost_last_error());
+    return 1;
+  }
+  int64_t info[16];
+  fdmhost_problem_info(pb, info);
+  const int dim = int(info[0]), pp = int(info[1]), nc = int(info[2]), npatch = int(info[5]), npc = int(info[7]);
+  const int64_t ndof = info[3], sum_nj = info[8];
+  fdmgpu::Context c;
+  c.dim = dim;
+  c.p = pp;
+  c.n1 = pp + 1;
+  c.npc = npc;
+  c.ncells = nc;
+  c.ndof = ndof;
+  c.sep_order = order;
+  const int n1 = pp + 1;
+  std::vector<double> S(n1 * n1), At(n1 * n1), Bt(n1 * n1), Ah(n1 * n1), Bh(n1 * n1), lam(n1), par(n1), nodes(n1);
+  c.h_Anz.resize(n1 * n1);
+  c.h_Bnz.resize(n1 * n1);
+  fdmhost_get_basis(pb, S.data(), At.data(), Bt.data(), c.h_Anz.data(), c.h_Bnz.data(), lam.data(), par.data(),
+                    Ah.data(), Bh.data(), nodes.data());
+  c.h_cell_dofs.resize(size_t(nc) * npc);
+  std::vector<int32_t> cm(size_t(nc) * npc);
+  fdmhost_get_maps(pb, c.h_cell_dofs.data(), cm.data(), nullptr, nullptr, nullptr, nullptr);
+  std::vector<int32_t> vert(npatch), dofs(sum_nj), perm(sum_nj), cells(size_t(npatch) << dim), col(npatch);
+  std::vector<int64_t> ptr(npatch + 1);
+  fdmhost_get_patches(pb, vert.data(), ptr.data(), dofs.data(), perm.data(), cells.data(), col.data());
+  fdmgpu::analyze_patches(c, npatch, vert.data(), ptr.data(), dofs.data(), perm.data(), cells.data());
+  const auto& L = c.L;
+  int64_t blocks8 = 0, diag_blocks = 0;
+  for (int t = 0; t < L.ntiles; ++t) {
+    const int b = __builtin_popcountll(uint64_t(L.tile_mask8[t]));
+    blocks8 += b;
+    if (L.tile_row[t] == L.tile_col[t]) diag_blocks += b;
+  }
+  const int64_t nnz_sep = L.nnz_L - int64_t(dim + 1) * L.nI;
+  std::printf("config %d p %d: n %d nI %d m %d nT %d tiles %d lead_cols %d\n", config, pp, L.n, L.nI, L.m, L.nT,
+              L.ntiles, L.lead_cols);
+  std::printf("nnz_L %lld (reference order %lld), separator nnz %lld, flops %lld (ref %lld), tile gemms %lld, pairs %zu\n",
+              (long long)L.nnz_L, (long long)L.nnz_L_reference, (long long)nnz_sep, (long long)L.flops_ref,
+              (long long)L.flops_reference, (long long)L.tile_gemms, L.pair_a.size());
+  const double rec = double(L.tile_poff8.back()) * 8;
+  std::printf("stored record bytes / patch %.0f (headers %.0f, 8x8 blocks %lld = %.0f B), nnz bytes %.0f: ratio %.4f\n",
+              rec, 128.0 * L.ntiles, (long long)blocks8, 512.0 * blocks8, 8.0 * nnz_sep, rec / (8.0 * nnz_sep));
+  std::printf("diag-tile blocks %lld; dense tile flops %.4e vs in-use %.4e (x%.2f)\n", (long long)diag_blocks,
+              2.0 * 64 * 64 * 64 * double(L.tile_gemms), 2.0 * double(L.flops_ref),
+              2.0 * 64 * 64 * 64 * double(L.tile_gemms) / (2.0 * double(L.flops_ref)));
+  fdmhost_problem_destroy(pb);
+  return 0;
+}
