@@ -73,7 +73,7 @@ void symbolic_tiles(PatchLayout& L, const std::function<void(int, std::vector<in
           tmark[size_t((k - L.nI) / T) * L.nT + (jj - L.nI) / T] = 1;
           ++nnz_sep;
           m16[size_t((k - L.nI) / 16) * (L.mpad / 16) + (jj - L.nI) / 16] = 1;
-          m8[size_t((k - L.nI) / 8) * (L.mpad / 8) + (jj - L.nI) / 8] = 1;
+          ++m8[size_t((k - L.nI) / 8) * (L.mpad / 8) + (jj - L.nI) / 8];  // strictly-lower entries per 8x8 block
           if (dbg) m32[size_t((k - L.nI) / 32) * (L.mpad / 32) + (jj - L.nI) / 32] = 1;
         }
       }
@@ -86,9 +86,34 @@ void symbolic_tiles(PatchLayout& L, const std::function<void(int, std::vector<in
   L.nnz_L_reference = L.nnz_L;
   L.flops_reference = L.flops_ref;
   for (int K = 0; K < L.nT; ++K) tmark[size_t(K) * L.nT + K] = 1;
+  if (dbg_env && dbg_env[0] == '2') {
+    // fill of the off-diagonal 8x8 blocks of the solve records, by tile column
+    std::vector<int64_t> hist(65, 0), pad_col(L.nT, 0), blk_col(L.nT, 0);
+    const int nb8 = L.mpad / 8;
+    for (int bi = 0; bi < nb8; ++bi)
+      for (int bj = 0; bj < bi; ++bj) {
+        const int v = m8[size_t(bi) * nb8 + bj];
+        if (!v) continue;
+        ++hist[v];
+        pad_col[bj / 8] += 64 - v;
+        ++blk_col[bj / 8];
+      }
+    int64_t pad = 0, blocks = 0;
+    for (int v = 1; v <= 64; ++v) {
+      pad += hist[v] * (64 - v);
+      blocks += hist[v];
+    }
+    std::fprintf(stderr, "[fdmgpu] off-diagonal 8x8 blocks %lld, padded slots %lld (%.2f %%)\n", (long long)blocks,
+                 (long long)pad, 100.0 * pad / (64.0 * blocks));
+    for (int v = 1; v <= 64; ++v)
+      if (hist[v]) std::fprintf(stderr, "[fdmgpu]   fill %2d: %lld blocks\n", v, (long long)hist[v]);
+    for (int K = 0; K < L.nT; ++K)
+      std::fprintf(stderr, "[fdmgpu]   tile column %d: %lld blocks, %lld padded slots\n", K, (long long)blk_col[K],
+                   (long long)pad_col[K]);
+  }
   if (dbg) {
     int64_t t64 = 0, t32 = 0, t16 = 0, t8 = 0;
-    for (auto v : m8) t8 += v;
+    for (auto v : m8) t8 += v != 0;
     std::fprintf(stderr, "[fdmgpu] blocks8 %lld (%.3f)\n", (long long)t8, double(nnz_sep + L.m) / (t8 * 64.0));
     for (auto v : tmark) t64 += v;
     for (auto v : m32) t32 += v;

@@ -68,6 +68,40 @@ int main(int argc, char** argv) {
   std::printf("diag-tile blocks %lld; dense tile flops %.4e vs in-use %.4e (x%.2f)\n", (long long)diag_blocks,
               2.0 * 64 * 64 * 64 * double(L.tile_gemms), 2.0 * double(L.flops_ref),
               2.0 * 64 * 64 * 64 * double(L.tile_gemms) / (2.0 * double(L.flops_ref)));
+  // DMMA work the factor kernels execute: tile_gemm_abt skips the 16-wide k
+  // panels where a warp's A rows (two 16-row sub-blocks) or B rows hold no
+  // structural nonzero (kernels/patch.cu); warp w: A sub-rows 2(w>>2), 2(w>>2)+1, B sub-row w&3.
+  auto gemm_flops = [&](int ma, int mb) {
+    double f = 0.0;
+    for (int w = 0; w < 8; ++w) {
+      const int wr = w >> 2, wc = w & 3;
+      for (int q = 0; q < 4; ++q) {
+        const bool a_on = (((ma >> ((2 * wr) * 4 + q)) | (ma >> ((2 * wr + 1) * 4 + q))) & 1) != 0;
+        const bool b_on = ((mb >> (wc * 4 + q)) & 1) != 0;
+        if (a_on && b_on) f += 2.0 * 32 * 16 * 16;
+      }
+    }
+    return f;
+  };
+  double exec = 0.0;
+  for (int t = 0; t < L.ntiles; ++t) {
+    for (int q = L.pair_ptr[t]; q < L.pair_ptr[t + 1]; ++q) exec += gemm_flops(L.tile_mask[L.pair_a[q]], L.tile_mask[L.pair_b[q]]);
+    const int K = L.tile_col[t];
+    if (L.tile_row[t] != K) exec += gemm_flops(L.tile_mask[t], L.tile_mask[L.col_start[K]]);  // trsm
+  }
+  if (std::getenv("PER_COLUMN")) {
+    for (int K = 0; K < L.nT; ++K) {
+      double f = 0.0;
+      int np = 0;
+      for (int t = L.col_start[K]; t < L.col_start[K + 1]; ++t) {
+        for (int q = L.pair_ptr[t]; q < L.pair_ptr[t + 1]; ++q, ++np) f += gemm_flops(L.tile_mask[L.pair_a[q]], L.tile_mask[L.pair_b[q]]);
+        if (L.tile_row[t] != K) f += gemm_flops(L.tile_mask[t], L.tile_mask[L.col_start[K]]);
+      }
+      std::printf("col %d tiles %d pairs %d exec_flops %.4e\n", K, L.col_start[K + 1] - L.col_start[K], np, f);
+    }
+  }
+  std::printf("executed DMMA flops / patch %.4e (x%.2f of in-use), diagonal POTRF+inverse tiles %d\n", exec,
+              exec / (2.0 * double(L.flops_ref)), L.nT);
   fdmhost_problem_destroy(pb);
   return 0;
 }
