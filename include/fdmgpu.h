@@ -68,6 +68,8 @@ typedef struct {
   int32_t separator_order;   /* 0 plane, 1 reference                              */
   int32_t pad2_;
   int64_t stream_bytes;      /* packed factor bytes streamed per sweep, all patches */
+  int64_t dmma_flops;        /* FP64 tensor-pipe flops the batched factorisation issues per patch
+                                (dense 64x64 tile GEMMs minus the skipped zero 16-wide panels) */
 } fdmgpu_layout;
 
 /* Operator ids for fdmgpu_apply. */

@@ -836,6 +836,9 @@ fdmgpu_status fdmgpu_set_patches(fdmgpu_handle h, int32_t npatch, const int32_t*
     c.tile_mask8.upload(L.tile_mask8, c.stream);
     c.tile_poff8.upload(L.tile_poff8, c.stream);
     c.tile_hdr.upload(L.tile_hdr, c.stream);
+    c.tile_bptr.upload(L.tile_bptr, c.stream);
+    c.tile_blk.upload(L.tile_blk, c.stream);
+    c.tile_ccol.upload(L.tile_ccol, c.stream);
     c.lead_diag.upload(L.lead_diag, c.stream);
     c.lead_trsm.upload(L.lead_trsm, c.stream);
     c.active.upload(L.active, c.stream);
@@ -1037,6 +1040,7 @@ fdmgpu_status fdmgpu_get_layout(fdmgpu_handle h, fdmgpu_layout* out) {
     L.flops_reference = c.L.flops_reference;
     L.separator_order = c.sep_order;
     L.stream_bytes = int64_t(c.L.tile_poff8.back()) * 8 * c.npatch;
+    L.dmma_flops = c.L.dmma_flops;
     *out = L;
   });
 }

@@ -15,6 +15,8 @@
 namespace fdmgpu {
 
 constexpr int kTile = 64;  // dense tile edge of the interface factor
+constexpr int kHdrBytes = 144;  // solve-record header: 2 x 64 sub-block indices + full / compact counts
+constexpr int kCompact = 10;    // doubles per compact 8x8 sub-block (8 row values + 8 column bytes + pad)
 
 struct Error : std::runtime_error {
   fdmgpu_status status;
@@ -73,9 +75,12 @@ struct PatchLayout {
   std::vector<int32_t> tile_poff8;            // stream record offset (doubles): header + sub-blocks
   int lead_cols = 0;                          // leading tile columns without updates (batched)
   std::vector<int32_t> lead_diag, lead_trsm;  // their diagonal tiles; (tile, diagonal tile) pairs
-  std::vector<uint8_t> tile_hdr;              // 128-byte record header per tile
+  std::vector<uint8_t> tile_hdr;              // kHdrBytes record header per tile
+  std::vector<int32_t> tile_bptr, tile_blk;   // per tile: its record's sub-blocks (bit bi*8 + bj), in record order
+  std::vector<int64_t> tile_ccol;             // per record sub-block: compact column bytes (0 for full blocks)
   std::vector<int32_t> active, active_ptr;    // per column: tiles the update kernel must visit
   int64_t nnz_L = 0, flops_ref = 0, tile_gemms = 0;          // order in use
+  int64_t dmma_flops = 0;                                   // tensor-pipe flops the factor kernels issue
   int64_t nnz_L_reference = 0, flops_reference = 0;         // reference patch_ordering
 };
 
@@ -150,7 +155,8 @@ struct Context {
   PatchLayout L;
   DevArray<int32_t> pdofs, lat, pos_of_lat, pcells, pg_ptr, pg_idx;
   DevArray<int32_t> tile_row, tile_col, col_start, pair_ptr, pair_a, pair_b, entries, tile_mask, active, tile_poff8, lead_diag, lead_trsm;
-  DevArray<int64_t> tile_mask8;
+  DevArray<int64_t> tile_mask8, tile_ccol;
+  DevArray<int32_t> tile_bptr, tile_blk;
   DevArray<uint8_t> tile_hdr;
   DevArray<double> corr, tiles, nK;
   // packed solve records in their own buffer when memory allows (packing then

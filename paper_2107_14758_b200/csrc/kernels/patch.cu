@@ -253,6 +253,17 @@ struct TileAcc {
   }
 };
 
+// 16-column panels of a 64x64 tile (column-major: 16 x 64 doubles, 8 KB,
+// contiguous) and the panels a 16x16 sub-block mask (bit bi*4 + bj) touches.
+constexpr int PANEL = 16 * T;
+__device__ __forceinline__ int panel_cols(int mask) {
+  int pm = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    if (mask & (0x1111 << q)) pm |= 1 << q;
+  return pm;
+}
+
 __device__ __forceinline__ void tile_gemm_abt(const double* __restrict__ A, const double* __restrict__ B, TileAcc& acc,
                                               int maskA = 0xffff, int maskB = 0xffff) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -420,23 +431,28 @@ __global__ void __launch_bounds__(kUpdThreads, 3) k_patch_update(PatchArgs a, in
   }
   __syncthreads();
   pdl_wait();  // operands of column K-1 come from the previous launch
+  // Only the 16-column panels both operands hold nonzeros in are copied (the
+  // GEMM skips the others): light columns' sparse tiles move half the bytes.
+  auto issue = [&](int s, int i) {
+    const int ia = pair_a[p0 + i], ib = pair_b[p0 + i];
+    const int pm = panel_cols(tile_mask[ia]) & panel_cols(tile_mask[ib]);
+    mbar_arrive_expect_tx(&full[s], __popc(pm) * 2 * PANEL * sizeof(double));
+    for (int q = 0; q < 4; ++q)
+      if ((pm >> q) & 1) {
+        bulk_g2s(buf + (2 * s) * TT + q * PANEL, base + size_t(ia) * TT + q * PANEL, PANEL * sizeof(double), &full[s]);
+        bulk_g2s(buf + (2 * s + 1) * TT + q * PANEL, base + size_t(ib) * TT + q * PANEL, PANEL * sizeof(double),
+                 &full[s]);
+      }
+  };
   if (tid == 0)
-    for (int s = 0; s < nst && s < np; ++s) {
-      mbar_arrive_expect_tx(&full[s], 2 * TT * sizeof(double));
-      bulk_g2s(buf + (2 * s) * TT, base + size_t(pair_a[p0 + s]) * TT, TT * sizeof(double), &full[s]);
-      bulk_g2s(buf + (2 * s + 1) * TT, base + size_t(pair_b[p0 + s]) * TT, TT * sizeof(double), &full[s]);
-    }
+    for (int s = 0; s < nst && s < np; ++s) issue(s, s);
   TileAcc acc = {};
   for (int i = 0; i < np; ++i) {
     const int s = i % nst;
     mbar_wait(&full[s], (i / nst) & 1);
     tile_gemm_abt(buf + (2 * s) * TT, buf + (2 * s + 1) * TT, acc, tile_mask[pair_a[p0 + i]], tile_mask[pair_b[p0 + i]]);
     __syncthreads();
-    if (tid == 0 && i + nst < np) {
-      mbar_arrive_expect_tx(&full[s], 2 * TT * sizeof(double));
-      bulk_g2s(buf + (2 * s) * TT, base + size_t(pair_a[p0 + i + nst]) * TT, TT * sizeof(double), &full[s]);
-      bulk_g2s(buf + (2 * s + 1) * TT, base + size_t(pair_b[p0 + i + nst]) * TT, TT * sizeof(double), &full[s]);
-    }
+    if (tid == 0 && i + nst < np) issue(s, i + nst);
   }
   double* ct = base + size_t(t) * TT;
   if (I != K) {
@@ -485,10 +501,14 @@ __global__ void __launch_bounds__(kUpdThreads) k_patch_trsm(PatchArgs a, int K, 
   }
   __syncthreads();
   pdl_wait();
-  if (tid == 0) {
-    mbar_arrive_expect_tx(&full[0], 2 * TT * sizeof(double));
-    bulk_g2s(Cs, base + size_t(t) * TT, TT * sizeof(double), &full[0]);
-    bulk_g2s(Ls, base + size_t(t0) * TT, TT * sizeof(double), &full[0]);
+  if (tid == 0) {  // the panels the GEMM reads (panel_cols of the operands)
+    const int pm = panel_cols(tile_mask[t]) & panel_cols(tile_mask[t0]);
+    mbar_arrive_expect_tx(&full[0], __popc(pm) * 2 * PANEL * sizeof(double));
+    for (int q = 0; q < 4; ++q)
+      if ((pm >> q) & 1) {
+        bulk_g2s(Cs + q * PANEL, base + size_t(t) * TT + q * PANEL, PANEL * sizeof(double), &full[0]);
+        bulk_g2s(Ls + q * PANEL, base + size_t(t0) * TT + q * PANEL, PANEL * sizeof(double), &full[0]);
+      }
   }
   mbar_wait(&full[0], 0);
   TileAcc acc = {};
@@ -507,18 +527,46 @@ __global__ void __launch_bounds__(kUpdThreads) k_patch_trsm(PatchArgs a, int K, 
 constexpr int kSolveConsumers = 8;                         // consumer warps
 constexpr int kSolveThreads = 32 * (kSolveConsumers + 1);  // + 1 TMA producer warp
 constexpr int SB8 = 64;   // doubles per packed 8x8 sub-block (solve stream)
-constexpr int kHdr = 16;  // doubles of the per-tile stream header (128 block-index bytes)
+constexpr int kHdr = kHdrBytes / 8;  // doubles of the per-tile stream header (context.hpp)
 constexpr int kSlot = TT + kHdr;  // ring slot: the densest possible record
 
-// Packed solve stream.  After factorisation every 64x64 tile is compacted in
-// place into one record: the 128-byte block-index header (tile_hdr) and the
-// structurally nonzero 8x8 sub-blocks (mask bit bi*8 + bj, packed in bit
-// order; sub-block layout below).  Exact: the dropped sub-blocks are
-// structural zeros of the factor, which the factorisation produces as exact 0.0.
-__global__ void k_patch_pack(int ntiles, const int64_t* __restrict__ mask8, const int32_t* __restrict__ poff8,
+// Packed solve stream.  After factorisation every 64x64 tile is compacted
+// into one record (layout.cpp): the kHdrBytes header (tile_hdr: record index
+// of each sub-block, row- and column-major, and the full / compact block
+// counts), the structurally nonzero full 8x8 sub-blocks (layout below), then
+// the compact sub-blocks (at most one structural entry per row: the 8 row
+// values and the 8 column bytes).  Exact: the dropped entries are structural
+// zeros of the factor.  `cur` is the dense swizzled tile, `blk` / `ccol` the
+// tile's record sub-blocks (bit bi*8 + bj) and compact column bytes.
+__device__ __forceinline__ void write_record(const double* __restrict__ cur, double* __restrict__ dst,
+                                             const uint8_t* __restrict__ hdr_t, const int32_t* __restrict__ blk,
+                                             const int64_t* __restrict__ ccol) {
+  if (threadIdx.x < kHdr) dst[threadIdx.x] = reinterpret_cast<const double*>(hdr_t)[threadIdx.x];
+  const int nf = reinterpret_cast<const int32_t*>(hdr_t + 128)[0], nc = reinterpret_cast<const int32_t*>(hdr_t + 128)[1];
+  dst += kHdr;
+  for (int d = threadIdx.x; d < nf * SB8; d += blockDim.x) {
+    const int bit = blk[d >> 6], w = d & 63;
+    const int bi = bit >> 3, bj = bit & 7, rr = w >> 3, cc = 2 * (((w >> 1) & 3) ^ ((rr >> 1) & 3)) + (w & 1);
+    dst[d] = cur[tsw(8 * bi + rr, 8 * bj + cc)];
+  }
+  dst += nf * SB8;
+  for (int d = threadIdx.x; d < nc * kCompact; d += blockDim.x) {
+    const int cb = d / kCompact, w = d - cb * kCompact;
+    const int bit = blk[nf + cb];
+    const long long cc = ccol[nf + cb];
+    double v = 0.0;
+    if (w < 8)
+      v = cur[tsw(8 * (bit >> 3) + w, 8 * (bit & 7) + int((cc >> (8 * w)) & 0xff))];
+    else if (w == 8)
+      v = __longlong_as_double(cc);
+    dst[d] = v;
+  }
+}
+
+__global__ void k_patch_pack(int ntiles, const int32_t* __restrict__ bptr, const int32_t* __restrict__ blk,
+                             const int64_t* __restrict__ ccol, const int32_t* __restrict__ poff8,
                              const uint8_t* __restrict__ hdr, double* __restrict__ tiles) {
   extern __shared__ __align__(128) double tile[];  // 2 x TT (double buffer, filled by TMA)
-  __shared__ int bits[64];
   __shared__ __align__(8) uint64_t bar[2];
   double* base = tiles + size_t(blockIdx.x) * ntiles * TT;
   auto load = [&](int t) {  // one thread
@@ -537,21 +585,9 @@ __global__ void k_patch_pack(int ntiles, const int64_t* __restrict__ mask8, cons
     // source region starts at (t+1)*TT >= the end of tile t's packed
     // destination, so the in-place compaction never overwrites unread data.
     if (threadIdx.x == 0 && t + 1 < ntiles) load(t + 1);
-    const double* cur = tile + (t & 1) * TT;
-    const unsigned long long m = static_cast<unsigned long long>(mask8[t]);
-    if (threadIdx.x < 64 && ((m >> threadIdx.x) & 1ull))
-      bits[__popcll(m & ((1ull << threadIdx.x) - 1ull))] = int(threadIdx.x);
     mbar_wait(&bar[t & 1], (t >> 1) & 1);
-    __syncthreads();  // bits ready
-    const int cnt = __popcll(m);
-    double* dst = base + size_t(poff8[t]);
-    if (threadIdx.x < kHdr) dst[threadIdx.x] = reinterpret_cast<const double*>(hdr + size_t(t) * 8 * kHdr)[threadIdx.x];
-    dst += kHdr;
-    for (int d = threadIdx.x; d < cnt * SB8; d += blockDim.x) {
-      const int bit = bits[d >> 6], w = d & 63;
-      const int bi = bit >> 3, bj = bit & 7, rr = w >> 3, cc = 2 * (((w >> 1) & 3) ^ ((rr >> 1) & 3)) + (w & 1);
-      dst[d] = cur[tsw(8 * bi + rr, 8 * bj + cc)];
-    }
+    write_record(tile + (t & 1) * TT, base + size_t(poff8[t]), hdr + size_t(t) * kHdrBytes, blk + bptr[t],
+                 ccol + bptr[t]);
     __syncthreads();
   }
 }
@@ -560,28 +596,20 @@ __global__ void k_patch_pack(int ntiles, const int64_t* __restrict__ mask8, cons
 // every patch (blockIdx.y): launched per tile column on a side stream while
 // the factorisation continues, so the packing hides under the compute-bound
 // updates (the dense tiles stay intact as update operands).
-__global__ void __launch_bounds__(256) k_patch_pack_cols(int t0, int ntiles, const int64_t* __restrict__ mask8,
+__global__ void __launch_bounds__(256) k_patch_pack_cols(int t0, int ntiles, const int32_t* __restrict__ bptr,
+                                                        const int32_t* __restrict__ blk,
+                                                        const int64_t* __restrict__ ccol,
                                                         const int32_t* __restrict__ poff8,
                                                         const uint8_t* __restrict__ hdr,
                                                         const double* __restrict__ tiles, double* __restrict__ packed,
                                                         int64_t pstride) {
   __shared__ __align__(16) double cur[TT];
-  __shared__ int bits[64];
   const int t = t0 + blockIdx.x, j = blockIdx.y;
   const double2* src = reinterpret_cast<const double2*>(tiles + (size_t(j) * ntiles + t) * TT);
   for (int i = threadIdx.x; i < TT / 2; i += blockDim.x) reinterpret_cast<double2*>(cur)[i] = __ldcs(src + i);
-  const unsigned long long m = static_cast<unsigned long long>(mask8[t]);
-  if (threadIdx.x < 64 && ((m >> threadIdx.x) & 1ull)) bits[__popcll(m & ((1ull << threadIdx.x) - 1ull))] = int(threadIdx.x);
   __syncthreads();
-  const int cnt = __popcll(m);
-  double* dst = packed + size_t(j) * pstride + poff8[t];
-  if (threadIdx.x < kHdr) dst[threadIdx.x] = reinterpret_cast<const double*>(hdr + size_t(t) * 8 * kHdr)[threadIdx.x];
-  dst += kHdr;
-  for (int d = threadIdx.x; d < cnt * SB8; d += blockDim.x) {
-    const int bit = bits[d >> 6], w = d & 63;
-    const int bi = bit >> 3, bj = bit & 7, rr = w >> 3, cc = 2 * (((w >> 1) & 3) ^ ((rr >> 1) & 3)) + (w & 1);
-    dst[d] = cur[tsw(8 * bi + rr, 8 * bj + cc)];
-  }
+  write_record(cur, packed + size_t(j) * pstride + poff8[t], hdr + size_t(t) * kHdrBytes, blk + bptr[t],
+               ccol + bptr[t]);
 }
 
 // Packed 8x8 sub-block layout: row-major, element (r, c) at
@@ -604,11 +632,22 @@ __device__ __forceinline__ void ld_row8(const double* __restrict__ B, int r, dou
   }
 }
 
-// Sub-block (bi, bj) of a stream record: header byte -> packed index.
-__device__ __forceinline__ const double* rec_block(const double* rec, const double* zblk, unsigned long long hw,
-                                                   int e) {
+// Row r of sub-block e of a stream record (header word hw: its record index
+// byte): a full block (four 16-byte loads), the shared zero block, or a
+// compact block expanded in registers (one value at its column byte).
+__device__ __forceinline__ void ld_blk_row(const double* __restrict__ rec, const double* __restrict__ zblk,
+                                           unsigned long long hw, int e, int r, double v[8]) {
   const unsigned idx = unsigned(hw >> (8 * e)) & 0xffu;
-  return idx == 0xffu ? zblk : rec + kHdr + idx * SB8;
+  if (idx < 0x80u || idx == 0xffu) {
+    ld_row8(idx == 0xffu ? zblk : rec + kHdr + idx * SB8, r, v);
+  } else {
+    const int nf = reinterpret_cast<const int*>(rec)[32];  // header byte 128
+    const double* cb = rec + kHdr + nf * SB8 + (idx & 0x7fu) * kCompact;
+    const double val = cb[r];
+    const int col = reinterpret_cast<const unsigned char*>(cb + 8)[r];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = k == col ? val : 0.0;
+  }
 }
 
 // Forward, rows map: lane (r, g) owns block-rows g and 7 - g (two sub-block
@@ -628,7 +667,7 @@ __device__ __forceinline__ void tile_fwd(const double* __restrict__ rec, const d
 #pragma unroll
     for (int jj = 0; jj < 2; ++jj) {
       double v[8];
-      ld_row8(rec_block(rec, zblk, jj ? hw1 : hw0, bj), r, v);
+      ld_blk_row(rec, zblk, jj ? hw1 : hw0, bj, r, v);
 #pragma unroll
       for (int k = 0; k < 8; ++k) a[jj][k & 3] = fma(v[k], x[8 * bj + k], a[jj][k & 3]);
     }
@@ -648,7 +687,7 @@ __device__ __forceinline__ void tile_bwd(const double* __restrict__ rec, const d
 #pragma unroll
     for (int bi = 0; bi < 8; ++bi) {
       double v[8];
-      ld_row8(rec_block(rec, zblk, hw, bi), r, v);
+      ld_blk_row(rec, zblk, hw, bi, r, v);
 #pragma unroll
       for (int k = 0; k < 8; ++k) acc[jj][k] = fma(v[k], yv[bi], acc[jj][k]);
     }
@@ -1436,9 +1475,9 @@ void launch_patch_pack_col(Context& c, int K) {
   const int t0 = c.L.col_start[K], n = c.L.col_start[K + 1] - t0;
   FDM_CUDA(cudaEventRecord(c.pack_ev, c.stream));
   FDM_CUDA(cudaStreamWaitEvent(c.pack_stream, c.pack_ev, 0));
-  k_patch_pack_cols<<<dim3(n, c.npatch), 256, 0, c.pack_stream>>>(t0, c.L.ntiles, c.tile_mask8.p, c.tile_poff8.p,
-                                                                  c.tile_hdr.p, c.tiles.p, c.packed.p,
-                                                                  int64_t(c.L.tile_poff8.back()));
+  k_patch_pack_cols<<<dim3(n, c.npatch), 256, 0, c.pack_stream>>>(t0, c.L.ntiles, c.tile_bptr.p, c.tile_blk.p,
+                                                                  c.tile_ccol.p, c.tile_poff8.p, c.tile_hdr.p,
+                                                                  c.tiles.p, c.packed.p, int64_t(c.L.tile_poff8.back()));
   FDM_LAUNCH_CHECK(c);
 }
 
@@ -1452,7 +1491,9 @@ void launch_patch_pack_join(Context& c) {
 void launch_patch_pack(Context& c) {
   KernelTimer timer(c, 1);
   FDM_CUDA(cudaFuncSetAttribute(k_patch_pack, cudaFuncAttributeMaxDynamicSharedMemorySize, int(2 * TT * sizeof(double))));
-  k_patch_pack<<<c.npatch, 512, 2 * TT * sizeof(double), c.stream>>>(c.L.ntiles, c.tile_mask8.p, c.tile_poff8.p, c.tile_hdr.p, c.tiles.p);
+  k_patch_pack<<<c.npatch, 512, 2 * TT * sizeof(double), c.stream>>>(c.L.ntiles, c.tile_bptr.p, c.tile_blk.p,
+                                                                     c.tile_ccol.p, c.tile_poff8.p, c.tile_hdr.p,
+                                                                     c.tiles.p);
   FDM_LAUNCH_CHECK(c);
 }
 

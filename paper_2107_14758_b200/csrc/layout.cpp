@@ -56,6 +56,8 @@ void symbolic_tiles(PatchLayout& L, const std::function<void(int, std::vector<in
   const bool dbg = dbg_env && dbg_env[0] == '1';
   std::vector<uint8_t> m32(dbg ? size_t(L.mpad / 32) * (L.mpad / 32) : 0), m16(size_t(L.mpad / 16) * (L.mpad / 16), 0);
   std::vector<uint8_t> m8(size_t(L.mpad / 8) * (L.mpad / 8), 0);
+  const bool dbg3 = dbg_env && dbg_env[0] == '3';
+  std::vector<uint64_t> bits8(m8.size(), 0);  // strictly-lower element mask per 8x8 block
   int64_t nnz_sep = 0;
   std::vector<int> nb;
   for (int k = 0; k < L.n; ++k) {
@@ -74,6 +76,8 @@ void symbolic_tiles(PatchLayout& L, const std::function<void(int, std::vector<in
           ++nnz_sep;
           m16[size_t((k - L.nI) / 16) * (L.mpad / 16) + (jj - L.nI) / 16] = 1;
           ++m8[size_t((k - L.nI) / 8) * (L.mpad / 8) + (jj - L.nI) / 8];  // strictly-lower entries per 8x8 block
+          bits8[size_t((k - L.nI) / 8) * (L.mpad / 8) + (jj - L.nI) / 8] |= uint64_t(1)
+                                                                          << (((k - L.nI) % 8) * 8 + (jj - L.nI) % 8);
           if (dbg) m32[size_t((k - L.nI) / 32) * (L.mpad / 32) + (jj - L.nI) / 32] = 1;
         }
       }
@@ -86,6 +90,43 @@ void symbolic_tiles(PatchLayout& L, const std::function<void(int, std::vector<in
   L.nnz_L_reference = L.nnz_L;
   L.flops_reference = L.flops_ref;
   for (int K = 0; K < L.nT; ++K) tmark[size_t(K) * L.nT + K] = 1;
+  if (dbg3) {
+    // pattern classes of the partially filled off-diagonal 8x8 blocks
+    const int nb8 = L.mpad / 8;
+    int64_t onerow = 0, onecol = 0, perrow1 = 0, percol1 = 0, other = 0, full = 0, otherslots = 0;
+    for (int bi = 0; bi < nb8; ++bi)
+      for (int bj = 0; bj < bi; ++bj) {
+        const uint64_t b = bits8[size_t(bi) * nb8 + bj];
+        if (!b) continue;
+        if (b == ~uint64_t(0)) {
+          ++full;
+          continue;
+        }
+        int rows = 0, cols = 0, maxr = 0, maxc = 0;
+        for (int r = 0; r < 8; ++r) {
+          const int n = __builtin_popcountll((b >> (8 * r)) & 0xff);
+          rows += n > 0;
+          maxr = std::max(maxr, n);
+        }
+        for (int c = 0; c < 8; ++c) {
+          int n = 0;
+          for (int r = 0; r < 8; ++r) n += (b >> (8 * r + c)) & 1;
+          cols += n > 0;
+          maxc = std::max(maxc, n);
+        }
+        if (rows == 1) ++onerow;
+        else if (cols == 1) ++onecol;
+        else if (maxr == 1) ++perrow1;
+        else if (maxc == 1) ++percol1;
+        else {
+          ++other;
+          otherslots += 64 - __builtin_popcountll(b);
+        }
+      }
+    std::fprintf(stderr, "[fdmgpu] 8x8 blocks: full %lld, one row %lld, one column %lld, <=1 per row %lld, <=1 per column %lld, other %lld (%lld padded slots)\n",
+                 (long long)full, (long long)onerow, (long long)onecol, (long long)perrow1, (long long)percol1,
+                 (long long)other, (long long)otherslots);
+  }
   if (dbg_env && dbg_env[0] == '2') {
     // fill of the off-diagonal 8x8 blocks of the solve records, by tile column
     std::vector<int64_t> hist(65, 0), pad_col(L.nT, 0), blk_col(L.nT, 0);
@@ -150,29 +191,68 @@ void symbolic_tiles(PatchLayout& L, const std::function<void(int, std::vector<in
     L.tile_mask[t] = mask;
   }
   // 8x8 sub-block masks (bit bi*8 + bj) of the packed solve stream, same rule.
+  // Stream record of a tile: a 144-byte header -- the record index of every
+  // sub-block, row-major then column-major (0xff = structurally zero, < 0x80 a
+  // full 8x8 block, 0x80 | c the c-th compact block), then the full-block count
+  // F and compact count C -- followed by F full blocks (64 doubles) and C
+  // compact blocks (10 doubles: one value per row, then the 8 column bytes).
+  // Compact blocks are the off-diagonal sub-blocks with at most one structural
+  // entry per row (facet couplings across a shared axis that runs fast in one
+  // facet's numbering: one column, or a shifted diagonal): 8 values instead of
+  // 64.  FDMGPU_COMPACT=0 keeps every sub-block full.
+  const char* cenv = std::getenv("FDMGPU_COMPACT");
+  const bool compact = !(cenv && cenv[0] == '0');
   const int nb8 = L.mpad / 8;
   L.tile_mask8.assign(L.ntiles, 0);
   L.tile_poff8.assign(L.ntiles + 1, 0);
-  L.tile_hdr.assign(size_t(L.ntiles) * 128, 0);
+  L.tile_hdr.assign(size_t(L.ntiles) * kHdrBytes, 0);
+  L.tile_bptr.assign(L.ntiles + 1, 0);
+  L.tile_blk.clear();
+  L.tile_ccol.clear();
   for (int t = 0; t < L.ntiles; ++t) {
     const int I = L.tile_row[t], K = L.tile_col[t];
-    uint64_t mask = 0;
+    uint64_t mask = 0, cmask = 0;
     for (int bi = 0; bi < 8; ++bi)
       for (int bj = 0; bj < 8; ++bj) {
-        const bool on = I == K ? bi >= bj : m8[size_t(8 * I + bi) * nb8 + (8 * K + bj)] != 0;
-        if (on) mask |= uint64_t(1) << (bi * 8 + bj);
+        const size_t b8 = size_t(8 * I + bi) * nb8 + (8 * K + bj);
+        const bool on = I == K ? bi >= bj : m8[b8] != 0;
+        if (!on) continue;
+        mask |= uint64_t(1) << (bi * 8 + bj);
+        if (compact && I != K) {
+          bool sparse_rows = true;
+          for (int r = 0; r < 8; ++r) sparse_rows = sparse_rows && __builtin_popcountll((bits8[b8] >> (8 * r)) & 0xff) <= 1;
+          if (sparse_rows) cmask |= uint64_t(1) << (bi * 8 + bj);
+        }
       }
     L.tile_mask8[t] = int64_t(mask);
-    // stream record: 16-double header (block index per sub-block, row-major
-    // then column-major, 0xff = structurally zero) + the present sub-blocks
-    uint8_t* hr = &L.tile_hdr[size_t(t) * 128];
-    int q = 0;
-    for (int b = 0; b < 64; ++b) {
-      const uint8_t v = (mask >> b) & 1 ? uint8_t(q++) : uint8_t(0xff);
-      hr[b] = v;                              // [bi*8 + bj]
-      hr[64 + (b & 7) * 8 + (b >> 3)] = v;    // [bj*8 + bi]
-    }
-    L.tile_poff8[t + 1] = L.tile_poff8[t] + 16 + 64 * q;
+    uint8_t* hr = &L.tile_hdr[size_t(t) * kHdrBytes];
+    int nf = 0, nc = 0;
+    for (int pass = 0; pass < 2; ++pass)  // full blocks first, then compact ones
+      for (int b = 0; b < 64; ++b) {
+        if (!((mask >> b) & 1) || ((cmask >> b) & 1) != uint64_t(pass)) continue;
+        const uint8_t v = pass ? uint8_t(0x80 | nc++) : uint8_t(nf++);
+        hr[b] = v;                            // [bi*8 + bj]
+        hr[64 + (b & 7) * 8 + (b >> 3)] = v;  // [bj*8 + bi]
+        int64_t cc = 0;
+        if (pass) {  // column of each row's entry (0 for an empty row: its values are zero)
+          const uint64_t e = bits8[size_t(8 * I + (b >> 3)) * nb8 + (8 * K + (b & 7))];
+          for (int r = 0; r < 8; ++r) {
+            const unsigned row = unsigned(e >> (8 * r)) & 0xffu;
+            cc |= int64_t(row ? __builtin_ctz(row) : 0) << (8 * r);
+          }
+        }
+        L.tile_blk.push_back(b);
+        L.tile_ccol.push_back(cc);
+      }
+    for (int b = 0; b < 64; ++b)
+      if (!((mask >> b) & 1)) {
+        hr[b] = 0xff;
+        hr[64 + (b & 7) * 8 + (b >> 3)] = 0xff;
+      }
+    reinterpret_cast<int32_t*>(hr + 128)[0] = nf;
+    reinterpret_cast<int32_t*>(hr + 128)[1] = nc;
+    L.tile_bptr[t + 1] = int32_t(L.tile_blk.size());
+    L.tile_poff8[t + 1] = L.tile_poff8[t] + kHdrBytes / 8 + 64 * nf + kCompact * nc;
     // the in-place compaction (k_patch_pack) needs every packed prefix to end
     // before the next unpacked tile starts
     if (int64_t(L.tile_poff8[t + 1]) > int64_t(t + 1) * T * T)
@@ -183,7 +263,14 @@ void symbolic_tiles(PatchLayout& L, const std::function<void(int, std::vector<in
     const int I = L.tile_row[t], K = L.tile_col[t];
     for (int J = 0; J < K; ++J) {
       const int a = tidx[size_t(I) * L.nT + J], bb = tidx[size_t(K) * L.nT + J];
-      if (a >= 0 && bb >= 0) {
+      // a pair contributes only through the 16-column panels both tiles occupy
+      auto panels = [&](int m) {
+        int pm = 0;
+        for (int q = 0; q < 4; ++q)
+          if (m & (0x1111 << q)) pm |= 1 << q;
+        return pm;
+      };
+      if (a >= 0 && bb >= 0 && (panels(L.tile_mask[a]) & panels(L.tile_mask[bb]))) {
         L.pair_a.push_back(a);
         L.pair_b.push_back(bb);
       }
@@ -192,6 +279,28 @@ void symbolic_tiles(PatchLayout& L, const std::function<void(int, std::vector<in
     if (I != K) ++L.tile_gemms;  // TRSM against the diagonal inverse
   }
   L.tile_gemms += int64_t(L.pair_a.size());
+  // FP64 tensor-pipe work the factor kernels issue per patch: tile_gemm_abt
+  // (kernels/patch.cu) skips the 16-wide k panels where a warp's A rows (two
+  // 16-row sub-blocks) or its B rows hold no structural nonzero.
+  auto gemm_flops = [&](int ma, int mb) {
+    int64_t f = 0;
+    for (int w = 0; w < 8; ++w) {
+      const int wr = w >> 2, wc = w & 3;
+      for (int q = 0; q < 4; ++q) {
+        const bool a_on = (((ma >> ((2 * wr) * 4 + q)) | (ma >> ((2 * wr + 1) * 4 + q))) & 1) != 0;
+        const bool b_on = ((mb >> (wc * 4 + q)) & 1) != 0;
+        if (a_on && b_on) f += 2 * 32 * 16 * 16;
+      }
+    }
+    return f;
+  };
+  L.dmma_flops = 0;
+  for (int t = 0; t < L.ntiles; ++t) {
+    for (int q = L.pair_ptr[t]; q < L.pair_ptr[t + 1]; ++q)
+      L.dmma_flops += gemm_flops(L.tile_mask[L.pair_a[q]], L.tile_mask[L.pair_b[q]]);
+    const int K = L.tile_col[t];
+    if (L.tile_row[t] != K) L.dmma_flops += gemm_flops(L.tile_mask[t], L.tile_mask[L.col_start[K]]);  // trsm
+  }
   // Update launches only visit tiles with work: the diagonal tile (factor +
   // invert) and off-diagonal tiles with at least one update pair.
   L.active_ptr.assign(1, 0);

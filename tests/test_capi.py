@@ -53,3 +53,26 @@ def test_status_strings(pkg):
     lib = pkg.lib()
     lib.fdmgpu_status_string.restype = ctypes.c_char_p
     assert lib.fdmgpu_status_string(2) == b"matrix not SPD"
+
+
+def test_python_structs_match_the_header(pkg, tmp_path):
+    """The ctypes mirrors of fdmgpu_layout / fdmgpu_krylov_report have the C
+    layout of include/fdmgpu.h (size and every field offset, compiled here)."""
+    import subprocess
+
+    checks = []
+    for cname, py in (("fdmgpu_layout", pkg.Layout), ("fdmgpu_krylov_report", pkg.KrylovReport)):
+        checks.append(f'printf("{cname} %zu\\n", sizeof({cname}));')
+        for f, _ in py._fields_:
+            checks.append(f'printf("{cname}.{f} %zu\\n", offsetof({cname}, {f}));')
+    src = tmp_path / "layout.c"
+    src.write_text('#include <stddef.h>\n#include <stdio.h>\n#include "fdmgpu.h"\nint main(void) {\n' +
+                   "\n".join(checks) + "\nreturn 0;\n}\n")
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    got = dict(line.split() for line in subprocess.run([str(exe)], capture_output=True, text=True,
+                                                       check=True).stdout.splitlines())
+    for cname, py in (("fdmgpu_layout", pkg.Layout), ("fdmgpu_krylov_report", pkg.KrylovReport)):
+        assert int(got[cname]) == ctypes.sizeof(py), cname
+        for f, _ in py._fields_:
+            assert int(got[f"{cname}.{f}"]) == getattr(py, f).offset, (cname, f)

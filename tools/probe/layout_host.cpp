@@ -97,7 +97,16 @@ int main(int argc, char** argv) {
         for (int q = L.pair_ptr[t]; q < L.pair_ptr[t + 1]; ++q, ++np) f += gemm_flops(L.tile_mask[L.pair_a[q]], L.tile_mask[L.pair_b[q]]);
         if (L.tile_row[t] != K) f += gemm_flops(L.tile_mask[t], L.tile_mask[L.col_start[K]]);
       }
-      std::printf("col %d tiles %d pairs %d exec_flops %.4e\n", K, L.col_start[K + 1] - L.col_start[K], np, f);
+      // operand bytes: full tiles vs only the 16-column panels both operands hold nonzeros in
+      double full = 0, panel = 0;
+      auto colmask = [&](int m) { int cm = 0; for (int q = 0; q < 4; ++q) for (int b = 0; b < 4; ++b) if ((m >> (b * 4 + q)) & 1) cm |= 1 << q; return cm; };
+      for (int t = L.col_start[K]; t < L.col_start[K + 1]; ++t)
+        for (int q = L.pair_ptr[t]; q < L.pair_ptr[t + 1]; ++q) {
+          full += 65536;
+          panel += 16384.0 * __builtin_popcount(colmask(L.tile_mask[L.pair_a[q]]) & colmask(L.tile_mask[L.pair_b[q]]));
+        }
+      std::printf("col %d tiles %d pairs %d exec_flops %.4e operand MB/patch full %.2f panels %.2f\n", K,
+                  L.col_start[K + 1] - L.col_start[K], np, f, full / 1e6, panel / 1e6);
     }
   }
   std::printf("executed DMMA flops / patch %.4e (x%.2f of in-use), diagonal POTRF+inverse tiles %d\n", exec,
