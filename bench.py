@@ -568,6 +568,11 @@ def run_ours(args):
                 "pcg_iterations": e["pcg"]["iterations"], "e2e": e["e2e"]["value"]}
         except Exception as ex:  # reported, not fatal for the headline line
             result["elasticity"] = {"failed": str(ex)}
+        # the DG half of SURVEY.md 8(f)3: SIPG two-level solver, 3D 4^3 cells, DG Q5
+        try:
+            result["sipg"] = sipg_measure("3,4,5", min(args.steps, 20), args.warmup)
+        except Exception as ex:
+            result["sipg"] = {"failed": str(ex)}
     replicas.barrier()
     replicas.finalize()
     if rank == 0:
@@ -720,6 +725,53 @@ def elastic_measure(spec, steps, warmup, no_cpu):
     return result
 
 
+def sipg_measure(spec, steps, warmup):
+    """SIPG-DG workload (src/sipg.cpp): the two-level DG solver of
+    tests/test_sipg.cpp:184-197 on dq_space(unit DIM-cube, N^DIM cells, Q_P), weak
+    Dirichlet, default penalty; one step = one relaxation apply (S, the DG vertex-star
+    patch solves with (2P+2)^DIM DOFs each, S^T), device-resident vectors."""
+    import torch
+
+    import paper_2107_14758_b200 as pkg
+
+    dim, n, p = (int(v) for v in spec.split(","))
+    dev = torch.device("cuda", 0)
+    stream = torch.cuda.current_stream(dev)
+    prob = pkg.Problem.sipg(dim, n, p)
+    sol = pkg.Solver(prob, device=0, stream=stream)
+    L = sol.layout()
+
+    def ev_time(fn, reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record(stream)
+        for _ in range(reps):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps
+
+    factor_ms = min(ev_time(sol.factor, 1) for _ in range(2))
+    r = torch.from_numpy(prob.rhs()).to(dev)
+    z = torch.empty_like(r)
+    for _ in range(max(warmup, 3)):
+        sol.smooth(r, z)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    ms = 0.0
+    for _ in range(steps):  # L2 flushed before every step (the DG factors of small meshes fit in L2)
+        flush.zero_()
+        ms += ev_time(lambda: sol.smooth(r, z), 1)
+    ms /= steps
+    a_ms = ev_time(lambda: sol.apply_A(r, z), max(5, min(steps, 50)))
+    cal = sol.calibrate_damping()
+    _, rep = sol.pcg(r, rtol=1e-8, maxit=200)
+    return {"workload": f"SIPG DG (src/sipg.cpp) dim {dim}, {n}^{dim} cells, DG Q{p}, eta (p+1)(p+d), "
+                        f"{prob.npatches} vertex stars of {L['n']} DOFs", "value": prob.nfree / (ms * 1e-3) / 1e9,
+            "unit": "GDOF/s", "ms_per_step": ms, "l2": "flushed before every step", "apply_A_ms": a_ms,
+            "factor_ms": factor_ms, "factor_nnz_per_patch": L["nnz_L"],
+            "pcg": {"iterations": rep["iterations"], "converged": rep["converged"], "omega": cal["omega"]}}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -732,13 +784,17 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-pcg", action="store_true")
     ap.add_argument("--elastic", default=None, help="DIM,N,P,LAMBDA: linear-elasticity workload (SURVEY.md 8(f)3)")
-    ap.add_argument("--no-elastic", action="store_true", help="skip the elasticity sub-line of the default run")
+    ap.add_argument("--no-elastic", action="store_true", help="skip the elasticity and SIPG sub-lines of the default run")
+    ap.add_argument("--sipg", default=None, help="DIM,N,P: SIPG-DG workload (SURVEY.md 8(f)3)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         return run_reference(args)
     if args.elastic:
         return run_elastic(args)
+    if args.sipg:
+        print(json.dumps(sipg_measure(args.sipg, args.steps, args.warmup)), flush=True)
+        return 0
     return run_ours(args)
 
 

@@ -1,6 +1,7 @@
-"""Generates tests/golden/elastic_table2.json and dg_two_level.json from the oracle
-(the committed fixtures freeze the oracle's elasticity / SIPG results; the reference
-tests pin them only to +-20 % / upper bounds)."""
+"""Generates tests/golden/variants/elastic_table2.json and
+tests/golden/variants/dg_two_level.json from the oracle.  These are oracle
+regression snapshots (they freeze the oracle's elasticity / SIPG results; the
+reference tests pin those only to +-20 % / upper bounds), not reference output."""
 import json
 import os
 import sys
