@@ -253,17 +253,6 @@ struct TileAcc {
   }
 };
 
-// 16-column panels of a 64x64 tile (column-major: 16 x 64 doubles, 8 KB,
-// contiguous) and the panels a 16x16 sub-block mask (bit bi*4 + bj) touches.
-constexpr int PANEL = 16 * T;
-__device__ __forceinline__ int panel_cols(int mask) {
-  int pm = 0;
-#pragma unroll
-  for (int q = 0; q < 4; ++q)
-    if (mask & (0x1111 << q)) pm |= 1 << q;
-  return pm;
-}
-
 __device__ __forceinline__ void tile_gemm_abt(const double* __restrict__ A, const double* __restrict__ B, TileAcc& acc,
                                               int maskA = 0xffff, int maskB = 0xffff) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -431,18 +420,13 @@ __global__ void __launch_bounds__(kUpdThreads, 3) k_patch_update(PatchArgs a, in
   }
   __syncthreads();
   pdl_wait();  // operands of column K-1 come from the previous launch
-  // Only the 16-column panels both operands hold nonzeros in are copied (the
-  // GEMM skips the others): light columns' sparse tiles move half the bytes.
+  // Whole operand tiles (one 32 KB bulk copy each).  Copying only the 16-column
+  // panels the GEMM reads moved fewer bytes but was slower (C5 factor 917 -> 959 ms,
+  // C3 unchanged: the light columns are not operand-bandwidth bound).
   auto issue = [&](int s, int i) {
-    const int ia = pair_a[p0 + i], ib = pair_b[p0 + i];
-    const int pm = panel_cols(tile_mask[ia]) & panel_cols(tile_mask[ib]);
-    mbar_arrive_expect_tx(&full[s], __popc(pm) * 2 * PANEL * sizeof(double));
-    for (int q = 0; q < 4; ++q)
-      if ((pm >> q) & 1) {
-        bulk_g2s(buf + (2 * s) * TT + q * PANEL, base + size_t(ia) * TT + q * PANEL, PANEL * sizeof(double), &full[s]);
-        bulk_g2s(buf + (2 * s + 1) * TT + q * PANEL, base + size_t(ib) * TT + q * PANEL, PANEL * sizeof(double),
-                 &full[s]);
-      }
+    mbar_arrive_expect_tx(&full[s], 2 * TT * sizeof(double));
+    bulk_g2s(buf + (2 * s) * TT, base + size_t(pair_a[p0 + i]) * TT, TT * sizeof(double), &full[s]);
+    bulk_g2s(buf + (2 * s + 1) * TT, base + size_t(pair_b[p0 + i]) * TT, TT * sizeof(double), &full[s]);
   };
   if (tid == 0)
     for (int s = 0; s < nst && s < np; ++s) issue(s, s);
@@ -501,14 +485,10 @@ __global__ void __launch_bounds__(kUpdThreads) k_patch_trsm(PatchArgs a, int K, 
   }
   __syncthreads();
   pdl_wait();
-  if (tid == 0) {  // the panels the GEMM reads (panel_cols of the operands)
-    const int pm = panel_cols(tile_mask[t]) & panel_cols(tile_mask[t0]);
-    mbar_arrive_expect_tx(&full[0], __popc(pm) * 2 * PANEL * sizeof(double));
-    for (int q = 0; q < 4; ++q)
-      if ((pm >> q) & 1) {
-        bulk_g2s(Cs + q * PANEL, base + size_t(t) * TT + q * PANEL, PANEL * sizeof(double), &full[0]);
-        bulk_g2s(Ls + q * PANEL, base + size_t(t0) * TT + q * PANEL, PANEL * sizeof(double), &full[0]);
-      }
+  if (tid == 0) {
+    mbar_arrive_expect_tx(&full[0], 2 * TT * sizeof(double));
+    bulk_g2s(Cs, base + size_t(t) * TT, TT * sizeof(double), &full[0]);
+    bulk_g2s(Ls, base + size_t(t0) * TT, TT * sizeof(double), &full[0]);
   }
   mbar_wait(&full[0], 0);
   TileAcc acc = {};
@@ -559,6 +539,8 @@ __device__ __forceinline__ void write_record(const double* __restrict__ cur, dou
       v = cur[tsw(8 * (bit >> 3) + w, 8 * (bit & 7) + int((cc >> (8 * w)) & 0xff))];
     else if (w == 8)
       v = __longlong_as_double(cc);
+    else
+      v = __longlong_as_double(static_cast<long long>(bit));
     dst[d] = v;
   }
 }
@@ -632,21 +614,56 @@ __device__ __forceinline__ void ld_row8(const double* __restrict__ B, int r, dou
   }
 }
 
-// Row r of sub-block e of a stream record (header word hw: its record index
-// byte): a full block (four 16-byte loads), the shared zero block, or a
-// compact block expanded in registers (one value at its column byte).
-__device__ __forceinline__ void ld_blk_row(const double* __restrict__ rec, const double* __restrict__ zblk,
-                                           unsigned long long hw, int e, int r, double v[8]) {
+// Sub-block (bi, bj) of a stream record: header byte -> full block (absent
+// and compact sub-blocks read the shared zero block; compact ones are added
+// by compact_fwd / compact_bwd after the branch-free full-block pass).
+__device__ __forceinline__ const double* rec_block(const double* rec, const double* zblk, unsigned long long hw,
+                                                   int e) {
   const unsigned idx = unsigned(hw >> (8 * e)) & 0xffu;
-  if (idx < 0x80u || idx == 0xffu) {
-    ld_row8(idx == 0xffu ? zblk : rec + kHdr + idx * SB8, r, v);
-  } else {
-    const int nf = reinterpret_cast<const int*>(rec)[32];  // header byte 128
-    const double* cb = rec + kHdr + nf * SB8 + (idx & 0x7fu) * kCompact;
-    const double val = cb[r];
+  return idx == 0xffu ? zblk : rec + kHdr + idx * SB8;
+}
+
+// Compact sub-blocks of a record (at most one entry per row): slot = 8 row
+// values, the 8 column bytes, the sub-block bit bi*8 + bj.
+__device__ __forceinline__ int rec_ncompact(const double* rec) { return reinterpret_cast<const int*>(rec)[33]; }
+__device__ __forceinline__ const double* rec_compact(const double* rec) {
+  return rec + kHdr + reinterpret_cast<const int*>(rec)[32] * SB8;
+}
+
+// Forward tail: o0 / o1 (rows 8g + r, 8(7-g) + r) += L(row, 8 bj + col_r) x(8 bj + col_r), x in shared memory.
+__device__ __forceinline__ void compact_fwd(const double* __restrict__ rec, int r, int g, const double* __restrict__ xs,
+                                            double& o0, double& o1) {
+  const int nc = rec_ncompact(rec);
+  const double* cb = rec_compact(rec);
+  for (int c = 0; c < nc; ++c, cb += kCompact) {
+    const int bit = int(__double_as_longlong(cb[9])), bi = bit >> 3, bj = bit & 7;
+    if (bi != g && bi != 7 - g) continue;
     const int col = reinterpret_cast<const unsigned char*>(cb + 8)[r];
+    const double t = cb[r] * xs[8 * bj + col];
+    if (bi == g)
+      o0 += t;
+    else
+      o1 += t;
+  }
+}
+
+// Backward tail: acc[jj][col_r] += L(8 bi + r, 8 bj + col_r) y(8 bi + r) for bj = g (jj 0) / 7 - g (jj 1).
+__device__ __forceinline__ void compact_bwd(const double* __restrict__ rec, int r, int g, const double* __restrict__ ys,
+                                            double (&acc)[2][8]) {
+  const int nc = rec_ncompact(rec);
+  const double* cb = rec_compact(rec);
+  for (int c = 0; c < nc; ++c, cb += kCompact) {
+    const int bit = int(__double_as_longlong(cb[9])), bi = bit >> 3, bj = bit & 7;
+    if (bj != g && bj != 7 - g) continue;
+    const int col = reinterpret_cast<const unsigned char*>(cb + 8)[r];
+    const double t = cb[r] * ys[8 * bi + r];
+    if (bj == g) {
 #pragma unroll
-    for (int k = 0; k < 8; ++k) v[k] = k == col ? val : 0.0;
+      for (int k = 0; k < 8; ++k) acc[0][k] += k == col ? t : 0.0;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc[1][k] += k == col ? t : 0.0;
+    }
   }
 }
 
@@ -654,7 +671,7 @@ __device__ __forceinline__ void ld_blk_row(const double* __restrict__ rec, const
 // rows of 8 doubles each per block-column) and the whole x = y_K in
 // registers, so its two output rows need no cross-lane reduction.
 __device__ __forceinline__ void tile_fwd(const double* __restrict__ rec, const double* __restrict__ zblk, int r, int g,
-                                         const double (&x)[64], double& o0, double& o1) {
+                                         const double (&x)[64], double& o0, double& o1, const double* __restrict__ xs) {
   const unsigned long long* hrow = reinterpret_cast<const unsigned long long*>(rec);  // [bi][bj] bytes
   const unsigned long long hw0 = hrow[g], hw1 = hrow[7 - g];
   double a[2][4];  // 4 independent chains per output row (both rows interleaved)
@@ -667,19 +684,20 @@ __device__ __forceinline__ void tile_fwd(const double* __restrict__ rec, const d
 #pragma unroll
     for (int jj = 0; jj < 2; ++jj) {
       double v[8];
-      ld_blk_row(rec, zblk, jj ? hw1 : hw0, bj, r, v);
+      ld_row8(rec_block(rec, zblk, jj ? hw1 : hw0, bj), r, v);
 #pragma unroll
       for (int k = 0; k < 8; ++k) a[jj][k & 3] = fma(v[k], x[8 * bj + k], a[jj][k & 3]);
     }
   }
   o0 = (a[0][0] + a[0][1]) + (a[0][2] + a[0][3]);
   o1 = (a[1][0] + a[1][1]) + (a[1][2] + a[1][3]);
+  compact_fwd(rec, r, g, xs, o0, o1);
 }
 
 // Backward, columns map: acc[jj][k] += sum_bi L_tile(8 bi + r, 8 bj + k) * yv[bi]
 // for the lane's block-columns bj = g, 7 - g;  yv[bi] = x[8 bi + r].
 __device__ __forceinline__ void tile_bwd(const double* __restrict__ rec, const double* __restrict__ zblk, int r, int g,
-                                         const double yv[8], double (&acc)[2][8]) {
+                                         const double yv[8], double (&acc)[2][8], const double* __restrict__ ys) {
   const unsigned long long* hcol = reinterpret_cast<const unsigned long long*>(rec) + 8;  // [bj][bi] bytes
 #pragma unroll
   for (int jj = 0; jj < 2; ++jj) {
@@ -687,11 +705,12 @@ __device__ __forceinline__ void tile_bwd(const double* __restrict__ rec, const d
 #pragma unroll
     for (int bi = 0; bi < 8; ++bi) {
       double v[8];
-      ld_blk_row(rec, zblk, hw, bi, r, v);
+      ld_row8(rec_block(rec, zblk, hw, bi), r, v);
 #pragma unroll
       for (int k = 0; k < 8; ++k) acc[jj][k] = fma(v[k], yv[bi], acc[jj][k]);
     }
   }
+  compact_bwd(rec, r, g, ys, acc);
 }
 
 // Sum acc over the 8 row lanes sharing g (recursive halving, 14 shuffles).
@@ -851,7 +870,7 @@ __global__ void __launch_bounds__(kSolveThreads)
     if (warp == (q & 7)) {
       load_x(yK, xr);
       const double* rec = acquire(q);
-      tile_fwd(rec, zblk, rl, g, xr, o0, o1);  // L_KK^{-1} y_K
+      tile_fwd(rec, zblk, rl, g, xr, o0, o1, yK);  // L_KK^{-1} y_K
       release(q);
       yK[8 * g + rl] = o0;
       yK[8 * (7 - g) + rl] = o1;
@@ -863,7 +882,7 @@ __global__ void __launch_bounds__(kSolveThreads)
     for (; i < cnt; i += 8) {
       const int qi = q + i - 1;
       const double* rec = acquire(qi);
-      tile_fwd(rec, zblk, rl, g, xr, o0, o1);
+      tile_fwd(rec, zblk, rl, g, xr, o0, o1, yK);
       release(qi);
       double* yI = y + tile_row[t0 + i] * T;
       yI[8 * g + rl] -= o0;
@@ -890,7 +909,7 @@ __global__ void __launch_bounds__(kSolveThreads)
 #pragma unroll
         for (int bi = 0; bi < 8; ++bi) yv[bi] = yI[8 * bi + rl];
         const double* rec = acquire(qi);
-        tile_bwd(rec, zblk, rl, g, yv, acc);
+        tile_bwd(rec, zblk, rl, g, yv, acc, yI);
         release(qi);
       }
       double s0, s1;
@@ -922,7 +941,7 @@ __global__ void __launch_bounds__(kSolveThreads)
 #pragma unroll
         for (int k = 0; k < 8; ++k) acc[jj][k] = 0.0;
       const double* rec = acquire(q);
-      tile_bwd(rec, zblk, rl, g, yv, acc);  // x_K = L_KK^{-T} y_K
+      tile_bwd(rec, zblk, rl, g, yv, acc, y + K * T);  // x_K = L_KK^{-T} y_K (no compact blocks)
       release(q);
       double s0, s1;
       int c;
@@ -1080,7 +1099,7 @@ __global__ void __launch_bounds__(kSolveThreads)
         if (warp == (q & 7)) {
           load_x(yK, xr);
           const double* rec = acquire(q);
-          tile_fwd(rec, zblk, rl, g, xr, o0, o1);
+          tile_fwd(rec, zblk, rl, g, xr, o0, o1, yK);
           release(q);
 #pragma unroll
           for (int d = 0; d < CS; ++d) {
@@ -1099,7 +1118,7 @@ __global__ void __launch_bounds__(kSolveThreads)
       for (; i < noff; i += 8) {
         const int qi = q + i;
         const double* rec = acquire(qi);
-        tile_fwd(rec, zblk, rl, g, xr, o0, o1);
+        tile_fwd(rec, zblk, rl, g, xr, o0, o1, yK);
         release(qi);
         double* yI = y + tile_row[cl_list[s0 + own + i]] * T;
         yI[8 * g + rl] -= o0;
@@ -1128,7 +1147,7 @@ __global__ void __launch_bounds__(kSolveThreads)
 #pragma unroll
           for (int bi = 0; bi < 8; ++bi) yv[bi] = yI[8 * bi + rl];
           const double* rec = acquire(qi);
-          tile_bwd(rec, zblk, rl, g, yv, acc);
+          tile_bwd(rec, zblk, rl, g, yv, acc, yI);
           release(qi);
         }
         double s0v, s1v;
@@ -1176,7 +1195,7 @@ __global__ void __launch_bounds__(kSolveThreads)
 #pragma unroll
             for (int k = 0; k < 8; ++k) acc[jj][k] = 0.0;
           const double* rec = acquire(q);
-          tile_bwd(rec, zblk, rl, g, yv, acc);
+          tile_bwd(rec, zblk, rl, g, yv, acc, yK);  // diagonal tile: no compact blocks
           release(q);
           double s0v, s1v;
           int c;

@@ -192,16 +192,19 @@ void symbolic_tiles(PatchLayout& L, const std::function<void(int, std::vector<in
   }
   // 8x8 sub-block masks (bit bi*8 + bj) of the packed solve stream, same rule.
   // Stream record of a tile: a 144-byte header -- the record index of every
-  // sub-block, row-major then column-major (0xff = structurally zero, < 0x80 a
-  // full 8x8 block, 0x80 | c the c-th compact block), then the full-block count
-  // F and compact count C -- followed by F full blocks (64 doubles) and C
-  // compact blocks (10 doubles: one value per row, then the 8 column bytes).
+  // full sub-block, row-major then column-major (0xff = absent or compact),
+  // then the full-block count F and compact count C -- followed by F full
+  // blocks (64 doubles) and C compact blocks (10 doubles: one value per row,
+  // the 8 column bytes, the sub-block bit bi*8 + bj).
   // Compact blocks are the off-diagonal sub-blocks with at most one structural
   // entry per row (facet couplings across a shared axis that runs fast in one
   // facet's numbering: one column, or a shifted diagonal): 8 values instead of
-  // 64.  FDMGPU_COMPACT=0 keeps every sub-block full.
+  // 64.  Opt-in (FDMGPU_COMPACT=1): 6.5 % (C5) / 12 % (C3) fewer streamed bytes,
+  // but the solve's consumers then bound it (C5 19.29 -> 19.42 ms, C3 1.13 ->
+  // 1.32 ms, profiles/r2_solve_records.md), so the default keeps every
+  // present sub-block full.
   const char* cenv = std::getenv("FDMGPU_COMPACT");
-  const bool compact = !(cenv && cenv[0] == '0');
+  const bool compact = cenv && cenv[0] == '1';
   const int nb8 = L.mpad / 8;
   L.tile_mask8.assign(L.ntiles, 0);
   L.tile_poff8.assign(L.ntiles + 1, 0);
@@ -230,7 +233,8 @@ void symbolic_tiles(PatchLayout& L, const std::function<void(int, std::vector<in
     for (int pass = 0; pass < 2; ++pass)  // full blocks first, then compact ones
       for (int b = 0; b < 64; ++b) {
         if (!((mask >> b) & 1) || ((cmask >> b) & 1) != uint64_t(pass)) continue;
-        const uint8_t v = pass ? uint8_t(0x80 | nc++) : uint8_t(nf++);
+        // compact sub-blocks read as absent in the full-block pass (0xff)
+        const uint8_t v = pass ? uint8_t(0xff + 0 * nc++) : uint8_t(nf++);
         hr[b] = v;                            // [bi*8 + bj]
         hr[64 + (b & 7) * 8 + (b >> 3)] = v;  // [bj*8 + bi]
         int64_t cc = 0;

@@ -465,3 +465,22 @@ def test_inplace_and_separate_packing_agree(pkg, torch, monkeypatch):
     sol2 = pkg.Solver(prob)
     sol2.factor()
     assert np.array_equal(sol2.smooth(r), z_sep)
+
+
+@pytest.mark.parametrize("cfg", [(4, 3, 15), (2, 0, 0)])
+def test_compact_solve_records_opt_in(pkg, oracle, torch, monkeypatch, cfg):
+    """FDMGPU_COMPACT=1: sparse 8x8 sub-blocks of the solve records stored as one
+    value per row (layout.cpp) give the same relaxation as the default records."""
+    prob = pkg.Problem(*cfg)
+    sol = pkg.Solver(prob)
+    sol.factor()
+    monkeypatch.setenv("FDMGPU_COMPACT", "1")
+    comp = pkg.Solver(prob)
+    comp.factor()
+    assert comp.layout()["stream_bytes"] < sol.layout()["stream_bytes"]
+    ref = oracle.Problem(*cfg, build_global=False, threads=os.cpu_count())
+    ref.factor()
+    rt = ref.apply_St(prob.rhs())
+    z = comp.patch_apply(rt)
+    assert rel(z, ref.patch_apply(rt)) <= TOL_RELAX
+    assert rel(z, sol.patch_apply(rt)) <= 1e-13
