@@ -472,6 +472,8 @@ fdmgpu_status fdmgpu_create(fdmgpu_handle* out, int32_t dim, int32_t p, int32_t 
     if (cs && cs[0] >= '1' && cs[0] <= '4' && cs[1] == 0) cc.solve_cs = cs[0] - '0';
     const char* st = std::getenv("FDMGPU_SOLVE_TAIL");
     cc.solve_tail = !(st && st[0] == '0');
+    const char* fu = std::getenv("FDMGPU_FUSED");
+    cc.fused_columns = !(fu && fu[0] == '0');
     cc.E.alloc(size_t(cc.ncells) * cc.npc);
     for (auto& v : cc.w) v.alloc(cc.ndof);
     cc.red.alloc(4 * fdmgpu::kRedBlocks);
@@ -854,6 +856,9 @@ fdmgpu_status fdmgpu_set_patches(fdmgpu_handle h, int32_t npatch, const int32_t*
     c.pg_ptr.upload(pptr, c.stream);
     c.pg_idx.upload(pidx, c.stream);
     c.corr.alloc(size_t(npatch) * m);
+    c.fac_flag.alloc(size_t(npatch) * L.nT);
+    FDM_CUDA(cudaMemsetAsync(c.fac_flag.p, 0, c.fac_flag.bytes(), c.stream));
+    c.fac_epoch = 0;
     c.tiles.alloc(size_t(npatch) * L.ntiles * fdmgpu::kTile * fdmgpu::kTile);
     // Separate solve-record buffer when it takes under a quarter of the free
     // memory (C3: 3.7 GB; packing then overlaps the factorisation, 24.3 -> 23.8 ms);
@@ -985,9 +990,14 @@ fdmgpu_status fdmgpu_factor(fdmgpu_handle h) {
       fdmgpu::launch_patch_assemble(c);
     fdmgpu::launch_patch_lead(c);
     for (int K = 0; K < c.L.lead_cols; ++K) fdmgpu::launch_patch_pack_col(c, K);
+    ++c.fac_epoch;
     for (int K = c.L.lead_cols; K < c.L.nT; ++K) {
-      fdmgpu::launch_patch_update(c, K);
-      fdmgpu::launch_patch_trsm(c, K);
+      if (c.fused_columns) {
+        fdmgpu::launch_patch_column(c, K);
+      } else {
+        fdmgpu::launch_patch_update(c, K);
+        fdmgpu::launch_patch_trsm(c, K);
+      }
       fdmgpu::launch_patch_pack_col(c, K);  // no-op when packing in place
     }
     if (c.packed.p)

@@ -171,6 +171,9 @@ struct Context {
   DevArray<int32_t> cl_list, cl_col;     // per-rank tile lists of the cluster solve
   int cl_fit[5] = {-1, -1, -1, -1, -1};  // co-resident clusters per cluster size (memo)
   DevArray<unsigned> tail_sync;          // finished split-tail CTAs, completed calls
+  DevArray<unsigned> fac_flag;           // npatch x nT: epoch at which L_KK^{-1} was published (k_patch_column)
+  unsigned fac_epoch = 0;                // factorisation count (flags never need a reset)
+  bool fused_columns = true;             // FDMGPU_FUSED=0: separate update / trsm launches
   bool have_patches = false, factored = false;
   DevArray<unsigned long long> d_err;
 
@@ -283,6 +286,7 @@ void launch_dg_facets(Context& c, const double* x);                    // adds t
 void launch_patch_assemble_one(Context& c, int j, double* out);  // S_G of patch j, tile layout
 void launch_patch_update(Context& c, int K);
 void launch_patch_trsm(Context& c, int K);
+void launch_patch_column(Context& c, int K);  // fused update + diagonal factor + trsm of tile column K
 void launch_patch_lead(Context& c);
 void launch_patch_pack(Context& c);
 void launch_patch_pack_col(Context& c, int K);   // separate record buffer, side stream

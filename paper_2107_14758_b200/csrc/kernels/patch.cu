@@ -464,6 +464,98 @@ __global__ void __launch_bounds__(kUpdThreads, 3) k_patch_update(PatchArgs a, in
   diag_factor_invert(Dm, Wm, ct, a, K, j);
 }
 
+// Fused tile column K: for every stored tile (I, K) of every patch,
+// C(I,K) = A(I,K) - sum_J L(I,J) L(K,J)^T (left-looking, as k_patch_update);
+// the diagonal CTA factors and inverts its tile and publishes L_KK^{-1} through
+// a device-scope flag; each off-diagonal CTA then finishes
+// L(I,K) = C(I,K) L_KK^{-T} itself (k_patch_trsm's GEMM) -- one launch per
+// column instead of two, and C(I,K) never leaves the SM.  Grid (npatch, tiles
+// of the column), blockIdx.y = 0 the diagonal tile: every patch's diagonal CTA
+// has a lower linear block index than any off-diagonal CTA of the column, so it
+// is dispatched first and the waits cannot starve it.
+__global__ void __launch_bounds__(kUpdThreads, 3) k_patch_column(PatchArgs a, int K, const int32_t* __restrict__ col_start,
+                                                                const int32_t* __restrict__ pair_ptr,
+                                                                const int32_t* __restrict__ pair_a,
+                                                                const int32_t* __restrict__ pair_b,
+                                                                const int32_t* __restrict__ tile_mask,
+                                                                double* __restrict__ tiles,
+                                                                unsigned* __restrict__ diag_flag, unsigned epoch) {
+  extern __shared__ __align__(128) double sm[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm);
+  double* buf = sm + 16;  // [A, B][TT] operand stage, then Dm / Wm or C / L_KK^{-1}
+  const int t0 = col_start[K], t = t0 + blockIdx.y, j = blockIdx.x;
+  double* base = tiles + size_t(j) * a.ntiles * TT;
+  const int p0 = pair_ptr[t], np = pair_ptr[t + 1] - p0;
+  const int tid = threadIdx.x;
+  pdl_trigger();
+  if (tid == 0) {
+    mbar_init(&full[0], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  pdl_wait();  // operands of column K-1 come from the previous launch
+  auto issue = [&](int i) {
+    mbar_arrive_expect_tx(&full[0], 2 * TT * sizeof(double));
+    bulk_g2s(buf, base + size_t(pair_a[p0 + i]) * TT, TT * sizeof(double), &full[0]);
+    bulk_g2s(buf + TT, base + size_t(pair_b[p0 + i]) * TT, TT * sizeof(double), &full[0]);
+  };
+  if (tid == 0 && np > 0) issue(0);
+  TileAcc acc = {};
+  for (int i = 0; i < np; ++i) {
+    mbar_wait(&full[0], i & 1);
+    tile_gemm_abt(buf, buf + TT, acc, tile_mask[pair_a[p0 + i]], tile_mask[pair_b[p0 + i]]);
+    __syncthreads();
+    if (tid == 0 && i + 1 < np) issue(i + 1);
+  }
+  double* ct = base + size_t(t) * TT;
+  if (t == t0) {  // diagonal tile: factor, invert, publish
+    constexpr int LD = T + 1;
+    double* Dm = buf;
+    double* Wm = buf + T * LD;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int r = acc.row(i), cc = acc.col(jj, e);
+          Dm[cc * LD + r] = ct[tsw(r, cc)] - acc.v[i][jj][e];
+        }
+    __syncthreads();
+    diag_factor_invert(Dm, Wm, ct, a, K, j);
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(diag_flag + size_t(j) * a.nT + K), "r"(epoch) : "memory");
+    }
+    return;
+  }
+  double* Cs = buf;
+  double* Ls = buf + TT;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int idx = tsw(acc.row(i), acc.col(jj, e));
+        Cs[idx] = ct[idx] - acc.v[i][jj][e];
+      }
+  if (tid == 0) wait_geq(diag_flag + size_t(j) * a.nT + K, epoch);
+  __syncthreads();
+  const double2* dt = reinterpret_cast<const double2*>(base + size_t(t0) * TT);
+  for (int i = tid; i < TT / 2; i += kUpdThreads) reinterpret_cast<double2*>(Ls)[i] = __ldcg(dt + i);
+  __syncthreads();
+  TileAcc lk = {};
+  tile_gemm_abt(Cs, Ls, lk, tile_mask[t], tile_mask[t0]);
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) ct[tsw(lk.row(i), lk.col(jj, e))] = lk.v[i][jj][e];
+}
+
 // L(I,K) = C(I,K) L_KK^{-T} for the off-diagonal tiles of column K.
 __global__ void __launch_bounds__(kUpdThreads) k_patch_trsm(PatchArgs a, int K, const int32_t* __restrict__ col_start,
                                                               const int32_t* __restrict__ lead,
@@ -1315,6 +1407,20 @@ void launch_patch_lead(Context& c) {
                                                                          c.tile_mask.p, c.tiles.p);
     FDM_LAUNCH_CHECK(c);
   }
+}
+
+void launch_patch_column(Context& c, int K) {
+  PatchArgs a = make_args(c);
+  const size_t diag_area = size_t(T + 1) * T + 16 * T * 4 + T;  // Dm, Lp, rdiag
+  const size_t smem = sizeof(double) * (16 + std::max(size_t(2 * TT), diag_area));
+  FDM_CUDA(cudaFuncSetAttribute(k_patch_column, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  const int cnt = c.L.col_start[K + 1] - c.L.col_start[K];
+  dim3 grid(c.npatch, cnt);
+  KernelTimer timer(c, 1);
+  launch_pdl(c.pdl && !c.timing, k_patch_column, grid, dim3(kUpdThreads), smem, c.stream, a, K,
+             (const int32_t*)c.col_start.p, (const int32_t*)c.pair_ptr.p, (const int32_t*)c.pair_a.p,
+             (const int32_t*)c.pair_b.p, (const int32_t*)c.tile_mask.p, c.tiles.p, c.fac_flag.p, c.fac_epoch);
+  FDM_LAUNCH_CHECK(c);
 }
 
 void launch_patch_trsm(Context& c, int K) {

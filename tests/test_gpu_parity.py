@@ -484,3 +484,19 @@ def test_compact_solve_records_opt_in(pkg, oracle, torch, monkeypatch, cfg):
     z = comp.patch_apply(rt)
     assert rel(z, ref.patch_apply(rt)) <= TOL_RELAX
     assert rel(z, sol.patch_apply(rt)) <= 1e-13
+
+
+@pytest.mark.parametrize("cfg", [(3, 3, 15), (2, 0, 0), (5, 2, 7)])
+def test_fused_column_factorisation(pkg, torch, monkeypatch, cfg):
+    """k_patch_column (update + diagonal factor + trsm of a tile column in one
+    launch, flag-synchronised) gives the same factor, bit for bit, as the
+    separate k_patch_update / k_patch_trsm launches (FDMGPU_FUSED=0)."""
+    prob = pkg.Problem(*cfg)
+    r = prob.rhs()
+    fused = pkg.Solver(prob)
+    fused.factor()
+    fused.factor()  # second factorisation: the flags' epoch advances, no reset needed
+    monkeypatch.setenv("FDMGPU_FUSED", "0")
+    split = pkg.Solver(prob)
+    split.factor()
+    assert np.array_equal(fused.smooth(r), split.smooth(r))
