@@ -544,16 +544,6 @@ def run_ours(args):
             result["sub_results"] = {"C3": sub_measure(3, min(args.steps, 50), args.warmup, stream, local)}
         except Exception as ex:  # reported, not fatal for the headline line
             result["sub_results"] = {"C3": {"failed": str(ex)}}
-    if rank == 0 and not args.no_cpu:
-        try:
-            threads = os.cpu_count() or 1
-            cb = cpu_sample(args.config, CPU_STEPS, 1, threads, args.cpu_sample_patches or threads)
-            result["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
-            result["cpu_spread_ms"] = {"min": cb["ms_min"], "median": cb["ms_per_step"], "max": cb["ms_max"]}
-            result["host"] = cb["host"]
-        except Exception as e:  # reported, not fatal for the GPU line
-            result["cpu_baseline"] = {"value": None, "unit": "GDOF/s", "cores": os.cpu_count(), "kind": "port",
-                                      "sample": f"failed: {e}"}
     if rank == 0 and world == 1 and not args.no_elastic:
         # the widened row, reported beside the headline: 3D elasticity,
         # 8^3 cells, vector Q15 (bench.py --elastic 3,8,15,1 gives the full line)
@@ -573,6 +563,17 @@ def run_ours(args):
             result["sipg"] = sipg_measure("3,4,5", min(args.steps, 20), args.warmup)
         except Exception as ex:
             result["sipg"] = {"failed": str(ex)}
+    # the CPU leg last: its host threads and memory do not disturb the GPU sub-lines' host copies
+    if rank == 0 and not args.no_cpu:
+        try:
+            threads = os.cpu_count() or 1
+            cb = cpu_sample(args.config, CPU_STEPS, 1, threads, args.cpu_sample_patches or threads)
+            result["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            result["cpu_spread_ms"] = {"min": cb["ms_min"], "median": cb["ms_per_step"], "max": cb["ms_max"]}
+            result["host"] = cb["host"]
+        except Exception as e:  # reported, not fatal for the GPU line
+            result["cpu_baseline"] = {"value": None, "unit": "GDOF/s", "cores": os.cpu_count(), "kind": "port",
+                                      "sample": f"failed: {e}"}
     replicas.barrier()
     replicas.finalize()
     if rank == 0:

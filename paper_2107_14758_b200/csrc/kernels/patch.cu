@@ -469,10 +469,11 @@ __global__ void __launch_bounds__(kUpdThreads, 3) k_patch_update(PatchArgs a, in
 // the diagonal CTA factors and inverts its tile and publishes L_KK^{-1} through
 // a device-scope flag; each off-diagonal CTA then finishes
 // L(I,K) = C(I,K) L_KK^{-T} itself (k_patch_trsm's GEMM) -- one launch per
-// column instead of two, and C(I,K) never leaves the SM.  Grid (npatch, tiles
-// of the column), blockIdx.y = 0 the diagonal tile: every patch's diagonal CTA
-// has a lower linear block index than any off-diagonal CTA of the column, so it
-// is dispatched first and the waits cannot starve it.
+// column instead of two, and C(I,K) never leaves the SM.  1D grid: blocks
+// [0, npatch) are the diagonal tiles of every patch, the rest the off-diagonal
+// tiles patch by patch (consecutive CTAs share their patch's L(K,J) operands in
+// L2).  Every diagonal CTA has a lower block index than any off-diagonal CTA,
+// so it is dispatched first and the waits cannot starve it.
 __global__ void __launch_bounds__(kUpdThreads, 3) k_patch_column(PatchArgs a, int K, const int32_t* __restrict__ col_start,
                                                                 const int32_t* __restrict__ pair_ptr,
                                                                 const int32_t* __restrict__ pair_a,
@@ -483,7 +484,10 @@ __global__ void __launch_bounds__(kUpdThreads, 3) k_patch_column(PatchArgs a, in
   extern __shared__ __align__(128) double sm[];
   uint64_t* full = reinterpret_cast<uint64_t*>(sm);
   double* buf = sm + 16;  // [A, B][TT] operand stage, then Dm / Wm or C / L_KK^{-1}
-  const int t0 = col_start[K], t = t0 + blockIdx.y, j = blockIdx.x;
+  const int t0 = col_start[K], noff = col_start[K + 1] - t0 - 1;
+  const int npatch = int(gridDim.x) / (noff + 1), b = blockIdx.x;
+  const int j = b < npatch ? b : (b - npatch) / noff;
+  const int t = b < npatch ? t0 : t0 + 1 + (b - npatch) % noff;
   double* base = tiles + size_t(j) * a.ntiles * TT;
   const int p0 = pair_ptr[t], np = pair_ptr[t + 1] - p0;
   const int tid = threadIdx.x;
@@ -1415,7 +1419,7 @@ void launch_patch_column(Context& c, int K) {
   const size_t smem = sizeof(double) * (16 + std::max(size_t(2 * TT), diag_area));
   FDM_CUDA(cudaFuncSetAttribute(k_patch_column, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   const int cnt = c.L.col_start[K + 1] - c.L.col_start[K];
-  dim3 grid(c.npatch, cnt);
+  dim3 grid(unsigned(c.npatch * cnt));
   KernelTimer timer(c, 1);
   launch_pdl(c.pdl && !c.timing, k_patch_column, grid, dim3(kUpdThreads), smem, c.stream, a, K,
              (const int32_t*)c.col_start.p, (const int32_t*)c.pair_ptr.p, (const int32_t*)c.pair_a.p,
