@@ -563,8 +563,9 @@ def run_ours(args):
             result["sipg"] = sipg_measure("3,4,5", min(args.steps, 20), args.warmup)
         except Exception as ex:
             result["sipg"] = {"failed": str(ex)}
-    # the CPU leg last: its host threads and memory do not disturb the GPU sub-lines' host copies
-    if rank == 0 and not args.no_cpu:
+    # the CPU leg last (its host threads and memory do not disturb the GPU sub-lines' host
+    # copies), on rank 0 of single-GPU runs only
+    if rank == 0 and world == 1 and not args.no_cpu:
         try:
             threads = os.cpu_count() or 1
             cb = cpu_sample(args.config, CPU_STEPS, 1, threads, args.cpu_sample_patches or threads)

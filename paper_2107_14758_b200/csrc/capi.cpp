@@ -834,7 +834,6 @@ fdmgpu_status fdmgpu_set_patches(fdmgpu_handle h, int32_t npatch, const int32_t*
     c.col_start.upload(L.col_start, c.stream);
     c.pair_ptr.upload(L.pair_ptr, c.stream);
     c.entries.upload(L.entries, c.stream);
-    c.ent_ptr.upload(L.ent_ptr, c.stream);
     c.tile_mask.upload(L.tile_mask, c.stream);
     c.tile_mask8.upload(L.tile_mask8, c.stream);
     c.tile_poff8.upload(L.tile_poff8, c.stream);

@@ -69,8 +69,7 @@ struct PatchLayout {
   std::vector<int32_t> pos_of_lat;   // span^d: elimination position or -1
   std::vector<int32_t> tile_row, tile_col, col_start;  // tile pattern, column-major order
   std::vector<int32_t> pair_ptr, pair_a, pair_b;       // left-looking update pairs per tile
-  std::vector<int32_t> entries;      // structural nonzeros of S_G: tile << 12 | col << 6 | row (sorted)
-  std::vector<int32_t> ent_ptr;      // ntiles + 1: each tile's range of `entries`
+  std::vector<int32_t> entries;      // structural nonzeros of S_G: tile << 12 | col << 6 | row
   std::vector<int32_t> tile_mask;             // 16x16 sub-blocks the factorisation touches per tile (GEMM panel skips)
   std::vector<int64_t> tile_mask8;            // 8x8 sub-blocks per tile kept in the solve stream
   std::vector<int32_t> tile_poff8;            // stream record offset (doubles): header + sub-blocks
@@ -157,7 +156,6 @@ struct Context {
   DevArray<int32_t> pdofs, lat, pos_of_lat, pcells, pg_ptr, pg_idx;
   DevArray<int32_t> tile_row, tile_col, col_start, pair_ptr, pair_a, pair_b, entries, tile_mask, active, tile_poff8, lead_diag, lead_trsm;
   DevArray<int64_t> tile_mask8, tile_ccol;
-  DevArray<int32_t> ent_ptr;
   DevArray<int32_t> tile_bptr, tile_blk;
   DevArray<uint8_t> tile_hdr;
   DevArray<double> corr, tiles, nK;

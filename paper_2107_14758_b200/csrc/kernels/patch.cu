@@ -216,56 +216,6 @@ __global__ void k_patch_assemble(PatchArgs a, int nentries, const int32_t* __res
   }
 }
 
-// Tile-parallel assembly: one CTA per (tile, patch) builds the whole tile in
-// shared memory -- zeros, the structural entries of S_G (this tile's range of
-// `entries`), the identity of absent / padded positions -- and writes it once
-// with coalesced stores, so the tiles need no separate zero fill (C3: a 5.7 GB
-// memset; C5: 84 GB).
-__global__ void __launch_bounds__(256) k_patch_assemble_tiles(PatchArgs a, const int32_t* __restrict__ ent_ptr,
-                                                              const int32_t* __restrict__ entries,
-                                                              const int32_t* __restrict__ tile_row,
-                                                              const int32_t* __restrict__ tile_col,
-                                                              double* __restrict__ tiles) {
-  extern __shared__ __align__(16) double sm[];
-  double* tl = sm;               // TT
-  double* At = tl + TT;
-  double* Bt = At + a.n1 * a.n1;
-  double* mup = Bt + a.n1 * a.n1;  // 2^d x d
-  const int t = blockIdx.x, j = blockIdx.y;
-  const int ncorner = 1 << a.dim;
-  for (int i = threadIdx.x; i < TT / 2; i += blockDim.x) reinterpret_cast<double2*>(tl)[i] = make_double2(0.0, 0.0);
-  for (int i = threadIdx.x; i < a.n1 * a.n1; i += blockDim.x) {
-    At[i] = a.At[i];
-    Bt[i] = a.Bt[i];
-  }
-  int smask = 0;
-  for (int s = 0; s < ncorner; ++s) smask |= (a.pcells[size_t(j) * ncorner + s] >= 0) << s;
-  for (int i = threadIdx.x; i < ncorner * a.dim; i += blockDim.x) {
-    const int s = i / a.dim, q = i % a.dim, K = a.pcells[size_t(j) * ncorner + s];
-    mup[i] = K >= 0 ? a.mu[size_t(K) * a.dim + q] : 0.0;
-  }
-  __syncthreads();
-  const int32_t* sep = a.psep + size_t(j) * a.m;
-  const bool whole = smask == (1 << ncorner) - 1;
-  const int I = tile_row[t], K = tile_col[t];
-  for (int e = ent_ptr[t] + threadIdx.x; e < ent_ptr[t + 1]; e += blockDim.x) {
-    const int code = entries[e];
-    const int cc = (code >> 6) & 63, rr = code & 63;
-    const int r = I * T + rr, c = K * T + cc;
-    double v;
-    if (!whole && (sep[r] < 0 || sep[c] < 0))
-      v = r == c ? 1.0 : 0.0;  // absent position of a boundary star: decoupled identity row
-    else
-      v = schur_entry(a, mup, smask, r, c, At, Bt);
-    tl[tsw(rr, cc)] = v;
-  }
-  if (I == K && I == a.nT - 1)  // padded positions m..mpad-1 of the last diagonal tile
-    for (int r = a.m + threadIdx.x; r < a.mpad; r += blockDim.x) tl[tsw(r % T, r % T)] = 1.0;
-  __syncthreads();
-  double2* dst = reinterpret_cast<double2*>(tiles + (size_t(j) * a.ntiles + t) * TT);
-  for (int i = threadIdx.x; i < TT / 2; i += blockDim.x) __stcs(dst + i, reinterpret_cast<const double2*>(tl)[i]);
-}
-
 // Identity on the padded separator positions m..mpad-1 (last diagonal tile)
 // and the interior pivots D_k > 0 (the first n_I pivots of the reference order).
 __global__ void k_patch_pad_check(PatchArgs a, double* __restrict__ tiles, int last_diag) {
@@ -1398,12 +1348,12 @@ static const double* rec_base(const Context& c) { return c.packed.p ? c.packed.p
 void launch_patch_assemble(Context& c) {
   PatchArgs a = make_args(c);
   KernelTimer timer(c, 1);
-  const size_t smem = sizeof(double) * (size_t(TT) + 2 * size_t(c.n1) * c.n1 + 24);
-  FDM_CUDA(cudaFuncSetAttribute(k_patch_assemble_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  k_patch_assemble_tiles<<<dim3(c.L.ntiles, c.npatch), 256, smem, c.stream>>>(a, c.ent_ptr.p, c.entries.p,
-                                                                               c.tile_row.p, c.tile_col.p, c.tiles.p);
+  FDM_CUDA(cudaMemsetAsync(c.tiles.p, 0, c.tiles.bytes(), c.stream));
+  const size_t smem = sizeof(double) * (2 * size_t(c.n1) * c.n1 + 24);
+  const int ne = int(c.L.entries.size());
+  dim3 grid(unsigned((ne + 255) / 256 < 64 ? (ne + 255) / 256 : 64), c.npatch);
+  k_patch_assemble<<<grid, 256, smem, c.stream>>>(a, ne, c.entries.p, c.tile_row.p, c.tile_col.p, c.tiles.p, 0);
   FDM_LAUNCH_CHECK(c);
-  // interior pivots D_k > 0 (the padding identity is written above)
   k_patch_pad_check<<<c.npatch, 256, 0, c.stream>>>(a, c.tiles.p, c.L.col_start[c.L.nT - 1]);
   FDM_LAUNCH_CHECK(c);
 }

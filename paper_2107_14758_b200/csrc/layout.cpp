@@ -362,9 +362,6 @@ void symbolic_tiles(PatchLayout& L, const std::function<void(int, std::vector<in
     }
   }
   std::sort(L.entries.begin(), L.entries.end());
-  L.ent_ptr.assign(L.ntiles + 1, 0);
-  for (int32_t code : L.entries) ++L.ent_ptr[(code >> 12) + 1];
-  for (int t = 0; t < L.ntiles; ++t) L.ent_ptr[t + 1] += L.ent_ptr[t];
 }
 
 // Builds c.L, c.h_pdofs, c.h_pcells from the patch lists.
