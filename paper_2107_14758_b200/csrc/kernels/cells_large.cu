@@ -491,8 +491,27 @@ __global__ void __launch_bounds__(256) k_cells_t1_32(int dir, int flags, const d
       v *= sign[size_t(c) * kNpc32 + l];
     return v;
   };
-#pragma unroll 4
-  for (int i = tid; i < 8 * kSlab32; i += 256) slab[(i & ~1023) + pos32(i & 1023)] = fetch(z0 * kSlab32 + i);
+  // gather in batches of 8 per thread: all map loads first, then the independent
+  // value loads (8 DRAM round trips in flight per thread instead of a chain)
+#pragma unroll 1
+  for (int h = 0; h < 4; ++h) {
+    int gi[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) gi[u] = cd[z0 * kSlab32 + tid + 256 * (8 * h + u)];
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int l = z0 * kSlab32 + tid + 256 * (8 * h + u), g = gi[u];
+      const double xv = in[g];
+      const double w = dir == 0 ? inv_mult[g] : (sign ? sign[size_t(c) * kNpc32 + l] : 1.0);
+      v[u] = cons[g] ? 0.0 : xv * w;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = tid + 256 * (8 * h + u);
+      slab[(i & ~1023) + pos32(i & 1023)] = v[u];
+    }
+  }
   if (recon)
     for (int i = tid; i < 2 * kSlab32; i += 256) zf[i] = fetch((i >> 10) * (kL32 - 1) * kSlab32 + (i & 1023));
   __syncthreads();
