@@ -1058,7 +1058,7 @@ fdmgpu_status fdmgpu_get_layout(fdmgpu_handle h, fdmgpu_layout* out) {
 fdmgpu_status fdmgpu_patch_schur(fdmgpu_handle h, int32_t j, double* out) {
   return fdmgpu::guarded(h, [&](Context& c) {
     c.check_ready(true, false, false);
-    if (c.ncomp > 1) throw Error(FDMGPU_UNSUPPORTED, "patch_schur: scalar handles only");
+    if (c.ncomp > 1 || c.dg) throw Error(FDMGPU_UNSUPPORTED, "patch_schur: scalar CG handles only");
     if (j < 0 || j >= c.npatch || !out) throw Error(FDMGPU_INVALID_ARGUMENT, "patch_schur: bad patch index");
     const auto& L = c.L;
     const size_t tt = size_t(fdmgpu::kTile) * fdmgpu::kTile;
@@ -1087,7 +1087,7 @@ fdmgpu_status fdmgpu_patch_solve_one(fdmgpu_handle h, int32_t j, const double* r
   return fdmgpu::guarded(h, [&](Context& c) {
     fdmgpu::NvtxRange nvtx_("fdmgpu_patch_solve_one");
     c.check_ready(true, true, false);
-    if (c.ncomp > 1) throw Error(FDMGPU_UNSUPPORTED, "patch_solve_one: scalar handles only");
+    if (c.ncomp > 1 || c.dg) throw Error(FDMGPU_UNSUPPORTED, "patch_solve_one: scalar CG handles only");
     if (j < 0 || j >= c.npatch || !rhs || !out) throw Error(FDMGPU_INVALID_ARGUMENT, "patch_solve_one: bad arguments");
     const int n = c.L.n, ncorner = 1 << c.dim;
     std::vector<int32_t> dofs;

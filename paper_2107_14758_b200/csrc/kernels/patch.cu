@@ -639,6 +639,8 @@ __device__ __forceinline__ void write_record(const double* __restrict__ cur, dou
       v = __longlong_as_double(static_cast<long long>(bit));
     dst[d] = v;
   }
+  if (nc > 0 && threadIdx.x < 16)  // compact index table
+    dst[nc * kCompact + threadIdx.x] = reinterpret_cast<const double*>(hdr_t + kHdrBytes)[threadIdx.x];
 }
 
 __global__ void k_patch_pack(int ntiles, const int32_t* __restrict__ bptr, const int32_t* __restrict__ blk,
@@ -664,7 +666,7 @@ __global__ void k_patch_pack(int ntiles, const int32_t* __restrict__ bptr, const
     // destination, so the in-place compaction never overwrites unread data.
     if (threadIdx.x == 0 && t + 1 < ntiles) load(t + 1);
     mbar_wait(&bar[t & 1], (t >> 1) & 1);
-    write_record(tile + (t & 1) * TT, base + size_t(poff8[t]), hdr + size_t(t) * kHdrBytes, blk + bptr[t],
+    write_record(tile + (t & 1) * TT, base + size_t(poff8[t]), hdr + size_t(t) * kHdrHost, blk + bptr[t],
                  ccol + bptr[t]);
     __syncthreads();
   }
@@ -686,7 +688,7 @@ __global__ void __launch_bounds__(256) k_patch_pack_cols(int t0, int ntiles, con
   const double2* src = reinterpret_cast<const double2*>(tiles + (size_t(j) * ntiles + t) * TT);
   for (int i = threadIdx.x; i < TT / 2; i += blockDim.x) reinterpret_cast<double2*>(cur)[i] = __ldcs(src + i);
   __syncthreads();
-  write_record(cur, packed + size_t(j) * pstride + poff8[t], hdr + size_t(t) * kHdrBytes, blk + bptr[t],
+  write_record(cur, packed + size_t(j) * pstride + poff8[t], hdr + size_t(t) * kHdrHost, blk + bptr[t],
                ccol + bptr[t]);
 }
 
@@ -720,45 +722,67 @@ __device__ __forceinline__ const double* rec_block(const double* rec, const doub
 }
 
 // Compact sub-blocks of a record (at most one entry per row): slot = 8 row
-// values, the 8 column bytes, the sub-block bit bi*8 + bj.
+// values, the 8 column bytes, the sub-block bit.  After the compact blocks the
+// record holds the compact index table (row-major then column-major bytes,
+// 0xff = not compact), read exactly like the header: the compact pass runs
+// the full-block loop structure with one value per lane row, absent positions
+// reading a zero slot, so it stays branch-free (only records with compact
+// blocks take it; warp-uniform).
 __device__ __forceinline__ int rec_ncompact(const double* rec) { return reinterpret_cast<const int*>(rec)[33]; }
 __device__ __forceinline__ const double* rec_compact(const double* rec) {
   return rec + kHdr + reinterpret_cast<const int*>(rec)[32] * SB8;
 }
-
-// Forward tail: o0 / o1 (rows 8g + r, 8(7-g) + r) += L(row, 8 bj + col_r) x(8 bj + col_r), x in shared memory.
-__device__ __forceinline__ void compact_fwd(const double* __restrict__ rec, int r, int g, const double* __restrict__ xs,
-                                            double& o0, double& o1) {
-  const int nc = rec_ncompact(rec);
-  const double* cb = rec_compact(rec);
-  for (int c = 0; c < nc; ++c, cb += kCompact) {
-    const int bit = int(__double_as_longlong(cb[9])), bi = bit >> 3, bj = bit & 7;
-    if (bi != g && bi != 7 - g) continue;
-    const int col = reinterpret_cast<const unsigned char*>(cb + 8)[r];
-    const double t = cb[r] * xs[8 * bj + col];
-    if (bi == g)
-      o0 += t;
-    else
-      o1 += t;
-  }
+__device__ __forceinline__ const double* cmp_slot(const double* cbase, const double* czero, unsigned long long hw, int e) {
+  const unsigned idx = unsigned(hw >> (8 * e)) & 0xffu;
+  return idx == 0xffu ? czero : cbase + idx * kCompact;
 }
 
-// Backward tail: acc[jj][col_r] += L(8 bi + r, 8 bj + col_r) y(8 bi + r) for bj = g (jj 0) / 7 - g (jj 1).
-__device__ __forceinline__ void compact_bwd(const double* __restrict__ rec, int r, int g, const double* __restrict__ ys,
-                                            double (&acc)[2][8]) {
+// Forward: o0 / o1 (rows 8g + r, 8(7-g) + r) += L(row, 8 bj + col_r) x(8 bj + col_r).
+__device__ __forceinline__ void compact_fwd(const double* __restrict__ rec, const double* __restrict__ czero, int r,
+                                            int g, const double (&x)[64], double& o0, double& o1) {
   const int nc = rec_ncompact(rec);
-  const double* cb = rec_compact(rec);
-  for (int c = 0; c < nc; ++c, cb += kCompact) {
-    const int bit = int(__double_as_longlong(cb[9])), bi = bit >> 3, bj = bit & 7;
-    if (bj != g && bj != 7 - g) continue;
-    const int col = reinterpret_cast<const unsigned char*>(cb + 8)[r];
-    const double t = cb[r] * ys[8 * bi + r];
-    if (bj == g) {
+  if (nc == 0) return;
+  const double* cbase = rec_compact(rec);
+  const unsigned long long* crow = reinterpret_cast<const unsigned long long*>(cbase + nc * kCompact);
+  const unsigned long long hw0 = crow[g], hw1 = crow[7 - g];
+  double a0 = 0.0, a1 = 0.0;
 #pragma unroll
-      for (int k = 0; k < 8; ++k) acc[0][k] += k == col ? t : 0.0;
-    } else {
+  for (int bj = 0; bj < 8; ++bj) {
 #pragma unroll
-      for (int k = 0; k < 8; ++k) acc[1][k] += k == col ? t : 0.0;
+    for (int jj = 0; jj < 2; ++jj) {
+      const double* cb = cmp_slot(cbase, czero, jj ? hw1 : hw0, bj);
+      const double val = cb[r];
+      const int col = reinterpret_cast<const unsigned char*>(cb + 8)[r];
+      double xs = 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) xs = k == col ? x[8 * bj + k] : xs;
+      if (jj)
+        a1 = fma(val, xs, a1);
+      else
+        a0 = fma(val, xs, a0);
+    }
+  }
+  o0 += a0;
+  o1 += a1;
+}
+
+// Backward: acc[jj][col_r] += L(8 bi + r, 8 bj + col_r) y(8 bi + r) for bj = g (jj 0) / 7 - g (jj 1).
+__device__ __forceinline__ void compact_bwd(const double* __restrict__ rec, const double* __restrict__ czero, int r,
+                                            int g, const double yv[8], double (&acc)[2][8]) {
+  const int nc = rec_ncompact(rec);
+  if (nc == 0) return;
+  const double* cbase = rec_compact(rec);
+  const unsigned long long* ccolt = reinterpret_cast<const unsigned long long*>(cbase + nc * kCompact) + 8;
+#pragma unroll
+  for (int jj = 0; jj < 2; ++jj) {
+    const unsigned long long hw = ccolt[jj ? 7 - g : g];
+#pragma unroll
+    for (int bi = 0; bi < 8; ++bi) {
+      const double* cb = cmp_slot(cbase, czero, hw, bi);
+      const double t = cb[r] * yv[bi];
+      const int col = reinterpret_cast<const unsigned char*>(cb + 8)[r];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc[jj][k] += k == col ? t : 0.0;
     }
   }
 }
@@ -787,7 +811,7 @@ __device__ __forceinline__ void tile_fwd(const double* __restrict__ rec, const d
   }
   o0 = (a[0][0] + a[0][1]) + (a[0][2] + a[0][3]);
   o1 = (a[1][0] + a[1][1]) + (a[1][2] + a[1][3]);
-  compact_fwd(rec, r, g, xs, o0, o1);
+  compact_fwd(rec, zblk, r, g, x, o0, o1);
 }
 
 // Backward, columns map: acc[jj][k] += sum_bi L_tile(8 bi + r, 8 bj + k) * yv[bi]
@@ -806,7 +830,7 @@ __device__ __forceinline__ void tile_bwd(const double* __restrict__ rec, const d
       for (int k = 0; k < 8; ++k) acc[jj][k] = fma(v[k], yv[bi], acc[jj][k]);
     }
   }
-  compact_bwd(rec, r, g, ys, acc);
+  compact_bwd(rec, zblk, r, g, yv, acc);
 }
 
 // Sum acc over the 8 row lanes sharing g (recursive halving, 14 shuffles).

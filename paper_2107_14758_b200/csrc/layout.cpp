@@ -194,8 +194,9 @@ void symbolic_tiles(PatchLayout& L, const std::function<void(int, std::vector<in
   // Stream record of a tile: a 144-byte header -- the record index of every
   // full sub-block, row-major then column-major (0xff = absent or compact),
   // then the full-block count F and compact count C -- followed by F full
-  // blocks (64 doubles) and C compact blocks (10 doubles: one value per row,
-  // the 8 column bytes, the sub-block bit bi*8 + bj).
+  // blocks (64 doubles), C compact blocks (10 doubles: one value per row, the 8
+  // column bytes, the sub-block bit bi*8 + bj) and, when C > 0, the 128-byte
+  // compact index table (row-major, column-major; 0xff = not compact).
   // Compact blocks are the off-diagonal sub-blocks with at most one structural
   // entry per row (facet couplings across a shared axis that runs fast in one
   // facet's numbering: one column, or a shifted diagonal): 8 values instead of
@@ -208,7 +209,7 @@ void symbolic_tiles(PatchLayout& L, const std::function<void(int, std::vector<in
   const int nb8 = L.mpad / 8;
   L.tile_mask8.assign(L.ntiles, 0);
   L.tile_poff8.assign(L.ntiles + 1, 0);
-  L.tile_hdr.assign(size_t(L.ntiles) * kHdrBytes, 0);
+  L.tile_hdr.assign(size_t(L.ntiles) * kHdrHost, 0);
   L.tile_bptr.assign(L.ntiles + 1, 0);
   L.tile_blk.clear();
   L.tile_ccol.clear();
@@ -228,15 +229,23 @@ void symbolic_tiles(PatchLayout& L, const std::function<void(int, std::vector<in
         }
       }
     L.tile_mask8[t] = int64_t(mask);
-    uint8_t* hr = &L.tile_hdr[size_t(t) * kHdrBytes];
+    uint8_t* hr = &L.tile_hdr[size_t(t) * kHdrHost];
+    uint8_t* ct = hr + kHdrBytes;  // compact index table (stored after the compact blocks when C > 0)
+    std::fill(ct, ct + 128, uint8_t(0xff));
     int nf = 0, nc = 0;
     for (int pass = 0; pass < 2; ++pass)  // full blocks first, then compact ones
       for (int b = 0; b < 64; ++b) {
         if (!((mask >> b) & 1) || ((cmask >> b) & 1) != uint64_t(pass)) continue;
-        // compact sub-blocks read as absent in the full-block pass (0xff)
-        const uint8_t v = pass ? uint8_t(0xff + 0 * nc++) : uint8_t(nf++);
+        // compact sub-blocks read as absent in the full-block pass (0xff) and
+        // through the compact table in the compact pass
+        const uint8_t v = pass ? uint8_t(0xff) : uint8_t(nf++);
         hr[b] = v;                            // [bi*8 + bj]
         hr[64 + (b & 7) * 8 + (b >> 3)] = v;  // [bj*8 + bi]
+        if (pass) {
+          ct[b] = uint8_t(nc);
+          ct[64 + (b & 7) * 8 + (b >> 3)] = uint8_t(nc);
+          ++nc;
+        }
         int64_t cc = 0;
         if (pass) {  // column of each row's entry (0 for an empty row: its values are zero)
           const uint64_t e = bits8[size_t(8 * I + (b >> 3)) * nb8 + (8 * K + (b & 7))];
@@ -256,7 +265,7 @@ void symbolic_tiles(PatchLayout& L, const std::function<void(int, std::vector<in
     reinterpret_cast<int32_t*>(hr + 128)[0] = nf;
     reinterpret_cast<int32_t*>(hr + 128)[1] = nc;
     L.tile_bptr[t + 1] = int32_t(L.tile_blk.size());
-    L.tile_poff8[t + 1] = L.tile_poff8[t] + kHdrBytes / 8 + 64 * nf + kCompact * nc;
+    L.tile_poff8[t + 1] = L.tile_poff8[t] + kHdrBytes / 8 + 64 * nf + kCompact * nc + (nc ? 16 : 0);
     // the in-place compaction (k_patch_pack) needs every packed prefix to end
     // before the next unpacked tile starts
     if (int64_t(L.tile_poff8[t + 1]) > int64_t(t + 1) * T * T)

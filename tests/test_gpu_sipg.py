@@ -56,6 +56,14 @@ def test_dg_setup_matches_oracle(dg_pair):
     assert L["nnz_L"] == pt["nnz"][first_full]
 
 
+def test_dg_rejects_cg_only_entries(pkg, dg_pair):
+    prob, sol, ref = dg_pair
+    with pytest.raises(pkg.FdmGpuError, match="scalar CG handles only"):
+        sol.patch_schur(0)
+    with pytest.raises(pkg.FdmGpuError, match="scalar CG handles only"):
+        sol.patch_solve_one(0, np.zeros(10))
+
+
 def test_dg_operators_match_oracle(dg_pair):
     prob, sol, ref = dg_pair
     rng = np.random.default_rng(prob.p)

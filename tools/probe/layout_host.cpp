@@ -5,6 +5,7 @@
 //   g++ -O2 -std=c++20 -I include -I paper_2107_14758_b200/csrc tools/probe/layout_host.cpp \
 //       -L paper_2107_14758_b200/lib -lfdmgpu -Wl,-rpath,$PWD/paper_2107_14758_b200/lib -o /tmp/layout_host
 #include <cstdio>
+#include <algorithm>
 #include <cstdlib>
 #include <vector>
 
@@ -111,6 +112,24 @@ int main(int argc, char** argv) {
   }
   std::printf("executed DMMA flops / patch %.4e (x%.2f of in-use), diagonal POTRF+inverse tiles %d\n", exec,
               exec / (2.0 * double(L.flops_ref)), L.nT);
+  if (std::getenv("COMPACT_STATS")) {  // compact sub-blocks per tile (FDMGPU_COMPACT=1 layouts)
+    std::vector<int> hist(65, 0);
+    int tiles_with = 0, maxrow = 0;
+    for (int t = 0; t < L.ntiles; ++t) {
+      const uint8_t* hr = &L.tile_hdr[size_t(t) * fdmgpu::kHdrHost];
+      const int nc = reinterpret_cast<const int32_t*>(hr + 128)[1];
+      ++hist[nc];
+      tiles_with += nc > 0;
+      int rows[8] = {0};
+      for (int q = L.tile_bptr[t]; q < L.tile_bptr[t + 1]; ++q)
+        if (L.tile_ccol[q] != 0 || (q - L.tile_bptr[t]) >= reinterpret_cast<const int32_t*>(hr + 128)[0]) ++rows[L.tile_blk[q] >> 3];
+      for (int r = 0; r < 8; ++r) maxrow = std::max(maxrow, rows[r]);
+    }
+    std::printf("tiles with compact blocks %d of %d; max per block-row %d; nc histogram:", tiles_with, L.ntiles, maxrow);
+    for (int v = 1; v <= 64; ++v)
+      if (hist[v]) std::printf(" %d:%d", v, hist[v]);
+    std::printf("\n");
+  }
   fdmhost_problem_destroy(pb);
   return 0;
 }
