@@ -1,7 +1,10 @@
-"""SIPG DG oracle (oracle/sipg.cpp, Cartesian facets) pinned by the reference's
-own known-answer tests (tests/test_sipg.cpp).  CPU only: the DG half of SURVEY.md
-8(f)3 has its oracle here; the device path for DG patches is the next row
-(DESIGN.md section 8)."""
+"""SIPG DG oracle (oracle/sipg.cpp, Cartesian facets) pinned by the Cartesian
+subset of the reference's own known-answer tests (tests/test_sipg.cpp: penalty,
+nodal facet traces, transformed-system exactness and stencils, patch rows, the
+Cartesian two-level run).  Not restated: the flipped / pentagon two-level
+variant, the Kronecker-vs-facet-quadrature check and the CG/DG energy check
+(non-Cartesian meshes).  CPU only; the device path is checked against this
+oracle in tests/test_gpu_sipg.py."""
 import numpy as np
 import pytest
 
