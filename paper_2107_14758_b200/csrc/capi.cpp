@@ -558,6 +558,8 @@ fdmgpu_status fdmgpu_set_sipg(fdmgpu_handle h, double eta, const double* deriv_t
     for (int f = 0; f < nfacets; ++f) {
       const int ax = facet_axis[f];
       if (ax < 0 || ax >= c.dim || facet_tags[f] > 2) throw Error(FDMGPU_INVALID_ARGUMENT, "set_sipg: bad facet");
+      if ((facet_cells[2 * f] < 0 || facet_cells[2 * f + 1] < 0) && facet_tags[f] == 0)
+        throw Error(FDMGPU_INVALID_ARGUMENT, "set_sipg: boundary facet tagged interior (Mesh::finalize tags them)");
       for (int r = 0; r < 2; ++r) {
         const int K = facet_cells[2 * f + r];
         if (K < 0) continue;
