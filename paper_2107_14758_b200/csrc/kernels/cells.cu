@@ -511,14 +511,21 @@ __global__ void __launch_bounds__(kLines16, 2) k_cells_stiffness16(const double*
   double* b1 = b0 + kNpc16;
   const Pos16 P;
   const int c = blockIdx.x, r = threadIdx.x;
+  pdl_trigger();
+  // static data (1D matrices, the cell map, mu) before the wait for x: with
+  // programmatic dependent launch this overlaps the previous kernel's tail
   load_rows16(As, Ahat);
   load_rows16(Bs, Bhat);
   const int32_t* cd = cdofs + size_t(c) * kNpc16;
+  int gi[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) gi[u] = cd[r + kLines16 * u];
+  pdl_wait();  // x comes from the previous kernel
 #pragma unroll 1
   for (int h = 0; h < 2; ++h) {
-    int gi[8];
+    if (h)
 #pragma unroll
-    for (int u = 0; u < 8; ++u) gi[u] = cd[r + kLines16 * (8 * h + u)];
+      for (int u = 0; u < 8; ++u) gi[u] = cd[r + kLines16 * (8 + u)];
     double v[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
@@ -988,8 +995,9 @@ void launch_cells_stiffness_kron(Context& c, const double* x) {
     const size_t smem16 = sizeof(double) * (2 * kL16 * kL16 + 2 * size_t(kNpc16));
     set_smem(k_cells_stiffness16, smem16);
     KernelTimer timer(c, 3);
-    k_cells_stiffness16<<<c.ncells, kLines16, smem16, c.stream>>>(x, c.E.p, c.cell_dofs.p, c.constrained.p, c.mu.p,
-                                                                   c.Ahat.p, c.Bhat.p);
+    launch_pdl(c.pdl && !c.timing, k_cells_stiffness16, dim3(c.ncells), dim3(kLines16), smem16, c.stream, x,
+               c.E.p, (const int32_t*)c.cell_dofs.p, (const uint8_t*)c.constrained.p, (const double*)c.mu.p,
+               (const double*)c.Ahat.p, (const double*)c.Bhat.p);
     FDM_LAUNCH_CHECK(c);
     return;
   }
