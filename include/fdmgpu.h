@@ -214,6 +214,12 @@ fdmgpu_status fdmgpu_patch_schur(fdmgpu_handle h, int32_t j, double* out);
  * length n_j.  Runs the batched device solve and keeps patch j's
  * correction only (cost of one relaxation's patch stage). */
 fdmgpu_status fdmgpu_patch_solve_one(fdmgpu_handle h, int32_t j, const double* rhs, double* out);
+/* Debug / parity entry: the separator Cholesky factor L of patch j (dense m x m,
+ * column-major, lower triangle; S_G = L L^T with fdmgpu_patch_schur's S_G) -- the
+ * factor cholesky() computes (src/cholesky.cpp:9-87) for the separator block.
+ * Needs the dense factor tiles, i.e. a factor whose solve records were packed
+ * into their own buffer (FDMGPU_UNSUPPORTED for factors packed in place). */
+fdmgpu_status fdmgpu_patch_factor(fdmgpu_handle h, int32_t j, double* out);
 /* Per-patch global DOFs in elimination order (npatch x n): dofs[perm[k]]. */
 fdmgpu_status fdmgpu_get_patch_elimination_dofs(fdmgpu_handle h, int32_t* out);
 

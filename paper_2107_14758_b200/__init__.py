@@ -87,6 +87,7 @@ def lib():
         L.fdmhost_write_matrix_market.argtypes = [C.c_char_p, C.c_int64, C.c_int64, _vp, _vp, _vp, C.c_int]
         L.fdmgpu_patch_schur.argtypes = [_vp, C.c_int32, _vp]
         L.fdmgpu_patch_solve_one.argtypes = [_vp, C.c_int32, _vp, _vp]
+        L.fdmgpu_patch_factor.argtypes = [_vp, C.c_int32, _vp]
         L.fdmgpu_set_separator_order.argtypes = [_vp, C.c_int32]
         L.fdmgpu_set_patches.argtypes = [_vp, C.c_int32, _vp, _vp, _vp, _vp, _vp]
         L.fdmhost_problem_info.argtypes = [_vp, _vp]
@@ -401,6 +402,13 @@ class Solver:
         m = self.layout()["n_interface"]
         out = np.zeros((m, m), order="F")
         self._chk(lib().fdmgpu_patch_schur(self.h, int(j), _ptr(out)))
+        return out
+
+    def patch_factor(self, j):
+        """Separator Cholesky factor L of patch j (dense m x m lower; S_G = L L^T)."""
+        m = self.layout()["n_interface"]
+        out = np.zeros((m, m), order="F")
+        self._chk(lib().fdmgpu_patch_factor(self.h, int(j), _ptr(out)))
         return out
 
     def patch_solve_one(self, j, rj):

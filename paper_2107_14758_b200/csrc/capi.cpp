@@ -1137,6 +1137,49 @@ fdmgpu_status fdmgpu_patch_solve_one(fdmgpu_handle h, int32_t j, const double* r
   });
 }
 
+fdmgpu_status fdmgpu_patch_factor(fdmgpu_handle h, int32_t j, double* out) {
+  return fdmgpu::guarded(h, [&](Context& c) {
+    c.check_ready(true, true, false);
+    if (c.ncomp > 1) throw Error(FDMGPU_UNSUPPORTED, "patch_factor: scalar handles only");
+    if (j < 0 || j >= c.npatch || !out) throw Error(FDMGPU_INVALID_ARGUMENT, "patch_factor: bad patch index");
+    if (!c.packed.p)
+      throw Error(FDMGPU_UNSUPPORTED, "patch_factor: the dense factor tiles were packed in place (large factor)");
+    const auto& L = c.L;
+    const int T = fdmgpu::kTile, m = L.m;
+    const size_t tt = size_t(T) * T;
+    std::vector<double> h_t(size_t(L.ntiles) * tt);
+    FDM_CUDA(cudaMemcpyAsync(h_t.data(), c.tiles.p + size_t(j) * L.ntiles * tt, h_t.size() * sizeof(double),
+                             cudaMemcpyDeviceToHost, c.stream));
+    FDM_CUDA(cudaStreamSynchronize(c.stream));
+    std::fill(out, out + size_t(m) * m, 0.0);
+    std::vector<double> W(tt), Ld(tt);
+    for (int t = 0; t < L.ntiles; ++t) {
+      for (int cc = 0; cc < T; ++cc)
+        for (int rr = 0; rr < T; ++rr) {
+          const int swz = ((cc & 3) << 2) | ((cc >> 2) & 3);  // tile swizzle (kernels/common.cuh tsw)
+          W[size_t(cc) * T + rr] = h_t[size_t(t) * tt + size_t(cc) * T + (rr ^ swz)];
+        }
+      if (L.tile_row[t] == L.tile_col[t]) {  // stored L_KK^{-1} (lower): invert back to L_KK
+        std::fill(Ld.begin(), Ld.end(), 0.0);
+        for (int col = 0; col < T; ++col) {
+          // solve W x = e_col (W lower triangular), x = column col of L_KK
+          for (int r = col; r < T; ++r) {
+            double v = r == col ? 1.0 : 0.0;
+            for (int k = col; k < r; ++k) v -= W[size_t(k) * T + r] * Ld[size_t(col) * T + k];
+            Ld[size_t(col) * T + r] = v / W[size_t(r) * T + r];
+          }
+        }
+        W = Ld;
+      }
+      for (int cc = 0; cc < T; ++cc)
+        for (int rr = 0; rr < T; ++rr) {
+          const int r = L.tile_row[t] * T + rr, col = L.tile_col[t] * T + cc;
+          if (r < m && col < m && r >= col) out[size_t(col) * m + r] = W[size_t(cc) * T + rr];
+        }
+    }
+  });
+}
+
 fdmgpu_status fdmgpu_get_patch_elimination_dofs(fdmgpu_handle h, int32_t* out) {
   return fdmgpu::guarded(h, [&](Context& c) {
     c.check_ready(true, false, false);

@@ -500,3 +500,20 @@ def test_fused_column_factorisation(pkg, torch, monkeypatch, cfg):
     split = pkg.Solver(prob)
     split.factor()
     assert np.array_equal(fused.smooth(r), split.smooth(r))
+
+
+@pytest.mark.parametrize("cfg", [(2, 0, 0), (4, 3, 5), (5, 2, 7), (1, 4, 5)])
+def test_patch_factor_residual(pkg, torch, cfg):
+    """K2: the device factor of sampled patches reproduces the
+    matrix it factors, ||L L^T - S_G||_max / ||S_G||_max <= 1e-12 (S_G the
+    separator Schur complement, fdmgpu_patch_schur), L lower triangular with a
+    positive diagonal."""
+    prob = pkg.Problem(*cfg)
+    sol = pkg.Solver(prob)
+    sol.factor()
+    npatch = sol.layout()["npatch"]
+    for j in sorted({0, npatch // 2, npatch - 1}):
+        S = sol.patch_schur(j)
+        L = sol.patch_factor(j)
+        assert np.array_equal(L, np.tril(L)) and (np.diag(L) > 0).all()
+        assert np.abs(L @ L.T - S).max() <= 1e-12 * np.abs(S).max()
