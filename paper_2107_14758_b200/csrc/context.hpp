@@ -82,6 +82,7 @@ struct PatchLayout {
   std::vector<int32_t> active, active_ptr;    // per column: tiles the update kernel must visit
   int64_t nnz_L = 0, flops_ref = 0, tile_gemms = 0;          // order in use
   int64_t dmma_flops = 0;                                   // tensor-pipe flops the factor kernels issue
+  std::vector<int> colcount;                                // nnz per factor column (elimination order; diagnostics)
   int64_t nnz_L_reference = 0, flops_reference = 0;         // reference patch_ordering
 };
 

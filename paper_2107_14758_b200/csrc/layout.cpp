@@ -87,6 +87,7 @@ void symbolic_tiles(PatchLayout& L, const std::function<void(int, std::vector<in
     L.nnz_L += colcount[k];
     L.flops_ref += int64_t(colcount[k]) * (colcount[k] - 1) / 2;
   }
+  L.colcount = colcount;
   L.nnz_L_reference = L.nnz_L;
   L.flops_reference = L.flops_ref;
   for (int K = 0; K < L.nT; ++K) tmark[size_t(K) * L.nT + K] = 1;

@@ -112,6 +112,26 @@ int main(int argc, char** argv) {
   }
   std::printf("executed DMMA flops / patch %.4e (x%.2f of in-use), diagonal POTRF+inverse tiles %d\n", exec,
               exec / (2.0 * double(L.flops_ref)), L.nT);
+  if (std::getenv("GROUP_STATS")) {  // nnz(L) and flops by separator group (CG layouts)
+    const char* names[6] = {"interior", "plane0 facets", "plane1 facets", "plane2 facets", "edges", "vertex"};
+    int64_t nnz[6] = {0}, fl[6] = {0}, cnt[6] = {0};
+    for (int k = 0; k < L.n; ++k) {
+      const int code = L.lat[k];
+      int P[3] = {code & 255, (code >> 8) & 255, (code >> 16) & 255}, at = 0, ax = 0;
+      for (int a = 0; a < dim; ++a)
+        if (P[a] == pp) {
+          ++at;
+          ax = a;
+        }
+      const int gidx = at == 0 ? 0 : at == 1 ? 1 + ax : at == 2 ? 4 : 5;
+      nnz[gidx] += L.colcount[k];
+      fl[gidx] += int64_t(L.colcount[k]) * (L.colcount[k] - 1) / 2;
+      ++cnt[gidx];
+    }
+    for (int g = 0; g < 6; ++g)
+      std::printf("%-14s %7lld columns  nnz %12lld  madds %14lld\n", names[g], (long long)cnt[g], (long long)nnz[g],
+                  (long long)fl[g]);
+  }
   if (std::getenv("COMPACT_STATS")) {  // compact sub-blocks per tile (FDMGPU_COMPACT=1 layouts)
     std::vector<int> hist(65, 0);
     int tiles_with = 0, maxrow = 0;
