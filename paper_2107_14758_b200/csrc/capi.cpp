@@ -17,6 +17,79 @@
 #include "context.hpp"
 
 namespace fdmgpu {
+void analyze_schur_split(Context& c);
+
+// Schur-split solve state (SchurSplit, context.hpp): host analysis, index
+// uploads and the split's buffers -- the L_RR records (c.packed), the diagonal
+// L_KK side copies, per-patch values, right-hand side / work vectors.  Left
+// off (full-factor stream) when the layout does not split or memory is short.
+void setup_schur_split(Context& c) {
+  c.sx = SchurSplit();
+  for (auto* a : {&c.sx_comp0, &c.sx_comp1, &c.sx_comp_fr, &c.sx_rf_ptr, &c.sx_rf_col, &c.sx_fr_ptr, &c.sx_fr_col,
+                  &c.sx_fr_row, &c.sx_pdofs, &c.sx_pairs, &c.sx_tidx, &c.sx_tile_row, &c.sx_tile_col, &c.sx_col_start,
+                  &c.sx_poff8, &c.sx_bptr, &c.sx_blk})
+    a->reset();
+  c.sx_ccol.reset();
+  c.sx_hdr.reset();
+  for (auto* a : {&c.sx_vals, &c.sx_tR, &c.sx_F, &c.diagL}) a->reset();
+  if (c.dg) return;
+  analyze_schur_split(c);
+  SchurSplit& S = c.sx;
+  if (!S.on) return;
+  const auto& L = c.L;
+  const int K0 = S.nF / kTile;
+  const size_t np = size_t(c.npatch);
+  const size_t need = sizeof(double) * (np * size_t(S.R.tile_poff8.back()) + np * size_t(L.nT - K0) * kTile * kTile +
+                                        np * size_t(S.vstride) + np * size_t(S.nR + S.nF));
+  size_t fb = 0, tb = 0;
+  FDM_CUDA(cudaMemGetInfo(&fb, &tb));
+  if (need + (size_t(1) << 30) > fb) {  // keep 1 GiB of headroom for work vectors
+    S = SchurSplit();
+    return;
+  }
+  // every R x R tile of the full factor must exist (L_RR is dense)
+  std::vector<int32_t> tidx(size_t(L.nT) * L.nT, -1);
+  for (int t = 0; t < L.ntiles; ++t) tidx[size_t(L.tile_row[t]) * L.nT + L.tile_col[t]] = t;
+  for (int I = K0; I < L.nT; ++I)
+    for (int J = K0; J <= I; ++J)
+      if (tidx[size_t(I) * L.nT + J] < 0) {
+        S = SchurSplit();
+        return;
+      }
+  std::vector<int32_t> pairs;
+  for (int r = 0; r < S.nR; ++r)
+    for (int e = S.rf_ptr[r]; e < S.rf_ptr[r + 1]; ++e) pairs.push_back((S.nF + r) | (S.rf_col[e] << 16));
+  for (size_t f = 0; f < S.fr_row.size(); ++f)
+    for (int e = S.fr_ptr[f]; e < S.fr_ptr[f + 1]; ++e) pairs.push_back(S.fr_row[f] | ((S.nF + S.fr_col[e]) << 16));
+  std::vector<int32_t> rp(np * S.nR);
+  for (size_t i = 0; i < rp.size(); ++i) rp[i] = int32_t(i);
+  c.sx_K0 = K0;
+  c.sx_comp0.upload(S.comp0, c.stream);
+  c.sx_comp1.upload(S.comp1, c.stream);
+  c.sx_comp_fr.upload(S.comp_fr, c.stream);
+  c.sx_rf_ptr.upload(S.rf_ptr, c.stream);
+  c.sx_rf_col.upload(S.rf_col.empty() ? std::vector<int32_t>{0} : S.rf_col, c.stream);
+  c.sx_fr_ptr.upload(S.fr_ptr, c.stream);
+  c.sx_fr_col.upload(S.fr_col.empty() ? std::vector<int32_t>{0} : S.fr_col, c.stream);
+  c.sx_fr_row.upload(S.fr_row, c.stream);
+  c.sx_pairs.upload(pairs.empty() ? std::vector<int32_t>{0} : pairs, c.stream);
+  c.sx_pdofs.upload(rp, c.stream);
+  c.sx_tidx.upload(tidx, c.stream);
+  c.sx_tile_row.upload(S.R.tile_row, c.stream);
+  c.sx_tile_col.upload(S.R.tile_col, c.stream);
+  c.sx_col_start.upload(S.R.col_start, c.stream);
+  c.sx_poff8.upload(S.R.tile_poff8, c.stream);
+  c.sx_bptr.upload(S.R.tile_bptr, c.stream);
+  c.sx_blk.upload(S.R.tile_blk, c.stream);
+  c.sx_ccol.upload(S.R.tile_ccol, c.stream);
+  c.sx_hdr.upload(S.R.tile_hdr, c.stream);
+  c.packed.alloc(np * size_t(S.R.tile_poff8.back()));
+  c.diagL.alloc(np * size_t(L.nT - K0) * kTile * kTile);
+  c.sx_vals.alloc(np * size_t(S.vstride));
+  c.sx_tR.alloc(np * size_t(S.nR));
+  c.sx_F.alloc(np * size_t(S.nF));
+}
+
 void analyze_patches(Context& c, int npatch, const int32_t* vertex, const int64_t* ptr, const int32_t* dofs,
                      const int32_t* perm, const int32_t* star_cells);
 void analyze_dg_patches(Context& c, int npatch, const int32_t* vertex, const int64_t* ptr, const int32_t* dofs,
@@ -867,7 +940,8 @@ fdmgpu_status fdmgpu_set_patches(fdmgpu_handle h, int32_t npatch, const int32_t*
     // else (C5: 63.5 GB) the records are packed in place after the factorisation.
     // FDMGPU_PACK=inplace forces the latter.
     c.packed.reset();
-    {
+    fdmgpu::setup_schur_split(c);
+    if (!c.sx.on) {
       const char* pk = std::getenv("FDMGPU_PACK");
       const size_t rec_bytes = size_t(npatch) * size_t(L.tile_poff8.back()) * sizeof(double);
       size_t fb = 0, tb = 0;
@@ -990,6 +1064,7 @@ fdmgpu_status fdmgpu_factor(fdmgpu_handle h) {
       fdmgpu::launch_dg_patch_assemble(c);
     else
       fdmgpu::launch_patch_assemble(c);
+    fdmgpu::launch_schur_setup(c);  // no-op without the Schur split
     fdmgpu::launch_patch_lead(c);
     for (int K = 0; K < c.L.lead_cols; ++K) fdmgpu::launch_patch_pack_col(c, K);
     ++c.fac_epoch;
@@ -1002,7 +1077,9 @@ fdmgpu_status fdmgpu_factor(fdmgpu_handle h) {
       }
       fdmgpu::launch_patch_pack_col(c, K);  // no-op when packing in place
     }
-    if (c.packed.p)
+    if (c.sx.on)
+      fdmgpu::launch_schur_retile(c);  // L_RR -> dense records; the full tiles stay intact
+    else if (c.packed.p)
       fdmgpu::launch_patch_pack_join(c);
     else
       fdmgpu::launch_patch_pack(c);  // dense tiles -> packed 8x8 sub-block records, in place
@@ -1051,8 +1128,26 @@ fdmgpu_status fdmgpu_get_layout(fdmgpu_handle h, fdmgpu_layout* out) {
     L.nnz_L_reference = c.L.nnz_L_reference;
     L.flops_reference = c.L.flops_reference;
     L.separator_order = c.sep_order;
-    L.stream_bytes = int64_t(c.L.tile_poff8.back()) * 8 * c.npatch;
     L.dmma_flops = c.L.dmma_flops;
+    const auto& S = c.sx;
+    if (S.on) {
+      L.stream_bytes = int64_t(S.R.tile_poff8.back()) * 8 * c.npatch;
+      L.schur_split = 1;
+      L.n_top = S.nR;
+      int64_t comp = 0;
+      for (int k = 0; k < S.ncomp; ++k) {
+        int64_t a0 = 0, a1 = 0;
+        for (int i = 0; i < S.c0; ++i) a0 += S.comp0[size_t(k) * S.c0 + i] >= 0;
+        for (int i = 0; i < S.c1; ++i) a1 += S.comp1[size_t(k) * S.c1 + i] >= 0;
+        comp += a1 * a0 + a1 * (a1 + 1) / 2 + a0;
+      }
+      L.solve_values = 2 * S.R.nnz_L + 2 * comp + int64_t(S.rf_col.size() + S.fr_col.size());
+    } else {
+      L.stream_bytes = int64_t(c.L.tile_poff8.back()) * 8 * c.npatch;
+      L.schur_split = 0;
+      L.n_top = 0;
+      L.solve_values = 2 * (c.L.nnz_L - int64_t(c.dim + 1) * c.L.nI);
+    }
     *out = L;
   });
 }

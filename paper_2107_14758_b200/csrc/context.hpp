@@ -86,6 +86,33 @@ struct PatchLayout {
   int64_t nnz_L_reference = 0, flops_reference = 0;         // reference patch_ordering
 };
 
+// Two-level Schur split of the separator solve (schur_split.cpp).  With the
+// plane-by-plane separator order the first two facet planes F = P0 | P1 have
+// diagonal self-couplings, and P0 couples P1 only inside small components
+// (3D: the facets sharing one tangential index, 2(p-1) + 2(p-1) DOFs), so
+// S_FF^{-1} is applied exactly from S_FF's own entries (component-wise: a
+// dense coupling block, the Cholesky inverse of its P1 Schur complement and
+// the P0 diagonal), S_RF / S_FR stay unfactored, and only the dense Cholesky
+// factor of S~_RR = S_RR - S_RF S_FF^{-1} S_FR (the top separator: the last
+// plane, the edges and the vertex) is streamed:
+//   x_R = S~_RR^{-1} (b_R - S_RF S_FF^{-1} b_F),  x_F = S_FF^{-1} (b_F - S_FR x_R).
+// The fill block L_RF (a dense |R| x |P1| block, 62 % of the separator
+// factor's nonzeros at p = 31) is never read by the solve.
+struct SchurSplit {
+  bool on = false;
+  int nF = 0, n0 = 0, n1 = 0, nR = 0;
+  int ncomp = 0, c0 = 0, c1 = 0;          // components; max P0 / P1 members (padded storage)
+  std::vector<int32_t> comp0, comp1;      // ncomp x c0 / c1 separator positions (-1 = pad)
+  std::vector<int32_t> rf_ptr, rf_col;    // S_RF, CSR over R rows (R-local), F columns (separator positions)
+  std::vector<int32_t> fr_ptr, fr_col;    // S_FR, CSR over the F rows in component order, R-local columns
+  std::vector<int32_t> fr_row;            // F row (separator position) of each S_FR row
+  std::vector<int32_t> comp_fr;           // ncomp + 1: component k's S_FR rows (its P0 members, then P1)
+  int64_t comp_stride = 0;                // doubles per component: M (c1 x c0), Linv (c1 x c1), d0 (c0)
+  int64_t vstride = 0;                    // doubles per patch: components, S_RF values, S_FR values
+  int64_t rf_off = 0, fr_off = 0;         // value offsets inside a patch's block
+  PatchLayout R;                          // dense tile layout of L_RR (rows / columns nF..m-1)
+};
+
 // Device-resident PCG scalars (kernels/pcg.cu).
 struct PcgDev {
   double bnorm, rtol, rz, rz_new, pAp, alpha, beta, res;
@@ -167,7 +194,16 @@ struct Context {
   cudaStream_t pack_stream = nullptr;
   cudaEvent_t pack_ev = nullptr;
   std::vector<int32_t> h_pdofs, h_pcells;
-  int solve_cs = 0;                      // CTAs per split patch (FDMGPU_SOLVE_CS; 0 = auto, 1 = no split)
+  // Schur-split solve (SchurSplit above; FDMGPU_SCHUR=0 keeps the full-factor stream)
+  SchurSplit sx;
+  bool schur_enabled = true;
+  DevArray<int32_t> sx_comp0, sx_comp1, sx_comp_fr, sx_rf_ptr, sx_rf_col, sx_fr_ptr, sx_fr_col, sx_fr_row, sx_pdofs, sx_pairs, sx_tidx;
+  DevArray<int32_t> sx_tile_row, sx_tile_col, sx_col_start, sx_poff8, sx_bptr, sx_blk;
+  DevArray<int64_t> sx_ccol;
+  DevArray<uint8_t> sx_hdr;
+  DevArray<double> sx_vals, sx_tR, sx_F, diagL;  // per-patch values; R right-hand sides; F work; L_KK of R tiles
+  int sx_K0 = 0;                                 // first full-factor tile column overlapping R
+  int solve_cs = 0;                     // CTAs per split patch (FDMGPU_SOLVE_CS; 0 = auto, 1 = no split)
   bool solve_tail = true;                // cluster-split only the last partial wave (FDMGPU_SOLVE_TAIL)
   int cl_cs = 0;                         // cluster size cl_list / cl_col were built for
   DevArray<int32_t> cl_list, cl_col;     // per-rank tile lists of the cluster solve
@@ -293,6 +329,8 @@ void launch_patch_lead(Context& c);
 void launch_patch_pack(Context& c);
 void launch_patch_pack_col(Context& c, int K);   // separate record buffer, side stream
 void launch_patch_pack_join(Context& c);
+void launch_schur_setup(Context& c);   // Schur split: S_FF components, S_RF / S_FR values (any time after set_cell_coeffs)
+void launch_schur_retile(Context& c);  // Schur split: L_RR records from the factored tiles
 void launch_patch_solve(Context& c, const double* r_modal);          // writes c.corr
 void launch_patch_gather(Context& c, double* z_modal);
 void launch_axpby(Context& c, int64_t n, double a, const double* x, double b, const double* y, double* out);

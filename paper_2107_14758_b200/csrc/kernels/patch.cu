@@ -36,6 +36,10 @@ struct PatchArgs {
   const double* Bt;
   unsigned long long* err;
   int64_t rec_stride;  // doubles per patch in the solve-record buffer
+  int64_t out_stride;  // solve output: corr + j * out_stride + out_off (the separator solution)
+  int out_off;
+  double* diagL;       // Schur split: L_KK of the diagonal tiles K >= diagK0 (npatch x diagNT tiles), or null
+  int diagK0, diagNT;
 };
 
 PatchArgs make_args(Context& c) {
@@ -59,6 +63,11 @@ PatchArgs make_args(Context& c) {
   a.At = c.At.p;
   a.Bt = c.Bt.p;
   a.err = c.d_err.p;
+  a.out_stride = c.L.m;
+  a.out_off = 0;
+  a.diagL = c.sx.on ? c.diagL.p : nullptr;
+  a.diagK0 = c.sx_K0;
+  a.diagNT = c.L.nT - c.sx_K0;
   return a;
 }
 
@@ -174,7 +183,7 @@ __device__ double schur_entry(const PatchArgs& a, const double* __restrict__ mu_
 }
 
 __device__ __forceinline__ void record_pivot_error(unsigned long long* err, int patch, int pivot) {
-  atomicMin(err, (static_cast<unsigned long long>(patch) << 32) | static_cast<unsigned>(pivot));
+  if (err) atomicMin(err, (static_cast<unsigned long long>(patch) << 32) | static_cast<unsigned>(pivot));
 }
 
 // Separator Schur complement S_G on the structural nonzeros only (`entries`,
@@ -388,6 +397,13 @@ __device__ void diag_factor_invert(double* Dm, double* Wm, double* out, const Pa
   for (int e = tid; e < TT; e += blockDim.x) {
     const int r = e % T, cc = e / T;
     out[tsw(r, cc)] = r >= cc ? Dm[cc * LD + r] : 0.0;
+  }
+  if (a.diagL && K >= a.diagK0 && patch >= 0) {  // the Schur split re-tiles L_RR from L itself
+    double* o = a.diagL + (size_t(patch) * a.diagNT + (K - a.diagK0)) * TT;
+    for (int e = tid; e < TT; e += blockDim.x) {
+      const int r = e % T, cc = e / T;
+      o[tsw(r, cc)] = r >= cc ? Lp[size_t(cc >> 2) * T * 4 + r * 4 + (cc & 3)] : 0.0;
+    }
   }
 }
 
@@ -1074,7 +1090,7 @@ __global__ void __launch_bounds__(kSolveThreads)
   }
 
   // ---- phase D: write the separator solution x_G (interiors are rebuilt per cell)
-  double* cj = corr + size_t(j) * a.m;
+  double* cj = corr + size_t(j) * a.out_stride + a.out_off;
   for (int r = tid; r < a.m; r += NC) cj[r] = y[r];
   if (tail_ctas > 0 && blockIdx.x == 0 && tid == 0) {
     // tail_sync[0]: finished tail CTAs (cumulative), [1]: calls completed
@@ -1334,7 +1350,7 @@ __global__ void __launch_bounds__(kSolveThreads)
       mbar_wait(&bbar[K], 0);
     }
     named_sync(1, NC);
-    double* cj = corr + size_t(j) * a.m;
+    double* cj = corr + size_t(j) * a.out_stride + a.out_off;
     for (int r = tid; r < a.m; r += NC)
       if ((r / T) % CS == rank) cj[r] = y[r];
   }
@@ -1362,6 +1378,391 @@ __global__ void k_patch_gather(int64_t ndof, const double* __restrict__ corr, co
   double s = q1 > q0 ? corr[i0] : 0.0;
   for (int q = q0 + 1; q < q1; ++q) s += corr[idx[q]];
   z[g] = s;
+}
+
+
+// ---- Schur split of the separator solve (SchurSplit, context.hpp; schur_split.cpp) --------
+// Block elimination with F = P0 | P1 (the first two facet planes) and R (the
+// last plane, edges, vertex):
+//   x_R = S~_RR^{-1} (b_R - S_RF S_FF^{-1} b_F),  x_F = S_FF^{-1} (b_F - S_FR x_R),
+// S~_RR's Cholesky factor L_RR is the R block of the full separator factor
+// (re-tiled from it after the factorisation), S_FF^{-1} is applied per
+// component: with M = S_{P1,P0} of the component, D0 = diag S_{P0,P0} and
+// W = chol(diag S_{P1,P1} - M D0^{-1} M^T)^{-1},
+//   x1 = W^T W (b1 - M D0^{-1} b0),  x0 = D0^{-1} (b0 - M^T x1).
+struct SchurArgs {
+  int nF, nR, m, ncomp, c0, c1;
+  int64_t vstride, comp_stride, rf_off, fr_off;
+  const int32_t* comp0;
+  const int32_t* comp1;
+  const int32_t* comp_fr;
+  const int32_t* rf_ptr;
+  const int32_t* rf_col;
+  const int32_t* fr_ptr;
+  const int32_t* fr_col;
+  const int32_t* fr_row;
+  double* vals;
+};
+
+SchurArgs make_schur_args(Context& c) {
+  const SchurSplit& S = c.sx;
+  SchurArgs s;
+  s.nF = S.nF;
+  s.nR = S.nR;
+  s.m = c.L.m;
+  s.ncomp = S.ncomp;
+  s.c0 = S.c0;
+  s.c1 = S.c1;
+  s.vstride = S.vstride;
+  s.comp_stride = S.comp_stride;
+  s.rf_off = S.rf_off;
+  s.fr_off = S.fr_off;
+  s.comp0 = c.sx_comp0.p;
+  s.comp1 = c.sx_comp1.p;
+  s.comp_fr = c.sx_comp_fr.p;
+  s.rf_ptr = c.sx_rf_ptr.p;
+  s.rf_col = c.sx_rf_col.p;
+  s.fr_ptr = c.sx_fr_ptr.p;
+  s.fr_col = c.sx_fr_col.p;
+  s.fr_row = c.sx_fr_row.p;
+  s.vals = c.sx_vals.p;
+  return s;
+}
+
+// Patch-star coefficients and the 1D tables in shared memory (as k_patch_assemble).
+__device__ __forceinline__ int load_patch_coeffs(const PatchArgs& a, int j, double* At, double* Bt, double* mup) {
+  const int ncorner = 1 << a.dim;
+  for (int i = threadIdx.x; i < a.n1 * a.n1; i += blockDim.x) {
+    At[i] = a.At[i];
+    Bt[i] = a.Bt[i];
+  }
+  int smask = 0;
+  for (int s = 0; s < ncorner; ++s) smask |= (a.pcells[size_t(j) * ncorner + s] >= 0) << s;
+  for (int i = threadIdx.x; i < ncorner * a.dim; i += blockDim.x) {
+    const int s = i / a.dim, q = i % a.dim, K = a.pcells[size_t(j) * ncorner + s];
+    mup[i] = K >= 0 ? a.mu[size_t(K) * a.dim + q] : 0.0;
+  }
+  return smask;
+}
+
+// S_G(r, c) of patch j as the assembly writes it (absent positions of a
+// boundary star: decoupled identity rows).
+__device__ __forceinline__ double sg_entry(const PatchArgs& a, const int32_t* sep, bool whole, const double* mup,
+                                           int smask, int r, int c, const double* At, const double* Bt) {
+  if (!whole && (sep[r] < 0 || sep[c] < 0)) return r == c ? 1.0 : 0.0;
+  return schur_entry(a, mup, smask, r, c, At, Bt);
+}
+
+// S_RF and S_FR values (`pairs`: r | c << 16, S_RF's entries then S_FR's).
+__global__ void k_schur_couplings(PatchArgs a, SchurArgs s, int npairs, const int32_t* __restrict__ pairs) {
+  extern __shared__ double sm[];
+  double* At = sm;
+  double* Bt = At + a.n1 * a.n1;
+  double* mup = Bt + a.n1 * a.n1;
+  const int j = blockIdx.y;
+  const int smask = load_patch_coeffs(a, j, At, Bt, mup);
+  __syncthreads();
+  const int32_t* sep = a.psep + size_t(j) * a.m;
+  const bool whole = smask == (1 << (1 << a.dim)) - 1;
+  double* out = s.vals + size_t(j) * s.vstride + s.rf_off;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < npairs; e += gridDim.x * blockDim.x) {
+    const unsigned pc = unsigned(pairs[e]);
+    out[e] = sg_entry(a, sep, whole, mup, smask, int(pc & 0xffffu), int(pc >> 16), At, Bt);
+  }
+}
+
+// Per (component, patch): M, D0 and W = chol(S'_11)^{-1} (diag_factor_invert
+// on the 64x64 identity-padded matrix).  256 threads.
+__global__ void __launch_bounds__(256) k_schur_comps(PatchArgs a, SchurArgs s) {
+  extern __shared__ __align__(128) double sm[];
+  constexpr int LD = T + 1;
+  double* Dm = sm;                        // 64 x 65
+  double* Wm = Dm + T * LD;               // 16 x 64 x 4 + 64
+  double* Wo = Wm + 16 * T * 4 + T;       // 64 x 64 swizzled L^{-1}
+  double* M = Wo + TT;                    // 64 x 65
+  double* d0 = M + T * LD;                // 64
+  double* d1 = d0 + T;                    // 64
+  double* At = d1 + T;
+  double* Bt = At + a.n1 * a.n1;
+  double* mup = Bt + a.n1 * a.n1;  // 24
+  const int k = blockIdx.x, j = blockIdx.y, tid = threadIdx.x;
+  const int smask = load_patch_coeffs(a, j, At, Bt, mup);
+  __syncthreads();
+  const int32_t* sep = a.psep + size_t(j) * a.m;
+  const bool whole = smask == (1 << (1 << a.dim)) - 1;
+  const int32_t* m0 = s.comp0 + size_t(k) * s.c0;
+  const int32_t* m1 = s.comp1 + size_t(k) * s.c1;
+  for (int idx = tid; idx < s.c1 * s.c0; idx += blockDim.x) {
+    const int i = idx / s.c0, jj = idx % s.c0, r = m1[i], c = m0[jj];
+    M[i * LD + jj] = (r < 0 || c < 0) ? 0.0 : sg_entry(a, sep, whole, mup, smask, r, c, At, Bt);
+  }
+  for (int jj = tid; jj < s.c0; jj += blockDim.x) {
+    const int c = m0[jj];
+    d0[jj] = c < 0 ? 1.0 : sg_entry(a, sep, whole, mup, smask, c, c, At, Bt);
+  }
+  for (int i = tid; i < s.c1; i += blockDim.x) {
+    const int r = m1[i];
+    d1[i] = r < 0 ? 1.0 : sg_entry(a, sep, whole, mup, smask, r, r, At, Bt);
+  }
+  __syncthreads();
+  for (int idx = tid; idx < TT; idx += blockDim.x) {
+    const int cc = idx / T, r = idx % T;
+    double v = r == cc ? 1.0 : 0.0;
+    if (r < s.c1 && cc < s.c1) {
+      v = r == cc ? d1[r] : 0.0;
+      for (int jj = 0; jj < s.c0; ++jj) v -= M[r * LD + jj] * M[cc * LD + jj] / d0[jj];
+    }
+    Dm[cc * LD + r] = v;
+  }
+  __syncthreads();
+  PatchArgs an = a;
+  an.err = nullptr;  // the full factorisation reports non-SPD pivots
+  an.diagL = nullptr;
+  diag_factor_invert(Dm, Wm, Wo, an, 0, -1);
+  __syncthreads();
+  double* out = s.vals + size_t(j) * s.vstride + size_t(k) * s.comp_stride;
+  const int ldm = s.c0 | 1, ldw = s.c1 | 1;
+  for (int idx = tid; idx < s.c1 * ldm; idx += blockDim.x) {
+    const int i = idx / ldm, jj = idx % ldm;
+    out[idx] = jj < s.c0 ? M[i * LD + jj] : 0.0;
+  }
+  out += s.c1 * ldm;
+  for (int idx = tid; idx < s.c1 * ldw; idx += blockDim.x) {
+    const int i = idx / ldw, q = idx % ldw;
+    out[idx] = q < s.c1 ? Wo[tsw(i, q)] : 0.0;
+  }
+  out += s.c1 * ldw;
+  for (int jj = tid; jj < s.c0; jj += blockDim.x) out[jj] = d0[jj];
+}
+
+// R block of the full separator factor, re-tiled from row / column nF on:
+// tile (I, J) of L_RR; diagonal tiles are inverted (the solve reads
+// L_KK^{-1}), then packed as stream records of the dense R layout.
+__global__ void __launch_bounds__(256) k_schur_retile(PatchArgs a, int nF, int K0, const int32_t* __restrict__ tidx,
+                                                      const int32_t* __restrict__ rrow,
+                                                      const int32_t* __restrict__ rcol,
+                                                      const int32_t* __restrict__ bptr, const int32_t* __restrict__ blk,
+                                                      const int64_t* __restrict__ ccol,
+                                                      const int32_t* __restrict__ poff8,
+                                                      const uint8_t* __restrict__ hdr, const double* __restrict__ tiles,
+                                                      const double* __restrict__ diagL, double* __restrict__ packed,
+                                                      int64_t pstride) {
+  extern __shared__ __align__(128) double sm[];
+  double* cur = sm;      // TT
+  double* Lm = sm + TT;  // T x (T + 1)
+  const int t = blockIdx.x, j = blockIdx.y, tid = threadIdx.x;
+  const int I = rrow[t], J = rcol[t];
+  const bool diag = I == J;
+  const double* tb = tiles + size_t(j) * a.ntiles * TT;
+  const double* db = diagL + size_t(j) * a.diagNT * TT;
+  for (int e = tid; e < TT; e += blockDim.x) {
+    const int r = e % T, cc = e / T;
+    const int R0 = nF + I * T + r, C0 = nF + J * T + cc;
+    double v = 0.0;
+    if (R0 >= a.m || C0 >= a.m)
+      v = (diag && r == cc) ? 1.0 : 0.0;  // padding: identity
+    else if (C0 <= R0) {
+      const int oI = R0 / T, oJ = C0 / T;
+      const int idx = tsw(R0 % T, C0 % T);
+      v = oI == oJ ? db[size_t(oI - K0) * TT + idx] : tb[size_t(tidx[oI * a.nT + oJ]) * TT + idx];
+    }
+    if (diag)
+      Lm[cc * (T + 1) + r] = v;
+    else
+      cur[tsw(r, cc)] = v;
+  }
+  __syncthreads();
+  if (diag) {
+    // W = L^{-1} by columns: W(k, c) = (delta_kc - sum_{c <= q < k} L(k, q) W(q, c)) / L(k, k)
+    double* Wc = cur;  // column-major scratch, then swizzled
+    if (tid < T) {
+      const int c = tid;
+      for (int kk = 0; kk < c; ++kk) Wc[c * T + kk] = 0.0;
+      for (int kk = c; kk < T; ++kk) {
+        double sum = kk == c ? 1.0 : 0.0;
+        for (int q = c; q < kk; ++q) sum -= Lm[q * (T + 1) + kk] * Wc[c * T + q];
+        Wc[c * T + kk] = sum / Lm[kk * (T + 1) + kk];
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < TT; e += blockDim.x) Lm[(e / T) * (T + 1) + e % T] = Wc[e];
+    __syncthreads();
+    for (int e = tid; e < TT; e += blockDim.x) {
+      const int r = e % T, cc = e / T;
+      cur[tsw(r, cc)] = Lm[cc * (T + 1) + r];
+    }
+    __syncthreads();
+  }
+  write_record(cur, packed + size_t(j) * pstride + poff8[t], hdr + size_t(t) * kHdrHost, blk + bptr[t], ccol + bptr[t]);
+}
+
+// S_FF^{-1} of one component (128 threads): the component's value block --
+// M (c1 x c0, row stride c0|1), W = chol(S'_11)^{-1} (c1 x c1 lower, row
+// stride c1|1), D0 (c0) -- arrives in shared memory by one TMA bulk copy
+// issued at entry; b from the S^T output (mode 0, forward half) or from
+// c_F = b_F - S_FR x_R (mode 1, backward half).  Every product runs two
+// threads per output (row or column halves, combined by one shuffle); the odd
+// row strides make both row-wise and column-wise reads conflict free.
+// Output: mode 0 -> Fw (npatch x nF), mode 1 -> corr (F part of the separator solution).
+constexpr int kCompThreads = 128;
+__global__ void __launch_bounds__(kCompThreads) k_schur_comp(PatchArgs a, SchurArgs s, const double* __restrict__ rt,
+                                                             const double* __restrict__ cF, double* __restrict__ out,
+                                                             int mode) {
+  extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ double b0[64], b1[64], t0[64], t1[64];
+  const int k = blockIdx.x, j = blockIdx.y, tid = threadIdx.x;
+  const int c0 = s.c0, c1 = s.c1, ldm = c0 | 1, ldw = c1 | 1;
+  const double* src = s.vals + size_t(j) * s.vstride + size_t(k) * s.comp_stride;
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    mbar_fence_init();
+    const uint32_t bytes = uint32_t(s.comp_stride * sizeof(double));
+    mbar_arrive_expect_tx(&bar, bytes);
+    bulk_g2s(sm, src, bytes, &bar);  // values do not depend on the predecessor
+  }
+  __syncthreads();  // the barrier is initialised before anyone waits on it
+  const int32_t* m0 = s.comp0 + size_t(k) * c0;
+  const int32_t* m1 = s.comp1 + size_t(k) * c1;
+  const int32_t* sep = a.psep + size_t(j) * a.m;
+  int p0 = -1, p1 = -1, g0 = -1, g1 = -1;
+  if (tid < c0) {
+    p0 = m0[tid];
+    g0 = p0 >= 0 ? (mode == 0 ? sep[p0] : p0) : -1;
+  }
+  if (tid < c1) {
+    p1 = m1[tid];
+    g1 = p1 >= 0 ? (mode == 0 ? sep[p1] : p1) : -1;
+  }
+  pdl_trigger();
+  pdl_wait();
+  const double* bsrc = mode == 0 ? rt : cF + size_t(j) * s.nF;
+  if (tid < 64) {
+    b0[tid] = g0 >= 0 ? bsrc[g0] : 0.0;
+    b1[tid] = g1 >= 0 ? bsrc[g1] : 0.0;
+  }
+  mbar_wait(&bar, 0);
+  const double* M = sm;
+  const double* W = sm + c1 * ldm;
+  const double* d0 = W + c1 * ldw;
+  __syncthreads();
+  if (tid < c0) t0[tid] = b0[tid] / d0[tid];  // u0 = D0^{-1} b0
+  __syncthreads();
+  // thread pair (2 o, 2 o + 1) computes output o; h = half
+  const int o = tid >> 1, h = tid & 1;
+  {  // r1 = b1 - M u0 (rows)
+    double acc = 0.0;
+    if (o < c1) {
+      const double* row = M + o * ldm;
+      for (int q = h; q < c0; q += 2) acc = fma(row[q], t0[q], acc);
+    }
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    if (o < c1 && h == 0) t1[o] = b1[o] - acc;
+  }
+  __syncthreads();
+  {  // y = W r1 (rows, lower)
+    double acc = 0.0;
+    if (o < c1) {
+      const double* row = W + o * ldw;
+      for (int q = h; q <= o; q += 2) acc = fma(row[q], t1[q], acc);
+    }
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    if (o < c1 && h == 0) b1[o] = acc;
+  }
+  __syncthreads();
+  {  // x1 = W^T y (columns)
+    double acc = 0.0;
+    if (o < c1)
+      for (int q = o + h; q < c1; q += 2) acc = fma(W[q * ldw + o], b1[q], acc);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    if (o < c1 && h == 0) t1[o] = acc;
+  }
+  __syncthreads();
+  {  // x0 = D0^{-1} (b0 - M^T x1) (columns)
+    double acc = 0.0;
+    if (o < c0)
+      for (int i = h; i < c1; i += 2) acc = fma(M[i * ldm + o], t1[i], acc);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    if (o < c0 && h == 0) t0[o] = (b0[o] - acc) / d0[o];
+  }
+  __syncthreads();
+  double* op = out + size_t(j) * (mode == 0 ? s.nF : s.m);
+  if (p0 >= 0) op[p0] = t0[tid];
+  if (p1 >= 0) op[p1] = t1[tid];
+}
+
+// Unfilled couplings, one warp per 8 rows (loads of the 8 rows interleaved):
+//   mode 0: t_R = b_R - S_RF w   (rows R, x = Fw, out = tR)
+//   mode 1: c_F = b_F - S_FR x_R (rows F in component order, x = x_R in corr, out = cF)
+__global__ void __launch_bounds__(256) k_schur_spmv(PatchArgs a, SchurArgs s, const double* __restrict__ rt,
+                                                    const double* __restrict__ xin, double* __restrict__ out,
+                                                    int mode) {
+  constexpr int RW = 8;
+  const int j = blockIdx.y, lane = threadIdx.x & 31;
+  const int nrows = mode == 0 ? s.nR : s.nF;
+  const int r0 = (blockIdx.x * 8 + (threadIdx.x >> 5)) * RW;
+  const int32_t* ptr = mode == 0 ? s.rf_ptr : s.fr_ptr;
+  const int32_t* col = mode == 0 ? s.rf_col : s.fr_col;
+  const double* v = s.vals + size_t(j) * s.vstride + (mode == 0 ? s.rf_off : s.fr_off);
+  const double* x = mode == 0 ? xin + size_t(j) * s.nF : xin + size_t(j) * s.m + s.nF;
+  const int32_t* sep = a.psep + size_t(j) * a.m;
+  pdl_trigger();
+  if (r0 >= nrows) return;
+  int e0[RW], e1[RW], pos[RW], g[RW];
+  int len = 0;
+#pragma unroll
+  for (int q = 0; q < RW; ++q) {
+    const int r = r0 + q;
+    e0[q] = r < nrows ? ptr[r] : 0;
+    e1[q] = r < nrows ? ptr[r + 1] : 0;
+    pos[q] = r < nrows ? (mode == 0 ? s.nF + r : s.fr_row[r]) : -1;
+    g[q] = pos[q] >= 0 ? sep[pos[q]] : -1;
+    len = max(len, e1[q] - e0[q]);
+  }
+  pdl_wait();
+  double acc[RW];
+#pragma unroll
+  for (int q = 0; q < RW; ++q) acc[q] = 0.0;
+  // b of this lane's output row, loaded before the row products
+  double bl = 0.0;
+  {
+    int gl = g[0];
+#pragma unroll
+    for (int q = 1; q < RW; ++q)
+      if (lane == q) gl = g[q];
+    if (lane < RW && gl >= 0) bl = rt[gl];
+  }
+  for (int o = lane; o < len; o += 32) {
+    double vv[RW];
+    int cc[RW];
+#pragma unroll
+    for (int q = 0; q < RW; ++q) {
+      const int e = e0[q] + o;
+      const bool in = e < e1[q];
+      vv[q] = in ? v[e] : 0.0;
+      cc[q] = in ? col[e] : 0;
+    }
+#pragma unroll
+    for (int q = 0; q < RW; ++q) acc[q] = fma(vv[q], x[cc[q]], acc[q]);
+  }
+#pragma unroll
+  for (int q = 0; q < RW; ++q) acc[q] = warp_sum(acc[q]);
+  if (lane < RW) {
+    double av = acc[0];
+    int pl = pos[0];
+#pragma unroll
+    for (int q = 1; q < RW; ++q)
+      if (lane == q) {
+        av = acc[q];
+        pl = pos[q];
+      }
+    if (pl >= 0) {
+      if (mode == 0)
+        out[size_t(j) * s.nR + (r0 + lane)] = bl - av;
+      else
+        out[size_t(j) * s.nF + pl] = bl - av;
+    }
+  }
 }
 
 }  // namespace
@@ -1464,10 +1865,24 @@ void launch_patch_trsm(Context& c, int K) {
   FDM_LAUNCH_CHECK(c);
 }
 
+// What the separator solve streams: the full factor's records, or (Schur
+// split) the dense L_RR records with right-hand sides from the split's tR.
+struct SolveView {
+  const PatchLayout* L;
+  const int32_t* col_start;
+  const int32_t* tile_row;
+  const int32_t* poff8;
+  const int32_t* pdofs;
+};
+static SolveView solve_view(const Context& c) {
+  if (c.sx.on) return {&c.sx.R, c.sx_col_start.p, c.sx_tile_row.p, c.sx_poff8.p, c.sx_pdofs.p};
+  return {&c.L, c.col_start.p, c.tile_row.p, c.tile_poff8.p, c.pdofs.p};
+}
+
 // Cluster solve (k_patch_solve_cl): per-rank tile lists, built once per CS.
 static void build_cluster_lists(Context& c, int cs) {
   if (c.cl_cs == cs) return;
-  const auto& L = c.L;
+  const auto& L = *solve_view(c).L;
   std::vector<int32_t> list, colp(size_t(cs) * (L.nT + 1));
   for (int r = 0; r < cs; ++r) {
     colp[size_t(r) * (L.nT + 1)] = int32_t(list.size());
@@ -1484,12 +1899,13 @@ static void build_cluster_lists(Context& c, int cs) {
 
 template <int CS>
 static size_t solve_cl_smem(const Context& c, int* ring_out) {
+  const PatchLayout& L = *solve_view(c).L;
   const size_t budget = 227 * 1024;
-  const size_t fixed = sizeof(double) * (size_t(c.L.mpad) + 2 * kSolveConsumers * T + CS * T + SB8) +
-                       2 * kRingEntries * sizeof(uint64_t) + 3 * size_t(c.L.nT) * sizeof(uint64_t) +
+  const size_t fixed = sizeof(double) * (size_t(L.mpad) + 2 * kSolveConsumers * T + CS * T + SB8) +
+                       2 * kRingEntries * sizeof(uint64_t) + 3 * size_t(L.nT) * sizeof(uint64_t) +
                        kRingEntries * sizeof(int);
   int max_rec = 0;
-  for (int t = 0; t < c.L.ntiles; ++t) max_rec = std::max(max_rec, c.L.tile_poff8[t + 1] - c.L.tile_poff8[t]);
+  for (int t = 0; t < L.ntiles; ++t) max_rec = std::max(max_rec, L.tile_poff8[t + 1] - L.tile_poff8[t]);
   const int ring = fixed < budget ? int(((budget - fixed) / sizeof(double)) & ~size_t(15)) : 0;
   if (ring < max_rec) throw Error(FDMGPU_UNSUPPORTED, "separator too large for the shared-memory cluster solve");
   *ring_out = ring;
@@ -1534,29 +1950,72 @@ template <int CS>
 static void launch_solve_cl(Context& c, const PatchArgs& a, const double* r_modal, int j0) {
   int ring = 0;
   const size_t smem = solve_cl_smem<CS>(c, &ring);
+  const SolveView v = solve_view(c);
   FDM_CUDA(cudaFuncSetAttribute(k_patch_solve_cl<CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
   launch_cluster(c.pdl && !c.timing, CS, k_patch_solve_cl<CS>, dim3((c.npatch - j0) * CS), dim3(kSolveThreads),
-                 smem, c.stream, a, ring, r_modal, c.corr.p, rec_base(c), (const int32_t*)c.pdofs.p,
-                 (const int32_t*)c.tile_row.p, (const int32_t*)c.tile_poff8.p, (const int32_t*)c.cl_list.p,
-                 (const int32_t*)c.cl_col.p, j0, c.tail_sync.p);
+                 smem, c.stream, a, ring, r_modal, c.corr.p, rec_base(c), v.pdofs, v.tile_row, v.poff8,
+                 (const int32_t*)c.cl_list.p, (const int32_t*)c.cl_col.p, j0, c.tail_sync.p);
 }
 
 // Ring size (doubles) of the separator solve: all shared memory left after
 // the separator vector, the backward partials, the zero block and the barriers.
 static int solve_ring(const Context& c, size_t* smem_out) {
+  const PatchLayout& L = *solve_view(c).L;
   const size_t budget = 227 * 1024;
-  const size_t fixed = sizeof(double) * (size_t(c.L.mpad) + kSolveConsumers * T + SB8) +
+  const size_t fixed = sizeof(double) * (size_t(L.mpad) + kSolveConsumers * T + SB8) +
                        2 * kRingEntries * sizeof(uint64_t) + kRingEntries * sizeof(int);
   int max_rec = 0;
-  for (int t = 0; t < c.L.ntiles; ++t) max_rec = std::max(max_rec, c.L.tile_poff8[t + 1] - c.L.tile_poff8[t]);
+  for (int t = 0; t < L.ntiles; ++t) max_rec = std::max(max_rec, L.tile_poff8[t + 1] - L.tile_poff8[t]);
   const int ring = fixed < budget ? int(((budget - fixed) / sizeof(double)) & ~size_t(15)) : 0;
   if (ring < max_rec) throw Error(FDMGPU_UNSUPPORTED, "separator too large for the shared-memory solve");
   *smem_out = fixed + size_t(ring) * sizeof(double);
   return ring;
 }
 
+static void launch_dense_solve(Context& c, const PatchArgs& a, const double* r_modal);
+
 void launch_patch_solve(Context& c, const double* r_modal) {
+  KernelTimer timer(c, 0);  // one interval for the whole separator solve (all launches)
   PatchArgs a = make_args(c);
+  if (!c.sx.on) {
+    launch_dense_solve(c, a, r_modal);
+    return;
+  }
+  const SchurSplit& S = c.sx;
+  const SchurArgs s = make_schur_args(c);
+  const bool pdl = c.pdl && !c.timing;
+  const size_t csm = sizeof(double) * size_t(S.comp_stride);
+  FDM_CUDA(cudaFuncSetAttribute(k_schur_comp, cudaFuncAttributeMaxDynamicSharedMemorySize, int(csm)));
+  const dim3 cgrid(S.ncomp, c.npatch);
+  // w = S_FF^{-1} b_F;  t_R = b_R - S_RF w
+  launch_pdl(pdl, k_schur_comp, cgrid, dim3(kCompThreads), csm, c.stream, a, s, r_modal, (const double*)nullptr,
+             c.sx_F.p, 0);
+  FDM_LAUNCH_CHECK(c);
+  launch_pdl(pdl, k_schur_spmv, dim3((S.nR + 63) / 64, c.npatch), dim3(256), size_t(0), c.stream, a, s, r_modal,
+             (const double*)c.sx_F.p, c.sx_tR.p, 0);
+  FDM_LAUNCH_CHECK(c);
+  // x_R = S~_RR^{-1} t_R (dense stream) -> corr[nF..m)
+  PatchArgs aR = a;
+  aR.m = S.R.m;
+  aR.mpad = S.R.mpad;
+  aR.nT = S.R.nT;
+  aR.ntiles = S.R.ntiles;
+  aR.rec_stride = int64_t(S.R.tile_poff8.back());
+  aR.out_stride = c.L.m;
+  aR.out_off = S.nF;
+  launch_dense_solve(c, aR, c.sx_tR.p);
+  // c_F = b_F - S_FR x_R;  x_F = S_FF^{-1} c_F -> corr[0..nF)
+  launch_pdl(pdl, k_schur_spmv, dim3((S.nF + 63) / 64, c.npatch), dim3(256), size_t(0), c.stream, a, s, r_modal,
+             (const double*)c.corr.p, c.sx_F.p, 1);
+  FDM_LAUNCH_CHECK(c);
+  launch_pdl(pdl, k_schur_comp, cgrid, dim3(kCompThreads), csm, c.stream, a, s, r_modal, (const double*)c.sx_F.p,
+             c.corr.p, 1);
+  FDM_LAUNCH_CHECK(c);
+}
+
+static void launch_dense_solve(Context& c, const PatchArgs& a, const double* r_modal) {
+  const SolveView v = solve_view(c);
+  const PatchLayout& L = *v.L;
   // Patches [0, nsolo): one CTA each (full waves); [nsolo, npatch): the last
   // partial wave, each patch split over several SMs (all patches when
   // solve_tail is off).  The split launch goes first and triggers the
@@ -1565,11 +2024,10 @@ void launch_patch_solve(Context& c, const double* r_modal) {
   // waits for that grid sees both.
   int nsolo = 0;
   unsigned tail_ctas = 0;
-  KernelTimer timer(c, 0);  // one interval for the whole separator solve (both launches)
   // Split only separators of >= 16 tile columns: below that the per-column
   // exchange costs more than the chain it shortens (C2, 8 columns: 41 us
   // split vs 35 us whole).
-  if (c.solve_cs != 1 && c.L.nT >= 16) {
+  if (c.solve_cs != 1 && L.nT >= 16) {
     int nsm = 0;
     FDM_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c.device));
     nsolo = c.solve_tail ? (c.npatch / nsm) * nsm : 0;
@@ -1612,15 +2070,48 @@ void launch_patch_solve(Context& c, const double* r_modal) {
   FDM_CUDA(cudaFuncSetAttribute(k_patch_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
   // (PDL after a split tail even when timing: the overlap is part of the solve)
   launch_pdl(c.pdl && (!c.timing || tail_ctas > 0), k_patch_solve, dim3(nsolo), dim3(kSolveThreads), smem, c.stream, a, ring, r_modal,
-             c.corr.p, rec_base(c), (const int32_t*)c.pdofs.p, (const int32_t*)c.col_start.p,
-             (const int32_t*)c.tile_row.p, (const int32_t*)c.tile_poff8.p, 0, c.tail_sync.p, tail_ctas);
+             c.corr.p, rec_base(c), v.pdofs, v.col_start, v.tile_row, v.poff8, 0, c.tail_sync.p, tail_ctas);
+  FDM_LAUNCH_CHECK(c);
+}
+
+// Schur split, factor side: S_FF components and the S_RF / S_FR values from mu
+// (independent of the factorisation; the same S_G entries as k_patch_assemble).
+void launch_schur_setup(Context& c) {
+  if (!c.sx.on) return;
+  PatchArgs a = make_args(c);
+  const SchurArgs s = make_schur_args(c);
+  KernelTimer timer(c, 1);
+  const size_t smem_c = sizeof(double) * (2 * size_t(c.n1) * c.n1 + 24);
+  const int np = int(c.sx.rf_col.size() + c.sx.fr_col.size());
+  if (np > 0) {
+    dim3 grid(unsigned(std::min(64, (np + 255) / 256)), c.npatch);
+    k_schur_couplings<<<grid, 256, smem_c, c.stream>>>(a, s, np, c.sx_pairs.p);
+    FDM_LAUNCH_CHECK(c);
+  }
+  const size_t smem = sizeof(double) * (size_t(T) * (T + 1) * 2 + 16 * T * 4 + T + TT + 2 * T + 2 * size_t(c.n1) * c.n1 + 24);
+  FDM_CUDA(cudaFuncSetAttribute(k_schur_comps, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  k_schur_comps<<<dim3(c.sx.ncomp, c.npatch), 256, smem, c.stream>>>(a, s);
+  FDM_LAUNCH_CHECK(c);
+}
+
+// Schur split: the R block of the factored tiles -> dense L_RR stream records.
+void launch_schur_retile(Context& c) {
+  if (!c.sx.on) return;
+  PatchArgs a = make_args(c);
+  KernelTimer timer(c, 1);
+  const auto& R = c.sx.R;
+  const size_t smem = sizeof(double) * (TT + size_t(T) * (T + 1));
+  FDM_CUDA(cudaFuncSetAttribute(k_schur_retile, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  k_schur_retile<<<dim3(R.ntiles, c.npatch), 256, smem, c.stream>>>(
+      a, c.sx.nF, c.sx_K0, c.sx_tidx.p, c.sx_tile_row.p, c.sx_tile_col.p, c.sx_bptr.p, c.sx_blk.p, c.sx_ccol.p,
+      c.sx_poff8.p, c.sx_hdr.p, c.tiles.p, c.diagL.p, c.packed.p, int64_t(R.tile_poff8.back()));
   FDM_LAUNCH_CHECK(c);
 }
 
 // Column-wise packing into the separate record buffer (side stream): call
 // after column K's tiles are final (after its trsm).
 void launch_patch_pack_col(Context& c, int K) {
-  if (!c.packed.p) return;
+  if (!c.packed.p || c.sx.on) return;
   if (!c.pack_stream) {
     FDM_CUDA(cudaStreamCreateWithFlags(&c.pack_stream, cudaStreamNonBlocking));
     FDM_CUDA(cudaEventCreateWithFlags(&c.pack_ev, cudaEventDisableTiming));
@@ -1636,7 +2127,7 @@ void launch_patch_pack_col(Context& c, int K) {
 
 // Joins the side stream (the records are complete when the handle stream passes this).
 void launch_patch_pack_join(Context& c) {
-  if (!c.packed.p || !c.pack_stream) return;
+  if (!c.packed.p || !c.pack_stream || c.sx.on) return;
   FDM_CUDA(cudaEventRecord(c.pack_ev, c.pack_stream));
   FDM_CUDA(cudaStreamWaitEvent(c.stream, c.pack_ev, 0));
 }

@@ -1,0 +1,209 @@
+// Two-level Schur split of the separator solve: host analysis (see
+// SchurSplit in context.hpp for the algebra).
+//
+// Reference path: CholFactor::solve (src/cholesky.cpp:89-110) applied to the
+// patch matrix of PatchSolver::apply (src/schwarz.cpp:41-54).  The device
+// factorisation is unchanged (the full separator Cholesky, kernels/patch.cu);
+// only what the relaxation streams changes.  With the separator ordered
+// P0 | P1 | R (facet planes 0 and 1 first, layout.cpp "plane" order), block
+// elimination gives the same solution as the full triangular solves up to
+// rounding, while the solve reads the dense factor of the last block
+// (|R| = (2p-1)^2 ... at p = 31: 3781 of 10981 separator DOFs; 7.15 M of the
+// 21.0 M separator-factor nonzeros) and S's own unfilled couplings.
+//
+// Everything here is derived from the canonical symbolic pattern of S_G
+// (L.entries) and checked; when a check fails (reference separator order,
+// DG layouts, 2D with a large P1 block, ...) the split stays off and the
+// full-factor stream is used.
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <numeric>
+
+#include "context.hpp"
+
+namespace fdmgpu {
+
+namespace {
+
+int find(std::vector<int>& par, int x) {
+  while (par[x] != x) x = par[x] = par[par[x]];
+  return x;
+}
+
+// Dense lower tile layout of an nR x nR block with full-block records: 8x8
+// sub-blocks inside the block (diagonal tiles: bi >= bj), a header like
+// symbolic_tiles' (no compact blocks).
+void dense_layout(PatchLayout& R, int nR) {
+  const int T = kTile;
+  R = PatchLayout();
+  R.m = nR;
+  R.nT = (nR + T - 1) / T;
+  R.mpad = R.nT * T;
+  for (int K = 0; K < R.nT; ++K) {
+    R.col_start.push_back(int32_t(R.tile_row.size()));
+    for (int I = K; I < R.nT; ++I) {
+      R.tile_row.push_back(I);
+      R.tile_col.push_back(K);
+    }
+  }
+  R.col_start.push_back(int32_t(R.tile_row.size()));
+  R.ntiles = int(R.tile_row.size());
+  R.tile_mask8.assign(R.ntiles, 0);
+  R.tile_poff8.assign(R.ntiles + 1, 0);
+  R.tile_hdr.assign(size_t(R.ntiles) * kHdrHost, 0);
+  R.tile_bptr.assign(R.ntiles + 1, 0);
+  const int nb = (nR + 7) / 8;  // 8-row blocks holding a row of the block
+  for (int t = 0; t < R.ntiles; ++t) {
+    const int I = R.tile_row[t], K = R.tile_col[t];
+    uint64_t mask = 0;
+    for (int bi = 0; bi < 8; ++bi)
+      for (int bj = 0; bj < 8; ++bj)
+        if (8 * I + bi < nb && 8 * K + bj < nb && (I != K || bi >= bj)) mask |= uint64_t(1) << (bi * 8 + bj);
+    R.tile_mask8[t] = int64_t(mask);
+    uint8_t* hr = &R.tile_hdr[size_t(t) * kHdrHost];
+    std::fill(hr + kHdrBytes, hr + kHdrHost, uint8_t(0xff));
+    int nf = 0;
+    for (int b = 0; b < 64; ++b) {
+      const uint8_t v = ((mask >> b) & 1) ? uint8_t(nf) : uint8_t(0xff);
+      hr[b] = v;
+      hr[64 + (b & 7) * 8 + (b >> 3)] = v;
+      if ((mask >> b) & 1) {
+        ++nf;
+        R.tile_blk.push_back(b);
+        R.tile_ccol.push_back(0);
+      }
+    }
+    reinterpret_cast<int32_t*>(hr + 128)[0] = nf;
+    reinterpret_cast<int32_t*>(hr + 128)[1] = 0;
+    R.tile_bptr[t + 1] = int32_t(R.tile_blk.size());
+    R.tile_poff8[t + 1] = R.tile_poff8[t] + kHdrBytes / 8 + 64 * nf;
+  }
+  R.nnz_L = int64_t(nR) * (nR + 1) / 2;
+}
+
+}  // namespace
+
+void analyze_schur_split(Context& c) {
+  SchurSplit& S = c.sx;
+  S = SchurSplit();
+  const PatchLayout& L = c.L;
+  const char* env = std::getenv("FDMGPU_SCHUR");
+  if (!c.schur_enabled || (env && env[0] == '0') || c.dg || L.m < 2) return;
+  const int d = c.dim, p = c.p, m = L.m;
+  auto group = [&](int r) {
+    const int32_t v = L.lat[L.nI + r];
+    const int P[3] = {v & 255, (v >> 8) & 255, (v >> 16) & 255};
+    int cnt = 0, ax = 0;
+    for (int a = 0; a < d; ++a)
+      if (P[a] == p) {
+        ++cnt;
+        ax = a;
+      }
+    return cnt == 1 ? ax : d + cnt;  // facet axis, else edge / vertex
+  };
+  // P0 = [0, n0), P1 = [n0, nF) must be the leading contiguous groups 0 and 1
+  int n0 = 0;
+  while (n0 < m && group(n0) == 0) ++n0;
+  int nF = n0;
+  while (nF < m && group(nF) == 1) ++nF;
+  if (n0 == 0 || nF == n0 || nF >= m) return;
+  for (int r = nF; r < m; ++r)
+    if (group(r) <= 1) return;
+  // structural nonzeros (r > c) of S_G
+  std::vector<std::pair<int, int>> pr;
+  pr.reserve(L.entries.size());
+  for (int32_t code : L.entries) {
+    const int t = code >> 12, cc = (code >> 6) & 63, rr = code & 63;
+    const int r = L.tile_row[t] * kTile + rr, col = L.tile_col[t] * kTile + cc;
+    if (r != col) pr.emplace_back(r, col);
+  }
+  std::vector<int> par(nF);
+  std::iota(par.begin(), par.end(), 0);
+  for (auto [r, col] : pr) {
+    if (r < nF && col < nF) {
+      const bool r0 = r < n0, c0 = col < n0;
+      if (r0 == c0) return;  // a coupling inside P0 or inside P1: S_FF is not of the split form
+      par[find(par, r)] = find(par, col);
+    }
+  }
+  // components in order of their smallest position
+  std::vector<int> cid(nF, -1);
+  std::vector<std::vector<int>> m0, m1;
+  for (int r = 0; r < nF; ++r) {
+    const int root = find(par, r);
+    if (cid[root] < 0) {
+      cid[root] = int(m0.size());
+      m0.emplace_back();
+      m1.emplace_back();
+    }
+    (r < n0 ? m0 : m1)[cid[root]].push_back(r);
+  }
+  const int ncomp = int(m0.size());
+  int c0 = 1, c1 = 1;
+  for (int k = 0; k < ncomp; ++k) {
+    c0 = std::max(c0, int(m0[k].size()));
+    c1 = std::max(c1, int(m1[k].size()));
+  }
+  if (c0 > 64 || c1 > 64) return;  // the component kernel holds one component per CTA in registers / smem
+  S.n0 = n0;
+  S.n1 = nF - n0;
+  S.nF = nF;
+  S.nR = m - nF;
+  S.ncomp = ncomp;
+  S.c0 = c0;
+  S.c1 = c1;
+  S.comp0.assign(size_t(ncomp) * c0, -1);
+  S.comp1.assign(size_t(ncomp) * c1, -1);
+  for (int k = 0; k < ncomp; ++k) {
+    std::copy(m0[k].begin(), m0[k].end(), S.comp0.begin() + size_t(k) * c0);
+    std::copy(m1[k].begin(), m1[k].end(), S.comp1.begin() + size_t(k) * c1);
+  }
+  // S_RF (R rows, F columns) and its transpose S_FR (F rows in component order)
+  std::vector<std::vector<int>> rf(S.nR), fr(nF);
+  for (auto [r, col] : pr)
+    if (r >= nF && col < nF) {
+      rf[r - nF].push_back(col);
+      fr[col].push_back(r - nF);
+    }
+  S.rf_ptr.assign(1, 0);
+  for (auto& row : rf) {
+    std::sort(row.begin(), row.end());
+    S.rf_col.insert(S.rf_col.end(), row.begin(), row.end());
+    S.rf_ptr.push_back(int32_t(S.rf_col.size()));
+  }
+  S.fr_ptr.assign(1, 0);
+  S.comp_fr.assign(1, 0);
+  for (int k = 0; k < ncomp; ++k, S.comp_fr.push_back(int32_t(S.fr_row.size())))
+    for (const auto* mem : {&m0[k], &m1[k]})
+      for (int f : *mem) {
+        auto& row = fr[f];
+        std::sort(row.begin(), row.end());
+        S.fr_row.push_back(f);
+        S.fr_col.insert(S.fr_col.end(), row.begin(), row.end());
+        S.fr_ptr.push_back(int32_t(S.fr_col.size()));
+      }
+  // M (c1 rows, stride c0 | 1), W (c1 rows, stride c1 | 1), D0 (c0): odd row strides keep the
+  // component kernel's row-per-thread and column-per-thread reads bank-conflict free
+  S.comp_stride = (int64_t(c1) * (c0 | 1) + int64_t(c1) * (c1 | 1) + c0 + 1) & ~int64_t(1);  // 16-byte aligned
+  S.rf_off = S.comp_stride * ncomp;
+  S.fr_off = S.rf_off + int64_t(S.rf_col.size());
+  S.vstride = (S.fr_off + int64_t(S.fr_col.size()) + 1) & ~int64_t(1);  // 16-byte aligned patch blocks
+  dense_layout(S.R, S.nR);
+  // worth it only when the split reads clearly fewer values than the full
+  // stream (3D: ~0.35 of them; 2D: R is the vertex alone, no gain)
+  int64_t comp = 0;
+  for (int k = 0; k < ncomp; ++k) {
+    const int64_t a0 = int64_t(m0[k].size()), a1 = int64_t(m1[k].size());
+    comp += a1 * a0 + a1 * (a1 + 1) / 2 + a0;
+  }
+  const int64_t split_vals = 2 * S.R.nnz_L + 2 * comp + int64_t(S.rf_col.size() + S.fr_col.size());
+  const int64_t full_vals = 2 * (L.nnz_L - int64_t(d + 1) * L.nI);
+  if (4 * split_vals > 3 * full_vals && !(env && env[0] == '1')) {
+    S = SchurSplit();
+    return;
+  }
+  S.on = true;
+}
+
+}  // namespace fdmgpu

@@ -15,6 +15,7 @@
 namespace fdmgpu {
 void analyze_patches(Context& c, int npatch, const int32_t* vertex, const int64_t* ptr, const int32_t* dofs,
                      const int32_t* perm, const int32_t* star_cells);
+void analyze_schur_split(Context& c);
 }
 
 int main(int argc, char** argv) {
@@ -51,6 +52,16 @@ int main(int argc, char** argv) {
   fdmhost_get_patches(pb, vert.data(), ptr.data(), dofs.data(), perm.data(), cells.data(), col.data());
   fdmgpu::analyze_patches(c, npatch, vert.data(), ptr.data(), dofs.data(), perm.data(), cells.data());
   const auto& L = c.L;
+  fdmgpu::analyze_schur_split(c);
+  {
+    const auto& S = c.sx;
+    const double dense = double(S.R.tile_poff8.empty() ? 0 : S.R.tile_poff8.back()) * 8;
+    const double vals = double(S.vstride) * 8;
+    std::printf("schur split %d: n0 %d n1 %d nR %d comps %d (c0 %d c1 %d) rf nnz %zu fr nnz %zu; R tiles %d records %.0f B, "
+                "values %.0f B (components %.0f B); per sweep (fwd+bwd records, comps x2, rf, fr) %.0f B\n",
+                int(S.on), S.n0, S.n1, S.nR, S.ncomp, S.c0, S.c1, S.rf_col.size(), S.fr_col.size(), S.R.ntiles, dense,
+                vals, 8.0 * S.rf_off, 2 * dense + 2 * 8.0 * S.rf_off + 8.0 * (S.rf_col.size() + S.fr_col.size()));
+  }
   int64_t blocks8 = 0, diag_blocks = 0;
   for (int t = 0; t < L.ntiles; ++t) {
     const int b = __builtin_popcountll(uint64_t(L.tile_mask8[t]));
