@@ -25,13 +25,14 @@ void analyze_schur_split(Context& c);
 // off (full-factor stream) when the layout does not split or memory is short.
 void setup_schur_split(Context& c) {
   c.sx = SchurSplit();
-  for (auto* a : {&c.sx_comp0, &c.sx_comp1, &c.sx_comp_fr, &c.sx_rf_ptr, &c.sx_rf_col, &c.sx_fr_ptr, &c.sx_fr_col,
+  for (auto* a : {&c.sx_comp0, &c.sx_comp1, &c.sx_comp_fr, &c.sx_rf_blk, &c.sx_fr_blk, &c.sx_rf_ptr, &c.sx_rf_col, &c.sx_fr_ptr, &c.sx_fr_col,
                   &c.sx_fr_row, &c.sx_pdofs, &c.sx_pairs, &c.sx_tidx, &c.sx_tile_row, &c.sx_tile_col, &c.sx_col_start,
                   &c.sx_poff8, &c.sx_bptr, &c.sx_blk})
     a->reset();
   c.sx_ccol.reset();
   c.sx_hdr.reset();
-  for (auto* a : {&c.sx_vals, &c.sx_tR, &c.sx_F, &c.diagL}) a->reset();
+  for (auto* a : {&c.sx_vals, &c.sx_tR, &c.sx_F, &c.diagL, &c.sx_UT, &c.sx_part}) a->reset();
+  c.sx_chunk.reset();
   if (c.dg) return;
   analyze_schur_split(c);
   SchurSplit& S = c.sx;
@@ -39,8 +40,35 @@ void setup_schur_split(Context& c) {
   const auto& L = c.L;
   const int K0 = S.nF / kTile;
   const size_t np = size_t(c.npatch);
-  const size_t need = sizeof(double) * (np * size_t(S.R.tile_poff8.back()) + np * size_t(L.nT - K0) * kTile * kTile +
-                                        np * size_t(S.vstride) + np * size_t(S.nR + S.nF));
+  const size_t tt = size_t(kTile) * kTile, rtiles = size_t(S.R.ntiles) * tt;
+  const size_t rec = S.inv ? std::max(size_t(S.R.tile_poff8.back()), rtiles) : size_t(S.R.tile_poff8.back());
+  if (S.inv) {  // symmetric product: chunks per patch so that npatch x nchunk CTAs fill whole waves
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c.device);
+    int best = 1;
+    double best_eff = 0.0;
+    for (int g = 1; g <= 16; ++g) {
+      if (g > S.R.ntiles) break;
+      const double waves = double(c.npatch) * g / nsm, eff = waves / std::ceil(waves);
+      if (eff > best_eff + 0.01 || (g >= 4 && best < 4 && eff > best_eff - 0.05)) {
+        best = g;
+        best_eff = eff;
+      }
+    }
+    S.nchunk = best;
+    S.chunk_start.assign(1, 0);
+    const int64_t total = S.R.tile_poff8.back();
+    for (int g = 1; g < S.nchunk; ++g) {
+      const int64_t target = total * g / S.nchunk;
+      int t = S.chunk_start.back();
+      while (t < S.R.ntiles && S.R.tile_poff8[t] < target) ++t;
+      S.chunk_start.push_back(t);
+    }
+    S.chunk_start.push_back(S.R.ntiles);
+  }
+  const size_t need = sizeof(double) * (np * rec + np * size_t(L.nT - K0) * tt + np * size_t(S.vstride) +
+                                        np * size_t(S.nR + S.nF) +
+                                        (S.inv ? np * rtiles + np * S.nchunk * size_t(S.R.mpad) : 0));
   size_t fb = 0, tb = 0;
   FDM_CUDA(cudaMemGetInfo(&fb, &tb));
   if (need + (size_t(1) << 30) > fb) {  // keep 1 GiB of headroom for work vectors
@@ -56,17 +84,21 @@ void setup_schur_split(Context& c) {
         S = SchurSplit();
         return;
       }
-  std::vector<int32_t> pairs;
+  // (r | c << 16) of every stored coupling value (S_RF then S_FR, block padding -1 = zero)
+  std::vector<int32_t> pairs(S.rf_col.size() + S.fr_col.size(), -1);
   for (int r = 0; r < S.nR; ++r)
-    for (int e = S.rf_ptr[r]; e < S.rf_ptr[r + 1]; ++e) pairs.push_back((S.nF + r) | (S.rf_col[e] << 16));
+    for (int e = S.rf_ptr[r]; e < S.rf_ptr[r + 1]; ++e) pairs[e] = (S.nF + r) | (S.rf_col[e] << 16);
   for (size_t f = 0; f < S.fr_row.size(); ++f)
-    for (int e = S.fr_ptr[f]; e < S.fr_ptr[f + 1]; ++e) pairs.push_back(S.fr_row[f] | ((S.nF + S.fr_col[e]) << 16));
+    for (int e = S.fr_ptr[f]; e < S.fr_ptr[f + 1]; ++e)
+      pairs[S.rf_col.size() + e] = S.fr_row[f] | ((S.nF + S.fr_col[e]) << 16);
   std::vector<int32_t> rp(np * S.nR);
   for (size_t i = 0; i < rp.size(); ++i) rp[i] = int32_t(i);
   c.sx_K0 = K0;
   c.sx_comp0.upload(S.comp0, c.stream);
   c.sx_comp1.upload(S.comp1, c.stream);
   c.sx_comp_fr.upload(S.comp_fr, c.stream);
+  c.sx_rf_blk.upload(S.rf_blk, c.stream);
+  c.sx_fr_blk.upload(S.fr_blk, c.stream);
   c.sx_rf_ptr.upload(S.rf_ptr, c.stream);
   c.sx_rf_col.upload(S.rf_col.empty() ? std::vector<int32_t>{0} : S.rf_col, c.stream);
   c.sx_fr_ptr.upload(S.fr_ptr, c.stream);
@@ -83,7 +115,12 @@ void setup_schur_split(Context& c) {
   c.sx_blk.upload(S.R.tile_blk, c.stream);
   c.sx_ccol.upload(S.R.tile_ccol, c.stream);
   c.sx_hdr.upload(S.R.tile_hdr, c.stream);
-  c.packed.alloc(np * size_t(S.R.tile_poff8.back()));
+  c.packed.alloc(np * rec);
+  if (S.inv) {
+    c.sx_UT.alloc(np * rtiles);
+    c.sx_part.alloc(np * S.nchunk * size_t(S.R.mpad));
+    c.sx_chunk.upload(S.chunk_start, c.stream);
+  }
   c.diagL.alloc(np * size_t(L.nT - K0) * kTile * kTile);
   c.sx_vals.alloc(np * size_t(S.vstride));
   c.sx_tR.alloc(np * size_t(S.nR));
@@ -1141,7 +1178,7 @@ fdmgpu_status fdmgpu_get_layout(fdmgpu_handle h, fdmgpu_layout* out) {
         for (int i = 0; i < S.c1; ++i) a1 += S.comp1[size_t(k) * S.c1 + i] >= 0;
         comp += a1 * a0 + a1 * (a1 + 1) / 2 + a0;
       }
-      L.solve_values = 2 * S.R.nnz_L + 2 * comp + int64_t(S.rf_col.size() + S.fr_col.size());
+      L.solve_values = 2 * S.R.nnz_L + 2 * comp + S.rf_nnz + S.fr_nnz;
     } else {
       L.stream_bytes = int64_t(c.L.tile_poff8.back()) * 8 * c.npatch;
       L.schur_split = 0;

@@ -18,6 +18,7 @@ constexpr int kTile = 64;  // dense tile edge of the interface factor
 constexpr int kHdrBytes = 144;  // solve-record header: 2 x 64 sub-block indices + full / compact counts
 constexpr int kCompact = 10;    // doubles per compact 8x8 sub-block (8 row values + 8 column bytes + pad)
 constexpr int kHdrHost = kHdrBytes + 128;  // host tile_hdr stride: record header + compact index table
+constexpr int kSpmvRows = 32;   // rows per block of the Schur split's coupling products
 
 struct Error : std::runtime_error {
   fdmgpu_status status;
@@ -107,10 +108,16 @@ struct SchurSplit {
   std::vector<int32_t> fr_ptr, fr_col;    // S_FR, CSR over the F rows in component order, R-local columns
   std::vector<int32_t> fr_row;            // F row (separator position) of each S_FR row
   std::vector<int32_t> comp_fr;           // ncomp + 1: component k's S_FR rows (its P0 members, then P1)
+  std::vector<int32_t> rf_blk, fr_blk;    // entry offset of every kSpmvRows-row block (4-aligned; + end)
+  int rf_bmax = 0, fr_bmax = 0;           // largest block (entries, padding included)
+  int64_t rf_nnz = 0, fr_nnz = 0;         // structural entries (without the block padding)
   int64_t comp_stride = 0;                // doubles per component: M (c1 x c0), Linv (c1 x c1), d0 (c0)
   int64_t vstride = 0;                    // doubles per patch: components, S_RF values, S_FR values
   int64_t rf_off = 0, fr_off = 0;         // value offsets inside a patch's block
-  PatchLayout R;                          // dense tile layout of L_RR (rows / columns nF..m-1)
+  PatchLayout R;                          // dense tile layout of L_RR / S~_RR^{-1} (rows / columns nF..m-1)
+  bool inv = true;                        // stream S~_RR^{-1} (symmetric, one pass) instead of L_RR (two passes)
+  int nchunk = 1;                         // inverse: CTAs per patch of the symmetric product
+  std::vector<int32_t> chunk_start;       // nchunk + 1 tile offsets
 };
 
 // Device-resident PCG scalars (kernels/pcg.cu).
@@ -197,11 +204,12 @@ struct Context {
   // Schur-split solve (SchurSplit above; FDMGPU_SCHUR=0 keeps the full-factor stream)
   SchurSplit sx;
   bool schur_enabled = true;
-  DevArray<int32_t> sx_comp0, sx_comp1, sx_comp_fr, sx_rf_ptr, sx_rf_col, sx_fr_ptr, sx_fr_col, sx_fr_row, sx_pdofs, sx_pairs, sx_tidx;
+  DevArray<int32_t> sx_comp0, sx_comp1, sx_comp_fr, sx_rf_blk, sx_fr_blk, sx_rf_ptr, sx_rf_col, sx_fr_ptr, sx_fr_col, sx_fr_row, sx_pdofs, sx_pairs, sx_tidx;
   DevArray<int32_t> sx_tile_row, sx_tile_col, sx_col_start, sx_poff8, sx_bptr, sx_blk;
   DevArray<int64_t> sx_ccol;
   DevArray<uint8_t> sx_hdr;
-  DevArray<double> sx_vals, sx_tR, sx_F, diagL;  // per-patch values; R right-hand sides; F work; L_KK of R tiles
+  DevArray<int32_t> sx_chunk;
+  DevArray<double> sx_vals, sx_tR, sx_F, diagL, sx_UT, sx_part;  // per-patch values; R right-hand sides; F work; L_KK of R tiles
   int sx_K0 = 0;                                 // first full-factor tile column overlapping R
   int solve_cs = 0;                     // CTAs per split patch (FDMGPU_SOLVE_CS; 0 = auto, 1 = no split)
   bool solve_tail = true;                // cluster-split only the last partial wave (FDMGPU_SOLVE_TAIL)

@@ -1396,6 +1396,8 @@ struct SchurArgs {
   const int32_t* comp0;
   const int32_t* comp1;
   const int32_t* comp_fr;
+  const int32_t* rf_blk;
+  const int32_t* fr_blk;
   const int32_t* rf_ptr;
   const int32_t* rf_col;
   const int32_t* fr_ptr;
@@ -1420,6 +1422,8 @@ SchurArgs make_schur_args(Context& c) {
   s.comp0 = c.sx_comp0.p;
   s.comp1 = c.sx_comp1.p;
   s.comp_fr = c.sx_comp_fr.p;
+  s.rf_blk = c.sx_rf_blk.p;
+  s.fr_blk = c.sx_fr_blk.p;
   s.rf_ptr = c.sx_rf_ptr.p;
   s.rf_col = c.sx_rf_col.p;
   s.fr_ptr = c.sx_fr_ptr.p;
@@ -1466,8 +1470,9 @@ __global__ void k_schur_couplings(PatchArgs a, SchurArgs s, int npairs, const in
   const bool whole = smask == (1 << (1 << a.dim)) - 1;
   double* out = s.vals + size_t(j) * s.vstride + s.rf_off;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < npairs; e += gridDim.x * blockDim.x) {
-    const unsigned pc = unsigned(pairs[e]);
-    out[e] = sg_entry(a, sep, whole, mup, smask, int(pc & 0xffffu), int(pc >> 16), At, Bt);
+    const int32_t pv = pairs[e];
+    const unsigned pc = unsigned(pv);
+    out[e] = pv < 0 ? 0.0 : sg_entry(a, sep, whole, mup, smask, int(pc & 0xffffu), int(pc >> 16), At, Bt);
   }
 }
 
@@ -1546,7 +1551,7 @@ __global__ void __launch_bounds__(256) k_schur_retile(PatchArgs a, int nF, int K
                                                       const int32_t* __restrict__ poff8,
                                                       const uint8_t* __restrict__ hdr, const double* __restrict__ tiles,
                                                       const double* __restrict__ diagL, double* __restrict__ packed,
-                                                      int64_t pstride) {
+                                                      int64_t pstride, int dense_out) {
   extern __shared__ __align__(128) double sm[];
   double* cur = sm;      // TT
   double* Lm = sm + TT;  // T x (T + 1)
@@ -1593,7 +1598,278 @@ __global__ void __launch_bounds__(256) k_schur_retile(PatchArgs a, int nF, int K
     }
     __syncthreads();
   }
+  if (dense_out) {  // dense swizzled tile t (the inverse-top path inverts L_RR next)
+    double* o = packed + size_t(j) * pstride + size_t(t) * TT;
+    for (int e = tid; e < TT; e += blockDim.x) o[e] = cur[e];
+    return;
+  }
   write_record(cur, packed + size_t(j) * pstride + poff8[t], hdr + size_t(t) * kHdrHost, blk + bptr[t], ccol + bptr[t]);
+}
+
+// Inverse top block, step 1: U = W^T for W = L_RR^{-1}, tile (I, J) of the
+// dense R layout (index col_start[J] + I - J) holding W_IJ^T:
+//   W_JJ = L_JJ^{-1} (the re-tiled diagonal),  W_IJ = -W_II sum_{K=J}^{I-1} L_IK W_KJ  (I > J).
+// CTA per (column J, patch), rows I in order; C^T = sum_K U(K,J) L(I,K)^T and
+// U(I,J) = -C^T W_II^T run on the FP64 tensor pipe (tile_gemm_abt), operands
+// by TMA bulk copy (one stage; three CTAs per SM overlap each other).
+__global__ void __launch_bounds__(kUpdThreads, 3) k_schur_uinv(int nT, const int32_t* __restrict__ col_start,
+                                                              const double* __restrict__ RT, double* __restrict__ UT,
+                                                              int64_t stride) {
+  extern __shared__ __align__(128) double sm[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm);
+  double* buf = sm + 16;  // [A, B][TT]
+  const int J = blockIdx.x, j = blockIdx.y, tid = threadIdx.x;
+  const double* rt = RT + size_t(j) * stride;
+  double* ut = UT + size_t(j) * stride;
+  auto tix = [&](int I, int K) { return col_start[K] + (I - K); };
+  if (tid == 0) {
+    mbar_init(&full[0], 1);
+    mbar_fence_init();
+  }
+  {  // U(J,J) = W_JJ^T
+    const double* d = rt + size_t(tix(J, J)) * TT;
+    double* o = ut + size_t(tix(J, J)) * TT;
+    for (int e = tid; e < TT; e += blockDim.x) {
+      const int r = e % T, c = e / T;
+      o[tsw(r, c)] = d[tsw(c, r)];
+    }
+  }
+  fence_proxy_async_global();
+  __syncthreads();
+  unsigned phase = 0;
+  for (int I = J + 1; I < nT; ++I) {
+    TileAcc acc = {};
+    for (int K = J; K < I; ++K) {
+      if (tid == 0) {
+        mbar_arrive_expect_tx(&full[0], 2 * TT * sizeof(double));
+        bulk_g2s(buf, ut + size_t(tix(K, J)) * TT, TT * sizeof(double), &full[0]);
+        bulk_g2s(buf + TT, rt + size_t(tix(I, K)) * TT, TT * sizeof(double), &full[0]);
+      }
+      mbar_wait(&full[0], phase);
+      phase ^= 1;
+      tile_gemm_abt(buf, buf + TT, acc);
+      __syncthreads();
+    }
+    if (tid == 0) {
+      mbar_arrive_expect_tx(&full[0], TT * sizeof(double));
+      bulk_g2s(buf + TT, rt + size_t(tix(I, I)) * TT, TT * sizeof(double), &full[0]);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) buf[tsw(acc.row(i), acc.col(jj, e))] = acc.v[i][jj][e];
+    __syncthreads();
+    mbar_wait(&full[0], phase);
+    phase ^= 1;
+    TileAcc u = {};
+    tile_gemm_abt(buf, buf + TT, u);
+    double* o = ut + size_t(tix(I, J)) * TT;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) o[tsw(u.row(i), u.col(jj, e))] = -u.v[i][jj][e];
+    fence_proxy_async_global();
+    __syncthreads();
+  }
+}
+
+// Inverse top block, step 2: A = S~_RR^{-1} = W^T W, A_IJ = sum_{K>=I} U(K,I) U(K,J)^T
+// for every lower tile (I >= J; diagonal tiles full), packed into the stream
+// records of the symmetric dense layout.  CTA per (tile, patch).
+__global__ void __launch_bounds__(kUpdThreads, 3) k_schur_ainv(int nT, const int32_t* __restrict__ col_start,
+                                                              const int32_t* __restrict__ rrow,
+                                                              const int32_t* __restrict__ rcol,
+                                                              const double* __restrict__ UT, int64_t ustride,
+                                                              const int32_t* __restrict__ bptr,
+                                                              const int32_t* __restrict__ blk,
+                                                              const int64_t* __restrict__ ccol,
+                                                              const int32_t* __restrict__ poff8,
+                                                              const uint8_t* __restrict__ hdr,
+                                                              double* __restrict__ packed, int64_t pstride) {
+  extern __shared__ __align__(128) double sm[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm);
+  double* buf = sm + 16;
+  const int t = blockIdx.x, j = blockIdx.y, tid = threadIdx.x;
+  const int I = rrow[t], J = rcol[t];
+  const double* ut = UT + size_t(j) * ustride;
+  auto tix = [&](int R, int K) { return col_start[K] + (R - K); };
+  if (tid == 0) {
+    mbar_init(&full[0], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  TileAcc acc = {};
+  for (int K = I; K < nT; ++K) {
+    if (tid == 0) {
+      mbar_arrive_expect_tx(&full[0], 2 * TT * sizeof(double));
+      bulk_g2s(buf, ut + size_t(tix(K, I)) * TT, TT * sizeof(double), &full[0]);
+      bulk_g2s(buf + TT, ut + size_t(tix(K, J)) * TT, TT * sizeof(double), &full[0]);
+    }
+    mbar_wait(&full[0], (K - I) & 1);
+    tile_gemm_abt(buf, buf + TT, acc);
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) buf[tsw(acc.row(i), acc.col(jj, e))] = acc.v[i][jj][e];
+  __syncthreads();
+  write_record(buf, packed + size_t(j) * pstride + poff8[t], hdr + size_t(t) * kHdrHost, blk + bptr[t], ccol + bptr[t]);
+}
+
+// Inverse top block, solve: x_R = A t_R with A symmetric, each lower tile
+// streamed once: x_I += A_IJ t_J and, off the diagonal, x_J += A_IJ^T t_I.
+// No dependency chain, so each patch's tile stream is split into `nchunk`
+// contiguous chunks, one CTA each (grid: patch-major).  A producer warp
+// streams the chunk's records through the byte ring (as k_patch_solve);
+// consumer warp w takes the stream positions q = w mod 8 (tile_fwd for the
+// row part, tile_bwd + reduce_cols for the column part); per round of 8
+// positions the warps stage their two 64-vectors and the stages are added
+// to the CTA accumulator in warp order, so the sums are deterministic.  The
+// accumulator goes to partial[patch][chunk] (summed in chunk order by k_schur_xsum).
+__global__ void __launch_bounds__(kSolveThreads)
+    k_schur_symv(PatchArgs a, int ring_len, int nchunk, const int32_t* __restrict__ chunk_start,
+                 const double* __restrict__ tR, const double* __restrict__ recs, const int32_t* __restrict__ tile_row,
+                 const int32_t* __restrict__ tile_col, const int32_t* __restrict__ rec_off,
+                 double* __restrict__ partial) {
+  extern __shared__ __align__(128) double sm[];
+  double* ring = sm;                       // ring_len doubles
+  double* tv = ring + ring_len;            // mpad: t_R
+  double* xa = tv + a.mpad;                // mpad: accumulator
+  double* stage = xa + a.mpad;             // kSolveConsumers x 2T
+  double* zblk = stage + kSolveConsumers * 2 * T;  // SB8 zeros
+  uint64_t* full = reinterpret_cast<uint64_t*>(zblk + SB8);
+  uint64_t* empty = full + kRingEntries;
+  int* slot_off = reinterpret_cast<int*>(empty + kRingEntries);
+  const int j = blockIdx.x / nchunk, ch = blockIdx.x % nchunk;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int t0 = chunk_start[ch], nt = chunk_start[ch + 1] - t0;
+  const double* tb = recs + size_t(j) * a.rec_stride;
+  pdl_trigger();
+  if (tid == 0) {
+    for (int e = 0; e < kRingEntries; ++e) {
+      mbar_init(&full[e], 1);
+      mbar_init(&empty[e], 1);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (warp == kSolveConsumers) {
+    if (lane == 0) {
+      int q = 0, qt = 0, head = 0;
+      const uint64_t pol = policy_evict_first();  // every record is read once per sweep
+      auto release_oldest = [&]() {
+        mbar_wait(&empty[qt & (kRingEntries - 1)], (qt / kRingEntries) & 1);
+        ++qt;
+      };
+      for (int i = 0; i < nt; ++i) {
+        const int t = t0 + i;
+        const int len = rec_off[t + 1] - rec_off[t];
+        while (q - qt >= kRingEntries) release_oldest();
+        for (;;) {
+          if (qt == q) {
+            if (head + len > ring_len) head = 0;
+            break;
+          }
+          const int tail = slot_off[qt & (kRingEntries - 1)];
+          if (tail < head) {
+            if (head + len <= ring_len) break;
+            if (len <= tail) {
+              head = 0;
+              break;
+            }
+          } else if (tail > head && head + len <= tail) {
+            break;
+          }
+          release_oldest();
+        }
+        const int e = q & (kRingEntries - 1);
+        slot_off[e] = head;
+        const uint32_t bytes = uint32_t(len) * sizeof(double);
+        mbar_arrive_expect_tx(&full[e], bytes);
+        bulk_g2s_hint(ring + head, tb + rec_off[t], bytes, &full[e], pol);
+        head += len;
+        ++q;
+      }
+    }
+    return;
+  }
+  constexpr int NC = 32 * kSolveConsumers;
+  const int rl = lane & 7, g = lane >> 3;
+  pdl_wait();
+  for (int r = tid; r < a.mpad; r += NC) {
+    tv[r] = r < a.m ? tR[size_t(j) * a.m + r] : 0.0;
+    xa[r] = 0.0;
+  }
+  for (int r = tid; r < SB8; r += NC) zblk[r] = 0.0;
+  named_sync(1, NC);
+  double* st = stage + warp * 2 * T;
+  double xr[64];
+  for (int base = 0; base < nt; base += kSolveConsumers) {
+    const int q = base + warp;
+    if (q < nt) {
+      const int t = t0 + q, I = tile_row[t], J = tile_col[t];
+      const int e = q & (kRingEntries - 1);
+      mbar_wait(&full[e], (q / kRingEntries) & 1);
+      const double* rec = ring + slot_off[e];
+      double o0, o1;
+      load_x(tv + J * T, xr);
+      tile_fwd(rec, zblk, rl, g, xr, o0, o1, nullptr);
+      double s0 = 0.0, s1 = 0.0;
+      int c = 0;
+      if (I != J) {
+        double yv[8], acc[2][8];
+#pragma unroll
+        for (int bi = 0; bi < 8; ++bi) yv[bi] = tv[I * T + 8 * bi + rl];
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+          for (int k = 0; k < 8; ++k) acc[jj][k] = 0.0;
+        tile_bwd(rec, zblk, rl, g, yv, acc, nullptr);
+        reduce_cols(acc, lane, s0, s1, c);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[e]);
+      st[8 * g + rl] = o0;
+      st[8 * (7 - g) + rl] = o1;
+      if (I != J) {
+        st[T + c] = s0;
+        st[T + c + 1] = s1;
+      }
+    }
+    named_sync(1, NC);
+    const int nw = min(kSolveConsumers, nt - base);
+    for (int w = 0; w < nw; ++w) {  // warp order: deterministic sums
+      const int t = t0 + base + w, I = tile_row[t], J = tile_col[t];
+      if (tid < T)
+        xa[I * T + tid] += stage[w * 2 * T + tid];
+      else if (tid < 2 * T && I != J)
+        xa[J * T + tid - T] += stage[w * 2 * T + tid];
+      named_sync(1, NC);
+    }
+  }
+  double* pj = partial + (size_t(j) * nchunk + ch) * a.mpad;
+  for (int r = tid; r < a.mpad; r += NC) pj[r] = xa[r];
+}
+
+// x_R = sum of the chunk partials in chunk order -> corr[patch][nF + r].
+__global__ void k_schur_xsum(int nR, int mpadR, int nchunk, int m, int nF, const double* __restrict__ partial,
+                             double* __restrict__ corr) {
+  const int j = blockIdx.y;
+  pdl_trigger();
+  pdl_wait();
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nR; r += gridDim.x * blockDim.x) {
+    const double* p = partial + size_t(j) * nchunk * mpadR + r;
+    double s = p[0];
+    for (int c = 1; c < nchunk; ++c) s += p[size_t(c) * mpadR];
+    corr[size_t(j) * m + nF + r] = s;
+  }
 }
 
 // S_FF^{-1} of one component (128 threads): the component's value block --
@@ -1691,77 +1967,62 @@ __global__ void __launch_bounds__(kCompThreads) k_schur_comp(PatchArgs a, SchurA
   if (p1 >= 0) op[p1] = t1[tid];
 }
 
-// Unfilled couplings, one warp per 8 rows (loads of the 8 rows interleaved):
+// Unfilled couplings, one CTA per block of kSpmvRows rows of one patch:
 //   mode 0: t_R = b_R - S_RF w   (rows R, x = Fw, out = tR)
 //   mode 1: c_F = b_F - S_FR x_R (rows F in component order, x = x_R in corr, out = cF)
-__global__ void __launch_bounds__(256) k_schur_spmv(PatchArgs a, SchurArgs s, const double* __restrict__ rt,
-                                                    const double* __restrict__ xin, double* __restrict__ out,
-                                                    int mode) {
-  constexpr int RW = 8;
-  const int j = blockIdx.y, lane = threadIdx.x & 31;
-  const int nrows = mode == 0 ? s.nR : s.nF;
-  const int r0 = (blockIdx.x * 8 + (threadIdx.x >> 5)) * RW;
+// The block's values and column indices (contiguous, 16-byte aligned) arrive
+// in shared memory by two TMA bulk copies issued at entry; 8 threads per row.
+constexpr int kSpmvThreads = 8 * kSpmvRows;
+__global__ void __launch_bounds__(kSpmvThreads) k_schur_spmv(PatchArgs a, SchurArgs s, const double* __restrict__ rt,
+                                                             const double* __restrict__ xin, double* __restrict__ out,
+                                                             int mode) {
+  extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) uint64_t bar;
+  const int b = blockIdx.x, j = blockIdx.y, tid = threadIdx.x;
+  const int32_t* blk = mode == 0 ? s.rf_blk : s.fr_blk;
   const int32_t* ptr = mode == 0 ? s.rf_ptr : s.fr_ptr;
   const int32_t* col = mode == 0 ? s.rf_col : s.fr_col;
   const double* v = s.vals + size_t(j) * s.vstride + (mode == 0 ? s.rf_off : s.fr_off);
+  const int e0 = blk[b], ne = blk[b + 1] - e0;
+  double* vs = sm;
+  int32_t* cs = reinterpret_cast<int32_t*>(sm + ne);
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    mbar_fence_init();
+    if (ne > 0) {
+      mbar_arrive_expect_tx(&bar, uint32_t(ne) * 12u);
+      bulk_g2s(vs, v + e0, uint32_t(ne) * 8u, &bar);
+      bulk_g2s(cs, col + e0, uint32_t(ne) * 4u, &bar);
+    } else {
+      mbar_arrive(&bar);
+    }
+  }
+  __syncthreads();
+  const int nrows = mode == 0 ? s.nR : s.nF;
+  const int rl = tid >> 3, sub = tid & 7, r = b * kSpmvRows + rl;
+  const bool live = r < nrows;
+  int r0 = 0, r1 = 0, pos = -1, g = -1;
+  if (live) {
+    r0 = ptr[r] - e0;
+    r1 = ptr[r + 1] - e0;
+    pos = mode == 0 ? s.nF + r : s.fr_row[r];
+    g = a.psep[size_t(j) * a.m + pos];
+  }
   const double* x = mode == 0 ? xin + size_t(j) * s.nF : xin + size_t(j) * s.m + s.nF;
-  const int32_t* sep = a.psep + size_t(j) * a.m;
   pdl_trigger();
-  if (r0 >= nrows) return;
-  int e0[RW], e1[RW], pos[RW], g[RW];
-  int len = 0;
-#pragma unroll
-  for (int q = 0; q < RW; ++q) {
-    const int r = r0 + q;
-    e0[q] = r < nrows ? ptr[r] : 0;
-    e1[q] = r < nrows ? ptr[r + 1] : 0;
-    pos[q] = r < nrows ? (mode == 0 ? s.nF + r : s.fr_row[r]) : -1;
-    g[q] = pos[q] >= 0 ? sep[pos[q]] : -1;
-    len = max(len, e1[q] - e0[q]);
-  }
   pdl_wait();
-  double acc[RW];
-#pragma unroll
-  for (int q = 0; q < RW; ++q) acc[q] = 0.0;
-  // b of this lane's output row, loaded before the row products
-  double bl = 0.0;
-  {
-    int gl = g[0];
-#pragma unroll
-    for (int q = 1; q < RW; ++q)
-      if (lane == q) gl = g[q];
-    if (lane < RW && gl >= 0) bl = rt[gl];
-  }
-  for (int o = lane; o < len; o += 32) {
-    double vv[RW];
-    int cc[RW];
-#pragma unroll
-    for (int q = 0; q < RW; ++q) {
-      const int e = e0[q] + o;
-      const bool in = e < e1[q];
-      vv[q] = in ? v[e] : 0.0;
-      cc[q] = in ? col[e] : 0;
-    }
-#pragma unroll
-    for (int q = 0; q < RW; ++q) acc[q] = fma(vv[q], x[cc[q]], acc[q]);
-  }
-#pragma unroll
-  for (int q = 0; q < RW; ++q) acc[q] = warp_sum(acc[q]);
-  if (lane < RW) {
-    double av = acc[0];
-    int pl = pos[0];
-#pragma unroll
-    for (int q = 1; q < RW; ++q)
-      if (lane == q) {
-        av = acc[q];
-        pl = pos[q];
-      }
-    if (pl >= 0) {
-      if (mode == 0)
-        out[size_t(j) * s.nR + (r0 + lane)] = bl - av;
-      else
-        out[size_t(j) * s.nF + pl] = bl - av;
-    }
+  const double bv = (sub == 0 && g >= 0) ? rt[g] : 0.0;
+  mbar_wait(&bar, 0);
+  double acc = 0.0;
+  for (int e = r0 + sub; e < r1; e += 8) acc = fma(vs[e], x[cs[e]], acc);
+  acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+  acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+  acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+  if (live && sub == 0) {
+    if (mode == 0)
+      out[size_t(j) * s.nR + r] = bv - acc;
+    else
+      out[size_t(j) * s.nF + pos] = bv - acc;
   }
 }
 
@@ -1991,8 +2252,11 @@ void launch_patch_solve(Context& c, const double* r_modal) {
   launch_pdl(pdl, k_schur_comp, cgrid, dim3(kCompThreads), csm, c.stream, a, s, r_modal, (const double*)nullptr,
              c.sx_F.p, 0);
   FDM_LAUNCH_CHECK(c);
-  launch_pdl(pdl, k_schur_spmv, dim3((S.nR + 63) / 64, c.npatch), dim3(256), size_t(0), c.stream, a, s, r_modal,
-             (const double*)c.sx_F.p, c.sx_tR.p, 0);
+  const size_t smem_rf = size_t(S.rf_bmax) * 12, smem_fr = size_t(S.fr_bmax) * 12;
+  FDM_CUDA(cudaFuncSetAttribute(k_schur_spmv, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(std::max(smem_rf, smem_fr))));
+  launch_pdl(pdl, k_schur_spmv, dim3(int(S.rf_blk.size()) - 1, c.npatch), dim3(kSpmvThreads), smem_rf, c.stream, a, s,
+             r_modal, (const double*)c.sx_F.p, c.sx_tR.p, 0);
   FDM_LAUNCH_CHECK(c);
   // x_R = S~_RR^{-1} t_R (dense stream) -> corr[nF..m)
   PatchArgs aR = a;
@@ -2003,10 +2267,29 @@ void launch_patch_solve(Context& c, const double* r_modal) {
   aR.rec_stride = int64_t(S.R.tile_poff8.back());
   aR.out_stride = c.L.m;
   aR.out_off = S.nF;
-  launch_dense_solve(c, aR, c.sx_tR.p);
+  if (S.inv) {
+    const size_t budget = 227 * 1024;
+    const size_t fixed = sizeof(double) * (2 * size_t(S.R.mpad) + 2 * kSolveConsumers * T + SB8) +
+                         2 * kRingEntries * sizeof(uint64_t) + kRingEntries * sizeof(int);
+    int max_rec = 0;
+    for (int t = 0; t < S.R.ntiles; ++t) max_rec = std::max(max_rec, S.R.tile_poff8[t + 1] - S.R.tile_poff8[t]);
+    const int ring = fixed < budget ? int(((budget - fixed) / sizeof(double)) & ~size_t(15)) : 0;
+    if (ring < max_rec) throw Error(FDMGPU_UNSUPPORTED, "top separator too large for the shared-memory product");
+    const size_t smem = fixed + size_t(ring) * sizeof(double);
+    FDM_CUDA(cudaFuncSetAttribute(k_schur_symv, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    launch_pdl(pdl, k_schur_symv, dim3(c.npatch * S.nchunk), dim3(kSolveThreads), smem, c.stream, aR, ring, S.nchunk,
+               (const int32_t*)c.sx_chunk.p, (const double*)c.sx_tR.p, rec_base(c), (const int32_t*)c.sx_tile_row.p,
+               (const int32_t*)c.sx_tile_col.p, (const int32_t*)c.sx_poff8.p, c.sx_part.p);
+    FDM_LAUNCH_CHECK(c);
+    launch_pdl(pdl, k_schur_xsum, dim3((S.nR + 255) / 256, c.npatch), dim3(256), size_t(0), c.stream, S.nR, S.R.mpad,
+               S.nchunk, c.L.m, S.nF, (const double*)c.sx_part.p, c.corr.p);
+    FDM_LAUNCH_CHECK(c);
+  } else {
+    launch_dense_solve(c, aR, c.sx_tR.p);
+  }
   // c_F = b_F - S_FR x_R;  x_F = S_FF^{-1} c_F -> corr[0..nF)
-  launch_pdl(pdl, k_schur_spmv, dim3((S.nF + 63) / 64, c.npatch), dim3(256), size_t(0), c.stream, a, s, r_modal,
-             (const double*)c.corr.p, c.sx_F.p, 1);
+  launch_pdl(pdl, k_schur_spmv, dim3(int(S.fr_blk.size()) - 1, c.npatch), dim3(kSpmvThreads), smem_fr, c.stream, a, s,
+             r_modal, (const double*)c.corr.p, c.sx_F.p, 1);
   FDM_LAUNCH_CHECK(c);
   launch_pdl(pdl, k_schur_comp, cgrid, dim3(kCompThreads), csm, c.stream, a, s, r_modal, (const double*)c.sx_F.p,
              c.corr.p, 1);
@@ -2082,7 +2365,7 @@ void launch_schur_setup(Context& c) {
   const SchurArgs s = make_schur_args(c);
   KernelTimer timer(c, 1);
   const size_t smem_c = sizeof(double) * (2 * size_t(c.n1) * c.n1 + 24);
-  const int np = int(c.sx.rf_col.size() + c.sx.fr_col.size());
+  const int np = int(c.sx.rf_col.size() + c.sx.fr_col.size());  // stored entries (block padding included)
   if (np > 0) {
     dim3 grid(unsigned(std::min(64, (np + 255) / 256)), c.npatch);
     k_schur_couplings<<<grid, 256, smem_c, c.stream>>>(a, s, np, c.sx_pairs.p);
@@ -2102,9 +2385,25 @@ void launch_schur_retile(Context& c) {
   const auto& R = c.sx.R;
   const size_t smem = sizeof(double) * (TT + size_t(T) * (T + 1));
   FDM_CUDA(cudaFuncSetAttribute(k_schur_retile, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  const bool inv = c.sx.inv;
+  const int64_t rstride = int64_t(R.ntiles) * TT;
   k_schur_retile<<<dim3(R.ntiles, c.npatch), 256, smem, c.stream>>>(
       a, c.sx.nF, c.sx_K0, c.sx_tidx.p, c.sx_tile_row.p, c.sx_tile_col.p, c.sx_bptr.p, c.sx_blk.p, c.sx_ccol.p,
-      c.sx_poff8.p, c.sx_hdr.p, c.tiles.p, c.diagL.p, c.packed.p, int64_t(R.tile_poff8.back()));
+      c.sx_poff8.p, c.sx_hdr.p, c.tiles.p, c.diagL.p, c.packed.p, inv ? rstride : int64_t(R.tile_poff8.back()),
+      inv ? 1 : 0);
+  FDM_LAUNCH_CHECK(c);
+  if (!inv) return;
+  // S~_RR^{-1} = W^T W, W = L_RR^{-1}: U = W^T from the dense L_RR tiles, then A
+  // into the stream records (over the dense tiles, which U no longer needs)
+  const size_t gsm = sizeof(double) * (16 + 2 * TT);
+  FDM_CUDA(cudaFuncSetAttribute(k_schur_uinv, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gsm)));
+  FDM_CUDA(cudaFuncSetAttribute(k_schur_ainv, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gsm)));
+  k_schur_uinv<<<dim3(R.nT, c.npatch), kUpdThreads, gsm, c.stream>>>(R.nT, c.sx_col_start.p, c.packed.p, c.sx_UT.p,
+                                                                     rstride);
+  FDM_LAUNCH_CHECK(c);
+  k_schur_ainv<<<dim3(R.ntiles, c.npatch), kUpdThreads, gsm, c.stream>>>(
+      R.nT, c.sx_col_start.p, c.sx_tile_row.p, c.sx_tile_col.p, c.sx_UT.p, rstride, c.sx_bptr.p, c.sx_blk.p,
+      c.sx_ccol.p, c.sx_poff8.p, c.sx_hdr.p, c.packed.p, int64_t(R.tile_poff8.back()));
   FDM_LAUNCH_CHECK(c);
 }
 

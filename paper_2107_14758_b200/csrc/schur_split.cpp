@@ -19,6 +19,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <numeric>
+#include <string>
 
 #include "context.hpp"
 
@@ -32,9 +33,9 @@ int find(std::vector<int>& par, int x) {
 }
 
 // Dense lower tile layout of an nR x nR block with full-block records: 8x8
-// sub-blocks inside the block (diagonal tiles: bi >= bj), a header like
-// symbolic_tiles' (no compact blocks).
-void dense_layout(PatchLayout& R, int nR) {
+// sub-blocks inside the block (diagonal tiles: bi >= bj, or all of them for the
+// symmetric inverse, sym), a header like symbolic_tiles' (no compact blocks).
+void dense_layout(PatchLayout& R, int nR, bool sym) {
   const int T = kTile;
   R = PatchLayout();
   R.m = nR;
@@ -59,7 +60,7 @@ void dense_layout(PatchLayout& R, int nR) {
     uint64_t mask = 0;
     for (int bi = 0; bi < 8; ++bi)
       for (int bj = 0; bj < 8; ++bj)
-        if (8 * I + bi < nb && 8 * K + bj < nb && (I != K || bi >= bj)) mask |= uint64_t(1) << (bi * 8 + bj);
+        if (8 * I + bi < nb && 8 * K + bj < nb && (sym || I != K || bi >= bj)) mask |= uint64_t(1) << (bi * 8 + bj);
     R.tile_mask8[t] = int64_t(mask);
     uint8_t* hr = &R.tile_hdr[size_t(t) * kHdrHost];
     std::fill(hr + kHdrBytes, hr + kHdrHost, uint8_t(0xff));
@@ -166,30 +167,51 @@ void analyze_schur_split(Context& c) {
       rf[r - nF].push_back(col);
       fr[col].push_back(r - nF);
     }
-  S.rf_ptr.assign(1, 0);
-  for (auto& row : rf) {
-    std::sort(row.begin(), row.end());
-    S.rf_col.insert(S.rf_col.end(), row.begin(), row.end());
-    S.rf_ptr.push_back(int32_t(S.rf_col.size()));
-  }
-  S.fr_ptr.assign(1, 0);
-  S.comp_fr.assign(1, 0);
-  for (int k = 0; k < ncomp; ++k, S.comp_fr.push_back(int32_t(S.fr_row.size())))
-    for (const auto* mem : {&m0[k], &m1[k]})
-      for (int f : *mem) {
-        auto& row = fr[f];
-        std::sort(row.begin(), row.end());
-        S.fr_row.push_back(f);
-        S.fr_col.insert(S.fr_col.end(), row.begin(), row.end());
-        S.fr_ptr.push_back(int32_t(S.fr_col.size()));
+  // Row blocks of kSpmvRows rows, each block's entries starting on a 4-entry
+  // boundary (padding: column 0, value 0) so the solve stages a block's values
+  // and columns with one 16-byte-aligned bulk copy each.
+  auto blocked = [&](int nrows, auto&& row_of, std::vector<int32_t>& ptr, std::vector<int32_t>& col,
+                     std::vector<int32_t>& blk, int& bmax, int64_t& nnz) {
+    ptr.assign(nrows + 1, 0);
+    col.clear();
+    blk.clear();
+    bmax = 0;
+    nnz = 0;
+    for (int r = 0; r < nrows; ++r) {
+      if (r % kSpmvRows == 0) {
+        while (col.size() % 4) col.push_back(0);
+        if (!blk.empty()) bmax = std::max(bmax, int(col.size()) - blk.back());
+        blk.push_back(int32_t(col.size()));
       }
-  // M (c1 rows, stride c0 | 1), W (c1 rows, stride c1 | 1), D0 (c0): odd row strides keep the
-  // component kernel's row-per-thread and column-per-thread reads bank-conflict free
+      auto& row = row_of(r);
+      std::sort(row.begin(), row.end());
+      ptr[r] = int32_t(col.size());
+      col.insert(col.end(), row.begin(), row.end());
+      nnz += int64_t(row.size());
+    }
+    ptr[nrows] = int32_t(col.size());
+    while (col.size() % 4) col.push_back(0);
+    if (!blk.empty()) bmax = std::max(bmax, int(col.size()) - blk.back());
+    blk.push_back(int32_t(col.size()));
+  };
+  blocked(S.nR, [&](int r) -> std::vector<int>& { return rf[r]; }, S.rf_ptr, S.rf_col, S.rf_blk, S.rf_bmax, S.rf_nnz);
+  S.comp_fr.assign(1, 0);
+  for (int k = 0; k < ncomp; ++k) {
+    for (const auto* mem : {&m0[k], &m1[k]})
+      for (int f : *mem) S.fr_row.push_back(f);
+    S.comp_fr.push_back(int32_t(S.fr_row.size()));
+  }
+  blocked(nF, [&](int i) -> std::vector<int>& { return fr[S.fr_row[i]]; }, S.fr_ptr, S.fr_col, S.fr_blk, S.fr_bmax,
+          S.fr_nnz);
   S.comp_stride = (int64_t(c1) * (c0 | 1) + int64_t(c1) * (c1 | 1) + c0 + 1) & ~int64_t(1);  // 16-byte aligned
   S.rf_off = S.comp_stride * ncomp;
   S.fr_off = S.rf_off + int64_t(S.rf_col.size());
-  S.vstride = (S.fr_off + int64_t(S.fr_col.size()) + 1) & ~int64_t(1);  // 16-byte aligned patch blocks
-  dense_layout(S.R, S.nR);
+  S.vstride = (S.fr_off + int64_t(S.fr_col.size()) + 3) & ~int64_t(3);  // 32-byte aligned patch blocks
+  // top block: the symmetric inverse S~_RR^{-1} (default; one streamed pass per
+  // solve) or its Cholesky factor L_RR (FDMGPU_TOP=chol: forward + backward passes)
+  const char* top = std::getenv("FDMGPU_TOP");
+  S.inv = !(top && std::string(top) == "chol");
+  dense_layout(S.R, S.nR, S.inv);
   // worth it only when the split reads clearly fewer values than the full
   // stream (3D: ~0.35 of them; 2D: R is the vertex alone, no gain)
   int64_t comp = 0;
@@ -197,7 +219,7 @@ void analyze_schur_split(Context& c) {
     const int64_t a0 = int64_t(m0[k].size()), a1 = int64_t(m1[k].size());
     comp += a1 * a0 + a1 * (a1 + 1) / 2 + a0;
   }
-  const int64_t split_vals = 2 * S.R.nnz_L + 2 * comp + int64_t(S.rf_col.size() + S.fr_col.size());
+  const int64_t split_vals = 2 * S.R.nnz_L + 2 * comp + S.rf_nnz + S.fr_nnz;
   const int64_t full_vals = 2 * (L.nnz_L - int64_t(d + 1) * L.nI);
   if (4 * split_vals > 3 * full_vals && !(env && env[0] == '1')) {
     S = SchurSplit();

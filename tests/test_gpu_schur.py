@@ -1,5 +1,10 @@
 """Schur-split separator solve (SchurSplit, paper_2107_14758_b200/csrc/context.hpp).
 
+Two forms of the top block: its explicit symmetric inverse S~_RR^{-1} = W^T W
+(W = L_RR^{-1}; default: one streamed pass, a chunk-parallel symmetric product)
+and its Cholesky factor L_RR (FDMGPU_TOP=chol: forward + backward triangular
+solves).  Both are checked here.
+
 The default stream for scalar CG layouts: the first two facet planes
 F = P0 | P1 are eliminated from S's own entries (component-wise), S_RF / S_FR
 stay unfactored and only the dense factor of the top separator R is streamed:
@@ -32,17 +37,20 @@ def torch():
     return T
 
 
-def _solver(pkg, prob, split):
-    old = os.environ.get("FDMGPU_SCHUR")
-    os.environ["FDMGPU_SCHUR"] = "1" if split else "0"
+def _solver(pkg, prob, split, top="inverse"):
+    """split: FDMGPU_SCHUR; top: "inverse" (S~_RR^{-1}, default) | "chol" (L_RR, FDMGPU_TOP=chol)."""
+    env = {"FDMGPU_SCHUR": "1" if split else "0", "FDMGPU_TOP": top}
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
     try:
         sol = pkg.Solver(prob)
         sol.factor()
     finally:
-        if old is None:
-            del os.environ["FDMGPU_SCHUR"]
-        else:
-            os.environ["FDMGPU_SCHUR"] = old
+        for k, v in old.items():
+            if v is None:
+                del os.environ[k]
+            else:
+                os.environ[k] = v
     return sol
 
 
@@ -110,3 +118,34 @@ def test_split_matches_full_stream_at_full_size(cfg, pkg, torch):
         gc.collect()
         torch.cuda.synchronize()
     assert rel(out[True], out[False]) <= 1e-12
+
+
+@pytest.mark.parametrize("case", [(2, 3, 3, False), (4, 4, 5, True), (3, 2, 15, True), (4, 3, 15, True)],
+                         ids=lambda c: "C%d_n%d_p%d_%s" % (c[0], c[1], c[2], "skip" if c[3] else "all"))
+def test_cholesky_top_matches_inverse_top_and_oracle(case, pkg, oracle, torch):
+    cfg, n, p, skip = case
+    prob = pkg.Problem(cfg, n, p, skip_boundary_patches=skip)
+    inv = _solver(pkg, prob, True, "inverse")
+    chol = _solver(pkg, prob, True, "chol")
+    ref = oracle.Problem(cfg, n, p, build_global=True, threads=os.cpu_count(), skip_boundary_patches=skip)
+    ref.factor()
+    r = prob.rhs()
+    rt = ref.apply_St(r)
+    zi, zc, zr = inv.patch_apply(rt), chol.patch_apply(rt), ref.patch_apply(rt)
+    assert rel(zi, zc) <= 1e-12
+    assert rel(zc, zr) <= TOL_RELAX and rel(zi, zr) <= TOL_RELAX
+
+
+def test_inverse_top_at_c3_matches_cholesky_top(pkg, torch):
+    """Full C3 (343 patches, several product chunks per patch)."""
+    import gc
+
+    prob = pkg.Problem(3)
+    r = torch.from_numpy(prob.rhs()).cuda()
+    out = {}
+    for top in ("inverse", "chol"):
+        sol = _solver(pkg, prob, True, top)
+        out[top] = sol.smooth(r).cpu().numpy()
+        del sol
+        gc.collect()
+    assert rel(out["inverse"], out["chol"]) <= 1e-12
