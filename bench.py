@@ -266,10 +266,39 @@ CPU_STEPS = 5  # CPU-leg samples in the GPU arm (median of 5 after 1 warm-up, BA
 
 
 def solve_kernel_bytes(L, prob):
-    """Algorithmic bytes of one separator solve launch (k_patch_solve + split tail):
-    16 B x separator nnz(L_j) of the factor in use (fwd + bwd) + 20 B x m per patch."""
-    nnz_sep = (L["nnz_L"] - (prob.dim + 1) * L["n_interior"]) * L["npatch"]
-    return 16.0 * nnz_sep + 2 * 8.0 * L["npatch"] * L["n_interface"] + 4.0 * L["npatch"] * L["n_interface"]
+    """Algorithmic bytes of one separator solve (every launch of the patch solve):
+    8 B x the matrix values the solve reads per patch (fdmgpu_layout.solve_values: Schur split
+    = S~_RR^{-1} lower triangle once (or L_RR twice) + 2 x the S_FF components + S_RF + S_FR;
+    full stream = 2 x separator nnz(L_j)) + 20 B x m per patch (RHS gather, solution write,
+    gather map)."""
+    return 8.0 * L["solve_values"] * L["npatch"] + 20.0 * L["npatch"] * L["n_interface"]
+
+
+def top_kernel_bytes(L):
+    """Algorithmic bytes of the top-block stage (k_schur_symv): the lower triangle of
+    S~_RR^{-1} once (FDMGPU_TOP=chol: L_RR twice) + t_R read / x_R write, per patch."""
+    nr = L["n_top"]
+    passes = 2 if os.environ.get("FDMGPU_TOP") == "chol" else 1
+    return (8.0 * passes * nr * (nr + 1) / 2 + 16.0 * nr) * L["npatch"]
+
+
+def inverse_issued_flops(L):
+    """FP64 tensor-pipe flops k_schur_uinv / k_schur_ainv issue per factorisation (dense 64x64
+    tile GEMMs: column J of U takes sum_{I>J} (I - J + 1), tile (I, J) of A takes nT - I)."""
+    if not L["schur_split"] or os.environ.get("FDMGPU_TOP") == "chol":
+        return 0.0
+    nt = -(-L["n_top"] // 64)
+    gemms = sum(I - J + 1 for J in range(nt) for I in range(J + 1, nt)) + sum(nt - I for I in range(nt)
+                                                                             for J in range(I + 1))
+    return 2.0 * 64 ** 3 * gemms * L["npatch"]
+
+
+def inverse_flops(L):
+    """Flops of the top-block inverse per factorisation: W = L_RR^{-1} (n^3/6 multiply-adds)
+    and S~_RR^{-1} = W^T W (n^3/6), n = |R|, all patches (0 for FDMGPU_TOP=chol or no split)."""
+    if not L["schur_split"] or os.environ.get("FDMGPU_TOP") == "chol":
+        return 0.0
+    return 2.0 * (L["n_top"] ** 3 / 3.0) * L["npatch"]
 
 
 def sub_measure(config, steps, warmup, stream, device):
@@ -310,20 +339,31 @@ def sub_measure(config, steps, warmup, stream, device):
         sol.smooth(r, z)
     torch.cuda.synchronize()
     solve_ms = sol.kernel_time("patch_solve")[0] / n
+    top_ms = sol.kernel_time("top_block")[0] / n
     sol.kernel_timing(False)
     hbm_peak, _ = measured_peaks()
     kb = solve_kernel_bytes(L, prob)
+    tb = top_kernel_bytes(L)
     cal = sol.calibrate_damping()
     _, rep = sol.pcg(r, rtol=1e-8, maxit=200)
-    fac_flops = 2.0 * L["flops_ref"] * L["npatch"]
+    fac_flops = 2.0 * L["flops_ref"] * L["npatch"] + inverse_flops(L)
     return {"workload": WORKLOADS[config], "value": prob.nfree / (ms * 1e-3) / 1e9, "unit": "GDOF/s",
             "ms_per_step": ms, "steps": steps,
-            "roofline": {"kernel": "k_patch_solve (+ split tail)", "achieved": kb / (solve_ms * 1e-3) / 1e9,
-                         "peak": hbm_peak, "unit": "GB/s", "frac": kb / (solve_ms * 1e-3) / 1e9 / hbm_peak,
-                         "kernel_ms": solve_ms, "algorithmic_bytes": kb},
+            "roofline": {"kernel": "k_schur_symv (S~_RR^{-1} product)" if L["schur_split"] else
+                         "k_patch_solve (+ split tail)",
+                         "achieved": (tb if L["schur_split"] else kb) / ((top_ms if L["schur_split"] else solve_ms)
+                                                                          * 1e-3) / 1e9,
+                         "peak": hbm_peak, "unit": "GB/s",
+                         "frac": (tb if L["schur_split"] else kb) / ((top_ms if L["schur_split"] else solve_ms)
+                                                                     * 1e-3) / 1e9 / hbm_peak,
+                         "kernel_ms": top_ms if L["schur_split"] else solve_ms,
+                         "algorithmic_bytes": tb if L["schur_split"] else kb},
+            "solve_roofline": {"ms": solve_ms, "algorithmic_bytes": kb, "achieved": kb / (solve_ms * 1e-3) / 1e9,
+                               "frac": kb / (solve_ms * 1e-3) / 1e9 / hbm_peak},
             "factor_ms": min(fac),
             "factor_fp64_frac": fac_flops / (min(fac) * 1e-3) / 1e12 / FP64_PEAK_TFLOPS,
-            "factor_issued_frac": L["dmma_flops"] * L["npatch"] / (min(fac) * 1e-3) / 1e12 / FP64_PEAK_TFLOPS,
+            "factor_issued_frac": (L["dmma_flops"] * L["npatch"] + inverse_issued_flops(L)) / (min(fac) * 1e-3) / 1e12
+            / FP64_PEAK_TFLOPS,
             "pcg": {"iterations": rep["iterations"], "converged": rep["converged"], "omega": cal["omega"],
                     "solve_s": rep["wall_time"]}}
 
@@ -422,6 +462,7 @@ def run_ours(args):
         sol.smooth(r, z)
     torch.cuda.synchronize()
     solve_ms, solve_n = sol.kernel_time("patch_solve")
+    top_ms, top_n = sol.kernel_time("top_block")
     tr_ms, tr_n = sol.kernel_time("transform")
     sol.kernel_timing(False)
     ms = replicas.max_over_ranks(ms, dev)
@@ -472,23 +513,35 @@ def run_ours(args):
     try:
         tr = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")))
         ent = tr.get(str(args.config))
-        if ent and str(ent.get("kernel", "")).startswith("k_patch_solve"):
+        want = "k_schur_symv" if (L["schur_split"] and os.environ.get("FDMGPU_TOP") != "chol") else "k_patch_solve"
+        if ent and str(ent.get("kernel", "")).startswith(want):
             traffic = float(ent["dram_bytes_read"] + ent["dram_bytes_write"])
     except (OSError, ValueError, KeyError):
         traffic = None
     nnz_total = L["nnz_L_reference"] * L["npatch"]  # reference patch_ordering factor (SURVEY.md Bytes_relax)
     # separator columns of the factor the kernel streams (order in use; interior columns are never stored)
-    kern_bytes = solve_kernel_bytes(L, prob)
-    # per step: the separator solve is one launch of k_patch_solve plus, for the
-    # last partial wave of patches, one overlapping launch of the cluster-split
-    # k_patch_solve_cl (one timed interval around both)
-    kern_ms = solve_ms / n_timed
-    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
-    split = L["tile_cols"] >= 16 and L["npatch"] % nsm != 0 and os.environ.get("FDMGPU_SOLVE_CS") != "1"
-    solve_kernels = "k_patch_solve + k_patch_solve_cl (split tail, overlapped)" if split else "k_patch_solve"
+    solve_bytes = solve_kernel_bytes(L, prob)
+    solve_kms = solve_ms / n_timed  # every launch of the separator solve (one timed interval)
+    inv_top = L["schur_split"] and os.environ.get("FDMGPU_TOP") != "chol"
+    if L["schur_split"]:
+        # dominant kernel: the top-block stage of the Schur split
+        kern_bytes = top_kernel_bytes(L)
+        kern_ms = top_ms / n_timed
+        solve_kernels = ("k_schur_symv (S~_RR^{-1} symmetric product, chunk-parallel)" if inv_top else
+                         "k_patch_solve (+ split tail) on L_RR")
+        bytes_def = ("8 B x |R|(|R|+1)/2 (lower triangle of S~_RR^{-1}, streamed once) + t_R read / x_R write, "
+                     "per patch, all patches" if inv_top else
+                     "16 B x nnz(L_RR) (fwd + bwd) + t_R read / x_R write, per patch, all patches")
+    else:
+        kern_bytes, kern_ms = solve_bytes, solve_kms
+        nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+        split = L["tile_cols"] >= 16 and L["npatch"] % nsm != 0 and os.environ.get("FDMGPU_SOLVE_CS") != "1"
+        solve_kernels = "k_patch_solve + k_patch_solve_cl (split tail, overlapped)" if split else "k_patch_solve"
+        bytes_def = ("16 B x separator nnz(L_j) of the factor in use (fwd + bwd; plane-by-plane separator order) "
+                     "+ separator RHS gather / solution write, per launch, all patches")
     achieved = kern_bytes / (kern_ms * 1e-3) / 1e9
     relax_bytes = 8.0 * (2 * nnz_total + 2 * prob.sum_nj + 4 * prob.ndof)  # SURVEY.md §8(d) Bytes_relax
-    fac_flops = 2.0 * L["flops_ref"] * L["npatch"]  # factor in use
+    fac_flops = 2.0 * L["flops_ref"] * L["npatch"] + inverse_flops(L)  # factor in use (+ top-block inverse)
     fac_flops_refeq = 2.0 * L["flops_reference"] * L["npatch"]  # reference patch_ordering factor
     result = {
         "metric": METRIC, "value": value, "unit": "GDOF/s", "n_gpus": world, "steps": args.steps,
@@ -503,9 +556,15 @@ def run_ours(args):
                      "traffic": traffic,
                      "peak_source": peak_src, "kernel_ms": kern_ms, "algorithmic_bytes": kern_bytes,
                      "share_of_step": kern_ms / ms_per_step if ms_per_step > 0 else None,
-                     "bytes_def": "16 B x separator nnz(L_j) of the factor in use (fwd + bwd; plane-by-plane "
-                                  "separator order) + separator RHS gather / solution write, per launch, all patches",
+                     "bytes_def": bytes_def,
                      "stored_bytes_per_pass": L["stream_bytes"]},
+        "solve_roofline": {
+            "kernels": "every launch of the separator solve (Schur split: S_FF components, S_RF / S_FR products, "
+                       "top block, partial sums)" if L["schur_split"] else solve_kernels,
+            "ms": solve_kms, "algorithmic_bytes": solve_bytes, "achieved": solve_bytes / (solve_kms * 1e-3) / 1e9,
+            "peak": hbm_peak, "unit": "GB/s", "frac": solve_bytes / (solve_kms * 1e-3) / 1e9 / hbm_peak,
+            "share_of_step": solve_kms / ms_per_step if ms_per_step > 0 else None,
+            "bytes_def": "8 B x fdmgpu_layout.solve_values x patches + 20 B x m x patches"},
         "relaxation_reference_equivalent": {
             "bytes": relax_bytes, "rate_GBps": relax_bytes / (ms_per_step * 1e-3) / 1e9,
             "note": "not a roofline fraction: SURVEY.md 8(d) Bytes_relax = 8*(2*NNZ + 2*sum n_j + 4*ndof) with NNZ of "
@@ -515,15 +574,19 @@ def run_ours(args):
         "transform_roofline": transform_roofline(prob, st_ms, hbm_peak),
         "factor_ms": factor_ms,
         "factor_roofline": {"bound": "fp64", "achieved": fac_flops / (factor_ms * 1e-3) / 1e12,
-                            "issued_TFLOPs": L["dmma_flops"] * L["npatch"] / (factor_ms * 1e-3) / 1e12,
-                            "issued_frac": L["dmma_flops"] * L["npatch"] / (factor_ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS,
+                            "issued_TFLOPs": (L["dmma_flops"] * L["npatch"] + inverse_issued_flops(L))
+                            / (factor_ms * 1e-3) / 1e12,
+                            "issued_frac": (L["dmma_flops"] * L["npatch"] + inverse_issued_flops(L))
+                            / (factor_ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS,
                             "issued_def": "FP64 tensor-pipe flops the tile kernels issue (dense 64x64 tile GEMMs "
                                           "minus skipped zero 16-wide panels; fdmgpu_layout.dmma_flops), not "
                                           "counting the diagonal-tile POTRF/inverse",
                             "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                             "frac": fac_flops / (factor_ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS,
                             "flops_def": "2 x CholFactor::flops (src/cholesky.cpp:74) of the factor in use, summed "
-                                         "over patches",
+                                         "over patches, + the top-block inverse (W = L_RR^{-1}, W^T W: 2 |R|^3 / 3 "
+                                         "per patch; 0 with FDMGPU_TOP=chol)",
+                            "inverse_flops": inverse_flops(L),
                             "reference_equivalent_TFLOPs": fac_flops_refeq / (factor_ms * 1e-3) / 1e12},
         "e2e": {"value": world * prob.nfree / (e2e_ms * 1e-3) / 1e9, "unit": "GDOF/s", "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": 8 * prob.ndof, "d2h_bytes_per_step": 8 * prob.ndof,

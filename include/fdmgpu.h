@@ -276,7 +276,9 @@ int64_t fdmgpu_launch_count(fdmgpu_handle h);
 
 /* Per-kernel CUDA-event timing on the handle stream (bench.py roofline):
  * enable != 0 starts recording (and clears earlier records); which = 0 patch
- * solve, 1 factorisation kernels, 2 cell transforms, 3 stiffness apply. */
+ * solve, 1 factorisation kernels, 2 cell transforms, 3 stiffness apply, 4 the
+ * top-block stage of the patch solve (Schur split: S~_RR^{-1} product or L_RR
+ * solves; part of class 0). */
 fdmgpu_status fdmgpu_kernel_timing(fdmgpu_handle h, int32_t enable);
 fdmgpu_status fdmgpu_kernel_time(fdmgpu_handle h, int32_t which, double* total_ms, int64_t* launches);
 

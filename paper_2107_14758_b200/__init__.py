@@ -428,7 +428,7 @@ class Solver:
     def launch_count(self):
         return int(lib().fdmgpu_launch_count(self.h))
 
-    KERNEL_CLASSES = {"patch_solve": 0, "factor": 1, "transform": 2, "stiffness": 3}
+    KERNEL_CLASSES = {"patch_solve": 0, "factor": 1, "transform": 2, "stiffness": 3, "top_block": 4}
 
     def kernel_timing(self, enable=True):
         """Start (and clear) or stop CUDA-event timing of the library's kernels."""

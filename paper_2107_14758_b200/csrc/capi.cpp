@@ -55,7 +55,8 @@ void setup_schur_split(Context& c) {
         best_eff = eff;
       }
     }
-    S.nchunk = best;
+    const char* ch = std::getenv("FDMGPU_SYMV_CHUNKS");  // override (tests / tuning)
+    S.nchunk = ch ? std::max(1, std::min(64, std::atoi(ch))) : best;
     S.chunk_start.assign(1, 0);
     const int64_t total = S.R.tile_poff8.back();
     for (int g = 1; g < S.nchunk; ++g) {
@@ -1178,7 +1179,7 @@ fdmgpu_status fdmgpu_get_layout(fdmgpu_handle h, fdmgpu_layout* out) {
         for (int i = 0; i < S.c1; ++i) a1 += S.comp1[size_t(k) * S.c1 + i] >= 0;
         comp += a1 * a0 + a1 * (a1 + 1) / 2 + a0;
       }
-      L.solve_values = 2 * S.R.nnz_L + 2 * comp + S.rf_nnz + S.fr_nnz;
+      L.solve_values = (S.inv ? 1 : 2) * S.R.nnz_L + 2 * comp + S.rf_nnz + S.fr_nnz;
     } else {
       L.stream_bytes = int64_t(c.L.tile_poff8.back()) * 8 * c.npatch;
       L.schur_split = 0;
@@ -1551,7 +1552,7 @@ fdmgpu_status fdmgpu_kernel_timing(fdmgpu_handle h, int32_t enable) {
 
 fdmgpu_status fdmgpu_kernel_time(fdmgpu_handle h, int32_t which, double* total_ms, int64_t* launches) {
   return fdmgpu::guarded(h, [&](Context& c) {
-    if (which < 0 || which > 3) throw Error(FDMGPU_INVALID_ARGUMENT, "kernel_time: class 0..3");
+    if (which < 0 || which > 4) throw Error(FDMGPU_INVALID_ARGUMENT, "kernel_time: class 0..4");
     FDM_CUDA(cudaStreamSynchronize(c.stream));
     double t = 0.0;
     int64_t n = 0;

@@ -264,7 +264,7 @@ struct Context {
   bool force_staged = false;  // FDMGPU_FORCE_STAGED=1: staged cell kernels for every p (tests)
   bool pdl = true;            // programmatic dependent launch in the relaxation chain (FDMGPU_PDL=0 disables)
   int sep_order = 0;  // 0 plane-by-plane facets (default), 1 reference patch_ordering (FDMGPU_SEP_ORDER)
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tev[4];
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tev[5];
 
   void check_ready(bool need_patches, bool need_factor, bool need_coarse) const;
   // Component sub-context ci, synchronised with this handle's launch state
@@ -298,7 +298,8 @@ struct Context {
 
 // Records CUDA events around one launch on the handle stream when timing is on.
 // Timed kernel classes: 0 patch solve, 1 factor (assemble/update/trsm),
-// 2 cell transforms, 3 stiffness apply.
+// 2 cell transforms, 3 stiffness apply, 4 the Schur split's top-block stage
+// of the patch solve (inside class 0).
 struct KernelTimer {
   Context& c;
   int slot;

@@ -1726,14 +1726,18 @@ __global__ void __launch_bounds__(kUpdThreads, 3) k_schur_ainv(int nT, const int
 // Inverse top block, solve: x_R = A t_R with A symmetric, each lower tile
 // streamed once: x_I += A_IJ t_J and, off the diagonal, x_J += A_IJ^T t_I.
 // No dependency chain, so each patch's tile stream is split into `nchunk`
-// contiguous chunks, one CTA each (grid: patch-major).  A producer warp
-// streams the chunk's records through the byte ring (as k_patch_solve);
-// consumer warp w takes the stream positions q = w mod 8 (tile_fwd for the
-// row part, tile_bwd + reduce_cols for the column part); per round of 8
-// positions the warps stage their two 64-vectors and the stages are added
-// to the CTA accumulator in warp order, so the sums are deterministic.  The
-// accumulator goes to partial[patch][chunk] (summed in chunk order by k_schur_xsum).
-__global__ void __launch_bounds__(kSolveThreads)
+// contiguous chunks, one CTA each (grid: patch-major).  Warp roles:
+//   producer (1 warp): streams the chunk's records through the byte ring (as k_patch_solve);
+//   consumers (NCONS warps): stream position q goes to warp q mod NCONS: tile_fwd (row part)
+//     and tile_bwd + reduce_cols (column part) on the record, the two 64-vectors
+//     into stage slot q mod kSymvSlots, the record released at once;
+//   committer (1 warp): adds the stage slots to the CTA accumulator in stream
+//     order (deterministic sums, no CTA-wide barrier per tile).
+// Slots and ring entries hand over through mbarriers.  The accumulator goes
+// to partial[patch][chunk] (summed in chunk order by k_schur_xsum).
+constexpr int kSymvSlots = 16;
+template <int NCONS>
+__global__ void __launch_bounds__(32 * (NCONS + 2))
     k_schur_symv(PatchArgs a, int ring_len, int nchunk, const int32_t* __restrict__ chunk_start,
                  const double* __restrict__ tR, const double* __restrict__ recs, const int32_t* __restrict__ tile_row,
                  const int32_t* __restrict__ tile_col, const int32_t* __restrict__ rec_off,
@@ -1742,25 +1746,33 @@ __global__ void __launch_bounds__(kSolveThreads)
   double* ring = sm;                       // ring_len doubles
   double* tv = ring + ring_len;            // mpad: t_R
   double* xa = tv + a.mpad;                // mpad: accumulator
-  double* stage = xa + a.mpad;             // kSolveConsumers x 2T
-  double* zblk = stage + kSolveConsumers * 2 * T;  // SB8 zeros
+  double* stage = xa + a.mpad;             // kSymvSlots x 2T
+  double* zblk = stage + kSymvSlots * 2 * T;  // SB8 zeros
   uint64_t* full = reinterpret_cast<uint64_t*>(zblk + SB8);
   uint64_t* empty = full + kRingEntries;
-  int* slot_off = reinterpret_cast<int*>(empty + kRingEntries);
+  uint64_t* sfull = empty + kRingEntries;
+  uint64_t* sempty = sfull + kSymvSlots;
+  int* slot_off = reinterpret_cast<int*>(sempty + kSymvSlots);
   const int j = blockIdx.x / nchunk, ch = blockIdx.x % nchunk;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int t0 = chunk_start[ch], nt = chunk_start[ch + 1] - t0;
   const double* tb = recs + size_t(j) * a.rec_stride;
+  constexpr int kProducer = NCONS, kCommitter = NCONS + 1;
+  constexpr int NW = 32 * (NCONS + 1);  // consumers + committer
   pdl_trigger();
   if (tid == 0) {
     for (int e = 0; e < kRingEntries; ++e) {
       mbar_init(&full[e], 1);
       mbar_init(&empty[e], 1);
     }
+    for (int e = 0; e < kSymvSlots; ++e) {
+      mbar_init(&sfull[e], 1);
+      mbar_init(&sempty[e], 1);
+    }
     mbar_fence_init();
   }
   __syncthreads();
-  if (warp == kSolveConsumers) {
+  if (warp == kProducer) {
     if (lane == 0) {
       int q = 0, qt = 0, head = 0;
       const uint64_t pol = policy_evict_first();  // every record is read once per sweep
@@ -1800,33 +1812,54 @@ __global__ void __launch_bounds__(kSolveThreads)
     }
     return;
   }
-  constexpr int NC = 32 * kSolveConsumers;
-  const int rl = lane & 7, g = lane >> 3;
   pdl_wait();
-  for (int r = tid; r < a.mpad; r += NC) {
+  const int ct = warp == kCommitter ? tid - 32 : tid;  // 0 .. NW-1 over consumers + committer
+  for (int r = ct; r < a.mpad; r += NW) {
     tv[r] = r < a.m ? tR[size_t(j) * a.m + r] : 0.0;
     xa[r] = 0.0;
   }
-  for (int r = tid; r < SB8; r += NC) zblk[r] = 0.0;
-  named_sync(1, NC);
-  double* st = stage + warp * 2 * T;
-  double xr[64];
-  for (int base = 0; base < nt; base += kSolveConsumers) {
-    const int q = base + warp;
-    if (q < nt) {
+  for (int r = ct; r < SB8; r += NW) zblk[r] = 0.0;
+  named_sync(1, NW);
+  if (warp == kCommitter) {
+    for (int q = 0; q < nt; ++q) {
+      const int sl = q & (kSymvSlots - 1);
       const int t = t0 + q, I = tile_row[t], J = tile_col[t];
-      const int e = q & (kRingEntries - 1);
+      mbar_wait(&sfull[sl], (q / kSymvSlots) & 1);
+      const double* st = stage + sl * 2 * T;
+      const double r0 = st[lane], r1 = st[lane + 32];
+      double c0 = 0.0, c1 = 0.0;
+      if (I != J) {
+        c0 = st[T + lane];
+        c1 = st[T + lane + 32];
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sempty[sl]);
+      xa[I * T + lane] += r0;
+      xa[I * T + lane + 32] += r1;
+      if (I != J) {
+        xa[J * T + lane] += c0;
+        xa[J * T + lane + 32] += c1;
+      }
+      __syncwarp();
+    }
+  } else {
+    const int rl = lane & 7, g = lane >> 3;
+    double xr[64];
+    for (int q = warp; q < nt; q += NCONS) {
+      const int t = t0 + q, I = tile_row[t], J = tile_col[t];
+      const int e = q & (kRingEntries - 1), sl = q & (kSymvSlots - 1);
+      load_x(tv + J * T, xr);
+      double yv[8];
+#pragma unroll
+      for (int bi = 0; bi < 8; ++bi) yv[bi] = tv[I * T + 8 * bi + rl];
       mbar_wait(&full[e], (q / kRingEntries) & 1);
       const double* rec = ring + slot_off[e];
       double o0, o1;
-      load_x(tv + J * T, xr);
       tile_fwd(rec, zblk, rl, g, xr, o0, o1, nullptr);
       double s0 = 0.0, s1 = 0.0;
       int c = 0;
       if (I != J) {
-        double yv[8], acc[2][8];
-#pragma unroll
-        for (int bi = 0; bi < 8; ++bi) yv[bi] = tv[I * T + 8 * bi + rl];
+        double acc[2][8];
 #pragma unroll
         for (int jj = 0; jj < 2; ++jj)
 #pragma unroll
@@ -1836,26 +1869,21 @@ __global__ void __launch_bounds__(kSolveThreads)
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[e]);
+      mbar_wait(&sempty[sl], ((q / kSymvSlots) & 1) ^ 1);
+      double* st = stage + sl * 2 * T;
       st[8 * g + rl] = o0;
       st[8 * (7 - g) + rl] = o1;
       if (I != J) {
         st[T + c] = s0;
         st[T + c + 1] = s1;
       }
-    }
-    named_sync(1, NC);
-    const int nw = min(kSolveConsumers, nt - base);
-    for (int w = 0; w < nw; ++w) {  // warp order: deterministic sums
-      const int t = t0 + base + w, I = tile_row[t], J = tile_col[t];
-      if (tid < T)
-        xa[I * T + tid] += stage[w * 2 * T + tid];
-      else if (tid < 2 * T && I != J)
-        xa[J * T + tid - T] += stage[w * 2 * T + tid];
-      named_sync(1, NC);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sfull[sl]);
     }
   }
+  named_sync(1, NW);
   double* pj = partial + (size_t(j) * nchunk + ch) * a.mpad;
-  for (int r = tid; r < a.mpad; r += NC) pj[r] = xa[r];
+  for (int r = ct; r < a.mpad; r += NW) pj[r] = xa[r];
 }
 
 // x_R = sum of the chunk partials in chunk order -> corr[patch][nF + r].
@@ -2267,17 +2295,24 @@ void launch_patch_solve(Context& c, const double* r_modal) {
   aR.rec_stride = int64_t(S.R.tile_poff8.back());
   aR.out_stride = c.L.m;
   aR.out_off = S.nF;
+  {
+  KernelTimer top_timer(c, 4);  // the top-block stage alone
   if (S.inv) {
     const size_t budget = 227 * 1024;
-    const size_t fixed = sizeof(double) * (2 * size_t(S.R.mpad) + 2 * kSolveConsumers * T + SB8) +
-                         2 * kRingEntries * sizeof(uint64_t) + kRingEntries * sizeof(int);
+    const size_t fixed = sizeof(double) * (2 * size_t(S.R.mpad) + 2 * kSymvSlots * T + SB8) +
+                         2 * (kRingEntries + kSymvSlots) * sizeof(uint64_t) + kRingEntries * sizeof(int);
     int max_rec = 0;
     for (int t = 0; t < S.R.ntiles; ++t) max_rec = std::max(max_rec, S.R.tile_poff8[t + 1] - S.R.tile_poff8[t]);
     const int ring = fixed < budget ? int(((budget - fixed) / sizeof(double)) & ~size_t(15)) : 0;
     if (ring < max_rec) throw Error(FDMGPU_UNSUPPORTED, "top separator too large for the shared-memory product");
     const size_t smem = fixed + size_t(ring) * sizeof(double);
-    FDM_CUDA(cudaFuncSetAttribute(k_schur_symv, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    launch_pdl(pdl, k_schur_symv, dim3(c.npatch * S.nchunk), dim3(kSolveThreads), smem, c.stream, aR, ring, S.nchunk,
+    // consumer warps: each holds its record while it computes, so fewer warps leave
+    // more of the ring in flight (FDMGPU_SYMV_WARPS: 4 | 8, tuning)
+    const char* wenv = std::getenv("FDMGPU_SYMV_WARPS");
+    const int ncons = wenv && std::atoi(wenv) == 8 ? 8 : 4;
+    auto kern = ncons == 8 ? k_schur_symv<8> : k_schur_symv<4>;
+    FDM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    launch_pdl(pdl, kern, dim3(c.npatch * S.nchunk), dim3(32 * (ncons + 2)), smem, c.stream, aR, ring, S.nchunk,
                (const int32_t*)c.sx_chunk.p, (const double*)c.sx_tR.p, rec_base(c), (const int32_t*)c.sx_tile_row.p,
                (const int32_t*)c.sx_tile_col.p, (const int32_t*)c.sx_poff8.p, c.sx_part.p);
     FDM_LAUNCH_CHECK(c);
@@ -2286,6 +2321,7 @@ void launch_patch_solve(Context& c, const double* r_modal) {
     FDM_LAUNCH_CHECK(c);
   } else {
     launch_dense_solve(c, aR, c.sx_tR.p);
+  }
   }
   // c_F = b_F - S_FR x_R;  x_F = S_FF^{-1} c_F -> corr[0..nF)
   launch_pdl(pdl, k_schur_spmv, dim3(int(S.fr_blk.size()) - 1, c.npatch), dim3(kSpmvThreads), smem_fr, c.stream, a, s,
