@@ -18,7 +18,7 @@ constexpr int kTile = 64;  // dense tile edge of the interface factor
 constexpr int kHdrBytes = 144;  // solve-record header: 2 x 64 sub-block indices + full / compact counts
 constexpr int kCompact = 10;    // doubles per compact 8x8 sub-block (8 row values + 8 column bytes + pad)
 constexpr int kHdrHost = kHdrBytes + 128;  // host tile_hdr stride: record header + compact index table
-constexpr int kSpmvRows = 32;   // rows per block of the Schur split's coupling products
+constexpr int kSpmvRows = 16;   // rows per block of the Schur split's coupling products
 
 struct Error : std::runtime_error {
   fdmgpu_status status;

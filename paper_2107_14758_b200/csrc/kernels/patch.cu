@@ -1526,17 +1526,15 @@ __global__ void __launch_bounds__(256) k_schur_comps(PatchArgs a, SchurArgs s) {
   diag_factor_invert(Dm, Wm, Wo, an, 0, -1);
   __syncthreads();
   double* out = s.vals + size_t(j) * s.vstride + size_t(k) * s.comp_stride;
-  const int ldm = s.c0 | 1, ldw = s.c1 | 1;
+  const int ldm = s.c0 | 1;
   for (int idx = tid; idx < s.c1 * ldm; idx += blockDim.x) {
     const int i = idx / ldm, jj = idx % ldm;
     out[idx] = jj < s.c0 ? M[i * LD + jj] : 0.0;
   }
   out += s.c1 * ldm;
-  for (int idx = tid; idx < s.c1 * ldw; idx += blockDim.x) {
-    const int i = idx / ldw, q = idx % ldw;
-    out[idx] = q < s.c1 ? Wo[tsw(i, q)] : 0.0;
-  }
-  out += s.c1 * ldw;
+  for (int i = tid >> 5; i < s.c1; i += blockDim.x >> 5)  // W lower triangle, row i at i(i+1)/2
+    for (int q = tid & 31; q <= i; q += 32) out[i * (i + 1) / 2 + q] = Wo[tsw(i, q)];
+  out += s.c1 * (s.c1 + 1) / 2;
   for (int jj = tid; jj < s.c0; jj += blockDim.x) out[jj] = d0[jj];
 }
 
@@ -1901,12 +1899,12 @@ __global__ void k_schur_xsum(int nR, int mpadR, int nchunk, int m, int nF, const
 }
 
 // S_FF^{-1} of one component (128 threads): the component's value block --
-// M (c1 x c0, row stride c0|1), W = chol(S'_11)^{-1} (c1 x c1 lower, row
-// stride c1|1), D0 (c0) -- arrives in shared memory by one TMA bulk copy
+// M (c1 x c0, row stride c0|1), W = chol(S'_11)^{-1} (c1 x c1 lower triangle,
+// packed by rows), D0 (c0) -- arrives in shared memory by one TMA bulk copy
 // issued at entry; b from the S^T output (mode 0, forward half) or from
 // c_F = b_F - S_FR x_R (mode 1, backward half).  Every product runs two
-// threads per output (row or column halves, combined by one shuffle); the odd
-// row strides make both row-wise and column-wise reads conflict free.
+// threads per output (row or column halves, combined by one shuffle); M's odd
+// row stride makes both its row-wise and column-wise reads conflict free.
 // Output: mode 0 -> Fw (npatch x nF), mode 1 -> corr (F part of the separator solution).
 constexpr int kCompThreads = 128;
 __global__ void __launch_bounds__(kCompThreads) k_schur_comp(PatchArgs a, SchurArgs s, const double* __restrict__ rt,
@@ -1916,7 +1914,7 @@ __global__ void __launch_bounds__(kCompThreads) k_schur_comp(PatchArgs a, SchurA
   __shared__ __align__(8) uint64_t bar;
   __shared__ double b0[64], b1[64], t0[64], t1[64];
   const int k = blockIdx.x, j = blockIdx.y, tid = threadIdx.x;
-  const int c0 = s.c0, c1 = s.c1, ldm = c0 | 1, ldw = c1 | 1;
+  const int c0 = s.c0, c1 = s.c1, ldm = c0 | 1;
   const double* src = s.vals + size_t(j) * s.vstride + size_t(k) * s.comp_stride;
   if (tid == 0) {
     mbar_init(&bar, 1);
@@ -1947,8 +1945,8 @@ __global__ void __launch_bounds__(kCompThreads) k_schur_comp(PatchArgs a, SchurA
   }
   mbar_wait(&bar, 0);
   const double* M = sm;
-  const double* W = sm + c1 * ldm;
-  const double* d0 = W + c1 * ldw;
+  const double* W = sm + c1 * ldm;  // lower triangle packed by rows: W(i, q) at i(i+1)/2 + q
+  const double* d0 = W + c1 * (c1 + 1) / 2;
   __syncthreads();
   if (tid < c0) t0[tid] = b0[tid] / d0[tid];  // u0 = D0^{-1} b0
   __syncthreads();
@@ -1967,7 +1965,7 @@ __global__ void __launch_bounds__(kCompThreads) k_schur_comp(PatchArgs a, SchurA
   {  // y = W r1 (rows, lower)
     double acc = 0.0;
     if (o < c1) {
-      const double* row = W + o * ldw;
+      const double* row = W + o * (o + 1) / 2;
       for (int q = h; q <= o; q += 2) acc = fma(row[q], t1[q], acc);
     }
     acc += __shfl_xor_sync(0xffffffffu, acc, 1);
@@ -1977,7 +1975,7 @@ __global__ void __launch_bounds__(kCompThreads) k_schur_comp(PatchArgs a, SchurA
   {  // x1 = W^T y (columns)
     double acc = 0.0;
     if (o < c1)
-      for (int q = o + h; q < c1; q += 2) acc = fma(W[q * ldw + o], b1[q], acc);
+      for (int q = o + h; q < c1; q += 2) acc = fma(W[q * (q + 1) / 2 + o], b1[q], acc);
     acc += __shfl_xor_sync(0xffffffffu, acc, 1);
     if (o < c1 && h == 0) t1[o] = acc;
   }

@@ -203,7 +203,10 @@ void analyze_schur_split(Context& c) {
   }
   blocked(nF, [&](int i) -> std::vector<int>& { return fr[S.fr_row[i]]; }, S.fr_ptr, S.fr_col, S.fr_blk, S.fr_bmax,
           S.fr_nnz);
-  S.comp_stride = (int64_t(c1) * (c0 | 1) + int64_t(c1) * (c1 | 1) + c0 + 1) & ~int64_t(1);  // 16-byte aligned
+  // component block: M (c1 rows, stride c0 | 1: the odd stride keeps row-per-thread and
+  // column-per-thread reads bank-conflict free), W lower triangle packed by rows (row i at
+  // i(i+1)/2), D0 (c0); 16-byte aligned for the bulk copy
+  S.comp_stride = (int64_t(c1) * (c0 | 1) + int64_t(c1) * (c1 + 1) / 2 + c0 + 1) & ~int64_t(1);
   S.rf_off = S.comp_stride * ncomp;
   S.fr_off = S.rf_off + int64_t(S.rf_col.size());
   S.vstride = (S.fr_off + int64_t(S.fr_col.size()) + 3) & ~int64_t(3);  // 32-byte aligned patch blocks
