@@ -278,14 +278,14 @@ def top_kernel_bytes(L):
     """Algorithmic bytes of the top-block stage (k_schur_symv): the lower triangle of
     S~_RR^{-1} once (FDMGPU_TOP=chol: L_RR twice) + t_R read / x_R write, per patch."""
     nr = L["n_top"]
-    passes = 2 if os.environ.get("FDMGPU_TOP") == "chol" else 1
+    passes = 1 if L["schur_split"] == 2 else 2
     return (8.0 * passes * nr * (nr + 1) / 2 + 16.0 * nr) * L["npatch"]
 
 
 def inverse_issued_flops(L):
     """FP64 tensor-pipe flops k_schur_uinv / k_schur_ainv issue per factorisation (dense 64x64
     tile GEMMs: column J of U takes sum_{I>J} (I - J + 1), tile (I, J) of A takes nT - I)."""
-    if not L["schur_split"] or os.environ.get("FDMGPU_TOP") == "chol":
+    if L["schur_split"] != 2:
         return 0.0
     nt = -(-L["n_top"] // 64)
     gemms = sum(I - J + 1 for J in range(nt) for I in range(J + 1, nt)) + sum(nt - I for I in range(nt)
@@ -296,7 +296,7 @@ def inverse_issued_flops(L):
 def inverse_flops(L):
     """Flops of the top-block inverse per factorisation: W = L_RR^{-1} (n^3/6 multiply-adds)
     and S~_RR^{-1} = W^T W (n^3/6), n = |R|, all patches (0 for FDMGPU_TOP=chol or no split)."""
-    if not L["schur_split"] or os.environ.get("FDMGPU_TOP") == "chol":
+    if L["schur_split"] != 2:
         return 0.0
     return 2.0 * (L["n_top"] ** 3 / 3.0) * L["npatch"]
 
@@ -349,7 +349,8 @@ def sub_measure(config, steps, warmup, stream, device):
     fac_flops = 2.0 * L["flops_ref"] * L["npatch"] + inverse_flops(L)
     return {"workload": WORKLOADS[config], "value": prob.nfree / (ms * 1e-3) / 1e9, "unit": "GDOF/s",
             "ms_per_step": ms, "steps": steps,
-            "roofline": {"kernel": "k_schur_symv (S~_RR^{-1} product)" if L["schur_split"] else
+            "roofline": {"kernel": "k_schur_symv (S~_RR^{-1} product)" if L["schur_split"] == 2 else
+                         "k_patch_solve on L_RR" if L["schur_split"] else
                          "k_patch_solve (+ split tail)",
                          "achieved": (tb if L["schur_split"] else kb) / ((top_ms if L["schur_split"] else solve_ms)
                                                                           * 1e-3) / 1e9,
@@ -513,7 +514,7 @@ def run_ours(args):
     try:
         tr = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")))
         ent = tr.get(str(args.config))
-        want = "k_schur_symv" if (L["schur_split"] and os.environ.get("FDMGPU_TOP") != "chol") else "k_patch_solve"
+        want = "k_schur_symv" if L["schur_split"] == 2 else "k_patch_solve"
         if ent and str(ent.get("kernel", "")).startswith(want):
             traffic = float(ent["dram_bytes_read"] + ent["dram_bytes_write"])
     except (OSError, ValueError, KeyError):
@@ -522,7 +523,7 @@ def run_ours(args):
     # separator columns of the factor the kernel streams (order in use; interior columns are never stored)
     solve_bytes = solve_kernel_bytes(L, prob)
     solve_kms = solve_ms / n_timed  # every launch of the separator solve (one timed interval)
-    inv_top = L["schur_split"] and os.environ.get("FDMGPU_TOP") != "chol"
+    inv_top = L["schur_split"] == 2
     if L["schur_split"]:
         # dominant kernel: the top-block stage of the Schur split
         kern_bytes = top_kernel_bytes(L)

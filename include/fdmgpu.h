@@ -70,7 +70,8 @@ typedef struct {
   int64_t stream_bytes;      /* packed factor bytes streamed per sweep, all patches */
   int64_t dmma_flops;        /* FP64 tensor-pipe flops the batched factorisation issues per patch
                                 (dense 64x64 tile GEMMs minus the skipped zero 16-wide panels) */
-  int32_t schur_split;       /* 1: the solve streams only the top-separator factor L_RR (Schur split) */
+  int32_t schur_split;       /* Schur split: 1 the solve streams the top-separator factor L_RR, 2 its
+                                symmetric inverse S~_RR^{-1} (default); 0 the full separator factor */
   int32_t n_top;             /* |R|: top-separator DOFs per patch (Schur split), else 0              */
   int64_t solve_values;      /* matrix values one relaxation solve reads per patch (fwd + bwd):
                                 split: 2 nnz(L_RR) + 2 x S_FF components + S_RF + S_FR; else 2 nnz(L_G) */

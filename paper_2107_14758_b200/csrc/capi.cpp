@@ -1170,7 +1170,7 @@ fdmgpu_status fdmgpu_get_layout(fdmgpu_handle h, fdmgpu_layout* out) {
     const auto& S = c.sx;
     if (S.on) {
       L.stream_bytes = int64_t(S.R.tile_poff8.back()) * 8 * c.npatch;
-      L.schur_split = 1;
+      L.schur_split = S.inv ? 2 : 1;
       L.n_top = S.nR;
       int64_t comp = 0;
       for (int k = 0; k < S.ncomp; ++k) {

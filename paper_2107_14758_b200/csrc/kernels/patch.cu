@@ -1479,24 +1479,31 @@ __global__ void k_schur_couplings(PatchArgs a, SchurArgs s, int npairs, const in
 // Per (component, patch): M, D0 and W = chol(S'_11)^{-1} (diag_factor_invert
 // on the 64x64 identity-padded matrix).  256 threads.
 __global__ void __launch_bounds__(256) k_schur_comps(PatchArgs a, SchurArgs s) {
-  extern __shared__ __align__(128) double sm[];
+  extern __shared__ __align__(16) double sm[];
   constexpr int LD = T + 1;
-  double* Dm = sm;                        // 64 x 65
-  double* Wm = Dm + T * LD;               // 16 x 64 x 4 + 64
-  double* Wo = Wm + 16 * T * 4 + T;       // 64 x 64 swizzled L^{-1}
-  double* M = Wo + TT;                    // 64 x 65
-  double* d0 = M + T * LD;                // 64
-  double* d1 = d0 + T;                    // 64
-  double* At = d1 + T;
-  double* Bt = At + a.n1 * a.n1;
-  double* mup = Bt + a.n1 * a.n1;  // 24
+  double* Dm = sm;                   // 64 x 65
+  double* Wm = Dm + T * LD;          // 16 x 64 x 4 + 64
+  double* MW = Wm + 16 * T * 4 + T;  // M (64 x 65), then the swizzled L^{-1}
+  double* d0 = MW + T * LD;          // 64
+  double* d1 = d0 + T;               // 64
+  double* mup = d1 + T;              // 24
   const int k = blockIdx.x, j = blockIdx.y, tid = threadIdx.x;
-  const int smask = load_patch_coeffs(a, j, At, Bt, mup);
+  // the 1D tables stay in global memory (L1-resident): two CTAs per SM at p = 31
+  int smask = 0;
+  const int ncorner = 1 << a.dim;
+  for (int sl = 0; sl < ncorner; ++sl) smask |= (a.pcells[size_t(j) * ncorner + sl] >= 0) << sl;
+  for (int i = tid; i < ncorner * a.dim; i += blockDim.x) {
+    const int sl = i / a.dim, q = i % a.dim, K = a.pcells[size_t(j) * ncorner + sl];
+    mup[i] = K >= 0 ? a.mu[size_t(K) * a.dim + q] : 0.0;
+  }
   __syncthreads();
+  const double* At = a.At;
+  const double* Bt = a.Bt;
   const int32_t* sep = a.psep + size_t(j) * a.m;
-  const bool whole = smask == (1 << (1 << a.dim)) - 1;
+  const bool whole = smask == (1 << ncorner) - 1;
   const int32_t* m0 = s.comp0 + size_t(k) * s.c0;
   const int32_t* m1 = s.comp1 + size_t(k) * s.c1;
+  double* M = MW;
   for (int idx = tid; idx < s.c1 * s.c0; idx += blockDim.x) {
     const int i = idx / s.c0, jj = idx % s.c0, r = m1[i], c = m0[jj];
     M[i * LD + jj] = (r < 0 || c < 0) ? 0.0 : sg_entry(a, sep, whole, mup, smask, r, c, At, Bt);
@@ -1510,6 +1517,12 @@ __global__ void __launch_bounds__(256) k_schur_comps(PatchArgs a, SchurArgs s) {
     d1[i] = r < 0 ? 1.0 : sg_entry(a, sep, whole, mup, smask, r, r, At, Bt);
   }
   __syncthreads();
+  double* out = s.vals + size_t(j) * s.vstride + size_t(k) * s.comp_stride;
+  const int ldm = s.c0 | 1;
+  for (int idx = tid; idx < s.c1 * ldm; idx += blockDim.x) {
+    const int i = idx / ldm, jj = idx % ldm;
+    out[idx] = jj < s.c0 ? M[i * LD + jj] : 0.0;
+  }
   for (int idx = tid; idx < TT; idx += blockDim.x) {
     const int cc = idx / T, r = idx % T;
     double v = r == cc ? 1.0 : 0.0;
@@ -1519,18 +1532,13 @@ __global__ void __launch_bounds__(256) k_schur_comps(PatchArgs a, SchurArgs s) {
     }
     Dm[cc * LD + r] = v;
   }
-  __syncthreads();
+  __syncthreads();  // M is dead: its space takes the inverse
   PatchArgs an = a;
   an.err = nullptr;  // the full factorisation reports non-SPD pivots
   an.diagL = nullptr;
+  double* Wo = MW;
   diag_factor_invert(Dm, Wm, Wo, an, 0, -1);
   __syncthreads();
-  double* out = s.vals + size_t(j) * s.vstride + size_t(k) * s.comp_stride;
-  const int ldm = s.c0 | 1;
-  for (int idx = tid; idx < s.c1 * ldm; idx += blockDim.x) {
-    const int i = idx / ldm, jj = idx % ldm;
-    out[idx] = jj < s.c0 ? M[i * LD + jj] : 0.0;
-  }
   out += s.c1 * ldm;
   for (int i = tid >> 5; i < s.c1; i += blockDim.x >> 5)  // W lower triangle, row i at i(i+1)/2
     for (int q = tid & 31; q <= i; q += 32) out[i * (i + 1) / 2 + q] = Wo[tsw(i, q)];
@@ -2039,8 +2047,21 @@ __global__ void __launch_bounds__(kSpmvThreads) k_schur_spmv(PatchArgs a, SchurA
   pdl_wait();
   const double bv = (sub == 0 && g >= 0) ? rt[g] : 0.0;
   mbar_wait(&bar, 0);
-  double acc = 0.0;
-  for (int e = r0 + sub; e < r1; e += 8) acc = fma(vs[e], x[cs[e]], acc);
+  // four independent gathers in flight per thread (the x reads are L1/L2 latency)
+  double a4[4] = {0.0, 0.0, 0.0, 0.0};
+  int e = r0 + sub;
+  for (; e + 24 < r1; e += 32) {
+    double xv[4], vv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      vv[u] = vs[e + 8 * u];
+      xv[u] = x[cs[e + 8 * u]];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) a4[u] = fma(vv[u], xv[u], a4[u]);
+  }
+  for (; e < r1; e += 8) a4[0] = fma(vs[e], x[cs[e]], a4[0]);
+  double acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
   acc += __shfl_xor_sync(0xffffffffu, acc, 4);
   acc += __shfl_xor_sync(0xffffffffu, acc, 2);
   acc += __shfl_xor_sync(0xffffffffu, acc, 1);
@@ -2405,7 +2426,7 @@ void launch_schur_setup(Context& c) {
     k_schur_couplings<<<grid, 256, smem_c, c.stream>>>(a, s, np, c.sx_pairs.p);
     FDM_LAUNCH_CHECK(c);
   }
-  const size_t smem = sizeof(double) * (size_t(T) * (T + 1) * 2 + 16 * T * 4 + T + TT + 2 * T + 2 * size_t(c.n1) * c.n1 + 24);
+  const size_t smem = sizeof(double) * (size_t(T) * (T + 1) * 2 + 16 * T * 4 + T + 2 * T + 24);
   FDM_CUDA(cudaFuncSetAttribute(k_schur_comps, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   k_schur_comps<<<dim3(c.sx.ncomp, c.npatch), 256, smem, c.stream>>>(a, s);
   FDM_LAUNCH_CHECK(c);

@@ -249,7 +249,9 @@ def test_launch_evidence(pkg, torch):
     sol.smooth(prob.rhs())
     # S^T cells, separator solve, patch gather, S cells (+ the Schur split's
     # F-block forward / R right-hand side / F-block backward launches)
-    assert sol.launch_count() - n0 == 6 + (3 if sol.layout()["schur_split"] else 0)
+    # split: + F-block forward, t_R, F-block backward, c_F launches; the inverse top block
+    # (schur_split 2) adds its chunk-sum launch
+    assert sol.launch_count() - n0 == 6 + {0: 0, 1: 3, 2: 5}[sol.layout()["schur_split"]]
     maps = open("/proc/self/maps").read()
     assert os.path.realpath(pkg.LIB_PATH) in maps or pkg.LIB_PATH in maps
 
@@ -473,6 +475,7 @@ def test_inplace_and_separate_packing_agree(pkg, torch, monkeypatch):
 def test_compact_solve_records_opt_in(pkg, oracle, torch, monkeypatch, cfg):
     """FDMGPU_COMPACT=1: sparse 8x8 sub-blocks of the solve records stored as one
     value per row (layout.cpp) give the same relaxation as the default records."""
+    monkeypatch.setenv("FDMGPU_SCHUR", "0")  # the option belongs to the full-factor stream
     prob = pkg.Problem(*cfg)
     sol = pkg.Solver(prob)
     sol.factor()

@@ -61,7 +61,7 @@ def test_split_matches_full_stream_and_oracle(case, pkg, oracle, torch):
     split = _solver(pkg, prob, True)
     full = _solver(pkg, prob, False)
     Ls, Lf = split.layout(), full.layout()
-    assert Ls["schur_split"] == 1 and Lf["schur_split"] == 0
+    assert Ls["schur_split"] == 2 and Lf["schur_split"] == 0
     assert 0 < Ls["n_top"] < Ls["n_interface"]
     if prob.dim == 3:  # 2D: R is the vertex alone, no byte saving (forced on here, off by default)
         assert 4 * Ls["solve_values"] <= 3 * Lf["solve_values"]
@@ -94,7 +94,7 @@ def test_split_survives_refactor_and_set_patches(pkg, oracle, torch):
     assert rel(sol.smooth(r), ref.smooth(r)) <= TOL_RELAX
     sol.set_patches(separator_order="plane")
     sol.factor()
-    assert sol.layout()["schur_split"] == 1
+    assert sol.layout()["schur_split"] == 2
     assert rel(sol.smooth(r), z0) <= 1e-13
 
 
@@ -110,7 +110,7 @@ def test_split_matches_full_stream_at_full_size(cfg, pkg, torch):
     out = {}
     for split in (True, False):
         sol = _solver(pkg, prob, split)
-        assert sol.layout()["schur_split"] == int(split)
+        assert sol.layout()["schur_split"] == (2 if split else 0)
         out[split] = sol.smooth(r).cpu().numpy()
         if split:
             assert np.array_equal(sol.smooth(r).cpu().numpy(), out[split])
