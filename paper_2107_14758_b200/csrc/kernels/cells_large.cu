@@ -463,7 +463,7 @@ __device__ __forceinline__ void load_rows32(double* __restrict__ Mt, const doubl
   for (int i = threadIdx.x; i < kL32 * kL32; i += blockDim.x) Mt[(i >> 5) + 32 * (i & 31)] = M[i];
 }
 
-__global__ void __launch_bounds__(256) k_cells_t1_32(int dir, int flags, const double* __restrict__ in,
+__global__ void __launch_bounds__(256, 2) k_cells_t1_32(int dir, int flags, const double* __restrict__ in,
                                                       const double* __restrict__ aux, double* __restrict__ E,
                                                       const int32_t* __restrict__ cdofs,
                                                       const double* __restrict__ inv_mult,
@@ -537,24 +537,55 @@ __global__ void __launch_bounds__(256) k_cells_t1_32(int dir, int flags, const d
     }
     __syncthreads();
   }
+  // x and y line passes, warp w on slab w: OUT(k, line) = sum_j M(k, j) X(j, line) as a
+  // 32 x 32 x 32 GEMM on the FP64 tensor pipe (DMMA m8n8k4; the 16 accumulator tiles in
+  // registers, A fragments of M and B fragments of the slab read from shared memory once
+  // per pass, OUT stored with the contracted index slowest so the second pass contracts y
+  // and restores the order)
   double* sl = slab + (tid >> 5) * kSlab32;
-  const int r = tid & 31;
+  const int lane = tid & 31, lq = lane >> 2, lr = lane & 3;
+#pragma unroll 1
   for (int pass = 0; pass < 2; ++pass) {
-    double x[32];
-    load_line32(sl, r, x);
-    __syncthreads();
-#pragma unroll 4
-    for (int k = 0; k < kL32; ++k) sl[pos32(r + 32 * k)] = dot32(Mt + 32 * k, x);
-    __syncthreads();
+    double d[4][4][2];  // [mt][nt] accumulators
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) d[mt][nt][0] = d[mt][nt][1] = 0.0;
+#pragma unroll
+    for (int kt = 0; kt < 8; ++kt) {
+      double xb[4];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) xb[nt] = sl[pos32(32 * (8 * nt + lq) + 4 * kt + lr)];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) {
+        const double fa = Mt[32 * (8 * mt + lq) + 4 * kt + lr];  // A fragment M(8 mt + lq, 4 kt + lr)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) dmma884(d[mt][nt][0], d[mt][nt][1], fa, xb[nt]);
+      }
+    }
+    __syncwarp();  // the whole slab is read before it is overwritten
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+        *reinterpret_cast<double2*>(sl + pos32(8 * nt + 2 * lr + 32 * (8 * mt + lq))) =
+            make_double2(d[mt][nt][0], d[mt][nt][1]);
+    __syncwarp();
   }
+  __syncthreads();
   double* e = E + size_t(c) * kNpc32 + size_t(z0) * kSlab32;
   for (int i = tid; i < 8 * kSlab32; i += 256) e[i] = slab[(i & ~1023) + pos32(i & 1023)];
 }
 
-__global__ void __launch_bounds__(256) k_cells_t2_32(int dir, int flags, double* __restrict__ E,
-                                                      const double* __restrict__ sign, const double* __restrict__ M,
-                                                      const double* __restrict__ mu, const double* __restrict__ At,
-                                                      const double* __restrict__ Bt) {
+// One z-line per thread, outputs streamed: each z value is contracted, gets its
+// x-face elimination term (a warp reduction over the lanes, which run along x)
+// and is stored at once; only the two z-face values wait for the line's
+// z-face sums.  Same arithmetic and order as materialising the line, in about
+// half the registers (two CTAs per SM instead of one).
+__global__ void __launch_bounds__(256, 2) k_cells_t2_32(int dir, int flags, double* __restrict__ E,
+                                                         const double* __restrict__ sign, const double* __restrict__ M,
+                                                         const double* __restrict__ mu, const double* __restrict__ At,
+                                                         const double* __restrict__ Bt) {
   extern __shared__ __align__(16) double sm[];
   double* Mt = sm;  // 1024
   Fdm32* t = reinterpret_cast<Fdm32*>(Mt + kL32 * kL32);
@@ -568,52 +599,53 @@ __global__ void __launch_bounds__(256) k_cells_t2_32(int dir, int flags, double*
 #pragma unroll
   for (int z = 0; z < kL32; ++z) u[z] = col[size_t(z) * kSlab32];
   __syncthreads();
-  double v[32];
-#pragma unroll
-  for (int k = 0; k < kL32; ++k) v[k] = dot32(Mt + 32 * k, u);
-  if (dir == 0 && sign) {
-    const double* sg = sign + size_t(c) * kNpc32 + 32 * y + x;
-#pragma unroll
-    for (int k = 0; k < kL32; ++k) v[k] *= sg[size_t(k) * kSlab32];
-  }
+  const double* sg = (dir == 0 && sign) ? sign + size_t(c) * kNpc32 + 32 * y + x : nullptr;
+  double m[3] = {0.0, 0.0, 0.0};
   if (schur) {
-    const double m[3] = {mu[size_t(c) * 3], mu[size_t(c) * 3 + 1], mu[size_t(c) * 3 + 2]};
-    const bool yi = y > 0 && y < kL32 - 1, xi = x > 0 && x < kL32 - 1;
-    // w_z = v_z / D(x, y, z) on interior points (0 elsewhere)
-    double w[32];
-#pragma unroll
-    for (int z = 0; z < kL32; ++z)
-      w[z] = (xi && yi && z > 0 && z < kL32 - 1) ? v[z] * (1.0 / diag32(*t, m, x, y, z)) : 0.0;
-    // x faces (e, y, z): sum over the lanes (x) of A~_{e x} w
-    if (yi) {
-#pragma unroll
-      for (int z = 1; z < kL32 - 1; ++z) {
-        double s0 = t->ar0[x] * w[z], sp = t->arp[x] * w[z];
+    m[0] = mu[size_t(c) * 3];
+    m[1] = mu[size_t(c) * 3 + 1];
+    m[2] = mu[size_t(c) * 3 + 2];
+  }
+  const bool yi = y > 0 && y < kL32 - 1, xi = x > 0 && x < kL32 - 1;
+  double v0 = 0.0, vp = 0.0, s0z = 0.0, spz = 0.0;
+#pragma unroll 2
+  for (int k = 0; k < kL32; ++k) {
+    double v = dot32(Mt + 32 * k, u);
+    if (sg) v *= sg[size_t(k) * kSlab32];
+    if (schur) {
+      const bool zi = k > 0 && k < kL32 - 1;
+      // w = v / D(x, y, z) on interior points (0 elsewhere)
+      const double w = (xi && yi && zi) ? v * (1.0 / diag32(*t, m, x, y, k)) : 0.0;
+      if (yi && zi) {  // x faces (e, y, z): sum over the lanes (x) of A~_{e x} w
+        double s0 = t->ar0[x] * w, sp = t->arp[x] * w;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
           s0 += __shfl_xor_sync(0xffffffffu, s0, o);
           sp += __shfl_xor_sync(0xffffffffu, sp, o);
         }
-        const double cx = m[0] * t->bd[y] * t->bd[z];
-        if (x == 0) v[z] -= cx * s0;
-        if (x == kL32 - 1) v[z] -= cx * sp;
+        const double cx = m[0] * t->bd[y] * t->bd[k];
+        if (x == 0) v -= cx * s0;
+        if (x == kL32 - 1) v -= cx * sp;
+      }
+      if (xi && yi && zi) {  // z faces (x, y, e): along the thread's own z-line
+        s0z = fma(t->ar0[k], w, s0z);
+        spz = fma(t->arp[k], w, spz);
       }
     }
-    // z faces (x, y, e): sum along the thread's own z-line
-    if (xi && yi) {
-      double s0 = 0.0, sp = 0.0;
-#pragma unroll
-      for (int z = 1; z < kL32 - 1; ++z) {
-        s0 = fma(t->ar0[z], w[z], s0);
-        sp = fma(t->arp[z], w[z], sp);
-      }
-      const double cz = m[2] * t->bd[x] * t->bd[y];
-      v[0] -= cz * s0;
-      v[kL32 - 1] -= cz * sp;
-    }
+    if (k == 0)
+      v0 = v;
+    else if (k == kL32 - 1)
+      vp = v;
+    else
+      col[size_t(k) * kSlab32] = v;
   }
-#pragma unroll
-  for (int k = 0; k < kL32; ++k) col[size_t(k) * kSlab32] = v[k];
+  if (schur && xi && yi) {
+    const double cz = m[2] * t->bd[x] * t->bd[y];
+    v0 -= cz * s0z;
+    vp -= cz * spz;
+  }
+  col[0] = v0;
+  col[size_t(kL32 - 1) * kSlab32] = vp;
 }
 
 // y faces (x, e, z) for x, z interior: thread per y-line.
@@ -770,7 +802,10 @@ void prepare_buffers(Context& c) {
 static void launch_cells_transform_32(Context& c, int dir, const double* in, int flags, const double* aux) {
   const double* M = dir == 0 ? c.St.p : c.S.p;
   const int32_t* cd = dir == 0 ? c.cell_dofs.p : c.cell_modes.p;
-  const size_t s1 = sizeof(double) * (kL32 * kL32 + 10 * kSlab32) + sizeof(Fdm32);
+  // the face planes and FDM tables only for the interior rebuild (S with recon):
+  // S^T fits three CTAs per SM
+  const bool recon = dir == 1 && (flags & 2);
+  const size_t s1 = sizeof(double) * (kL32 * kL32 + (recon ? 10 : 8) * kSlab32) + (recon ? sizeof(Fdm32) : 0);
   const size_t s2 = sizeof(double) * kL32 * kL32 + sizeof(Fdm32);
   FDM_CUDA(cudaFuncSetAttribute(k_cells_t1_32, cudaFuncAttributeMaxDynamicSharedMemorySize, int(s1)));
   KernelTimer timer(c, 2);
