@@ -482,15 +482,6 @@ __global__ void __launch_bounds__(256, 2) k_cells_t1_32(int dir, int flags, cons
   load_rows32(Mt, M);
   if (recon) load_fdm32(t, At, Bt);
   const int32_t* cd = cdofs + size_t(c) * kNpc32;
-  auto fetch = [&](int l) {
-    const int g = cd[l];
-    double v = cons[g] ? 0.0 : in[g];
-    if (dir == 0)
-      v *= inv_mult[g];
-    else if (sign)
-      v *= sign[size_t(c) * kNpc32 + l];
-    return v;
-  };
   // gather in batches of 8 per thread: all map loads first, then the independent
   // value loads (8 DRAM round trips in flight per thread instead of a chain)
 #pragma unroll 1
@@ -512,28 +503,62 @@ __global__ void __launch_bounds__(256, 2) k_cells_t1_32(int dir, int flags, cons
       slab[(i & ~1023) + pos32(i & 1023)] = v[u];
     }
   }
-  if (recon)
-    for (int i = tid; i < 2 * kSlab32; i += 256) zf[i] = fetch((i >> 10) * (kL32 - 1) * kSlab32 + (i & 1023));
+  if (recon) {  // the z = 0 / z = p face planes, gathered 8 per thread with the loads in flight together
+    int gi[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = tid + 256 * u;
+      gi[u] = cd[(i >> 10) * (kL32 - 1) * kSlab32 + (i & 1023)];
+    }
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = tid + 256 * u, l = (i >> 10) * (kL32 - 1) * kSlab32 + (i & 1023), g = gi[u];
+      const double xv = in[g];
+      const double w = sign ? sign[size_t(c) * kNpc32 + l] : 1.0;
+      v[u] = cons[g] ? 0.0 : xv * w;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) zf[tid + 256 * u] = v[u];
+  }
   __syncthreads();
   if (recon) {
     const double m[3] = {mu[size_t(c) * 3], mu[size_t(c) * 3 + 1], mu[size_t(c) * 3 + 2]};
     const double nk = nK[c];
-    constexpr int pm = kL32 - 2;
-    for (int i = tid; i < 8 * pm * pm; i += 256) {
-      const int s = i / (pm * pm), z = z0 + s;
-      if (z == 0 || z == kL32 - 1) continue;
-      const int y = 1 + (i / pm) % pm, x = 1 + i % pm;
-      double* sl = slab + s * kSlab32;
-      const int o = x + 32 * y;
-      double v = nk * aux[cd[size_t(z) * kSlab32 + o]];
-      // faces along x, y (this slab) and z (the face planes), as recon_interior
-      const double cx = m[0] * t->bd[y] * t->bd[z];
-      v -= cx * (t->ac0[x] * sl[pos32(0 + 32 * y)] + t->acp[x] * sl[pos32(kL32 - 1 + 32 * y)]);
-      const double cy = m[1] * t->bd[x] * t->bd[z];
-      v -= cy * (t->ac0[y] * sl[pos32(x)] + t->acp[y] * sl[pos32(x + 32 * (kL32 - 1))]);
-      const double cz = m[2] * t->bd[x] * t->bd[y];
-      v -= cz * (t->ac0[z] * zf[o] + t->acp[z] * zf[kSlab32 + o]);
-      sl[pos32(o)] = v * (1.0 / diag32(*t, m, x, y, z));
+    constexpr int pm = kL32 - 2, npts = 8 * pm * pm;
+    // interior rebuild, 8 points per thread per batch: the aux gathers of a batch are
+    // issued together (one dependent round trip per batch, not per point)
+#pragma unroll 1
+    for (int b0 = tid; b0 < npts; b0 += 256 * 8) {
+      double av[8];
+      {
+        int ga[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int i = b0 + 256 * u, s = i / (pm * pm), z = z0 + s;
+          const int y = 1 + (i / pm) % pm, x = 1 + i % pm;
+          ga[u] = (i < npts && z > 0 && z < kL32 - 1) ? cd[size_t(z) * kSlab32 + x + 32 * y] : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) av[u] = ga[u] >= 0 ? aux[ga[u]] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = b0 + 256 * u, s = i / (pm * pm), z = z0 + s;
+        if (i >= npts || z == 0 || z == kL32 - 1) continue;
+        const int y = 1 + (i / pm) % pm, x = 1 + i % pm;
+        double* sl = slab + s * kSlab32;
+        const int o = x + 32 * y;
+        double v = nk * av[u];
+        // faces along x, y (this slab) and z (the face planes), as recon_interior
+        const double cx = m[0] * t->bd[y] * t->bd[z];
+        v -= cx * (t->ac0[x] * sl[pos32(0 + 32 * y)] + t->acp[x] * sl[pos32(kL32 - 1 + 32 * y)]);
+        const double cy = m[1] * t->bd[x] * t->bd[z];
+        v -= cy * (t->ac0[y] * sl[pos32(x)] + t->acp[y] * sl[pos32(x + 32 * (kL32 - 1))]);
+        const double cz = m[2] * t->bd[x] * t->bd[y];
+        v -= cz * (t->ac0[z] * zf[o] + t->acp[z] * zf[kSlab32 + o]);
+        sl[pos32(o)] = v * (1.0 / diag32(*t, m, x, y, z));
+      }
     }
     __syncthreads();
   }
