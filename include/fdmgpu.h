@@ -201,7 +201,14 @@ fdmgpu_status fdmgpu_set_coarse_cells(fdmgpu_handle h, const int32_t* coarse_cel
 /* Batched numeric factorisation of every patch matrix A~_j under its
  * patch ordering (replaces cholesky(), src/cholesky.cpp:9-87, inside
  * build_patch_solver, src/schwarz.cpp:84-93).  Returns FDMGPU_NOT_SPD with
- * "cholesky: matrix not SPD at pivot k (patch j)" on a non-positive pivot. */
+ * "cholesky: matrix not SPD at pivot k (patch j)" on a non-positive pivot.
+ * With the plane-by-plane separator order (3D scalar CG layouts) it also
+ * prepares the Schur-split solve the relaxation then uses (fdmgpu_layout.
+ * schur_split): the first two facet planes are applied from the Schur
+ * complement's own entries and only the top separator block is streamed, as
+ * its explicit symmetric inverse (default) or its Cholesky factor (env
+ * FDMGPU_TOP=chol); env FDMGPU_SCHUR=0 at fdmgpu_set_patches keeps the full
+ * separator factor.  Patch solutions agree to rounding in every form. */
 fdmgpu_status fdmgpu_factor(fdmgpu_handle h);
 fdmgpu_status fdmgpu_get_layout(fdmgpu_handle h, fdmgpu_layout* out);
 /* The separator Schur complement S_G = A_BB - A_BI A_II^{-1} A_IB of patch j

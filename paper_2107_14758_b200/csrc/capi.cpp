@@ -232,7 +232,9 @@ void op_smooth(Context& c, const double* r, double* z) {
   launch_cells_transform(c, 0, r, 1, nullptr);  // S^T r, minus each cell's interior-elimination share
   launch_gather(c, 0, c.E.p, nullptr, c.w[6].p);
   launch_patch_solve(c, c.w[6].p);               // separator solves
-  launch_patch_gather(c, c.w[7].p);              // patch-summed separator corrections
+  // patch-summed separator corrections: only the cell-boundary entries -- the S
+  // transform rebuilds every cell-interior value from the faces and never reads them
+  launch_patch_gather_bnd(c, c.w[7].p);
   launch_cells_transform(c, 1, c.w[7].p, 2, c.w[6].p);  // rebuild interiors, S
   launch_gather(c, 1, c.E.p, nullptr, z);
 }
@@ -586,7 +588,10 @@ fdmgpu_status fdmgpu_create(fdmgpu_handle* out, int32_t dim, int32_t p, int32_t 
     const char* fu = std::getenv("FDMGPU_FUSED");
     cc.fused_columns = !(fu && fu[0] == '0');
     cc.E.alloc(size_t(cc.ncells) * cc.npc);
-    for (auto& v : cc.w) v.alloc(cc.ndof);
+    for (auto& v : cc.w) {
+      v.alloc(cc.ndof);
+      FDM_CUDA(cudaMemsetAsync(v.p, 0, v.bytes(), cc.stream));  // finite from the start (see bnd_list)
+    }
     cc.red.alloc(4 * fdmgpu::kRedBlocks);
     cc.d_err.alloc(1);
   });
@@ -810,6 +815,20 @@ fdmgpu_status fdmgpu_set_mesh_maps(fdmgpu_handle h, const int32_t* cell_dofs, co
       c.mode_sign.reset();
     c.inv_mult.upload(inv, c.stream);
     c.constrained.upload(c.h_constrained, c.stream);
+    {  // cell-boundary modal DOFs: positions with a lattice coordinate 0 or p in some cell
+      std::vector<uint8_t> on(c.ndof, 0);
+      const int n1 = c.n1;
+      for (int k = 0; k < c.ncells; ++k)
+        for (int l = 0; l < c.npc; ++l) {
+          bool bnd = false;
+          for (int a = 0, r = l; a < c.dim; ++a, r /= n1) bnd = bnd || r % n1 == 0 || r % n1 == n1 - 1;
+          if (bnd) on[c.h_cell_modes[size_t(k) * c.npc + l]] = 1;
+        }
+      std::vector<int32_t> list;
+      for (int64_t g = 0; g < c.ndof; ++g)
+        if (on[g]) list.push_back(int32_t(g));
+      c.bnd_list.upload(list, c.stream);
+    }
     FDM_CUDA(cudaStreamSynchronize(c.stream));
     c.have_maps = true;
   });

@@ -175,6 +175,9 @@ struct Context {
   // maps
   DevArray<int32_t> cell_dofs, cell_modes, g_ptr, g_idx, gm_ptr, gm_idx;
   DevArray<double> mode_sign, inv_mult, E, E2;
+  // modal DOFs on cell boundaries (ascending): the only entries of the patch-summed
+  // correction the interior-rebuilding S transform reads (op_smooth's compact patch gather)
+  DevArray<int32_t> bnd_list;
   DevArray<uint8_t> constrained;
   std::vector<int32_t> h_cell_dofs, h_cell_modes;
   std::vector<uint8_t> h_constrained;
@@ -342,6 +345,7 @@ void launch_schur_setup(Context& c);   // Schur split: S_FF components, S_RF / S
 void launch_schur_retile(Context& c);  // Schur split: L_RR records from the factored tiles
 void launch_patch_solve(Context& c, const double* r_modal);          // writes c.corr
 void launch_patch_gather(Context& c, double* z_modal);
+void launch_patch_gather_bnd(Context& c, double* z_modal);  // cell-boundary DOFs only (op_smooth)
 void launch_axpby(Context& c, int64_t n, double a, const double* x, double b, const double* y, double* out);
 void launch_dot_partials(Context& c, int64_t n, const double* x, const double* y, int k);
 void launch_restrict(Context& c, const double* fine, double* coarse);

@@ -1915,6 +1915,10 @@ __global__ void k_schur_xsum(int nR, int mpadR, int nchunk, int m, int nF, const
 // row stride makes both its row-wise and column-wise reads conflict free.
 // Output: mode 0 -> Fw (npatch x nF), mode 1 -> corr (F part of the separator solution).
 constexpr int kCompThreads = 128;
+// STAGED: the block is bulk-copied into shared memory (44 KB at p = 31: 5 CTAs per
+// SM); otherwise the products read it straight from global memory through L1
+// (2.5 KB of shared memory: up to 16 CTAs per SM).
+template <bool STAGED>
 __global__ void __launch_bounds__(kCompThreads) k_schur_comp(PatchArgs a, SchurArgs s, const double* __restrict__ rt,
                                                              const double* __restrict__ cF, double* __restrict__ out,
                                                              int mode) {
@@ -1924,14 +1928,16 @@ __global__ void __launch_bounds__(kCompThreads) k_schur_comp(PatchArgs a, SchurA
   const int k = blockIdx.x, j = blockIdx.y, tid = threadIdx.x;
   const int c0 = s.c0, c1 = s.c1, ldm = c0 | 1;
   const double* src = s.vals + size_t(j) * s.vstride + size_t(k) * s.comp_stride;
-  if (tid == 0) {
-    mbar_init(&bar, 1);
-    mbar_fence_init();
-    const uint32_t bytes = uint32_t(s.comp_stride * sizeof(double));
-    mbar_arrive_expect_tx(&bar, bytes);
-    bulk_g2s(sm, src, bytes, &bar);  // values do not depend on the predecessor
+  if (STAGED) {
+    if (tid == 0) {
+      mbar_init(&bar, 1);
+      mbar_fence_init();
+      const uint32_t bytes = uint32_t(s.comp_stride * sizeof(double));
+      mbar_arrive_expect_tx(&bar, bytes);
+      bulk_g2s(sm, src, bytes, &bar);  // values do not depend on the predecessor
+    }
+    __syncthreads();  // the barrier is initialised before anyone waits on it
   }
-  __syncthreads();  // the barrier is initialised before anyone waits on it
   const int32_t* m0 = s.comp0 + size_t(k) * c0;
   const int32_t* m1 = s.comp1 + size_t(k) * c1;
   const int32_t* sep = a.psep + size_t(j) * a.m;
@@ -1951,9 +1957,9 @@ __global__ void __launch_bounds__(kCompThreads) k_schur_comp(PatchArgs a, SchurA
     b0[tid] = g0 >= 0 ? bsrc[g0] : 0.0;
     b1[tid] = g1 >= 0 ? bsrc[g1] : 0.0;
   }
-  mbar_wait(&bar, 0);
-  const double* M = sm;
-  const double* W = sm + c1 * ldm;  // lower triangle packed by rows: W(i, q) at i(i+1)/2 + q
+  if (STAGED) mbar_wait(&bar, 0);
+  const double* M = STAGED ? sm : src;
+  const double* W = M + c1 * ldm;  // lower triangle packed by rows: W(i, q) at i(i+1)/2 + q
   const double* d0 = W + c1 * (c1 + 1) / 2;
   __syncthreads();
   if (tid < c0) t0[tid] = b0[tid] / d0[tid];  // u0 = D0^{-1} b0
@@ -2007,6 +2013,9 @@ __global__ void __launch_bounds__(kCompThreads) k_schur_comp(PatchArgs a, SchurA
 // The block's values and column indices (contiguous, 16-byte aligned) arrive
 // in shared memory by two TMA bulk copies issued at entry; 8 threads per row.
 constexpr int kSpmvThreads = 8 * kSpmvRows;
+// STAGED: the block's values / columns bulk-copied into shared memory; otherwise
+// read straight from global memory (coalesced: a row's entries are contiguous).
+template <bool STAGED>
 __global__ void __launch_bounds__(kSpmvThreads) k_schur_spmv(PatchArgs a, SchurArgs s, const double* __restrict__ rt,
                                                              const double* __restrict__ xin, double* __restrict__ out,
                                                              int mode) {
@@ -2018,20 +2027,22 @@ __global__ void __launch_bounds__(kSpmvThreads) k_schur_spmv(PatchArgs a, SchurA
   const int32_t* col = mode == 0 ? s.rf_col : s.fr_col;
   const double* v = s.vals + size_t(j) * s.vstride + (mode == 0 ? s.rf_off : s.fr_off);
   const int e0 = blk[b], ne = blk[b + 1] - e0;
-  double* vs = sm;
-  int32_t* cs = reinterpret_cast<int32_t*>(sm + ne);
-  if (tid == 0) {
-    mbar_init(&bar, 1);
-    mbar_fence_init();
-    if (ne > 0) {
-      mbar_arrive_expect_tx(&bar, uint32_t(ne) * 12u);
-      bulk_g2s(vs, v + e0, uint32_t(ne) * 8u, &bar);
-      bulk_g2s(cs, col + e0, uint32_t(ne) * 4u, &bar);
-    } else {
-      mbar_arrive(&bar);
+  const double* vs = STAGED ? sm : v + e0;
+  const int32_t* cs = STAGED ? reinterpret_cast<const int32_t*>(sm + ne) : col + e0;
+  if (STAGED) {
+    if (tid == 0) {
+      mbar_init(&bar, 1);
+      mbar_fence_init();
+      if (ne > 0) {
+        mbar_arrive_expect_tx(&bar, uint32_t(ne) * 12u);
+        bulk_g2s(sm, v + e0, uint32_t(ne) * 8u, &bar);
+        bulk_g2s(sm + ne, col + e0, uint32_t(ne) * 4u, &bar);
+      } else {
+        mbar_arrive(&bar);
+      }
     }
+    __syncthreads();
   }
-  __syncthreads();
   const int nrows = mode == 0 ? s.nR : s.nF;
   const int rl = tid >> 3, sub = tid & 7, r = b * kSpmvRows + rl;
   const bool live = r < nrows;
@@ -2046,7 +2057,7 @@ __global__ void __launch_bounds__(kSpmvThreads) k_schur_spmv(PatchArgs a, SchurA
   pdl_trigger();
   pdl_wait();
   const double bv = (sub == 0 && g >= 0) ? rt[g] : 0.0;
-  mbar_wait(&bar, 0);
+  if (STAGED) mbar_wait(&bar, 0);
   // four independent gathers in flight per thread (the x reads are L1/L2 latency)
   double a4[4] = {0.0, 0.0, 0.0, 0.0};
   int e = r0 + sub;
@@ -2071,6 +2082,26 @@ __global__ void __launch_bounds__(kSpmvThreads) k_schur_spmv(PatchArgs a, SchurA
     else
       out[size_t(j) * s.nF + pos] = bv - acc;
   }
+}
+
+// k_patch_gather over a list of DOFs (the cell-boundary ones): same sums, same order.
+__global__ void k_patch_gather_list(int64_t n, const int32_t* __restrict__ list, const double* __restrict__ corr,
+                                    const int32_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+                                    double* __restrict__ z) {
+  pdl_trigger();
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  int g = 0, q0 = 0, q1 = 0, i0 = 0;
+  if (i < n) {
+    g = list[i];
+    q0 = ptr[g];
+    q1 = ptr[g + 1];
+    if (q1 > q0) i0 = idx[q0];
+  }
+  pdl_wait();
+  if (i >= n) return;
+  double s = q1 > q0 ? corr[i0] : 0.0;
+  for (int q = q0 + 1; q < q1; ++q) s += corr[idx[q]];
+  z[g] = s;
 }
 
 }  // namespace
@@ -2292,17 +2323,22 @@ void launch_patch_solve(Context& c, const double* r_modal) {
   const SchurSplit& S = c.sx;
   const SchurArgs s = make_schur_args(c);
   const bool pdl = c.pdl && !c.timing;
-  const size_t csm = sizeof(double) * size_t(S.comp_stride);
-  FDM_CUDA(cudaFuncSetAttribute(k_schur_comp, cudaFuncAttributeMaxDynamicSharedMemorySize, int(csm)));
+  const char* cenv = std::getenv("FDMGPU_COMP_STAGED");
+  const bool staged = !(cenv && cenv[0] == '0');
+  auto kcomp = staged ? k_schur_comp<true> : k_schur_comp<false>;
+  const size_t csm = staged ? sizeof(double) * size_t(S.comp_stride) : 0;
+  FDM_CUDA(cudaFuncSetAttribute(kcomp, cudaFuncAttributeMaxDynamicSharedMemorySize, int(csm)));
   const dim3 cgrid(S.ncomp, c.npatch);
   // w = S_FF^{-1} b_F;  t_R = b_R - S_RF w
-  launch_pdl(pdl, k_schur_comp, cgrid, dim3(kCompThreads), csm, c.stream, a, s, r_modal, (const double*)nullptr,
+  launch_pdl(pdl, kcomp, cgrid, dim3(kCompThreads), csm, c.stream, a, s, r_modal, (const double*)nullptr,
              c.sx_F.p, 0);
   FDM_LAUNCH_CHECK(c);
-  const size_t smem_rf = size_t(S.rf_bmax) * 12, smem_fr = size_t(S.fr_bmax) * 12;
-  FDM_CUDA(cudaFuncSetAttribute(k_schur_spmv, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                int(std::max(smem_rf, smem_fr))));
-  launch_pdl(pdl, k_schur_spmv, dim3(int(S.rf_blk.size()) - 1, c.npatch), dim3(kSpmvThreads), smem_rf, c.stream, a, s,
+  const char* senv = std::getenv("FDMGPU_SPMV_STAGED");
+  const bool sstaged = !(senv && senv[0] == '0');
+  auto kspmv = sstaged ? k_schur_spmv<true> : k_schur_spmv<false>;
+  const size_t smem_rf = sstaged ? size_t(S.rf_bmax) * 12 : 0, smem_fr = sstaged ? size_t(S.fr_bmax) * 12 : 0;
+  FDM_CUDA(cudaFuncSetAttribute(kspmv, cudaFuncAttributeMaxDynamicSharedMemorySize, int(std::max(smem_rf, smem_fr))));
+  launch_pdl(pdl, kspmv, dim3(int(S.rf_blk.size()) - 1, c.npatch), dim3(kSpmvThreads), smem_rf, c.stream, a, s,
              r_modal, (const double*)c.sx_F.p, c.sx_tR.p, 0);
   FDM_LAUNCH_CHECK(c);
   // x_R = S~_RR^{-1} t_R (dense stream) -> corr[nF..m)
@@ -2343,10 +2379,10 @@ void launch_patch_solve(Context& c, const double* r_modal) {
   }
   }
   // c_F = b_F - S_FR x_R;  x_F = S_FF^{-1} c_F -> corr[0..nF)
-  launch_pdl(pdl, k_schur_spmv, dim3(int(S.fr_blk.size()) - 1, c.npatch), dim3(kSpmvThreads), smem_fr, c.stream, a, s,
+  launch_pdl(pdl, kspmv, dim3(int(S.fr_blk.size()) - 1, c.npatch), dim3(kSpmvThreads), smem_fr, c.stream, a, s,
              r_modal, (const double*)c.corr.p, c.sx_F.p, 1);
   FDM_LAUNCH_CHECK(c);
-  launch_pdl(pdl, k_schur_comp, cgrid, dim3(kCompThreads), csm, c.stream, a, s, r_modal, (const double*)c.sx_F.p,
+  launch_pdl(pdl, kcomp, cgrid, dim3(kCompThreads), csm, c.stream, a, s, r_modal, (const double*)c.sx_F.p,
              c.corr.p, 1);
   FDM_LAUNCH_CHECK(c);
 }
@@ -2492,6 +2528,16 @@ void launch_patch_pack(Context& c) {
   k_patch_pack<<<c.npatch, 512, 2 * TT * sizeof(double), c.stream>>>(c.L.ntiles, c.tile_bptr.p, c.tile_blk.p,
                                                                      c.tile_ccol.p, c.tile_poff8.p, c.tile_hdr.p,
                                                                      c.tiles.p);
+  FDM_LAUNCH_CHECK(c);
+}
+
+void launch_patch_gather_bnd(Context& c, double* z_modal) {
+  if (!c.bnd_list.p) return launch_patch_gather(c, z_modal);
+  const int threads = 256;
+  const int64_t n = int64_t(c.bnd_list.n), blocks = (n + threads - 1) / threads;
+  launch_pdl(c.pdl && !c.timing, k_patch_gather_list, dim3(unsigned(blocks)), dim3(threads), 0, c.stream, n,
+             (const int32_t*)c.bnd_list.p, (const double*)c.corr.p, (const int32_t*)c.pg_ptr.p,
+             (const int32_t*)c.pg_idx.p, z_modal);
   FDM_LAUNCH_CHECK(c);
 }
 
