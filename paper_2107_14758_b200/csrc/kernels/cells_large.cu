@@ -602,11 +602,15 @@ __global__ void __launch_bounds__(256, 2) k_cells_t1_32(int dir, int flags, cons
   for (int i = tid; i < 8 * kSlab32; i += 256) e[i] = slab[(i & ~1023) + pos32(i & 1023)];
 }
 
-// One z-line per thread, outputs streamed: each z value is contracted, gets its
-// x-face elimination term (a warp reduction over the lanes, which run along x)
-// and is stored at once; only the two z-face values wait for the line's
-// z-face sums.  Same arithmetic and order as materialising the line, in about
-// half the registers (two CTAs per SM instead of one).
+// z contraction, warp per y-plane of the cell: OUT(z', x) = sum_z M(z', z) U(z, x)
+// as a 32 x 32 x 32 GEMM on the FP64 tensor pipe (DMMA m8n8k4): B fragments
+// straight from the E-vector (lane: z = 4 kt + lane % 4, x = 8 nt + lane / 4),
+// A fragments of M from shared memory, the 16 accumulator tiles in registers.
+// Lane (lq, lr) then holds OUT(8 mt + lq, 8 nt + 2 lr + {0, 1}); the interior
+// elimination sums run on these fragments: the x-face sums (over x, per z')
+// reduce over the 4 lanes sharing lq, the z-face sums (over z', per x) over the
+// 8 lanes sharing lr.  Mode signs and the z-face corrections are applied
+// before the pairs are stored.
 __global__ void __launch_bounds__(256, 2) k_cells_t2_32(int dir, int flags, double* __restrict__ E,
                                                          const double* __restrict__ sign, const double* __restrict__ M,
                                                          const double* __restrict__ mu, const double* __restrict__ At,
@@ -615,62 +619,99 @@ __global__ void __launch_bounds__(256, 2) k_cells_t2_32(int dir, int flags, doub
   double* Mt = sm;  // 1024
   Fdm32* t = reinterpret_cast<Fdm32*>(Mt + kL32 * kL32);
   const int c = blockIdx.x >> 2;
-  const int tid = threadIdx.x, x = tid & 31, y = 8 * (blockIdx.x & 3) + (tid >> 5);
+  const int tid = threadIdx.x, lane = tid & 31, lq = lane >> 2, lr = lane & 3;
+  const int y = 8 * (blockIdx.x & 3) + (tid >> 5);
   const bool schur = dir == 0 && (flags & 1);
   load_rows32(Mt, M);
   if (schur) load_fdm32(t, At, Bt);
-  double* col = E + size_t(c) * kNpc32 + 32 * y + x;
-  double u[32];
+  double* pl = E + size_t(c) * kNpc32 + 32 * y;  // plane y: element (z, x) at z * kSlab32 + x
+  double d[4][4][2];
 #pragma unroll
-  for (int z = 0; z < kL32; ++z) u[z] = col[size_t(z) * kSlab32];
+  for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) d[mt][nt][0] = d[mt][nt][1] = 0.0;
   __syncthreads();
-  const double* sg = (dir == 0 && sign) ? sign + size_t(c) * kNpc32 + 32 * y + x : nullptr;
-  double m[3] = {0.0, 0.0, 0.0};
-  if (schur) {
-    m[0] = mu[size_t(c) * 3];
-    m[1] = mu[size_t(c) * 3 + 1];
-    m[2] = mu[size_t(c) * 3 + 2];
-  }
-  const bool yi = y > 0 && y < kL32 - 1, xi = x > 0 && x < kL32 - 1;
-  double v0 = 0.0, vp = 0.0, s0z = 0.0, spz = 0.0;
-#pragma unroll 2
-  for (int k = 0; k < kL32; ++k) {
-    double v = dot32(Mt + 32 * k, u);
-    if (sg) v *= sg[size_t(k) * kSlab32];
-    if (schur) {
-      const bool zi = k > 0 && k < kL32 - 1;
-      // w = v / D(x, y, z) on interior points (0 elsewhere)
-      const double w = (xi && yi && zi) ? v * (1.0 / diag32(*t, m, x, y, k)) : 0.0;
-      if (yi && zi) {  // x faces (e, y, z): sum over the lanes (x) of A~_{e x} w
-        double s0 = t->ar0[x] * w, sp = t->arp[x] * w;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          s0 += __shfl_xor_sync(0xffffffffu, s0, o);
-          sp += __shfl_xor_sync(0xffffffffu, sp, o);
+  for (int kt = 0; kt < 8; ++kt) {
+    double xb[4];
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) xb[nt] = pl[size_t(4 * kt + lr) * kSlab32 + 8 * nt + lq];
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) {
+      const double fa = Mt[32 * (8 * mt + lq) + 4 * kt + lr];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) dmma884(d[mt][nt][0], d[mt][nt][1], fa, xb[nt]);
+    }
+  }
+  __syncwarp();  // the plane is read before it is overwritten
+  if (dir == 0 && sign) {
+    const double* sg = sign + size_t(c) * kNpc32 + 32 * y;
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) d[mt][nt][e] *= sg[size_t(8 * mt + lq) * kSlab32 + 8 * nt + 2 * lr + e];
+  }
+  if (schur) {
+    const double m[3] = {mu[size_t(c) * 3], mu[size_t(c) * 3 + 1], mu[size_t(c) * 3 + 2]};
+    const bool yi = y > 0 && y < kL32 - 1;
+    double s0z[4][2], spz[4][2];  // z-face partial sums per (nt, e) column x
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) s0z[nt][0] = s0z[nt][1] = spz[nt][0] = spz[nt][1] = 0.0;
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) {
+      const int z = 8 * mt + lq;
+      const bool zi = z > 0 && z < kL32 - 1;
+      double s0 = 0.0, sp = 0.0;  // x-face partial sums of this lane's 8 x values at z
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int x = 8 * nt + 2 * lr + e;
+          const bool xi = x > 0 && x < kL32 - 1;
+          const double w = (xi && yi && zi) ? d[mt][nt][e] * (1.0 / diag32(*t, m, x, y, z)) : 0.0;
+          s0 = fma(t->ar0[x], w, s0);
+          sp = fma(t->arp[x], w, sp);
+          s0z[nt][e] = fma(t->ar0[z], w, s0z[nt][e]);
+          spz[nt][e] = fma(t->arp[z], w, spz[nt][e]);
         }
-        const double cx = m[0] * t->bd[y] * t->bd[k];
-        if (x == 0) v -= cx * s0;
-        if (x == kL32 - 1) v -= cx * sp;
-      }
-      if (xi && yi && zi) {  // z faces (x, y, e): along the thread's own z-line
-        s0z = fma(t->ar0[k], w, s0z);
-        spz = fma(t->arp[k], w, spz);
+      // x faces (e, y, z): over the 4 lanes sharing lq
+      s0 += __shfl_xor_sync(0xffffffffu, s0, 1);
+      sp += __shfl_xor_sync(0xffffffffu, sp, 1);
+      s0 += __shfl_xor_sync(0xffffffffu, s0, 2);
+      sp += __shfl_xor_sync(0xffffffffu, sp, 2);
+      if (yi && zi) {
+        const double cx = m[0] * t->bd[y] * t->bd[z];
+        if (lr == 0) d[mt][0][0] -= cx * s0;   // x = 0
+        if (lr == 3) d[mt][3][1] -= cx * sp;   // x = 31
       }
     }
-    if (k == 0)
-      v0 = v;
-    else if (k == kL32 - 1)
-      vp = v;
-    else
-      col[size_t(k) * kSlab32] = v;
+    // z faces (x, y, e): over the 8 lanes sharing lr
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        double a0 = s0z[nt][e], ap = spz[nt][e];
+#pragma unroll
+        for (int o = 4; o < 32; o <<= 1) {
+          a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+          ap += __shfl_xor_sync(0xffffffffu, ap, o);
+        }
+        const int x = 8 * nt + 2 * lr + e;
+        if (yi && x > 0 && x < kL32 - 1) {
+          const double cz = m[2] * t->bd[x] * t->bd[y];
+          if (lq == 0) d[0][nt][e] -= cz * a0;  // z = 0
+          if (lq == 7) d[3][nt][e] -= cz * ap;  // z = 31
+        }
+      }
   }
-  if (schur && xi && yi) {
-    const double cz = m[2] * t->bd[x] * t->bd[y];
-    v0 -= cz * s0z;
-    vp -= cz * spz;
-  }
-  col[0] = v0;
-  col[size_t(kL32 - 1) * kSlab32] = vp;
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+      *reinterpret_cast<double2*>(pl + size_t(8 * mt + lq) * kSlab32 + 8 * nt + 2 * lr) =
+          make_double2(d[mt][nt][0], d[mt][nt][1]);
 }
 
 // y faces (x, e, z) for x, z interior: thread per y-line.
