@@ -41,6 +41,7 @@ METRIC = "Schwarz relaxation apply GDOF/s (FP64) + % HBM roofline; patch factori
 # measured: tools/probe/fp64_peak.cu on this pool, DMMA 37.09 / DFMA 36.54 TFLOP/s at 1965 MHz
 # (profiles/r2a_fp64_peak.txt, with the clocks sampled during the run); MEASURED_PEAKS.json has no FP64 entry
 FP64_PEAK_TFLOPS = 37.0
+READ_PEAK_GBPS = 7399.3  # pure-read HBM stream on this pool's B200 (tools/probe/read_bw.cu, profiles/r3_read_bw.txt)
 WORKLOADS = {
     1: "C1: 2D Poisson 8x8 quads, Q7 GLL, 49 vertex-star patches",
     2: "C2: 3D Poisson 4^3 hexes, Q7 GLL, 27 vertex-star patches",
@@ -554,6 +555,10 @@ def run_ours(args):
                   "l2": l2_note},
         "roofline": {"kernel": solve_kernels, "bound": "hbm", "achieved": achieved, "peak": hbm_peak,
                      "unit": "GB/s", "frac": achieved / hbm_peak, "frac_nominal_8TBps": achieved / 8000.0,
+                     "read_peak": READ_PEAK_GBPS, "frac_of_read_peak": achieved / READ_PEAK_GBPS,
+                     "read_peak_source": "tools/probe/read_bw.cu: 16 GiB read by 32 KB cp.async.bulk chunks, "
+                                         "6-stage ring, one CTA per SM (profiles/r3_read_bw.txt); `peak` is "
+                                         "MEASURED_PEAKS' copy (read + write)",
                      "traffic": traffic,
                      "peak_source": peak_src, "kernel_ms": kern_ms, "algorithmic_bytes": kern_bytes,
                      "share_of_step": kern_ms / ms_per_step if ms_per_step > 0 else None,
