@@ -66,7 +66,8 @@ typedef struct {
   int64_t nnz_L_reference;   /* nnz(L_j) under the reference patch_ordering       */
   int64_t flops_reference;   /* CholFactor::flops under the reference ordering    */
   int32_t separator_order;   /* 0 plane, 1 reference                              */
-  int32_t pad2_;
+  int32_t top_direct;        /* 1: the Schur split forms S~_RR = S_RR - S_RF S_FF^{-1} S_FR from S's sparse
+                                couplings and factors it densely (no full separator factor); else 0   */
   int64_t stream_bytes;      /* packed factor bytes streamed per sweep, all patches */
   int64_t dmma_flops;        /* FP64 tensor-pipe flops the batched factorisation issues per patch
                                 (dense 64x64 tile GEMMs minus the skipped zero 16-wide panels) */

@@ -47,7 +47,7 @@ class Layout(C.Structure):
                 ("tile", C.c_int32), ("tile_cols", C.c_int32), ("tiles", C.c_int32), ("pad_", C.c_int32),
                 ("nnz_L", C.c_int64), ("flops_ref", C.c_int64), ("factor_bytes", C.c_int64),
                 ("tile_gemms", C.c_int64), ("nnz_L_reference", C.c_int64), ("flops_reference", C.c_int64),
-                ("separator_order", C.c_int32), ("pad2_", C.c_int32), ("stream_bytes", C.c_int64),
+                ("separator_order", C.c_int32), ("top_direct", C.c_int32), ("stream_bytes", C.c_int64),
                 ("dmma_flops", C.c_int64), ("schur_split", C.c_int32), ("n_top", C.c_int32),
                 ("solve_values", C.c_int64)]
 

@@ -31,7 +31,10 @@ void setup_schur_split(Context& c) {
     a->reset();
   c.sx_ccol.reset();
   c.sx_hdr.reset();
-  for (auto* a : {&c.sx_vals, &c.sx_tR, &c.sx_F, &c.diagL, &c.sx_UT, &c.sx_part}) a->reset();
+  for (auto* a : {&c.sx_vals, &c.sx_tR, &c.sx_F, &c.diagL, &c.sx_UT, &c.sx_part, &c.sx_inv, &c.sx_fv}) a->reset();
+  for (auto* a : {&c.sx_kr, &c.sx_rk_ent, &c.sx_rr_entries, &c.sx_form_I, &c.sx_form_J0, &c.sx_pair_ptr, &c.sx_pair_a,
+                  &c.sx_pair_b, &c.sx_tile_mask})
+    a->reset();
   c.sx_chunk.reset();
   if (c.dg) return;
   analyze_schur_split(c);
@@ -67,9 +70,11 @@ void setup_schur_split(Context& c) {
     }
     S.chunk_start.push_back(S.R.ntiles);
   }
-  const size_t need = sizeof(double) * (np * rec + np * size_t(L.nT - K0) * tt + np * size_t(S.vstride) +
-                                        np * size_t(S.nR + S.nF) +
-                                        (S.inv ? np * rtiles + np * S.nchunk * size_t(S.R.mpad) : 0));
+  // (the full factor tiles are allocated after this analysis, unless the top block is formed directly)
+  const size_t need = sizeof(double) * (np * rec + np * size_t(S.vstride) + np * size_t(S.nR + S.nF) +
+                                        (S.inv ? np * rtiles + np * S.nchunk * size_t(S.R.mpad) : 0) +
+                                        (S.direct ? np * size_t(S.ncomp) * S.nl * S.nl + np * S.rk_ent.size()
+                                                  : np * size_t(L.nT - K0) * tt + np * size_t(L.ntiles) * tt));
   size_t fb = 0, tb = 0;
   FDM_CUDA(cudaMemGetInfo(&fb, &tb));
   if (need + (size_t(1) << 30) > fb) {  // keep 1 GiB of headroom for work vectors
@@ -122,7 +127,21 @@ void setup_schur_split(Context& c) {
     c.sx_part.alloc(np * S.nchunk * size_t(S.R.mpad));
     c.sx_chunk.upload(S.chunk_start, c.stream);
   }
-  c.diagL.alloc(np * size_t(L.nT - K0) * kTile * kTile);
+  if (S.direct) {
+    c.sx_kr.upload(S.kr, c.stream);
+    c.sx_rk_ent.upload(S.rk_ent, c.stream);
+    c.sx_rr_entries.upload(S.rr_entries, c.stream);
+    c.sx_form_I.upload(S.form_I, c.stream);
+    c.sx_form_J0.upload(S.form_J0, c.stream);
+    c.sx_pair_ptr.upload(S.pair_ptr, c.stream);
+    c.sx_pair_a.upload(S.pair_a, c.stream);
+    c.sx_pair_b.upload(S.pair_b, c.stream);
+    c.sx_tile_mask.upload(S.tile_mask, c.stream);
+    c.sx_inv.alloc(np * size_t(S.ncomp) * S.nl * S.nl);
+    c.sx_fv.alloc(np * S.rk_ent.size());
+  } else {
+    c.diagL.alloc(np * size_t(L.nT - K0) * kTile * kTile);
+  }
   c.sx_vals.alloc(np * size_t(S.vstride));
   c.sx_tR.alloc(np * size_t(S.nR));
   c.sx_F.alloc(np * size_t(S.nF));
@@ -991,13 +1010,15 @@ fdmgpu_status fdmgpu_set_patches(fdmgpu_handle h, int32_t npatch, const int32_t*
     c.fac_flag.alloc(size_t(npatch) * L.nT);
     FDM_CUDA(cudaMemsetAsync(c.fac_flag.p, 0, c.fac_flag.bytes(), c.stream));
     c.fac_epoch = 0;
-    c.tiles.alloc(size_t(npatch) * L.ntiles * fdmgpu::kTile * fdmgpu::kTile);
     // Separate solve-record buffer when it takes under a quarter of the free
     // memory (C3: 3.7 GB; packing then overlaps the factorisation, 24.3 -> 23.8 ms);
     // else (C5: 63.5 GB) the records are packed in place after the factorisation.
     // FDMGPU_PACK=inplace forces the latter.
     c.packed.reset();
+    c.tiles.reset();
     fdmgpu::setup_schur_split(c);
+    // the full separator factor tiles; not needed when the split forms its top block directly
+    if (!(c.sx.on && c.sx.direct)) c.tiles.alloc(size_t(npatch) * L.ntiles * fdmgpu::kTile * fdmgpu::kTile);
     if (!c.sx.on) {
       const char* pk = std::getenv("FDMGPU_PACK");
       const size_t rec_bytes = size_t(npatch) * size_t(L.tile_poff8.back()) * sizeof(double);
@@ -1117,6 +1138,12 @@ fdmgpu_status fdmgpu_factor(fdmgpu_handle h) {
     }
     const unsigned long long none = ~0ULL;
     FDM_CUDA(cudaMemcpyAsync(c.d_err.p, &none, sizeof(none), cudaMemcpyHostToDevice, c.stream));
+    const bool direct = c.sx.on && c.sx.direct;  // top block formed directly: no full separator factor
+    if (direct) {
+      fdmgpu::launch_schur_setup(c);
+      ++c.fac_epoch;
+      fdmgpu::launch_schur_direct(c);
+    } else {
     if (c.dg)
       fdmgpu::launch_dg_patch_assemble(c);
     else
@@ -1140,6 +1167,7 @@ fdmgpu_status fdmgpu_factor(fdmgpu_handle h) {
       fdmgpu::launch_patch_pack_join(c);
     else
       fdmgpu::launch_patch_pack(c);  // dense tiles -> packed 8x8 sub-block records, in place
+    }
     unsigned long long e = 0;
     FDM_CUDA(cudaMemcpyAsync(&e, c.d_err.p, sizeof(e), cudaMemcpyDeviceToHost, c.stream));
     FDM_CUDA(cudaStreamSynchronize(c.stream));
@@ -1181,6 +1209,8 @@ fdmgpu_status fdmgpu_get_layout(fdmgpu_handle h, fdmgpu_layout* out) {
     L.nnz_L = c.L.nnz_L;
     L.flops_ref = c.L.flops_ref;
     L.factor_bytes = int64_t(c.tiles.bytes());
+    L.top_direct = (c.sx.on && c.sx.direct) ? 1 : 0;
+    if (L.top_direct) L.factor_bytes = int64_t(c.packed.bytes() + c.sx_UT.bytes() + c.sx_inv.bytes() + c.sx_fv.bytes());
     L.tile_gemms = c.L.tile_gemms;
     L.nnz_L_reference = c.L.nnz_L_reference;
     L.flops_reference = c.L.flops_reference;
@@ -1296,6 +1326,9 @@ fdmgpu_status fdmgpu_patch_factor(fdmgpu_handle h, int32_t j, double* out) {
     if (j < 0 || j >= c.npatch || !out) throw Error(FDMGPU_INVALID_ARGUMENT, "patch_factor: bad patch index");
     if (!c.packed.p)
       throw Error(FDMGPU_UNSUPPORTED, "patch_factor: the dense factor tiles were packed in place (large factor)");
+    if (!c.tiles.p)
+      throw Error(FDMGPU_UNSUPPORTED, "patch_factor: the top block is formed directly, the full separator factor does "
+                                      "not exist (FDMGPU_DIRECT=0 keeps it)");
     const auto& L = c.L;
     const int T = fdmgpu::kTile, m = L.m;
     const size_t tt = size_t(T) * T;

@@ -18,6 +18,7 @@ constexpr int kTile = 64;  // dense tile edge of the interface factor
 constexpr int kHdrBytes = 144;  // solve-record header: 2 x 64 sub-block indices + full / compact counts
 constexpr int kCompact = 10;    // doubles per compact 8x8 sub-block (8 row values + 8 column bytes + pad)
 constexpr int kHdrHost = kHdrBytes + 128;  // host tile_hdr stride: record header + compact index table
+constexpr int kFormG = 6;      // column tiles per CTA of the direct top-block assembly (k_schur_form)
 constexpr int kSpmvRows = 16;   // rows per block of the Schur split's coupling products
 
 struct Error : std::runtime_error {
@@ -118,6 +119,18 @@ struct SchurSplit {
   bool inv = true;                        // stream S~_RR^{-1} (symmetric, one pass) instead of L_RR (two passes)
   int nchunk = 1;                         // inverse: CTAs per patch of the symmetric product
   std::vector<int32_t> chunk_start;       // nchunk + 1 tile offsets
+  // Direct top block (default with inv; FDMGPU_DIRECT=0 keeps the full tile factorisation):
+  // S~_RR = S_RR - S_RF S_FF^{-1} S_FR is formed from S's sparse couplings and the explicit
+  // component inverses, then factored as a dense nR x nR matrix -- the dense |R| x |P1| fill
+  // block of the full factor is never computed.
+  bool direct = false;
+  int nl = 0;                             // c0 + c1: local indices of a component (P0 members, then P1)
+  int nRp = 0;                            // R.mpad
+  std::vector<int32_t> kr;                // ncomp x nRp: (first entry << 8 | count) of row r's S_RF entries in component k
+  std::vector<int32_t> rk_ent;            // entries sorted by (component, row): local index | rf entry << 8
+  std::vector<int32_t> rr_entries;        // structural S_RR entries + padding diagonal: tile << 12 | col << 6 | row (R layout)
+  std::vector<int32_t> form_I, form_J0;   // form CTAs: row tile I, first column tile (kFormG column tiles per CTA)
+  std::vector<int32_t> pair_ptr, pair_a, pair_b, tile_mask;  // dense left-looking update lists of the R layout
 };
 
 // Device-resident PCG scalars (kernels/pcg.cu).
@@ -212,6 +225,8 @@ struct Context {
   DevArray<int64_t> sx_ccol;
   DevArray<uint8_t> sx_hdr;
   DevArray<int32_t> sx_chunk;
+  DevArray<int32_t> sx_kr, sx_rk_ent, sx_rr_entries, sx_form_I, sx_form_J0, sx_pair_ptr, sx_pair_a, sx_pair_b, sx_tile_mask;
+  DevArray<double> sx_inv, sx_fv;  // direct top block: component inverses (npatch x ncomp x nl x nl), S_RF values in rk_ent order
   DevArray<double> sx_vals, sx_tR, sx_F, diagL, sx_UT, sx_part;  // per-patch values; R right-hand sides; F work; L_KK of R tiles
   int sx_K0 = 0;                                 // first full-factor tile column overlapping R
   int solve_cs = 0;                     // CTAs per split patch (FDMGPU_SOLVE_CS; 0 = auto, 1 = no split)
@@ -343,6 +358,7 @@ void launch_patch_pack_col(Context& c, int K);   // separate record buffer, side
 void launch_patch_pack_join(Context& c);
 void launch_schur_setup(Context& c);   // Schur split: S_FF components, S_RF / S_FR values (any time after set_cell_coeffs)
 void launch_schur_retile(Context& c);  // Schur split: L_RR records from the factored tiles
+void launch_schur_direct(Context& c);  // Schur split, direct top block: S~_RR formed and factored without the full factor
 void launch_patch_solve(Context& c, const double* r_modal);          // writes c.corr
 void launch_patch_gather(Context& c, double* z_modal);
 void launch_patch_gather_bnd(Context& c, double* z_modal);  // cell-boundary DOFs only (op_smooth)

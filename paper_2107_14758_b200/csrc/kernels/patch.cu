@@ -40,6 +40,7 @@ struct PatchArgs {
   int out_off;
   double* diagL;       // Schur split: L_KK of the diagonal tiles K >= diagK0 (npatch x diagNT tiles), or null
   int diagK0, diagNT;
+  const int32_t* err_map;  // pivot position of a failing row (component factorisations), or null: K T + row
 };
 
 PatchArgs make_args(Context& c) {
@@ -68,6 +69,7 @@ PatchArgs make_args(Context& c) {
   a.diagL = c.sx.on ? c.diagL.p : nullptr;
   a.diagK0 = c.sx_K0;
   a.diagNT = c.L.nT - c.sx_K0;
+  a.err_map = nullptr;
   return a;
 }
 
@@ -230,7 +232,8 @@ __global__ void k_patch_assemble(PatchArgs a, int nentries, const int32_t* __res
 __global__ void k_patch_pad_check(PatchArgs a, double* __restrict__ tiles, int last_diag) {
   const int j = blockIdx.x;
   double* dt = tiles + (size_t(j) * a.ntiles + last_diag) * TT;
-  for (int r = a.m + threadIdx.x; r < a.mpad; r += blockDim.x) dt[tsw(r % T, r % T)] = 1.0;
+  if (tiles)
+    for (int r = a.m + threadIdx.x; r < a.mpad; r += blockDim.x) dt[tsw(r % T, r % T)] = 1.0;
   const int ncorner = 1 << a.dim;
   double mup[24];
   for (int i = 0; i < ncorner * a.dim; ++i) {
@@ -327,8 +330,8 @@ __device__ void diag_factor_invert(double* Dm, double* Wm, double* out, const Pa
         const int j = j0 + jj;
         double d = P[j * 4 + jj];
         if (lane == 0 && !(d > 0.0)) {
-          const int pos = K * T + j;
-          if (pos < a.m) record_pivot_error(a.err, patch, a.nI + pos);
+          const int pos = a.err_map ? a.err_map[j] : K * T + j;
+          if (pos >= 0 && pos < a.m) record_pivot_error(a.err, patch, a.nI + pos);
         }
         if (!(d > 0.0)) d = 1.0;
         const double s = rsqrt(d);
@@ -1478,7 +1481,7 @@ __global__ void k_schur_couplings(PatchArgs a, SchurArgs s, int npairs, const in
 
 // Per (component, patch): M, D0 and W = chol(S'_11)^{-1} (diag_factor_invert
 // on the 64x64 identity-padded matrix).  256 threads.
-__global__ void __launch_bounds__(256) k_schur_comps(PatchArgs a, SchurArgs s) {
+__global__ void __launch_bounds__(256) k_schur_comps(PatchArgs a, SchurArgs s, int report) {
   extern __shared__ __align__(16) double sm[];
   constexpr int LD = T + 1;
   double* Dm = sm;                   // 64 x 65
@@ -1511,6 +1514,7 @@ __global__ void __launch_bounds__(256) k_schur_comps(PatchArgs a, SchurArgs s) {
   for (int jj = tid; jj < s.c0; jj += blockDim.x) {
     const int c = m0[jj];
     d0[jj] = c < 0 ? 1.0 : sg_entry(a, sep, whole, mup, smask, c, c, At, Bt);
+    if (report && !(d0[jj] > 0.0)) record_pivot_error(a.err, j, a.nI + c);
   }
   for (int i = tid; i < s.c1; i += blockDim.x) {
     const int r = m1[i];
@@ -1534,10 +1538,11 @@ __global__ void __launch_bounds__(256) k_schur_comps(PatchArgs a, SchurArgs s) {
   }
   __syncthreads();  // M is dead: its space takes the inverse
   PatchArgs an = a;
-  an.err = nullptr;  // the full factorisation reports non-SPD pivots
+  if (!report) an.err = nullptr;  // the full factorisation reports non-SPD pivots
+  an.err_map = m1;
   an.diagL = nullptr;
   double* Wo = MW;
-  diag_factor_invert(Dm, Wm, Wo, an, 0, -1);
+  diag_factor_invert(Dm, Wm, Wo, an, 0, j);
   __syncthreads();
   out += s.c1 * ldm;
   for (int i = tid >> 5; i < s.c1; i += blockDim.x >> 5)  // W lower triangle, row i at i(i+1)/2
@@ -1727,6 +1732,193 @@ __global__ void __launch_bounds__(kUpdThreads, 3) k_schur_ainv(int nT, const int
       for (int e = 0; e < 2; ++e) buf[tsw(acc.row(i), acc.col(jj, e))] = acc.v[i][jj][e];
   __syncthreads();
   write_record(buf, packed + size_t(j) * pstride + poff8[t], hdr + size_t(t) * kHdrHost, blk + bptr[t], ccol + bptr[t]);
+}
+
+
+// ---- Direct top block: S~_RR = S_RR - S_RF S_FF^{-1} S_FR without the full factor ----
+// The full separator factor spends most of its flops on the dense |R| x |P1|
+// fill block and its update of the R x R block (C5: 51 of 69 GFLOP per patch).
+// S_FF^{-1} is block diagonal over the components and every R row holds only a
+// few S_RF entries per component (facet rows: one P0 and one P1 mode), so
+//   S~(r, c) = S(r, c) - sum_k sum_{a in row r, comp k} sum_{b in row c, comp k} S(r,a) Inv_k(a,b) S(c,b)
+// costs ~4 multiply-adds per (r, c, k).  k_schur_inv forms the explicit
+// component inverses, k_schur_form the correction tile by tile, k_schur_rr adds
+// S_RR's own structural entries; the dense Cholesky of the R layout follows
+// (k_patch_column on the dense pair lists).
+
+// Inv_k = S_{Fk,Fk}^{-1} (nl x nl, P0 members then P1) from M, W, D0:
+//   X = W^T W, Z = X M D0^{-1}:  [D0^{-1} + D0^{-1} M^T Z, -Z^T; -Z, X].
+__global__ void __launch_bounds__(256) k_schur_inv(SchurArgs s, int nl, double* __restrict__ inv) {
+  extern __shared__ __align__(16) double sm[];
+  const int k = blockIdx.x, j = blockIdx.y, tid = threadIdx.x;
+  const int c0 = s.c0, c1 = s.c1, ldm = c0 | 1, ldx = c1 | 1, ldz = c0 | 1;
+  double* M = sm;
+  double* W = M + c1 * ldm;
+  double* d0 = W + c1 * (c1 + 1) / 2;
+  double* X = d0 + c0;
+  double* Z = X + c1 * ldx;
+  const double* src = s.vals + size_t(j) * s.vstride + size_t(k) * s.comp_stride;
+  const int nin = c1 * ldm + c1 * (c1 + 1) / 2 + c0;
+  for (int i = tid; i < nin; i += blockDim.x) sm[i] = src[i];
+  __syncthreads();
+  for (int idx = tid; idx < c1 * c1; idx += blockDim.x) {
+    const int a = idx / c1, b = idx % c1;
+    if (b > a) continue;
+    double acc = 0.0;
+    for (int q = a; q < c1; ++q) acc = fma(W[q * (q + 1) / 2 + a], W[q * (q + 1) / 2 + b], acc);
+    X[a * ldx + b] = acc;
+    X[b * ldx + a] = acc;
+  }
+  __syncthreads();
+  for (int idx = tid; idx < c1 * c0; idx += blockDim.x) {
+    const int a = idx / c0, jj = idx % c0;
+    double acc = 0.0;
+    for (int i = 0; i < c1; ++i) acc = fma(X[a * ldx + i], M[i * ldm + jj], acc);
+    Z[a * ldz + jj] = acc / d0[jj];
+  }
+  __syncthreads();
+  double* out = inv + (size_t(j) * s.ncomp + k) * nl * nl;
+  for (int idx = tid; idx < c1 * c1; idx += blockDim.x) {
+    const int a = idx / c1, b = idx % c1;
+    out[size_t(c0 + a) * nl + c0 + b] = X[a * ldx + b];
+  }
+  for (int idx = tid; idx < c1 * c0; idx += blockDim.x) {
+    const int a = idx / c0, jj = idx % c0;
+    const double v = -Z[a * ldz + jj];
+    out[size_t(c0 + a) * nl + jj] = v;
+    out[size_t(jj) * nl + c0 + a] = v;
+  }
+  for (int idx = tid; idx < c0 * c0; idx += blockDim.x) {
+    const int jj = idx / c0, j2 = idx % c0;
+    if (j2 > jj) continue;
+    double acc = 0.0;
+    for (int i = 0; i < c1; ++i) acc = fma(M[i * ldm + jj], Z[i * ldz + j2], acc);
+    const double v = (jj == j2 ? 1.0 : 0.0) / d0[jj] + acc / d0[jj];
+    out[size_t(jj) * nl + j2] = v;
+    out[size_t(j2) * nl + jj] = v;
+  }
+}
+
+// S_RF values in (component, row) entry order: fv[patch][e] = S_RF value of rk_ent[e].
+__global__ void k_schur_fv(SchurArgs s, int nent, const int32_t* __restrict__ rk_ent, double* __restrict__ fv) {
+  const int j = blockIdx.y;
+  const double* v = s.vals + size_t(j) * s.vstride + s.rf_off;
+  double* o = fv + size_t(j) * nent;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nent; e += gridDim.x * blockDim.x) o[e] = v[rk_ent[e] >> 8];
+}
+
+// -(S_RF S_FF^{-1} S_FR) on row tile I and up to G column tiles J0.. of one patch
+// (512 threads).  Per component k, phase A: Y[rr][lb] = sum_a S(r, a) Inv_k(a, lb)
+// for the tile's 64 rows (warp per row, lanes along lb: coalesced rows of Inv_k);
+// phase B: thread (column cl, 8 rows) adds Y[rr][lb] S(c, b) over column c's
+// entries of component k.  Y is double buffered: one barrier per component.
+constexpr int kFormThreads = 512;
+template <int G>
+__global__ void __launch_bounds__(kFormThreads, 1)
+    k_schur_form(int nR, int nRp, int ncomp, int nl, const int32_t* __restrict__ form_I,
+                 const int32_t* __restrict__ form_J0, const int32_t* __restrict__ kr,
+                 const int32_t* __restrict__ rk_ent, int nent, const double* __restrict__ fv,
+                 const double* __restrict__ inv, const int32_t* __restrict__ col_start, double* __restrict__ RT,
+                 int64_t rstride) {
+  extern __shared__ __align__(16) double sm[];
+  const int pitch = nl | 1;
+  double* Yb[2] = {sm, sm + T * pitch};
+  const int f = blockIdx.x, j = blockIdx.y, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int I = form_I[f], J0 = form_J0[f];
+  const int nG = min(G, I - J0 + 1);
+  const double* fvj = fv + size_t(j) * nent;
+  const double* invj = inv + size_t(j) * ncomp * nl * nl;
+  const int cl = tid & 63, rg = tid >> 6;
+  double acc[G][8];
+#pragma unroll
+  for (int g = 0; g < G; ++g)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[g][i] = 0.0;
+  auto phaseA = [&](int k, double* Y) {
+    const double* ik = invj + size_t(k) * nl * nl;
+#pragma unroll 1
+    for (int i = 0; i < T / 16; ++i) {
+      const int rr = warp + 16 * i, r = I * T + rr;
+      double y[4] = {0.0, 0.0, 0.0, 0.0};
+      const int pk = kr[size_t(k) * nRp + r];
+      const int e0 = pk >> 8, cnt = pk & 255;
+      for (int e = e0; e < e0 + cnt; ++e) {
+        const int la = rk_ent[e] & 255;
+        const double va = fvj[e];
+        const double* row = ik + size_t(la) * nl;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int lb = lane + 32 * q;
+          if (lb < nl) y[q] = fma(va, row[lb], y[q]);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int lb = lane + 32 * q;
+        if (lb < nl) Y[rr * pitch + lb] = y[q];
+      }
+    }
+  };
+  auto phaseB = [&](int k, const double* Y) {
+    const double* yr = Y + rg * 8 * pitch;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      if (g < nG) {
+        const int pk = kr[size_t(k) * nRp + (J0 + g) * T + cl];
+        const int e0 = pk >> 8, cnt = pk & 255;
+        for (int e = e0; e < e0 + cnt; ++e) {
+          const int lb = rk_ent[e] & 255;
+          const double vb = fvj[e];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) acc[g][i] = fma(yr[i * pitch + lb], vb, acc[g][i]);
+        }
+      }
+    }
+  };
+  phaseA(0, Yb[0]);
+  __syncthreads();
+#pragma unroll 1
+  for (int k = 0; k < ncomp; ++k) {
+    if (k + 1 < ncomp) phaseA(k + 1, Yb[(k + 1) & 1]);
+    phaseB(k, Yb[k & 1]);
+    __syncthreads();
+  }
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    if (g < nG) {
+      const int J = J0 + g;
+      double* o = RT + size_t(j) * rstride + size_t(col_start[J] + I - J) * TT;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) o[tsw(rg * 8 + i, cl)] = -acc[g][i];
+    }
+  }
+}
+
+// += S_RR's own structural entries (and the identity on the padding rows).
+__global__ void k_schur_rr(PatchArgs a, int nF, int nentries, const int32_t* __restrict__ entries,
+                           const int32_t* __restrict__ rrow, const int32_t* __restrict__ rcol,
+                           double* __restrict__ RT, int64_t rstride) {
+  extern __shared__ double sm[];
+  double* At = sm;
+  double* Bt = At + a.n1 * a.n1;
+  double* mup = Bt + a.n1 * a.n1;
+  const int j = blockIdx.y;
+  const int smask = load_patch_coeffs(a, j, At, Bt, mup);
+  __syncthreads();
+  const int32_t* sep = a.psep + size_t(j) * a.m;
+  const bool whole = smask == (1 << (1 << a.dim)) - 1;
+  double* base = RT + size_t(j) * rstride;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nentries; e += gridDim.x * blockDim.x) {
+    const int code = entries[e];
+    const int t = code >> 12, cc = (code >> 6) & 63, rr = code & 63;
+    const int r = nF + rrow[t] * T + rr, c = nF + rcol[t] * T + cc;
+    double v;
+    if (r >= a.m || c >= a.m)
+      v = r == c ? 1.0 : 0.0;
+    else
+      v = sg_entry(a, sep, whole, mup, smask, r, c, At, Bt);
+    base[size_t(t) * TT + tsw(rr, cc)] += v;
+  }
 }
 
 // Inverse top block, solve: x_R = A t_R with A symmetric, each lower tile
@@ -2464,8 +2656,65 @@ void launch_schur_setup(Context& c) {
   }
   const size_t smem = sizeof(double) * (size_t(T) * (T + 1) * 2 + 16 * T * 4 + T + 2 * T + 24);
   FDM_CUDA(cudaFuncSetAttribute(k_schur_comps, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  k_schur_comps<<<dim3(c.sx.ncomp, c.npatch), 256, smem, c.stream>>>(a, s);
+  k_schur_comps<<<dim3(c.sx.ncomp, c.npatch), 256, smem, c.stream>>>(a, s, c.sx.direct ? 1 : 0);
   FDM_LAUNCH_CHECK(c);
+}
+
+static void launch_top_inverse(Context& c);
+
+// Schur split with the top block formed directly (SchurSplit::direct): interior
+// pivot check, component inverses, S~_RR into the dense R tiles, its dense tile
+// Cholesky (k_patch_column on the R layout's pair lists), then the inverse.
+void launch_schur_direct(Context& c) {
+  PatchArgs a = make_args(c);
+  const SchurArgs s = make_schur_args(c);
+  const auto& S = c.sx;
+  const auto& R = S.R;
+  KernelTimer timer(c, 1);
+  k_patch_pad_check<<<c.npatch, 256, 0, c.stream>>>(a, nullptr, 0);
+  FDM_LAUNCH_CHECK(c);
+  const int c0 = S.c0, c1 = S.c1;
+  const size_t smem_i = sizeof(double) * (size_t(c1) * (c0 | 1) + size_t(c1) * (c1 + 1) / 2 + c0 + size_t(c1) * (c1 | 1) +
+                                          size_t(c1) * (c0 | 1) + 2);
+  FDM_CUDA(cudaFuncSetAttribute(k_schur_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_i)));
+  k_schur_inv<<<dim3(S.ncomp, c.npatch), 256, smem_i, c.stream>>>(s, S.nl, c.sx_inv.p);
+  FDM_LAUNCH_CHECK(c);
+  const int nent = int(S.rk_ent.size());
+  k_schur_fv<<<dim3(unsigned(std::min(64, (nent + 255) / 256)), c.npatch), 256, 0, c.stream>>>(s, nent, c.sx_rk_ent.p,
+                                                                                                c.sx_fv.p);
+  FDM_LAUNCH_CHECK(c);
+  const int64_t rstride = int64_t(R.ntiles) * TT;
+  const size_t smem_f = sizeof(double) * 2 * T * size_t(S.nl | 1);
+  FDM_CUDA(cudaFuncSetAttribute(k_schur_form<kFormG>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_f)));
+  k_schur_form<kFormG><<<dim3(unsigned(S.form_I.size()), c.npatch), kFormThreads, smem_f, c.stream>>>(
+      S.nR, S.nRp, S.ncomp, S.nl, c.sx_form_I.p, c.sx_form_J0.p, c.sx_kr.p, c.sx_rk_ent.p, nent, c.sx_fv.p, c.sx_inv.p,
+      c.sx_col_start.p, c.packed.p, rstride);
+  FDM_LAUNCH_CHECK(c);
+  const size_t smem_c = sizeof(double) * (2 * size_t(c.n1) * c.n1 + 24);
+  const int nrr = int(S.rr_entries.size());
+  k_schur_rr<<<dim3(unsigned(std::min(64, (nrr + 255) / 256)), c.npatch), 256, smem_c, c.stream>>>(
+      a, S.nF, nrr, c.sx_rr_entries.p, c.sx_tile_row.p, c.sx_tile_col.p, c.packed.p, rstride);
+  FDM_LAUNCH_CHECK(c);
+  // dense left-looking tile Cholesky of S~_RR in place (diagonal tiles end as L_KK^{-1})
+  PatchArgs ar = a;
+  ar.m = S.nR;
+  ar.mpad = R.mpad;
+  ar.nT = R.nT;
+  ar.ntiles = R.ntiles;
+  ar.nI = c.L.nI + S.nF;  // pivot positions reported in the patch numbering
+  ar.diagL = nullptr;
+  const size_t diag_area = size_t(T + 1) * T + 16 * T * 4 + T;
+  const size_t smem_k = sizeof(double) * (16 + std::max(size_t(2 * TT), diag_area));
+  FDM_CUDA(cudaFuncSetAttribute(k_patch_column, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_k)));
+  for (int K = 0; K < R.nT; ++K) {
+    const int cnt = R.col_start[K + 1] - R.col_start[K];
+    launch_pdl(c.pdl && !c.timing && K > 0, k_patch_column, dim3(unsigned(c.npatch * cnt)), dim3(kUpdThreads), smem_k,
+               c.stream, ar, K, (const int32_t*)c.sx_col_start.p, (const int32_t*)c.sx_pair_ptr.p,
+               (const int32_t*)c.sx_pair_a.p, (const int32_t*)c.sx_pair_b.p, (const int32_t*)c.sx_tile_mask.p,
+               c.packed.p, c.fac_flag.p, c.fac_epoch);
+    FDM_LAUNCH_CHECK(c);
+  }
+  launch_top_inverse(c);
 }
 
 // Schur split: the R block of the factored tiles -> dense L_RR stream records.
@@ -2484,8 +2733,14 @@ void launch_schur_retile(Context& c) {
       inv ? 1 : 0);
   FDM_LAUNCH_CHECK(c);
   if (!inv) return;
-  // S~_RR^{-1} = W^T W, W = L_RR^{-1}: U = W^T from the dense L_RR tiles, then A
-  // into the stream records (over the dense tiles, which U no longer needs)
+  launch_top_inverse(c);
+}
+
+// S~_RR^{-1} = W^T W, W = L_RR^{-1}: U = W^T from the dense L_RR tiles, then A
+// into the stream records (over the dense tiles, which U no longer needs)
+static void launch_top_inverse(Context& c) {
+  const auto& R = c.sx.R;
+  const int64_t rstride = int64_t(R.ntiles) * TT;
   const size_t gsm = sizeof(double) * (16 + 2 * TT);
   FDM_CUDA(cudaFuncSetAttribute(k_schur_uinv, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gsm)));
   FDM_CUDA(cudaFuncSetAttribute(k_schur_ainv, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gsm)));

@@ -229,6 +229,80 @@ void analyze_schur_split(Context& c) {
     return;
   }
   S.on = true;
+  // Direct top block: per-component views of S_RF, the structural entries of
+  // S_RR in the R tile layout and the dense left-looking update lists.
+  const char* dir = std::getenv("FDMGPU_DIRECT");
+  S.direct = S.inv && !(dir && dir[0] == '0') && c0 + c1 <= 128 && S.rf_col.size() < (size_t(1) << 23);
+  if (!S.direct) return;
+  S.nl = c0 + c1;
+  S.nRp = S.R.mpad;
+  std::vector<int> fcomp(nF, 0), floc(nF, 0);
+  for (int k = 0; k < ncomp; ++k) {
+    for (size_t i = 0; i < m0[k].size(); ++i) {
+      fcomp[m0[k][i]] = k;
+      floc[m0[k][i]] = int(i);
+    }
+    for (size_t i = 0; i < m1[k].size(); ++i) {
+      fcomp[m1[k][i]] = k;
+      floc[m1[k][i]] = c0 + int(i);
+    }
+  }
+  std::vector<std::vector<int32_t>> bucket(size_t(ncomp) * S.nR);  // (component, row) -> entries
+  for (int r = 0; r < S.nR; ++r)
+    for (int e = S.rf_ptr[r]; e < S.rf_ptr[r + 1]; ++e) {
+      const int f = S.rf_col[e];
+      bucket[size_t(fcomp[f]) * S.nR + r].push_back(int32_t(floc[f] | (e << 8)));
+    }
+  S.kr.assign(size_t(ncomp) * S.nRp, 0);
+  S.rk_ent.clear();
+  for (int k = 0; k < ncomp; ++k)
+    for (int r = 0; r < S.nR; ++r) {
+      const auto& b = bucket[size_t(k) * S.nR + r];
+      if (b.size() > 255 || S.rk_ent.size() >= (size_t(1) << 23)) {
+        S.direct = false;
+        return;
+      }
+      S.kr[size_t(k) * S.nRp + r] = int32_t((S.rk_ent.size() << 8) | b.size());
+      S.rk_ent.insert(S.rk_ent.end(), b.begin(), b.end());
+    }
+  if (S.rk_ent.empty()) S.rk_ent.push_back(0);
+  // S_RR: structural entries of S_G inside R x R (both triangles inside diagonal tiles),
+  // the diagonal, and the identity on the padding rows
+  std::vector<int32_t> tix(size_t(S.R.nT) * S.R.nT, -1);
+  for (int t = 0; t < S.R.ntiles; ++t) tix[size_t(S.R.tile_row[t]) * S.R.nT + S.R.tile_col[t]] = t;
+  auto add_rr = [&](int r, int col) {
+    const int I = r / kTile, J = col / kTile;
+    if (I < J) return;
+    S.rr_entries.push_back(int32_t((tix[size_t(I) * S.R.nT + J] << 12) | ((col % kTile) << 6) | (r % kTile)));
+  };
+  for (auto [r, col] : pr)
+    if (r >= nF && col >= nF) {
+      add_rr(r - nF, col - nF);
+      add_rr(col - nF, r - nF);
+    }
+  for (int r = 0; r < S.nRp; ++r) add_rr(r, r);
+  std::sort(S.rr_entries.begin(), S.rr_entries.end());
+  S.rr_entries.erase(std::unique(S.rr_entries.begin(), S.rr_entries.end()), S.rr_entries.end());
+  for (int I = 0; I < S.R.nT; ++I)
+    for (int J0 = 0; J0 <= I; J0 += kFormG) {
+      S.form_I.push_back(I);
+      S.form_J0.push_back(J0);
+    }
+  // dense left-looking updates: tile (I, K) -= sum_{J < K} L(I, J) L(K, J)^T
+  S.pair_ptr.assign(1, 0);
+  for (int t = 0; t < S.R.ntiles; ++t) {
+    const int I = S.R.tile_row[t], K = S.R.tile_col[t];
+    for (int J = 0; J < K; ++J) {
+      S.pair_a.push_back(tix[size_t(I) * S.R.nT + J]);
+      S.pair_b.push_back(tix[size_t(K) * S.R.nT + J]);
+    }
+    S.pair_ptr.push_back(int32_t(S.pair_a.size()));
+  }
+  if (S.pair_a.empty()) {
+    S.pair_a.push_back(0);
+    S.pair_b.push_back(0);
+  }
+  S.tile_mask.assign(S.R.ntiles, 0xffff);
 }
 
 }  // namespace fdmgpu

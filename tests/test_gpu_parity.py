@@ -496,6 +496,7 @@ def test_fused_column_factorisation(pkg, torch, monkeypatch, cfg):
     """k_patch_column (update + diagonal factor + trsm of a tile column in one
     launch, flag-synchronised) gives the same factor, bit for bit, as the
     separate k_patch_update / k_patch_trsm launches (FDMGPU_FUSED=0)."""
+    monkeypatch.setenv("FDMGPU_DIRECT", "0")  # the full separator factorisation (the direct top block skips it)
     prob = pkg.Problem(*cfg)
     r = prob.rhs()
     fused = pkg.Solver(prob)
@@ -508,11 +509,12 @@ def test_fused_column_factorisation(pkg, torch, monkeypatch, cfg):
 
 
 @pytest.mark.parametrize("cfg", [(2, 0, 0), (4, 3, 5), (5, 2, 7), (1, 4, 5)])
-def test_patch_factor_residual(pkg, torch, cfg):
+def test_patch_factor_residual(pkg, torch, monkeypatch, cfg):
     """K2: the device factor of sampled patches reproduces the
     matrix it factors, ||L L^T - S_G||_max / ||S_G||_max <= 1e-12 (S_G the
     separator Schur complement, fdmgpu_patch_schur), L lower triangular with a
     positive diagonal."""
+    monkeypatch.setenv("FDMGPU_DIRECT", "0")  # keeps the full separator factor tiles
     prob = pkg.Problem(*cfg)
     sol = pkg.Solver(prob)
     sol.factor()

@@ -37,9 +37,11 @@ def torch():
     return T
 
 
-def _solver(pkg, prob, split, top="inverse"):
-    """split: FDMGPU_SCHUR; top: "inverse" (S~_RR^{-1}, default) | "chol" (L_RR, FDMGPU_TOP=chol)."""
-    env = {"FDMGPU_SCHUR": "1" if split else "0", "FDMGPU_TOP": top}
+def _solver(pkg, prob, split, top="inverse", direct=True):
+    """split: FDMGPU_SCHUR; top: "inverse" (S~_RR^{-1}, default) | "chol" (L_RR, FDMGPU_TOP=chol);
+    direct: S~_RR formed from S's sparse couplings and factored densely (default) or taken from
+    the full separator factorisation (FDMGPU_DIRECT=0)."""
+    env = {"FDMGPU_SCHUR": "1" if split else "0", "FDMGPU_TOP": top, "FDMGPU_DIRECT": "1" if direct else "0"}
     old = {k: os.environ.get(k) for k in env}
     os.environ.update(env)
     try:
@@ -149,3 +151,42 @@ def test_inverse_top_at_c3_matches_cholesky_top(pkg, torch):
         del sol
         gc.collect()
     assert rel(out["inverse"], out["chol"]) <= 1e-12
+
+
+@pytest.mark.parametrize("case", CASES + [(3, 0, 0, True)],
+                         ids=lambda c: "C%d_n%d_p%d_%s" % (c[0], c[1], c[2], "skip" if c[3] else "all"))
+def test_direct_top_block_matches_full_factorisation(case, pkg, torch):
+    """The direct top block (S~_RR = S_RR - S_RF S_FF^{-1} S_FR from the component
+    inverses, dense tile Cholesky; no full separator factor) against the top block
+    taken from the full tile factorisation (FDMGPU_DIRECT=0): the same matrix up
+    to rounding, so the relaxations agree to 1e-12; boundary stars included."""
+    import gc
+
+    cfg, n, p, skip = case
+    prob = pkg.Problem(cfg, n, p, skip_boundary_patches=skip) if n else pkg.Problem(cfg)
+    r = torch.from_numpy(prob.rhs()).cuda()
+    out = {}
+    for direct in (True, False):
+        sol = _solver(pkg, prob, True, "inverse", direct)
+        L = sol.layout()
+        assert L["schur_split"] == 2 and L["top_direct"] == (1 if direct else 0)
+        out[direct] = sol.smooth(r).cpu().numpy()
+        if direct:
+            sol.factor()  # refactor: the flag epoch advances
+            assert np.array_equal(sol.smooth(r).cpu().numpy(), out[direct])
+        del sol
+        gc.collect()
+    assert rel(out[True], out[False]) <= 1e-12
+
+
+def test_direct_top_block_reports_not_spd(pkg, torch):
+    """Negative coefficients: the interior pivot check still reports pivot 0."""
+    prob = pkg.Problem(3, 2, 5)
+    sol = _solver(pkg, prob, True)
+    assert sol.layout()["top_direct"] == 1
+    mu = prob.geometry()["mu"].copy()
+    sol.set_cell_coeffs(-mu)
+    with pytest.raises(pkg.NotSPDError, match="not SPD at pivot 0"):
+        sol.factor()
+    sol.set_cell_coeffs(mu)
+    sol.factor()
