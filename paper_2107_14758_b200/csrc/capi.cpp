@@ -73,7 +73,7 @@ void setup_schur_split(Context& c) {
   // (the full factor tiles are allocated after this analysis, unless the top block is formed directly)
   const size_t need = sizeof(double) * (np * rec + np * size_t(S.vstride) + np * size_t(S.nR + S.nF) +
                                         (S.inv ? np * rtiles + np * S.nchunk * size_t(S.R.mpad) : 0) +
-                                        (S.direct ? np * size_t(S.ncomp) * S.nl * S.nl + np * S.rk_ent.size()
+                                        (S.direct ? np * size_t(S.ncomp) * S.nl * S.nl + np * S.rk_ent.size() + np * size_t(S.ncomp) * S.nRp * 2
                                                   : np * size_t(L.nT - K0) * tt + np * size_t(L.ntiles) * tt));
   size_t fb = 0, tb = 0;
   FDM_CUDA(cudaMemGetInfo(&fb, &tb));
@@ -139,6 +139,8 @@ void setup_schur_split(Context& c) {
     c.sx_tile_mask.upload(S.tile_mask, c.stream);
     c.sx_inv.alloc(np * size_t(S.ncomp) * S.nl * S.nl);
     c.sx_fv.alloc(np * S.rk_ent.size());
+    c.sx_e2.upload(S.e2, c.stream);
+    c.sx_fv2.alloc(np * size_t(S.ncomp) * S.nRp * 2);
   } else {
     c.diagL.alloc(np * size_t(L.nT - K0) * kTile * kTile);
   }

@@ -128,6 +128,7 @@ struct SchurSplit {
   int nRp = 0;                            // R.mpad
   std::vector<int32_t> kr;                // ncomp x nRp: (first entry << 8 | count) of row r's S_RF entries in component k
   std::vector<int32_t> rk_ent;            // entries sorted by (component, row): local index | rf entry << 8
+  std::vector<int32_t> e2;                // ncomp x nRp: the first two entries' local indices | min(count, 2) << 16 | (count > 2) << 18
   std::vector<int32_t> rr_entries;        // structural S_RR entries + padding diagonal: tile << 12 | col << 6 | row (R layout)
   std::vector<int32_t> form_I, form_J0;   // form CTAs: row tile I, first column tile (kFormG column tiles per CTA)
   std::vector<int32_t> pair_ptr, pair_a, pair_b, tile_mask;  // dense left-looking update lists of the R layout
@@ -226,6 +227,8 @@ struct Context {
   DevArray<uint8_t> sx_hdr;
   DevArray<int32_t> sx_chunk;
   DevArray<int32_t> sx_kr, sx_rk_ent, sx_rr_entries, sx_form_I, sx_form_J0, sx_pair_ptr, sx_pair_a, sx_pair_b, sx_tile_mask;
+  DevArray<int32_t> sx_e2;         // direct top block: SchurSplit::e2
+  DevArray<double> sx_fv2;         // direct top block: the first two S_RF values of (component, row), npatch x ncomp x nRp x 2
   DevArray<double> sx_inv, sx_fv;  // direct top block: component inverses (npatch x ncomp x nl x nl), S_RF values in rk_ent order
   DevArray<double> sx_vals, sx_tR, sx_F, diagL, sx_UT, sx_part;  // per-patch values; R right-hand sides; F work; L_KK of R tiles
   int sx_K0 = 0;                                 // first full-factor tile column overlapping R

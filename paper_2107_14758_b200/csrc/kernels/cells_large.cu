@@ -171,6 +171,52 @@ __device__ __forceinline__ void dgemm_tc(int M, int N, int K, FA A, FB B, FO O) 
   }
 }
 
+// Row-strip form: a warp task is an 8 x (8 NF) output block -- one A fragment and NF B
+// fragments per k-step, NF independent accumulator chains (the 8 x 16 form above keeps two,
+// and its short dependent DMMA chains were the stall ncu showed in these kernels).  `rot`
+// rotates the task -> warp assignment so back-to-back calls fill the warps evenly.  Each
+// output's sum runs over k in the same order as dgemm_tc (bitwise the same result).
+template <int NF, int U, class FA, class FB, class FO>
+__device__ __forceinline__ void dgemm_tc_s(int M, int N, int K, int rot, FA A, FB B, FO O) {
+  const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int warp = int((threadIdx.x >> 5) + nw - rot % nw) % nw;
+  const int tm = M >> 3, tn = (N + 8 * NF - 1) / (8 * NF);
+  const int ar = lane >> 2, ak = lane & 3;
+  for (int task = warp; task < tm * tn; task += nw) {
+    const int m0 = 8 * (task / tn), n0 = 8 * NF * (task % tn);
+    double d[NF][2];
+#pragma unroll
+    for (int f = 0; f < NF; ++f) d[f][0] = d[f][1] = 0.0;
+#pragma unroll(U)
+    for (int k0 = 0; k0 < K; k0 += 4) {
+      const double a = A(m0 + ar, k0 + ak);
+      double b[NF];
+#pragma unroll
+      for (int f = 0; f < NF; ++f) b[f] = n0 + 8 * f < N ? B(k0 + ak, n0 + 8 * f + ar) : 0.0;
+#pragma unroll
+      for (int f = 0; f < NF; ++f)
+        if (n0 + 8 * f < N) dmma884(d[f][0], d[f][1], a, b[f]);
+    }
+    const int r = m0 + ar;
+#pragma unroll
+    for (int f = 0; f < NF; ++f) {
+      const int c = n0 + 8 * f + 2 * ak;
+      if (n0 + 8 * f < N) {
+        O(r, c, d[f][0]);
+        O(r, c + 1, d[f][1]);
+      }
+    }
+  }
+}
+
+template <int S, int NF, class FA, class FB, class FO>
+__device__ __forceinline__ void qgemm(int M, int N, int K, int rot, FA A, FB B, FO O) {
+  if constexpr (S > 0)
+    dgemm_tc_s<NF, 2 * S>(M, N, K, rot, A, B, O);
+  else
+    dgemm_tc(M, N, K, A, B, O);
+}
+
 // V, D padded: Vp[qx + kQP i] (zero for qx >= q)
 __device__ __forceinline__ void load_vd_padded(double* Vp, double* Dp, const double* __restrict__ Vq,
                                                const double* __restrict__ Dq, int q, int n1, int n1p) {
@@ -188,6 +234,7 @@ __host__ __device__ __forceinline__ int pad4(int n) { return (n + 3) & ~3; }
 // Stage 1: per (cell, z-level kz): t0 = V_x u, t1 = D_x u, then
 // T[c][0] = V_y t0 (-> d/dz path), T[c][1] = D_y t0 (d/dy), T[c][2] = V_y t1 (d/dx);
 // layout T[c][f][kz][qy][qx].
+template <int STRIP>
 __global__ void __launch_bounds__(256) k_quad_stage1(int n1, int q, const double* __restrict__ x,
                                                       const int32_t* __restrict__ cdofs,
                                                       const uint8_t* __restrict__ cons, const double* __restrict__ Vq,
@@ -213,21 +260,21 @@ __global__ void __launch_bounds__(256) k_quad_stage1(int n1, int q, const double
   }
   __syncthreads();
   auto Au = [&](int j, int i) { return u[j * su + i]; };
-  dgemm_tc(n1p, kQP, n1k, Au, [&](int i, int qx) { return Vp[qx + kQP * i]; },
+  qgemm<STRIP, 5>(n1p, kQP, n1k, 0, Au, [&](int i, int qx) { return Vp[qx + kQP * i]; },
            [&](int j, int qx, double v) { t0[j * kQP + qx] = v; });
-  dgemm_tc(n1p, kQP, n1k, Au, [&](int i, int qx) { return Dp[qx + kQP * i]; },
+  qgemm<STRIP, 5>(n1p, kQP, n1k, n1p >> 3, Au, [&](int i, int qx) { return Dp[qx + kQP * i]; },
            [&](int j, int qx, double v) { t1[j * kQP + qx] = v; });
   __syncthreads();
   double* out = T + size_t(c) * 3 * n1 * q2 + size_t(kz) * q2;
   auto AV = [&](int qy, int j) { return Vp[qy + kQP * j]; };
   auto B0 = [&](int j, int qx) { return t0[j * kQP + qx]; };
-  dgemm_tc(kQP, kQP, n1k, AV, B0, [&](int qy, int qx, double v) {
+  qgemm<STRIP, 5>(kQP, kQP, n1k, 0, AV, B0, [&](int qy, int qx, double v) {
     if (qy < q && qx < q) out[qx + q * qy] = v;
   });
-  dgemm_tc(kQP, kQP, n1k, [&](int qy, int j) { return Dp[qy + kQP * j]; }, B0, [&](int qy, int qx, double v) {
+  qgemm<STRIP, 5>(kQP, kQP, n1k, kQP >> 3, [&](int qy, int j) { return Dp[qy + kQP * j]; }, B0, [&](int qy, int qx, double v) {
     if (qy < q && qx < q) out[size_t(n1) * q2 + qx + q * qy] = v;
   });
-  dgemm_tc(kQP, kQP, n1k, AV, [&](int j, int qx) { return t1[j * kQP + qx]; }, [&](int qy, int qx, double v) {
+  qgemm<STRIP, 5>(kQP, kQP, n1k, 2 * (kQP >> 3), AV, [&](int j, int qx) { return t1[j * kQP + qx]; }, [&](int qy, int qx, double v) {
     if (qy < q && qx < q) out[2 * size_t(n1) * q2 + qx + q * qy] = v;
   });
 }
@@ -237,6 +284,7 @@ __global__ void __launch_bounds__(256) k_quad_stage1(int n1, int q, const double
 // f = w kappa G g with G = det J^{-1} J^{-T} of the trilinear map (Jacobian
 // from the 8 cell corners, src/geometry.cpp:33-43); project back in place:
 // T0 <- V_z^T f_x, T1 <- V_z^T f_y, T2 <- D_z^T f_z.
+template <int STRIP>
 __global__ void __launch_bounds__(256) k_quad_stage2(int n1, int q, double* __restrict__ T,
                                                       const double* __restrict__ Vq, const double* __restrict__ Dq,
                                                       const double* __restrict__ wq, const double* __restrict__ xyz,
@@ -299,11 +347,11 @@ __global__ void __launch_bounds__(256) k_quad_stage2(int n1, int q, double* __re
   }
   const int kq2 = kQP * kQP;
   auto AVz = [&](int qz, int k) { return Vp[qz + kQP * k]; };
-  dgemm_tc(kQP, kQP, n1k, AVz, [&](int k, int qx) { return C[(2 * n1k + k) * kQP + qx]; },
+  qgemm<STRIP, 5>(kQP, kQP, n1k, 0, AVz, [&](int k, int qx) { return C[(2 * n1k + k) * kQP + qx]; },
            [&](int qz, int qx, double v) { G[qz * kQP + qx] = v; });
-  dgemm_tc(kQP, kQP, n1k, AVz, [&](int k, int qx) { return C[(n1k + k) * kQP + qx]; },
+  qgemm<STRIP, 5>(kQP, kQP, n1k, kQP >> 3, AVz, [&](int k, int qx) { return C[(n1k + k) * kQP + qx]; },
            [&](int qz, int qx, double v) { G[kq2 + qz * kQP + qx] = v; });
-  dgemm_tc(kQP, kQP, n1k, [&](int qz, int k) { return Dp[qz + kQP * k]; }, [&](int k, int qx) { return C[k * kQP + qx]; },
+  qgemm<STRIP, 5>(kQP, kQP, n1k, 2 * (kQP >> 3), [&](int qz, int k) { return Dp[qz + kQP * k]; }, [&](int k, int qx) { return C[k * kQP + qx]; },
            [&](int qz, int qx, double v) { G[2 * kq2 + qz * kQP + qx] = v; });
   __syncthreads();
   const double kap = kappa[c], wy = W[qy];
@@ -342,13 +390,13 @@ __global__ void __launch_bounds__(256) k_quad_stage2(int n1, int q, double* __re
   __syncthreads();
   const int Kq = (q + 3) & ~3;  // projection over qz (rows >= q are zero)
   auto BVk = [&](int k, int qz) { return Vp[qz + kQP * k]; };
-  dgemm_tc(n1p, kQP, Kq, BVk, [&](int qz, int qx) { return G[qz * kQP + qx]; }, [&](int k, int qx, double v) {
+  qgemm<STRIP, 5>(n1p, kQP, Kq, 0, BVk, [&](int qz, int qx) { return G[qz * kQP + qx]; }, [&](int k, int qx, double v) {
     if (qx < q && k < n1) base[size_t(k) * q2 + qx] = v;
   });
-  dgemm_tc(n1p, kQP, Kq, BVk, [&](int qz, int qx) { return G[kq2 + qz * kQP + qx]; }, [&](int k, int qx, double v) {
+  qgemm<STRIP, 5>(n1p, kQP, Kq, n1p >> 3, BVk, [&](int qz, int qx) { return G[kq2 + qz * kQP + qx]; }, [&](int k, int qx, double v) {
     if (qx < q && k < n1) base[size_t(n1 + k) * q2 + qx] = v;
   });
-  dgemm_tc(n1p, kQP, Kq, [&](int k, int qz) { return Dp[qz + kQP * k]; },
+  qgemm<STRIP, 5>(n1p, kQP, Kq, 2 * (n1p >> 3), [&](int k, int qz) { return Dp[qz + kQP * k]; },
            [&](int qz, int qx) { return G[2 * kq2 + qz * kQP + qx]; }, [&](int k, int qx, double v) {
              if (qx < q && k < n1) base[size_t(2 * n1 + k) * q2 + qx] = v;
            });
@@ -356,6 +404,7 @@ __global__ void __launch_bounds__(256) k_quad_stage2(int n1, int q, double* __re
 
 // Stage 3: per (cell, kz): b0 = V_y^T T0, b12 = D_y^T T1 + V_y^T T2,
 // E = D_x^T b0 + V_x^T b12.
+template <int STRIP>
 __global__ void __launch_bounds__(256) k_quad_stage3(int n1, int q, const double* __restrict__ T,
                                                       const double* __restrict__ Vq, const double* __restrict__ Dq,
                                                       double* __restrict__ E) {
@@ -378,9 +427,9 @@ __global__ void __launch_bounds__(256) k_quad_stage3(int n1, int q, const double
       },
       [&](int i, double v) { P[i] = v; });
   __syncthreads();
-  dgemm_tc(n1p, kQP, Kq, [&](int j, int qy) { return Vp[qy + kQP * j]; }, [&](int qy, int qx) { return P[qy * kQP + qx]; },
+  qgemm<STRIP, 5>(n1p, kQP, Kq, 0, [&](int j, int qy) { return Vp[qy + kQP * j]; }, [&](int qy, int qx) { return P[qy * kQP + qx]; },
            [&](int j, int qx, double v) { b0[j * kQP + qx] = v; });
-  dgemm_tc(n1p, kQP, 2 * Kq, [&](int j, int k) { return k < Kq ? Dp[k + kQP * j] : Vp[k - Kq + kQP * j]; },
+  qgemm<STRIP, 5>(n1p, kQP, 2 * Kq, n1p >> 3, [&](int j, int k) { return k < Kq ? Dp[k + kQP * j] : Vp[k - Kq + kQP * j]; },
            [&](int k, int qx) { return P[pl + k * kQP + qx]; },  // T1 rows then T2 rows (contiguous)
            [&](int j, int qx, double v) { b12[j * kQP + qx] = v; });
   __syncthreads();
@@ -834,16 +883,20 @@ void launch_cells_quadrature(Context& c, const double* x) {
   const size_t s3 = sizeof(double) * (4 * size_t(kQP) * n1p + 3 * size_t(Kq) * kQP);
   if (q > kQP || s1 > 227 * 1024 || s2 > 227 * 1024 || s3 > 227 * 1024)
     throw Error(FDMGPU_UNSUPPORTED, "true-form quadrature operator: p too large");
-  FDM_CUDA(cudaFuncSetAttribute(k_quad_stage1, cudaFuncAttributeMaxDynamicSharedMemorySize, int(s1)));
-  k_quad_stage1<<<c.ncells * n1, 256, s1, c.stream>>>(n1, q, x, c.cell_dofs.p, c.constrained.p, c.Vq.p, c.Dq.p,
-                                                       c.Qbuf.p);
+  // FDMGPU_QUAD_STRIP=0: the 8 x 16 warp tasks (A/B switch; same sums, bitwise equal results)
+  const char* senv = std::getenv("FDMGPU_QUAD_STRIP");
+  const int strip = senv ? std::atoi(senv) : 2;  // 1 | 2: k-loop unrolled by 2 | 4 (C5 residual 2.02 -> 1.81 | 1.77 ms)
+  auto k1 = strip == 0 ? k_quad_stage1<0> : strip == 2 ? k_quad_stage1<2> : k_quad_stage1<1>;
+  auto k2 = strip == 0 ? k_quad_stage2<0> : strip == 2 ? k_quad_stage2<2> : k_quad_stage2<1>;
+  auto k3 = strip == 0 ? k_quad_stage3<0> : strip == 2 ? k_quad_stage3<2> : k_quad_stage3<1>;
+  FDM_CUDA(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, int(s1)));
+  k1<<<c.ncells * n1, 256, s1, c.stream>>>(n1, q, x, c.cell_dofs.p, c.constrained.p, c.Vq.p, c.Dq.p, c.Qbuf.p);
   FDM_LAUNCH_CHECK(c);
-  FDM_CUDA(cudaFuncSetAttribute(k_quad_stage2, cudaFuncAttributeMaxDynamicSharedMemorySize, int(s2)));
-  k_quad_stage2<<<c.ncells * q, 256, s2, c.stream>>>(n1, q, c.Qbuf.p, c.Vq.p, c.Dq.p, c.wq.p, c.xyz.p, c.kappa.p,
-                                                      c.qpts.p);
+  FDM_CUDA(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, int(s2)));
+  k2<<<c.ncells * q, 256, s2, c.stream>>>(n1, q, c.Qbuf.p, c.Vq.p, c.Dq.p, c.wq.p, c.xyz.p, c.kappa.p, c.qpts.p);
   FDM_LAUNCH_CHECK(c);
-  FDM_CUDA(cudaFuncSetAttribute(k_quad_stage3, cudaFuncAttributeMaxDynamicSharedMemorySize, int(s3)));
-  k_quad_stage3<<<c.ncells * n1, 256, s3, c.stream>>>(n1, q, c.Qbuf.p, c.Vq.p, c.Dq.p, c.E.p);
+  FDM_CUDA(cudaFuncSetAttribute(k3, cudaFuncAttributeMaxDynamicSharedMemorySize, int(s3)));
+  k3<<<c.ncells * n1, 256, s3, c.stream>>>(n1, q, c.Qbuf.p, c.Vq.p, c.Dq.p, c.E.p);
   FDM_LAUNCH_CHECK(c);
 }
 

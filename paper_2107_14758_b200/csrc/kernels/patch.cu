@@ -1807,26 +1807,55 @@ __global__ void k_schur_fv(SchurArgs s, int nent, const int32_t* __restrict__ rk
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nent; e += gridDim.x * blockDim.x) o[e] = v[rk_ent[e] >> 8];
 }
 
+// The first two S_RF values of every (component, row): fv2[patch][k][r] = (v0, v1), zero where absent
+// (and on the padding rows); the local indices are in SchurSplit::e2.
+__global__ void k_schur_fv2(SchurArgs s, int nRp, const int32_t* __restrict__ kr, const int32_t* __restrict__ rk_ent,
+                            double* __restrict__ fv2) {
+  const int j = blockIdx.y;
+  const double* v = s.vals + size_t(j) * s.vstride + s.rf_off;
+  const int n = s.ncomp * nRp;
+  double2* o = reinterpret_cast<double2*>(fv2) + size_t(j) * n;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int pk = kr[i], e0 = pk >> 8, cnt = pk & 255;
+    double2 w;
+    w.x = cnt > 0 ? v[rk_ent[e0] >> 8] : 0.0;
+    w.y = cnt > 1 ? v[rk_ent[e0 + 1] >> 8] : 0.0;
+    o[i] = w;
+  }
+}
+
 // -(S_RF S_FF^{-1} S_FR) on row tile I and up to G column tiles J0.. of one patch
 // (512 threads).  Per component k, phase A: Y[rr][lb] = sum_a S(r, a) Inv_k(a, lb)
 // for the tile's 64 rows (warp per row, lanes along lb: coalesced rows of Inv_k);
 // phase B: thread (column cl, 8 rows) adds Y[rr][lb] S(c, b) over column c's
 // entries of component k.  Y is double buffered: one barrier per component.
+// A (component, row) pair's first two entries come from the direct-indexed
+// tables e2 / fv2 (loads that depend on nothing but (k, row): all of a phase's
+// table loads are in flight at once, and phase B's are issued before phase A
+// of the next component); rows with more entries (edge modes) continue through
+// kr / rk_ent / fv.  Sums run in entry order either way.
 constexpr int kFormThreads = 512;
 template <int G>
 __global__ void __launch_bounds__(kFormThreads, 1)
     k_schur_form(int nR, int nRp, int ncomp, int nl, const int32_t* __restrict__ form_I,
                  const int32_t* __restrict__ form_J0, const int32_t* __restrict__ kr,
                  const int32_t* __restrict__ rk_ent, int nent, const double* __restrict__ fv,
-                 const double* __restrict__ inv, const int32_t* __restrict__ col_start, double* __restrict__ RT,
-                 int64_t rstride) {
+                 const int32_t* __restrict__ e2, const double* __restrict__ fv2, const double* __restrict__ inv,
+                 const int32_t* __restrict__ col_start, double* __restrict__ RT, int64_t rstride) {
   extern __shared__ __align__(16) double sm[];
+  __shared__ __align__(8) uint64_t bar[2], barA[2];
+  __shared__ __align__(16) double2 rowV[2 * T];  // phase A's table rows (the tile's 64 rows), two components in flight
+  __shared__ __align__(16) int32_t rowE[2 * T];
   const int pitch = nl | 1;
-  double* Yb[2] = {sm, sm + T * pitch};
+  double2* tabV = reinterpret_cast<double2*>(sm);                // [2][G T] first two values
+  int32_t* tabE = reinterpret_cast<int32_t*>(tabV + 2 * G * T);  // [2][G T] their local indices | flags
+  double* ybase = reinterpret_cast<double*>(tabE + 2 * G * T);
+  double* Yb[2] = {ybase, ybase + T * pitch};
   const int f = blockIdx.x, j = blockIdx.y, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int I = form_I[f], J0 = form_J0[f];
   const int nG = min(G, I - J0 + 1);
   const double* fvj = fv + size_t(j) * nent;
+  const double2* f2j = reinterpret_cast<const double2*>(fv2) + size_t(j) * ncomp * nRp;
   const double* invj = inv + size_t(j) * ncomp * nl * nl;
   const int cl = tid & 63, rg = tid >> 6;
   double acc[G][8];
@@ -1836,20 +1865,32 @@ __global__ void __launch_bounds__(kFormThreads, 1)
     for (int i = 0; i < 8; ++i) acc[g][i] = 0.0;
   auto phaseA = [&](int k, double* Y) {
     const double* ik = invj + size_t(k) * nl * nl;
-#pragma unroll 1
-    for (int i = 0; i < T / 16; ++i) {
-      const int rr = warp + 16 * i, r = I * T + rr;
-      double y[4] = {0.0, 0.0, 0.0, 0.0};
-      const int pk = kr[size_t(k) * nRp + r];
-      const int e0 = pk >> 8, cnt = pk & 255;
-      for (int e = e0; e < e0 + cnt; ++e) {
-        const int la = rk_ent[e] & 255;
-        const double va = fvj[e];
-        const double* row = ik + size_t(la) * nl;
+    mbar_wait(&barA[k & 1], (k >> 1) & 1);
+    const int32_t* pk = rowE + (k & 1) * T;
+    const double2* v = rowV + (k & 1) * T;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int lb = lane + 32 * q;
-          if (lb < nl) y[q] = fma(va, row[lb], y[q]);
+    for (int ii = 0; ii < T / 16; ++ii) {
+      const int i = warp + 16 * ii;
+      const int rr = i;
+      const double* row0 = ik + size_t(pk[i] & 255) * nl;
+      const double* row1 = ik + size_t((pk[i] >> 8) & 255) * nl;
+      double y[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int lb = lane + 32 * q;
+        y[q] = lb < nl ? fma(v[i].y, row1[lb], v[i].x * row0[lb]) : 0.0;
+      }
+      if (pk[i] >> 18) {  // more than two entries
+        const int kk = kr[size_t(k) * nRp + I * T + rr];
+        const int e0 = kk >> 8, cnt = kk & 255;
+        for (int e = e0 + 2; e < e0 + cnt; ++e) {
+          const double va = fvj[e];
+          const double* row = ik + size_t(rk_ent[e] & 255) * nl;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int lb = lane + 32 * q;
+            if (lb < nl) y[q] = fma(va, row[lb], y[q]);
+          }
         }
       }
 #pragma unroll
@@ -1859,28 +1900,68 @@ __global__ void __launch_bounds__(kFormThreads, 1)
       }
     }
   };
-  auto phaseB = [&](int k, const double* Y) {
-    const double* yr = Y + rg * 8 * pitch;
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      if (g < nG) {
-        const int pk = kr[size_t(k) * nRp + (J0 + g) * T + cl];
-        const int e0 = pk >> 8, cnt = pk & 255;
-        for (int e = e0; e < e0 + cnt; ++e) {
-          const int lb = rk_ent[e] & 255;
-          const double vb = fvj[e];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) acc[g][i] = fma(yr[i * pitch + lb], vb, acc[g][i]);
-        }
-      }
-    }
+  // phase B's table rows of component k (the CTA's nG x 64 columns are contiguous in e2 / fv2)
+  // arrive by two TMA bulk copies, one component ahead
+  const uint32_t nb = uint32_t(nG) * T;
+  auto fetchB = [&](int k) {
+    const int b = k & 1;
+    mbar_arrive_expect_tx(&bar[b], nb * 20u);
+    bulk_g2s(tabV + b * G * T, f2j + size_t(k) * nRp + J0 * T, nb * 16u, &bar[b]);
+    bulk_g2s(tabE + b * G * T, e2 + size_t(k) * nRp + J0 * T, nb * 4u, &bar[b]);
   };
+  auto fetchA = [&](int k) {
+    const int b = k & 1;
+    mbar_arrive_expect_tx(&barA[b], uint32_t(T) * 20u);
+    bulk_g2s(rowV + b * T, f2j + size_t(k) * nRp + I * T, uint32_t(T) * 16u, &barA[b]);
+    bulk_g2s(rowE + b * T, e2 + size_t(k) * nRp + I * T, uint32_t(T) * 4u, &barA[b]);
+  };
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_init(&barA[0], 1);
+    mbar_init(&barA[1], 1);
+    mbar_fence_init();
+    fetchA(0);
+    if (ncomp > 1) fetchA(1);
+    fetchB(0);
+  }
+  __syncthreads();  // the barriers are initialised before anyone waits on them
   phaseA(0, Yb[0]);
   __syncthreads();
 #pragma unroll 1
   for (int k = 0; k < ncomp; ++k) {
+    if (tid == 0) {  // both target buffers were last read before the previous barrier
+      if (k + 1 < ncomp) fetchB(k + 1);
+      if (k + 2 < ncomp) fetchA(k + 2);
+    }
     if (k + 1 < ncomp) phaseA(k + 1, Yb[(k + 1) & 1]);
-    phaseB(k, Yb[k & 1]);
+    mbar_wait(&bar[k & 1], (k >> 1) & 1);
+    const int32_t* pk = tabE + (k & 1) * G * T + cl;
+    const double2* v = tabV + (k & 1) * G * T + cl;
+    const double* yr = Yb[k & 1] + rg * 8 * pitch;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      if (g < nG) {
+        const int pg = pk[g * T];
+        const double2 vg = v[g * T];
+        const double* y0 = yr + (pg & 255);
+        const double* y1 = yr + ((pg >> 8) & 255);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[g][i] = fma(y0[i * pitch], vg.x, acc[g][i]);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[g][i] = fma(y1[i * pitch], vg.y, acc[g][i]);
+        if (pg >> 18) {
+          const int kk = kr[size_t(k) * nRp + (J0 + g) * T + cl];
+          const int e0 = kk >> 8, cnt = kk & 255;
+          for (int e = e0 + 2; e < e0 + cnt; ++e) {
+            const int lb = rk_ent[e] & 255;
+            const double vb = fvj[e];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) acc[g][i] = fma(yr[i * pitch + lb], vb, acc[g][i]);
+          }
+        }
+      }
+    }
     __syncthreads();
   }
 #pragma unroll
@@ -2684,11 +2765,14 @@ void launch_schur_direct(Context& c) {
                                                                                                 c.sx_fv.p);
   FDM_LAUNCH_CHECK(c);
   const int64_t rstride = int64_t(R.ntiles) * TT;
-  const size_t smem_f = sizeof(double) * 2 * T * size_t(S.nl | 1);
+  const size_t smem_f = sizeof(double) * 2 * T * size_t(S.nl | 1) + size_t(2) * kFormG * T * 20;
   FDM_CUDA(cudaFuncSetAttribute(k_schur_form<kFormG>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_f)));
+  k_schur_fv2<<<dim3(unsigned(std::min(64, (S.ncomp * S.nRp + 255) / 256)), c.npatch), 256, 0, c.stream>>>(
+      s, S.nRp, c.sx_kr.p, c.sx_rk_ent.p, c.sx_fv2.p);
+  FDM_LAUNCH_CHECK(c);
   k_schur_form<kFormG><<<dim3(unsigned(S.form_I.size()), c.npatch), kFormThreads, smem_f, c.stream>>>(
-      S.nR, S.nRp, S.ncomp, S.nl, c.sx_form_I.p, c.sx_form_J0.p, c.sx_kr.p, c.sx_rk_ent.p, nent, c.sx_fv.p, c.sx_inv.p,
-      c.sx_col_start.p, c.packed.p, rstride);
+      S.nR, S.nRp, S.ncomp, S.nl, c.sx_form_I.p, c.sx_form_J0.p, c.sx_kr.p, c.sx_rk_ent.p, nent, c.sx_fv.p, c.sx_e2.p,
+      c.sx_fv2.p, c.sx_inv.p, c.sx_col_start.p, c.packed.p, rstride);
   FDM_LAUNCH_CHECK(c);
   const size_t smem_c = sizeof(double) * (2 * size_t(c.n1) * c.n1 + 24);
   const int nrr = int(S.rr_entries.size());

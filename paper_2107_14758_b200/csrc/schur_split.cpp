@@ -266,6 +266,15 @@ void analyze_schur_split(Context& c) {
       S.rk_ent.insert(S.rk_ent.end(), b.begin(), b.end());
     }
   if (S.rk_ent.empty()) S.rk_ent.push_back(0);
+  // direct-indexed view of the first two entries (the common case: one P0 and one P1 mode)
+  S.e2.assign(size_t(ncomp) * S.nRp, 0);
+  for (int k = 0; k < ncomp; ++k)
+    for (int r = 0; r < S.nR; ++r) {
+      const auto& b = bucket[size_t(k) * S.nR + r];
+      const int n = int(b.size());
+      const int l0 = n > 0 ? (b[0] & 255) : 0, l1 = n > 1 ? (b[1] & 255) : 0;
+      S.e2[size_t(k) * S.nRp + r] = int32_t(l0 | (l1 << 8) | (std::min(n, 2) << 16) | ((n > 2 ? 1 : 0) << 18));
+    }
   // S_RR: structural entries of S_G inside R x R (both triangles inside diagonal tiles),
   // the diagonal, and the identity on the padding rows
   std::vector<int32_t> tix(size_t(S.R.nT) * S.R.nT, -1);

@@ -1,0 +1,9 @@
+#!/bin/bash
+# Re-entry evidence run at the current head: full GPU suite, smoke, default bench, reference arm, C5 launch list.
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.max.sm,clocks.sm,power.limit --format=csv > gpurun_out/r5a_gpu.txt 2>&1
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r5a_smoke.log 2>&1; echo "rc=$?" >> gpurun_out/r5a_smoke.log
+timeout 1800 python bench.py --steps 20 --warmup 5 > gpurun_out/r5a_bench.json 2> gpurun_out/r5a_bench.err; echo "rc=$?" >> gpurun_out/r5a_bench.err
+timeout 1800 python bench.py --impl reference --steps 20 --warmup 5 > gpurun_out/r5a_ref.json 2> gpurun_out/r5a_ref.err; echo "rc=$?" >> gpurun_out/r5a_ref.err
+timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/r5a_launches_c5.csv python tools/op_launches.py 5,0,0 > gpurun_out/r5a_ncu_c5.log 2>&1
+timeout 2400 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/r5a_tests.log 2>&1; echo "rc=$?" >> gpurun_out/r5a_tests.log
