@@ -1527,16 +1527,24 @@ __global__ void __launch_bounds__(256) k_schur_comps(PatchArgs a, SchurArgs s, i
     const int i = idx / ldm, jj = idx % ldm;
     out[idx] = jj < s.c0 ? M[i * LD + jj] : 0.0;
   }
+  // M D0^{-1} once (in the factor's work area, free until diag_factor_invert), then
+  // S'_11 = D1 - (M D0^{-1}) M^T: one division per entry of M, not per product term
+  double* Ms = Wm;
+  for (int idx = tid; idx < s.c1 * s.c0; idx += blockDim.x) {
+    const int i = idx / s.c0, jj = idx % s.c0;
+    Ms[i * LD + jj] = M[i * LD + jj] / d0[jj];
+  }
+  __syncthreads();
   for (int idx = tid; idx < TT; idx += blockDim.x) {
     const int cc = idx / T, r = idx % T;
     double v = r == cc ? 1.0 : 0.0;
     if (r < s.c1 && cc < s.c1) {
       v = r == cc ? d1[r] : 0.0;
-      for (int jj = 0; jj < s.c0; ++jj) v -= M[r * LD + jj] * M[cc * LD + jj] / d0[jj];
+      for (int jj = 0; jj < s.c0; ++jj) v -= M[r * LD + jj] * Ms[cc * LD + jj];
     }
     Dm[cc * LD + r] = v;
   }
-  __syncthreads();  // M is dead: its space takes the inverse
+  __syncthreads();  // M and its scaled copy are dead: their space takes the factor's work area and the inverse
   PatchArgs an = a;
   if (!report) an.err = nullptr;  // the full factorisation reports non-SPD pivots
   an.err_map = m1;
@@ -1826,14 +1834,17 @@ __global__ void k_schur_fv2(SchurArgs s, int nRp, const int32_t* __restrict__ kr
 
 // -(S_RF S_FF^{-1} S_FR) on row tile I and up to G column tiles J0.. of one patch
 // (512 threads).  Per component k, phase A: Y[rr][lb] = sum_a S(r, a) Inv_k(a, lb)
-// for the tile's 64 rows (warp per row, lanes along lb: coalesced rows of Inv_k);
-// phase B: thread (column cl, 8 rows) adds Y[rr][lb] S(c, b) over column c's
-// entries of component k.  Y is double buffered: one barrier per component.
-// A (component, row) pair's first two entries come from the direct-indexed
-// tables e2 / fv2 (loads that depend on nothing but (k, row): all of a phase's
-// table loads are in flight at once, and phase B's are issued before phase A
-// of the next component); rows with more entries (edge modes) continue through
-// kr / rk_ent / fv.  Sums run in entry order either way.
+// for the tile's 64 rows (warp per row, lanes along lb); phase B: thread
+// (column cl, 8 rows) adds Y[rr][lb] S(c, b) over column c's entries of
+// component k.  Everything phase A and B read arrives in shared memory by TMA
+// bulk copies issued ahead: Inv_k (nl x nl, single buffer: fetched while phase
+// B of the previous component runs -- with Inv_k read from global memory every
+// warp sat in the same L2 round trips at the same time, ncu: 36 % of stall
+// samples at the barrier, 23 % on those loads) and the direct-indexed tables
+// e2 / fv2 of the first two entries of every (component, row) (the tile's 64
+// rows for phase A, the CTA's nG x 64 columns for phase B, double buffered).
+// Rows with more entries (edge modes) continue through kr / rk_ent / fv.
+// Sums run in entry order.
 constexpr int kFormThreads = 512;
 template <int G>
 __global__ void __launch_bounds__(kFormThreads, 1)
@@ -1842,15 +1853,15 @@ __global__ void __launch_bounds__(kFormThreads, 1)
                  const int32_t* __restrict__ rk_ent, int nent, const double* __restrict__ fv,
                  const int32_t* __restrict__ e2, const double* __restrict__ fv2, const double* __restrict__ inv,
                  const int32_t* __restrict__ col_start, double* __restrict__ RT, int64_t rstride) {
-  extern __shared__ __align__(16) double sm[];
-  __shared__ __align__(8) uint64_t bar[2], barA[2];
+  extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) uint64_t bar[2], barA[2], barI;
   __shared__ __align__(16) double2 rowV[2 * T];  // phase A's table rows (the tile's 64 rows), two components in flight
   __shared__ __align__(16) int32_t rowE[2 * T];
   const int pitch = nl | 1;
-  double2* tabV = reinterpret_cast<double2*>(sm);                // [2][G T] first two values
+  double* Ism = sm;                                              // Inv_k, nl x nl
+  double2* tabV = reinterpret_cast<double2*>(Ism + nl * nl);     // [2][G T] first two values
   int32_t* tabE = reinterpret_cast<int32_t*>(tabV + 2 * G * T);  // [2][G T] their local indices | flags
-  double* ybase = reinterpret_cast<double*>(tabE + 2 * G * T);
-  double* Yb[2] = {ybase, ybase + T * pitch};
+  double* Y = reinterpret_cast<double*>(tabE + 2 * G * T);       // [T][pitch]
   const int f = blockIdx.x, j = blockIdx.y, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int I = form_I[f], J0 = form_J0[f];
   const int nG = min(G, I - J0 + 1);
@@ -1863,46 +1874,7 @@ __global__ void __launch_bounds__(kFormThreads, 1)
   for (int g = 0; g < G; ++g)
 #pragma unroll
     for (int i = 0; i < 8; ++i) acc[g][i] = 0.0;
-  auto phaseA = [&](int k, double* Y) {
-    const double* ik = invj + size_t(k) * nl * nl;
-    mbar_wait(&barA[k & 1], (k >> 1) & 1);
-    const int32_t* pk = rowE + (k & 1) * T;
-    const double2* v = rowV + (k & 1) * T;
-#pragma unroll
-    for (int ii = 0; ii < T / 16; ++ii) {
-      const int i = warp + 16 * ii;
-      const int rr = i;
-      const double* row0 = ik + size_t(pk[i] & 255) * nl;
-      const double* row1 = ik + size_t((pk[i] >> 8) & 255) * nl;
-      double y[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int lb = lane + 32 * q;
-        y[q] = lb < nl ? fma(v[i].y, row1[lb], v[i].x * row0[lb]) : 0.0;
-      }
-      if (pk[i] >> 18) {  // more than two entries
-        const int kk = kr[size_t(k) * nRp + I * T + rr];
-        const int e0 = kk >> 8, cnt = kk & 255;
-        for (int e = e0 + 2; e < e0 + cnt; ++e) {
-          const double va = fvj[e];
-          const double* row = ik + size_t(rk_ent[e] & 255) * nl;
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int lb = lane + 32 * q;
-            if (lb < nl) y[q] = fma(va, row[lb], y[q]);
-          }
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int lb = lane + 32 * q;
-        if (lb < nl) Y[rr * pitch + lb] = y[q];
-      }
-    }
-  };
-  // phase B's table rows of component k (the CTA's nG x 64 columns are contiguous in e2 / fv2)
-  // arrive by two TMA bulk copies, one component ahead
-  const uint32_t nb = uint32_t(nG) * T;
+  const uint32_t nb = uint32_t(nG) * T, ibytes = uint32_t(nl) * nl * 8u;
   auto fetchB = [&](int k) {
     const int b = k & 1;
     mbar_arrive_expect_tx(&bar[b], nb * 20u);
@@ -1915,30 +1887,78 @@ __global__ void __launch_bounds__(kFormThreads, 1)
     bulk_g2s(rowV + b * T, f2j + size_t(k) * nRp + I * T, uint32_t(T) * 16u, &barA[b]);
     bulk_g2s(rowE + b * T, e2 + size_t(k) * nRp + I * T, uint32_t(T) * 4u, &barA[b]);
   };
+  auto fetchI = [&](int k) {
+    mbar_arrive_expect_tx(&barI, ibytes);
+    bulk_g2s(Ism, invj + size_t(k) * nl * nl, ibytes, &barI);
+  };
   if (tid == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
     mbar_init(&barA[0], 1);
     mbar_init(&barA[1], 1);
+    mbar_init(&barI, 1);
     mbar_fence_init();
+    fetchI(0);
     fetchA(0);
     if (ncomp > 1) fetchA(1);
     fetchB(0);
   }
   __syncthreads();  // the barriers are initialised before anyone waits on them
-  phaseA(0, Yb[0]);
-  __syncthreads();
 #pragma unroll 1
   for (int k = 0; k < ncomp; ++k) {
-    if (tid == 0) {  // both target buffers were last read before the previous barrier
-      if (k + 1 < ncomp) fetchB(k + 1);
+    // ---- phase A: Y = S_RF(rows of tile I, component k) Inv_k
+    mbar_wait(&barA[k & 1], (k >> 1) & 1);
+    mbar_wait(&barI, k & 1);
+    {
+      const int32_t* pk = rowE + (k & 1) * T;
+      const double2* v = rowV + (k & 1) * T;
+#pragma unroll
+      for (int ii = 0; ii < T / 16; ++ii) {
+        const int rr = warp + 16 * ii;
+        const int pr = pk[rr];
+        const double2 vr = v[rr];
+        const double* row0 = Ism + (pr & 255) * nl;
+        const double* row1 = Ism + ((pr >> 8) & 255) * nl;
+        double y[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int lb = lane + 32 * q;
+          y[q] = lb < nl ? fma(vr.y, row1[lb], vr.x * row0[lb]) : 0.0;
+        }
+        if (pr >> 18) {  // more than two entries
+          const int kk = kr[size_t(k) * nRp + I * T + rr];
+          const int e0 = kk >> 8, cnt = kk & 255;
+          for (int e = e0 + 2; e < e0 + cnt; ++e) {
+            const double va = fvj[e];
+            const double* row = Ism + (rk_ent[e] & 255) * nl;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int lb = lane + 32 * q;
+              if (lb < nl) y[q] = fma(va, row[lb], y[q]);
+            }
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int lb = lane + 32 * q;
+          if (lb < nl) Y[rr * pitch + lb] = y[q];
+        }
+      }
+    }
+    __syncthreads();
+    // Inv_{k+1} streams in under phase B; the table buffers refilled here were last read before this barrier
+    if (tid == 0) {
+      if (k + 1 < ncomp) {
+        fetchI(k + 1);
+        fetchB(k + 1);
+      }
       if (k + 2 < ncomp) fetchA(k + 2);
     }
-    if (k + 1 < ncomp) phaseA(k + 1, Yb[(k + 1) & 1]);
+    // ---- phase B: acc(rows, column cl of tile J0 + g) += Y(rows, lb) S(c, b)
     mbar_wait(&bar[k & 1], (k >> 1) & 1);
     const int32_t* pk = tabE + (k & 1) * G * T + cl;
     const double2* v = tabV + (k & 1) * G * T + cl;
-    const double* yr = Yb[k & 1] + rg * 8 * pitch;
+    const double* yr = Y + rg * 8 * pitch;
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       if (g < nG) {
@@ -1962,7 +1982,7 @@ __global__ void __launch_bounds__(kFormThreads, 1)
         }
       }
     }
-    __syncthreads();
+    __syncthreads();  // Y is free for the next component
   }
 #pragma unroll
   for (int g = 0; g < G; ++g) {
@@ -2765,7 +2785,7 @@ void launch_schur_direct(Context& c) {
                                                                                                 c.sx_fv.p);
   FDM_LAUNCH_CHECK(c);
   const int64_t rstride = int64_t(R.ntiles) * TT;
-  const size_t smem_f = sizeof(double) * 2 * T * size_t(S.nl | 1) + size_t(2) * kFormG * T * 20;
+  const size_t smem_f = sizeof(double) * (size_t(S.nl) * S.nl + T * size_t(S.nl | 1)) + size_t(2) * kFormG * T * 20;
   FDM_CUDA(cudaFuncSetAttribute(k_schur_form<kFormG>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_f)));
   k_schur_fv2<<<dim3(unsigned(std::min(64, (S.ncomp * S.nRp + 255) / 256)), c.npatch), 256, 0, c.stream>>>(
       s, S.nRp, c.sx_kr.p, c.sx_rk_ent.p, c.sx_fv2.p);

@@ -232,7 +232,7 @@ void analyze_schur_split(Context& c) {
   // Direct top block: per-component views of S_RF, the structural entries of
   // S_RR in the R tile layout and the dense left-looking update lists.
   const char* dir = std::getenv("FDMGPU_DIRECT");
-  S.direct = S.inv && !(dir && dir[0] == '0') && c0 + c1 <= 128 && S.rf_col.size() < (size_t(1) << 23);
+  S.direct = S.inv && !(dir && dir[0] == '0') && c0 + c1 <= 128 && (c0 + c1) % 2 == 0 && S.rf_col.size() < (size_t(1) << 23);  // (even: Inv_k moves by 16-byte bulk copies)
   if (!S.direct) return;
   S.nl = c0 + c1;
   S.nRp = S.R.mpad;
