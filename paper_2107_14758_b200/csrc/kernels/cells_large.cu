@@ -209,10 +209,37 @@ __device__ __forceinline__ void dgemm_tc_s(int M, int N, int K, int rot, FA A, F
   }
 }
 
+// One row strip (rows m0 .. m0 + 7, all 8 NF columns) into registers / from registers to O:
+// the two halves of dgemm_tc_s, for outputs that overwrite an operand (stored after a barrier).
+template <int NF, int U, class FA, class FB>
+__device__ __forceinline__ void strip_compute(int m0, int K, FA A, FB B, double (&d)[NF][2]) {
+  const int lane = threadIdx.x & 31, ar = lane >> 2, ak = lane & 3;
+#pragma unroll
+  for (int f = 0; f < NF; ++f) d[f][0] = d[f][1] = 0.0;
+#pragma unroll(U)
+  for (int k0 = 0; k0 < K; k0 += 4) {
+    const double a = A(m0 + ar, k0 + ak);
+    double b[NF];
+#pragma unroll
+    for (int f = 0; f < NF; ++f) b[f] = B(k0 + ak, 8 * f + ar);
+#pragma unroll
+    for (int f = 0; f < NF; ++f) dmma884(d[f][0], d[f][1], a, b[f]);
+  }
+}
+template <int NF, class FO>
+__device__ __forceinline__ void strip_store(int m0, const double (&d)[NF][2], FO O) {
+  const int lane = threadIdx.x & 31, r = m0 + (lane >> 2), c0 = 2 * (lane & 3);
+#pragma unroll
+  for (int f = 0; f < NF; ++f) {
+    O(r, 8 * f + c0, d[f][0]);
+    O(r, 8 * f + c0 + 1, d[f][1]);
+  }
+}
+
 template <int S, int NF, class FA, class FB, class FO>
 __device__ __forceinline__ void qgemm(int M, int N, int K, int rot, FA A, FB B, FO O) {
   if constexpr (S > 0)
-    dgemm_tc_s<NF, 2 * S>(M, N, K, rot, A, B, O);
+    dgemm_tc_s<NF, (S >= 2 ? 4 : 2)>(M, N, K, rot, A, B, O);
   else
     dgemm_tc(M, N, K, A, B, O);
 }
@@ -295,8 +322,10 @@ __global__ void __launch_bounds__(256) k_quad_stage2(int n1, int q, double* __re
   double* Vp = sm;
   double* Dp = Vp + kQP * n1p;
   double* C = Dp + kQP * n1p;         // C[f][kz < n1k][qx] (stride kQP, zero padded)
-  double* G = C + 3 * n1k * kQP;      // g / f [field][qz][qx] (kQP x kQP, zero padded)
-  double* W = G + 3 * kQP * kQP;      // q weights, q points
+  // g / f [field][qz][qx] (kQP x kQP, zero padded); STRIP == 3: over C (the z interpolation keeps its
+  // outputs in registers until every warp has read C) -- 63 KB instead of 91 KB, three CTAs per SM
+  double* G = STRIP == 3 ? C : C + 3 * n1k * kQP;
+  double* W = STRIP == 3 ? C + max(3 * n1k * kQP, 3 * kQP * kQP) : G + 3 * kQP * kQP;  // q weights, q points
   double* X = W + 2 * q;              // 24 corner coordinates, X[3 b + r]
   double* J0 = X + 24;                // Jacobian tables [q][3] x 4
   double* J2 = J0 + 3 * q;
@@ -347,12 +376,42 @@ __global__ void __launch_bounds__(256) k_quad_stage2(int n1, int q, double* __re
   }
   const int kq2 = kQP * kQP;
   auto AVz = [&](int qz, int k) { return Vp[qz + kQP * k]; };
-  qgemm<STRIP, 5>(kQP, kQP, n1k, 0, AVz, [&](int k, int qx) { return C[(2 * n1k + k) * kQP + qx]; },
-           [&](int qz, int qx, double v) { G[qz * kQP + qx] = v; });
-  qgemm<STRIP, 5>(kQP, kQP, n1k, kQP >> 3, AVz, [&](int k, int qx) { return C[(n1k + k) * kQP + qx]; },
-           [&](int qz, int qx, double v) { G[kq2 + qz * kQP + qx] = v; });
-  qgemm<STRIP, 5>(kQP, kQP, n1k, 2 * (kQP >> 3), [&](int qz, int k) { return Dp[qz + kQP * k]; }, [&](int k, int qx) { return C[k * kQP + qx]; },
-           [&](int qz, int qx, double v) { G[2 * kq2 + qz * kQP + qx] = v; });
+  auto ADz = [&](int qz, int k) { return Dp[qz + kQP * k]; };
+  auto BC2 = [&](int k, int qx) { return C[(2 * n1k + k) * kQP + qx]; };
+  auto BC1 = [&](int k, int qx) { return C[(n1k + k) * kQP + qx]; };
+  auto BC0 = [&](int k, int qx) { return C[k * kQP + qx]; };
+  if constexpr (STRIP == 3) {
+    // 3 x 5 strip tasks over the 8 warps (t = warp, warp + 8), results held in registers
+    constexpr int NS = kQP / 8;
+    const int warp = threadIdx.x >> 5;
+    double dA[NS][2], dB[NS][2];
+    auto run = [&](int t, double (&d)[NS][2]) {
+      const int gm = t / NS, m0 = 8 * (t % NS);
+      if (gm == 0)
+        strip_compute<NS, 4>(m0, n1k, AVz, BC2, d);
+      else if (gm == 1)
+        strip_compute<NS, 4>(m0, n1k, AVz, BC1, d);
+      else
+        strip_compute<NS, 4>(m0, n1k, ADz, BC0, d);
+    };
+    auto put = [&](int t, const double (&d)[NS][2]) {
+      const int gm = t / NS;
+      strip_store<NS>(8 * (t % NS), d, [&](int qz, int qx, double v) { G[gm * kq2 + qz * kQP + qx] = v; });
+    };
+    for (int w0 = 0; w0 < 3 * NS; w0 += 16) {  // (blockDim.x = 256: one round)
+      const int t0 = w0 + warp, t1 = w0 + warp + 8;
+      if (t0 < 3 * NS) run(t0, dA);
+      if (t1 < 3 * NS) run(t1, dB);
+      __syncthreads();  // every warp has read C
+      if (t0 < 3 * NS) put(t0, dA);
+      if (t1 < 3 * NS) put(t1, dB);
+    }
+  } else {
+    qgemm<STRIP, 5>(kQP, kQP, n1k, 0, AVz, BC2, [&](int qz, int qx, double v) { G[qz * kQP + qx] = v; });
+    qgemm<STRIP, 5>(kQP, kQP, n1k, kQP >> 3, AVz, BC1, [&](int qz, int qx, double v) { G[kq2 + qz * kQP + qx] = v; });
+    qgemm<STRIP, 5>(kQP, kQP, n1k, 2 * (kQP >> 3), ADz, BC0,
+                    [&](int qz, int qx, double v) { G[2 * kq2 + qz * kQP + qx] = v; });
+  }
   __syncthreads();
   const double kap = kappa[c], wy = W[qy];
   for (int pnt = threadIdx.x; pnt < kq2; pnt += blockDim.x) {
@@ -413,7 +472,9 @@ __global__ void __launch_bounds__(256) k_quad_stage3(int n1, int q, const double
   double* Vp = sm;
   double* Dp = Vp + kQP * n1p;
   double* P = Dp + kQP * n1p;        // 3 planes [f][qy < Kq][qx < kQP], zero padded
-  double* b0 = P + 3 * Kq * kQP;     // b0[j * kQP + qx]
+  // b0[j * kQP + qx], b12: STRIP == 3 keeps the y projections in registers until every warp has read
+  // P and stores them over it (55 KB instead of 75 KB: more CTAs per SM)
+  double* b0 = STRIP == 3 ? P : P + 3 * Kq * kQP;
   double* b12 = b0 + kQP * n1p;
   const int c = blockIdx.x / n1, kz = blockIdx.x % n1;
   const int q2 = q * q, pl = Kq * kQP;
@@ -427,11 +488,30 @@ __global__ void __launch_bounds__(256) k_quad_stage3(int n1, int q, const double
       },
       [&](int i, double v) { P[i] = v; });
   __syncthreads();
-  qgemm<STRIP, 5>(n1p, kQP, Kq, 0, [&](int j, int qy) { return Vp[qy + kQP * j]; }, [&](int qy, int qx) { return P[qy * kQP + qx]; },
-           [&](int j, int qx, double v) { b0[j * kQP + qx] = v; });
-  qgemm<STRIP, 5>(n1p, kQP, 2 * Kq, n1p >> 3, [&](int j, int k) { return k < Kq ? Dp[k + kQP * j] : Vp[k - Kq + kQP * j]; },
-           [&](int k, int qx) { return P[pl + k * kQP + qx]; },  // T1 rows then T2 rows (contiguous)
-           [&](int j, int qx, double v) { b12[j * kQP + qx] = v; });
+  auto AV = [&](int j, int qy) { return Vp[qy + kQP * j]; };
+  auto ADV = [&](int j, int k) { return k < Kq ? Dp[k + kQP * j] : Vp[k - Kq + kQP * j]; };
+  auto BP0 = [&](int qy, int qx) { return P[qy * kQP + qx]; };
+  auto BP12 = [&](int k, int qx) { return P[pl + k * kQP + qx]; };  // T1 rows then T2 rows (contiguous)
+  if constexpr (STRIP == 3) {
+    constexpr int NS = kQP / 8;
+    const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5, ns = n1p >> 3;
+    for (int w0 = 0; w0 < 2 * ns; w0 += nw) {
+      const int t = w0 + warp;
+      double d[NS][2];
+      if (t < ns)
+        strip_compute<NS, 4>(8 * t, Kq, AV, BP0, d);
+      else if (t < 2 * ns)
+        strip_compute<NS, 4>(8 * (t - ns), 2 * Kq, ADV, BP12, d);
+      __syncthreads();  // every warp has read P (one round at n1p = 32, 8 warps)
+      if (t < ns)
+        strip_store<NS>(8 * t, d, [&](int j, int qx, double v) { b0[j * kQP + qx] = v; });
+      else if (t < 2 * ns)
+        strip_store<NS>(8 * (t - ns), d, [&](int j, int qx, double v) { b12[j * kQP + qx] = v; });
+    }
+  } else {
+    qgemm<STRIP, 5>(n1p, kQP, Kq, 0, AV, BP0, [&](int j, int qx, double v) { b0[j * kQP + qx] = v; });
+    qgemm<STRIP, 5>(n1p, kQP, 2 * Kq, n1p >> 3, ADV, BP12, [&](int j, int qx, double v) { b12[j * kQP + qx] = v; });
+  }
   __syncthreads();
   double* out = E + size_t(c) * n1 * n1 * n1 + size_t(kz) * n1 * n1;
   dgemm_tc(n1p, n1p, 2 * Kq, [&](int j, int k) { return k < Kq ? b0[j * kQP + k] : b12[j * kQP + k - Kq]; },
@@ -885,18 +965,24 @@ void launch_cells_quadrature(Context& c, const double* x) {
     throw Error(FDMGPU_UNSUPPORTED, "true-form quadrature operator: p too large");
   // FDMGPU_QUAD_STRIP=0: the 8 x 16 warp tasks (A/B switch; same sums, bitwise equal results)
   const char* senv = std::getenv("FDMGPU_QUAD_STRIP");
-  const int strip = senv ? std::atoi(senv) : 2;  // 1 | 2: k-loop unrolled by 2 | 4 (C5 residual 2.02 -> 1.81 | 1.77 ms)
-  auto k1 = strip == 0 ? k_quad_stage1<0> : strip == 2 ? k_quad_stage1<2> : k_quad_stage1<1>;
-  auto k2 = strip == 0 ? k_quad_stage2<0> : strip == 2 ? k_quad_stage2<2> : k_quad_stage2<1>;
-  auto k3 = strip == 0 ? k_quad_stage3<0> : strip == 2 ? k_quad_stage3<2> : k_quad_stage3<1>;
+  const int strip = senv ? std::atoi(senv) : 2;  // 3: stage 2 also keeps g over its input (3 CTAs per SM)
+   // 1 | 2: k-loop unrolled by 2 | 4 (C5 residual 2.02 -> 1.81 | 1.77 ms)
+  auto k1 = strip == 0 ? k_quad_stage1<0> : strip >= 2 ? k_quad_stage1<2> : k_quad_stage1<1>;
+  auto k2 = strip == 0 ? k_quad_stage2<0> : strip == 3 ? k_quad_stage2<3> : strip == 2 ? k_quad_stage2<2> : k_quad_stage2<1>;
+  auto k3 = strip == 0 ? k_quad_stage3<0> : strip == 3 ? k_quad_stage3<3> : strip == 2 ? k_quad_stage3<2> : k_quad_stage3<1>;
   FDM_CUDA(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, int(s1)));
   k1<<<c.ncells * n1, 256, s1, c.stream>>>(n1, q, x, c.cell_dofs.p, c.constrained.p, c.Vq.p, c.Dq.p, c.Qbuf.p);
   FDM_LAUNCH_CHECK(c);
-  FDM_CUDA(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, int(s2)));
-  k2<<<c.ncells * q, 256, s2, c.stream>>>(n1, q, c.Qbuf.p, c.Vq.p, c.Dq.p, c.wq.p, c.xyz.p, c.kappa.p, c.qpts.p);
+  const size_t s2a = sizeof(double) * (2 * size_t(kQP) * n1p + std::max(3 * size_t(n1k) * kQP, 3 * size_t(kQP) * kQP) +
+                                       2 * q + 24 + 12 * size_t(q));
+  const size_t s2u = strip == 3 ? s2a : s2;
+  FDM_CUDA(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, int(s2u)));
+  k2<<<c.ncells * q, 256, s2u, c.stream>>>(n1, q, c.Qbuf.p, c.Vq.p, c.Dq.p, c.wq.p, c.xyz.p, c.kappa.p, c.qpts.p);
   FDM_LAUNCH_CHECK(c);
-  FDM_CUDA(cudaFuncSetAttribute(k3, cudaFuncAttributeMaxDynamicSharedMemorySize, int(s3)));
-  k3<<<c.ncells * n1, 256, s3, c.stream>>>(n1, q, c.Qbuf.p, c.Vq.p, c.Dq.p, c.E.p);
+  const size_t s3a = sizeof(double) * (2 * size_t(kQP) * n1p + std::max(3 * size_t(Kq) * kQP, 2 * size_t(kQP) * n1p));
+  const size_t s3u = strip == 3 ? s3a : s3;
+  FDM_CUDA(cudaFuncSetAttribute(k3, cudaFuncAttributeMaxDynamicSharedMemorySize, int(s3u)));
+  k3<<<c.ncells * n1, 256, s3u, c.stream>>>(n1, q, c.Qbuf.p, c.Vq.p, c.Dq.p, c.E.p);
   FDM_LAUNCH_CHECK(c);
 }
 

@@ -2305,11 +2305,11 @@ __global__ void __launch_bounds__(kCompThreads) k_schur_comp(PatchArgs a, SchurA
 //   mode 1: c_F = b_F - S_FR x_R (rows F in component order, x = x_R in corr, out = cF)
 // The block's values and column indices (contiguous, 16-byte aligned) arrive
 // in shared memory by two TMA bulk copies issued at entry; 8 threads per row.
-constexpr int kSpmvThreads = 8 * kSpmvRows;
+constexpr int kSpmvThreads = 8 * kSpmvRows;  // TPR = 8 (16 threads per row: 2 x kSpmvThreads)
 // STAGED: the block's values / columns bulk-copied into shared memory; otherwise
 // read straight from global memory (coalesced: a row's entries are contiguous).
-template <bool STAGED>
-__global__ void __launch_bounds__(kSpmvThreads) k_schur_spmv(PatchArgs a, SchurArgs s, const double* __restrict__ rt,
+template <bool STAGED, int TPR>
+__global__ void __launch_bounds__(TPR * kSpmvRows) k_schur_spmv(PatchArgs a, SchurArgs s, const double* __restrict__ rt,
                                                              const double* __restrict__ xin, double* __restrict__ out,
                                                              int mode) {
   extern __shared__ __align__(128) double sm[];
@@ -2337,7 +2337,7 @@ __global__ void __launch_bounds__(kSpmvThreads) k_schur_spmv(PatchArgs a, SchurA
     __syncthreads();
   }
   const int nrows = mode == 0 ? s.nR : s.nF;
-  const int rl = tid >> 3, sub = tid & 7, r = b * kSpmvRows + rl;
+  const int rl = tid / TPR, sub = tid % TPR, r = b * kSpmvRows + rl;
   const bool live = r < nrows;
   int r0 = 0, r1 = 0, pos = -1, g = -1;
   if (live) {
@@ -2354,18 +2354,31 @@ __global__ void __launch_bounds__(kSpmvThreads) k_schur_spmv(PatchArgs a, SchurA
   // four independent gathers in flight per thread (the x reads are L1/L2 latency)
   double a4[4] = {0.0, 0.0, 0.0, 0.0};
   int e = r0 + sub;
-  for (; e + 24 < r1; e += 32) {
+  for (; e + 3 * TPR < r1; e += 4 * TPR) {
     double xv[4], vv[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      vv[u] = vs[e + 8 * u];
-      xv[u] = x[cs[e + 8 * u]];
+      vv[u] = vs[e + TPR * u];
+      xv[u] = x[cs[e + TPR * u]];
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) a4[u] = fma(vv[u], xv[u], a4[u]);
   }
-  for (; e < r1; e += 8) a4[0] = fma(vs[e], x[cs[e]], a4[0]);
+  if (TPR == 16) {  // the tail's gathers in flight together as well (a row is ~ 7 entries per thread)
+    double xv[3], vv[3];
+#pragma unroll
+    for (int u = 0; u < 3; ++u) {
+      const bool in = e + TPR * u < r1;
+      vv[u] = in ? vs[e + TPR * u] : 0.0;
+      xv[u] = in ? x[cs[e + TPR * u]] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 3; ++u) a4[u] = fma(vv[u], xv[u], a4[u]);
+  } else {
+    for (; e < r1; e += TPR) a4[0] = fma(vs[e], x[cs[e]], a4[0]);
+  }
   double acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
+  if (TPR == 16) acc += __shfl_xor_sync(0xffffffffu, acc, 8);
   acc += __shfl_xor_sync(0xffffffffu, acc, 4);
   acc += __shfl_xor_sync(0xffffffffu, acc, 2);
   acc += __shfl_xor_sync(0xffffffffu, acc, 1);
@@ -2628,10 +2641,14 @@ void launch_patch_solve(Context& c, const double* r_modal) {
   FDM_LAUNCH_CHECK(c);
   const char* senv = std::getenv("FDMGPU_SPMV_STAGED");
   const bool sstaged = !(senv && senv[0] == '0');
-  auto kspmv = sstaged ? k_schur_spmv<true> : k_schur_spmv<false>;
+  const char* tenv = std::getenv("FDMGPU_SPMV_TPR");  // threads per row: 8 | 16 (A/B)
+  const int tpr = tenv && std::atoi(tenv) == 16 ? 16 : 8;
+  auto kspmv = tpr == 16 ? (sstaged ? k_schur_spmv<true, 16> : k_schur_spmv<false, 16>)
+                         : (sstaged ? k_schur_spmv<true, 8> : k_schur_spmv<false, 8>);
+  const int spmv_threads = tpr * kSpmvRows;
   const size_t smem_rf = sstaged ? size_t(S.rf_bmax) * 12 : 0, smem_fr = sstaged ? size_t(S.fr_bmax) * 12 : 0;
   FDM_CUDA(cudaFuncSetAttribute(kspmv, cudaFuncAttributeMaxDynamicSharedMemorySize, int(std::max(smem_rf, smem_fr))));
-  launch_pdl(pdl, kspmv, dim3(int(S.rf_blk.size()) - 1, c.npatch), dim3(kSpmvThreads), smem_rf, c.stream, a, s,
+  launch_pdl(pdl, kspmv, dim3(int(S.rf_blk.size()) - 1, c.npatch), dim3(spmv_threads), smem_rf, c.stream, a, s,
              r_modal, (const double*)c.sx_F.p, c.sx_tR.p, 0);
   FDM_LAUNCH_CHECK(c);
   // x_R = S~_RR^{-1} t_R (dense stream) -> corr[nF..m)
@@ -2672,7 +2689,7 @@ void launch_patch_solve(Context& c, const double* r_modal) {
   }
   }
   // c_F = b_F - S_FR x_R;  x_F = S_FF^{-1} c_F -> corr[0..nF)
-  launch_pdl(pdl, kspmv, dim3(int(S.fr_blk.size()) - 1, c.npatch), dim3(kSpmvThreads), smem_fr, c.stream, a, s,
+  launch_pdl(pdl, kspmv, dim3(int(S.fr_blk.size()) - 1, c.npatch), dim3(spmv_threads), smem_fr, c.stream, a, s,
              r_modal, (const double*)c.corr.p, c.sx_F.p, 1);
   FDM_LAUNCH_CHECK(c);
   launch_pdl(pdl, kcomp, cgrid, dim3(kCompThreads), csm, c.stream, a, s, r_modal, (const double*)c.sx_F.p,
