@@ -45,3 +45,15 @@ def test_product_does_not_import_oracle():
             "print(any(m == 'oracle' or m.startswith('oracle.') for m in sys.modules))" % ROOT)
     res = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300, check=True)
     assert res.stdout.strip().splitlines()[-1] == "False"
+
+
+def test_factor_flops_follow_the_path_that_runs():
+    """With the direct top block the full factor is never formed: the roofline counts the dense
+    Cholesky of S~_RR and its inverse (n^3 per patch), not CholFactor::flops of the full factor."""
+    import bench
+
+    L = {"top_direct": 1, "n_top": 100, "npatch": 3, "schur_split": 2, "flops_ref": 10 ** 9, "dmma_flops": 10 ** 9}
+    assert bench.factor_flops(L) == 3 * 100.0 ** 3
+    assert bench.factor_issued_flops(L) > bench.factor_flops(L)  # padded 64 x 64 tiles
+    L["top_direct"] = 0
+    assert bench.factor_flops(L) == 2.0 * 10 ** 9 * 3 + bench.inverse_flops(L)

@@ -284,6 +284,25 @@ def test_p31_slab_path(pkg, oracle, torch):
     assert rel(z, staged.smooth(r)) <= TOL_RELAX
 
 
+@pytest.mark.parametrize("cfg", [(5, 2, 5), (5, 2, 31)])
+def test_quadrature_gemm_task_shapes_are_bitwise_equal(pkg, torch, cfg):
+    # trilinear residual (k_quad_stage1..3): the 8 x 16 warp tasks (FDMGPU_QUAD_STRIP=0), the row
+    # strips (1 / 2: k-loop unrolled by 2 / 4) and the variant that keeps stage 2 / 3 outputs over
+    # their input (3) sum every output over k in the same order: identical bits
+    prob = pkg.Problem(*cfg)
+    sol = pkg.Solver(prob)
+    r = prob.rhs()
+    out = {}
+    for mode in ("0", "1", "2", "3"):
+        os.environ["FDMGPU_QUAD_STRIP"] = mode
+        try:
+            out[mode] = np.array(sol.apply_A(r), copy=True)
+        finally:
+            del os.environ["FDMGPU_QUAD_STRIP"]
+    for mode in ("1", "2", "3"):
+        assert np.array_equal(out["0"], out[mode]), mode
+
+
 @pytest.mark.parametrize("cfg", [(2, 0, 0), (1, 0, 0), (5, 3, 4)])
 def test_cellwise_transfer_matches_csr(pkg, torch, cfg):
     # the sum-factorised restriction / prolongation (fdmgpu_set_coarse_cells)
