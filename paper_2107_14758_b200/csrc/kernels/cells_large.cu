@@ -963,9 +963,11 @@ void launch_cells_quadrature(Context& c, const double* x) {
   const size_t s3 = sizeof(double) * (4 * size_t(kQP) * n1p + 3 * size_t(Kq) * kQP);
   if (q > kQP || s1 > 227 * 1024 || s2 > 227 * 1024 || s3 > 227 * 1024)
     throw Error(FDMGPU_UNSUPPORTED, "true-form quadrature operator: p too large");
-  // FDMGPU_QUAD_STRIP=0: the 8 x 16 warp tasks (A/B switch; same sums, bitwise equal results)
+  // FDMGPU_QUAD_STRIP (A/B switch; same sums, bitwise equal results):
   const char* senv = std::getenv("FDMGPU_QUAD_STRIP");
-  const int strip = senv ? std::atoi(senv) : 2;  // 3: stage 2 also keeps g over its input (3 CTAs per SM)
+  // 0: 8 x 16 tasks (2.02 ms at C5) | 1, 2: row strips, k-loop unrolled by 2, 4 (1.81, 1.77 ms) | 3 (default): strips, and
+  // stages 2 / 3 keep their intermediate over its input (63 / 55 KB: three CTAs per SM; 1.60 ms)
+  const int strip = senv ? std::atoi(senv) : 3;
    // 1 | 2: k-loop unrolled by 2 | 4 (C5 residual 2.02 -> 1.81 | 1.77 ms)
   auto k1 = strip == 0 ? k_quad_stage1<0> : strip >= 2 ? k_quad_stage1<2> : k_quad_stage1<1>;
   auto k2 = strip == 0 ? k_quad_stage2<0> : strip == 3 ? k_quad_stage2<3> : strip == 2 ? k_quad_stage2<2> : k_quad_stage2<1>;
