@@ -251,6 +251,20 @@ void op_smooth(Context& c, const double* r, double* z) {
     return;
   }
   launch_cells_transform(c, 0, r, 1, nullptr);  // S^T r, minus each cell's interior-elimination share
+  // p = 31 slab path: only the cell-boundary entries of S^T r are summed over the cells (the
+  // separator solves read nothing else); the cell-interior entries have one owner and stay where
+  // the S^T pass left them, in the E-vector, for the S pass's interior rebuild (FDMGPU_SMOOTH_LOCAL=0:
+  // the full gather and the rebuild through the global vector)
+  const char* lenv = std::getenv("FDMGPU_SMOOTH_LOCAL");
+  const bool local = !(lenv && lenv[0] == '0') && cells_slab32(c) && c.bnd_list.p;
+  if (local) {
+    launch_gather_bnd(c, c.E.p, c.w[6].p);
+    launch_patch_solve(c, c.w[6].p);
+    launch_patch_gather_bnd(c, c.w[7].p);
+    launch_cells_transform(c, 1, c.w[7].p, 2 | 4, c.E.p);  // rebuild interiors from E, S
+    launch_gather(c, 1, c.E.p, nullptr, z);
+    return;
+  }
   launch_gather(c, 0, c.E.p, nullptr, c.w[6].p);
   launch_patch_solve(c, c.w[6].p);               // separator solves
   // patch-summed separator corrections: only the cell-boundary entries -- the S

@@ -343,6 +343,8 @@ void launch_cells_transform(Context& c, int dir, const double* in, int flags, co
 void launch_cells_schur(Context& c, const double* in);              // writes c.E
 void launch_cells_recon(Context& c, double* z, const double* rb);
 void launch_gather(Context& c, int mode, const double* E, const double* x, double* out);
+void launch_gather_bnd(Context& c, const double* E, double* out);  // mode 0 over the cell-boundary DOFs only
+bool cells_slab32(const Context& c);  // the p = 31 slab transform path is the one launch_cells_transform takes
 void launch_gather_vec(Context& c, int mode, const double* E, const double* x, double* out);  // all components
 void launch_cells_stiffness(Context& c, const double* x);            // writes c.E
 void launch_cells_quadrature(Context& c, const double* x);           // writes c.E (true form)

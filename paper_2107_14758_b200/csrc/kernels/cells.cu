@@ -898,6 +898,31 @@ __global__ void k_gather(int64_t ndof, int mode, const double* __restrict__ E, c
   out[g] = s;
 }
 
+// k_gather (mode 0: plain sums, constrained DOFs zero) over a list of DOFs: the same sums in
+// the same order; entries of `out` outside the list are left alone.
+__global__ void k_gather_list(int64_t n, const int32_t* __restrict__ list, const double* __restrict__ E,
+                              const int32_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+                              const uint8_t* __restrict__ cons, double* __restrict__ out) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  pdl_trigger();
+  int g = 0, q0 = 0, q1 = 0, i0 = 0, i1 = 0;
+  bool c = false;
+  if (i < n) {
+    g = list[i];
+    q0 = ptr[g];
+    q1 = ptr[g + 1];
+    c = cons[g];
+    if (q1 > q0) i0 = idx[q0];
+    if (q1 > q0 + 1) i1 = idx[q0 + 1];
+  }
+  pdl_wait();
+  if (i >= n) return;
+  double s = q1 > q0 ? E[i0] : 0.0;
+  if (q1 > q0 + 1) s += E[i1];
+  for (int q = q0 + 2; q < q1; ++q) s += E[idx[q]];
+  out[g] = c ? 0.0 : s;
+}
+
 size_t fdm_tables_bytes(const Context& c) {
   int ni = 1;
   for (int a = 0; a < c.dim; ++a) ni *= c.p - 1;
@@ -966,6 +991,18 @@ void launch_gather(Context& c, int mode, const double* E, const double* x, doubl
   launch_pdl(c.pdl && !c.timing, k_gather<false>, dim3(unsigned(blocks)), dim3(threads), 0, c.stream, c.ndof, mode, E,
              modes ? c.gm_ptr.p : c.g_ptr.p, modes ? c.gm_idx.p : c.g_idx.p, c.inv_mult.p, c.constrained.p, x, out,
              c.ndof, int64_t(0));
+  FDM_LAUNCH_CHECK(c);
+}
+
+// S^T gather (mode 0) of the cell-boundary DOFs only (Context::bnd_list); the others keep their old values.
+void launch_gather_bnd(Context& c, const double* E, double* out) {
+  if (!c.bnd_list.p) return launch_gather(c, 0, E, nullptr, out);
+  const bool modes = !c.modes_alias;
+  const int threads = 256;
+  const int64_t n = int64_t(c.bnd_list.n), blocks = (n + threads - 1) / threads;
+  launch_pdl(c.pdl && !c.timing, k_gather_list, dim3(unsigned(blocks)), dim3(threads), 0, c.stream, n,
+             (const int32_t*)c.bnd_list.p, E, (const int32_t*)(modes ? c.gm_ptr.p : c.g_ptr.p),
+             (const int32_t*)(modes ? c.gm_idx.p : c.g_idx.p), (const uint8_t*)c.constrained.p, out);
   FDM_LAUNCH_CHECK(c);
 }
 

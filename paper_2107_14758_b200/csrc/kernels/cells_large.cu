@@ -592,8 +592,10 @@ __device__ __forceinline__ void load_rows32(double* __restrict__ Mt, const doubl
   for (int i = threadIdx.x; i < kL32 * kL32; i += blockDim.x) Mt[(i >> 5) + 32 * (i & 31)] = M[i];
 }
 
+template <int GB>  // gather batch: map loads, then value loads, GB per thread in flight
 __global__ void __launch_bounds__(256, 2) k_cells_t1_32(int dir, int flags, const double* __restrict__ in,
-                                                      const double* __restrict__ aux, double* __restrict__ E,
+                                                      const double* __restrict__ aux, const double* eaux,
+                                                      double* __restrict__ E,
                                                       const int32_t* __restrict__ cdofs,
                                                       const double* __restrict__ inv_mult,
                                                       const uint8_t* __restrict__ cons,
@@ -614,21 +616,21 @@ __global__ void __launch_bounds__(256, 2) k_cells_t1_32(int dir, int flags, cons
   // gather in batches of 8 per thread: all map loads first, then the independent
   // value loads (8 DRAM round trips in flight per thread instead of a chain)
 #pragma unroll 1
-  for (int h = 0; h < 4; ++h) {
-    int gi[8];
+  for (int h = 0; h < 32 / GB; ++h) {
+    int gi[GB];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) gi[u] = cd[z0 * kSlab32 + tid + 256 * (8 * h + u)];
-    double v[8];
+    for (int u = 0; u < GB; ++u) gi[u] = cd[z0 * kSlab32 + tid + 256 * (GB * h + u)];
+    double v[GB];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int l = z0 * kSlab32 + tid + 256 * (8 * h + u), g = gi[u];
+    for (int u = 0; u < GB; ++u) {
+      const int l = z0 * kSlab32 + tid + 256 * (GB * h + u), g = gi[u];
       const double xv = in[g];
       const double w = dir == 0 ? inv_mult[g] : (sign ? sign[size_t(c) * kNpc32 + l] : 1.0);
       v[u] = cons[g] ? 0.0 : xv * w;
     }
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int i = tid + 256 * (8 * h + u);
+    for (int u = 0; u < GB; ++u) {
+      const int i = tid + 256 * (GB * h + u);
       slab[(i & ~1023) + pos32(i & 1023)] = v[u];
     }
   }
@@ -666,10 +668,15 @@ __global__ void __launch_bounds__(256, 2) k_cells_t1_32(int dir, int flags, cons
         for (int u = 0; u < 8; ++u) {
           const int i = b0 + 256 * u, s = i / (pm * pm), z = z0 + s;
           const int y = 1 + (i / pm) % pm, x = 1 + i % pm;
-          ga[u] = (i < npts && z > 0 && z < kL32 - 1) ? cd[size_t(z) * kSlab32 + x + 32 * y] : -1;
+          const bool in = i < npts && z > 0 && z < kL32 - 1;
+          // flags & 4: aux is the cell-local E-vector of the S^T pass (the interior right-hand
+          // side where that pass left it: no map load, contiguous reads; this CTA's slabs of E
+          // are read here, before its own stores)
+          ga[u] = !in ? -1 : (flags & 4) ? z * kSlab32 + x + 32 * y : cd[size_t(z) * kSlab32 + x + 32 * y];
         }
+        const double* asrc = (flags & 4) ? eaux + size_t(c) * kNpc32 : aux;
 #pragma unroll
-        for (int u = 0; u < 8; ++u) av[u] = ga[u] >= 0 ? aux[ga[u]] : 0.0;
+        for (int u = 0; u < 8; ++u) av[u] = ga[u] >= 0 ? asrc[ga[u]] : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
@@ -1014,9 +1021,11 @@ static void launch_cells_transform_32(Context& c, int dir, const double* in, int
   const bool recon = dir == 1 && (flags & 2);
   const size_t s1 = sizeof(double) * (kL32 * kL32 + (recon ? 10 : 8) * kSlab32) + (recon ? sizeof(Fdm32) : 0);
   const size_t s2 = sizeof(double) * kL32 * kL32 + sizeof(Fdm32);
-  FDM_CUDA(cudaFuncSetAttribute(k_cells_t1_32, cudaFuncAttributeMaxDynamicSharedMemorySize, int(s1)));
+  const char* benv = std::getenv("FDMGPU_T1_BATCH");  // gathers in flight per thread: 8 | 16 (A/B)
+  auto kt1 = benv && std::atoi(benv) == 16 ? k_cells_t1_32<16> : k_cells_t1_32<8>;
+  FDM_CUDA(cudaFuncSetAttribute(kt1, cudaFuncAttributeMaxDynamicSharedMemorySize, int(s1)));
   KernelTimer timer(c, 2);
-  k_cells_t1_32<<<c.ncells * 4, 256, s1, c.stream>>>(dir, flags, in, aux, c.E.p, cd, c.inv_mult.p, c.constrained.p,
+  kt1<<<c.ncells * 4, 256, s1, c.stream>>>(dir, flags, in, (flags & 4) ? nullptr : aux, (flags & 4) ? aux : nullptr, c.E.p, cd, c.inv_mult.p, c.constrained.p,
                                                      c.mode_sign.p, M, c.mu.p, c.At.p, c.Bt.p, c.nK.p);
   FDM_LAUNCH_CHECK(c);
   k_cells_t2_32<<<c.ncells * 4, 256, s2, c.stream>>>(dir, flags, c.E.p, c.mode_sign.p, M, c.mu.p, c.At.p, c.Bt.p);
@@ -1026,6 +1035,8 @@ static void launch_cells_transform_32(Context& c, int dir, const double* in, int
     FDM_LAUNCH_CHECK(c);
   }
 }
+
+bool cells_slab32(const Context& c) { return !cells_fit_smem(c) && c.n1 == kL32 && c.dim == 3 && !c.force_staged; }
 
 void launch_cells_transform(Context& c, int dir, const double* in, int flags, const double* aux) {
   if (cells_fit_smem(c))

@@ -62,6 +62,24 @@ def test_p31_relaxation_matches_oracle(one_patch):
     assert rel(sol.patch_solve_one(0, rj), ref.patch_solve_one(0, rj)) <= TOL_RELAX
 
 
+def test_p31_smooth_keeps_interior_rhs_cell_local(one_patch):
+    """The slab path sums only the cell-boundary entries of S^T r over the cells and rebuilds the
+    cell interiors from the E-vector of the S^T pass (single-owner entries: the same values the
+    full gather would copy).  FDMGPU_SMOOTH_LOCAL=0 is the full gather: identical bits, also on a
+    second right-hand side (nothing stale is read)."""
+    prob, sol, ref = one_patch
+    rng = np.random.default_rng(5)
+    for r in (prob.rhs(), rng.uniform(-1, 1, prob.ndof)):
+        z_local = np.array(sol.smooth(r), copy=True)
+        os.environ["FDMGPU_SMOOTH_LOCAL"] = "0"
+        try:
+            z_full = np.array(sol.smooth(r), copy=True)
+        finally:
+            del os.environ["FDMGPU_SMOOTH_LOCAL"]
+        assert np.array_equal(z_local, z_full)
+        assert rel(z_local, ref.smooth(r)) <= TOL_RELAX
+
+
 def test_p31_two_level_and_pcg_match_oracle(one_patch, torch):
     prob, sol, ref = one_patch
     w = sol.calibrate_damping()
