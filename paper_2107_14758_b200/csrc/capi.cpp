@@ -31,8 +31,8 @@ void setup_schur_split(Context& c) {
     a->reset();
   c.sx_ccol.reset();
   c.sx_hdr.reset();
-  for (auto* a : {&c.sx_vals, &c.sx_tR, &c.sx_F, &c.diagL, &c.sx_UT, &c.sx_part, &c.sx_inv, &c.sx_fv}) a->reset();
-  for (auto* a : {&c.sx_kr, &c.sx_rk_ent, &c.sx_rr_entries, &c.sx_form_I, &c.sx_form_J0, &c.sx_pair_ptr, &c.sx_pair_a,
+  for (auto* a : {&c.sx_vals, &c.sx_tR, &c.sx_F, &c.diagL, &c.sx_UT, &c.sx_part, &c.sx_inv, &c.sx_fv, &c.sx_fv2}) a->reset();
+  for (auto* a : {&c.sx_kr, &c.sx_rk_ent, &c.sx_rr_entries, &c.sx_form_I, &c.sx_form_J0, &c.sx_form2_I, &c.sx_form2_J0, &c.sx_e2, &c.sx_pair_ptr, &c.sx_pair_a,
                   &c.sx_pair_b, &c.sx_tile_mask})
     a->reset();
   c.sx_chunk.reset();
@@ -133,6 +133,8 @@ void setup_schur_split(Context& c) {
     c.sx_rr_entries.upload(S.rr_entries, c.stream);
     c.sx_form_I.upload(S.form_I, c.stream);
     c.sx_form_J0.upload(S.form_J0, c.stream);
+    c.sx_form2_I.upload(S.form2_I, c.stream);
+    c.sx_form2_J0.upload(S.form2_J0, c.stream);
     c.sx_pair_ptr.upload(S.pair_ptr, c.stream);
     c.sx_pair_a.upload(S.pair_a, c.stream);
     c.sx_pair_b.upload(S.pair_b, c.stream);

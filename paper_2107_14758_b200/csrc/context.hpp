@@ -19,6 +19,7 @@ constexpr int kHdrBytes = 144;  // solve-record header: 2 x 64 sub-block indices
 constexpr int kCompact = 10;    // doubles per compact 8x8 sub-block (8 row values + 8 column bytes + pad)
 constexpr int kHdrHost = kHdrBytes + 128;  // host tile_hdr stride: record header + compact index table
 constexpr int kFormG = 6;      // column tiles per CTA of the direct top-block assembly (k_schur_form)
+constexpr int kFormG2 = 12;    // column tiles per CTA of its half-row-tile form (k_schur_form2)
 constexpr int kSpmvRows = 16;   // rows per block of the Schur split's coupling products
 
 struct Error : std::runtime_error {
@@ -131,6 +132,7 @@ struct SchurSplit {
   std::vector<int32_t> e2;                // ncomp x nRp: the first two entries' local indices | min(count, 2) << 16 | (count > 2) << 18
   std::vector<int32_t> rr_entries;        // structural S_RR entries + padding diagonal: tile << 12 | col << 6 | row (R layout)
   std::vector<int32_t> form_I, form_J0;   // form CTAs: row tile I, first column tile (kFormG column tiles per CTA)
+  std::vector<int32_t> form2_I, form2_J0; // k_schur_form2 CTAs: half row tile 2 I + h, first column tile (kFormG2 per CTA)
   std::vector<int32_t> pair_ptr, pair_a, pair_b, tile_mask;  // dense left-looking update lists of the R layout
 };
 
@@ -226,6 +228,7 @@ struct Context {
   DevArray<int64_t> sx_ccol;
   DevArray<uint8_t> sx_hdr;
   DevArray<int32_t> sx_chunk;
+  DevArray<int32_t> sx_form2_I, sx_form2_J0;
   DevArray<int32_t> sx_kr, sx_rk_ent, sx_rr_entries, sx_form_I, sx_form_J0, sx_pair_ptr, sx_pair_a, sx_pair_b, sx_tile_mask;
   DevArray<int32_t> sx_e2;         // direct top block: SchurSplit::e2
   DevArray<double> sx_fv2;         // direct top block: the first two S_RF values of (component, row), npatch x ncomp x nRp x 2

@@ -1995,6 +1995,171 @@ __global__ void __launch_bounds__(kFormThreads, 1)
   }
 }
 
+// k_schur_form on half row tiles (32 rows x up to G column tiles per CTA, thread = column x 4
+// rows): phase A of a CTA halves (the rows' products with Inv_k are recomputed by every CTA of the
+// row tile), and Y is double buffered, so a warp goes from phase B of component k straight to
+// phase A of k + 1 -- one barrier per component, the two phases of different warps overlap.
+// Inv_{k+2} is fetched after that barrier and lands under phase B of k + 1.  Same sums, same order.
+template <int G>
+__global__ void __launch_bounds__(kFormThreads, 1)
+    k_schur_form2(int nR, int nRp, int ncomp, int nl, const int32_t* __restrict__ form_Ih,
+                  const int32_t* __restrict__ form_J0, const int32_t* __restrict__ kr,
+                  const int32_t* __restrict__ rk_ent, int nent, const double* __restrict__ fv,
+                  const int32_t* __restrict__ e2, const double* __restrict__ fv2, const double* __restrict__ inv,
+                  const int32_t* __restrict__ col_start, double* __restrict__ RT, int64_t rstride) {
+  constexpr int HR = T / 2;
+  extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) uint64_t bar[2], barA[2], barI;
+  __shared__ __align__(16) double2 rowV[2 * HR];
+  __shared__ __align__(16) int32_t rowE[2 * HR];
+  const int pitch = nl | 1;
+  double* Ism = sm;                                              // Inv_k, nl x nl
+  double2* tabV = reinterpret_cast<double2*>(Ism + nl * nl);     // [2][G T]
+  int32_t* tabE = reinterpret_cast<int32_t*>(tabV + 2 * G * T);  // [2][G T]
+  double* Y0 = reinterpret_cast<double*>(tabE + 2 * G * T);      // [2][HR][pitch]
+  const int f = blockIdx.x, j = blockIdx.y, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int Ih = form_Ih[f], I = Ih >> 1, r0 = (Ih & 1) * HR, J0 = form_J0[f];
+  const int nG = min(G, I - J0 + 1);
+  const double* fvj = fv + size_t(j) * nent;
+  const double2* f2j = reinterpret_cast<const double2*>(fv2) + size_t(j) * ncomp * nRp;
+  const double* invj = inv + size_t(j) * ncomp * nl * nl;
+  const int cl = tid & 63, rg = tid >> 6;
+  double acc[G][4];
+#pragma unroll
+  for (int g = 0; g < G; ++g)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[g][i] = 0.0;
+  const uint32_t nb = uint32_t(nG) * T, ibytes = uint32_t(nl) * nl * 8u;
+  auto fetchB = [&](int k) {
+    const int b = k & 1;
+    mbar_arrive_expect_tx(&bar[b], nb * 20u);
+    bulk_g2s(tabV + b * G * T, f2j + size_t(k) * nRp + J0 * T, nb * 16u, &bar[b]);
+    bulk_g2s(tabE + b * G * T, e2 + size_t(k) * nRp + J0 * T, nb * 4u, &bar[b]);
+  };
+  auto fetchA = [&](int k) {
+    const int b = k & 1;
+    mbar_arrive_expect_tx(&barA[b], uint32_t(HR) * 20u);
+    bulk_g2s(rowV + b * HR, f2j + size_t(k) * nRp + I * T + r0, uint32_t(HR) * 16u, &barA[b]);
+    bulk_g2s(rowE + b * HR, e2 + size_t(k) * nRp + I * T + r0, uint32_t(HR) * 4u, &barA[b]);
+  };
+  auto fetchI = [&](int k) {
+    mbar_arrive_expect_tx(&barI, ibytes);
+    bulk_g2s(Ism, invj + size_t(k) * nl * nl, ibytes, &barI);
+  };
+  auto phaseA = [&](int k) {
+    double* Y = Y0 + (k & 1) * HR * pitch;
+    mbar_wait(&barA[k & 1], (k >> 1) & 1);
+    mbar_wait(&barI, k & 1);
+    const int32_t* pk = rowE + (k & 1) * HR;
+    const double2* v = rowV + (k & 1) * HR;
+#pragma unroll
+    for (int ii = 0; ii < HR / 16; ++ii) {
+      const int rr = warp + 16 * ii;
+      const int pr = pk[rr];
+      const double2 vr = v[rr];
+      const double* row0 = Ism + (pr & 255) * nl;
+      const double* row1 = Ism + ((pr >> 8) & 255) * nl;
+      double y[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int lb = lane + 32 * q;
+        y[q] = lb < nl ? fma(vr.y, row1[lb], vr.x * row0[lb]) : 0.0;
+      }
+      if (pr >> 18) {  // more than two entries
+        const int kk = kr[size_t(k) * nRp + I * T + r0 + rr];
+        const int e0 = kk >> 8, cnt = kk & 255;
+        for (int e = e0 + 2; e < e0 + cnt; ++e) {
+          const double va = fvj[e];
+          const double* row = Ism + (rk_ent[e] & 255) * nl;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int lb = lane + 32 * q;
+            if (lb < nl) y[q] = fma(va, row[lb], y[q]);
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int lb = lane + 32 * q;
+        if (lb < nl) Y[rr * pitch + lb] = y[q];
+      }
+    }
+  };
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_init(&barA[0], 1);
+    mbar_init(&barA[1], 1);
+    mbar_init(&barI, 1);
+    mbar_fence_init();
+    fetchI(0);
+    fetchA(0);
+    if (ncomp > 1) fetchA(1);
+    fetchB(0);
+    if (ncomp > 1) fetchB(1);
+  }
+  __syncthreads();  // the barriers are initialised before anyone waits on them
+  phaseA(0);
+  __syncthreads();
+  if (tid == 0) {
+    if (ncomp > 1) fetchI(1);
+    if (ncomp > 2) fetchA(2);
+  }
+#pragma unroll 1
+  for (int k = 0; k < ncomp; ++k) {
+    // ---- phase B(k)
+    mbar_wait(&bar[k & 1], (k >> 1) & 1);
+    {
+      const int32_t* pk = tabE + (k & 1) * G * T + cl;
+      const double2* v = tabV + (k & 1) * G * T + cl;
+      const double* yr = Y0 + (k & 1) * HR * pitch + rg * 4 * pitch;
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        if (g < nG) {
+          const int pg = pk[g * T];
+          const double2 vg = v[g * T];
+          const double* y0 = yr + (pg & 255);
+          const double* y1 = yr + ((pg >> 8) & 255);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) acc[g][i] = fma(y0[i * pitch], vg.x, acc[g][i]);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) acc[g][i] = fma(y1[i * pitch], vg.y, acc[g][i]);
+          if (pg >> 18) {
+            const int kk = kr[size_t(k) * nRp + (J0 + g) * T + cl];
+            const int e0 = kk >> 8, cnt = kk & 255;
+            for (int e = e0 + 2; e < e0 + cnt; ++e) {
+              const int lb = rk_ent[e] & 255;
+              const double vb = fvj[e];
+#pragma unroll
+              for (int i = 0; i < 4; ++i) acc[g][i] = fma(yr[i * pitch + lb], vb, acc[g][i]);
+            }
+          }
+        }
+      }
+    }
+    // ---- phase A(k + 1) into the other Y buffer
+    if (k + 1 < ncomp) phaseA(k + 1);
+    __syncthreads();
+    // Inv's buffer, table buffer k & 1 and row-table buffer (k + 1) & 1 were last read before this barrier
+    if (tid == 0) {
+      if (k + 2 < ncomp) {
+        fetchI(k + 2);
+        fetchB(k + 2);
+      }
+      if (k + 3 < ncomp) fetchA(k + 3);
+    }
+  }
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    if (g < nG) {
+      const int J = J0 + g;
+      double* o = RT + size_t(j) * rstride + size_t(col_start[J] + I - J) * TT;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) o[tsw(r0 + rg * 4 + i, cl)] = -acc[g][i];
+    }
+  }
+}
+
 // += S_RR's own structural entries (and the identity on the padding rows).
 __global__ void k_schur_rr(PatchArgs a, int nF, int nentries, const int32_t* __restrict__ entries,
                            const int32_t* __restrict__ rrow, const int32_t* __restrict__ rcol,
@@ -2803,13 +2968,24 @@ void launch_schur_direct(Context& c) {
   FDM_LAUNCH_CHECK(c);
   const int64_t rstride = int64_t(R.ntiles) * TT;
   const size_t smem_f = sizeof(double) * (size_t(S.nl) * S.nl + T * size_t(S.nl | 1)) + size_t(2) * kFormG * T * 20;
-  FDM_CUDA(cudaFuncSetAttribute(k_schur_form<kFormG>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_f)));
   k_schur_fv2<<<dim3(unsigned(std::min(64, (S.ncomp * S.nRp + 255) / 256)), c.npatch), 256, 0, c.stream>>>(
       s, S.nRp, c.sx_kr.p, c.sx_rk_ent.p, c.sx_fv2.p);
   FDM_LAUNCH_CHECK(c);
-  k_schur_form<kFormG><<<dim3(unsigned(S.form_I.size()), c.npatch), kFormThreads, smem_f, c.stream>>>(
-      S.nR, S.nRp, S.ncomp, S.nl, c.sx_form_I.p, c.sx_form_J0.p, c.sx_kr.p, c.sx_rk_ent.p, nent, c.sx_fv.p, c.sx_e2.p,
-      c.sx_fv2.p, c.sx_inv.p, c.sx_col_start.p, c.packed.p, rstride);
+  // half-row-tile form (double-buffered Y, one barrier per component) when it fits; FDMGPU_FORM=1 keeps the
+  // whole-row-tile kernel
+  const size_t smem_f2 = sizeof(double) * (size_t(S.nl) * S.nl + T * size_t(S.nl | 1)) + size_t(2) * kFormG2 * T * 20;
+  const char* fenv = std::getenv("FDMGPU_FORM");
+  if (!(fenv && fenv[0] == '1') && smem_f2 + 4096 <= 227 * 1024) {
+    FDM_CUDA(cudaFuncSetAttribute(k_schur_form2<kFormG2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_f2)));
+    k_schur_form2<kFormG2><<<dim3(unsigned(S.form2_I.size()), c.npatch), kFormThreads, smem_f2, c.stream>>>(
+        S.nR, S.nRp, S.ncomp, S.nl, c.sx_form2_I.p, c.sx_form2_J0.p, c.sx_kr.p, c.sx_rk_ent.p, nent, c.sx_fv.p,
+        c.sx_e2.p, c.sx_fv2.p, c.sx_inv.p, c.sx_col_start.p, c.packed.p, rstride);
+  } else {
+    FDM_CUDA(cudaFuncSetAttribute(k_schur_form<kFormG>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_f)));
+    k_schur_form<kFormG><<<dim3(unsigned(S.form_I.size()), c.npatch), kFormThreads, smem_f, c.stream>>>(
+        S.nR, S.nRp, S.ncomp, S.nl, c.sx_form_I.p, c.sx_form_J0.p, c.sx_kr.p, c.sx_rk_ent.p, nent, c.sx_fv.p, c.sx_e2.p,
+        c.sx_fv2.p, c.sx_inv.p, c.sx_col_start.p, c.packed.p, rstride);
+  }
   FDM_LAUNCH_CHECK(c);
   const size_t smem_c = sizeof(double) * (2 * size_t(c.n1) * c.n1 + 24);
   const int nrr = int(S.rr_entries.size());

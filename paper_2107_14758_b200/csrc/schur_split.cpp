@@ -297,6 +297,11 @@ void analyze_schur_split(Context& c) {
       S.form_I.push_back(I);
       S.form_J0.push_back(J0);
     }
+  for (int Ih = 0; Ih < 2 * S.R.nT; ++Ih)
+    for (int J0 = 0; J0 <= Ih / 2; J0 += kFormG2) {
+      S.form2_I.push_back(Ih);
+      S.form2_J0.push_back(J0);
+    }
   // dense left-looking updates: tile (I, K) -= sum_{J < K} L(I, J) L(K, J)^T
   S.pair_ptr.assign(1, 0);
   for (int t = 0; t < S.R.ntiles; ++t) {
