@@ -179,6 +179,21 @@ def test_direct_top_block_matches_full_factorisation(case, pkg, torch):
     assert rel(out[True], out[False]) <= 1e-12
 
 
+@pytest.mark.parametrize("case", [(3, 2, 15, True), (4, 3, 15, True), (3, 3, 5, False)],
+                         ids=lambda c: "C%d_n%d_p%d_%s" % (c[0], c[1], c[2], "skip" if c[3] else "all"))
+def test_form_kernels_agree(case, pkg, torch, monkeypatch):
+    """The two kernels that form S~_RR's correction -- half row tiles with a double-buffered
+    Y (k_schur_form2, default) and whole row tiles (k_schur_form, FDMGPU_FORM=1) -- add the
+    same products; the relaxations agree to rounding (1e-13)."""
+    cfg, n, p, skip = case
+    prob = pkg.Problem(cfg, n, p, skip_boundary_patches=skip)
+    r = torch.from_numpy(prob.rhs()).cuda()
+    z2 = _solver(pkg, prob, True).smooth(r).cpu().numpy()
+    monkeypatch.setenv("FDMGPU_FORM", "1")
+    z1 = _solver(pkg, prob, True).smooth(r).cpu().numpy()
+    assert np.isfinite(z1).all() and rel(z1, z2) <= 1e-13
+
+
 def test_direct_top_block_reports_not_spd(pkg, torch):
     """Negative coefficients: the interior pivot check still reports pivot 0."""
     prob = pkg.Problem(3, 2, 5)
